@@ -1,0 +1,170 @@
+/*
+ * leafi_b200.h -- C-ABI of the B200-native LeaFi hot path (arXiv 2502.01836).
+ *
+ * The reference (`leafsearch`, pure Python/numpy) has no FFI: its seams are
+ * Python functions.  Each entry point below replaces one of them and is bound
+ * from Python with ctypes.  Conventions:
+ *
+ *   - every pointer named d_* is DEVICE memory owned by the caller (torch
+ *     tensors in the Python host layer); h_* pointers are host memory;
+ *   - `stream` is a cudaStream_t passed as void*; all work is stream-ordered;
+ *   - functions return 0 on success, a nonzero LF_E* code otherwise; the
+ *     message is available from lf_last_error() (thread-local);
+ *   - no torch types, no C++ types cross this boundary.
+ *
+ * Series are stored fp32 (lossless: the reference keeps fp32-exact values,
+ * series.py:48-50) in LEAF-CONTIGUOUS order: leaves in ascending node id,
+ * members of a leaf in ascending series id (tree.py:102-106,152,184).
+ */
+#ifndef LEAFI_B200_H
+#define LEAFI_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LF_OK 0
+#define LF_EINVAL 1     /* bad argument (maps to ValueError in Python) */
+#define LF_ECUDA 2      /* CUDA runtime error (maps to RuntimeError) */
+#define LF_ENOMEM 3
+
+#define LF_MAX_SEG 64
+#define LF_N_STATS 6    /* visited, searched, lb_pruned, filter_pruned, inferences, series_scanned */
+
+/* Device-resident index (the GPU image of reference tree.Index, tree.py:93-122). */
+typedef struct lf_index {
+    int64_t n_series;        /* rows in X */
+    int32_t m;               /* series length */
+    int32_t n_seg;           /* segments (summarize.py:15-37) */
+    int32_t n_nodes;         /* all tree nodes, ids 0..n_nodes-1 */
+    int32_t n_leaves;        /* leaves, slots 0..n_leaves-1 in ascending node id */
+    int64_t max_leaf_rows;   /* largest leaf (rows) */
+    int32_t seg_start[LF_MAX_SEG];
+    int32_t seg_width[LF_MAX_SEG];
+    const float* d_X;            /* [n_series][m] leaf-contiguous */
+    const int64_t* d_row_id;     /* [n_series] original series id of each row */
+    const int64_t* d_leaf_ptr;   /* [n_leaves+1] row offsets */
+    const int32_t* d_node_leaf;  /* [n_nodes] leaf slot, -1 for internal nodes */
+    const double* d_env_min;     /* [n_seg][n_nodes] SoA envelope minima */
+    const double* d_env_max;     /* [n_seg][n_nodes] SoA envelope maxima */
+    const int32_t* d_leaf_filter;/* [n_leaves] filter slot or -1 (may be NULL) */
+} lf_index;
+
+/* Options of one batched search (tree.py:220-229 search_engine keyword args). */
+typedef struct lf_search_opts {
+    int32_t k;                   /* 1 <= k <= n_series */
+    double bsf_factor;           /* tree.py:261,282; 1/(1+eps) for cli.py:57-65 */
+    const float* d_pred;         /* [Q][n_filters] filter predictions, or NULL */
+    const double* d_pred_f64;    /* same in fp64 (host predictor callables); used if non-NULL */
+    const double* d_offset;      /* [n_filters] conformal offsets (enhanced.py:127-134) */
+    int32_t n_filters;
+    int32_t sequential;          /* 1: one scanned leaf per query per round (exact
+                                    reference semantics, every counter identical);
+                                    0: doubling rounds 1,2,4,..,max_round_leaves */
+    int32_t max_round_leaves;    /* cap of the doubling schedule (>= 1) */
+    int32_t want_trace;          /* fill the trace buffers below */
+} lf_search_opts;
+
+/* Optional per-query trace (tree.py:77-83 TraceEntry), capacity n_leaves per query. */
+typedef struct lf_trace {
+    int32_t* d_len;        /* [Q] entries written */
+    int32_t* d_leaf;       /* [Q][n_leaves] node id of the visited leaf */
+    double* d_lb;          /* [Q][n_leaves] its lower bound */
+    int8_t* d_searched;    /* [Q][n_leaves] 1 if scanned */
+    double* d_leaf_nn;     /* [Q][n_leaves] min distance in the leaf (NaN if not scanned) */
+    double* d_bsf_before;  /* [Q][n_leaves] best-so-far used for the decision */
+} lf_trace;
+
+const char* lf_last_error(void);
+int lf_version(void);
+int lf_device_sm_count(int device);
+
+/*
+ * Query segment means and node lower bounds.
+ * Replaces summarize.summarize_series/matrix (summarize.py:44-56) and
+ * lower_bound_from_summary / lower_bounds_batch (summarize.py:97-122).
+ *   lb_mode 0: the search-path bound (np.dot: one FMA chain), tree.py:256,273
+ *   lb_mode 1: the batched traingen bound (einsum order), traingen.py:167-169
+ * Outputs d_qsumm [Q][n_seg] and d_lb [Q][n_nodes] (n_nodes of the SoA arrays).
+ */
+int lf_bounds(const float* d_queries, int64_t Q, const lf_index* idx,
+              const double* d_env_min, const double* d_env_max, int32_t n_env,
+              int32_t lb_mode, double* d_qsumm, double* d_lb, void* stream);
+
+/*
+ * Batched best-first search: bounds, per-query (lb, node id) visit order,
+ * round-driven cascade lb -> filter -> leaf scan, top-k by (distance, id).
+ * Replaces tree.search_engine (tree.py:220-297) for a batch of Q queries.
+ * Outputs: d_out_ids [Q][k] (int64), d_out_dists [Q][k], d_out_stats [Q][6].
+ * `trace` may be NULL.
+ */
+int lf_search(const lf_index* idx, const float* d_queries, int64_t Q,
+              const lf_search_opts* opts, int64_t* d_out_ids, double* d_out_dists,
+              int64_t* d_out_stats, const lf_trace* trace, void* stream);
+
+/*
+ * Filter inference for every (query, filter) pair, batch-invariant fp32.
+ * Replaces MlpModel.forward (mlp.py:90-95) as called per leaf at tree.py:281.
+ *   W1 [F][m][m] (x @ W1 layout, mlp.py:94), b1 [F][m], W2 [F][m], b2 [F]
+ * Output d_pred [Q][F].
+ */
+int lf_filter_predict(const float* d_queries, int64_t Q, int32_t m,
+                      const float* d_W1, const float* d_b1, const float* d_W2,
+                      const float* d_b2, int32_t F, float* d_pred, void* stream);
+
+/*
+ * Exact query x leaf minimum distance (direct form, fp64 accumulation).
+ * Replaces batch_distances(...).min(axis=1) (series.py:127-139) as used by
+ * collect_targets (traingen.py:175-188) and collect_local_targets (:138).
+ *   d_leaf_sel [S]: leaf slots; output d_dl [Q][S] (row stride ldd >= S).
+ */
+int lf_leaf_min_dist(const float* d_queries, int64_t Q, const lf_index* idx,
+                     const int32_t* d_leaf_sel, int32_t S, double* d_dl, int64_t ldd,
+                     void* stream);
+
+/*
+ * Same, but queries come in groups that are each compared with ONE leaf
+ * (collect_local_targets, traingen.py:135-144): group g = queries
+ * [h_qptr[g], h_qptr[g+1]) against leaf slot h_group_leaf[g].  h_* are host
+ * arrays (n_groups+1 / n_groups entries).  Output d_dl [Q].
+ */
+int lf_local_min_dist(const float* d_queries, const lf_index* idx, const int64_t* h_qptr,
+                      const int32_t* h_group_leaf, int32_t n_groups, double* d_dl,
+                      void* stream);
+
+/*
+ * Full distance matrix between queries and an arbitrary row block
+ * (series.batch_distances, series.py:127-139). d_block [B][m], out [Q][B].
+ */
+int lf_batch_distances(const float* d_queries, int64_t Q, const float* d_block, int64_t B,
+                       int32_t m, double* d_out, void* stream);
+
+/*
+ * Native index build (tree.build_index, tree.py:164-189), bit-identical node
+ * table.  Host memory.  Opaque handle protocol:
+ *   h = lf_tree_build(values, n, m, n_seg, max_leaf_size, n_threads)
+ *   lf_tree_info(h, &n_nodes, &n_leaves)
+ *   lf_tree_export(h, ...)   (arrays sized by lf_tree_info; members sized n)
+ *   lf_tree_free(h)
+ */
+typedef struct lf_tree lf_tree;
+lf_tree* lf_tree_build(const float* h_values, int64_t n, int32_t m, int32_t n_seg,
+                       int64_t max_leaf_size, int32_t n_threads);
+int lf_tree_info(const lf_tree* t, int32_t* n_nodes, int32_t* n_leaves);
+int lf_tree_export(const lf_tree* t, double* env_min /*[n_nodes][n_seg]*/,
+                   double* env_max, int32_t* left, int32_t* right, int32_t* split_seg,
+                   double* split_thr, int64_t* size, int8_t* oversized,
+                   int64_t* member_ptr /*[n_nodes+1]*/, int64_t* members /*[n]*/);
+void lf_tree_free(lf_tree* t);
+
+/* Segment means for host rows (summarize_matrix, summarize.py:52-56), numpy order. */
+int lf_paa_host(const float* h_values, int64_t n, int32_t m, int32_t n_seg, double* h_out,
+                int32_t n_threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LEAFI_B200_H */

@@ -1,0 +1,47 @@
+"""B200-native LeaFi hot path (arXiv 2502.01836).
+
+Query-time search (bounds -> learned filters -> leaf scan) and build-time
+training-data generation run as hand-written sm_100a CUDA kernels behind the
+C-ABI in include/leafi_b200.h (library: _lib/libleafi_b200.so).  The Python
+layer mirrors the reference package's seams (`leafsearch`: search_engine,
+exact_search, search, SearchRequest, collect_targets, ...) so callers switch
+by changing the import.  There is no CPU fallback.
+"""
+
+from .index import DeviceIndex, TreeIndex, build_index, segment_layout, segment_means
+from .engine import (
+    BatchResult,
+    SearchOutcome,
+    SearchStats,
+    TraceEntry,
+    batch_distances,
+    epsilon_search,
+    exact_search,
+    linear_scan,
+    pruning_ratio,
+    search_batch,
+    search_engine,
+)
+from .filters import FilterPack
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BatchResult",
+    "DeviceIndex",
+    "FilterPack",
+    "SearchOutcome",
+    "SearchStats",
+    "TraceEntry",
+    "TreeIndex",
+    "batch_distances",
+    "build_index",
+    "epsilon_search",
+    "exact_search",
+    "linear_scan",
+    "pruning_ratio",
+    "search_batch",
+    "search_engine",
+    "segment_layout",
+    "segment_means",
+]

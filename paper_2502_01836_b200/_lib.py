@@ -1,0 +1,143 @@
+"""ctypes binding of the C-ABI in include/leafi_b200.h.
+
+The product path has NO CPU fallback: if the shared library is missing or no
+CUDA device is present, every compute entry point raises.  Host-only entry
+points (the native tree builder, segment means) work without a GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libleafi_b200.so"
+MAX_SEG = 64
+N_STATS = 6
+
+LF_OK, LF_EINVAL, LF_ECUDA, LF_ENOMEM = 0, 1, 2, 3
+
+
+class LfIndex(C.Structure):
+    _fields_ = [
+        ("n_series", C.c_int64),
+        ("m", C.c_int32),
+        ("n_seg", C.c_int32),
+        ("n_nodes", C.c_int32),
+        ("n_leaves", C.c_int32),
+        ("max_leaf_rows", C.c_int64),
+        ("seg_start", C.c_int32 * MAX_SEG),
+        ("seg_width", C.c_int32 * MAX_SEG),
+        ("d_X", C.c_void_p),
+        ("d_row_id", C.c_void_p),
+        ("d_leaf_ptr", C.c_void_p),
+        ("d_node_leaf", C.c_void_p),
+        ("d_env_min", C.c_void_p),
+        ("d_env_max", C.c_void_p),
+        ("d_leaf_filter", C.c_void_p),
+    ]
+
+
+class LfSearchOpts(C.Structure):
+    _fields_ = [
+        ("k", C.c_int32),
+        ("bsf_factor", C.c_double),
+        ("d_pred", C.c_void_p),
+        ("d_pred_f64", C.c_void_p),
+        ("d_offset", C.c_void_p),
+        ("n_filters", C.c_int32),
+        ("sequential", C.c_int32),
+        ("max_round_leaves", C.c_int32),
+        ("want_trace", C.c_int32),
+    ]
+
+
+class LfTrace(C.Structure):
+    _fields_ = [
+        ("d_len", C.c_void_p),
+        ("d_leaf", C.c_void_p),
+        ("d_lb", C.c_void_p),
+        ("d_searched", C.c_void_p),
+        ("d_leaf_nn", C.c_void_p),
+        ("d_bsf_before", C.c_void_p),
+    ]
+
+
+_P = C.c_void_p
+_I64 = C.c_int64
+_I32 = C.c_int32
+
+# symbol -> (restype, argtypes); mirrors include/leafi_b200.h one to one
+SIGNATURES = {
+    "lf_last_error": (C.c_char_p, []),
+    "lf_version": (C.c_int, []),
+    "lf_device_sm_count": (C.c_int, [C.c_int]),
+    "lf_bounds": (C.c_int, [_P, _I64, C.POINTER(LfIndex), _P, _P, _I32, _I32, _P, _P, _P]),
+    "lf_search": (C.c_int, [C.POINTER(LfIndex), _P, _I64, C.POINTER(LfSearchOpts), _P, _P, _P,
+                            C.POINTER(LfTrace), _P]),
+    "lf_filter_predict": (C.c_int, [_P, _I64, _I32, _P, _P, _P, _P, _I32, _P, _P]),
+    "lf_leaf_min_dist": (C.c_int, [_P, _I64, C.POINTER(LfIndex), _P, _I32, _P, _I64, _P]),
+    "lf_local_min_dist": (C.c_int, [_P, C.POINTER(LfIndex), _P, _P, _I32, _P, _P]),
+    "lf_batch_distances": (C.c_int, [_P, _I64, _P, _I64, _I32, _P, _P]),
+    "lf_tree_build": (_P, [_P, _I64, _I32, _I32, _I64, _I32]),
+    "lf_tree_info": (C.c_int, [_P, C.POINTER(_I32), C.POINTER(_I32)]),
+    "lf_tree_export": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "lf_tree_free": (None, [_P]),
+    "lf_paa_host": (C.c_int, [_P, _I64, _I32, _I32, _P, _I32]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load (once) the in-tree library; raise loudly when it is absent."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2502_01836_b200._build` "
+                "(there is no CPU fallback)")
+        h = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(h, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = h
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc == LF_OK:
+        return
+    msg = lib().lf_last_error().decode(errors="replace")
+    if rc == LF_EINVAL:
+        raise ValueError(msg)
+    raise RuntimeError(f"leafi_b200 error {rc}: {msg}")
+
+
+def require_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2502_01836_b200 needs a CUDA device (no CPU fallback)")
+    return torch
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def ptr(t) -> int | None:
+    """Device (or host) address of a tensor / ndarray, None for None."""
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        return int(t.data_ptr())
+    return int(t.ctypes.data)
+
+
+def threads() -> int:
+    return max(1, min(32, os.cpu_count() or 1))

@@ -1,0 +1,93 @@
+// Shared helpers for the sm_100a LeaFi kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/leafi_b200.h"
+
+namespace lf {
+
+int fail(int code, const std::string& msg);
+
+#define LF_CUDA(expr)                                                                   \
+    do {                                                                                \
+        cudaError_t e_ = (expr);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return ::lf::fail(LF_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define LF_REQUIRE(cond, msg)                                  \
+    do {                                                       \
+        if (!(cond)) return ::lf::fail(LF_EINVAL, (msg));      \
+    } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int sm_count();
+
+// Stream-ordered scratch allocation that frees itself.
+struct Scratch {
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    Scratch() = default;
+    Scratch(const Scratch&) = delete;
+    Scratch& operator=(const Scratch&) = delete;
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, s);
+    }
+    cudaError_t alloc(size_t bytes, cudaStream_t st) {
+        s = st;
+        return cudaMallocAsync(&p, bytes ? bytes : 16, st);
+    }
+    template <class T>
+    T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+// numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src,
+// pairwise_sum_DOUBLE) over fp32 inputs promoted to fp64.  np.add.reduceat
+// seeds each segment with its first element and adds the pairwise sum of the
+// rest: summarize.py:49,56 therefore computes a[s] + pairwise(a[s+1 .. s+w)).
+__device__ __host__ inline double np_pairwise_f32(const float* a, int n) {
+    if (n < 8) {
+        double r = 0.0;
+        for (int i = 0; i < n; ++i) r += (double)a[i];
+        return r;
+    }
+    if (n <= 128) {
+        double r[8];
+        for (int j = 0; j < 8; ++j) r[j] = (double)a[j];
+        int i = 8;
+        for (; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; ++j) r[j] += (double)a[i + j];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += (double)a[i];
+        return res;
+    }
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    return np_pairwise_f32(a, n2) + np_pairwise_f32(a + n2, n - n2);
+}
+
+// Segment mean as the reference computes it (summarize.py:49).
+__device__ __host__ inline double segment_mean(const float* row, int start, int width) {
+    double s = (double)row[start] + np_pairwise_f32(row + start + 1, width - 1);
+    return s / (double)width;
+}
+
+__device__ inline double warp_sum_f64(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// (distance, id) lexicographic order: tree.py:212 lexsort((ids, dists)).
+__device__ inline bool pair_less(double da, long long ia, double db, long long ib) {
+    return da < db || (da == db && ia < ib);
+}
+
+constexpr double kInf = __builtin_huge_val();
+
+}  // namespace lf

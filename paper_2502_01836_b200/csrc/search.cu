@@ -1,0 +1,541 @@
+// K2-K4: the batched best-first search (tree.py:220-297) as rounds over a
+// per-query visit order.
+//
+//   bounds (K1)  ->  stable (lb, node id) sort per query (K2; the heap of
+//   tree.py:256-275 pops in exactly this order)  ->  rounds:
+//     plan   : one thread per query walks its order from a cursor, applying the
+//              break rule lb > bsf*f (tree.py:261-269) and the filter rule
+//              pred - offset > bsf*f (tree.py:277-286) with the round-start
+//              bsf, and selects up to R leaves to scan;
+//     scan   : leaf chunks of CH rows; each warp computes fp64 direct-form
+//              distances (series.py:142-146) from 128-bit loads and a
+//              warp-shuffle reduction; per-chunk top-k candidates;
+//     merge  : one warp per query folds candidates into the running top-k by
+//              (distance, id) (tree.py:192-217) and refreshes bsf.
+// With sequential=1 every round scans one leaf per query, which reproduces
+// the reference's traversal, counters and trace exactly.
+#include <algorithm>
+#include <vector>
+
+#include "bounds.cuh"
+#include "common.cuh"
+
+namespace lf {
+
+constexpr int CH = 256;          // rows per scan task (256 KiB at m = 256)
+constexpr int SCAN_THREADS = 256;
+constexpr int SCAN_WARPS = SCAN_THREADS / 32;
+
+struct RoundState {
+    int64_t Q;
+    int k, kc;                   // kc = candidates kept per task = min(k, CH)
+    int R, Rcap;                 // leaves per query this round, and the buffer stride
+    double f;                    // bsf_factor
+    const int* order;            // [Q][Nn]
+    const double* lbs;           // [Q][Nn]
+    int* cursor;                 // [Q]
+    int* done;                   // [Q]
+    double* top_d;               // [Q][k]   running top-k (round-start state)
+    long long* top_i;            // [Q][k]
+    int* top_n;                  // [Q]
+    double* top_d_out;           // merge writes here; host swaps after each round
+    long long* top_i_out;
+    int* top_n_out;
+    int n_leaves;
+    long long* stats;            // [Q][6]
+    int* sel_leaf;               // [Q][Rcap]
+    int* sel_trace;              // [Q][Rcap]
+    int* sel_pre;                // [Q][Rcap+1] chunk prefix within the query
+    int* n_sel;                  // [Q]
+    long long* chunk_off;        // [Q+1]
+    double* cand_d;              // [max_tasks][kc]
+    long long* cand_i;
+    double* task_min;            // [max_tasks] (trace only)
+    int* n_active;
+    const float* pred;           // [Q][F]
+    const double* pred64;        // [Q][F] (alternative to pred)
+    const double* offset;        // [F]
+    int F;
+    int want_trace;
+    lf_trace tr;
+};
+
+__device__ inline double query_bsf(const RoundState& s, int64_t q) {
+    return s.top_n[q] == s.k ? s.top_d[q * s.k + s.k - 1] : kInf;
+}
+
+// ---------------------------------------------------------------- plan ----
+__global__ void plan_kernel(RoundState s, lf_index idx) {
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= s.Q) return;
+    const int Nn = idx.n_nodes;
+    int ns = 0, nch = 0;
+    int* pre = s.sel_pre + q * (s.Rcap + 1);
+    if (!s.done[q]) {
+        const double bsf = query_bsf(s, q);
+        const double thr = bsf * s.f;
+        const int* ord = s.order + q * Nn;
+        const double* lbs = s.lbs + q * Nn;
+        long long* st = s.stats + q * LF_N_STATS;
+        int cur = s.cursor[q];
+        bool fin = false;
+        int tl = s.want_trace ? s.tr.d_len[q] : 0;
+        const int64_t tbase = q * (int64_t)idx.n_leaves;
+        while (cur < Nn) {
+            const int node = ord[cur];
+            const double lb = lbs[cur];
+            const int leaf = idx.d_node_leaf[node];
+            if (lb > thr) {                      // tree.py:261
+                if (leaf >= 0) {
+                    st[0]++; st[2]++;
+                    if (s.want_trace) {
+                        s.tr.d_leaf[tbase + tl] = node; s.tr.d_lb[tbase + tl] = lb;
+                        s.tr.d_searched[tbase + tl] = 0; s.tr.d_leaf_nn[tbase + tl] = __longlong_as_double(0x7ff8000000000000LL);
+                        s.tr.d_bsf_before[tbase + tl] = bsf; ++tl;
+                    }
+                }
+                fin = true;
+                break;
+            }
+            ++cur;
+            if (leaf < 0) continue;              // internal: children follow in order
+            st[0]++;
+            const int fs = (idx.d_leaf_filter != nullptr && (s.pred != nullptr || s.pred64 != nullptr))
+                               ? idx.d_leaf_filter[leaf] : -1;
+            if (fs >= 0) {                        // tree.py:279-286
+                st[4]++;
+                const double pv = s.pred64 != nullptr ? s.pred64[q * s.F + fs] : (double)s.pred[q * s.F + fs];
+                const double p = pv - s.offset[fs];
+                if (p > thr) {
+                    st[3]++;
+                    if (s.want_trace) {
+                        s.tr.d_leaf[tbase + tl] = node; s.tr.d_lb[tbase + tl] = lb;
+                        s.tr.d_searched[tbase + tl] = 0; s.tr.d_leaf_nn[tbase + tl] = __longlong_as_double(0x7ff8000000000000LL);
+                        s.tr.d_bsf_before[tbase + tl] = bsf; ++tl;
+                    }
+                    continue;
+                }
+            }
+            const int64_t rows = idx.d_leaf_ptr[leaf + 1] - idx.d_leaf_ptr[leaf];
+            st[1]++; st[5] += rows;              // tree.py:290-291: whole leaves
+            s.sel_leaf[q * s.Rcap + ns] = leaf;
+            if (s.want_trace) {
+                s.sel_trace[q * s.Rcap + ns] = tl;
+                s.tr.d_leaf[tbase + tl] = node; s.tr.d_lb[tbase + tl] = lb;
+                s.tr.d_searched[tbase + tl] = 1; s.tr.d_bsf_before[tbase + tl] = bsf; ++tl;
+            }
+            pre[ns] = nch;
+            nch += (int)((rows + CH - 1) / CH);
+            ++ns;
+            if (ns == s.R) break;
+        }
+        if (cur >= Nn) fin = true;
+        s.cursor[q] = cur;
+        if (s.want_trace) s.tr.d_len[q] = tl;
+        if (fin) s.done[q] = 1;
+        else atomicAdd(s.n_active, 1);
+    }
+    pre[ns] = nch;
+    s.n_sel[q] = ns;
+    s.chunk_off[q + 1] = nch;   // counts; turned into offsets by offsets_kernel
+}
+
+// Exclusive scan of per-query chunk counts (single CTA; Q is small).
+__global__ void offsets_kernel(long long* off, int64_t Q) {
+    __shared__ long long part[1024];
+    __shared__ long long carry;
+    if (threadIdx.x == 0) { carry = 0; off[0] = 0; }
+    __syncthreads();
+    for (int64_t base = 0; base < Q; base += blockDim.x) {
+        int64_t i = base + threadIdx.x;
+        long long v = i < Q ? off[i + 1] : 0;
+        part[threadIdx.x] = v;
+        __syncthreads();
+        for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+            long long add = threadIdx.x >= (unsigned)o ? part[threadIdx.x - o] : 0;
+            __syncthreads();
+            part[threadIdx.x] += add;
+            __syncthreads();
+        }
+        if (i < Q) off[i + 1] = carry + part[threadIdx.x];
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry += part[threadIdx.x];
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- scan ----
+// Each lane owns VEC float4 slots of the series (slot v = lane + 32*u), so one
+// warp reads a row with fully coalesced 128-bit loads.
+template <int VEC>
+__device__ inline void load_query(const float* qrow, int m4, int lane, double (&qv)[VEC][4]) {
+#pragma unroll
+    for (int u = 0; u < VEC; ++u) {
+        int v = lane + 32 * u;
+        float4 x = v < m4 ? reinterpret_cast<const float4*>(qrow)[v] : make_float4(0.f, 0.f, 0.f, 0.f);
+        qv[u][0] = x.x; qv[u][1] = x.y; qv[u][2] = x.z; qv[u][3] = x.w;
+    }
+}
+
+template <int VEC>
+__device__ inline double row_partial(const float4 (&x)[VEC], const double (&qv)[VEC][4]) {
+    double acc = 0.0;
+#pragma unroll
+    for (int u = 0; u < VEC; ++u) {
+        double d0 = (double)x[u].x - qv[u][0];
+        double d1 = (double)x[u].y - qv[u][1];
+        double d2 = (double)x[u].z - qv[u][2];
+        double d3 = (double)x[u].w - qv[u][3];
+        acc = __fma_rn(d0, d0, acc);
+        acc = __fma_rn(d1, d1, acc);
+        acc = __fma_rn(d2, d2, acc);
+        acc = __fma_rn(d3, d3, acc);
+    }
+    return acc;
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(SCAN_THREADS) scan_kernel(RoundState s, lf_index idx,
+                                                            const float* __restrict__ queries) {
+    __shared__ double sd[CH];
+    __shared__ long long sid[CH];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long total = s.chunk_off[s.Q];
+    const int m = idx.m, m4 = m >> 2;
+    const bool vec_ok = (m & 3) == 0;
+    for (long long t = blockIdx.x; t < total; t += gridDim.x) {
+        // locate (query, selected leaf, chunk)
+        int64_t lo = 0, hi = s.Q;               // chunk_off[lo] <= t < chunk_off[hi]
+        while (hi - lo > 1) {
+            int64_t mid = (lo + hi) >> 1;
+            if (s.chunk_off[mid] <= t) lo = mid; else hi = mid;
+        }
+        const int64_t q = lo;
+        const int local = (int)(t - s.chunk_off[q]);
+        const int* pre = s.sel_pre + q * (s.Rcap + 1);
+        int j = 0;
+        while (pre[j + 1] <= local) ++j;
+        const int leaf = s.sel_leaf[q * s.Rcap + j];
+        const int c = local - pre[j];
+        const int64_t lbeg = idx.d_leaf_ptr[leaf], lend = idx.d_leaf_ptr[leaf + 1];
+        const int64_t r0 = lbeg + (int64_t)c * CH;
+        const int nrows = (int)min((int64_t)CH, lend - r0);
+        const double bsf = query_bsf(s, q);
+        const float* qrow = queries + q * m;
+
+        if (vec_ok) {
+            double qv[VEC][4];
+            load_query<VEC>(qrow, m4, lane, qv);
+            int r = warp;
+            for (; r + SCAN_WARPS < nrows; r += 2 * SCAN_WARPS) {
+                float4 xa[VEC], xb[VEC];
+                const float4* pa = reinterpret_cast<const float4*>(idx.d_X + (r0 + r) * m);
+                const float4* pb = reinterpret_cast<const float4*>(idx.d_X + (r0 + r + SCAN_WARPS) * m);
+#pragma unroll
+                for (int u = 0; u < VEC; ++u) {
+                    int v = lane + 32 * u;
+                    xa[u] = v < m4 ? __ldcs(pa + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    xb[u] = v < m4 ? __ldcs(pb + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+                double a = warp_sum_f64(row_partial<VEC>(xa, qv));
+                double b = warp_sum_f64(row_partial<VEC>(xb, qv));
+                if (lane == 0) {
+                    sd[r] = sqrt(a); sid[r] = idx.d_row_id[r0 + r];
+                    sd[r + SCAN_WARPS] = sqrt(b); sid[r + SCAN_WARPS] = idx.d_row_id[r0 + r + SCAN_WARPS];
+                }
+            }
+            for (; r < nrows; r += SCAN_WARPS) {
+                float4 xa[VEC];
+                const float4* pa = reinterpret_cast<const float4*>(idx.d_X + (r0 + r) * m);
+#pragma unroll
+                for (int u = 0; u < VEC; ++u) {
+                    int v = lane + 32 * u;
+                    xa[u] = v < m4 ? __ldcs(pa + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+                double a = warp_sum_f64(row_partial<VEC>(xa, qv));
+                if (lane == 0) { sd[r] = sqrt(a); sid[r] = idx.d_row_id[r0 + r]; }
+            }
+        } else {
+            for (int r = warp; r < nrows; r += SCAN_WARPS) {
+                const float* x = idx.d_X + (r0 + r) * m;
+                double acc = 0.0;
+                for (int i = lane; i < m; i += 32) {
+                    double d = (double)x[i] - (double)qrow[i];
+                    acc = __fma_rn(d, d, acc);
+                }
+                acc = warp_sum_f64(acc);
+                if (lane == 0) { sd[r] = sqrt(acc); sid[r] = idx.d_row_id[r0 + r]; }
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+            double* cd = s.cand_d + t * s.kc;
+            long long* ci = s.cand_i + t * s.kc;
+            if (s.want_trace) {
+                double mn = kInf;
+                for (int i = lane; i < nrows; i += 32) mn = fmin(mn, sd[i]);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                if (lane == 0) s.task_min[t] = mn;
+            }
+            // drop what cannot enter the top-k (tree.py:207 keeps d <= bsf)
+            for (int i = lane; i < nrows; i += 32)
+                if (!(sd[i] <= bsf)) sd[i] = kInf;
+            __syncwarp();
+            if (s.kc >= nrows) {
+                for (int i = lane; i < s.kc; i += 32) {
+                    cd[i] = i < nrows ? sd[i] : kInf;
+                    ci[i] = (i < nrows && sd[i] != kInf) ? sid[i] : -1;
+                }
+            } else {
+                for (int sel = 0; sel < s.kc; ++sel) {
+                    double bd = kInf; long long bi = LLONG_MAX; int bp = -1;
+                    for (int i = lane; i < nrows; i += 32) {
+                        if (pair_less(sd[i], sid[i], bd, bi)) { bd = sd[i]; bi = sid[i]; bp = i; }
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        double od = __shfl_xor_sync(0xffffffffu, bd, o);
+                        long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                        int op = __shfl_xor_sync(0xffffffffu, bp, o);
+                        if (pair_less(od, oi, bd, bi)) { bd = od; bi = oi; bp = op; }
+                    }
+                    if (lane == 0) {
+                        cd[sel] = bd;
+                        ci[sel] = (bd == kInf) ? -1 : bi;
+                        if (bp >= 0) { sd[bp] = kInf; sid[bp] = LLONG_MAX; }
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// --------------------------------------------------------------- merge ----
+// One warp per query: k smallest (d, id) among the running top-k and this
+// round's candidates (each series is scanned at most once per query, so all
+// (d, id) pairs are distinct and repeated "next larger than the last pick"
+// selection is exact).  Reads top_* (round-start state), writes top_*_out.
+__global__ void merge_kernel(RoundState s) {
+    const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (q >= s.Q) return;
+    const int ns = s.n_sel[q];
+    const double* td = s.top_d + q * s.k;
+    const long long* ti = s.top_i + q * s.k;
+    double* od = s.top_d_out + q * s.k;
+    long long* oi = s.top_i_out + q * s.k;
+    const int tn = s.top_n[q];
+    if (ns == 0) {
+        for (int i = lane; i < tn; i += 32) { od[i] = td[i]; oi[i] = ti[i]; }
+        if (lane == 0) s.top_n_out[q] = tn;
+        return;
+    }
+    const long long c0 = s.chunk_off[q], c1 = s.chunk_off[q + 1];
+    const long long nc = (c1 - c0) * s.kc;
+    const double* cd = s.cand_d + c0 * s.kc;
+    const long long* ci = s.cand_i + c0 * s.kc;
+
+    if (s.want_trace) {
+        const int* pre = s.sel_pre + q * (s.Rcap + 1);
+        for (int j = lane; j < ns; j += 32) {
+            double mn = kInf;
+            for (int c = pre[j]; c < pre[j + 1]; ++c) mn = fmin(mn, s.task_min[c0 + c]);
+            const int te = s.sel_trace[q * s.Rcap + j];
+            s.tr.d_leaf_nn[q * (int64_t)s.n_leaves + te] = mn;
+        }
+    }
+
+    double last_d = -1.0;
+    long long last_i = -1;
+    int filled = 0;
+    for (int sel = 0; sel < s.k; ++sel) {
+        double bd = kInf;
+        long long bi = LLONG_MAX;
+        for (int i = lane; i < tn; i += 32) {
+            const double d = td[i];
+            const long long id = ti[i];
+            if (pair_less(last_d, last_i, d, id) && pair_less(d, id, bd, bi)) { bd = d; bi = id; }
+        }
+        for (long long i = lane; i < nc; i += 32) {
+            const long long id = ci[i];
+            if (id < 0) continue;
+            const double d = cd[i];
+            if (pair_less(last_d, last_i, d, id) && pair_less(d, id, bd, bi)) { bd = d; bi = id; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double xd = __shfl_xor_sync(0xffffffffu, bd, o);
+            const long long xi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (pair_less(xd, xi, bd, bi)) { bd = xd; bi = xi; }
+        }
+        if (bi == LLONG_MAX) break;
+        if (lane == 0) { od[sel] = bd; oi[sel] = bi; }
+        last_d = bd;
+        last_i = bi;
+        ++filled;
+    }
+    if (lane == 0) s.top_n_out[q] = filled;
+}
+
+__global__ void init_state_kernel(RoundState s) {
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= s.Q) return;
+    s.cursor[q] = 0;
+    s.done[q] = 0;
+    s.top_n[q] = 0;
+    for (int i = 0; i < LF_N_STATS; ++i) s.stats[q * LF_N_STATS + i] = 0;
+    if (s.want_trace) s.tr.d_len[q] = 0;
+}
+
+__global__ void finish_kernel(RoundState s, int64_t* out_ids, double* out_d) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= s.Q * s.k) return;
+    int64_t q = t / s.k;
+    int i = (int)(t - q * s.k);
+    bool ok = i < s.top_n[q];
+    out_ids[t] = ok ? s.top_i[t] : -1;
+    out_d[t] = ok ? s.top_d[t] : kInf;
+}
+
+template <int VEC>
+static cudaError_t launch_scan(const RoundState& s, const lf_index& idx, const float* q, int grid,
+                               cudaStream_t st) {
+    scan_kernel<VEC><<<grid, SCAN_THREADS, 0, st>>>(s, idx, q);
+    return cudaGetLastError();
+}
+
+int run_search(const lf_index& idx, const float* d_q, int64_t Q, const lf_search_opts& o,
+               int64_t* out_ids, double* out_d, int64_t* out_stats, const lf_trace* trace,
+               cudaStream_t st) {
+    const int Nn = idx.n_nodes;
+    RoundState s{};
+    s.Q = Q;
+    s.k = o.k;
+    s.kc = std::min(o.k, CH);
+    s.f = o.bsf_factor;
+    s.Rcap = o.sequential ? 1 : std::max(1, std::min(o.max_round_leaves, idx.n_leaves));
+    s.pred = o.d_pred;
+    s.pred64 = o.d_pred_f64;
+    s.offset = o.d_offset;
+    s.F = o.n_filters;
+    s.want_trace = (o.want_trace && trace != nullptr) ? 1 : 0;
+    if (s.want_trace) s.tr = *trace;
+    s.n_leaves = idx.n_leaves;
+    s.stats = reinterpret_cast<long long*>(out_stats);
+
+    const int64_t max_chunks_leaf = (idx.max_leaf_rows + CH - 1) / CH;
+    const int64_t max_tasks = std::max<int64_t>(1, Q * s.Rcap * max_chunks_leaf);
+
+    Scratch qsumm, lb, lbs, order, cursor, done, topd, topi, topn, topd2, topi2, topn2, sel_leaf,
+        sel_trace, sel_pre, n_sel, chunk_off, cand_d, cand_i, task_min, n_active;
+    LF_CUDA(qsumm.alloc(sizeof(double) * Q * idx.n_seg, st));
+    LF_CUDA(lb.alloc(sizeof(double) * Q * Nn, st));
+    LF_CUDA(lbs.alloc(sizeof(double) * Q * Nn, st));
+    LF_CUDA(order.alloc(sizeof(int) * Q * Nn, st));
+    LF_CUDA(cursor.alloc(sizeof(int) * Q, st));
+    LF_CUDA(done.alloc(sizeof(int) * Q, st));
+    LF_CUDA(topd.alloc(sizeof(double) * Q * s.k, st));
+    LF_CUDA(topi.alloc(sizeof(long long) * Q * s.k, st));
+    LF_CUDA(topn.alloc(sizeof(int) * Q, st));
+    LF_CUDA(topd2.alloc(sizeof(double) * Q * s.k, st));
+    LF_CUDA(topi2.alloc(sizeof(long long) * Q * s.k, st));
+    LF_CUDA(topn2.alloc(sizeof(int) * Q, st));
+    LF_CUDA(sel_leaf.alloc(sizeof(int) * Q * s.Rcap, st));
+    LF_CUDA(sel_trace.alloc(sizeof(int) * Q * s.Rcap, st));
+    LF_CUDA(sel_pre.alloc(sizeof(int) * Q * (s.Rcap + 1), st));
+    LF_CUDA(n_sel.alloc(sizeof(int) * Q, st));
+    LF_CUDA(chunk_off.alloc(sizeof(long long) * (Q + 1), st));
+    LF_CUDA(cand_d.alloc(sizeof(double) * max_tasks * s.kc, st));
+    LF_CUDA(cand_i.alloc(sizeof(long long) * max_tasks * s.kc, st));
+    LF_CUDA(task_min.alloc(sizeof(double) * (s.want_trace ? max_tasks : 1), st));
+    LF_CUDA(n_active.alloc(sizeof(int), st));
+
+    int rc = launch_bounds(d_q, Q, idx, idx.d_env_min, idx.d_env_max, Nn, 0, qsumm.as<double>(),
+                           lb.as<double>(), st);
+    if (rc) return rc;
+    rc = sort_visit_order(lb.as<double>(), Q, Nn, lbs.as<double>(), order.as<int>(), st);
+    if (rc) return rc;
+
+    s.order = order.as<int>();
+    s.lbs = lbs.as<double>();
+    s.cursor = cursor.as<int>();
+    s.done = done.as<int>();
+    s.top_d = topd.as<double>();
+    s.top_i = topi.as<long long>();
+    s.top_n = topn.as<int>();
+    s.top_d_out = topd2.as<double>();
+    s.top_i_out = topi2.as<long long>();
+    s.top_n_out = topn2.as<int>();
+    s.sel_leaf = sel_leaf.as<int>();
+    s.sel_trace = sel_trace.as<int>();
+    s.sel_pre = sel_pre.as<int>();
+    s.n_sel = n_sel.as<int>();
+    s.chunk_off = chunk_off.as<long long>();
+    s.cand_d = cand_d.as<double>();
+    s.cand_i = cand_i.as<long long>();
+    s.task_min = task_min.as<double>();
+    s.n_active = n_active.as<int>();
+
+    const unsigned qb = (unsigned)((Q + 127) / 128);
+    init_state_kernel<<<qb, 128, 0, st>>>(s);
+    LF_CUDA(cudaGetLastError());
+
+    int* h_active = nullptr;
+    LF_CUDA(cudaMallocHost(&h_active, sizeof(int)));
+    const int grid = sm_count() * 4;
+    const int m4 = idx.m / 4;
+    int err = LF_OK;
+    for (int round = 0;; ++round) {
+        s.R = o.sequential ? 1 : (int)std::min<int64_t>(s.Rcap, (int64_t)1 << std::min(round, 30));
+        if (cudaMemsetAsync(s.n_active, 0, sizeof(int), st) != cudaSuccess) { err = fail(LF_ECUDA, "memset"); break; }
+        plan_kernel<<<qb, 128, 0, st>>>(s, idx);
+        offsets_kernel<<<1, 1024, 0, st>>>(s.chunk_off, Q);
+        cudaError_t ce;
+        if ((idx.m & 3) != 0 || m4 <= 32) ce = launch_scan<1>(s, idx, d_q, grid, st);
+        else if (m4 <= 64) ce = launch_scan<2>(s, idx, d_q, grid, st);
+        else if (m4 <= 128) ce = launch_scan<4>(s, idx, d_q, grid, st);
+        else if (m4 <= 256) ce = launch_scan<8>(s, idx, d_q, grid, st);
+        else { err = fail(LF_EINVAL, "series length > 1024 not supported"); break; }
+        if (ce != cudaSuccess) { err = fail(LF_ECUDA, cudaGetErrorString(ce)); break; }
+        merge_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s);
+        if ((ce = cudaGetLastError()) != cudaSuccess) { err = fail(LF_ECUDA, cudaGetErrorString(ce)); break; }
+        std::swap(s.top_d, s.top_d_out);
+        std::swap(s.top_i, s.top_i_out);
+        std::swap(s.top_n, s.top_n_out);
+        if (cudaMemcpyAsync(h_active, s.n_active, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess) {
+            err = fail(LF_ECUDA, "round sync failed");
+            break;
+        }
+        if (*h_active == 0) break;
+    }
+    if (err == LF_OK) {
+        int64_t n = Q * s.k;
+        finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s, out_ids, out_d);
+        cudaError_t ce = cudaGetLastError();
+        if (ce != cudaSuccess) err = fail(LF_ECUDA, cudaGetErrorString(ce));
+    }
+    cudaFreeHost(h_active);
+    return err;
+}
+
+}  // namespace lf
+
+extern "C" int lf_search(const lf_index* idx, const float* d_queries, int64_t Q,
+                         const lf_search_opts* opts, int64_t* d_out_ids, double* d_out_dists,
+                         int64_t* d_out_stats, const lf_trace* trace, void* stream) {
+    LF_REQUIRE(idx != nullptr && opts != nullptr, "NULL argument");
+    LF_REQUIRE(Q >= 0, "negative query count");
+    LF_REQUIRE(opts->k >= 1 && opts->k <= idx->n_series, "k must be in [1, n]");
+    LF_REQUIRE(idx->n_seg >= 1 && idx->n_seg <= LF_MAX_SEG, "bad segment count");
+    LF_REQUIRE((opts->d_pred == nullptr && opts->d_pred_f64 == nullptr) ||
+                   (opts->d_offset != nullptr && idx->d_leaf_filter != nullptr),
+               "filter predictions need offsets and a leaf->filter map");
+    LF_REQUIRE(opts->sequential || opts->max_round_leaves >= 1, "max_round_leaves must be >= 1");
+    if (Q == 0) return LF_OK;
+    return lf::run_search(*idx, d_queries, Q, *opts, d_out_ids, d_out_dists, d_out_stats, trace,
+                          lf::as_stream(stream));
+}

@@ -1,0 +1,90 @@
+"""The learned filters of an index as one device pack, and their inference.
+
+Reference: one `MlpModel` per selected leaf (mlp.py:52-102), wired into the
+search as a dict of per-leaf callables (enhanced.py:120, tree.py:278-286).
+Here all F filters live in stacked HBM tensors (W1 [F, m, m] in the
+reference's `x @ W1` layout, b1 [F, m], W2 [F, m], b2 [F], fp32) and one
+`lf_filter_predict` launch evaluates every (query, filter) pair.  The kernel
+is batch-invariant, so the predictions used to calibrate offsets and the
+ones used to search are bit-identical (enhanced.py:283-285).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+
+
+class FilterPack:
+    def __init__(self, leaf_ids, W1, b1, W2, b2, device=None):
+        torch = _lib.require_cuda()
+        dev = torch.device(device if device is not None else "cuda")
+        self.leaf_ids = [int(l) for l in leaf_ids]
+        if sorted(self.leaf_ids) != self.leaf_ids:
+            raise ValueError("filter leaf ids must be ascending")
+
+        def t(a, shape):
+            x = torch.as_tensor(np.asarray(a, dtype=np.float32) if not isinstance(a, torch.Tensor) else a,
+                                dtype=torch.float32).to(dev).contiguous()
+            if tuple(x.shape) != shape:
+                raise ValueError(f"filter tensor shape {tuple(x.shape)} != {shape}")
+            return x
+
+        F = len(self.leaf_ids)
+        m = int(np.shape(W1)[-1]) if F else 0
+        self.m = m
+        self.W1 = t(W1, (F, m, m))
+        self.b1 = t(b1, (F, m))
+        self.W2 = t(W2, (F, m))
+        self.b2 = t(b2, (F,))
+        self.device = dev
+        self._slot_maps = {}
+
+    @property
+    def n_filters(self) -> int:
+        return len(self.leaf_ids)
+
+    @classmethod
+    def from_models(cls, models: dict, device=None) -> "FilterPack":
+        """From {leaf_id: model} where model has W1, b1, W2, b2 (reference MlpModel)."""
+        ids = sorted(int(l) for l in models)
+        if not ids:
+            return cls([], np.zeros((0, 0, 0)), np.zeros((0, 0)), np.zeros((0, 0)), np.zeros(0), device)
+        W1 = np.stack([np.asarray(models[l].W1, dtype=np.float32) for l in ids])
+        b1 = np.stack([np.asarray(models[l].b1, dtype=np.float32) for l in ids])
+        W2 = np.stack([np.asarray(models[l].W2, dtype=np.float32) for l in ids])
+        b2 = np.array([np.float32(models[l].b2) for l in ids], dtype=np.float32)
+        return cls(ids, W1, b1, W2, b2, device)
+
+    def predict(self, queries, stream=None):
+        """fp32 [Q, F] predictions for device (or host) queries."""
+        torch = _lib.require_cuda()
+        if isinstance(queries, torch.Tensor):
+            q = queries.to(device=self.device, dtype=torch.float32).contiguous()
+        else:
+            q = torch.from_numpy(np.ascontiguousarray(np.atleast_2d(queries), dtype=np.float32)).to(self.device)
+        Q = q.shape[0]
+        out = torch.empty((Q, self.n_filters), dtype=torch.float32, device=self.device)
+        if Q and self.n_filters:
+            if q.shape[1] != self.m:
+                raise ValueError(f"input shape {tuple(q.shape)} does not match model dim {self.m}")
+            _lib.check(_lib.lib().lf_filter_predict(q.data_ptr(), Q, self.m, self.W1.data_ptr(),
+                                                    self.b1.data_ptr(), self.W2.data_ptr(),
+                                                    self.b2.data_ptr(), self.n_filters,
+                                                    out.data_ptr(), _lib.stream_ptr(stream)))
+        return out
+
+    def leaf_filter(self, dindex):
+        """int32 [n_leaves]: filter slot of each leaf slot of a DeviceIndex, -1 if none."""
+        torch = _lib.require_cuda()
+        key = id(dindex)
+        if key not in self._slot_maps:
+            m = np.full(dindex.n_leaves, -1, dtype=np.int32)
+            for s, lid in enumerate(self.leaf_ids):
+                j = dindex.slot_of_leaf.get(lid)
+                if j is None:
+                    raise ValueError(f"filter leaf {lid} does not exist in the index")
+                m[j] = s
+            self._slot_maps[key] = torch.from_numpy(m).to(self.device)
+        return self._slot_maps[key]

@@ -1,0 +1,248 @@
+"""Host image of the summarization tree and its HBM layout.
+
+`TreeIndex` carries the same node table as the reference `tree.Index`
+(tree.py:93-122): envelopes over segment means, split rules, leaf members.
+It is produced by the native builder (`build_index`, bit-identical to
+tree.build_index, tree.py:164-189) or adopted from a reference Index object
+(`TreeIndex.from_reference`, duck-typed; the drop-in path).
+
+`DeviceIndex` is the HBM layout the kernels read:
+
+* ``X``        fp32 [n, m], LEAF-CONTIGUOUS: leaves in ascending node id,
+               members in ascending series id (tree.py:102-106);
+* ``row_id``   int64 [n]: original series id of every row;
+* ``leaf_ptr`` int64 [L+1]: row range of leaf slot j;
+* ``node_leaf`` int32 [nodes]: leaf slot of a node, -1 for internal nodes;
+* ``env_min`` / ``env_max`` fp64 [segments][nodes], structure-of-arrays so
+  one warp reads one segment of 32 consecutive nodes in one transaction.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+
+
+def segment_layout(m: int, n_seg: int) -> tuple:
+    """Equal widths, leading segments +1 (summarize.py:27-37)."""
+    if not 1 <= n_seg <= m:
+        raise ValueError(f"num_segments must be in [1, length], got {n_seg} for length {m}")
+    base, rem = divmod(m, n_seg)
+    widths = np.full(n_seg, base, dtype=np.int64)
+    widths[:rem] += 1
+    starts = np.zeros(n_seg, dtype=np.int64)
+    starts[1:] = np.cumsum(widths)[:-1]
+    return starts, widths
+
+
+def as_f32_rows(values) -> np.ndarray:
+    """fp32 storage of a collection; the reference keeps fp32-exact values (series.py:48-50)."""
+    v = np.asarray(values)
+    if v.ndim != 2:
+        raise ValueError(f"dataset values must be 2-d, got shape {v.shape}")
+    if v.dtype == np.float32:
+        return np.ascontiguousarray(v)
+    v32 = np.ascontiguousarray(v, dtype=np.float32)
+    if not np.array_equal(v32.astype(v.dtype), v):
+        raise ValueError("dataset values are not fp32-exact (quantize with series.quantize32 first)")
+    return v32
+
+
+@dataclass
+class TreeIndex:
+    values: np.ndarray              # fp32 [n, m], original row order
+    starts: np.ndarray
+    widths: np.ndarray
+    max_leaf_size: int
+    env_min: np.ndarray             # fp64 [nodes, segments]
+    env_max: np.ndarray
+    left: np.ndarray                # int32 [nodes], -1 for leaves
+    right: np.ndarray
+    split_seg: np.ndarray
+    split_thr: np.ndarray
+    size: np.ndarray                # int64 [nodes]
+    oversized: np.ndarray           # bool [nodes]
+    member_ptr: np.ndarray          # int64 [nodes + 1]; internal nodes have empty ranges
+    members: np.ndarray             # int64 [n]
+    _device: dict = field(default_factory=dict, repr=False, compare=False)
+
+    # ------------------------------------------------------------- shape --
+    @property
+    def n(self) -> int:
+        return int(self.values.shape[0])
+
+    @property
+    def m(self) -> int:
+        return int(self.values.shape[1])
+
+    @property
+    def n_seg(self) -> int:
+        return int(self.widths.shape[0])
+
+    @property
+    def n_nodes(self) -> int:
+        return int(self.left.shape[0])
+
+    @property
+    def is_leaf(self) -> np.ndarray:
+        return self.left < 0
+
+    @property
+    def leaf_ids(self) -> np.ndarray:
+        return np.nonzero(self.is_leaf)[0].astype(np.int64)
+
+    @property
+    def n_leaves(self) -> int:
+        return int(self.is_leaf.sum())
+
+    def leaf_members(self, leaf_id: int) -> np.ndarray:
+        return self.members[self.member_ptr[leaf_id]:self.member_ptr[leaf_id + 1]]
+
+    def leaf_sizes(self) -> list:
+        """(leaf id, size) pairs in ascending leaf id (tree.py:112-113)."""
+        return [(int(l), int(self.size[l])) for l in self.leaf_ids]
+
+    def has_oversized_leaves(self) -> bool:
+        return bool(self.oversized[self.is_leaf].any())
+
+    # ------------------------------------------------------ constructors --
+    @classmethod
+    def from_reference(cls, index) -> "TreeIndex":
+        """Adopt a reference `tree.Index` (duck-typed) without copying its tree logic."""
+        nodes = index.nodes
+        l = int(index.cfg.num_segments)
+        nn = len(nodes)
+        members = [nd.members if nd.members is not None else [] for nd in nodes]
+        ptr = np.zeros(nn + 1, dtype=np.int64)
+        ptr[1:] = np.cumsum([len(mm) for mm in members])
+        flat = np.fromiter((i for mm in members for i in mm), dtype=np.int64, count=int(ptr[-1]))
+        t = cls(
+            values=as_f32_rows(index.dataset.values),
+            starts=np.asarray(index.cfg.starts, dtype=np.int64),
+            widths=np.asarray(index.cfg.widths, dtype=np.int64),
+            max_leaf_size=int(index.max_leaf_size),
+            env_min=np.stack([np.asarray(nd.envelope.mean_min, dtype=np.float64) for nd in nodes]).reshape(nn, l),
+            env_max=np.stack([np.asarray(nd.envelope.mean_max, dtype=np.float64) for nd in nodes]).reshape(nn, l),
+            left=np.array([-1 if nd.left is None else nd.left.node_id for nd in nodes], dtype=np.int32),
+            right=np.array([-1 if nd.right is None else nd.right.node_id for nd in nodes], dtype=np.int32),
+            split_seg=np.array([-1 if nd.split_segment is None else nd.split_segment for nd in nodes], dtype=np.int32),
+            split_thr=np.array([np.nan if nd.split_threshold is None else nd.split_threshold for nd in nodes]),
+            size=np.array([nd.size for nd in nodes], dtype=np.int64),
+            oversized=np.array([bool(nd.oversized) for nd in nodes]),
+            member_ptr=ptr,
+            members=flat,
+        )
+        return t
+
+    # ------------------------------------------------------------ device --
+    def device(self, device=None) -> "DeviceIndex":
+        torch = _lib.require_cuda()
+        dev = torch.device(device if device is not None else "cuda")
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        key = str(dev)
+        if key not in self._device:
+            self._device[key] = DeviceIndex(self, dev)
+        return self._device[key]
+
+
+def build_index(values, max_leaf_size: int = 1000, segments: int = 8,
+                n_threads: int | None = None) -> TreeIndex:
+    """Native tree build, bit-identical to tree.build_index (tree.py:164-189)."""
+    if max_leaf_size < 2:
+        raise ValueError(f"max_leaf_size must be >= 2, got {max_leaf_size}")
+    v = as_f32_rows(values)
+    n, m = v.shape
+    if n < 1 or m < 2:
+        raise ValueError(f"dataset needs n >= 1 and m >= 2, got {v.shape}")
+    if not np.isfinite(v).all():
+        raise ValueError("dataset contains non-finite values")
+    starts, widths = segment_layout(m, segments)
+    L = _lib.lib()
+    h = L.lf_tree_build(_lib.ptr(v), n, m, segments, max_leaf_size, n_threads or _lib.threads())
+    if not h:
+        _lib.check(_lib.LF_EINVAL)
+    try:
+        nn, nl = C.c_int32(), C.c_int32()
+        _lib.check(L.lf_tree_info(h, C.byref(nn), C.byref(nl)))
+        k = nn.value
+        env_min = np.empty((k, segments)); env_max = np.empty((k, segments))
+        left = np.empty(k, np.int32); right = np.empty(k, np.int32)
+        sseg = np.empty(k, np.int32); sthr = np.empty(k)
+        size = np.empty(k, np.int64); over = np.empty(k, np.int8)
+        mptr = np.empty(k + 1, np.int64); mem = np.empty(n, np.int64)
+        _lib.check(L.lf_tree_export(h, *(_lib.ptr(a) for a in (env_min, env_max, left, right, sseg,
+                                                              sthr, size, over, mptr, mem))))
+    finally:
+        L.lf_tree_free(h)
+    return TreeIndex(v, starts, widths, int(max_leaf_size), env_min, env_max, left, right, sseg, sthr,
+                     size, over.astype(bool), mptr, mem)
+
+
+def segment_means(values, segments: int = 8) -> np.ndarray:
+    """Host segment means in numpy's reduceat order (summarize.py:52-56)."""
+    v = as_f32_rows(np.atleast_2d(values))
+    out = np.empty((v.shape[0], segments))
+    _lib.check(_lib.lib().lf_paa_host(_lib.ptr(v), v.shape[0], v.shape[1], segments, _lib.ptr(out),
+                                      _lib.threads()))
+    return out
+
+
+class DeviceIndex:
+    """The tree in HBM (see module docstring for the layout)."""
+
+    def __init__(self, t: TreeIndex, dev):
+        import torch
+
+        self.tree = t
+        self.device = dev
+        leaf_ids = t.leaf_ids
+        sizes = t.member_ptr[leaf_ids + 1] - t.member_ptr[leaf_ids]
+        leaf_ptr = np.zeros(leaf_ids.shape[0] + 1, dtype=np.int64)
+        leaf_ptr[1:] = np.cumsum(sizes)
+        order = np.concatenate([t.leaf_members(l) for l in leaf_ids]) if leaf_ids.size else np.zeros(0, np.int64)
+        node_leaf = np.full(t.n_nodes, -1, dtype=np.int32)
+        node_leaf[leaf_ids] = np.arange(leaf_ids.shape[0], dtype=np.int32)
+        with torch.cuda.device(dev):
+            rid = torch.from_numpy(order).to(dev)
+            src = torch.from_numpy(t.values).to(dev)
+            self.X = src.index_select(0, rid).contiguous()
+            del src
+            self.row_id = rid
+            self.leaf_ptr = torch.from_numpy(leaf_ptr).to(dev)
+            self.node_leaf = torch.from_numpy(node_leaf).to(dev)
+            self.env_min = torch.from_numpy(np.ascontiguousarray(t.env_min.T)).to(dev)
+            self.env_max = torch.from_numpy(np.ascontiguousarray(t.env_max.T)).to(dev)
+        self.leaf_ids = leaf_ids
+        self.leaf_ptr_host = leaf_ptr
+        self.slot_of_leaf = {int(l): j for j, l in enumerate(leaf_ids)}
+        self.max_leaf_rows = int(sizes.max()) if sizes.size else 0
+
+    @property
+    def n_leaves(self) -> int:
+        return int(self.leaf_ids.shape[0])
+
+    def struct(self, leaf_filter=None) -> _lib.LfIndex:
+        t = self.tree
+        s = _lib.LfIndex()
+        s.n_series = t.n
+        s.m = t.m
+        s.n_seg = t.n_seg
+        s.n_nodes = t.n_nodes
+        s.n_leaves = self.n_leaves
+        s.max_leaf_rows = self.max_leaf_rows
+        for i in range(t.n_seg):
+            s.seg_start[i] = int(t.starts[i])
+            s.seg_width[i] = int(t.widths[i])
+        s.d_X = self.X.data_ptr()
+        s.d_row_id = self.row_id.data_ptr()
+        s.d_leaf_ptr = self.leaf_ptr.data_ptr()
+        s.d_node_leaf = self.node_leaf.data_ptr()
+        s.d_env_min = self.env_min.data_ptr()
+        s.d_env_max = self.env_max.data_ptr()
+        s.d_leaf_filter = None if leaf_filter is None else leaf_filter.data_ptr()
+        return s

@@ -1,0 +1,225 @@
+"""Training-data generation on the GPU: exact query x leaf minimum distances.
+
+Mirrors the reference build seam:
+
+* ``collect_targets(index, selected_leaves, queries, calibration_count) ->
+  GlobalTrainSet`` (traingen.py:147-220) -- lower-bound matrix (bit-exact,
+  lf_bounds mode 1), stable visit order, pass 1 (every selected leaf x every
+  query, lf_leaf_min_dist), calibration tail against every leaf, and the
+  pass-2 nearest-neighbour walk (break on lb >= bsf, traingen.py:193-208);
+* ``collect_local_targets(index, local) -> LocalQueries`` (traingen.py:135-144);
+* ``local_targets_all`` -- every selected leaf's local queries in ONE launch
+  (the reference loops leaf by leaf, enhanced.py:258-262).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .engine import as_tree
+
+
+@dataclass
+class GlobalTrainSet:
+    """traingen.py:59-97 (same fields, shapes and column conventions)."""
+
+    queries: np.ndarray
+    selected_leaves: list
+    dl_selected: np.ndarray        # (n_global, n_selected)
+    nn_distance: np.ndarray
+    leaf_ids: np.ndarray
+    lb_matrix: np.ndarray          # (n_global, n_leaves)
+    visit_order: np.ndarray        # (n_global, n_leaves) int32 column positions
+    calibration_count: int
+    dl_calib_full: np.ndarray      # (calibration_count, n_leaves)
+
+    @property
+    def n_global(self) -> int:
+        return self.queries.shape[0]
+
+    @property
+    def train_pool_size(self) -> int:
+        return self.n_global - self.calibration_count
+
+    def leaf_column(self, leaf_id: int) -> int:
+        pos = int(np.searchsorted(self.leaf_ids, leaf_id))
+        if pos >= self.leaf_ids.shape[0] or self.leaf_ids[pos] != leaf_id:
+            raise KeyError(f"unknown leaf id {leaf_id}")
+        return pos
+
+    def selected_column(self, leaf_id: int) -> int:
+        try:
+            return self.selected_leaves.index(leaf_id)
+        except ValueError:
+            raise KeyError(f"leaf {leaf_id} was not selected") from None
+
+
+@dataclass
+class LocalQueries:
+    """traingen.py:49-56."""
+
+    leaf_id: int
+    queries: np.ndarray
+    levels: np.ndarray
+    source_ids: np.ndarray
+    targets: np.ndarray | None = None
+    lbs: np.ndarray | None = None
+
+
+_QCHUNK = 64 * 65535   # lf_leaf_min_dist query-tile grid limit
+
+
+def leaf_min_distances(index, queries, leaf_slots) -> "torch.Tensor":
+    """Device fp64 [Q, S]: min distance from each query to each leaf slot (lf_leaf_min_dist)."""
+    torch = _lib.require_cuda()
+    t = as_tree(index)
+    di = t.device()
+    q = queries if isinstance(queries, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(np.atleast_2d(queries), dtype=np.float32))
+    q = q.to(device=di.device, dtype=torch.float32).contiguous()
+    sel = torch.as_tensor(np.asarray(leaf_slots, dtype=np.int32)).to(di.device)
+    Q, S = q.shape[0], sel.shape[0]
+    out = torch.empty((Q, S), dtype=torch.float64, device=di.device)
+    st = di.struct(None)
+    for s0 in range(0, S, 65535):
+        s1 = min(S, s0 + 65535)
+        for q0 in range(0, Q, _QCHUNK):
+            q1 = min(Q, q0 + _QCHUNK)
+            _lib.check(_lib.lib().lf_leaf_min_dist(
+                q[q0:q1].data_ptr(), q1 - q0, st, sel[s0:s1].data_ptr(), s1 - s0,
+                out[q0:q1, s0:s1].data_ptr(), S, _lib.stream_ptr()))
+    return out
+
+
+def leaf_bounds(index, queries, mode: int = 1):
+    """(qsumm, lb) of queries against every LEAF envelope, columns in ascending leaf id."""
+    torch = _lib.require_cuda()
+    t = as_tree(index)
+    di = t.device()
+    leaf_ids = t.leaf_ids
+    if not hasattr(di, "_leaf_env"):
+        di._leaf_env = (torch.from_numpy(np.ascontiguousarray(t.env_min[leaf_ids].T)).to(di.device),
+                        torch.from_numpy(np.ascontiguousarray(t.env_max[leaf_ids].T)).to(di.device))
+    mn, mx = di._leaf_env
+    q = queries if isinstance(queries, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(np.atleast_2d(queries), dtype=np.float32))
+    q = q.to(device=di.device, dtype=torch.float32).contiguous()
+    Q = q.shape[0]
+    qs = torch.empty((Q, t.n_seg), dtype=torch.float64, device=di.device)
+    lb = torch.empty((Q, leaf_ids.shape[0]), dtype=torch.float64, device=di.device)
+    _lib.check(_lib.lib().lf_bounds(q.data_ptr(), Q, di.struct(None), mn.data_ptr(), mx.data_ptr(),
+                                    leaf_ids.shape[0], mode, qs.data_ptr(), lb.data_ptr(),
+                                    _lib.stream_ptr()))
+    return qs, lb
+
+
+def collect_targets(index, selected_leaves, queries, calibration_count: int) -> GlobalTrainSet:
+    """GPU twin of traingen.collect_targets (traingen.py:147-220)."""
+    torch = _lib.require_cuda()
+    t = as_tree(index)
+    di = t.device()
+    Qh = np.atleast_2d(np.asarray(queries, dtype=np.float64))
+    n_q = Qh.shape[0]
+    if not 1 <= calibration_count < n_q:
+        raise ValueError("calibration_count must be in [1, n_queries)")
+    selected = sorted(int(s) for s in selected_leaves)
+    leaf_ids = t.leaf_ids.astype(np.int64)
+    unknown = set(selected) - set(int(i) for i in leaf_ids)
+    if unknown:
+        raise ValueError(f"unknown leaf ids in selection: {sorted(unknown)}")
+    q = torch.from_numpy(Qh.astype(np.float32)).to(di.device)
+    _, lb = leaf_bounds(t, q, mode=1)
+    # stable sort: ties resolve to the smaller column = smaller leaf id (traingen.py:170-171)
+    order = torch.sort(lb, dim=1, stable=True).indices.to(torch.int32)
+    sel_slots = [di.slot_of_leaf[l] for l in selected]
+    dl_sel = leaf_min_distances(t, q, sel_slots) if selected else torch.empty((n_q, 0), dtype=torch.float64,
+                                                                              device=di.device)
+    c0 = n_q - calibration_count
+    L = leaf_ids.shape[0]
+    dcal = torch.empty((calibration_count, L), dtype=torch.float64, device=di.device)
+    sel_set = set(selected)
+    col_of = {l: c for c, l in enumerate(selected)}
+    sel_pos = [p for p, l in enumerate(leaf_ids) if int(l) in sel_set]
+    other_pos = [p for p, l in enumerate(leaf_ids) if int(l) not in sel_set]
+    if sel_pos:
+        dcal[:, sel_pos] = dl_sel[c0:, [col_of[int(leaf_ids[p])] for p in sel_pos]]
+    if other_pos:
+        dcal[:, other_pos] = leaf_min_distances(t, q[c0:], other_pos)
+    # pass 2 (traingen.py:190-208): walk the visit order, break on lb >= bsf
+    lbh = lb.cpu().numpy()
+    orh = order.cpu().numpy()
+    dsel_h = dl_sel.cpu().numpy()
+    nn = np.empty(n_q)
+    dcal_h = dcal.cpu().numpy()
+    nn[c0:] = dcal_h.min(axis=1)
+    if c0 > 0:
+        d_other = None
+        if other_pos:
+            d_other = np.full((c0, L), np.inf)
+            d_other[:, other_pos] = leaf_min_distances(t, q[:c0], other_pos).cpu().numpy()
+        dfull = np.full((c0, L), np.inf)
+        if sel_pos:
+            dfull[:, sel_pos] = dsel_h[:c0, [col_of[int(leaf_ids[p])] for p in sel_pos]]
+        if d_other is not None:
+            dfull[:, other_pos] = d_other[:, other_pos]
+        bsf = dsel_h[:c0].min(axis=1) if selected else np.full(c0, np.inf)
+        alive = np.ones(c0, dtype=bool)
+        rows = np.arange(c0)
+        for p in range(L):
+            col = orh[:c0, p]
+            lbp = lbh[rows, col]
+            alive &= ~(lbp >= bsf)
+            if not alive.any():
+                break
+            np.minimum(bsf, np.where(alive, dfull[rows, col], np.inf), out=bsf)
+        nn[:c0] = bsf
+    return GlobalTrainSet(Qh, selected, dsel_h, nn, leaf_ids, lbh, orh, calibration_count, dcal_h)
+
+
+def collect_local_targets(index, local: LocalQueries) -> LocalQueries:
+    """GPU twin of traingen.collect_local_targets (traingen.py:135-144)."""
+    t = as_tree(index)
+    res = local_targets_all(t, {local.leaf_id: local.queries})
+    local.targets, local.lbs = res[local.leaf_id]
+    return local
+
+
+def own_leaf_bounds(t, leaf_id: int, queries: np.ndarray) -> np.ndarray:
+    """lb of each query against one leaf envelope, in the einsum order of
+    lower_bounds_batch (summarize.py:114-122): sum_s (g_s * g_s) * w_s, s ascending."""
+    from .index import segment_means
+
+    qs = segment_means(queries, t.n_seg)
+    g = np.maximum(t.env_min[leaf_id][None, :] - qs, qs - t.env_max[leaf_id][None, :])
+    g = np.maximum(g, 0.0)
+    acc = np.zeros(qs.shape[0])
+    w = t.widths.astype(np.float64)
+    for s in range(t.n_seg):
+        acc = acc + (g[:, s] * g[:, s]) * w[s]
+    return np.sqrt(acc)
+
+
+def local_targets_all(index, queries_by_leaf: dict) -> dict:
+    """{leaf_id: queries} -> {leaf_id: (targets, lbs)} in one lf_local_min_dist launch per 65535 leaves."""
+    torch = _lib.require_cuda()
+    t = as_tree(index)
+    di = t.device()
+    leaves = list(queries_by_leaf)
+    out = {}
+    for g0 in range(0, len(leaves), 65535):
+        grp = leaves[g0:g0 + 65535]
+        qs = [np.atleast_2d(np.asarray(queries_by_leaf[l], dtype=np.float64)) for l in grp]
+        qptr = np.zeros(len(grp) + 1, dtype=np.int64)
+        qptr[1:] = np.cumsum([a.shape[0] for a in qs])
+        allq = torch.from_numpy(np.concatenate(qs).astype(np.float32)).to(di.device)
+        gleaf = np.array([di.slot_of_leaf[int(l)] for l in grp], dtype=np.int32)
+        dl = torch.empty(int(qptr[-1]), dtype=torch.float64, device=di.device)
+        _lib.check(_lib.lib().lf_local_min_dist(allq.data_ptr(), di.struct(None), _lib.ptr(qptr),
+                                                _lib.ptr(gleaf), len(grp), dl.data_ptr(), _lib.stream_ptr()))
+        dlh = dl.cpu().numpy()
+        for gi, l in enumerate(grp):
+            out[l] = (dlh[qptr[gi]:qptr[gi + 1]], own_leaf_bounds(t, l, qs[gi]))
+    return out

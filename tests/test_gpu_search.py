@@ -1,0 +1,249 @@
+"""GPU parity of the search path against the oracle and the reference's golden
+vectors.  Every call goes through the C-ABI library (lf_search, lf_bounds,
+lf_filter_predict, lf_batch_distances).
+
+Tolerances: ids, counters, visit order and bounds are exact.  Distances are
+fp64 direct-form sums in a different order than numpy's einsum, so they are
+compared at rel 1e-12 (the bar in north_star is 1e-4).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import leafi_oracle as lo
+
+pytestmark = pytest.mark.gpu
+
+DIST_RTOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def small_tree():
+    from paper_2502_01836_b200 import build_index
+
+    return build_index(lo.randwalk(2000, 32, 7), max_leaf_size=128)
+
+
+@pytest.fixture(scope="module")
+def pipe_tree():
+    from paper_2502_01836_b200 import build_index
+
+    return build_index(lo.randwalk(4000, 32, 17), max_leaf_size=200)
+
+
+def _stats_row(out):
+    s = out.stats
+    return [s.leaves_visited, s.leaves_searched, s.leaves_lb_pruned, s.leaves_filter_pruned,
+            s.filter_inferences, s.series_scanned]
+
+
+@pytest.mark.parametrize("m", [256, 96, 32])
+def test_bounds_bit_exact(knowns, m):
+    from paper_2502_01836_b200.engine import query_bounds
+
+    starts, widths = lo.seg_layout(m, 8)
+    # recover the query rows behind the golden summaries is not possible; use paa rows
+    rows = knowns[f"paa_{m}_rows"]
+    qs, lb0 = query_bounds(rows, knowns[f"lb_{m}_mins"], knowns[f"lb_{m}_maxs"], starts, widths, 0)
+    np.testing.assert_array_equal(qs, knowns[f"paa_{m}"])
+    ref0 = np.array([[lo.node_lb(q, a, b, widths) for a, b in zip(knowns[f"lb_{m}_mins"], knowns[f"lb_{m}_maxs"])]
+                     for q in qs])
+    np.testing.assert_array_equal(lb0, ref0)
+    _, lb1 = query_bounds(rows, knowns[f"lb_{m}_mins"], knowns[f"lb_{m}_maxs"], starts, widths, 1)
+    np.testing.assert_array_equal(lb1, lo.lb_matrix(qs, knowns[f"lb_{m}_mins"], knowns[f"lb_{m}_maxs"], widths))
+
+
+@pytest.mark.parametrize("m", [256, 96, 32])
+def test_batch_distances(knowns, m):
+    from paper_2502_01836_b200 import batch_distances
+
+    got = batch_distances(knowns[f"dist_{m}_q"], knowns[f"dist_{m}_block"])
+    np.testing.assert_allclose(got, knowns[f"dist_{m}_batch"], rtol=DIST_RTOL, atol=0)
+    x = lo.randwalk(70, 32, 5)
+    assert (np.diag(batch_distances(x, x)) == 0.0).all()      # test_series.py:89-92
+
+
+@pytest.mark.parametrize("k", [1, 3])
+def test_exact_search_matches_reference(small_tree, small_golden, k):
+    from paper_2502_01836_b200 import search_engine
+
+    g = small_golden
+    for qi, q in enumerate(g["queries"]):
+        out = search_engine(small_tree, q, k, want_trace=True)
+        assert [i for i, _ in out.results] == g[f"k{k}_ids"][qi].tolist()
+        np.testing.assert_allclose([d for _, d in out.results], g[f"k{k}_dists"][qi], rtol=DIST_RTOL)
+        assert _stats_row(out) == g[f"k{k}_stats"][qi].tolist()
+        a, b = g[f"k{k}_trace_ptr"][qi], g[f"k{k}_trace_ptr"][qi + 1]
+        assert [e.leaf_id for e in out.trace] == g[f"k{k}_trace_leaf"][a:b].tolist()
+        assert [e.lower_bound for e in out.trace] == g[f"k{k}_trace_lb"][a:b].tolist()
+        assert [e.searched for e in out.trace] == g[f"k{k}_trace_searched"][a:b].tolist()
+        np.testing.assert_allclose([e.bsf_before for e in out.trace], g[f"k{k}_trace_bsf"][a:b], rtol=DIST_RTOL)
+        nn = [np.nan if e.leaf_nn_distance is None else e.leaf_nn_distance for e in out.trace]
+        np.testing.assert_allclose(nn, g[f"k{k}_trace_nn"][a:b], rtol=DIST_RTOL)
+
+
+def test_batched_rounds_exact_answers(small_tree, small_golden):
+    """Round schedule: same exact answers; at least the sequential scan volume (F3)."""
+    from paper_2502_01836_b200 import search_batch
+
+    g = small_golden
+    for k in (1, 3):
+        res = search_batch(small_tree, g["queries"], k)
+        np.testing.assert_array_equal(res.ids, g[f"k{k}_ids"])
+        np.testing.assert_allclose(res.dists, g[f"k{k}_dists"], rtol=DIST_RTOL)
+        assert (res.stats[:, 5] >= g[f"k{k}_stats"][:, 5]).all()
+        seq = search_batch(small_tree, g["queries"], k, sequential=True)
+        np.testing.assert_array_equal(seq.stats, g[f"k{k}_stats"])
+
+
+def test_epsilon_search(small_tree, small_golden):
+    from paper_2502_01836_b200 import epsilon_search
+
+    g = small_golden
+    for qi, q in enumerate(g["queries"]):
+        out = epsilon_search(small_tree, q, 1, 1.0)          # bsf_factor 0.5
+        assert out.results[0][0] == g["eps1_ids"][qi][0]
+        assert _stats_row(out) == g["eps1_stats"][qi].tolist()
+
+
+def test_matches_linear_scan_5000(small_golden):
+    """Reference test_tree.py:93-102: 5000x32, cap 256, k=5 vs linear scan."""
+    from paper_2502_01836_b200 import build_index, linear_scan, search_batch
+
+    g = small_golden
+    data = lo.randwalk(5000, 32, 1)
+    t = build_index(data, 256)
+    res = search_batch(t, g["ls_queries"], 5, sequential=True)
+    np.testing.assert_array_equal(res.ids, g["ls_ids"])
+    np.testing.assert_array_equal(res.ids, g["ls_linear_ids"])
+    np.testing.assert_array_equal(res.stats, g["ls_stats"])
+    for qi in (0, 17, 99):
+        assert [i for i, _ in linear_scan(t, g["ls_queries"][qi], 5)] == g["ls_linear_ids"][qi].tolist()
+
+
+def test_k_equals_n(small_golden):
+    from paper_2502_01836_b200 import build_index, pruning_ratio, search_engine
+
+    g = small_golden
+    t = build_index(lo.randwalk(200, 16, 3), 32)
+    out = search_engine(t, g["kn_queries"][0], 200)
+    assert [i for i, _ in out.results] == g["kn_ids"][0].tolist()
+    assert pruning_ratio(out.stats) == 0.0
+
+
+def test_self_query_and_validation(small_tree):
+    from paper_2502_01836_b200 import exact_search
+
+    assert exact_search(small_tree, small_tree.values[123].astype(np.float64), 1).results == [(123, 0.0)]
+    with pytest.raises(ValueError):
+        exact_search(small_tree, np.zeros(7), 1)
+    with pytest.raises(ValueError):
+        exact_search(small_tree, np.zeros(32), 0)
+
+
+def test_oversized_leaf():
+    from paper_2502_01836_b200 import build_index, exact_search
+
+    row = np.linspace(-1.0, 1.0, 16).astype(np.float32).astype(np.float64)  # fp32 storage contract
+    t = build_index(np.tile(row, (40, 1)), 8)
+    assert [i for i, _ in exact_search(t, row, 3).results] == [0, 1, 2]
+
+
+# ------------------------------------------------------------------ filters --
+def _pack(g):
+    from paper_2502_01836_b200 import FilterPack
+
+    return FilterPack(g["selected"].tolist(), g["W1"], g["b1"], g["W2"], g["b2"])
+
+
+def test_filter_predictions_vs_reference(pipeline_golden):
+    g = pipeline_golden
+    pred = _pack(g).predict(g["queries"]).cpu().numpy().astype(np.float64)
+    np.testing.assert_allclose(pred, g["pred_queries"], rtol=2e-5, atol=2e-5)
+
+
+def test_filter_predictions_batch_invariant(pipeline_golden):
+    """F6: a query's predictions do not depend on the batch it is in."""
+    g = pipeline_golden
+    pk = _pack(g)
+    full = pk.predict(g["queries"]).cpu().numpy()
+    for lo_, hi in ((0, 1), (7, 8), (5, 60), (33, 47)):
+        np.testing.assert_array_equal(pk.predict(g["queries"][lo_:hi]).cpu().numpy(), full[lo_:hi])
+
+
+def test_filter_known_answers(knowns):
+    from paper_2502_01836_b200 import FilterPack
+
+    for m in (32, 256):
+        pk = FilterPack([0], knowns[f"mlp_{m}_W1"][None], knowns[f"mlp_{m}_b1"][None],
+                        knowns[f"mlp_{m}_W2"][None], knowns[f"mlp_{m}_b2"].reshape(1))
+        got = pk.predict(knowns[f"mlp_{m}_x"]).cpu().numpy()[:, 0]
+        np.testing.assert_allclose(got, knowns[f"mlp_{m}_y"], rtol=1e-5, atol=1e-5)
+    hand = FilterPack([0], np.eye(2)[None], np.zeros((1, 2)), np.array([[0.5, 1.25]]), np.zeros(1))
+    assert float(hand.predict(np.array([[1.0, 1.0]]))[0, 0]) == 1.75    # test_mlp.py:52-58
+
+
+@pytest.mark.parametrize("target", [0.9, 0.95, 0.99, 1.0])
+def test_filtered_search_reference_predictions(pipe_tree, pipeline_golden, target):
+    """Same predictions as the reference (injected fp64) -> identical outcome and counters."""
+    import torch
+    from paper_2502_01836_b200 import search_batch
+
+    g = pipeline_golden
+    pk = _pack(g)
+    di = pipe_tree.device()
+    res = search_batch(pipe_tree, g["queries"], 1, predictions=torch.from_numpy(g["pred_queries"]),
+                       offsets=g[f"off_{target}"], leaf_filter=pk.leaf_filter(di), sequential=True)
+    np.testing.assert_array_equal(res.ids, g[f"t{target}_ids"])
+    np.testing.assert_allclose(res.dists, g[f"t{target}_dists"], rtol=DIST_RTOL)
+    np.testing.assert_array_equal(res.stats, g[f"t{target}_stats"])
+
+
+@pytest.mark.parametrize("target", [0.9, 0.99])
+def test_filtered_search_gpu_predictions(pipe_tree, pipeline_golden, target):
+    """GPU predictions (fp32, different summation order): outcome equals the oracle
+    run with the SAME predictions, and tracks the reference closely."""
+    from paper_2502_01836_b200 import search_batch
+
+    g = pipeline_golden
+    pk = _pack(g)
+    pred = pk.predict(g["queries"])
+    offs = g[f"off_{target}"]
+    res = search_batch(pipe_tree, g["queries"], 1, predictions=pred, offsets=offs,
+                       leaf_filter=pk.leaf_filter(pipe_tree.device()), sequential=True)
+    ot = lo.build_tree(lo.randwalk(4000, 32, 17), 200)
+    P = pred.cpu().numpy().astype(np.float64)
+    sel = g["selected"].tolist()
+    for qi, q in enumerate(g["queries"]):
+        preds = {l: (lambda _x, v=float(P[qi, s]): v) for s, l in enumerate(sel)}
+        o = lo.search(ot, q, 1, predictors=preds, offsets=dict(zip(sel, offs.tolist())))
+        assert res.ids[qi, 0] == o.results[0][0]
+        assert res.stats[qi].tolist() == [o.stats[s] for s in lo.STAT_KEYS]
+    agree = np.mean(res.ids[:, 0] == g[f"t{target}_ids"][:, 0])
+    assert agree >= 0.95
+
+
+def test_host_callable_predictors(pipe_tree, pipeline_golden):
+    """The reference seam: a dict of per-leaf callables (tree.py:278-286)."""
+    from paper_2502_01836_b200 import search_engine
+
+    g = pipeline_golden
+    sel = g["selected"].tolist()
+    offs = dict(zip(sel, g["off_0.9"].tolist()))
+    for qi in range(0, 60, 6):
+        preds = {l: (lambda _x, v=float(g["pred_queries"][qi, s]): v) for s, l in enumerate(sel)}
+        out = search_engine(pipe_tree, g["queries"][qi], 1, predictors=preds, offsets=offs)
+        assert out.results[0][0] == g["t0.9_ids"][qi][0]
+        assert _stats_row(out) == g["t0.9_stats"][qi].tolist()
+    with pytest.raises(ValueError):
+        search_engine(pipe_tree, g["queries"][0], 1, predictors={sel[0]: lambda _x: 0.0})
+
+
+def test_infinite_prediction_prunes(small_tree, small_golden):
+    """Reference test_tree.py:197-207."""
+    from paper_2502_01836_b200 import search_engine
+
+    leaf = int(small_tree.leaf_ids[-1])
+    out = search_engine(small_tree, small_golden["queries"][0], 1, predictors={leaf: lambda q: 1e9},
+                        offsets={leaf: 0.0})
+    assert out.stats.leaves_filter_pruned + out.stats.leaves_lb_pruned >= 1
