@@ -160,6 +160,15 @@ int lf_tree_export(const lf_tree* t, double* env_min /*[n_nodes][n_seg]*/,
                    int64_t* member_ptr /*[n_nodes+1]*/, int64_t* members /*[n]*/);
 void lf_tree_free(lf_tree* t);
 
+/* Same build from precomputed segment means (host fp64 [n][n_seg], e.g. from
+ * lf_paa_device): the collection itself never has to visit the host. */
+lf_tree* lf_tree_build_from_summaries(const double* h_summs, int64_t n, int32_t n_seg,
+                                      int64_t max_leaf_size);
+
+/* Segment means of device rows (summarize_matrix, summarize.py:52-56), numpy order. */
+int lf_paa_device(const float* d_values, int64_t n, int32_t m, int32_t n_seg, double* d_out,
+                  void* stream);
+
 /* Segment means for host rows (summarize_matrix, summarize.py:52-56), numpy order. */
 int lf_paa_host(const float* h_values, int64_t n, int32_t m, int32_t n_seg, double* h_out,
                 int32_t n_threads);

@@ -8,7 +8,7 @@ exact_search, search, SearchRequest, collect_targets, ...) so callers switch
 by changing the import.  There is no CPU fallback.
 """
 
-from .index import DeviceIndex, TreeIndex, build_index, segment_layout, segment_means
+from .index import DeviceIndex, DeviceRows, TreeIndex, build_index, build_index_device, segment_layout, segment_means
 from .engine import (
     BatchResult,
     SearchOutcome,
@@ -36,6 +36,8 @@ __all__ = [
     "TreeIndex",
     "batch_distances",
     "build_index",
+    "build_index_device",
+    "DeviceRows",
     "epsilon_search",
     "exact_search",
     "linear_scan",

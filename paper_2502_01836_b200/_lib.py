@@ -84,6 +84,8 @@ SIGNATURES = {
     "lf_tree_export": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "lf_tree_free": (None, [_P]),
     "lf_paa_host": (C.c_int, [_P, _I64, _I32, _I32, _P, _I32]),
+    "lf_tree_build_from_summaries": (_P, [_P, _I64, _I32, _I64]),
+    "lf_paa_device": (C.c_int, [_P, _I64, _I32, _I32, _P, _P]),
 }
 
 _lib = None

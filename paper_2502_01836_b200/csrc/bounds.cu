@@ -117,3 +117,22 @@ extern "C" int lf_bounds(const float* d_queries, int64_t Q, const lf_index* idx,
     return lf::launch_bounds(d_queries, Q, *idx, d_env_min, d_env_max, n_env, lb_mode, d_qsumm,
                              d_lb, lf::as_stream(stream));
 }
+
+extern "C" int lf_paa_device(const float* d_values, int64_t n, int32_t m, int32_t n_seg, double* d_out,
+                             void* stream) {
+    LF_REQUIRE(n_seg >= 1 && n_seg <= m && n_seg <= LF_MAX_SEG, "num_segments must be in [1, length]");
+    if (n == 0) return LF_OK;
+    lf_index idx{};
+    idx.m = m;
+    idx.n_seg = n_seg;
+    const int base = m / n_seg, rem = m % n_seg;
+    for (int i = 0, s = 0; i < n_seg; ++i) {
+        idx.seg_width[i] = base + (i < rem ? 1 : 0);
+        idx.seg_start[i] = s;
+        s += idx.seg_width[i];
+    }
+    const int64_t total = n * n_seg;
+    lf::paa_kernel<<<(unsigned)((total + 255) / 256), 256, 0, lf::as_stream(stream)>>>(d_values, n, idx, d_out);
+    LF_CUDA(cudaGetLastError());
+    return LF_OK;
+}

@@ -151,21 +151,14 @@ int lf_paa_host(const float* h_values, int64_t n, int32_t m, int32_t n_seg, doub
     return LF_OK;
 }
 
-lf_tree* lf_tree_build(const float* h_values, int64_t n, int32_t m, int32_t n_seg,
-                       int64_t max_leaf_size, int32_t n_threads) {
-    if (n < 1 || m < 2 || n_seg < 1 || n_seg > m || n_seg > LF_MAX_SEG || max_leaf_size < 2) {
-        lf::fail(LF_EINVAL, "bad tree build arguments");
-        return nullptr;
-    }
+static lf_tree* build_from(const double* summs, int64_t n, int32_t n_seg, int64_t max_leaf_size) {
     auto* t = new lf_tree();
     t->n_seg = n_seg;
     t->cap = max_leaf_size;
     t->n = n;
-    std::vector<double> summs((size_t)n * n_seg);
-    paa_rows(h_values, n, m, n_seg, summs.data(), n_threads);
     new_node(*t);
     for (int64_t sid = 0; sid < n; ++sid) {
-        const double* s = summs.data() + sid * n_seg;
+        const double* s = summs + sid * n_seg;
         int node = 0;
         while (!t->is_leaf[node]) {
             t->size[node] += 1;
@@ -175,9 +168,29 @@ lf_tree* lf_tree_build(const float* h_values, int64_t n, int32_t m, int32_t n_se
         t->members[node].push_back(sid);
         t->size[node] += 1;
         widen(*t, node, s);
-        if (t->size[node] > t->cap) try_split(*t, node, summs.data());
+        if (t->size[node] > t->cap) try_split(*t, node, summs);
     }
     return t;
+}
+
+lf_tree* lf_tree_build(const float* h_values, int64_t n, int32_t m, int32_t n_seg,
+                       int64_t max_leaf_size, int32_t n_threads) {
+    if (n < 1 || m < 2 || n_seg < 1 || n_seg > m || n_seg > LF_MAX_SEG || max_leaf_size < 2) {
+        lf::fail(LF_EINVAL, "bad tree build arguments");
+        return nullptr;
+    }
+    std::vector<double> summs((size_t)n * n_seg);
+    paa_rows(h_values, n, m, n_seg, summs.data(), n_threads);
+    return build_from(summs.data(), n, n_seg, max_leaf_size);
+}
+
+lf_tree* lf_tree_build_from_summaries(const double* h_summs, int64_t n, int32_t n_seg,
+                                      int64_t max_leaf_size) {
+    if (n < 1 || n_seg < 1 || n_seg > LF_MAX_SEG || max_leaf_size < 2) {
+        lf::fail(LF_EINVAL, "bad tree build arguments");
+        return nullptr;
+    }
+    return build_from(h_summs, n, n_seg, max_leaf_size);
 }
 
 int lf_tree_info(const lf_tree* t, int32_t* n_nodes, int32_t* n_leaves) {

@@ -52,9 +52,27 @@ def as_f32_rows(values) -> np.ndarray:
     return v32
 
 
+class DeviceRows:
+    """Row access to a device-resident collection with numpy semantics (rows -> host fp32)."""
+
+    def __init__(self, tensor):
+        self.tensor = tensor
+        self.shape = tuple(tensor.shape)
+        self.dtype = np.float32
+
+    def __getitem__(self, ids):
+        import torch
+
+        idx = torch.as_tensor(np.asarray(ids, dtype=np.int64)).to(self.tensor.device)
+        return self.tensor.index_select(0, idx.reshape(-1)).cpu().numpy().reshape(*np.shape(ids), self.shape[1])
+
+    def __len__(self) -> int:
+        return self.shape[0]
+
+
 @dataclass
 class TreeIndex:
-    values: np.ndarray              # fp32 [n, m], original row order
+    values: object                  # fp32 [n, m] host ndarray, or DeviceRows (original row order)
     starts: np.ndarray
     widths: np.ndarray
     max_leaf_size: int
@@ -167,20 +185,49 @@ def build_index(values, max_leaf_size: int = 1000, segments: int = 8,
     if not h:
         _lib.check(_lib.LF_EINVAL)
     try:
-        nn, nl = C.c_int32(), C.c_int32()
-        _lib.check(L.lf_tree_info(h, C.byref(nn), C.byref(nl)))
-        k = nn.value
-        env_min = np.empty((k, segments)); env_max = np.empty((k, segments))
-        left = np.empty(k, np.int32); right = np.empty(k, np.int32)
-        sseg = np.empty(k, np.int32); sthr = np.empty(k)
-        size = np.empty(k, np.int64); over = np.empty(k, np.int8)
-        mptr = np.empty(k + 1, np.int64); mem = np.empty(n, np.int64)
-        _lib.check(L.lf_tree_export(h, *(_lib.ptr(a) for a in (env_min, env_max, left, right, sseg,
-                                                              sthr, size, over, mptr, mem))))
+        arrays = _export(L, h, n, segments)
     finally:
         L.lf_tree_free(h)
-    return TreeIndex(v, starts, widths, int(max_leaf_size), env_min, env_max, left, right, sseg, sthr,
-                     size, over.astype(bool), mptr, mem)
+    return TreeIndex(v, starts, widths, int(max_leaf_size), *arrays)
+
+
+def build_index_device(X, max_leaf_size: int = 1000, segments: int = 8) -> TreeIndex:
+    """Tree build for a DEVICE collection (fp32 [n, m] torch tensor): segment means on
+    the GPU (lf_paa_device, numpy order), insertion/split loop on the host from the
+    means alone (lf_tree_build_from_summaries) -- the rows never visit the host."""
+    import torch
+
+    if max_leaf_size < 2:
+        raise ValueError(f"max_leaf_size must be >= 2, got {max_leaf_size}")
+    n, m = int(X.shape[0]), int(X.shape[1])
+    starts, widths = segment_layout(m, segments)
+    summ = torch.empty((n, segments), dtype=torch.float64, device=X.device)
+    _lib.check(_lib.lib().lf_paa_device(X.data_ptr(), n, m, segments, summ.data_ptr(), _lib.stream_ptr()))
+    hs = summ.cpu().numpy()
+    del summ
+    L = _lib.lib()
+    h = L.lf_tree_build_from_summaries(_lib.ptr(hs), n, segments, max_leaf_size)
+    if not h:
+        _lib.check(_lib.LF_EINVAL)
+    try:
+        arrays = _export(L, h, n, segments)
+    finally:
+        L.lf_tree_free(h)
+    return TreeIndex(DeviceRows(X), starts, widths, int(max_leaf_size), *arrays)
+
+
+def _export(L, h, n: int, segments: int) -> tuple:
+    nn, nl = C.c_int32(), C.c_int32()
+    _lib.check(L.lf_tree_info(h, C.byref(nn), C.byref(nl)))
+    k = nn.value
+    env_min = np.empty((k, segments)); env_max = np.empty((k, segments))
+    left = np.empty(k, np.int32); right = np.empty(k, np.int32)
+    sseg = np.empty(k, np.int32); sthr = np.empty(k)
+    size = np.empty(k, np.int64); over = np.empty(k, np.int8)
+    mptr = np.empty(k + 1, np.int64); mem = np.empty(n, np.int64)
+    _lib.check(L.lf_tree_export(h, *(_lib.ptr(a) for a in (env_min, env_max, left, right, sseg,
+                                                          sthr, size, over, mptr, mem))))
+    return env_min, env_max, left, right, sseg, sthr, size, over.astype(bool), mptr, mem
 
 
 def segment_means(values, segments: int = 8) -> np.ndarray:
@@ -209,9 +256,12 @@ class DeviceIndex:
         node_leaf[leaf_ids] = np.arange(leaf_ids.shape[0], dtype=np.int32)
         with torch.cuda.device(dev):
             rid = torch.from_numpy(order).to(dev)
-            src = torch.from_numpy(t.values).to(dev)
-            self.X = src.index_select(0, rid).contiguous()
-            del src
+            if isinstance(t.values, DeviceRows):
+                self.X = t.values.tensor.index_select(0, rid).contiguous()
+            else:
+                src = torch.from_numpy(t.values).to(dev)
+                self.X = src.index_select(0, rid).contiguous()
+                del src
             self.row_id = rid
             self.leaf_ptr = torch.from_numpy(leaf_ptr).to(dev)
             self.node_leaf = torch.from_numpy(node_leaf).to(dev)

@@ -1,0 +1,337 @@
+"""LeaFi enhancement and filtered search (the reference's enhanced.py seam).
+
+``enhance(index, plan, budget, seed, ...) -> EnhancedIndex`` follows the
+reference stages (enhanced.py:189-313) with the GPU doing the heavy ones:
+
+  select          threshold + greedy selection (select.py:100-131), host
+  global-queries  numpy stream identical to the reference (traingen.py:110-117)
+  collect-targets lf_bounds + lf_leaf_min_dist (targets.collect_targets)
+  local-queries   numpy streams per leaf, ONE lf_local_min_dist launch
+  train-filters   all filters batched on the GPU (training.train_filters)
+  fit-tuners      calibration predictions from lf_filter_predict -- the same
+                  kernel as search (F6) -- then the replay/curve fit
+                  (calibration.fit_auto_tuners)
+
+``search(eidx, SearchRequest)`` is the single-query drop-in (enhanced.py:137-144,
+exact reference semantics); ``search_queries`` is the batched product path
+(one filter launch + one lf_search per batch).  A reference EnhancedIndex can
+be passed to both: its filters are packed onto the GPU and its curves used.
+"""
+
+from __future__ import annotations
+
+import logging
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .calibration import build_skeleton, compute_alphas, fit_auto_tuners, tune
+from .engine import SearchOutcome, as_tree, search_batch
+from .filters import FilterPack
+from .synth import generate_global_queries, generate_local_queries
+from .targets import collect_targets, local_targets_all
+from .training import TrainConfig, TrainingDivergedError, init_weights, train_filters
+
+log = logging.getLogger(__name__)
+FILTER_OVERHEAD_BYTES = 64          # select.py:17
+
+
+class EnhanceError(RuntimeError):
+    """enhanced.py:58-63: a stage failed; carries the stage name."""
+
+    def __init__(self, stage: str, cause: BaseException):
+        super().__init__(f"enhancement stage '{stage}' failed: {cause}")
+        self.stage = stage
+
+
+def derive_seed(master: int, tag: int) -> int:
+    """enhanced.py:66-67."""
+    return (master * 1_000_003 + tag) % (2**31 - 1)
+
+
+@dataclass(frozen=True)
+class SplitPlan:
+    """traingen.py:26-46."""
+
+    n_global: int = 1500
+    n_local: int = 500
+    calibration: int = 300
+
+    def __post_init__(self):
+        if self.n_global < 1 or self.n_local < 0 or self.calibration < 1:
+            raise ValueError("plan counts must be positive")
+        if self.calibration >= self.n_global:
+            raise ValueError("calibration must be smaller than the global pool")
+
+
+@dataclass(frozen=True)
+class RuntimeConstants:
+    """select.py:31-39."""
+
+    t_series: float
+    t_filter: float
+    filter_bytes: int
+
+    def __post_init__(self):
+        if not (self.t_series > 0 and self.t_filter > 0 and self.filter_bytes > 0):
+            raise ValueError("runtime constants must be strictly positive")
+
+
+@dataclass(frozen=True)
+class SelectionBudget:
+    """select.py:42-51."""
+
+    capacity_bytes: int
+    a: float = 2.0
+
+    def __post_init__(self):
+        if self.capacity_bytes < 0:
+            raise ValueError("capacity must be >= 0")
+        if self.a < 1:
+            raise ValueError("a must be >= 1")
+
+
+def filter_memory_bytes(m: int) -> int:
+    """select.py:54-55 with mlp.weight_byte_size (mlp.py:257-259)."""
+    return 4 * (m * m + 2 * m + 1) + FILTER_OVERHEAD_BYTES
+
+
+def compute_threshold(constants: RuntimeConstants, a: float) -> int:
+    """select.py:100-102."""
+    return math.ceil(a * constants.t_filter / constants.t_series)
+
+
+def select_greedy(leaves, threshold: int, budget: SelectionBudget, filter_bytes: int) -> list:
+    """select.py:113-131: largest first (ties by id), size >= threshold, within budget."""
+    if filter_bytes <= 0:
+        raise ValueError("filter_bytes must be positive")
+    chosen, used = [], 0
+    for lid, size in sorted(leaves, key=lambda it: (-it[1], it[0])):
+        if size < threshold or used + filter_bytes > budget.capacity_bytes:
+            break
+        chosen.append(lid)
+        used += filter_bytes
+    return chosen
+
+
+@dataclass(frozen=True)
+class SearchRequest:
+    """enhanced.py:70-84."""
+
+    query: object
+    k: int = 1
+    target: float | None = None
+    exact: bool = False
+
+    def __post_init__(self):
+        if self.k < 1:
+            raise ValueError("k must be >= 1")
+        if not self.exact:
+            if self.target is None:
+                raise ValueError("request needs a recall target or the exact flag")
+            if not 0.0 <= self.target <= 1.0:
+                raise ValueError(f"target must be in [0, 1], got {self.target}")
+
+
+@dataclass
+class FilterModel:
+    """One filter's parameters (the fields of mlp.MlpModel)."""
+
+    W1: np.ndarray
+    b1: np.ndarray
+    W2: np.ndarray
+    b2: float
+
+
+class EnhancedIndex:
+    """enhanced.py:87-134: base index + filters + curves, with a device filter pack."""
+
+    def __init__(self, base, filters: dict, curves: dict, plan: SplitPlan | None = None,
+                 budget: SelectionBudget | None = None, constants: RuntimeConstants | None = None,
+                 selection: dict | None = None, train_reports: dict | None = None, pack: FilterPack | None = None):
+        self.base = as_tree(base)
+        leaf_set = set(int(l) for l in self.base.leaf_ids)
+        for lid in filters:
+            if lid not in leaf_set:
+                raise ValueError(f"filter leaf {lid} does not exist in the index")
+            if lid not in curves:
+                raise ValueError(f"filter leaf {lid} has no fitted curve")
+        self.filters = dict(sorted(filters.items()))
+        self.curves = curves
+        self.plan, self.budget, self.constants = plan, budget, constants
+        self.selection = selection or {}
+        self.train_reports = train_reports or {}
+        self._pack = pack
+        self._offset_cache = {}
+
+    @classmethod
+    def adopt(cls, ref_eidx) -> "EnhancedIndex":
+        """Wrap a reference enhanced.EnhancedIndex (duck-typed)."""
+        filters = {int(l): FilterModel(np.asarray(m.W1), np.asarray(m.b1), np.asarray(m.W2), float(m.b2))
+                   for l, m in ref_eidx.filters.items()}
+        return cls(ref_eidx.base, filters, dict(ref_eidx.curves), ref_eidx.plan, ref_eidx.budget,
+                   ref_eidx.constants, ref_eidx.selection, ref_eidx.train_reports)
+
+    @property
+    def filter_leaf_ids(self) -> list:
+        return list(self.filters)
+
+    @property
+    def pack(self) -> FilterPack:
+        if self._pack is None:
+            self._pack = FilterPack.from_models(self.filters)
+        return self._pack
+
+    def tuned_offsets(self, target: float) -> dict:
+        """Per-filter offsets, memoised on the exact target (enhanced.py:127-134)."""
+        key = float(target)
+        got = self._offset_cache.get(key)
+        if got is None:
+            got = tune(self.curves, key)
+            self._offset_cache[key] = got
+        return got
+
+    def offset_vector(self, target: float) -> np.ndarray:
+        offs = self.tuned_offsets(target)
+        return np.array([offs[l] for l in self.pack.leaf_ids], dtype=np.float64)
+
+
+_adopted_eidx = {}
+
+
+def _as_enhanced(eidx) -> EnhancedIndex:
+    if isinstance(eidx, EnhancedIndex):
+        return eidx
+    key = id(eidx)
+    got = _adopted_eidx.get(key)
+    if got is None or got[0] is not eidx:
+        got = (eidx, EnhancedIndex.adopt(eidx))
+        _adopted_eidx[key] = got
+    return got[1]
+
+
+def search_queries(eidx, queries, k: int = 1, *, target: float | None = None, exact: bool = False,
+                   sequential: bool = False, max_round_leaves: int = 64, want_trace: bool = False,
+                   stream=None):
+    """Batched LeaFi search: one lf_filter_predict + one lf_search for the whole batch."""
+    e = _as_enhanced(eidx)
+    if exact or not e.filters:
+        return search_batch(e.base, queries, k, sequential=sequential, max_round_leaves=max_round_leaves,
+                            want_trace=want_trace, stream=stream)
+    if target is None or not 0.0 <= target <= 1.0:
+        raise ValueError(f"target must be in [0, 1], got {target}")
+    torch = _lib.require_cuda()
+    di = e.base.device()
+    pk = e.pack
+    q = queries if isinstance(queries, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(np.atleast_2d(queries), dtype=np.float32))
+    q = q.to(device=di.device, dtype=torch.float32)
+    pred = pk.predict(q, stream=stream)
+    return search_batch(e.base, q, k, predictions=pred, offsets=e.offset_vector(target),
+                        leaf_filter=pk.leaf_filter(di), sequential=sequential,
+                        max_round_leaves=max_round_leaves, want_trace=want_trace, stream=stream)
+
+
+def search(eidx, req: SearchRequest) -> SearchOutcome:
+    """enhanced.py:137-144 drop-in (reference traversal semantics)."""
+    t0 = time.perf_counter()
+    res = search_queries(eidx, np.asarray(req.query, dtype=np.float64)[None, :], req.k,
+                         target=req.target, exact=req.exact, sequential=True)
+    out = res.outcome(0)
+    out.stats.wall_time_s = time.perf_counter() - t0
+    return out
+
+
+# --------------------------------------------------------------- enhance ----
+def enhance(index, plan: SplitPlan, budget: SelectionBudget, seed: int, *,
+            constants: RuntimeConstants | None = None, train_cfg: TrainConfig | None = None,
+            noise_range=(0.1, 0.4), record_trajectories: bool = False, timings: dict | None = None
+            ) -> EnhancedIndex:
+    """Build filters and auto-tuners over an index (enhanced.py:189-313), GPU stages."""
+    torch = _lib.require_cuda()
+    t = as_tree(index)
+    train_cfg = train_cfg or TrainConfig()
+    timings = timings if timings is not None else {}
+    stage = "init"
+    t_stage = time.perf_counter()
+
+    def begin(name):
+        nonlocal stage, t_stage
+        now = time.perf_counter()
+        timings[stage] = timings.get(stage, 0.0) + now - t_stage
+        stage, t_stage = name, now
+        log.info("enhancement stage: %s", name)
+
+    try:
+        begin("measure")
+        if constants is None:
+            raise ValueError("inject RuntimeConstants: selection must not depend on wall-clock noise "
+                             "(reference tests/conftest.py:11)")
+        begin("select")
+        threshold = compute_threshold(constants, budget.a)
+        selected = sorted(select_greedy(t.leaf_sizes(), threshold, budget, constants.filter_bytes))
+        sizes = dict(t.leaf_sizes())
+        report = {"t_S": constants.t_series, "t_F": constants.t_filter, "w": constants.filter_bytes,
+                  "a": budget.a, "th": threshold, "capacity": budget.capacity_bytes,
+                  "selected": [{"leaf_id": l, "size": sizes[l]} for l in selected]}
+        if not selected:
+            log.warning("selection is empty: search will behave exactly")
+            return EnhancedIndex(t, {}, {}, plan, budget, constants, report, {})
+
+        begin("global-queries")
+        gq, _ = generate_global_queries(t.values, plan.n_global, noise_range, derive_seed(seed, 2))
+
+        begin("collect-targets")
+        gts = collect_targets(t, selected, gq, plan.calibration)
+
+        begin("local-queries")
+        local_q = {}
+        for lid in selected:
+            q, _, _ = generate_local_queries(t, lid, plan.n_local, noise_range, derive_seed(seed, 10_000 + lid))
+            local_q[lid] = q
+        local = local_targets_all(t, local_q) if plan.n_local else {l: (np.zeros(0), np.zeros(0)) for l in selected}
+
+        begin("train-filters")
+        m, F, pool = t.m, len(selected), gts.train_pool_size
+        n_all = pool + plan.n_local
+        n_tr = (n_all * 4) // 5
+        bank = np.concatenate([gts.queries[:pool]] + [local_q[l] for l in selected]).astype(np.float32)
+        tr_idx = np.empty((F, n_tr), np.int64)
+        va_idx = np.empty((F, n_all - n_tr), np.int64)
+        tr_y = np.empty((F, n_tr))
+        va_y = np.empty((F, n_all - n_tr))
+        W1 = np.empty((F, m, m), np.float32); b1 = np.empty((F, m), np.float32)
+        W2 = np.empty((F, m), np.float32); b2 = np.empty(F, np.float32)
+        for s, lid in enumerate(selected):
+            rows = np.concatenate([np.arange(pool), pool + s * plan.n_local + np.arange(plan.n_local)])
+            y = np.concatenate([gts.dl_selected[:pool, s], local[lid][0]])
+            perm = np.random.default_rng(derive_seed(seed, 30_000 + lid)).permutation(n_all)
+            tr_idx[s], va_idx[s] = rows[perm[:n_tr]], rows[perm[n_tr:]]
+            tr_y[s], va_y[s] = y[perm[:n_tr]], y[perm[n_tr:]]
+            W1[s], b1[s], W2[s], b2[s] = init_weights(m, derive_seed(seed, 40_000 + lid))
+        dbank = torch.from_numpy(bank).cuda()
+        (W1, b1, W2, b2), reps = train_filters(dbank, tr_idx, tr_y, va_idx, va_y, (W1, b1, W2, b2), train_cfg,
+                                              seed=derive_seed(seed, 20_000), record_trajectories=record_trajectories)
+        filters = {lid: FilterModel(W1[s], b1[s], W2[s], float(b2[s])) for s, lid in enumerate(selected)}
+        reports = {lid: reps[s] for s, lid in enumerate(selected)}
+        pack = FilterPack(selected, W1, b1, W2, b2)
+
+        begin("fit-tuners")
+        calib = gts.queries[pool:]
+        cpred = pack.predict(calib).cpu().numpy().astype(np.float64)      # same kernel as search (F6)
+        preds = {lid: cpred[:, s] for s, lid in enumerate(selected)}
+        alphas = {lid: compute_alphas(preds[lid], gts.dl_selected[pool:, s]) for s, lid in enumerate(selected)}
+        sk = build_skeleton(gts.lb_matrix[pool:], gts.dl_calib_full, gts.visit_order[pool:],
+                            gts.nn_distance[pool:], gts.leaf_ids, selected, preds)
+        curves = fit_auto_tuners(sk, alphas)
+        begin("done")
+        e = EnhancedIndex(t, filters, curves, plan, budget, constants, report, reports, pack=pack)
+        e.global_set = gts
+        return e
+    except EnhanceError:
+        raise
+    except BaseException as exc:
+        raise EnhanceError(stage, exc) from exc

@@ -1,0 +1,171 @@
+"""GPU parity of training-data generation (lf_bounds mode 1, lf_leaf_min_dist,
+lf_local_min_dist) and of the LeaFi pipeline (batched training + calibration
+with the search kernel) against the reference's golden vectors / outcomes."""
+
+import json
+
+import numpy as np
+import pytest
+
+from oracle import leafi_oracle as lo
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def small_tree():
+    from paper_2502_01836_b200 import build_index
+
+    return build_index(lo.randwalk(2000, 32, 7), max_leaf_size=128)
+
+
+def test_collect_targets_small(small_tree, small_golden):
+    from paper_2502_01836_b200.targets import collect_targets
+
+    g = small_golden
+    gts = collect_targets(small_tree, g["tg_selected"].tolist(), g["tg_queries"], 30)
+    np.testing.assert_array_equal(gts.leaf_ids, g["tg_leaf_ids"])
+    np.testing.assert_array_equal(gts.lb_matrix, g["tg_lb_matrix"])           # bit-exact bounds
+    np.testing.assert_array_equal(gts.visit_order, g["tg_visit_order"])
+    np.testing.assert_allclose(gts.dl_selected, g["tg_dl_selected"], rtol=RTOL)
+    np.testing.assert_allclose(gts.dl_calib_full, g["tg_dl_calib_full"], rtol=RTOL)
+    np.testing.assert_allclose(gts.nn_distance, g["tg_nn_distance"], rtol=RTOL)
+
+
+def test_member_query_zero_target(small_tree):
+    """Reference test_traingen.py:76-82."""
+    from paper_2502_01836_b200.targets import collect_targets
+
+    lid = int(small_tree.leaf_ids[0])
+    row = small_tree.values[small_tree.leaf_members(lid)[0]].astype(np.float64)
+    gts = collect_targets(small_tree, [lid], np.stack([row] * 3), 1)
+    assert gts.dl_selected[0, 0] == 0.0
+
+
+def test_local_targets(small_tree, small_golden):
+    from paper_2502_01836_b200.synth import generate_local_queries
+    from paper_2502_01836_b200.targets import LocalQueries, collect_local_targets
+
+    g = small_golden
+    lid = int(g["lq_leaf"])
+    q, lv, src = generate_local_queries(small_tree, lid, 40, (0.1, 0.4), 4)
+    np.testing.assert_array_equal(q, g["lq_queries"])
+    np.testing.assert_array_equal(src, g["lq_sources"])
+    loc = collect_local_targets(small_tree, LocalQueries(lid, q, lv, src))
+    np.testing.assert_allclose(loc.targets, g["lq_targets"], rtol=RTOL)
+    np.testing.assert_array_equal(loc.lbs, g["lq_lbs"])
+    # zero noise -> exactly 0.0 (test_traingen.py:53-57)
+    l0 = int(small_tree.leaf_ids[0])
+    q0, lv0, s0 = generate_local_queries(small_tree, l0, 20, (0.0, 0.0), 5)
+    assert (collect_local_targets(small_tree, LocalQueries(l0, q0, lv0, s0)).targets == 0.0).all()
+
+
+def test_collect_targets_pipeline(pipeline_golden):
+    from paper_2502_01836_b200 import build_index
+    from paper_2502_01836_b200.targets import collect_targets
+
+    g = pipeline_golden
+    t = build_index(lo.randwalk(4000, 32, 17), 200)
+    gts = collect_targets(t, g["selected"].tolist(), g["gq"], 60)
+    np.testing.assert_array_equal(gts.lb_matrix, g["tg_lb_matrix"])
+    np.testing.assert_array_equal(gts.visit_order, g["tg_visit_order"])
+    np.testing.assert_allclose(gts.dl_selected, g["tg_dl_selected"], rtol=RTOL)
+    np.testing.assert_allclose(gts.nn_distance, g["tg_nn_distance"], rtol=RTOL)
+
+
+# -------------------------------------------------------------- pipeline --
+FIXED = dict(t_series=2e-7, t_filter=6e-6, filter_bytes=5 * 1024)   # reference tests/conftest.py:11
+
+
+@pytest.fixture(scope="module")
+def pipe(pipeline_golden):
+    """The reference conftest `pipeline` configuration, enhanced on the GPU."""
+    from paper_2502_01836_b200 import build_index
+    from paper_2502_01836_b200 import pipeline as pl
+    from paper_2502_01836_b200.training import TrainConfig
+
+    data = lo.randwalk(4000, 32, 17)
+    t = build_index(data, 200)
+    e = pl.enhance(t, pl.SplitPlan(240, 80, 60), pl.SelectionBudget(16 * 1024 * 1024), seed=23,
+                   constants=pl.RuntimeConstants(**FIXED), train_cfg=TrainConfig(max_epochs=150))
+    return {"data": data, "tree": t, "eidx": e, "queries": pipeline_golden["queries"]}
+
+
+def test_pipeline_selection_matches_reference(pipe, pipeline_golden):
+    assert pipe["eidx"].filter_leaf_ids == pipeline_golden["selected"].tolist()
+
+
+def test_pipeline_exact_mode_equivalence(pipe):
+    from paper_2502_01836_b200 import exact_search
+    from paper_2502_01836_b200.pipeline import SearchRequest, search
+
+    for q in pipe["queries"][:25]:
+        a = search(pipe["eidx"], SearchRequest(query=q, k=1, exact=True))
+        b = exact_search(pipe["tree"], q, 1)
+        assert a.results == b.results and a.stats.series_scanned == b.stats.series_scanned
+
+
+def test_pipeline_recall_and_pruning(pipe, pipeline_golden):
+    """Recall at target and pruning comparable to the reference's own filters."""
+    from paper_2502_01836_b200 import search_batch
+    from paper_2502_01836_b200.pipeline import search_queries
+
+    g = pipeline_golden
+    Q = pipe["queries"]
+    ex = search_batch(pipe["tree"], Q, 1)
+    for target in (0.9, 0.99):
+        res = search_queries(pipe["eidx"], Q, 1, target=target, sequential=True)
+        hits = [lo.recall_at_1(res.results(i), int(ex.ids[i, 0]), float(ex.dists[i, 0])) for i in range(len(Q))]
+        ours = float(np.mean(res.pruning_ratios()))
+        ref = float(np.mean(1.0 - g[f"t{target}_stats"][:, 5] / 4000))
+        ref_hits = np.mean(g[f"t{target}_ids"][:, 0] == g["exact_ids"][:, 0])
+        assert np.mean(hits) >= min(target, ref_hits) - 0.05
+        assert ours >= ref - 0.10
+        assert (res.dists[:, 0] >= ex.dists[:, 0] - 1e-12).all()          # never beats exact
+
+
+def test_pipeline_target_monotone(pipe):
+    from paper_2502_01836_b200.pipeline import search_queries
+
+    lo_ = search_queries(pipe["eidx"], pipe["queries"], 1, target=0.9, sequential=True)
+    hi = search_queries(pipe["eidx"], pipe["queries"], 1, target=1.0, sequential=True)
+    assert (hi.dists[:, 0] <= lo_.dists[:, 0]).all()
+
+
+def test_pipeline_max_offset_coverage(pipe):
+    """Offsets at alpha_max: recall 1.0 on the calibration queries (criterion 4),
+    with the GPU search itself (not the replay)."""
+    import torch
+    from paper_2502_01836_b200 import search_batch
+
+    e = pipe["eidx"]
+    gts = e.global_set
+    calib = gts.queries[gts.train_pool_size:]
+    amax = np.array([e.curves[l].alpha_max for l in e.pack.leaf_ids])
+    pred = e.pack.predict(calib)
+    res = search_batch(e.base, calib, 1, predictions=pred, offsets=amax, leaf_filter=e.pack.leaf_filter(e.base.device()),
+                       sequential=True)
+    ex = search_batch(e.base, calib, 1)
+    hits = [lo.recall_at_1(res.results(i), int(ex.ids[i, 0]), float(ex.dists[i, 0])) for i in range(len(calib))]
+    assert np.mean(hits) == 1.0
+
+
+def test_reference_filters_adopted(pipeline_golden):
+    """A reference-trained filter set on the GPU path: predictions from lf_filter_predict,
+    offsets from the reference curves; outcome equals the reference in >= 95% of queries."""
+    from paper_2502_01836_b200 import build_index
+    from paper_2502_01836_b200.calibration import QualityOffsetCurve
+    from paper_2502_01836_b200.pipeline import EnhancedIndex, FilterModel, search_queries
+
+    g = pipeline_golden
+    t = build_index(lo.randwalk(4000, 32, 17), 200)
+    sel = g["selected"].tolist()
+    filters = {l: FilterModel(g["W1"][s], g["b1"][s], g["W2"][s], float(g["b2"][s])) for s, l in enumerate(sel)}
+    curves = {l: QualityOffsetCurve(l, g[f"curve_{l}_alphas"], g[f"curve_{l}_kq"], g[f"curve_{l}_ko"],
+                                    bool(g[f"curve_{l}_deg"])) for l in sel}
+    e = EnhancedIndex(t, filters, curves)
+    for target in (0.9, 0.99):
+        np.testing.assert_array_equal(e.offset_vector(target), g[f"off_{target}"])
+        res = search_queries(e, g["queries"], 1, target=target, sequential=True)
+        assert np.mean(res.ids[:, 0] == g[f"t{target}_ids"][:, 0]) >= 0.95
