@@ -1,0 +1,464 @@
+#!/usr/bin/env python
+"""LeaFi hot-path benchmark on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): 25M random-walk series of length 256,
+DSTree-style tree with leaf cap 10,000, one learned filter per
+leaf (enhance() on the GPU, lr 1e-3 at m=256), 1,000 queries
+(250 per noise level 0.1/0.2/0.3/0.4), 1-NN at recall target
+0.99.  A "step" is one batch of the 1,000 queries through the LeaFi search:
+filter inference for every (query, filter) pair + bounds + visit order +
+round-driven leaf scan (lf_filter_predict + lf_search).
+
+Inputs: the collection is generated ON THE GPU (synth.randwalk_device: the
+reference's law, torch Philox stream -- not numpy-bit-identical at 25M; the
+parity tests use the numpy-exact generator at smaller n).  The collection
+(25.6 GB) is far larger than L2 (126 MB), so no L2 flush is needed between
+steps.
+
+Metric: queries/s over the whole job (`value`), with recall@1 (cli.py:83-88)
+against exact GPU search and leaves-pruned %.  `e2e` times the public API
+`pipeline.search_queries` from pinned host queries to host results.
+`roofline` is the leaf-scan kernel (the dominant kernel) against measured HBM
+bandwidth; `cpu_baseline` is the CPU oracle (oracle/leafi_oracle.py, the
+reference algorithm restated in numpy) on a bounded query sample, all host
+cores.  `--impl reference` times that oracle alone as the reference arm.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FIXED = dict(t_series=2e-7, t_filter=6e-6)       # injected constants (reference tests/conftest.py:11)
+NOISE_LEVELS = (0.1, 0.2, 0.3, 0.4)
+
+
+def log(*a):
+    print("[bench]", *a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        try:
+            for line in open(self.path):
+                p = [x.strip() for x in line.split(",")]
+                if len(p) < 9:
+                    continue
+                try:
+                    sm.append(float(p[1]))
+                    mx = float(p[2])
+                except ValueError:
+                    continue
+                for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), p[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(name)
+        except OSError:
+            pass
+        finally:
+            if self.path:
+                os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------- setup --
+def setup_workload(args, device):
+    """Collection, tree, filters, query batch and exact ground truth (untimed)."""
+    import torch
+
+    from paper_2502_01836_b200 import build_index_device, search_batch
+    from paper_2502_01836_b200 import pipeline as pl
+    from paper_2502_01836_b200.synth import queries_device, randwalk_device
+    from paper_2502_01836_b200.training import TrainConfig
+
+    t0 = time.perf_counter()
+    X = randwalk_device(args.n, args.m, args.seed, device=device)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    tree = build_index_device(X, max_leaf_size=args.leaf_cap, segments=8)
+    di = tree.device(device)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
+    log(f"collection {args.n}x{args.m} in {t_gen:.1f}s; tree {tree.n_leaves} leaves / {tree.n_nodes} nodes in {t_build:.1f}s")
+    fbytes = pl.filter_memory_bytes(args.m)
+    consts = pl.RuntimeConstants(FIXED["t_series"], FIXED["t_filter"], fbytes)
+    budget = pl.SelectionBudget(capacity_bytes=fbytes * tree.n_leaves, a=2.0)
+    timings = {}
+    t0 = time.perf_counter()
+    eidx = pl.enhance(tree, pl.SplitPlan(args.n_global, args.n_local, args.calibration), budget, args.seed,
+                      constants=consts, train_cfg=TrainConfig(initial_lr=1e-3), timings=timings)
+    torch.cuda.synchronize()
+    t_enh = time.perf_counter() - t0
+    log(f"enhance {len(eidx.filters)} filters in {t_enh:.1f}s: " +
+        ", ".join(f"{k}={v:.1f}s" for k, v in timings.items() if v > 0.05))
+    per = args.queries // len(NOISE_LEVELS)
+    Q = torch.cat([queries_device(X, per, nz, args.seed + int(10 * nz)) for nz in NOISE_LEVELS]).contiguous()
+    del X
+    torch.cuda.empty_cache()
+    t0 = time.perf_counter()
+    exact = search_batch(tree, Q, 1)
+    t_exact = time.perf_counter() - t0
+    log(f"exact ground truth for {Q.shape[0]} queries in {t_exact:.2f}s "
+        f"(pruning {np.mean(exact.pruning_ratios()):.4f})")
+    return {"tree": tree, "eidx": eidx, "Q": Q, "exact": exact, "di": di,
+            "setup_s": {"generate": t_gen, "build": t_build, "enhance": t_enh, "exact": t_exact, **timings}}
+
+
+def recall_of(res, exact) -> float:
+    """cli.py:83-88: id match, or distance within 1e-6 relative."""
+    rid, rd = res.ids[:, 0], res.dists[:, 0]
+    oid, od = exact.ids[:, 0], exact.dists[:, 0]
+    ok = (rid == oid) | (np.abs(rd - od) <= 1e-6 * np.maximum(od, 1e-300))
+    return float(np.mean(ok))
+
+
+# --------------------------------------------------------------- cpu oracle --
+_OR = {}
+
+
+def _oracle_worker(qi_list):
+    from oracle import leafi_oracle as lo
+
+    t, preds, offs, Qh = _OR["tree"], _OR["preds"], _OR["offs"], _OR["Q"]
+    out = []
+    for qi in qi_list:
+        o = lo.search(t, Qh[qi], 1, predictors=preds, offsets=offs)
+        out.append((qi, o.results[0][0], o.stats["series_scanned"]))
+    return out
+
+
+def oracle_setup(w) -> None:
+    """OracleTree over a host copy of the collection + numpy filter callables."""
+    from oracle import leafi_oracle as lo
+
+    tree, eidx = w["tree"], w["eidx"]
+    di = w["di"]
+    # host copy of the leaf-contiguous device rows, re-indexed by series id
+    X = di.X.cpu().numpy()
+    rowpos = np.empty(tree.n, dtype=np.int64)
+    rowpos[di.row_id.cpu().numpy()] = np.arange(tree.n)
+
+    class RowsById:
+        shape = (tree.n, tree.m)
+
+        def __getitem__(self, ids):
+            return X[rowpos[ids]]
+
+    ot = lo.OracleTree(RowsById(), tree.starts, tree.widths, tree.max_leaf_size)
+    for i in range(tree.n_nodes):
+        ot.env_min.append(tree.env_min[i]); ot.env_max.append(tree.env_max[i])
+        ot.left.append(int(tree.left[i])); ot.right.append(int(tree.right[i]))
+        ot.split_seg.append(int(tree.split_seg[i])); ot.split_thr.append(float(tree.split_thr[i]))
+        ot.member_lists.append(None if tree.left[i] >= 0 else [])
+        ot.size.append(int(tree.size[i])); ot.oversized.append(bool(tree.oversized[i]))
+    ot.members = {int(l): tree.leaf_members(int(l)) for l in tree.leaf_ids}
+    filt = eidx.filters
+    preds = {l: (lambda x, f=filt[l]: lo.mlp_forward(f.W1, f.b1, f.W2, f.b2, x)) for l in filt}
+    offs = eidx.tuned_offsets(w["target"])
+    _OR.update(tree=ot, preds=preds, offs=offs, Q=w["Q"].cpu().numpy().astype(np.float64))
+
+
+def oracle_time(sample_idx, workers: int) -> tuple:
+    """Run the oracle on `sample_idx` queries across `workers` forked processes."""
+    import multiprocessing as mp
+
+    chunks = [list(sample_idx[i::workers]) for i in range(workers)]
+    chunks = [c for c in chunks if c]
+    t0 = time.perf_counter()
+    if workers == 1:
+        res = _oracle_worker(chunks[0])
+    else:
+        with mp.get_context("fork").Pool(len(chunks)) as pool:
+            res = [r for part in pool.map(_oracle_worker, chunks) for r in part]
+    return time.perf_counter() - t0, res
+
+
+def oracle_sample_size(budget_s: float, workers: int) -> int:
+    """Calibrate the sample so the oracle leg stays within ~budget_s of CPU work."""
+    nQ = _OR["Q"].shape[0]
+    probe = [0, nQ // 4, nQ // 2, (3 * nQ) // 4]          # one query per noise level
+    t1, _ = oracle_time(probe, 1)
+    per_q = max(t1 / len(probe), 1e-3)
+    return int(max(workers, min(_OR["Q"].shape[0], budget_s * workers / per_q)))
+
+
+# ----------------------------------------------------------------- timing --
+def peaks() -> tuple:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the scan kernel from the committed ncu capture, if any."""
+    p = ROOT / "profiles" / "scan_kernel_ncu.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("dram_bytes_per_launch"), d.get("algorithmic_bytes_per_launch")
+    return None, None
+
+
+def run_ours(args, rank, world, device):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2502_01836_b200 import _lib
+    from paper_2502_01836_b200.pipeline import search_queries
+
+    w = setup_workload(args, device)
+    w["target"] = args.target
+    eidx, Q, exact, tree = w["eidx"], w["Q"], w["exact"], w["tree"]
+    nQ = Q.shape[0]
+    stream = torch.cuda.current_stream()
+    prof = np.zeros(_lib.N_PROF)
+
+    def step(profile=None):
+        return search_queries(eidx, Q, 1, target=args.target, copy_out=False, profile=profile)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # one checked run: recall and pruning of the exact workload being timed
+    chk = search_queries(eidx, Q, 1, target=args.target)
+    recall = recall_of(chk, exact)
+    per_noise = {}
+    per = nQ // len(NOISE_LEVELS)
+    for i, nz in enumerate(NOISE_LEVELS):
+        sl = slice(i * per, (i + 1) * per)
+        ok = (chk.ids[sl, 0] == exact.ids[sl, 0]) | (np.abs(chk.dists[sl, 0] - exact.dists[sl, 0]) <= 1e-6 * exact.dists[sl, 0])
+        per_noise[str(nz)] = {"recall": float(np.mean(ok)),
+                              "pruning": float(np.mean(chk.pruning_ratios()[sl])),
+                              "leaves_searched": float(np.mean(chk.stats[sl, 1]))}
+    leaves_pruned = 1.0 - float(np.mean(chk.stats[:, 1])) / tree.n_leaves
+    series_pruned = float(np.mean(chk.pruning_ratios()))
+    scanned_per_step = int(chk.stats[:, 5].sum())
+
+    # timed region: K steps, events on the launching stream, barrier + sync both sides
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    scan_ms, scan_launches, kernels = 0.0, 0, 0
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step(prof)
+            scan_ms += prof[2]
+            scan_launches += int(prof[4])
+            kernels += int(prof[5]) + 1          # + the filter-inference launch
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = nQ * args.steps / (ms / 1e3)
+    clocks = clk.summary()
+
+    # e2e through the public API: pinned host queries in, host results out
+    Qh = Q.cpu().pin_memory()
+    for _ in range(2):
+        search_queries(eidx, Qh, 1, target=args.target)
+    torch.cuda.synchronize()
+    e0 = time.perf_counter()
+    for _ in range(args.steps):
+        r = search_queries(eidx, Qh, 1, target=args.target)
+    torch.cuda.synchronize()
+    e_s = (time.perf_counter() - e0) / args.steps
+    e2e = {"value": nQ / e_s, "unit": "queries/s", "h2d_bytes_per_step": int(Q.numel() * 4),
+           "d2h_bytes_per_step": int(nQ * (8 + 8 + 6 * 8)), "ms_per_step": e_s * 1e3}
+
+    hbm, peak_src = peaks()
+    alg_bytes = scanned_per_step * tree.m * 4 * args.steps
+    achieved = alg_bytes / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else None
+    traffic, _ = ncu_traffic()
+    line = {
+        "metric": "1-NN queries/sec at 99% recall, 25M x 256 random-walk series; leaves pruned %",
+        "value": value,
+        "unit": "queries/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64-accumulated f32 series (scan/bounds), f32 filters",
+        "data": "synthetic random walk generated on device (reference law, Philox stream), 25.6 GB >> L2: no flush needed",
+        "config": {
+            "workload": f"DSTree+LeaFi {args.n}x{args.m}, leaf cap {args.leaf_cap}, {nQ} queries "
+                        f"(noise {'/'.join(map(str, NOISE_LEVELS))}), 1-NN, target {args.target}",
+            "n_series": args.n, "length": args.m, "leaf_cap": args.leaf_cap, "leaves": tree.n_leaves,
+            "filters": len(eidx.filters), "queries_per_step": nQ, "k": 1, "recall_target": args.target,
+            "parallelism": f"leaf-sharded x{world}" if world > 1 else "1 GPU",
+            "l2": "inputs larger than L2 (25.6 GB collection)",
+        },
+        "recall_at_1": recall,
+        "leaves_pruned_pct": 100.0 * leaves_pruned,
+        "series_pruning_ratio": series_pruned,
+        "per_noise": per_noise,
+        "clocks": clocks,
+        "e2e": e2e,
+        "gpu_launches": kernels,
+        "roofline": {
+            "kernel": "scan_kernel (leaf scan)", "bound": "hbm",
+            "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
+            "peak_source": peak_src,
+            "algorithmic_bytes_per_step": scanned_per_step * tree.m * 4,
+            "scan_ms_per_step": scan_ms / args.steps, "scan_launches_per_step": scan_launches / args.steps,
+            "phase_ms_last_step": {"bounds+sort": prof[0], "plan": prof[1], "scan": prof[2], "merge": prof[3]},
+        },
+        "setup_s": w["setup_s"],
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        workers = os.cpu_count() or 1
+        oracle_setup(w)
+        n_s = oracle_sample_size(args.cpu_budget_s, workers)
+        idx = np.linspace(0, nQ - 1, n_s).astype(int)
+        el, res = oracle_time(idx, workers)
+        agree = float(np.mean([chk.ids[qi, 0] == rid for qi, rid, _ in res]))
+        line["cpu_baseline"] = {"value": len(idx) / el, "unit": "queries/s", "cores": workers, "kind": "port",
+                                "sample": f"{len(idx)} of the {nQ} benchmark queries (evenly spaced over the 4 noise "
+                                          f"levels), oracle/leafi_oracle.search with the same tree, filters and "
+                                          f"offsets, {workers} forked processes, {el:.1f}s",
+                                "ids_agree_with_gpu": agree}
+    return line
+
+
+def run_reference(args, rank, world, device):
+    """The reference arm: the CPU oracle (restated reference algorithm) on the box's cores."""
+    w = setup_workload(args, device)
+    w["target"] = args.target
+    workers = os.cpu_count() or 1
+    oracle_setup(w)
+    nQ = w["Q"].shape[0]
+    n_s = oracle_sample_size(args.ref_step_s, workers)
+    idx_all = np.arange(nQ)
+    for s in range(args.warmup):
+        oracle_time(idx_all[:workers], workers)
+    times, n_done = [], 0
+    for s in range(args.steps):
+        idx = np.roll(idx_all, -s * n_s)[:n_s]
+        el, _ = oracle_time(idx, workers)
+        times.append(el)
+        n_done += len(idx)
+    value = n_done / sum(times)
+    return {
+        "impl": "reference",
+        "metric": "1-NN queries/sec at 99% recall, 25M x 256 random-walk series; leaves pruned %",
+        "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64 (numpy oracle)", "data": "same synthetic workload as the ours arm",
+        "config": {"workload": f"DSTree+LeaFi {args.n}x{args.m}, leaf cap {args.leaf_cap}, 1-NN, target {args.target}",
+                   "queries_per_step": n_s},
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": workers, "kind": "port",
+                         "sample": f"{n_s} queries per step over {workers} forked processes "
+                                   f"(oracle/leafi_oracle.search, reference algorithm restated)"},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--n", type=int, default=25_000_000)
+    ap.add_argument("--m", type=int, default=256)
+    ap.add_argument("--leaf-cap", type=int, default=10_000)
+    ap.add_argument("--queries", type=int, default=1000)
+    ap.add_argument("--target", type=float, default=0.99)
+    ap.add_argument("--seed", type=int, default=1234)
+    ap.add_argument("--n-global", type=int, default=1500)
+    ap.add_argument("--n-local", type=int, default=500)
+    ap.add_argument("--calibration", type=int, default=300)
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--ref-step-s", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warmup raised to 3 (timing rule)")
+        args.warmup = 3
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    if args.impl == "reference":
+        if rank != 0:
+            if world > 1:
+                dist.destroy_process_group()
+            return
+        line = run_reference(args, rank, world, device)
+    else:
+        line = run_ours(args, rank, world, device)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -66,7 +66,18 @@ typedef struct lf_search_opts {
                                     0: doubling rounds 1,2,4,..,max_round_leaves */
     int32_t max_round_leaves;    /* cap of the doubling schedule (>= 1) */
     int32_t want_trace;          /* fill the trace buffers below */
+    double* h_profile;           /* optional host array[LF_N_PROF]: CUDA-event times (ms)
+                                    accumulated per phase, see LF_PROF_* */
 } lf_search_opts;
+
+#define LF_N_PROF 8
+#define LF_PROF_BOUNDS_MS 0      /* segment means + node bounds + visit-order sort */
+#define LF_PROF_PLAN_MS 1        /* plan + chunk offsets, all rounds */
+#define LF_PROF_SCAN_MS 2        /* leaf-scan kernel, all rounds */
+#define LF_PROF_MERGE_MS 3       /* top-k merge, all rounds */
+#define LF_PROF_ROUNDS 4         /* rounds executed */
+#define LF_PROF_KERNELS 5        /* kernels launched by the library (own kernels; CUB sort counted as 1) */
+#define LF_PROF_TOTAL_MS 6       /* whole call, first to last event */
 
 /* Optional per-query trace (tree.py:77-83 TraceEntry), capacity n_leaves per query. */
 typedef struct lf_trace {

@@ -49,7 +49,12 @@ class LfSearchOpts(C.Structure):
         ("sequential", C.c_int32),
         ("max_round_leaves", C.c_int32),
         ("want_trace", C.c_int32),
+        ("h_profile", C.c_void_p),
     ]
+
+
+N_PROF = 8
+PROF_NAMES = ("bounds_ms", "plan_ms", "scan_ms", "merge_ms", "rounds", "kernels", "total_ms", "unused")
 
 
 class LfTrace(C.Structure):

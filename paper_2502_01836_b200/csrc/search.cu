@@ -140,6 +140,150 @@ __global__ void plan_kernel(RoundState s, lf_index idx) {
     s.chunk_off[q + 1] = nch;   // counts; turned into offsets by offsets_kernel
 }
 
+// Warp-parallel plan: one warp per query evaluates 32 consecutive visit-order
+// entries at a time.  Within a round every decision uses the round-start bsf,
+// so the entries are independent; ballots locate the first break (lb > bsf*f)
+// and the R-th selected leaf, and prefix counts place selections and trace
+// entries in visit order.  Counters, selections and traces are identical to
+// plan_kernel's serial walk.
+__global__ void plan_warp_kernel(RoundState s, lf_index idx) {
+    const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (q >= s.Q) return;
+    const unsigned below = (1u << lane) - 1u;
+    const int Nn = idx.n_nodes;
+    int* pre = s.sel_pre + q * (s.Rcap + 1);
+    int ns = 0, nch = 0;
+    if (!s.done[q]) {
+        const double bsf = query_bsf(s, q);
+        const double thr = bsf * s.f;
+        const int* ord = s.order + q * Nn;
+        const double* lbs = s.lbs + q * Nn;
+        long long* st = s.stats + q * LF_N_STATS;
+        int cur = s.cursor[q];
+        bool fin = false;
+        int tl = s.want_trace ? s.tr.d_len[q] : 0;
+        const int64_t tbase = q * (int64_t)idx.n_leaves;
+        long long c_vis = 0, c_srch = 0, c_lbp = 0, c_fp = 0, c_inf = 0, c_rows = 0;
+        while (!fin && cur < Nn) {
+            const int i = cur + lane;
+            const bool valid = i < Nn;
+            const int node = valid ? ord[i] : -1;
+            const double lb = valid ? lbs[i] : kInf;
+            const int leaf = valid ? idx.d_node_leaf[node] : -1;
+            const bool brk = valid && lb > thr;
+            const unsigned bmask = __ballot_sync(0xffffffffu, brk);
+            const int first_brk = bmask ? __ffs(bmask) - 1 : 32;
+            const bool visit = valid && leaf >= 0 && lane < first_brk;
+            int fs = -1;
+            bool fpr = false;
+            if (visit && idx.d_leaf_filter != nullptr && (s.pred != nullptr || s.pred64 != nullptr)) {
+                fs = idx.d_leaf_filter[leaf];
+                if (fs >= 0) {
+                    const double pv = s.pred64 != nullptr ? s.pred64[q * s.F + fs] : (double)s.pred[q * s.F + fs];
+                    fpr = (pv - s.offset[fs]) > thr;
+                }
+            }
+            const bool scan = visit && !fpr;
+            const unsigned smask = __ballot_sync(0xffffffffu, scan);
+            const int need = s.R - ns;
+            int end;                       // lanes [0, end) are consumed this iteration
+            bool quota = false;
+            if (__popc(smask) >= need) {
+                unsigned mm = smask;
+                for (int t = 1; t < need; ++t) mm &= mm - 1;      // clear the lowest need-1 bits
+                end = __ffs(mm);                                   // include the need-th selected lane
+                quota = true;
+            } else {
+                end = min(first_brk, Nn - cur);
+            }
+            const bool in = lane < end;
+            const bool v_in = visit && in;
+            const bool s_in = scan && in;
+            const bool f_in = v_in && fs >= 0;
+            const bool p_in = f_in && fpr;
+            long long rows = 0;
+            int chunks = 0;
+            if (s_in) {
+                rows = idx.d_leaf_ptr[leaf + 1] - idx.d_leaf_ptr[leaf];
+                chunks = (int)((rows + CH - 1) / CH);
+            }
+            // inclusive warp scan of chunk counts over selected lanes
+            int incl = chunks;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const unsigned sm_in = __ballot_sync(0xffffffffu, s_in);
+            const unsigned vm_in = __ballot_sync(0xffffffffu, v_in);
+            if (s_in) {
+                const int slot = ns + __popc(sm_in & below);
+                s.sel_leaf[q * s.Rcap + slot] = leaf;
+                pre[slot] = nch + incl - chunks;
+            }
+            if (s.want_trace && v_in) {
+                const int te = tl + __popc(vm_in & below);
+                s.tr.d_leaf[tbase + te] = node;
+                s.tr.d_lb[tbase + te] = lb;
+                s.tr.d_searched[tbase + te] = s_in ? 1 : 0;
+                s.tr.d_bsf_before[tbase + te] = bsf;
+                if (!s_in) s.tr.d_leaf_nn[tbase + te] = __longlong_as_double(0x7ff8000000000000LL);
+                else s.sel_trace[q * s.Rcap + ns + __popc(sm_in & below)] = te;
+            }
+            long long rsum = rows;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
+            c_vis += __popc(vm_in);
+            c_srch += __popc(sm_in);
+            c_inf += __popc(__ballot_sync(0xffffffffu, f_in));
+            c_fp += __popc(__ballot_sync(0xffffffffu, p_in));
+            c_rows += rsum;
+            tl += __popc(vm_in);
+            ns += __popc(sm_in);
+            nch += __shfl_sync(0xffffffffu, incl, 31);
+            if (quota) {
+                cur += end;
+            } else if (first_brk < 32 && first_brk < Nn - cur) {
+                // the break entry: a leaf counts as visited + lb-pruned (tree.py:261-269)
+                const int bnode = __shfl_sync(0xffffffffu, node, first_brk);
+                const int bleaf = __shfl_sync(0xffffffffu, leaf, first_brk);
+                const double blb = __shfl_sync(0xffffffffu, lb, first_brk);
+                if (bleaf >= 0) {
+                    c_vis += 1;
+                    c_lbp += 1;
+                    if (s.want_trace && lane == 0) {
+                        s.tr.d_leaf[tbase + tl] = bnode;
+                        s.tr.d_lb[tbase + tl] = blb;
+                        s.tr.d_searched[tbase + tl] = 0;
+                        s.tr.d_leaf_nn[tbase + tl] = __longlong_as_double(0x7ff8000000000000LL);
+                        s.tr.d_bsf_before[tbase + tl] = bsf;
+                    }
+                    tl += 1;
+                }
+                cur += first_brk;
+                fin = true;
+            } else {
+                cur += end;
+            }
+            if (quota) break;
+        }
+        if (cur >= Nn) fin = true;
+        if (lane == 0) {
+            st[0] += c_vis; st[1] += c_srch; st[2] += c_lbp; st[3] += c_fp; st[4] += c_inf; st[5] += c_rows;
+            s.cursor[q] = cur;
+            if (s.want_trace) s.tr.d_len[q] = tl;
+            if (fin) s.done[q] = 1;
+            else atomicAdd(s.n_active, 1);
+        }
+    }
+    if (lane == 0) {
+        pre[ns] = nch;
+        s.n_sel[q] = ns;
+        s.chunk_off[q + 1] = nch;
+    }
+}
+
 // Exclusive scan of per-query chunk counts (single CTA; Q is small).
 __global__ void offsets_kernel(long long* off, int64_t Q) {
     __shared__ long long part[1024];
@@ -453,11 +597,27 @@ int run_search(const lf_index& idx, const float* d_q, int64_t Q, const lf_search
     LF_CUDA(task_min.alloc(sizeof(double) * (s.want_trace ? max_tasks : 1), st));
     LF_CUDA(n_active.alloc(sizeof(int), st));
 
+    // optional phase timing with CUDA events on the launching stream
+    double* prof = o.h_profile;
+    cudaEvent_t ev[6] = {};
+    if (prof) {
+        for (int i = 0; i < LF_N_PROF; ++i) prof[i] = 0.0;
+        for (auto& e : ev) LF_CUDA(cudaEventCreate(&e));
+        LF_CUDA(cudaEventRecord(ev[0], st));
+    }
+    auto elapsed = [&](cudaEvent_t a, cudaEvent_t b) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        return (double)ms;
+    };
+    long long kernels = 0;
+
     int rc = launch_bounds(d_q, Q, idx, idx.d_env_min, idx.d_env_max, Nn, 0, qsumm.as<double>(),
                            lb.as<double>(), st);
     if (rc) return rc;
     rc = sort_visit_order(lb.as<double>(), Q, Nn, lbs.as<double>(), order.as<int>(), st);
     if (rc) return rc;
+    kernels += 4;
 
     s.order = order.as<int>();
     s.lbs = lbs.as<double>();
@@ -482,17 +642,22 @@ int run_search(const lf_index& idx, const float* d_q, int64_t Q, const lf_search
     const unsigned qb = (unsigned)((Q + 127) / 128);
     init_state_kernel<<<qb, 128, 0, st>>>(s);
     LF_CUDA(cudaGetLastError());
+    ++kernels;
+    if (prof) LF_CUDA(cudaEventRecord(ev[1], st));
 
     int* h_active = nullptr;
     LF_CUDA(cudaMallocHost(&h_active, sizeof(int)));
     const int grid = sm_count() * 4;
     const int m4 = idx.m / 4;
     int err = LF_OK;
+    int rounds = 0;
     for (int round = 0;; ++round) {
         s.R = o.sequential ? 1 : (int)std::min<int64_t>(s.Rcap, (int64_t)1 << std::min(round, 30));
         if (cudaMemsetAsync(s.n_active, 0, sizeof(int), st) != cudaSuccess) { err = fail(LF_ECUDA, "memset"); break; }
-        plan_kernel<<<qb, 128, 0, st>>>(s, idx);
+        if (prof) cudaEventRecord(ev[2], st);
+        plan_warp_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s, idx);
         offsets_kernel<<<1, 1024, 0, st>>>(s.chunk_off, Q);
+        if (prof) cudaEventRecord(ev[3], st);
         cudaError_t ce;
         if ((idx.m & 3) != 0 || m4 <= 32) ce = launch_scan<1>(s, idx, d_q, grid, st);
         else if (m4 <= 64) ce = launch_scan<2>(s, idx, d_q, grid, st);
@@ -500,8 +665,12 @@ int run_search(const lf_index& idx, const float* d_q, int64_t Q, const lf_search
         else if (m4 <= 256) ce = launch_scan<8>(s, idx, d_q, grid, st);
         else { err = fail(LF_EINVAL, "series length > 1024 not supported"); break; }
         if (ce != cudaSuccess) { err = fail(LF_ECUDA, cudaGetErrorString(ce)); break; }
+        if (prof) cudaEventRecord(ev[4], st);
         merge_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s);
         if ((ce = cudaGetLastError()) != cudaSuccess) { err = fail(LF_ECUDA, cudaGetErrorString(ce)); break; }
+        if (prof) cudaEventRecord(ev[5], st);
+        kernels += 4;
+        ++rounds;
         std::swap(s.top_d, s.top_d_out);
         std::swap(s.top_i, s.top_i_out);
         std::swap(s.top_n, s.top_n_out);
@@ -510,13 +679,28 @@ int run_search(const lf_index& idx, const float* d_q, int64_t Q, const lf_search
             err = fail(LF_ECUDA, "round sync failed");
             break;
         }
+        if (prof) {
+            if (round == 0) prof[LF_PROF_BOUNDS_MS] = elapsed(ev[0], ev[1]);
+            prof[LF_PROF_PLAN_MS] += elapsed(ev[2], ev[3]);
+            prof[LF_PROF_SCAN_MS] += elapsed(ev[3], ev[4]);
+            prof[LF_PROF_MERGE_MS] += elapsed(ev[4], ev[5]);
+        }
         if (*h_active == 0) break;
     }
     if (err == LF_OK) {
         int64_t n = Q * s.k;
         finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s, out_ids, out_d);
+        ++kernels;
         cudaError_t ce = cudaGetLastError();
         if (ce != cudaSuccess) err = fail(LF_ECUDA, cudaGetErrorString(ce));
+    }
+    if (prof) {
+        cudaEventRecord(ev[5], st);
+        cudaEventSynchronize(ev[5]);
+        prof[LF_PROF_ROUNDS] = rounds;
+        prof[LF_PROF_KERNELS] = (double)kernels;
+        prof[LF_PROF_TOTAL_MS] = elapsed(ev[0], ev[5]);
+        for (auto& e : ev) cudaEventDestroy(e);
     }
     cudaFreeHost(h_active);
     return err;

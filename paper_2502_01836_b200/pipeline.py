@@ -215,12 +215,12 @@ def _as_enhanced(eidx) -> EnhancedIndex:
 
 def search_queries(eidx, queries, k: int = 1, *, target: float | None = None, exact: bool = False,
                    sequential: bool = False, max_round_leaves: int = 64, want_trace: bool = False,
-                   stream=None):
+                   stream=None, copy_out: bool = True, profile=None):
     """Batched LeaFi search: one lf_filter_predict + one lf_search for the whole batch."""
     e = _as_enhanced(eidx)
     if exact or not e.filters:
         return search_batch(e.base, queries, k, sequential=sequential, max_round_leaves=max_round_leaves,
-                            want_trace=want_trace, stream=stream)
+                            want_trace=want_trace, stream=stream, copy_out=copy_out, profile=profile)
     if target is None or not 0.0 <= target <= 1.0:
         raise ValueError(f"target must be in [0, 1], got {target}")
     torch = _lib.require_cuda()
@@ -232,7 +232,8 @@ def search_queries(eidx, queries, k: int = 1, *, target: float | None = None, ex
     pred = pk.predict(q, stream=stream)
     return search_batch(e.base, q, k, predictions=pred, offsets=e.offset_vector(target),
                         leaf_filter=pk.leaf_filter(di), sequential=sequential,
-                        max_round_leaves=max_round_leaves, want_trace=want_trace, stream=stream)
+                        max_round_leaves=max_round_leaves, want_trace=want_trace, stream=stream,
+                        copy_out=copy_out, profile=profile)
 
 
 def search(eidx, req: SearchRequest) -> SearchOutcome:
