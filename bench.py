@@ -133,7 +133,8 @@ def setup_workload(args, device):
     timings = {}
     t0 = time.perf_counter()
     eidx = pl.enhance(tree, pl.SplitPlan(args.n_global, args.n_local, args.calibration), budget, args.seed,
-                      constants=consts, train_cfg=TrainConfig(initial_lr=1e-3), timings=timings)
+                      constants=consts, train_cfg=TrainConfig(initial_lr=1e-3, max_epochs=args.max_epochs),
+                      timings=timings)
     torch.cuda.synchronize()
     t_enh = time.perf_counter() - t0
     log(f"enhance {len(eidx.filters)} filters in {t_enh:.1f}s: " +
@@ -238,6 +239,12 @@ def peaks() -> tuple:
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def tf32_peak() -> float:
+    p = ROOT / "MEASURED_PEAKS.json"
+    bf16 = json.loads(p.read_text())["bf16_tflops"] if p.exists() else 1590.0
+    return float(bf16) / 2.0
+
+
 def ncu_traffic():
     """Per-launch DRAM bytes of the scan kernel from the committed ncu capture, if any."""
     p = ROOT / "profiles" / "scan_kernel_ncu.json"
@@ -278,6 +285,17 @@ def run_ours(args, rank, world, device):
         per_noise[str(nz)] = {"recall": float(np.mean(ok)),
                               "pruning": float(np.mean(chk.pruning_ratios()[sl])),
                               "leaves_searched": float(np.mean(chk.stats[sl, 1]))}
+    # filter inference alone (the tensor-core kernel), events on the launching stream
+    fe0 = torch.cuda.Event(enable_timing=True)
+    fe1 = torch.cuda.Event(enable_timing=True)
+    fe0.record(stream)
+    for _ in range(5):
+        eidx.pack.predict(Q)
+    fe1.record(stream)
+    torch.cuda.synchronize()
+    filter_ms = fe0.elapsed_time(fe1) / 5
+    F = eidx.pack.n_filters
+    filter_tflops = 2.0 * nQ * F * tree.m * (tree.m + 1) / (filter_ms / 1e3) / 1e12
     leaves_pruned = 1.0 - float(np.mean(chk.stats[:, 1])) / tree.n_leaves
     series_pruned = float(np.mean(chk.pruning_ratios()))
     scanned_per_step = int(chk.stats[:, 5].sum())
@@ -361,7 +379,14 @@ def run_ours(args, rank, world, device):
             "peak_source": peak_src,
             "algorithmic_bytes_per_step": scanned_per_step * tree.m * 4,
             "scan_ms_per_step": scan_ms / args.steps, "scan_launches_per_step": scan_launches / args.steps,
-            "phase_ms_last_step": {"bounds+sort": prof[0], "plan": prof[1], "scan": prof[2], "merge": prof[3]},
+            "phase_ms_last_step": {"filter_inference": filter_ms, "bounds+sort": prof[0], "plan": prof[1],
+                                   "scan": prof[2], "merge": prof[3], "lf_search_total": prof[6]},
+        },
+        "filter_kernel": {
+            "path": eidx.pack.path, "bound": "tensor", "ms": filter_ms, "achieved": filter_tflops,
+            "unit": "TFLOP/s", "peak": tf32_peak(), "frac": filter_tflops / tf32_peak(),
+            "flops_per_launch": 2.0 * nQ * F * tree.m * (tree.m + 1),
+            "peak_source": "dense tf32 = 1/2 of measured bf16 (MEASURED_PEAKS.json bf16_tflops)",
         },
         "setup_s": w["setup_s"],
     }
@@ -431,6 +456,7 @@ def main():
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--ref-step-s", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--max-epochs", type=int, default=1000, help="filter training cap (setup speed)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup raised to 3 (timing rule)")

@@ -127,6 +127,17 @@ int lf_filter_predict(const float* d_queries, int64_t Q, int32_t m,
                       const float* d_b2, int32_t F, float* d_pred, void* stream);
 
 /*
+ * Same on the 5th-gen tensor cores (tcgen05.mma kind::tf32, TMA-fed, TMEM
+ * accumulators, fused bias/rectifier/W2 epilogue).  W1T is the TRANSPOSED
+ * first layer, [F][hidden][in] (K-major B operand); m in {32, 64, ..., 256}.
+ * Batch-invariant like lf_filter_predict; precision is tf32 products with
+ * fp32 accumulation.
+ */
+int lf_filter_predict_tc(const float* d_queries, int64_t Q, int32_t m,
+                         const float* d_W1T, const float* d_b1, const float* d_W2,
+                         const float* d_b2, int32_t F, float* d_pred, void* stream);
+
+/*
  * Exact query x leaf minimum distance (direct form, fp64 accumulation).
  * Replaces batch_distances(...).min(axis=1) (series.py:127-139) as used by
  * collect_targets (traingen.py:175-188) and collect_local_targets (:138).

@@ -81,6 +81,7 @@ SIGNATURES = {
     "lf_search": (C.c_int, [C.POINTER(LfIndex), _P, _I64, C.POINTER(LfSearchOpts), _P, _P, _P,
                             C.POINTER(LfTrace), _P]),
     "lf_filter_predict": (C.c_int, [_P, _I64, _I32, _P, _P, _P, _P, _I32, _P, _P]),
+    "lf_filter_predict_tc": (C.c_int, [_P, _I64, _I32, _P, _P, _P, _P, _I32, _P, _P]),
     "lf_leaf_min_dist": (C.c_int, [_P, _I64, C.POINTER(LfIndex), _P, _I32, _P, _I64, _P]),
     "lf_local_min_dist": (C.c_int, [_P, C.POINTER(LfIndex), _P, _P, _I32, _P, _P]),
     "lf_batch_distances": (C.c_int, [_P, _I64, _P, _I64, _I32, _P, _P]),

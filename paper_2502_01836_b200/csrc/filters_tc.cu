@@ -1,0 +1,279 @@
+// K3 on the 5th-generation tensor cores: grouped filter GEMM with a fused
+// bias / rectifier / W2-dot epilogue.
+//
+//   pred[q, f] = b2[f] + sum_j W2[f, j] * relu(b1[f, j] + sum_i X[q, i] * W1[f, i, j])
+//   (mlp.py:90-95, evaluated for every (query, filter) pair; tree.py:278-286)
+//
+// Per tile (filter f, 128 queries): D[128 x m] = X_tile[128 x m] . W1_f[m x m]
+// with tcgen05.mma.kind::tf32 (M=128, N=m<=256, K=8 per instruction), operands
+// staged by TMA (SWIZZLE_128B, K-major: W1 is pre-transposed to [F][hidden][in])
+// through a 4-stage mbarrier pipeline, fp32 accumulators in TMEM (two 256-column
+// buffers so the epilogue of tile i overlaps the MMAs of tile i+1).  The
+// epilogue warps read their accumulator row with tcgen05.ld and fold bias,
+// rectifier and the W2 dot product in registers -- H never leaves the SM.
+//
+// Warp roles (192 threads, one persistent CTA per SM):
+//   warp 0: TMA producer    warp 1: TMEM owner + MMA issuer    warps 2-5: epilogue
+//
+// Batch invariance: an output's K order (k-blocks, then the four
+// K=8 MMAs inside a block) and its j order in the epilogue depend only on m,
+// never on Q or on the tile a query falls in.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace lf {
+namespace tc {
+
+constexpr int BM = 128;          // queries per tile (UMMA M)
+constexpr int BK = 32;           // fp32 elements per 128-byte swizzle row
+constexpr int STAGES = 4;
+constexpr int THREADS = 192;
+constexpr int A_BYTES = BM * BK * 4;          // 16 KiB
+constexpr int B_BYTES_MAX = 256 * BK * 4;     // 32 KiB (N = m <= 256)
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES_MAX;
+constexpr int TMEM_COLS = 512;                // 2 accumulator buffers x 256 columns
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "LF_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra LF_WAIT_%=;\n}" ::"r"(su32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            su32(dst)),
+        "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+                 : "memory");
+}
+
+// K-major, SWIZZLE_128B UMMA shared-memory descriptor (cute::UMMA::SmemDescriptor):
+// start>>4 | LBO(16 B, unused for swizzled K-major)>>4 <<16 | SBO(1024 B: 8 rows x 128 B)>>4 <<32
+// | version 1 <<46 | layout SWIZZLE_128B (2) <<61.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+// Instruction descriptor: D f32, A/B tf32, both K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+#define LF_TMEM_LD32(taddr, r)                                                                                 \
+    asm volatile(                                                                                              \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"      \
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                            \
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),    \
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),            \
+          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),          \
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),          \
+          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                                               \
+        : "r"(taddr))
+
+__global__ void __launch_bounds__(THREADS, 1)
+filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
+                 int64_t Q, int m, int F, const float* __restrict__ b1, const float* __restrict__ W2,
+                 const float* __restrict__ b2, float* __restrict__ pred) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_mb = (int)((Q + BM - 1) / BM);
+    const int64_t n_tiles = (int64_t)F * n_mb;
+    const int n_kb = m / BK;
+    const uint32_t b_bytes = (uint32_t)m * BK * 4;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {                                     // ---- TMA producer
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+                const int f = (int)(t / n_mb), mb = (int)(t % n_mb);
+                for (int kb = 0; kb < n_kb; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* sa = smem + stage * STAGE_BYTES;
+                    uint8_t* sb = sa + A_BYTES;
+                    mbar_expect_tx(&full[stage], A_BYTES + b_bytes);
+                    tma_2d(&map_x, &full[stage], sa, kb * BK, mb * BM);
+                    tma_2d(&map_w, &full[stage], sb, kb * BK, f * m);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {                                     // ---- MMA issuer (single thread)
+            const uint32_t idesc = idesc_tf32(BM, m);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);      // epilogue drained this buffer
+                tc_fence_after();
+                const uint32_t d = tmem_base + (uint32_t)(acc * 256);
+                for (int kb = 0; kb < n_kb; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = su32(smem + stage * STAGE_BYTES);
+                    const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < BK / 8; ++kk)          // K = 8 tf32 = 32 bytes per MMA
+                        mma_tf32(d, sw128_desc(sa + kk * 32), sw128_desc(sb + kk * 32), idesc,
+                                 (kb | kk) != 0 ? 1u : 0u);
+                    mma_commit(&empty[stage]);                  // smem slot free once these MMAs retire
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                mma_commit(&tfull[acc]);                        // accumulator ready for the epilogue
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else {                                                 // ---- epilogue (warps 2..5)
+        const int quarter = warp & 3;                        // TMEM lanes [32*quarter, +32)
+        const int row = quarter * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+            const int f = (int)(t / n_mb), mb = (int)(t % n_mb);
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const float* b1f = b1 + (int64_t)f * m;
+            const float* w2f = W2 + (int64_t)f * m;
+            float part = 0.f;
+            const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * 256);
+            for (int c0 = 0; c0 < m; c0 += 32) {
+                uint32_t r[32];
+                LF_TMEM_LD32(taddr + (uint32_t)c0, r);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float h = fmaxf(__fadd_rn(__uint_as_float(r[j]), __ldg(b1f + c0 + j)), 0.f);
+                    part = __fmaf_rn(h, __ldg(w2f + c0 + j), part);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            const int64_t q = (int64_t)mb * BM + row;
+            if (q < Q) pred[q * F + f] = __fadd_rn(part, b2[f]);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+    }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+            qr == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+static int make_map(CUtensorMap* map, const float* base, int64_t rows, int cols, int box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return fail(LF_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(float)};
+    cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(LF_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return LF_OK;
+}
+
+}  // namespace tc
+}  // namespace lf
+
+extern "C" int lf_filter_predict_tc(const float* d_queries, int64_t Q, int32_t m, const float* d_W1T,
+                                    const float* d_b1, const float* d_W2, const float* d_b2, int32_t F,
+                                    float* d_pred, void* stream) {
+    using namespace lf;
+    LF_REQUIRE(Q >= 0 && F >= 0, "bad sizes");
+    LF_REQUIRE(m >= 32 && m <= 256 && m % 32 == 0, "tensor-core filter path needs m in {32, 64, ..., 256}");
+    LF_REQUIRE(((uintptr_t)d_queries & 15) == 0 && ((uintptr_t)d_W1T & 15) == 0, "operands must be 16-byte aligned");
+    if (Q == 0 || F == 0) return LF_OK;
+    CUtensorMap mx, mw;
+    int rc = tc::make_map(&mx, d_queries, Q, m, tc::BM);
+    if (rc) return rc;
+    rc = tc::make_map(&mw, d_W1T, (int64_t)F * m, m, m);
+    if (rc) return rc;
+    static bool attr_set = false;
+    if (!attr_set) {
+        LF_CUDA(cudaFuncSetAttribute(tc::filter_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     tc::SMEM_BYTES));
+        attr_set = true;
+    }
+    const int64_t tiles = (int64_t)F * ((Q + tc::BM - 1) / tc::BM);
+    const int grid = (int)std::min<int64_t>(tiles, sm_count());
+    tc::filter_tc_kernel<<<grid, tc::THREADS, tc::SMEM_BYTES, as_stream(stream)>>>(mx, mw, Q, m, F, d_b1, d_W2,
+                                                                                    d_b2, d_pred);
+    LF_CUDA(cudaGetLastError());
+    return LF_OK;
+}

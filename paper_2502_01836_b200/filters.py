@@ -17,7 +17,11 @@ from . import _lib
 
 
 class FilterPack:
-    def __init__(self, leaf_ids, W1, b1, W2, b2, device=None):
+    """path: "tc" (tcgen05 tf32, default when m is a multiple of 32 up to 256) or
+    "simt" (fp32 CUDA-core FFMA).  Calibration and search must use the same pack
+    (same path) -- predictions are then bit-identical (F6)."""
+
+    def __init__(self, leaf_ids, W1, b1, W2, b2, device=None, path: str | None = None):
         torch = _lib.require_cuda()
         dev = torch.device(device if device is not None else "cuda")
         self.leaf_ids = [int(l) for l in leaf_ids]
@@ -40,13 +44,21 @@ class FilterPack:
         self.b2 = t(b2, (F,))
         self.device = dev
         self._slot_maps = {}
+        tc_ok = F > 0 and m % 32 == 0 and 32 <= m <= 256
+        self.path = path or ("tc" if tc_ok else "simt")
+        if self.path == "tc":
+            if not tc_ok:
+                raise ValueError("tensor-core filter path needs m in {32, 64, ..., 256}")
+            self.W1T = self.W1.transpose(1, 2).contiguous()     # K-major B operand [F][hidden][in]
+        elif self.path != "simt":
+            raise ValueError(f"unknown filter path {self.path!r}")
 
     @property
     def n_filters(self) -> int:
         return len(self.leaf_ids)
 
     @classmethod
-    def from_models(cls, models: dict, device=None) -> "FilterPack":
+    def from_models(cls, models: dict, device=None, path: str | None = None) -> "FilterPack":
         """From {leaf_id: model} where model has W1, b1, W2, b2 (reference MlpModel)."""
         ids = sorted(int(l) for l in models)
         if not ids:
@@ -55,7 +67,7 @@ class FilterPack:
         b1 = np.stack([np.asarray(models[l].b1, dtype=np.float32) for l in ids])
         W2 = np.stack([np.asarray(models[l].W2, dtype=np.float32) for l in ids])
         b2 = np.array([np.float32(models[l].b2) for l in ids], dtype=np.float32)
-        return cls(ids, W1, b1, W2, b2, device)
+        return cls(ids, W1, b1, W2, b2, device, path)
 
     def predict(self, queries, stream=None):
         """fp32 [Q, F] predictions for device (or host) queries."""
@@ -69,10 +81,10 @@ class FilterPack:
         if Q and self.n_filters:
             if q.shape[1] != self.m:
                 raise ValueError(f"input shape {tuple(q.shape)} does not match model dim {self.m}")
-            _lib.check(_lib.lib().lf_filter_predict(q.data_ptr(), Q, self.m, self.W1.data_ptr(),
-                                                    self.b1.data_ptr(), self.W2.data_ptr(),
-                                                    self.b2.data_ptr(), self.n_filters,
-                                                    out.data_ptr(), _lib.stream_ptr(stream)))
+            fn = _lib.lib().lf_filter_predict_tc if self.path == "tc" else _lib.lib().lf_filter_predict
+            w = self.W1T if self.path == "tc" else self.W1
+            _lib.check(fn(q.data_ptr(), Q, self.m, w.data_ptr(), self.b1.data_ptr(), self.W2.data_ptr(),
+                          self.b2.data_ptr(), self.n_filters, out.data_ptr(), _lib.stream_ptr(stream)))
         return out
 
     def leaf_filter(self, dindex):

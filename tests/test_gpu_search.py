@@ -150,37 +150,71 @@ def test_oversized_leaf():
 
 
 # ------------------------------------------------------------------ filters --
-def _pack(g):
+def _pack(g, path=None):
     from paper_2502_01836_b200 import FilterPack
 
-    return FilterPack(g["selected"].tolist(), g["W1"], g["b1"], g["W2"], g["b2"])
+    return FilterPack(g["selected"].tolist(), g["W1"], g["b1"], g["W2"], g["b2"], path=path)
 
 
-def test_filter_predictions_vs_reference(pipeline_golden):
+# tolerances: fp32 FFMA (simt) differs from OpenBLAS only in summation order;
+# tcgen05 kind::tf32 multiplies 10-bit-mantissa operands (fp32 accumulate).
+PRED_TOL = {"simt": dict(rtol=2e-5, atol=2e-5), "tc": dict(rtol=5e-3, atol=5e-3)}
+
+
+@pytest.mark.parametrize("path", ["simt", "tc"])
+def test_filter_predictions_vs_reference(pipeline_golden, path):
     g = pipeline_golden
-    pred = _pack(g).predict(g["queries"]).cpu().numpy().astype(np.float64)
-    np.testing.assert_allclose(pred, g["pred_queries"], rtol=2e-5, atol=2e-5)
+    pred = _pack(g, path).predict(g["queries"]).cpu().numpy().astype(np.float64)
+    np.testing.assert_allclose(pred, g["pred_queries"], **PRED_TOL[path])
 
 
-def test_filter_predictions_batch_invariant(pipeline_golden):
+@pytest.mark.parametrize("path", ["simt", "tc"])
+def test_filter_predictions_batch_invariant(pipeline_golden, path):
     """F6: a query's predictions do not depend on the batch it is in."""
     g = pipeline_golden
-    pk = _pack(g)
+    pk = _pack(g, path)
     full = pk.predict(g["queries"]).cpu().numpy()
     for lo_, hi in ((0, 1), (7, 8), (5, 60), (33, 47)):
         np.testing.assert_array_equal(pk.predict(g["queries"][lo_:hi]).cpu().numpy(), full[lo_:hi])
+
+
+@pytest.mark.parametrize("m", [32, 64, 96, 256])
+def test_filter_tc_vs_fp64(m):
+    """tcgen05 path against an fp64 numpy forward: many filters, ragged query count
+    (partial last M tile), multi-tile persistent schedule."""
+    from paper_2502_01836_b200 import FilterPack
+
+    rng = np.random.default_rng(m)
+    F, Q = 37, 301
+    W1 = rng.uniform(-1, 1, (F, m, m)).astype(np.float32) / np.sqrt(m)
+    b1 = (rng.standard_normal((F, m)) * 0.1).astype(np.float32)
+    W2 = rng.uniform(-1, 1, (F, m)).astype(np.float32) / np.sqrt(m)
+    b2 = rng.standard_normal(F).astype(np.float32)
+    X = lo.randwalk(Q, m, 3).astype(np.float32)
+    ref = np.einsum("fj,fqj->qf", W2.astype(np.float64),
+                    np.maximum(np.einsum("qi,fij->fqj", X.astype(np.float64), W1.astype(np.float64)) + b1[:, None, :], 0)) + b2
+    tc = FilterPack(list(range(F)), W1, b1, W2, b2, path="tc").predict(X).cpu().numpy()
+    simt = FilterPack(list(range(F)), W1, b1, W2, b2, path="simt").predict(X).cpu().numpy()
+    np.testing.assert_allclose(simt, ref, rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(tc, ref, rtol=5e-3, atol=5e-3)
 
 
 def test_filter_known_answers(knowns):
     from paper_2502_01836_b200 import FilterPack
 
     for m in (32, 256):
-        pk = FilterPack([0], knowns[f"mlp_{m}_W1"][None], knowns[f"mlp_{m}_b1"][None],
-                        knowns[f"mlp_{m}_W2"][None], knowns[f"mlp_{m}_b2"].reshape(1))
-        got = pk.predict(knowns[f"mlp_{m}_x"]).cpu().numpy()[:, 0]
-        np.testing.assert_allclose(got, knowns[f"mlp_{m}_y"], rtol=1e-5, atol=1e-5)
+        for path in ("simt", "tc"):
+            pk = FilterPack([0], knowns[f"mlp_{m}_W1"][None], knowns[f"mlp_{m}_b1"][None],
+                            knowns[f"mlp_{m}_W2"][None], knowns[f"mlp_{m}_b2"].reshape(1), path=path)
+            got = pk.predict(knowns[f"mlp_{m}_x"]).cpu().numpy()[:, 0]
+            np.testing.assert_allclose(got, knowns[f"mlp_{m}_y"], **PRED_TOL[path])
     hand = FilterPack([0], np.eye(2)[None], np.zeros((1, 2)), np.array([[0.5, 1.25]]), np.zeros(1))
     assert float(hand.predict(np.array([[1.0, 1.0]]))[0, 0]) == 1.75    # test_mlp.py:52-58
+    eye = np.zeros((1, 32, 32)); eye[0, 0, 0] = eye[0, 1, 1] = 1.0
+    w2 = np.zeros((1, 32)); w2[0, 0], w2[0, 1] = 0.5, 1.25
+    x = np.zeros((1, 32)); x[0, :2] = 1.0
+    tcp = FilterPack([0], eye, np.zeros((1, 32)), w2, np.zeros(1), path="tc")
+    assert float(tcp.predict(x)[0, 0]) == 1.75                          # exact in tf32 too
 
 
 @pytest.mark.parametrize("target", [0.9, 0.95, 0.99, 1.0])
