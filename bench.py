@@ -304,6 +304,8 @@ def run_ours(args, rank, world, device):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    if args.ncu:
+        torch.cuda.cudart().cudaProfilerStart()
     scan_ms, scan_launches, kernels = 0.0, 0, 0
     with ClockSampler(torch.cuda.current_device()) as clk:
         ev0 = torch.cuda.Event(enable_timing=True)
@@ -316,6 +318,8 @@ def run_ours(args, rank, world, device):
             kernels += int(prof[5]) + 1          # + the filter-inference launch
         ev1.record(stream)
         torch.cuda.synchronize()
+    if args.ncu:
+        torch.cuda.cudart().cudaProfilerStop()
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
@@ -457,6 +461,8 @@ def main():
     ap.add_argument("--ref-step-s", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--max-epochs", type=int, default=1000, help="filter training cap (setup speed)")
+    ap.add_argument("--ncu", action="store_true",
+                    help="bracket the timed steps with cudaProfilerStart/Stop (ncu --profile-from-start off)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup raised to 3 (timing rule)")

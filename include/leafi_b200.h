@@ -66,6 +66,9 @@ typedef struct lf_search_opts {
                                     0: doubling rounds 1,2,4,..,max_round_leaves */
     int32_t max_round_leaves;    /* cap of the doubling schedule (>= 1) */
     int32_t want_trace;          /* fill the trace buffers below */
+    int32_t early_abandon;       /* 1: abandon a row once its partial distance exceeds the
+                                    threshold (HBM bytes saved; results identical; off when
+                                    tracing; needs m % 64 == 0) */
     double* h_profile;           /* optional host array[LF_N_PROF]: CUDA-event times (ms)
                                     accumulated per phase, see LF_PROF_* */
 } lf_search_opts;
@@ -115,6 +118,26 @@ int lf_bounds(const float* d_queries, int64_t Q, const lf_index* idx,
 int lf_search(const lf_index* idx, const float* d_queries, int64_t Q,
               const lf_search_opts* opts, int64_t* d_out_ids, double* d_out_dists,
               int64_t* d_out_stats, const lf_trace* trace, void* stream);
+
+/*
+ * The same search split into rounds, for callers that exchange the per-query
+ * best-so-far between rounds (leaf-sharded multi-GPU: allreduce-min over NVLink).
+ *   s = lf_search_begin(idx, q, Q, opts, trace, d_stats, stream)   bounds + order
+ *   do lf_search_round(s, d_bound, d_bsf_out, &active)             one round
+ *   while (global active > 0)
+ *   lf_search_end(s, d_out_ids, d_out_dists); lf_search_free(s)
+ * d_bound [Q] (nullable): external bound; the round prunes with
+ * min(local k-th best, d_bound[q]).  d_bsf_out [Q] (nullable): local k-th best
+ * after the round (inf while fewer than k found).  Counters accumulate into
+ * d_stats [Q][6] (zeroed by begin).  The session is bound to `stream`.
+ */
+typedef struct lf_session lf_session;
+lf_session* lf_search_begin(const lf_index* idx, const float* d_queries, int64_t Q,
+                            const lf_search_opts* opts, const lf_trace* trace, int64_t* d_stats,
+                            void* stream);
+int lf_search_round(lf_session* s, const double* d_bound, double* d_bsf_out, int32_t* h_active);
+int lf_search_end(lf_session* s, int64_t* d_out_ids, double* d_out_dists);
+void lf_search_free(lf_session* s);
 
 /*
  * Filter inference for every (query, filter) pair, batch-invariant fp32.

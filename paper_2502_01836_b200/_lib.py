@@ -49,6 +49,7 @@ class LfSearchOpts(C.Structure):
         ("sequential", C.c_int32),
         ("max_round_leaves", C.c_int32),
         ("want_trace", C.c_int32),
+        ("early_abandon", C.c_int32),
         ("h_profile", C.c_void_p),
     ]
 
@@ -80,6 +81,10 @@ SIGNATURES = {
     "lf_bounds": (C.c_int, [_P, _I64, C.POINTER(LfIndex), _P, _P, _I32, _I32, _P, _P, _P]),
     "lf_search": (C.c_int, [C.POINTER(LfIndex), _P, _I64, C.POINTER(LfSearchOpts), _P, _P, _P,
                             C.POINTER(LfTrace), _P]),
+    "lf_search_begin": (_P, [C.POINTER(LfIndex), _P, _I64, C.POINTER(LfSearchOpts), C.POINTER(LfTrace), _P, _P]),
+    "lf_search_round": (C.c_int, [_P, _P, _P, C.POINTER(_I32)]),
+    "lf_search_end": (C.c_int, [_P, _P, _P]),
+    "lf_search_free": (None, [_P]),
     "lf_filter_predict": (C.c_int, [_P, _I64, _I32, _P, _P, _P, _P, _I32, _P, _P]),
     "lf_filter_predict_tc": (C.c_int, [_P, _I64, _I32, _P, _P, _P, _P, _I32, _P, _P]),
     "lf_leaf_min_dist": (C.c_int, [_P, _I64, C.POINTER(LfIndex), _P, _I32, _P, _I64, _P]),

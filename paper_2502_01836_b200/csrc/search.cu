@@ -42,6 +42,7 @@ struct RoundState {
     long long* top_i_out;
     int* top_n_out;
     int n_leaves;
+    const double* bound;         // [Q] external best-so-far bound (other shards), or NULL
     long long* stats;            // [Q][6]
     int* sel_leaf;               // [Q][Rcap]
     int* sel_trace;              // [Q][Rcap]
@@ -64,6 +65,14 @@ __device__ inline double query_bsf(const RoundState& s, int64_t q) {
     return s.top_n[q] == s.k ? s.top_d[q * s.k + s.k - 1] : kInf;
 }
 
+// The bound a round prunes with: the local k-th best, tightened by the bound
+// exchanged with the other leaf shards (min over ranks of their k-th best is
+// >= the global k-th best, so pruning with it stays exact).
+__device__ inline double round_bsf(const RoundState& s, int64_t q) {
+    const double b = query_bsf(s, q);
+    return s.bound != nullptr ? fmin(b, s.bound[q]) : b;
+}
+
 // ---------------------------------------------------------------- plan ----
 __global__ void plan_kernel(RoundState s, lf_index idx) {
     int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -72,7 +81,7 @@ __global__ void plan_kernel(RoundState s, lf_index idx) {
     int ns = 0, nch = 0;
     int* pre = s.sel_pre + q * (s.Rcap + 1);
     if (!s.done[q]) {
-        const double bsf = query_bsf(s, q);
+        const double bsf = round_bsf(s, q);
         const double thr = bsf * s.f;
         const int* ord = s.order + q * Nn;
         const double* lbs = s.lbs + q * Nn;
@@ -155,7 +164,7 @@ __global__ void plan_warp_kernel(RoundState s, lf_index idx) {
     int* pre = s.sel_pre + q * (s.Rcap + 1);
     int ns = 0, nch = 0;
     if (!s.done[q]) {
-        const double bsf = query_bsf(s, q);
+        const double bsf = round_bsf(s, q);
         const double thr = bsf * s.f;
         const int* ord = s.order + q * Nn;
         const double* lbs = s.lbs + q * Nn;
@@ -364,7 +373,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) scan_kernel(RoundState s, lf_ind
         const int64_t lbeg = idx.d_leaf_ptr[leaf], lend = idx.d_leaf_ptr[leaf + 1];
         const int64_t r0 = lbeg + (int64_t)c * CH;
         const int nrows = (int)min((int64_t)CH, lend - r0);
-        const double bsf = query_bsf(s, q);
+        const double bsf = round_bsf(s, q);
         const float* qrow = queries + q * m;
 
         if (vec_ok) {
@@ -437,6 +446,135 @@ __global__ void __launch_bounds__(SCAN_THREADS) scan_kernel(RoundState s, lf_ind
                     for (int i = lane; i < nrows; i += 32) {
                         if (pair_less(sd[i], sid[i], bd, bi)) { bd = sd[i]; bi = sid[i]; bp = i; }
                     }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        double od = __shfl_xor_sync(0xffffffffu, bd, o);
+                        long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                        int op = __shfl_xor_sync(0xffffffffu, bp, o);
+                        if (pair_less(od, oi, bd, bi)) { bd = od; bi = oi; bp = op; }
+                    }
+                    if (lane == 0) {
+                        cd[sel] = bd;
+                        ci[sel] = (bd == kInf) ? -1 : bi;
+                        if (bp >= 0) { sd[bp] = kInf; sid[bp] = LLONG_MAX; }
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Early-abandoning scan (m % 64 == 0).  Half a warp owns a row; each row is
+// read in 256-byte pieces (64 dims = one float4 per lane).  After every piece
+// the half-warp reduces its running squared distance and drops the row once it
+// exceeds the threshold, so the rest of the row is never fetched from HBM.
+// Threshold: the round-start k-th best (tree.py:207 keeps d <= bsf) and, for
+// k = 1, the best full distance this half-warp has seen; both with a 1e-12
+// relative margin so a dropped row is strictly worse after the sqrt.  Whole
+// leaves still count in series_scanned (F4).
+template <int NCH, int U>
+__global__ void __launch_bounds__(SCAN_THREADS) scan_ea_kernel(RoundState s, lf_index idx,
+                                                               const float* __restrict__ queries) {
+    __shared__ double sd[CH];
+    __shared__ long long sid[CH];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int hl = lane & 15;
+    const int slot = warp * 2 + (lane >> 4);          // 16 half-warps per CTA
+    const long long total = s.chunk_off[s.Q];
+    const int m = idx.m;
+    constexpr double kMargin = 1.0 + 1e-12;
+    for (long long t = blockIdx.x; t < total; t += gridDim.x) {
+        int64_t lo = 0, hi = s.Q;
+        while (hi - lo > 1) {
+            int64_t mid = (lo + hi) >> 1;
+            if (s.chunk_off[mid] <= t) lo = mid; else hi = mid;
+        }
+        const int64_t q = lo;
+        const int local = (int)(t - s.chunk_off[q]);
+        const int* pre = s.sel_pre + q * (s.Rcap + 1);
+        int j = 0;
+        while (pre[j + 1] <= local) ++j;
+        const int leaf = s.sel_leaf[q * s.Rcap + j];
+        const int c = local - pre[j];
+        const int64_t lbeg = idx.d_leaf_ptr[leaf], lend = idx.d_leaf_ptr[leaf + 1];
+        const int64_t r0 = lbeg + (int64_t)c * CH;
+        const int nrows = (int)min((int64_t)CH, lend - r0);
+        const double bsf = round_bsf(s, q);
+        const double bsf2 = bsf == kInf ? kInf : bsf * bsf * kMargin;
+        const float* qrow = queries + q * m;
+        double qv[NCH][4];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+            float4 x = reinterpret_cast<const float4*>(qrow + ch * 64)[hl];
+            qv[ch][0] = x.x; qv[ch][1] = x.y; qv[ch][2] = x.z; qv[ch][3] = x.w;
+        }
+        double best2 = kInf;                                   // k == 1: best full d^2 seen here
+        // warp-uniform trip count: both half-warps run every iteration (the
+        // half-warp reductions below use full-warp shuffles)
+        for (int b0 = 0; b0 < nrows; b0 += 16 * U) {
+            const int base = b0 + slot;
+            double acc[U];
+            bool alive[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) { acc[u] = 0.0; alive[u] = base + 16 * u < nrows; }
+            double p[U];
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch) {
+                float4 x[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const float4* rp = reinterpret_cast<const float4*>(idx.d_X + (r0 + base + 16 * u) * m + ch * 64);
+                    x[u] = alive[u] ? __ldcs(rp + hl) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    double d0 = (double)x[u].x - qv[ch][0], d1 = (double)x[u].y - qv[ch][1];
+                    double d2 = (double)x[u].z - qv[ch][2], d3 = (double)x[u].w - qv[ch][3];
+                    acc[u] = __fma_rn(d0, d0, acc[u]);
+                    acc[u] = __fma_rn(d1, d1, acc[u]);
+                    acc[u] = __fma_rn(d2, d2, acc[u]);
+                    acc[u] = __fma_rn(d3, d3, acc[u]);
+                    double v = acc[u];
+#pragma unroll
+                    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                    p[u] = v;
+                }
+                const double thr2 = s.k == 1 ? fmin(bsf2, best2 * kMargin) : bsf2;
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (alive[u] && p[u] > thr2) alive[u] = false;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int r = base + 16 * u;
+                if (r < nrows) {
+                    if (alive[u] && s.k == 1) best2 = fmin(best2, p[u]);
+                    if (hl == 0) {
+                        sd[r] = alive[u] ? sqrt(p[u]) : kInf;
+                        sid[r] = idx.d_row_id[r0 + r];
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+            double* cd = s.cand_d + t * s.kc;
+            long long* ci = s.cand_i + t * s.kc;
+            for (int i = lane; i < nrows; i += 32)
+                if (!(sd[i] <= bsf)) sd[i] = kInf;
+            __syncwarp();
+            if (s.kc >= nrows) {
+                for (int i = lane; i < s.kc; i += 32) {
+                    cd[i] = i < nrows ? sd[i] : kInf;
+                    ci[i] = (i < nrows && sd[i] != kInf) ? sid[i] : -1;
+                }
+            } else {
+                for (int sel = 0; sel < s.kc; ++sel) {
+                    double bd = kInf; long long bi = LLONG_MAX; int bp = -1;
+                    for (int i = lane; i < nrows; i += 32)
+                        if (pair_less(sd[i], sid[i], bd, bi)) { bd = sd[i]; bi = sid[i]; bp = i; }
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) {
                         double od = __shfl_xor_sync(0xffffffffu, bd, o);
@@ -544,6 +682,13 @@ __global__ void finish_kernel(RoundState s, int64_t* out_ids, double* out_d) {
     out_d[t] = ok ? s.top_d[t] : kInf;
 }
 
+template <int NCH>
+static cudaError_t launch_scan_ea(const RoundState& s, const lf_index& idx, const float* q, int grid,
+                                  cudaStream_t st) {
+    scan_ea_kernel<NCH, 4><<<grid, SCAN_THREADS, 0, st>>>(s, idx, q);
+    return cudaGetLastError();
+}
+
 template <int VEC>
 static cudaError_t launch_scan(const RoundState& s, const lf_index& idx, const float* q, int grid,
                                cudaStream_t st) {
@@ -551,166 +696,215 @@ static cudaError_t launch_scan(const RoundState& s, const lf_index& idx, const f
     return cudaGetLastError();
 }
 
-int run_search(const lf_index& idx, const float* d_q, int64_t Q, const lf_search_opts& o,
-               int64_t* out_ids, double* out_d, int64_t* out_stats, const lf_trace* trace,
-               cudaStream_t st) {
+}  // namespace lf
+
+// A search over one query batch, split into begin / rounds / end so a caller can
+// exchange the per-query best-so-far between rounds (leaf-sharded multi-GPU).
+struct lf_session {
+    lf_index idx{};
+    lf_search_opts opts{};
+    lf_trace tr{};
+    cudaStream_t st = nullptr;
+    int64_t Q = 0;
+    const float* d_q = nullptr;
+    lf::RoundState s{};
+    lf::Scratch qsumm, lb, lbs, order, cursor, done, topd, topi, topn, topd2, topi2, topn2, sel_leaf,
+        sel_trace, sel_pre, n_sel, chunk_off, cand_d, cand_i, task_min, n_active;
+    int* h_active = nullptr;
+    int round = 0;
+    long long kernels = 0;
+    cudaEvent_t ev[6] = {};
+    bool prof = false;
+};
+
+namespace lf {
+
+static int session_begin(lf_session* ss) {
+    const lf_index& idx = ss->idx;
+    const lf_search_opts& o = ss->opts;
+    cudaStream_t st = ss->st;
+    const int64_t Q = ss->Q;
     const int Nn = idx.n_nodes;
-    RoundState s{};
+    RoundState& s = ss->s;
     s.Q = Q;
     s.k = o.k;
     s.kc = std::min(o.k, CH);
     s.f = o.bsf_factor;
-    s.Rcap = o.sequential ? 1 : std::max(1, std::min(o.max_round_leaves, idx.n_leaves));
+    s.Rcap = o.sequential ? 1 : std::max(1, std::min(o.max_round_leaves, std::max(1, idx.n_leaves)));
     s.pred = o.d_pred;
     s.pred64 = o.d_pred_f64;
     s.offset = o.d_offset;
     s.F = o.n_filters;
-    s.want_trace = (o.want_trace && trace != nullptr) ? 1 : 0;
-    if (s.want_trace) s.tr = *trace;
+    s.want_trace = o.want_trace ? 1 : 0;
+    if (s.want_trace) s.tr = ss->tr;
     s.n_leaves = idx.n_leaves;
-    s.stats = reinterpret_cast<long long*>(out_stats);
+    s.bound = nullptr;
 
-    const int64_t max_chunks_leaf = (idx.max_leaf_rows + CH - 1) / CH;
+    const int64_t max_chunks_leaf = std::max<int64_t>(1, (idx.max_leaf_rows + CH - 1) / CH);
     const int64_t max_tasks = std::max<int64_t>(1, Q * s.Rcap * max_chunks_leaf);
+    LF_CUDA(ss->qsumm.alloc(sizeof(double) * Q * idx.n_seg, st));
+    LF_CUDA(ss->lb.alloc(sizeof(double) * Q * Nn, st));
+    LF_CUDA(ss->lbs.alloc(sizeof(double) * Q * Nn, st));
+    LF_CUDA(ss->order.alloc(sizeof(int) * Q * Nn, st));
+    LF_CUDA(ss->cursor.alloc(sizeof(int) * Q, st));
+    LF_CUDA(ss->done.alloc(sizeof(int) * Q, st));
+    LF_CUDA(ss->topd.alloc(sizeof(double) * Q * s.k, st));
+    LF_CUDA(ss->topi.alloc(sizeof(long long) * Q * s.k, st));
+    LF_CUDA(ss->topn.alloc(sizeof(int) * Q, st));
+    LF_CUDA(ss->topd2.alloc(sizeof(double) * Q * s.k, st));
+    LF_CUDA(ss->topi2.alloc(sizeof(long long) * Q * s.k, st));
+    LF_CUDA(ss->topn2.alloc(sizeof(int) * Q, st));
+    LF_CUDA(ss->sel_leaf.alloc(sizeof(int) * Q * s.Rcap, st));
+    LF_CUDA(ss->sel_trace.alloc(sizeof(int) * Q * s.Rcap, st));
+    LF_CUDA(ss->sel_pre.alloc(sizeof(int) * Q * (s.Rcap + 1), st));
+    LF_CUDA(ss->n_sel.alloc(sizeof(int) * Q, st));
+    LF_CUDA(ss->chunk_off.alloc(sizeof(long long) * (Q + 1), st));
+    LF_CUDA(ss->cand_d.alloc(sizeof(double) * max_tasks * s.kc, st));
+    LF_CUDA(ss->cand_i.alloc(sizeof(long long) * max_tasks * s.kc, st));
+    LF_CUDA(ss->task_min.alloc(sizeof(double) * (s.want_trace ? max_tasks : 1), st));
+    LF_CUDA(ss->n_active.alloc(sizeof(int), st));
+    LF_CUDA(cudaMallocHost(&ss->h_active, sizeof(int)));
 
-    Scratch qsumm, lb, lbs, order, cursor, done, topd, topi, topn, topd2, topi2, topn2, sel_leaf,
-        sel_trace, sel_pre, n_sel, chunk_off, cand_d, cand_i, task_min, n_active;
-    LF_CUDA(qsumm.alloc(sizeof(double) * Q * idx.n_seg, st));
-    LF_CUDA(lb.alloc(sizeof(double) * Q * Nn, st));
-    LF_CUDA(lbs.alloc(sizeof(double) * Q * Nn, st));
-    LF_CUDA(order.alloc(sizeof(int) * Q * Nn, st));
-    LF_CUDA(cursor.alloc(sizeof(int) * Q, st));
-    LF_CUDA(done.alloc(sizeof(int) * Q, st));
-    LF_CUDA(topd.alloc(sizeof(double) * Q * s.k, st));
-    LF_CUDA(topi.alloc(sizeof(long long) * Q * s.k, st));
-    LF_CUDA(topn.alloc(sizeof(int) * Q, st));
-    LF_CUDA(topd2.alloc(sizeof(double) * Q * s.k, st));
-    LF_CUDA(topi2.alloc(sizeof(long long) * Q * s.k, st));
-    LF_CUDA(topn2.alloc(sizeof(int) * Q, st));
-    LF_CUDA(sel_leaf.alloc(sizeof(int) * Q * s.Rcap, st));
-    LF_CUDA(sel_trace.alloc(sizeof(int) * Q * s.Rcap, st));
-    LF_CUDA(sel_pre.alloc(sizeof(int) * Q * (s.Rcap + 1), st));
-    LF_CUDA(n_sel.alloc(sizeof(int) * Q, st));
-    LF_CUDA(chunk_off.alloc(sizeof(long long) * (Q + 1), st));
-    LF_CUDA(cand_d.alloc(sizeof(double) * max_tasks * s.kc, st));
-    LF_CUDA(cand_i.alloc(sizeof(long long) * max_tasks * s.kc, st));
-    LF_CUDA(task_min.alloc(sizeof(double) * (s.want_trace ? max_tasks : 1), st));
-    LF_CUDA(n_active.alloc(sizeof(int), st));
-
-    // optional phase timing with CUDA events on the launching stream
-    double* prof = o.h_profile;
-    cudaEvent_t ev[6] = {};
-    if (prof) {
-        for (int i = 0; i < LF_N_PROF; ++i) prof[i] = 0.0;
-        for (auto& e : ev) LF_CUDA(cudaEventCreate(&e));
-        LF_CUDA(cudaEventRecord(ev[0], st));
+    if (o.h_profile) {
+        ss->prof = true;
+        for (int i = 0; i < LF_N_PROF; ++i) o.h_profile[i] = 0.0;
+        for (auto& e : ss->ev) LF_CUDA(cudaEventCreate(&e));
+        LF_CUDA(cudaEventRecord(ss->ev[0], st));
     }
-    auto elapsed = [&](cudaEvent_t a, cudaEvent_t b) {
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, a, b);
-        return (double)ms;
-    };
-    long long kernels = 0;
-
-    int rc = launch_bounds(d_q, Q, idx, idx.d_env_min, idx.d_env_max, Nn, 0, qsumm.as<double>(),
-                           lb.as<double>(), st);
+    int rc = launch_bounds(ss->d_q, Q, idx, idx.d_env_min, idx.d_env_max, Nn, 0, ss->qsumm.as<double>(),
+                           ss->lb.as<double>(), st);
     if (rc) return rc;
-    rc = sort_visit_order(lb.as<double>(), Q, Nn, lbs.as<double>(), order.as<int>(), st);
+    rc = sort_visit_order(ss->lb.as<double>(), Q, Nn, ss->lbs.as<double>(), ss->order.as<int>(), st);
     if (rc) return rc;
-    kernels += 4;
+    ss->kernels += 4;
 
-    s.order = order.as<int>();
-    s.lbs = lbs.as<double>();
-    s.cursor = cursor.as<int>();
-    s.done = done.as<int>();
-    s.top_d = topd.as<double>();
-    s.top_i = topi.as<long long>();
-    s.top_n = topn.as<int>();
-    s.top_d_out = topd2.as<double>();
-    s.top_i_out = topi2.as<long long>();
-    s.top_n_out = topn2.as<int>();
-    s.sel_leaf = sel_leaf.as<int>();
-    s.sel_trace = sel_trace.as<int>();
-    s.sel_pre = sel_pre.as<int>();
-    s.n_sel = n_sel.as<int>();
-    s.chunk_off = chunk_off.as<long long>();
-    s.cand_d = cand_d.as<double>();
-    s.cand_i = cand_i.as<long long>();
-    s.task_min = task_min.as<double>();
-    s.n_active = n_active.as<int>();
+    s.order = ss->order.as<int>();
+    s.lbs = ss->lbs.as<double>();
+    s.cursor = ss->cursor.as<int>();
+    s.done = ss->done.as<int>();
+    s.top_d = ss->topd.as<double>();
+    s.top_i = ss->topi.as<long long>();
+    s.top_n = ss->topn.as<int>();
+    s.top_d_out = ss->topd2.as<double>();
+    s.top_i_out = ss->topi2.as<long long>();
+    s.top_n_out = ss->topn2.as<int>();
+    s.sel_leaf = ss->sel_leaf.as<int>();
+    s.sel_trace = ss->sel_trace.as<int>();
+    s.sel_pre = ss->sel_pre.as<int>();
+    s.n_sel = ss->n_sel.as<int>();
+    s.chunk_off = ss->chunk_off.as<long long>();
+    s.cand_d = ss->cand_d.as<double>();
+    s.cand_i = ss->cand_i.as<long long>();
+    s.task_min = ss->task_min.as<double>();
+    s.n_active = ss->n_active.as<int>();
 
-    const unsigned qb = (unsigned)((Q + 127) / 128);
-    init_state_kernel<<<qb, 128, 0, st>>>(s);
+    init_state_kernel<<<(unsigned)((Q + 127) / 128), 128, 0, st>>>(s);
     LF_CUDA(cudaGetLastError());
-    ++kernels;
-    if (prof) LF_CUDA(cudaEventRecord(ev[1], st));
-
-    int* h_active = nullptr;
-    LF_CUDA(cudaMallocHost(&h_active, sizeof(int)));
-    const int grid = sm_count() * 4;
-    const int m4 = idx.m / 4;
-    int err = LF_OK;
-    int rounds = 0;
-    for (int round = 0;; ++round) {
-        s.R = o.sequential ? 1 : (int)std::min<int64_t>(s.Rcap, (int64_t)1 << std::min(round, 30));
-        if (cudaMemsetAsync(s.n_active, 0, sizeof(int), st) != cudaSuccess) { err = fail(LF_ECUDA, "memset"); break; }
-        if (prof) cudaEventRecord(ev[2], st);
-        plan_warp_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s, idx);
-        offsets_kernel<<<1, 1024, 0, st>>>(s.chunk_off, Q);
-        if (prof) cudaEventRecord(ev[3], st);
-        cudaError_t ce;
-        if ((idx.m & 3) != 0 || m4 <= 32) ce = launch_scan<1>(s, idx, d_q, grid, st);
-        else if (m4 <= 64) ce = launch_scan<2>(s, idx, d_q, grid, st);
-        else if (m4 <= 128) ce = launch_scan<4>(s, idx, d_q, grid, st);
-        else if (m4 <= 256) ce = launch_scan<8>(s, idx, d_q, grid, st);
-        else { err = fail(LF_EINVAL, "series length > 1024 not supported"); break; }
-        if (ce != cudaSuccess) { err = fail(LF_ECUDA, cudaGetErrorString(ce)); break; }
-        if (prof) cudaEventRecord(ev[4], st);
-        merge_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s);
-        if ((ce = cudaGetLastError()) != cudaSuccess) { err = fail(LF_ECUDA, cudaGetErrorString(ce)); break; }
-        if (prof) cudaEventRecord(ev[5], st);
-        kernels += 4;
-        ++rounds;
-        std::swap(s.top_d, s.top_d_out);
-        std::swap(s.top_i, s.top_i_out);
-        std::swap(s.top_n, s.top_n_out);
-        if (cudaMemcpyAsync(h_active, s.n_active, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-            cudaStreamSynchronize(st) != cudaSuccess) {
-            err = fail(LF_ECUDA, "round sync failed");
-            break;
-        }
-        if (prof) {
-            if (round == 0) prof[LF_PROF_BOUNDS_MS] = elapsed(ev[0], ev[1]);
-            prof[LF_PROF_PLAN_MS] += elapsed(ev[2], ev[3]);
-            prof[LF_PROF_SCAN_MS] += elapsed(ev[3], ev[4]);
-            prof[LF_PROF_MERGE_MS] += elapsed(ev[4], ev[5]);
-        }
-        if (*h_active == 0) break;
-    }
-    if (err == LF_OK) {
-        int64_t n = Q * s.k;
-        finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s, out_ids, out_d);
-        ++kernels;
-        cudaError_t ce = cudaGetLastError();
-        if (ce != cudaSuccess) err = fail(LF_ECUDA, cudaGetErrorString(ce));
-    }
-    if (prof) {
-        cudaEventRecord(ev[5], st);
-        cudaEventSynchronize(ev[5]);
-        prof[LF_PROF_ROUNDS] = rounds;
-        prof[LF_PROF_KERNELS] = (double)kernels;
-        prof[LF_PROF_TOTAL_MS] = elapsed(ev[0], ev[5]);
-        for (auto& e : ev) cudaEventDestroy(e);
-    }
-    cudaFreeHost(h_active);
-    return err;
+    ++ss->kernels;
+    if (ss->prof) LF_CUDA(cudaEventRecord(ss->ev[1], st));
+    return LF_OK;
 }
 
-}  // namespace lf
+static float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
+}
 
-extern "C" int lf_search(const lf_index* idx, const float* d_queries, int64_t Q,
-                         const lf_search_opts* opts, int64_t* d_out_ids, double* d_out_dists,
-                         int64_t* d_out_stats, const lf_trace* trace, void* stream) {
+__global__ void bsf_out_kernel(RoundState s, double* out) {
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < s.Q) out[q] = query_bsf(s, q);
+}
+
+static int session_round(lf_session* ss, const double* d_bound, double* d_bsf_out, int* active_out) {
+    RoundState& s = ss->s;
+    const lf_index& idx = ss->idx;
+    const lf_search_opts& o = ss->opts;
+    cudaStream_t st = ss->st;
+    const int64_t Q = ss->Q;
+    s.bound = d_bound;
+    s.R = o.sequential ? 1 : (int)std::min<int64_t>(s.Rcap, (int64_t)1 << std::min(ss->round, 30));
+    LF_CUDA(cudaMemsetAsync(s.n_active, 0, sizeof(int), st));
+    if (ss->prof) cudaEventRecord(ss->ev[2], st);
+    plan_warp_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s, idx);
+    offsets_kernel<<<1, 1024, 0, st>>>(s.chunk_off, Q);
+    if (ss->prof) cudaEventRecord(ss->ev[3], st);
+    const int grid = sm_count() * 4;
+    const int m4 = idx.m / 4;
+    cudaError_t ce;
+    const bool ea = o.early_abandon && !s.want_trace && (idx.m % 64) == 0 && idx.m <= 512;
+    if (ea) {
+        switch (idx.m / 64) {
+            case 1: ce = launch_scan_ea<1>(s, idx, ss->d_q, grid, st); break;
+            case 2: ce = launch_scan_ea<2>(s, idx, ss->d_q, grid, st); break;
+            case 3: ce = launch_scan_ea<3>(s, idx, ss->d_q, grid, st); break;
+            case 4: ce = launch_scan_ea<4>(s, idx, ss->d_q, grid, st); break;
+            case 5: ce = launch_scan_ea<5>(s, idx, ss->d_q, grid, st); break;
+            case 6: ce = launch_scan_ea<6>(s, idx, ss->d_q, grid, st); break;
+            case 7: ce = launch_scan_ea<7>(s, idx, ss->d_q, grid, st); break;
+            default: ce = launch_scan_ea<8>(s, idx, ss->d_q, grid, st); break;
+        }
+    } else if ((idx.m & 3) != 0 || m4 <= 32) ce = launch_scan<1>(s, idx, ss->d_q, grid, st);
+    else if (m4 <= 64) ce = launch_scan<2>(s, idx, ss->d_q, grid, st);
+    else if (m4 <= 128) ce = launch_scan<4>(s, idx, ss->d_q, grid, st);
+    else if (m4 <= 256) ce = launch_scan<8>(s, idx, ss->d_q, grid, st);
+    else return fail(LF_EINVAL, "series length > 1024 not supported");
+    if (ce != cudaSuccess) return fail(LF_ECUDA, cudaGetErrorString(ce));
+    if (ss->prof) cudaEventRecord(ss->ev[4], st);
+    merge_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s);
+    LF_CUDA(cudaGetLastError());
+    if (ss->prof) cudaEventRecord(ss->ev[5], st);
+    ss->kernels += 4;
+    std::swap(s.top_d, s.top_d_out);
+    std::swap(s.top_i, s.top_i_out);
+    std::swap(s.top_n, s.top_n_out);
+    if (d_bsf_out) {
+        bsf_out_kernel<<<(unsigned)((Q + 255) / 256), 256, 0, st>>>(s, d_bsf_out);
+        LF_CUDA(cudaGetLastError());
+        ++ss->kernels;
+    }
+    LF_CUDA(cudaMemcpyAsync(ss->h_active, s.n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+    LF_CUDA(cudaStreamSynchronize(st));
+    if (ss->prof) {
+        double* p = o.h_profile;
+        if (ss->round == 0) p[LF_PROF_BOUNDS_MS] = ev_ms(ss->ev[0], ss->ev[1]);
+        p[LF_PROF_PLAN_MS] += ev_ms(ss->ev[2], ss->ev[3]);
+        p[LF_PROF_SCAN_MS] += ev_ms(ss->ev[3], ss->ev[4]);
+        p[LF_PROF_MERGE_MS] += ev_ms(ss->ev[4], ss->ev[5]);
+    }
+    ++ss->round;
+    *active_out = *ss->h_active;
+    return LF_OK;
+}
+
+static int session_end(lf_session* ss, int64_t* out_ids, double* out_d, int64_t* out_stats) {
+    RoundState& s = ss->s;
+    cudaStream_t st = ss->st;
+    const int64_t n = ss->Q * s.k;
+    finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s, out_ids, out_d);
+    LF_CUDA(cudaGetLastError());
+    ++ss->kernels;
+    (void)out_stats;   // counters were accumulated in place (d_stats of lf_search_begin)
+    if (ss->prof) {
+        double* p = ss->opts.h_profile;
+        cudaEventRecord(ss->ev[5], st);
+        cudaEventSynchronize(ss->ev[5]);
+        p[LF_PROF_ROUNDS] = ss->round;
+        p[LF_PROF_KERNELS] = (double)ss->kernels;
+        p[LF_PROF_TOTAL_MS] = ev_ms(ss->ev[0], ss->ev[5]);
+    }
+    return LF_OK;
+}
+
+static void session_free(lf_session* ss) {
+    if (!ss) return;
+    for (auto& e : ss->ev)
+        if (e) cudaEventDestroy(e);
+    if (ss->h_active) cudaFreeHost(ss->h_active);
+    delete ss;   // Scratch members free their device buffers stream-ordered
+}
+
+static int check_args(const lf_index* idx, int64_t Q, const lf_search_opts* opts) {
     LF_REQUIRE(idx != nullptr && opts != nullptr, "NULL argument");
     LF_REQUIRE(Q >= 0, "negative query count");
     LF_REQUIRE(opts->k >= 1 && opts->k <= idx->n_series, "k must be in [1, n]");
@@ -719,7 +913,75 @@ extern "C" int lf_search(const lf_index* idx, const float* d_queries, int64_t Q,
                    (opts->d_offset != nullptr && idx->d_leaf_filter != nullptr),
                "filter predictions need offsets and a leaf->filter map");
     LF_REQUIRE(opts->sequential || opts->max_round_leaves >= 1, "max_round_leaves must be >= 1");
-    if (Q == 0) return LF_OK;
-    return lf::run_search(*idx, d_queries, Q, *opts, d_out_ids, d_out_dists, d_out_stats, trace,
-                          lf::as_stream(stream));
+    return LF_OK;
 }
+
+}  // namespace lf
+
+extern "C" {
+
+lf_session* lf_search_begin(const lf_index* idx, const float* d_queries, int64_t Q,
+                            const lf_search_opts* opts, const lf_trace* trace, int64_t* d_stats,
+                            void* stream) {
+    if (lf::check_args(idx, Q, opts) != LF_OK) return nullptr;
+    if (Q < 1) { lf::fail(LF_EINVAL, "empty query batch"); return nullptr; }
+    auto* ss = new lf_session();
+    ss->idx = *idx;
+    ss->opts = *opts;
+    ss->opts.want_trace = (opts->want_trace && trace != nullptr) ? 1 : 0;
+    if (ss->opts.want_trace) ss->tr = *trace;
+    ss->st = lf::as_stream(stream);
+    ss->Q = Q;
+    ss->d_q = d_queries;
+    ss->s.stats = reinterpret_cast<long long*>(d_stats);
+    if (lf::session_begin(ss) != LF_OK) {
+        lf::session_free(ss);
+        return nullptr;
+    }
+    return ss;
+}
+
+int lf_search_round(lf_session* ss, const double* d_bound, double* d_bsf_out, int32_t* h_active) {
+    LF_REQUIRE(ss != nullptr && h_active != nullptr, "NULL argument");
+    return lf::session_round(ss, d_bound, d_bsf_out, h_active);
+}
+
+int lf_search_end(lf_session* ss, int64_t* d_out_ids, double* d_out_dists) {
+    LF_REQUIRE(ss != nullptr, "NULL session");
+    int rc = lf::session_end(ss, d_out_ids, d_out_dists, nullptr);
+    return rc;
+}
+
+void lf_search_free(lf_session* ss) { lf::session_free(ss); }
+
+int lf_search(const lf_index* idx, const float* d_queries, int64_t Q, const lf_search_opts* opts,
+              int64_t* d_out_ids, double* d_out_dists, int64_t* d_out_stats, const lf_trace* trace,
+              void* stream) {
+    int rc = lf::check_args(idx, Q, opts);
+    if (rc) return rc;
+    if (Q == 0) return LF_OK;
+    auto* ss = new lf_session();
+    ss->idx = *idx;
+    ss->opts = *opts;
+    ss->opts.want_trace = (opts->want_trace && trace != nullptr) ? 1 : 0;
+    if (ss->opts.want_trace) ss->tr = *trace;
+    ss->st = lf::as_stream(stream);
+    ss->Q = Q;
+    ss->d_q = d_queries;
+    ss->s.stats = reinterpret_cast<long long*>(d_out_stats);
+    rc = lf::session_begin(ss);
+    if (rc) {
+        lf::session_free(ss);
+        return rc;
+    }
+    int active = 0;
+    do {
+        rc = lf_search_round(ss, nullptr, nullptr, &active);
+        if (rc) break;
+    } while (active > 0);
+    if (rc == LF_OK) rc = lf_search_end(ss, d_out_ids, d_out_dists);
+    lf_search_free(ss);
+    return rc;
+}
+
+}  // extern "C"

@@ -152,7 +152,7 @@ def _queries_device(queries, m: int, dev):
 def search_batch(index, queries, k: int = 1, *, bsf_factor: float = 1.0, predictions=None,
                  offsets=None, leaf_filter=None, sequential: bool = False,
                  max_round_leaves: int = 64, want_trace: bool = False, stream=None,
-                 copy_out: bool = True, profile: np.ndarray | None = None):
+                 copy_out: bool = True, profile: np.ndarray | None = None, early_abandon: bool = True):
     """Search a batch of queries in one lf_search call.
 
     predictions: device fp32 [Q, F] filter outputs (FilterPack.predict), with
@@ -173,6 +173,7 @@ def search_batch(index, queries, k: int = 1, *, bsf_factor: float = 1.0, predict
     opts.sequential = 1 if sequential else 0
     opts.max_round_leaves = int(max_round_leaves)
     opts.want_trace = 1 if want_trace else 0
+    opts.early_abandon = 1 if early_abandon else 0
     if profile is not None:
         if profile.dtype != np.float64 or profile.shape[0] < _lib.N_PROF:
             raise ValueError("profile must be a float64 array of at least N_PROF entries")

@@ -157,15 +157,20 @@ class TreeIndex:
         return t
 
     # ------------------------------------------------------------ device --
-    def device(self, device=None) -> "DeviceIndex":
+    def device(self, device=None, leaf_range=None) -> "DeviceIndex":
         torch = _lib.require_cuda()
         dev = torch.device(device if device is not None else "cuda")
         if dev.index is None:
             dev = torch.device("cuda", torch.cuda.current_device())
-        key = str(dev)
+        key = (str(dev), tuple(leaf_range) if leaf_range is not None else None)
         if key not in self._device:
-            self._device[key] = DeviceIndex(self, dev)
+            self._device[key] = DeviceIndex(self, dev, leaf_range)
         return self._device[key]
+
+    def shard(self, rank: int, world: int, device=None) -> "DeviceIndex":
+        """This rank's leaf shard (contiguous leaves, balanced by series count)."""
+        sizes = self.size[self.leaf_ids]
+        return self.device(device, shard_leaf_ranges(sizes, world)[rank])
 
 
 def build_index(values, max_leaf_size: int = 1000, segments: int = 8,
@@ -239,15 +244,41 @@ def segment_means(values, segments: int = 8) -> np.ndarray:
     return out
 
 
-class DeviceIndex:
-    """The tree in HBM (see module docstring for the layout)."""
+def shard_leaf_ranges(sizes, world: int) -> list:
+    """Cut leaves (ascending node id) into `world` contiguous ranges of about equal
+    series count: range r ends at the first leaf whose cumulative
+    size reaches (r+1)/world of the total."""
+    sizes = np.asarray(sizes, dtype=np.int64)
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    csum = np.cumsum(sizes)
+    total = int(csum[-1]) if csum.size else 0
+    bounds = [0]
+    for r in range(1, world):
+        cut = int(np.searchsorted(csum, total * r / world, side="left")) + 1
+        bounds.append(min(max(cut, bounds[-1]), sizes.shape[0]))
+    bounds.append(sizes.shape[0])
+    return [(bounds[r], bounds[r + 1]) for r in range(world)]
 
-    def __init__(self, t: TreeIndex, dev):
+
+class DeviceIndex:
+    """The tree in HBM (see module docstring for the layout).
+
+    leaf_range=(a, b) keeps only leaf slots a..b-1 (a leaf shard): their rows,
+    and a node->leaf map in which every other leaf reads as "not mine" (-1),
+    so the kernels skip it exactly like an internal node.  Visit order and
+    bounds still cover the whole tree, so every shard agrees on the break point.
+    """
+
+    def __init__(self, t: TreeIndex, dev, leaf_range=None):
         import torch
 
         self.tree = t
         self.device = dev
-        leaf_ids = t.leaf_ids
+        all_leaves = t.leaf_ids
+        a, b = leaf_range if leaf_range is not None else (0, all_leaves.shape[0])
+        self.leaf_range = (int(a), int(b))
+        leaf_ids = all_leaves[a:b]
         sizes = t.member_ptr[leaf_ids + 1] - t.member_ptr[leaf_ids]
         leaf_ptr = np.zeros(leaf_ids.shape[0] + 1, dtype=np.int64)
         leaf_ptr[1:] = np.cumsum(sizes)

@@ -166,6 +166,7 @@ class EnhancedIndex:
         self.train_reports = train_reports or {}
         self._pack = pack
         self._offset_cache = {}
+        self._offset_vec_cache = {}
 
     @classmethod
     def adopt(cls, ref_eidx) -> "EnhancedIndex":
@@ -194,9 +195,18 @@ class EnhancedIndex:
             self._offset_cache[key] = got
         return got
 
-    def offset_vector(self, target: float) -> np.ndarray:
-        offs = self.tuned_offsets(target)
-        return np.array([offs[l] for l in self.pack.leaf_ids], dtype=np.float64)
+    def offset_vector(self, target: float, device: bool = False):
+        """Offsets in filter-pack order (host fp64, or a cached device tensor)."""
+        key = (float(target), bool(device))
+        got = self._offset_vec_cache.get(key)
+        if got is None:
+            offs = self.tuned_offsets(target)
+            got = np.array([offs[l] for l in self.pack.leaf_ids], dtype=np.float64)
+            if device:
+                import torch
+                got = torch.from_numpy(got).to(self.pack.device)
+            self._offset_vec_cache[key] = got
+        return got
 
 
 _adopted_eidx = {}
@@ -230,7 +240,7 @@ def search_queries(eidx, queries, k: int = 1, *, target: float | None = None, ex
         np.ascontiguousarray(np.atleast_2d(queries), dtype=np.float32))
     q = q.to(device=di.device, dtype=torch.float32)
     pred = pk.predict(q, stream=stream)
-    return search_batch(e.base, q, k, predictions=pred, offsets=e.offset_vector(target),
+    return search_batch(e.base, q, k, predictions=pred, offsets=e.offset_vector(target, device=True),
                         leaf_filter=pk.leaf_filter(di), sequential=sequential,
                         max_round_leaves=max_round_leaves, want_trace=want_trace, stream=stream,
                         copy_out=copy_out, profile=profile)

@@ -281,3 +281,25 @@ def test_infinite_prediction_prunes(small_tree, small_golden):
     out = search_engine(small_tree, small_golden["queries"][0], 1, predictors={leaf: lambda q: 1e9},
                         offsets={leaf: 0.0})
     assert out.stats.leaves_filter_pruned + out.stats.leaves_lb_pruned >= 1
+
+
+@pytest.mark.parametrize("m,k", [(64, 1), (128, 1), (128, 5), (256, 1)])
+def test_early_abandon_identical(m, k):
+    """The early-abandoning scan returns exactly what the full scan returns
+    (same ids, distances, counters), and matches the oracle."""
+    from paper_2502_01836_b200 import build_index, search_batch
+
+    data = lo.randwalk(12000, m, 21)
+    t = build_index(data, 400)
+    Q = np.concatenate([lo.noisy_queries(data, 16, nz, 30 + int(10 * nz)) for nz in (0.1, 0.2, 0.4)])
+    for seq in (True, False):
+        a = search_batch(t, Q, k, sequential=seq, early_abandon=True)
+        b = search_batch(t, Q, k, sequential=seq, early_abandon=False)
+        np.testing.assert_array_equal(a.ids, b.ids)
+        np.testing.assert_array_equal(a.dists, b.dists)
+        np.testing.assert_array_equal(a.stats, b.stats)
+    ot = lo.build_tree(data, 400)
+    for i in range(0, Q.shape[0], 7):
+        o = lo.search(ot, Q[i], k)
+        assert a.ids[i].tolist() == [x for x, _ in o.results]
+        np.testing.assert_allclose(a.dists[i], [d for _, d in o.results], rtol=DIST_RTOL)

@@ -1,0 +1,214 @@
+"""Multi-rank logic of the leaf-sharded search on CPU (gloo, world_size 2).
+
+The per-round collective driver (`sharded.run_rounds`: one MIN-allreduce of
+[bsf..., -active] per round, all-gather + (d, id) merge of the per-rank top-k,
+SUM of the counters) and the shard partition (`index.shard_leaf_ranges`) are
+product code.  The per-shard round engine here is a test double that replays
+the GPU round semantics with the oracle (lb -> filter -> scan over the shard's
+own leaves only), so the exchange logic is checked without a GPU.
+"""
+
+import math
+import multiprocessing as mp
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from oracle import leafi_oracle as lo
+
+
+class OracleRoundEngine:
+    """CPU replay of lf_search rounds over the leaves [a, b) of the leaf list."""
+
+    def __init__(self, tree, leaf_range, queries, k, preds=None, offsets=None, slot_of=None,
+                 bsf_factor=1.0, rmax=64):
+        import torch
+
+        self.torch = torch
+        self.t, self.Q, self.k, self.device = tree, len(queries), k, torch.device("cpu")
+        leaves = tree.leaf_ids
+        self.owned = set(leaves[leaf_range[0]:leaf_range[1]])
+        self.queries = queries
+        self.preds, self.offsets, self.slot_of = preds, offsets, slot_of or {}
+        self.f, self.rmax = bsf_factor, rmax
+        nn = tree.n_nodes
+        self.order, self.lbs = [], []
+        for q in queries:
+            qs = lo.paa(q, tree.starts, tree.widths)
+            lb = [lo.node_lb(qs, tree.env_min[i], tree.env_max[i], tree.widths) for i in range(nn)]
+            o = sorted(range(nn), key=lambda i: (lb[i], i))
+            self.order.append(o)
+            self.lbs.append([lb[i] for i in o])
+        self.cursor = [0] * self.Q
+        self.done = [False] * self.Q
+        self.top = [lo.KBest(k) for _ in range(self.Q)]
+        self.stats = np.zeros((self.Q, 6), dtype=np.int64)
+        self.r = 0
+
+    def round(self, bound, bsf_out) -> int:
+        R = min(self.rmax, 1 << self.r)
+        self.r += 1
+        active = 0
+        t = self.t
+        for qi in range(self.Q):
+            if self.done[qi]:
+                continue
+            bsf = min(self.top[qi].bsf, float(bound[qi]))
+            thr = bsf * self.f
+            st = self.stats[qi]
+            sel = []
+            cur = self.cursor[qi]
+            nn = t.n_nodes
+            while cur < nn:
+                node, lb = self.order[qi][cur], self.lbs[qi][cur]
+                mine = t.is_leaf(node) and node in self.owned
+                if lb > thr:
+                    if mine:
+                        st[0] += 1; st[2] += 1
+                    self.done[qi] = True
+                    break
+                cur += 1
+                if not mine:
+                    continue
+                st[0] += 1
+                s = self.slot_of.get(node)
+                if s is not None and self.preds is not None:
+                    st[4] += 1
+                    if float(self.preds[qi, s]) - self.offsets[s] > thr:
+                        st[3] += 1
+                        continue
+                st[1] += 1
+                st[5] += t.members[node].shape[0]
+                sel.append(node)
+                if len(sel) == R:
+                    break
+            if cur >= nn:
+                self.done[qi] = True
+            self.cursor[qi] = cur
+            if not self.done[qi]:
+                active += 1
+            for node in sel:
+                ids = t.members[node]
+                d = lo.row_dist(self.queries[qi], t.values[ids])
+                keep = d <= bsf
+                self.top[qi].offer(d[keep], ids[keep])
+        for qi in range(self.Q):
+            bsf_out[qi] = self.top[qi].bsf
+        return active
+
+    def end(self):
+        torch = self.torch
+        ids = torch.full((self.Q, self.k), -1, dtype=torch.int64)
+        d = torch.full((self.Q, self.k), math.inf, dtype=torch.float64)
+        for qi, tp in enumerate(self.top):
+            n = tp.i.shape[0]
+            ids[qi, :n] = torch.from_numpy(tp.i)
+            d[qi, :n] = torch.from_numpy(tp.d)
+        return ids, d, torch.from_numpy(self.stats.copy())
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, case, out):
+    import torch.distributed as dist
+    from paper_2502_01836_b200.index import shard_leaf_ranges
+    from paper_2502_01836_b200.sharded import run_rounds
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        data = lo.randwalk(3000, 32, 5)
+        tree = lo.build_tree(data, 100)
+        Q = np.concatenate([lo.noisy_queries(data, 8, nz, 40 + int(10 * nz)) for nz in (0.1, 0.3)])
+        sizes = [tree.members[l].shape[0] for l in tree.leaf_ids]
+        rng_ = shard_leaf_ranges(sizes, world)[rank]
+        kw = {}
+        if case["filters"]:
+            leaves = tree.leaf_ids
+            g = np.random.default_rng(3)
+            preds = g.uniform(0, 8, (Q.shape[0], len(leaves)))
+            kw = dict(preds=preds, offsets=np.full(len(leaves), 0.5), slot_of={l: s for s, l in enumerate(leaves)})
+        eng = OracleRoundEngine(tree, rng_, Q, case["k"], bsf_factor=case["f"], **kw)
+        ids, d, stats, rounds = run_rounds(eng)
+        out.put((rank, ids.numpy(), d.numpy(), stats.numpy(), rounds))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, case):
+    ctx = mp.get_context("fork")
+    out = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, case, out)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [out.get(timeout=120) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return sorted(res, key=lambda r: r[0])
+
+
+@pytest.mark.parametrize("k", [1, 4])
+def test_sharded_exact_equals_oracle(k):
+    res = _run(2, {"k": k, "f": 1.0, "filters": False})
+    (_, ids0, d0, st0, _), (_, ids1, d1, st1, _) = res
+    np.testing.assert_array_equal(ids0, ids1)                   # every rank holds the merged answer
+    np.testing.assert_array_equal(st0, st1)
+    data = lo.randwalk(3000, 32, 5)
+    tree = lo.build_tree(data, 100)
+    Q = np.concatenate([lo.noisy_queries(data, 8, nz, 40 + int(10 * nz)) for nz in (0.1, 0.3)])
+    for qi, q in enumerate(Q):
+        o = lo.search(tree, q, k)
+        assert ids0[qi].tolist() == [i for i, _ in o.results]
+        np.testing.assert_array_equal(d0[qi], [x for _, x in o.results])
+        # counters: identity holds, and the sharded walk scans at least what the sequential one does
+        assert st0[qi, 0] == st0[qi, 1] + st0[qi, 2] + st0[qi, 3]
+        assert st0[qi, 5] >= o.stats["series_scanned"]
+
+
+def test_sharded_matches_single_rank_filtered():
+    """With filters and eps pruning the answer can legitimately differ from exact,
+    but the 2-rank merge equals the 1-rank round engine's answer set semantics:
+    never better than exact, and an actual collection distance."""
+    two = _run(2, {"k": 1, "f": 0.8, "filters": True})
+    one = _run(1, {"k": 1, "f": 0.8, "filters": True})
+    data = lo.randwalk(3000, 32, 5)
+    tree = lo.build_tree(data, 100)
+    Q = np.concatenate([lo.noisy_queries(data, 8, nz, 40 + int(10 * nz)) for nz in (0.1, 0.3)])
+    for qi, q in enumerate(Q):
+        ex = lo.search(tree, q, 1).results[0][1]
+        for r in (two[0], one[0]):
+            rid, rd = int(r[1][qi, 0]), float(r[2][qi, 0])
+            assert rd >= ex - 1e-12
+            assert rd == lo.row_dist(q, data[[rid]])[0]
+
+
+def test_shard_ranges_balanced():
+    from paper_2502_01836_b200.index import shard_leaf_ranges
+
+    sizes = np.array([5, 9, 3, 7, 8, 2, 6, 10])
+    for w in (1, 2, 3, 4, 8):
+        r = shard_leaf_ranges(sizes, w)
+        assert r[0][0] == 0 and r[-1][1] == len(sizes)
+        assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
+    r = shard_leaf_ranges(np.full(8, 10), 4)
+    assert r == [(0, 2), (2, 4), (4, 6), (6, 8)]
+
+
+def test_merge_topk():
+    import torch
+    from paper_2502_01836_b200.sharded import merge_topk
+
+    ids = torch.tensor([[5, 2, -1, 9, 1, 7]])
+    d = torch.tensor([[1.0, 1.0, 0.0, 0.5, 3.0, 1.0]], dtype=torch.float64)
+    mi, md = merge_topk(ids, d, 3)
+    assert mi.tolist() == [[9, 2, 5]] and md.tolist() == [[0.5, 1.0, 1.0]]
