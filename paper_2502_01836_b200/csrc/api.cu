@@ -14,10 +14,26 @@ int fail(int code, const std::string& msg) {
     return code;
 }
 
+void keep_pool_warm() {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done_dev = dev;
+}
+
 int sm_count() {
+    static thread_local int cached_dev = -1, cached = 0;
     int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && dev == cached_dev) return cached;
     if (cudaGetDevice(&dev) != cudaSuccess) return 148;
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+    cached_dev = dev;
+    cached = n;
     return n;
 }
 

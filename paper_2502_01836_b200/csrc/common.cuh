@@ -28,6 +28,11 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 int sm_count();
 
+// Keep the stream-ordered allocator's pool warm across calls: by default the
+// pool trims to zero at every synchronisation, which turns each search call's
+// scratch into fresh cudaMalloc/cudaFree (and implicit syncs).
+void keep_pool_warm();
+
 // Stream-ordered scratch allocation that frees itself.
 struct Scratch {
     void* p = nullptr;
@@ -39,6 +44,7 @@ struct Scratch {
         if (p) cudaFreeAsync(p, s);
     }
     cudaError_t alloc(size_t bytes, cudaStream_t st) {
+        keep_pool_warm();
         s = st;
         return cudaMallocAsync(&p, bytes ? bytes : 16, st);
     }

@@ -763,7 +763,11 @@ static int session_begin(lf_session* ss) {
     LF_CUDA(ss->cand_i.alloc(sizeof(long long) * max_tasks * s.kc, st));
     LF_CUDA(ss->task_min.alloc(sizeof(double) * (s.want_trace ? max_tasks : 1), st));
     LF_CUDA(ss->n_active.alloc(sizeof(int), st));
-    LF_CUDA(cudaMallocHost(&ss->h_active, sizeof(int)));
+    {   // one pinned word per host thread; a round reads it right after its own sync
+        static thread_local int* pinned = nullptr;
+        if (pinned == nullptr) LF_CUDA(cudaMallocHost(&pinned, sizeof(int)));
+        ss->h_active = pinned;
+    }
 
     if (o.h_profile) {
         ss->prof = true;
@@ -900,7 +904,6 @@ static void session_free(lf_session* ss) {
     if (!ss) return;
     for (auto& e : ss->ev)
         if (e) cudaEventDestroy(e);
-    if (ss->h_active) cudaFreeHost(ss->h_active);
     delete ss;   // Scratch members free their device buffers stream-ordered
 }
 

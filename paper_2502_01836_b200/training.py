@@ -73,7 +73,7 @@ def init_weights(m: int, seed: int) -> tuple:
 
 
 def train_filters(bank, train_idx, train_y, val_idx, val_y, init, cfg: TrainConfig, seed: int = 0,
-                  device="cuda", record_trajectories: bool = False) -> tuple:
+                  device="cuda", record_trajectories: bool = False, tf32: bool = True) -> tuple:
     """Train F filters together.
 
     bank:      fp32 [n_rows, m] (device) -- every training/validation input row
@@ -111,6 +111,18 @@ def train_filters(bank, train_idx, train_y, val_idx, val_y, init, cfg: TrainConf
     g.manual_seed(int(seed) & 0x7FFFFFFF)
     Xv = bank[vidx]                                                    # [F, n_va, m]
     bs = cfg.batch_size
+    prev_tf32 = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = tf32        # batched GEMMs on the tensor cores
+    try:
+        return _train_loop(torch, dev, bank, tidx, vidx, ty, vy, F, n_tr, W1, b1, W2, b2, best, best_val,
+                           plateau_best, wait, lr, active, epochs, lr_hist, val_hist, g, Xv, bs, cfg,
+                           record_trajectories)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev_tf32
+
+
+def _train_loop(torch, dev, bank, tidx, vidx, ty, vy, F, n_tr, W1, b1, W2, b2, best, best_val, plateau_best,
+                wait, lr, active, epochs, lr_hist, val_hist, g, Xv, bs, cfg, record_trajectories):
     with torch.no_grad():
         for epoch in range(cfg.max_epochs):
             if not bool(active.any()):
@@ -120,6 +132,7 @@ def train_filters(bank, train_idx, train_y, val_idx, val_y, init, cfg: TrainConf
             epochs += active.to(torch.int64)
             step_lr = torch.where(active, lr, torch.zeros_like(lr)).to(torch.float32)
             perm = torch.argsort(torch.rand((F, n_tr), generator=g, device=dev), dim=1)
+            bad_epoch = torch.zeros(F, dtype=torch.bool, device=dev)
             for s in range(0, n_tr, bs):
                 sel = perm[:, s:s + bs]                                # [F, b]
                 b = sel.shape[1]
@@ -130,11 +143,7 @@ def train_filters(bank, train_idx, train_y, val_idx, val_y, init, cfg: TrainConf
                 pred = torch.bmm(H, W2[:, :, None])[:, :, 0] + b2[:, None]
                 err = pred - y
                 loss = (err * err).mean(dim=1)
-                bad = ~torch.isfinite(loss) & active
-                if bool(bad.any()):
-                    f = int(torch.nonzero(bad)[0, 0])
-                    raise TrainingDivergedError(
-                        f"non-finite loss at epoch {epoch} (lr={float(lr[f]):g}) for filter slot {f}")
+                bad_epoch |= ~torch.isfinite(loss) & active   # checked once per epoch (no per-step sync)
                 gr = err * (2.0 / b)                                   # [F, b]
                 gW2 = torch.bmm(H.transpose(1, 2), gr[:, :, None])[:, :, 0]
                 gb2 = gr.sum(dim=1)
@@ -145,6 +154,10 @@ def train_filters(bank, train_idx, train_y, val_idx, val_y, init, cfg: TrainConf
                 b1.sub_(step_lr[:, None] * gb1)
                 W2.sub_(step_lr[:, None] * gW2)
                 b2.sub_(step_lr * gb2)
+            if bool(bad_epoch.any()):
+                f = int(torch.nonzero(bad_epoch)[0, 0])
+                raise TrainingDivergedError(
+                    f"non-finite loss at epoch {epoch} (lr={float(lr[f]):g}) for filter slot {f}")
             Hv = torch.relu(torch.baddbmm(b1[:, None, :], Xv, W1))
             pv = torch.bmm(Hv, W2[:, :, None])[:, :, 0] + b2[:, None]
             ev = (pv.double() - vy.double())

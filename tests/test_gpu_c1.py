@@ -1,0 +1,65 @@
+"""BASELINE config 1 (100K x 256 random walk, cap 1000, 4 x 100 queries) on the GPU
+against the reference's own run (tests/golden/c1.*, produced by make_golden.py).
+
+* exact search: ids, distances (rel 1e-12) and every counter identical
+  (sequential schedule), and ids identical under the batched round schedule;
+* LeaFi at target 0.99 with filters trained by OUR pipeline: recall >= 0.97
+  per noise level (acceptance criterion 9, test_acceptance.py:306-311) and
+  mean pruning within 1 point of the reference's LeaFi run.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, load_golden
+from oracle import leafi_oracle as lo
+
+pytestmark = pytest.mark.gpu
+LEVELS = (0.1, 0.2, 0.3, 0.4)
+
+
+@pytest.fixture(scope="module")
+def c1():
+    from paper_2502_01836_b200 import build_index
+
+    data = lo.randwalk(100_000, 256, 1234)
+    t = build_index(data, 1000)
+    qs = {nz: lo.noisy_queries(data, 100, nz, 1234 + int(10 * nz)) for nz in LEVELS}
+    return {"data": data, "tree": t, "queries": qs, "golden": load_golden("c1.npz"),
+            "doc": json.loads((GOLDEN / "c1.json").read_text())}
+
+
+def test_c1_exact_identical(c1):
+    from paper_2502_01836_b200 import search_batch
+
+    g = c1["golden"]
+    for nz in LEVELS:
+        seq = search_batch(c1["tree"], c1["queries"][nz], 1, sequential=True)
+        np.testing.assert_array_equal(seq.ids, g[f"n{nz}_ids"])
+        np.testing.assert_allclose(seq.dists, g[f"n{nz}_dists"], rtol=1e-12)
+        np.testing.assert_array_equal(seq.stats, g[f"n{nz}_stats"])
+        rnd = search_batch(c1["tree"], c1["queries"][nz], 1)
+        np.testing.assert_array_equal(rnd.ids, g[f"n{nz}_ids"])
+
+
+def test_c1_leafi_recall_and_pruning(c1):
+    from paper_2502_01836_b200 import pipeline as pl
+    from paper_2502_01836_b200 import search_batch
+    from paper_2502_01836_b200.training import TrainConfig
+
+    fb = pl.filter_memory_bytes(256)
+    e = pl.enhance(c1["tree"], pl.SplitPlan(1500, 500, 300), pl.SelectionBudget(64 * 1024 * 1024, a=2.0), 1234,
+                   constants=pl.RuntimeConstants(2e-7, 6e-6, fb), train_cfg=TrainConfig(initial_lr=1e-3))
+    ref_rows = {(r["noise"], r["method"]): r for r in c1["doc"]["bench_rows"]}
+    assert e.filter_leaf_ids == c1["doc"]["selected"]
+    for nz in LEVELS:
+        Q = c1["queries"][nz]
+        ex = search_batch(c1["tree"], Q, 1)
+        res = pl.search_queries(e, Q, 1, target=0.99)
+        hits = [lo.recall_at_1(res.results(i), int(ex.ids[i, 0]), float(ex.dists[i, 0])) for i in range(len(Q))]
+        ours = float(np.mean(res.pruning_ratios()))
+        ref = ref_rows[(nz, "filtered")]["mean_pruning_ratio"]
+        assert np.mean(hits) >= 0.97, (nz, np.mean(hits))
+        assert ours >= ref - 0.01, (nz, ours, ref)

@@ -296,7 +296,8 @@ def test_early_abandon_identical(m, k):
         a = search_batch(t, Q, k, sequential=seq, early_abandon=True)
         b = search_batch(t, Q, k, sequential=seq, early_abandon=False)
         np.testing.assert_array_equal(a.ids, b.ids)
-        np.testing.assert_array_equal(a.dists, b.dists)
+        # per-chunk half-warp sums vs whole-row warp sums: same terms, other order
+        np.testing.assert_allclose(a.dists, b.dists, rtol=1e-14)
         np.testing.assert_array_equal(a.stats, b.stats)
     ot = lo.build_tree(data, 400)
     for i in range(0, Q.shape[0], 7):
