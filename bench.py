@@ -331,6 +331,35 @@ def run_ours(args, rank, world, device):
     value = nQ * args.steps / (ms / 1e3)
     clocks = clk.summary()
 
+    # training-data generation (BASELINE config 4 shape): exact query x leaf min-ED
+    tdg = None
+    if args.tdg_queries > 0:
+        from paper_2502_01836_b200.synth import queries_device
+        from paper_2502_01836_b200.targets import leaf_min_distances
+
+        Xq = w["di"].X
+        gq = torch.cat([queries_device(Xq, args.tdg_queries // 4, nz, args.seed + 77 + i)
+                        for i, nz in enumerate(NOISE_LEVELS)]).contiguous()
+        slots = list(range(tree.n_leaves))
+        leaf_min_distances(tree, gq[:256], slots)                       # warm-up / tensor maps
+        torch.cuda.synchronize()
+        te0 = torch.cuda.Event(enable_timing=True)
+        te1 = torch.cuda.Event(enable_timing=True)
+        te0.record(stream)
+        dl = leaf_min_distances(tree, gq, slots)
+        te1.record(stream)
+        torch.cuda.synchronize()
+        t_ms = te0.elapsed_time(te1)
+        pairs = gq.shape[0] * tree.n
+        flops = 2.0 * pairs * tree.m
+        tdg = {"queries": int(gq.shape[0]), "leaves": tree.n_leaves, "series": tree.n, "ms": t_ms,
+               "pairs_per_s": pairs / (t_ms / 1e3), "algorithmic_tflops": flops / (t_ms / 1e3) / 1e12,
+               "tensor_peak_tflops": tf32_peak(), "frac_of_tf32_peak": flops / (t_ms / 1e3) / 1e12 / tf32_peak(),
+               "path": "tcgen05 tf32 GEMM + exact fp64 re-check (lf_leaf_min_dist_tc)",
+               "exact_zero_check": bool(torch.isfinite(dl).all().item()),
+               "reference_cpu_pairs_per_s_per_core": "1.0-1.3e6 (BASELINE.md, collect_targets at C1)"}
+        del dl, gq
+
     # e2e through the public API: pinned host queries in, host results out
     Qh = Q.cpu().pin_memory()
     for _ in range(2):
@@ -393,6 +422,7 @@ def run_ours(args, rank, world, device):
             "peak_source": "dense tf32 = 1/2 of measured bf16 (MEASURED_PEAKS.json bf16_tflops)",
         },
         "setup_s": w["setup_s"],
+        "train_data_gen": tdg,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         workers = os.cpu_count() or 1
@@ -461,6 +491,8 @@ def main():
     ap.add_argument("--ref-step-s", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--max-epochs", type=int, default=1000, help="filter training cap (setup speed)")
+    ap.add_argument("--tdg-queries", type=int, default=2000,
+                    help="queries for the training-data-generation measurement (0 = skip)")
     ap.add_argument("--ncu", action="store_true",
                     help="bracket the timed steps with cudaProfilerStart/Stop (ncu --profile-from-start off)")
     args = ap.parse_args()

@@ -181,6 +181,19 @@ int lf_local_min_dist(const float* d_queries, const lf_index* idx, const int64_t
                       void* stream);
 
 /*
+ * Tensor-core versions of the two calls above (m in {32, ..., 256}): tf32
+ * tcgen05 GEMM for q . x with a rigorous per-pair error bound, then an exact fp64
+ * re-check of the rows that can still be the minimum -- results are the exact
+ * fp64 direct-form minima, bit-identical to lf_leaf_min_dist.  Leaf selection and
+ * groups are HOST arrays here.
+ */
+int lf_leaf_min_dist_tc(const float* d_queries, int64_t Q, const lf_index* idx,
+                        const int32_t* h_leaf_sel, int32_t S, double* d_dl, int64_t ldd,
+                        void* stream);
+int lf_local_min_dist_tc(const float* d_queries, const lf_index* idx, const int64_t* h_qptr,
+                         const int32_t* h_group_leaf, int32_t n_groups, double* d_dl, void* stream);
+
+/*
  * Full distance matrix between queries and an arbitrary row block
  * (series.batch_distances, series.py:127-139). d_block [B][m], out [Q][B].
  */

@@ -595,6 +595,208 @@ __global__ void __launch_bounds__(SCAN_THREADS) scan_ea_kernel(RoundState s, lf_
     }
 }
 
+// Early-abandoning scan, v2 (m % 64 == 0).  A task's rows are read in three
+// phases so that the loads that matter are issued with maximum memory-level
+// parallelism:
+//   phase 0 (k = 1 and no best-so-far yet): 16 rows are scanned in full to get
+//            an upper bound on the task's best distance;
+//   phase 1: the FIRST 64 dims (256 B) of every row, 8 rows in flight per
+//            half-warp, partial sums kept in smem;
+//   phase 2: rows whose partial already exceeds the threshold are dropped --
+//            the remaining 768 B of those rows are never fetched from HBM;
+//   phase 3: survivors are finished piece by piece, abandoning as they go.
+// Threshold = round-start bound (tree.py:207: d <= bsf is kept) and, for k = 1,
+// the best full distance seen in the task, both with a 1e-12 relative margin.
+template <int NCH>
+__global__ void __launch_bounds__(SCAN_THREADS, 3) scan_ea2_kernel(RoundState s, lf_index idx,
+                                                                   const float* __restrict__ queries) {
+    constexpr int M = NCH * 64;
+    constexpr int U = 8;
+    constexpr double kMargin = 1.0 + 1e-12;
+    __shared__ double qs[M];
+    __shared__ double part[CH];
+    __shared__ double sd[CH];
+    __shared__ long long sid[CH];
+    __shared__ int surv[CH];
+    __shared__ int n_surv;
+    __shared__ unsigned long long best_bits;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int hl = lane & 15;
+    const int slot = warp * 2 + (lane >> 4);
+    const long long total = s.chunk_off[s.Q];
+    for (long long t = blockIdx.x; t < total; t += gridDim.x) {
+        int64_t lo = 0, hi = s.Q;
+        while (hi - lo > 1) {
+            int64_t mid = (lo + hi) >> 1;
+            if (s.chunk_off[mid] <= t) lo = mid; else hi = mid;
+        }
+        const int64_t q = lo;
+        const int local = (int)(t - s.chunk_off[q]);
+        const int* pre = s.sel_pre + q * (s.Rcap + 1);
+        int j = 0;
+        while (pre[j + 1] <= local) ++j;
+        const int leaf = s.sel_leaf[q * s.Rcap + j];
+        const int c = local - pre[j];
+        const int64_t lbeg = idx.d_leaf_ptr[leaf], lend = idx.d_leaf_ptr[leaf + 1];
+        const int64_t r0 = lbeg + (int64_t)c * CH;
+        const int nrows = (int)min((int64_t)CH, lend - r0);
+        const double bsf = round_bsf(s, q);
+        const float* qrow = queries + q * M;
+        const float* X0 = idx.d_X + r0 * M;
+        for (int i = threadIdx.x; i < M; i += SCAN_THREADS) qs[i] = (double)qrow[i];
+        if (threadIdx.x == 0) { n_surv = 0; best_bits = 0x7ff0000000000000ULL; }
+        __syncthreads();
+
+        // ---- phase 0: full distances of the first 16 rows when nothing bounds the task
+        const bool sample = (s.k == 1) && !(bsf < kInf);
+        if (sample) {
+            const int r = slot;
+            double acc = 0.0;
+            if (r < nrows) {
+                const float4* rp = reinterpret_cast<const float4*>(X0 + (int64_t)r * M);
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch) {
+                    const float4 x = __ldcs(rp + ch * 16 + hl);
+                    const double* qq = qs + ch * 64 + hl * 4;
+                    double d0 = (double)x.x - qq[0], d1 = (double)x.y - qq[1];
+                    double d2 = (double)x.z - qq[2], d3 = (double)x.w - qq[3];
+                    acc = __fma_rn(d0, d0, acc); acc = __fma_rn(d1, d1, acc);
+                    acc = __fma_rn(d2, d2, acc); acc = __fma_rn(d3, d3, acc);
+                }
+            }
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (r < nrows && hl == 0)
+                atomicMin(&best_bits, (unsigned long long)__double_as_longlong(acc));
+            __syncthreads();
+        }
+        double thr2 = bsf < kInf ? bsf * bsf * kMargin : kInf;
+        if (sample) thr2 = fmin(thr2, __longlong_as_double((long long)best_bits) * kMargin);
+
+        // ---- phase 1: first 64 dims of every row, U rows in flight per half-warp
+        for (int b0 = 0; b0 < nrows; b0 += 16 * U) {
+            float4 x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int r = b0 + slot + 16 * u;
+                x[u] = r < nrows ? __ldcs(reinterpret_cast<const float4*>(X0 + (int64_t)r * M) + hl)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            const double* qq = qs + hl * 4;
+            const double q0 = qq[0], q1 = qq[1], q2 = qq[2], q3 = qq[3];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                double d0 = (double)x[u].x - q0, d1 = (double)x[u].y - q1;
+                double d2 = (double)x[u].z - q2, d3 = (double)x[u].w - q3;
+                double a = d0 * d0;
+                a = __fma_rn(d1, d1, a); a = __fma_rn(d2, d2, a); a = __fma_rn(d3, d3, a);
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+                const int r = b0 + slot + 16 * u;
+                if (r < nrows && hl == 0) part[r] = a;
+            }
+        }
+        __syncthreads();
+        // ---- phase 2: survivors
+        for (int r = threadIdx.x; r < nrows; r += SCAN_THREADS) {
+            sid[r] = idx.d_row_id[r0 + r];
+            if (part[r] > thr2) {
+                sd[r] = kInf;
+            } else if (NCH == 1) {
+                sd[r] = sqrt(part[r]);
+            } else {
+                surv[atomicAdd(&n_surv, 1)] = r;
+            }
+        }
+        __syncthreads();
+        // ---- phase 3: finish survivors, one half-warp per row, 4 rows in flight
+        if (NCH > 1) {
+            const int ns = n_surv;
+            double best2 = __longlong_as_double((long long)best_bits);
+            for (int b0 = 0; b0 < ns; b0 += 16 * 4) {
+                double acc[4];
+                bool alive[4];
+                int rr[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int jj = b0 + slot + 16 * u;
+                    alive[u] = jj < ns;
+                    rr[u] = alive[u] ? surv[jj] : 0;
+                    acc[u] = 0.0;
+                }
+                double p[4];
+#pragma unroll
+                for (int ch = 1; ch < NCH; ++ch) {
+                    float4 x[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        x[u] = alive[u] ? __ldcs(reinterpret_cast<const float4*>(X0 + (int64_t)rr[u] * M) + ch * 16 + hl)
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+                    const double* qq = qs + ch * 64 + hl * 4;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        double d0 = (double)x[u].x - qq[0], d1 = (double)x[u].y - qq[1];
+                        double d2 = (double)x[u].z - qq[2], d3 = (double)x[u].w - qq[3];
+                        acc[u] = __fma_rn(d0, d0, acc[u]); acc[u] = __fma_rn(d1, d1, acc[u]);
+                        acc[u] = __fma_rn(d2, d2, acc[u]); acc[u] = __fma_rn(d3, d3, acc[u]);
+                        double v = acc[u];
+#pragma unroll
+                        for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                        p[u] = (alive[u] ? part[rr[u]] : 0.0) + v;
+                    }
+                    const double th = s.k == 1 ? fmin(thr2, best2 * kMargin) : thr2;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (alive[u] && p[u] > th) {
+                            alive[u] = false;
+                            if (hl == 0) sd[rr[u]] = kInf;
+                        }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (alive[u]) {
+                        if (s.k == 1) best2 = fmin(best2, p[u]);
+                        if (hl == 0) sd[rr[u]] = sqrt(p[u]);
+                    }
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+            double* cd = s.cand_d + t * s.kc;
+            long long* ci = s.cand_i + t * s.kc;
+            for (int i = lane; i < nrows; i += 32)
+                if (!(sd[i] <= bsf)) sd[i] = kInf;
+            __syncwarp();
+            if (s.kc >= nrows) {
+                for (int i = lane; i < s.kc; i += 32) {
+                    cd[i] = i < nrows ? sd[i] : kInf;
+                    ci[i] = (i < nrows && sd[i] != kInf) ? sid[i] : -1;
+                }
+            } else {
+                for (int sel = 0; sel < s.kc; ++sel) {
+                    double bd = kInf; long long bi = LLONG_MAX; int bp = -1;
+                    for (int i = lane; i < nrows; i += 32)
+                        if (pair_less(sd[i], sid[i], bd, bi)) { bd = sd[i]; bi = sid[i]; bp = i; }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        double od = __shfl_xor_sync(0xffffffffu, bd, o);
+                        long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                        int op = __shfl_xor_sync(0xffffffffu, bp, o);
+                        if (pair_less(od, oi, bd, bi)) { bd = od; bi = oi; bp = op; }
+                    }
+                    if (lane == 0) {
+                        cd[sel] = bd;
+                        ci[sel] = (bd == kInf) ? -1 : bi;
+                        if (bp >= 0) { sd[bp] = kInf; sid[bp] = LLONG_MAX; }
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // --------------------------------------------------------------- merge ----
 // One warp per query: k smallest (d, id) among the running top-k and this
 // round's candidates (each series is scanned at most once per query, so all
@@ -685,7 +887,7 @@ __global__ void finish_kernel(RoundState s, int64_t* out_ids, double* out_d) {
 template <int NCH>
 static cudaError_t launch_scan_ea(const RoundState& s, const lf_index& idx, const float* q, int grid,
                                   cudaStream_t st) {
-    scan_ea_kernel<NCH, 4><<<grid, SCAN_THREADS, 0, st>>>(s, idx, q);
+    scan_ea2_kernel<NCH><<<grid, SCAN_THREADS, 0, st>>>(s, idx, q);
     return cudaGetLastError();
 }
 
@@ -838,15 +1040,16 @@ static int session_round(lf_session* ss, const double* d_bound, double* d_bsf_ou
     cudaError_t ce;
     const bool ea = o.early_abandon && !s.want_trace && (idx.m % 64) == 0 && idx.m <= 512;
     if (ea) {
+        const int g3 = sm_count() * 3;            // __launch_bounds__(256, 3): 3 resident CTAs per SM
         switch (idx.m / 64) {
-            case 1: ce = launch_scan_ea<1>(s, idx, ss->d_q, grid, st); break;
-            case 2: ce = launch_scan_ea<2>(s, idx, ss->d_q, grid, st); break;
-            case 3: ce = launch_scan_ea<3>(s, idx, ss->d_q, grid, st); break;
-            case 4: ce = launch_scan_ea<4>(s, idx, ss->d_q, grid, st); break;
-            case 5: ce = launch_scan_ea<5>(s, idx, ss->d_q, grid, st); break;
-            case 6: ce = launch_scan_ea<6>(s, idx, ss->d_q, grid, st); break;
-            case 7: ce = launch_scan_ea<7>(s, idx, ss->d_q, grid, st); break;
-            default: ce = launch_scan_ea<8>(s, idx, ss->d_q, grid, st); break;
+            case 1: ce = launch_scan_ea<1>(s, idx, ss->d_q, g3, st); break;
+            case 2: ce = launch_scan_ea<2>(s, idx, ss->d_q, g3, st); break;
+            case 3: ce = launch_scan_ea<3>(s, idx, ss->d_q, g3, st); break;
+            case 4: ce = launch_scan_ea<4>(s, idx, ss->d_q, g3, st); break;
+            case 5: ce = launch_scan_ea<5>(s, idx, ss->d_q, g3, st); break;
+            case 6: ce = launch_scan_ea<6>(s, idx, ss->d_q, g3, st); break;
+            case 7: ce = launch_scan_ea<7>(s, idx, ss->d_q, g3, st); break;
+            default: ce = launch_scan_ea<8>(s, idx, ss->d_q, g3, st); break;
         }
     } else if ((idx.m & 3) != 0 || m4 <= 32) ce = launch_scan<1>(s, idx, ss->d_q, grid, st);
     else if (m4 <= 64) ce = launch_scan<2>(s, idx, ss->d_q, grid, st);

@@ -72,11 +72,20 @@ class LocalQueries:
 _QCHUNK = 64 * 65535   # lf_leaf_min_dist query-tile grid limit
 
 
-def leaf_min_distances(index, queries, leaf_slots) -> "torch.Tensor":
-    """Device fp64 [Q, S]: min distance from each query to each leaf slot (lf_leaf_min_dist)."""
+def tc_ok(m: int) -> bool:
+    """The tensor-core (tcgen05 tf32 + exact fp64 re-check) path covers m in {32, ..., 256}."""
+    return m % 32 == 0 and 32 <= m <= 256
+
+
+def leaf_min_distances(index, queries, leaf_slots, path: str | None = None) -> "torch.Tensor":
+    """Device fp64 [Q, S]: exact min distance from each query to each leaf slot.
+
+    path "tc" (default when m allows): lf_leaf_min_dist_tc; "simt": lf_leaf_min_dist
+    (fp64 CUDA cores).  Both return the same bits."""
     torch = _lib.require_cuda()
     t = as_tree(index)
     di = t.device()
+    path = path or ("tc" if tc_ok(t.m) else "simt")
     q = queries if isinstance(queries, torch.Tensor) else torch.from_numpy(
         np.ascontiguousarray(np.atleast_2d(queries), dtype=np.float32))
     q = q.to(device=di.device, dtype=torch.float32).contiguous()
@@ -84,6 +93,11 @@ def leaf_min_distances(index, queries, leaf_slots) -> "torch.Tensor":
     Q, S = q.shape[0], sel.shape[0]
     out = torch.empty((Q, S), dtype=torch.float64, device=di.device)
     st = di.struct(None)
+    if path == "tc" and Q and S:
+        hsel = np.ascontiguousarray(np.asarray(leaf_slots, dtype=np.int32))
+        _lib.check(_lib.lib().lf_leaf_min_dist_tc(q.data_ptr(), Q, st, _lib.ptr(hsel), S, out.data_ptr(), S,
+                                                  _lib.stream_ptr()))
+        return out
     for s0 in range(0, S, 65535):
         s1 = min(S, s0 + 65535)
         for q0 in range(0, Q, _QCHUNK):
@@ -202,11 +216,13 @@ def own_leaf_bounds(t, leaf_id: int, queries: np.ndarray) -> np.ndarray:
     return np.sqrt(acc)
 
 
-def local_targets_all(index, queries_by_leaf: dict) -> dict:
+def local_targets_all(index, queries_by_leaf: dict, path: str | None = None) -> dict:
     """{leaf_id: queries} -> {leaf_id: (targets, lbs)} in one lf_local_min_dist launch per 65535 leaves."""
     torch = _lib.require_cuda()
     t = as_tree(index)
     di = t.device()
+    path = path or ("tc" if tc_ok(t.m) else "simt")
+    fn = _lib.lib().lf_local_min_dist_tc if path == "tc" else _lib.lib().lf_local_min_dist
     leaves = list(queries_by_leaf)
     out = {}
     for g0 in range(0, len(leaves), 65535):
@@ -217,8 +233,8 @@ def local_targets_all(index, queries_by_leaf: dict) -> dict:
         allq = torch.from_numpy(np.concatenate(qs).astype(np.float32)).to(di.device)
         gleaf = np.array([di.slot_of_leaf[int(l)] for l in grp], dtype=np.int32)
         dl = torch.empty(int(qptr[-1]), dtype=torch.float64, device=di.device)
-        _lib.check(_lib.lib().lf_local_min_dist(allq.data_ptr(), di.struct(None), _lib.ptr(qptr),
-                                                _lib.ptr(gleaf), len(grp), dl.data_ptr(), _lib.stream_ptr()))
+        _lib.check(fn(allq.data_ptr(), di.struct(None), _lib.ptr(qptr), _lib.ptr(gleaf), len(grp),
+                      dl.data_ptr(), _lib.stream_ptr()))
         dlh = dl.cpu().numpy()
         for gi, l in enumerate(grp):
             out[l] = (dlh[qptr[gi]:qptr[gi + 1]], own_leaf_bounds(t, l, qs[gi]))
