@@ -268,14 +268,35 @@ def run_ours(args, rank, world, device):
     stream = torch.cuda.current_stream()
     prof = np.zeros(_lib.N_PROF)
 
-    def step(profile=None):
-        return search_queries(eidx, Q, 1, target=args.target, copy_out=False, profile=profile)
+    if world == 1 and not args.sharded:
+        def step(profile=None):
+            return search_queries(eidx, Q, 1, target=args.target, copy_out=False, profile=profile)
+
+        def checked(queries):
+            return search_queries(eidx, queries, 1, target=args.target)
+    else:
+        # leaf-sharded: this rank's leaves, rows and filters; one MIN-allreduce per round
+        from paper_2502_01836_b200.filters import FilterPack
+        from paper_2502_01836_b200.sharded import search_sharded
+
+        a, b = tree.shard(rank, world).leaf_range
+        local = [int(l) for l in tree.leaf_ids[a:b] if int(l) in eidx.filters]
+        lpack = FilterPack.from_models({l: eidx.filters[l] for l in local}) if local else None
+        offs_all = eidx.tuned_offsets(args.target)
+        loffs = np.array([offs_all[l] for l in local], dtype=np.float64)
+
+        def step(profile=None):
+            return search_sharded(tree, Q, 1, rank=rank, world=world, pack=lpack, offsets=loffs,
+                                  copy_out=False, profile=profile)
+
+        def checked(queries):
+            return search_sharded(tree, queries, 1, rank=rank, world=world, pack=lpack, offsets=loffs)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     # one checked run: recall and pruning of the exact workload being timed
-    chk = search_queries(eidx, Q, 1, target=args.target)
+    chk = checked(Q)
     recall = recall_of(chk, exact)
     per_noise = {}
     per = nQ // len(NOISE_LEVELS)
@@ -363,12 +384,16 @@ def run_ours(args, rank, world, device):
     # e2e through the public API: pinned host queries in, host results out
     Qh = Q.cpu().pin_memory()
     for _ in range(2):
-        search_queries(eidx, Qh, 1, target=args.target)
+        checked(Qh)
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     e0 = time.perf_counter()
     for _ in range(args.steps):
-        r = search_queries(eidx, Qh, 1, target=args.target)
+        r = checked(Qh)
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     e_s = (time.perf_counter() - e0) / args.steps
     e2e = {"value": nQ / e_s, "unit": "queries/s", "h2d_bytes_per_step": int(Q.numel() * 4),
            "d2h_bytes_per_step": int(nQ * (8 + 8 + 6 * 8)), "ms_per_step": e_s * 1e3}
@@ -491,6 +516,8 @@ def main():
     ap.add_argument("--ref-step-s", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--max-epochs", type=int, default=1000, help="filter training cap (setup speed)")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the leaf-sharded round driver even on one GPU (what N>1 runs)")
     ap.add_argument("--tdg-queries", type=int, default=2000,
                     help="queries for the training-data-generation measurement (0 = skip)")
     ap.add_argument("--ncu", action="store_true",

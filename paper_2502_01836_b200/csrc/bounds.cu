@@ -4,6 +4,7 @@
 // bound, np.dot -> one fp64 FMA chain over segments), summarize.py:114-122
 // (batched bound used by traingen, einsum -> sequential sum of (g*g)*w).
 // Both orders are reproduced bit-for-bit so visit orders and counters match.
+#include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 
 #include "bounds.cuh"
@@ -81,6 +82,102 @@ __global__ void iota_rows_kernel(int* __restrict__ v, int64_t Q, int n, int* __r
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t < Q * n) v[t] = (int)(t % n);
     if (t <= Q) offs[t] = (int)(t * n);
+}
+
+// Fused K1 + K2 for trees of up to 8192 nodes: one CTA per query computes every
+// node's search bound (lb_kernel<0> formula) straight into registers and sorts
+// the (lb, node id) pairs with a stable block radix sort in shared memory --
+// the bound matrix never round-trips through HBM before sorting.
+constexpr int FS_THREADS = 512;
+
+template <int ITEMS>
+__global__ void __launch_bounds__(FS_THREADS) bounds_sort_kernel(const double* __restrict__ qsumm, lf_index idx,
+                                                                 const double* __restrict__ env_min,
+                                                                 const double* __restrict__ env_max, int n_env,
+                                                                 double* __restrict__ lbs, int* __restrict__ order) {
+    using Sort = cub::BlockRadixSort<double, FS_THREADS, ITEMS, int>;
+    extern __shared__ __align__(16) uint8_t fs_smem[];
+    auto& tmp = *reinterpret_cast<typename Sort::TempStorage*>(fs_smem);
+    __shared__ double qs[LF_MAX_SEG];
+    __shared__ double ws[LF_MAX_SEG];
+    const int64_t q = blockIdx.x;
+    const int ns = idx.n_seg;
+    if (threadIdx.x < ns) {
+        qs[threadIdx.x] = qsumm[q * ns + threadIdx.x];
+        ws[threadIdx.x] = (double)idx.seg_width[threadIdx.x];
+    }
+    __syncthreads();
+    double keys[ITEMS];
+    int vals[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const int node = threadIdx.x * ITEMS + i;          // blocked arrangement: stable sort keeps id order
+        if (node < n_env) {
+            double acc = 0.0;
+            for (int sg = 0; sg < ns; ++sg) {
+                const double mn = env_min[(int64_t)sg * n_env + node];
+                const double mx = env_max[(int64_t)sg * n_env + node];
+                double g = fmax(mn - qs[sg], qs[sg] - mx);
+                g = fmax(g, 0.0);
+                acc = __fma_rn(__dmul_rn(ws[sg], g), g, acc);
+            }
+            keys[i] = sqrt(acc);
+            vals[i] = node;
+        } else {
+            keys[i] = kInf;                                // padding sorts last
+            vals[i] = INT_MAX;
+        }
+    }
+    Sort(tmp).Sort(keys, vals);
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const int pos = threadIdx.x * ITEMS + i;
+        if (pos < n_env) {
+            lbs[q * n_env + pos] = keys[i];
+            order[q * n_env + pos] = vals[i];
+        }
+    }
+}
+
+template <int ITEMS>
+static int launch_fused(const double* d_qsumm, int64_t Q, const lf_index& idx, int n, double* lbs, int* order,
+                        cudaStream_t st) {
+    using Sort = cub::BlockRadixSort<double, FS_THREADS, ITEMS, int>;
+    const int bytes = (int)sizeof(typename Sort::TempStorage);
+    static bool attr = false;
+    if (!attr) {
+        LF_CUDA(cudaFuncSetAttribute(bounds_sort_kernel<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        attr = true;
+    }
+    bounds_sort_kernel<ITEMS><<<(unsigned)Q, FS_THREADS, bytes, st>>>(d_qsumm, idx, idx.d_env_min, idx.d_env_max, n,
+                                                                      lbs, order);
+    LF_CUDA(cudaGetLastError());
+    return LF_OK;
+}
+
+// Segment means + bounds + per-query visit order in as few passes as the tree
+// size allows: fused block sort up to 8192 nodes, else bounds kernel + CUB.
+int bounds_and_order(const float* d_q, int64_t Q, const lf_index& idx, double* d_qsumm, double* d_lb_scratch,
+                     double* d_lbs, int* d_order, cudaStream_t st, int* kernels) {
+    const int n = idx.n_nodes;
+    if (Q == 0 || n == 0) return LF_OK;
+    if (n <= FS_THREADS * 16 && Q <= 0x7fffffff) {
+        {
+            int64_t tot = Q * idx.n_seg;
+            paa_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(d_q, Q, idx, d_qsumm);
+            LF_CUDA(cudaGetLastError());
+        }
+        int rc;
+        if (n <= FS_THREADS * 4) rc = launch_fused<4>(d_qsumm, Q, idx, n, d_lbs, d_order, st);
+        else if (n <= FS_THREADS * 8) rc = launch_fused<8>(d_qsumm, Q, idx, n, d_lbs, d_order, st);
+        else rc = launch_fused<16>(d_qsumm, Q, idx, n, d_lbs, d_order, st);
+        if (kernels) *kernels += 2;
+        return rc;
+    }
+    int rc = launch_bounds(d_q, Q, idx, idx.d_env_min, idx.d_env_max, n, 0, d_qsumm, d_lb_scratch, st);
+    if (rc) return rc;
+    if (kernels) *kernels += 4;
+    return sort_visit_order(d_lb_scratch, Q, n, d_lbs, d_order, st);
 }
 
 // Per-query stable sort of (lb, node id): the heap pop order of tree.py:256-275

@@ -22,7 +22,7 @@
 
 namespace lf {
 
-constexpr int CH = 256;          // rows per scan task (256 KiB at m = 256)
+constexpr int CH = 512;          // rows per scan task (512 KiB at m = 256)
 constexpr int SCAN_THREADS = 256;
 constexpr int SCAN_WARPS = SCAN_THREADS / 32;
 
@@ -49,6 +49,7 @@ struct RoundState {
     int* sel_pre;                // [Q][Rcap+1] chunk prefix within the query
     int* n_sel;                  // [Q]
     long long* chunk_off;        // [Q+1]
+    int4* tasks;                 // [max_tasks] (query, leaf slot, chunk, selection index)
     double* cand_d;              // [max_tasks][kc]
     long long* cand_i;
     double* task_min;            // [max_tasks] (trace only)
@@ -317,6 +318,22 @@ __global__ void offsets_kernel(long long* off, int64_t Q) {
     }
 }
 
+// Materialise this round's scan tasks: one warp per query writes
+// (query, leaf, chunk) for each chunk of each selected leaf at chunk_off[q] + ...
+__global__ void expand_tasks_kernel(RoundState s) {
+    const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (q >= s.Q) return;
+    const int ns = s.n_sel[q];
+    const long long base = s.chunk_off[q];
+    const int* pre = s.sel_pre + q * (s.Rcap + 1);
+    for (int j = 0; j < ns; ++j) {
+        const int leaf = s.sel_leaf[q * s.Rcap + j];
+        const int c0 = pre[j], n = pre[j + 1] - c0;
+        for (int c = lane; c < n; c += 32) s.tasks[base + c0 + c] = make_int4((int)q, leaf, c, j);
+    }
+}
+
 // ---------------------------------------------------------------- scan ----
 // Each lane owns VEC float4 slots of the series (slot v = lane + 32*u), so one
 // warp reads a row with fully coalesced 128-bit loads.
@@ -358,18 +375,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) scan_kernel(RoundState s, lf_ind
     const bool vec_ok = (m & 3) == 0;
     for (long long t = blockIdx.x; t < total; t += gridDim.x) {
         // locate (query, selected leaf, chunk)
-        int64_t lo = 0, hi = s.Q;               // chunk_off[lo] <= t < chunk_off[hi]
-        while (hi - lo > 1) {
-            int64_t mid = (lo + hi) >> 1;
-            if (s.chunk_off[mid] <= t) lo = mid; else hi = mid;
-        }
-        const int64_t q = lo;
-        const int local = (int)(t - s.chunk_off[q]);
-        const int* pre = s.sel_pre + q * (s.Rcap + 1);
-        int j = 0;
-        while (pre[j + 1] <= local) ++j;
-        const int leaf = s.sel_leaf[q * s.Rcap + j];
-        const int c = local - pre[j];
+        const int4 tk = s.tasks[t];             // (query, leaf slot, chunk) from expand_tasks_kernel
+        const int64_t q = tk.x;
+        const int leaf = tk.y;
+        const int c = tk.z;
         const int64_t lbeg = idx.d_leaf_ptr[leaf], lend = idx.d_leaf_ptr[leaf + 1];
         const int64_t r0 = lbeg + (int64_t)c * CH;
         const int nrows = (int)min((int64_t)CH, lend - r0);
@@ -486,18 +495,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) scan_ea_kernel(RoundState s, lf_
     const int m = idx.m;
     constexpr double kMargin = 1.0 + 1e-12;
     for (long long t = blockIdx.x; t < total; t += gridDim.x) {
-        int64_t lo = 0, hi = s.Q;
-        while (hi - lo > 1) {
-            int64_t mid = (lo + hi) >> 1;
-            if (s.chunk_off[mid] <= t) lo = mid; else hi = mid;
-        }
-        const int64_t q = lo;
-        const int local = (int)(t - s.chunk_off[q]);
-        const int* pre = s.sel_pre + q * (s.Rcap + 1);
-        int j = 0;
-        while (pre[j + 1] <= local) ++j;
-        const int leaf = s.sel_leaf[q * s.Rcap + j];
-        const int c = local - pre[j];
+        const int4 tk = s.tasks[t];             // (query, leaf slot, chunk) from expand_tasks_kernel
+        const int64_t q = tk.x;
+        const int leaf = tk.y;
+        const int c = tk.z;
         const int64_t lbeg = idx.d_leaf_ptr[leaf], lend = idx.d_leaf_ptr[leaf + 1];
         const int64_t r0 = lbeg + (int64_t)c * CH;
         const int nrows = (int)min((int64_t)CH, lend - r0);
@@ -625,18 +626,10 @@ __global__ void __launch_bounds__(SCAN_THREADS, 3) scan_ea2_kernel(RoundState s,
     const int slot = warp * 2 + (lane >> 4);
     const long long total = s.chunk_off[s.Q];
     for (long long t = blockIdx.x; t < total; t += gridDim.x) {
-        int64_t lo = 0, hi = s.Q;
-        while (hi - lo > 1) {
-            int64_t mid = (lo + hi) >> 1;
-            if (s.chunk_off[mid] <= t) lo = mid; else hi = mid;
-        }
-        const int64_t q = lo;
-        const int local = (int)(t - s.chunk_off[q]);
-        const int* pre = s.sel_pre + q * (s.Rcap + 1);
-        int j = 0;
-        while (pre[j + 1] <= local) ++j;
-        const int leaf = s.sel_leaf[q * s.Rcap + j];
-        const int c = local - pre[j];
+        const int4 tk = s.tasks[t];             // (query, leaf slot, chunk) from expand_tasks_kernel
+        const int64_t q = tk.x;
+        const int leaf = tk.y;
+        const int c = tk.z;
         const int64_t lbeg = idx.d_leaf_ptr[leaf], lend = idx.d_leaf_ptr[leaf + 1];
         const int64_t r0 = lbeg + (int64_t)c * CH;
         const int nrows = (int)min((int64_t)CH, lend - r0);
@@ -797,6 +790,171 @@ __global__ void __launch_bounds__(SCAN_THREADS, 3) scan_ea2_kernel(RoundState s,
     }
 }
 
+// Early-abandoning scan, v3 (m % 64 == 0): the abandon test is cheap fp32 and
+// conservative, the kept distances are exact fp64.
+//   phase 1: the first 64 dims of every row in fp32 (8 rows in flight per
+//            half-warp, the next batch's loads issued before this batch is
+//            reduced).  fp32 rounding of a 64-term sum is < 1e-5 relative, so
+//            a row is dropped only if partial32 * (1 - 1e-4) > thr^2 -- its
+//            exact distance then certainly exceeds thr;
+//   phase 2: every survivor is re-read whole (1 KiB, all four 256-byte pieces
+//            in flight at once) and summed exactly in fp64.
+// thr = the round-start bound (tree.py:207 keeps d <= bsf) and, for k = 1,
+// the best exact distance this CTA has found, shared through smem.
+template <int NCH>
+__global__ void __launch_bounds__(SCAN_THREADS, 4) scan_ea3_kernel(RoundState s, lf_index idx,
+                                                                   const float* __restrict__ queries) {
+    constexpr int M = NCH * 64;
+    constexpr int U = 8;
+    constexpr float kSafe = 1.0f - 1e-4f;
+    __shared__ float qf[M];
+    __shared__ double sd[CH];
+    __shared__ long long sid[CH];
+    __shared__ int surv[CH];
+    __shared__ int n_surv;
+    __shared__ unsigned long long best_bits;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int hl = lane & 15;
+    const int slot = warp * 2 + (lane >> 4);
+    const long long total = s.chunk_off[s.Q];
+    for (long long t = blockIdx.x; t < total; t += gridDim.x) {
+        const int4 tk = s.tasks[t];
+        const int64_t q = tk.x;
+        const int leaf = tk.y;
+        const int64_t lbeg = idx.d_leaf_ptr[leaf], lend = idx.d_leaf_ptr[leaf + 1];
+        const int64_t r0 = lbeg + (int64_t)tk.z * CH;
+        const int nrows = (int)min((int64_t)CH, lend - r0);
+        const double bsf = round_bsf(s, q);
+        const float* X0 = idx.d_X + r0 * M;
+        const float* qrow = queries + q * M;
+        for (int i = threadIdx.x; i < M; i += SCAN_THREADS) qf[i] = qrow[i];
+        if (threadIdx.x == 0) { n_surv = 0; best_bits = 0x7ff0000000000000ULL; }
+        __syncthreads();
+        const double thr2 = bsf < kInf ? bsf * bsf : kInf;
+
+        // exact fp64 distance of row r (whole row, 16 lanes, all pieces in flight)
+        auto exact_row = [&](int r, bool valid) -> double {
+            float4 x[NCH];
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch)
+                x[ch] = valid ? __ldg(reinterpret_cast<const float4*>(X0 + (int64_t)r * M) + ch * 16 + hl)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+            double acc = 0.0;
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch) {
+                const float* qq = qf + ch * 64 + hl * 4;
+                double d0 = (double)x[ch].x - (double)qq[0], d1 = (double)x[ch].y - (double)qq[1];
+                double d2 = (double)x[ch].z - (double)qq[2], d3 = (double)x[ch].w - (double)qq[3];
+                acc = __fma_rn(d0, d0, acc); acc = __fma_rn(d1, d1, acc);
+                acc = __fma_rn(d2, d2, acc); acc = __fma_rn(d3, d3, acc);
+            }
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            return acc;
+        };
+
+        // ---- phase 0 (k = 1, nothing bounds the task yet): 16 exact rows for a bound
+        if (s.k == 1 && !(bsf < kInf)) {
+            const bool v = slot < nrows;
+            const double e = exact_row(slot, v);
+            if (v && hl == 0) atomicMin(&best_bits, (unsigned long long)__double_as_longlong(e));
+            __syncthreads();
+        }
+        // ---- phase 1: first 64 dims in fp32, software-pipelined loads
+        {
+            const float q0 = qf[hl * 4], q1 = qf[hl * 4 + 1], q2 = qf[hl * 4 + 2], q3 = qf[hl * 4 + 3];
+            float4 cur[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int r = slot + 16 * u;
+                cur[u] = r < nrows ? __ldg(reinterpret_cast<const float4*>(X0 + (int64_t)r * M) + hl)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            for (int b0 = 0; b0 < nrows; b0 += 16 * U) {
+                float4 nxt[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int r = b0 + 16 * U + slot + 16 * u;
+                    nxt[u] = r < nrows ? __ldg(reinterpret_cast<const float4*>(X0 + (int64_t)r * M) + hl)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+                double thr_now = thr2;
+                if (s.k == 1) thr_now = fmin(thr_now, __longlong_as_double((long long)best_bits));
+                const float thr32 = thr_now < 3.0e38 ? (float)thr_now : 3.4e38f;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const float d0 = cur[u].x - q0, d1 = cur[u].y - q1, d2 = cur[u].z - q2, d3 = cur[u].w - q3;
+                    float a = d0 * d0;
+                    a = fmaf(d1, d1, a); a = fmaf(d2, d2, a); a = fmaf(d3, d3, a);
+#pragma unroll
+                    for (int o = 8; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+                    const int r = b0 + slot + 16 * u;
+                    if (r < nrows && hl == 0) {
+                        if (a * kSafe > thr32) {
+                            sd[r] = kInf;
+                        } else {
+                            surv[atomicAdd(&n_surv, 1)] = r;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+            }
+        }
+        __syncthreads();
+        // ---- phase 2: survivors, exact fp64 over the whole row
+        {
+            const int ns = n_surv;
+            for (int b0 = 0; b0 < ns; b0 += 16) {
+                const int jj = b0 + slot;
+                const bool v = jj < ns;
+                const int r = v ? surv[jj] : 0;
+                const double e = exact_row(r, v);
+                if (v && hl == 0) {
+                    sd[r] = sqrt(e);
+                    if (s.k == 1) atomicMin(&best_bits, (unsigned long long)__double_as_longlong(e));
+                }
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+            double* cd = s.cand_d + t * s.kc;
+            long long* ci = s.cand_i + t * s.kc;
+            for (int i = lane; i < nrows; i += 32) {
+                sid[i] = idx.d_row_id[r0 + i];
+                if (!(sd[i] <= bsf)) sd[i] = kInf;
+            }
+            __syncwarp();
+            if (s.kc >= nrows) {
+                for (int i = lane; i < s.kc; i += 32) {
+                    cd[i] = i < nrows ? sd[i] : kInf;
+                    ci[i] = (i < nrows && sd[i] != kInf) ? sid[i] : -1;
+                }
+            } else {
+                for (int sel = 0; sel < s.kc; ++sel) {
+                    double bd = kInf; long long bi = LLONG_MAX; int bp = -1;
+                    for (int i = lane; i < nrows; i += 32)
+                        if (pair_less(sd[i], sid[i], bd, bi)) { bd = sd[i]; bi = sid[i]; bp = i; }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        double od = __shfl_xor_sync(0xffffffffu, bd, o);
+                        long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                        int op = __shfl_xor_sync(0xffffffffu, bp, o);
+                        if (pair_less(od, oi, bd, bi)) { bd = od; bi = oi; bp = op; }
+                    }
+                    if (lane == 0) {
+                        cd[sel] = bd;
+                        ci[sel] = (bd == kInf) ? -1 : bi;
+                        if (bp >= 0) { sd[bp] = kInf; sid[bp] = LLONG_MAX; }
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // --------------------------------------------------------------- merge ----
 // One warp per query: k smallest (d, id) among the running top-k and this
 // round's candidates (each series is scanned at most once per query, so all
@@ -887,7 +1045,7 @@ __global__ void finish_kernel(RoundState s, int64_t* out_ids, double* out_d) {
 template <int NCH>
 static cudaError_t launch_scan_ea(const RoundState& s, const lf_index& idx, const float* q, int grid,
                                   cudaStream_t st) {
-    scan_ea2_kernel<NCH><<<grid, SCAN_THREADS, 0, st>>>(s, idx, q);
+    scan_ea3_kernel<NCH><<<grid, SCAN_THREADS, 0, st>>>(s, idx, q);
     return cudaGetLastError();
 }
 
@@ -911,7 +1069,7 @@ struct lf_session {
     const float* d_q = nullptr;
     lf::RoundState s{};
     lf::Scratch qsumm, lb, lbs, order, cursor, done, topd, topi, topn, topd2, topi2, topn2, sel_leaf,
-        sel_trace, sel_pre, n_sel, chunk_off, cand_d, cand_i, task_min, n_active;
+        sel_trace, sel_pre, n_sel, chunk_off, cand_d, cand_i, task_min, n_active, tasks;
     int* h_active = nullptr;
     int round = 0;
     long long kernels = 0;
@@ -945,7 +1103,7 @@ static int session_begin(lf_session* ss) {
     const int64_t max_chunks_leaf = std::max<int64_t>(1, (idx.max_leaf_rows + CH - 1) / CH);
     const int64_t max_tasks = std::max<int64_t>(1, Q * s.Rcap * max_chunks_leaf);
     LF_CUDA(ss->qsumm.alloc(sizeof(double) * Q * idx.n_seg, st));
-    LF_CUDA(ss->lb.alloc(sizeof(double) * Q * Nn, st));
+    LF_CUDA(ss->lb.alloc(Nn > 8192 ? sizeof(double) * Q * Nn : 16, st));   // only the unfused path uses it
     LF_CUDA(ss->lbs.alloc(sizeof(double) * Q * Nn, st));
     LF_CUDA(ss->order.alloc(sizeof(int) * Q * Nn, st));
     LF_CUDA(ss->cursor.alloc(sizeof(int) * Q, st));
@@ -965,6 +1123,7 @@ static int session_begin(lf_session* ss) {
     LF_CUDA(ss->cand_i.alloc(sizeof(long long) * max_tasks * s.kc, st));
     LF_CUDA(ss->task_min.alloc(sizeof(double) * (s.want_trace ? max_tasks : 1), st));
     LF_CUDA(ss->n_active.alloc(sizeof(int), st));
+    LF_CUDA(ss->tasks.alloc(sizeof(int4) * max_tasks, st));
     {   // one pinned word per host thread; a round reads it right after its own sync
         static thread_local int* pinned = nullptr;
         if (pinned == nullptr) LF_CUDA(cudaMallocHost(&pinned, sizeof(int)));
@@ -977,12 +1136,11 @@ static int session_begin(lf_session* ss) {
         for (auto& e : ss->ev) LF_CUDA(cudaEventCreate(&e));
         LF_CUDA(cudaEventRecord(ss->ev[0], st));
     }
-    int rc = launch_bounds(ss->d_q, Q, idx, idx.d_env_min, idx.d_env_max, Nn, 0, ss->qsumm.as<double>(),
-                           ss->lb.as<double>(), st);
+    int nk = 0;
+    int rc = bounds_and_order(ss->d_q, Q, idx, ss->qsumm.as<double>(), ss->lb.as<double>(), ss->lbs.as<double>(),
+                              ss->order.as<int>(), st, &nk);
     if (rc) return rc;
-    rc = sort_visit_order(ss->lb.as<double>(), Q, Nn, ss->lbs.as<double>(), ss->order.as<int>(), st);
-    if (rc) return rc;
-    ss->kernels += 4;
+    ss->kernels += nk;
 
     s.order = ss->order.as<int>();
     s.lbs = ss->lbs.as<double>();
@@ -1003,6 +1161,7 @@ static int session_begin(lf_session* ss) {
     s.cand_i = ss->cand_i.as<long long>();
     s.task_min = ss->task_min.as<double>();
     s.n_active = ss->n_active.as<int>();
+    s.tasks = ss->tasks.as<int4>();
 
     init_state_kernel<<<(unsigned)((Q + 127) / 128), 128, 0, st>>>(s);
     LF_CUDA(cudaGetLastError());
@@ -1034,13 +1193,14 @@ static int session_round(lf_session* ss, const double* d_bound, double* d_bsf_ou
     if (ss->prof) cudaEventRecord(ss->ev[2], st);
     plan_warp_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s, idx);
     offsets_kernel<<<1, 1024, 0, st>>>(s.chunk_off, Q);
+    expand_tasks_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s);
     if (ss->prof) cudaEventRecord(ss->ev[3], st);
     const int grid = sm_count() * 4;
     const int m4 = idx.m / 4;
     cudaError_t ce;
     const bool ea = o.early_abandon && !s.want_trace && (idx.m % 64) == 0 && idx.m <= 512;
     if (ea) {
-        const int g3 = sm_count() * 3;            // __launch_bounds__(256, 3): 3 resident CTAs per SM
+        const int g3 = sm_count() * 4;            // __launch_bounds__(256, 4): 4 resident CTAs per SM
         switch (idx.m / 64) {
             case 1: ce = launch_scan_ea<1>(s, idx, ss->d_q, g3, st); break;
             case 2: ce = launch_scan_ea<2>(s, idx, ss->d_q, g3, st); break;
@@ -1061,7 +1221,7 @@ static int session_round(lf_session* ss, const double* d_bound, double* d_bsf_ou
     merge_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s);
     LF_CUDA(cudaGetLastError());
     if (ss->prof) cudaEventRecord(ss->ev[5], st);
-    ss->kernels += 4;
+    ss->kernels += 5;
     std::swap(s.top_d, s.top_d_out);
     std::swap(s.top_i, s.top_i_out);
     std::swap(s.top_n, s.top_n_out);

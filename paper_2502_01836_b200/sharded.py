@@ -32,7 +32,7 @@ class GpuRoundEngine:
 
     def __init__(self, dindex, queries, k: int, *, predictions=None, offsets=None, leaf_filter=None,
                  bsf_factor: float = 1.0, max_round_leaves: int = 64, early_abandon: bool = True,
-                 stream=None):
+                 stream=None, profile=None):
         import torch
 
         self.torch = torch
@@ -60,6 +60,8 @@ class GpuRoundEngine:
                 o.d_pred = pr.data_ptr()
             o.d_offset = off.data_ptr()
             o.n_filters = int(off.shape[0])
+        if profile is not None:
+            o.h_profile = profile.ctypes.data
         self._opts = o
         self._ist = dindex.struct(lf)
         self.stats = torch.zeros((self.Q, _lib.N_STATS), dtype=torch.int64, device=self.device)
@@ -148,7 +150,8 @@ class ShardedResult:
 
 
 def search_sharded(tree, queries, k: int = 1, *, rank: int, world: int, pack=None, offsets=None,
-                   bsf_factor: float = 1.0, max_round_leaves: int = 64, group=None, copy_out: bool = True):
+                   bsf_factor: float = 1.0, max_round_leaves: int = 64, group=None, copy_out: bool = True,
+                   profile=None):
     """Leaf-sharded batched search on this rank's GPU (call on every rank).
 
     pack: this rank's FilterPack (its local filters only) with `offsets` in pack
@@ -162,7 +165,7 @@ def search_sharded(tree, queries, k: int = 1, *, rank: int, world: int, pack=Non
     kw = {}
     if pack is not None and pack.n_filters:
         kw = dict(predictions=pack.predict(q), offsets=offsets, leaf_filter=pack.leaf_filter(di))
-    eng = GpuRoundEngine(di, q, k, bsf_factor=bsf_factor, max_round_leaves=max_round_leaves, **kw)
+    eng = GpuRoundEngine(di, q, k, bsf_factor=bsf_factor, max_round_leaves=max_round_leaves, profile=profile, **kw)
     ids, d, stats, rounds = run_rounds(eng, group)
     if not copy_out:
         return ids, d, stats, rounds

@@ -304,3 +304,20 @@ def test_early_abandon_identical(m, k):
         o = lo.search(ot, Q[i], k)
         assert a.ids[i].tolist() == [x for x, _ in o.results]
         np.testing.assert_allclose(a.dists[i], [d for _, d in o.results], rtol=DIST_RTOL)
+
+
+def test_large_tree_unfused_order():
+    """> 8192 nodes: bounds kernel + CUB segmented sort instead of the fused block
+    sort; visit order, results and counters still equal the oracle's."""
+    from paper_2502_01836_b200 import build_index, search_batch
+
+    data = lo.randwalk(60000, 16, 12)
+    t = build_index(data, 12)
+    assert t.n_nodes > 8192
+    Q = lo.noisy_queries(data, 12, 0.2, 13)
+    res = search_batch(t, Q, 2, sequential=True)
+    ot = lo.build_tree(data, 12)
+    for i, q in enumerate(Q):
+        o = lo.search(ot, q, 2)
+        assert res.ids[i].tolist() == [a for a, _ in o.results]
+        assert res.stats[i].tolist() == [o.stats[s] for s in lo.STAT_KEYS]

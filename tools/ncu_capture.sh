@@ -12,7 +12,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start o
     > $OUT/ncu_bench.json 2> $OUT/ncu_bench.log
 echo "launch list rc=$?"
 ncu --set full --clock-control none --import-source on --profile-from-start off \
-    -k regex:"scan_ea_kernel|filter_tc_kernel|plan_warp_kernel" -c 6 -o $OUT/prof_full \
+    -k regex:"${KREGEX:-scan_ea2_kernel|filter_tc_kernel}" -c ${KCOUNT:-5} -o $OUT/prof_full \
     python bench.py --ncu --steps 1 --warmup 3 --no-cpu-baseline $EXTRA > $OUT/ncu_full.log 2>&1
 echo "full set rc=$?"
 ls -la $OUT
