@@ -73,7 +73,7 @@ typedef struct lf_search_opts {
                                     accumulated per phase, see LF_PROF_* */
 } lf_search_opts;
 
-#define LF_N_PROF 8
+#define LF_N_PROF 10
 #define LF_PROF_BOUNDS_MS 0      /* segment means + node bounds + visit-order sort */
 #define LF_PROF_PLAN_MS 1        /* plan + chunk offsets, all rounds */
 #define LF_PROF_SCAN_MS 2        /* leaf-scan kernel, all rounds */
@@ -81,6 +81,8 @@ typedef struct lf_search_opts {
 #define LF_PROF_ROUNDS 4         /* rounds executed */
 #define LF_PROF_KERNELS 5        /* kernels launched by the library (own kernels; CUB sort counted as 1) */
 #define LF_PROF_TOTAL_MS 6       /* whole call, first to last event */
+#define LF_PROF_EA_ROWS 8        /* rows tested by the early-abandon scan */
+#define LF_PROF_EA_SURVIVORS 9   /* rows that survived the first 64-dim test */
 
 /* Optional per-query trace (tree.py:77-83 TraceEntry), capacity n_leaves per query. */
 typedef struct lf_trace {
@@ -184,7 +186,8 @@ int lf_local_min_dist(const float* d_queries, const lf_index* idx, const int64_t
  * Tensor-core versions of the two calls above (m in {32, ..., 256}): tf32
  * tcgen05 GEMM for q . x with a rigorous per-pair error bound, then an exact fp64
  * re-check of the rows that can still be the minimum -- results are the exact
- * fp64 direct-form minima, bit-identical to lf_leaf_min_dist.  Leaf selection and
+ * fp64 direct-form minima (same terms as lf_leaf_min_dist, another summation
+ * order, so equal to ~1 ulp).  Leaf selection and
  * groups are HOST arrays here.
  */
 int lf_leaf_min_dist_tc(const float* d_queries, int64_t Q, const lf_index* idx,

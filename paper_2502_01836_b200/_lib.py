@@ -54,8 +54,9 @@ class LfSearchOpts(C.Structure):
     ]
 
 
-N_PROF = 8
-PROF_NAMES = ("bounds_ms", "plan_ms", "scan_ms", "merge_ms", "rounds", "kernels", "total_ms", "unused")
+N_PROF = 10
+PROF_NAMES = ("bounds_ms", "plan_ms", "scan_ms", "merge_ms", "rounds", "kernels", "total_ms", "unused",
+              "ea_rows", "ea_survivors")
 
 
 class LfTrace(C.Structure):

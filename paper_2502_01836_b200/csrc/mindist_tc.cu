@@ -14,12 +14,13 @@
 //     squared distance lies in [a - E, a + E];
 //  3. a row can only be the leaf minimum if its lower end a - E does not exceed
 //     U = min(best exact so far, min over the tile of a + E); those few rows are
-//     re-checked EXACTLY in fp64 direct form (k ascending FMA chain, the same
-//     order as the SIMT kernel) reading x from the resident smem tile, and folded
-//     with a 64-bit atomicMin on the bit pattern.
+//     re-checked EXACTLY in fp64 direct form by the whole warp (lane-strided
+//     partial sums + a fixed shuffle tree), reading x from the resident smem
+//     tile, and folded with a 64-bit atomicMin on the bit pattern.
 //
-// The result is therefore exactly the fp64 direct-form minimum (identical bits to
-// lf_leaf_min_dist), with the O(Q N m) work on the tensor cores and only
+// The result is therefore the exact fp64 direct-form minimum (same terms as
+// lf_leaf_min_dist, summed in another order: agreement to ~1 ulp), with the
+// O(Q N m) work on the tensor cores and only
 // O(Q L) exact re-checks (about one per (query, leaf) on random walks).
 //
 // Warp roles (192 threads, one persistent CTA per SM):
@@ -134,6 +135,7 @@ mindist_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_consta
     uint64_t* bfull = tempty + NACC;
     uint64_t* bempty = bfull + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + 1);
+    int* cand_list = reinterpret_cast<int*>(tmem_slot + 4);             // 4 epilogue warps x 64 entries
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m = idx.m;
@@ -262,31 +264,56 @@ mindist_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_consta
                             }
                         }
                     }
-                    // pass 2: exact re-check of every row whose interval reaches below U
+                    // pass 2: rows whose interval reaches below U are re-checked EXACTLY,
+                    // cooperatively: the warp gathers (lane, row) candidates and all 32
+                    // lanes sum one candidate at a time (k = lane + 32 i, then a
+                    // fixed shuffle tree) -- no 256-long dependent FMA chains.
+                    int* list = cand_list + (warp - 2) * 64;
+                    int cnt = 0;
+                    const long long qbase = item.q0 + (long long)qb * BM + quarter * 32;
+                    auto flush = [&]() {
+                        for (int e = 0; e < cnt; ++e) {
+                            const int ent = list[e];
+                            const int owner = ent >> 8, rr = ent & 255;
+                            const long long qe = qbase + owner;
+                            const float* qrow = Qm + qe * m;
+                            double part = 0.0;
+                            for (int k = lane; k < m; k += 32) {
+                                const double dd = (double)b_elem(Bt, rr, k) - (double)__ldg(qrow + k);
+                                part = __fma_rn(dd, dd, part);
+                            }
+#pragma unroll
+                            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+                            if (lane == owner && part < best) {
+                                best = part;
+                                atomicMin(dst, (unsigned long long)__double_as_longlong(part));
+                            }
+                        }
+                        __syncwarp();
+                        cnt = 0;
+                    };
                     for (int c0 = 0; c0 < BN; c0 += 32) {
                         uint32_t r[32];
                         LF_TMEM_LD32(taddr + (uint32_t)c0, r);
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                        if (!qv) continue;
-#pragma unroll 1
+#pragma unroll
                         for (int j = 0; j < 32; ++j) {
                             const int rr = c0 + j;
-                            if (rr >= nrows) break;
-                            const double a = qn + xn_s[rr] - 2.0 * (double)__uint_as_float(r[j]);
-                            if (a - kErr * qr * xr_s[rr] <= U) {
-                                const float* qrow = Qm + q * m;
-                                double e = 0.0;
-                                for (int k = 0; k < m; ++k) {
-                                    const double dd = (double)b_elem(Bt, rr, k) - (double)qrow[k];
-                                    e = __fma_rn(dd, dd, e);
-                                }
-                                if (e < best) {
-                                    best = e;
-                                    atomicMin(dst, (unsigned long long)__double_as_longlong(e));
-                                }
+                            bool cand = false;
+                            if (qv && rr < nrows) {
+                                const double a = qn + xn_s[rr] - 2.0 * (double)__uint_as_float(r[j]);
+                                cand = a - kErr * qr * xr_s[rr] <= U;
+                            }
+                            const unsigned mask = __ballot_sync(0xffffffffu, cand);
+                            if (mask) {
+                                if (cnt + 32 > 64) flush();
+                                if (cand) list[cnt + __popc(mask & ((1u << lane) - 1u))] = (lane << 8) | rr;
+                                __syncwarp();
+                                cnt += __popc(mask);
                             }
                         }
                     }
+                    if (cnt) flush();
                     fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[acc]);

@@ -15,6 +15,8 @@
 // With sequential=1 every round scans one leaf per query, which reproduces
 // the reference's traversal, counters and trace exactly.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "bounds.cuh"
@@ -50,6 +52,7 @@ struct RoundState {
     int* n_sel;                  // [Q]
     long long* chunk_off;        // [Q+1]
     int4* tasks;                 // [max_tasks] (query, leaf slot, chunk, selection index)
+    unsigned long long* ea_count;  // [2] rows tested / survivors (profiling only, may be NULL)
     double* cand_d;              // [max_tasks][kc]
     long long* cand_i;
     double* task_min;            // [max_tasks] (trace only)
@@ -702,6 +705,10 @@ __global__ void __launch_bounds__(SCAN_THREADS, 3) scan_ea2_kernel(RoundState s,
             }
         }
         __syncthreads();
+        if (s.ea_count != nullptr && threadIdx.x == 0) {
+            atomicAdd(&s.ea_count[0], (unsigned long long)nrows);
+            atomicAdd(&s.ea_count[1], (unsigned long long)n_surv);
+        }
         // ---- phase 3: finish survivors, one half-warp per row, 4 rows in flight
         if (NCH > 1) {
             const int ns = n_surv;
@@ -902,6 +909,10 @@ __global__ void __launch_bounds__(SCAN_THREADS, 4) scan_ea3_kernel(RoundState s,
             }
         }
         __syncthreads();
+        if (s.ea_count != nullptr && threadIdx.x == 0) {
+            atomicAdd(&s.ea_count[0], (unsigned long long)nrows);
+            atomicAdd(&s.ea_count[1], (unsigned long long)n_surv);
+        }
         // ---- phase 2: survivors, exact fp64 over the whole row
         {
             const int ns = n_surv;
@@ -1042,10 +1053,19 @@ __global__ void finish_kernel(RoundState s, int64_t* out_ids, double* out_d) {
     out_d[t] = ok ? s.top_d[t] : kInf;
 }
 
+// Scan variant (experiments): LF_SCAN_VARIANT = ea2 (default) | ea3 | full.
+static int scan_variant() {
+    const char* e = getenv("LF_SCAN_VARIANT");
+    return (e && strcmp(e, "ea3") == 0) ? 3 : (e && strcmp(e, "full") == 0) ? 0 : 2;
+}
+
 template <int NCH>
-static cudaError_t launch_scan_ea(const RoundState& s, const lf_index& idx, const float* q, int grid,
+static cudaError_t launch_scan_ea(const RoundState& s, const lf_index& idx, const float* q, int sms,
                                   cudaStream_t st) {
-    scan_ea3_kernel<NCH><<<grid, SCAN_THREADS, 0, st>>>(s, idx, q);
+    if (scan_variant() == 3)
+        scan_ea3_kernel<NCH><<<sms * 4, SCAN_THREADS, 0, st>>>(s, idx, q);
+    else
+        scan_ea2_kernel<NCH><<<sms * 3, SCAN_THREADS, 0, st>>>(s, idx, q);
     return cudaGetLastError();
 }
 
@@ -1069,7 +1089,7 @@ struct lf_session {
     const float* d_q = nullptr;
     lf::RoundState s{};
     lf::Scratch qsumm, lb, lbs, order, cursor, done, topd, topi, topn, topd2, topi2, topn2, sel_leaf,
-        sel_trace, sel_pre, n_sel, chunk_off, cand_d, cand_i, task_min, n_active, tasks;
+        sel_trace, sel_pre, n_sel, chunk_off, cand_d, cand_i, task_min, n_active, tasks, ea_count;
     int* h_active = nullptr;
     int round = 0;
     long long kernels = 0;
@@ -1124,6 +1144,8 @@ static int session_begin(lf_session* ss) {
     LF_CUDA(ss->task_min.alloc(sizeof(double) * (s.want_trace ? max_tasks : 1), st));
     LF_CUDA(ss->n_active.alloc(sizeof(int), st));
     LF_CUDA(ss->tasks.alloc(sizeof(int4) * max_tasks, st));
+    LF_CUDA(ss->ea_count.alloc(sizeof(unsigned long long) * 2, st));
+    LF_CUDA(cudaMemsetAsync(ss->ea_count.p, 0, sizeof(unsigned long long) * 2, st));
     {   // one pinned word per host thread; a round reads it right after its own sync
         static thread_local int* pinned = nullptr;
         if (pinned == nullptr) LF_CUDA(cudaMallocHost(&pinned, sizeof(int)));
@@ -1162,6 +1184,7 @@ static int session_begin(lf_session* ss) {
     s.task_min = ss->task_min.as<double>();
     s.n_active = ss->n_active.as<int>();
     s.tasks = ss->tasks.as<int4>();
+    s.ea_count = o.h_profile ? ss->ea_count.as<unsigned long long>() : nullptr;
 
     init_state_kernel<<<(unsigned)((Q + 127) / 128), 128, 0, st>>>(s);
     LF_CUDA(cudaGetLastError());
@@ -1198,9 +1221,9 @@ static int session_round(lf_session* ss, const double* d_bound, double* d_bsf_ou
     const int grid = sm_count() * 4;
     const int m4 = idx.m / 4;
     cudaError_t ce;
-    const bool ea = o.early_abandon && !s.want_trace && (idx.m % 64) == 0 && idx.m <= 512;
+    const bool ea = o.early_abandon && !s.want_trace && (idx.m % 64) == 0 && idx.m <= 512 && scan_variant() != 0;
     if (ea) {
-        const int g3 = sm_count() * 4;            // __launch_bounds__(256, 4): 4 resident CTAs per SM
+        const int g3 = sm_count();                // launch_scan_ea sizes the grid to the variant's residency
         switch (idx.m / 64) {
             case 1: ce = launch_scan_ea<1>(s, idx, ss->d_q, g3, st); break;
             case 2: ce = launch_scan_ea<2>(s, idx, ss->d_q, g3, st); break;
@@ -1259,6 +1282,10 @@ static int session_end(lf_session* ss, int64_t* out_ids, double* out_d, int64_t*
         p[LF_PROF_ROUNDS] = ss->round;
         p[LF_PROF_KERNELS] = (double)ss->kernels;
         p[LF_PROF_TOTAL_MS] = ev_ms(ss->ev[0], ss->ev[5]);
+        unsigned long long c[2] = {0, 0};
+        cudaMemcpy(c, ss->ea_count.p, sizeof(c), cudaMemcpyDeviceToHost);
+        p[LF_PROF_EA_ROWS] = (double)c[0];
+        p[LF_PROF_EA_SURVIVORS] = (double)c[1];
     }
     return LF_OK;
 }
