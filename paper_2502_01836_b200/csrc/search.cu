@@ -966,6 +966,193 @@ __global__ void __launch_bounds__(SCAN_THREADS, 4) scan_ea3_kernel(RoundState s,
     }
 }
 
+// Bounded scan over the int8 shadow (lf_quantize_rows): 1/4 of the bytes of
+// every row decide whether the exact fp32 row must be read at all.
+//   phase 1: half a warp per row, 8 rows in flight: dot = code . q (fp32),
+//            d^2 ~= |q|^2 + s^2 xx - 2 s dot, with its fp32 rounding bounded by
+//            tol = 1e-5 (|q|^2 + s^2 xx); the true distance then lies in
+//            [lo, hi] = [sqrt(d^2 - tol) - qerr, sqrt(d^2 + tol) + qerr] (both
+//            widened by 1e-6 for the sqrt rounding);
+//   phase 2: for k = 1 the task's best row is within min_r hi_r, so a row whose
+//            lo exceeds min(bsf, min hi) can never be the answer; every other
+//            row (the few that remain) is re-read whole and summed EXACTLY in
+//            fp64 -- kept distances are exact, dropped rows provably worse.
+template <int NCH>
+__global__ void __launch_bounds__(SCAN_THREADS, 4) scan_q8_kernel(RoundState s, lf_index idx,
+                                                                  const float* __restrict__ queries) {
+    constexpr int M = NCH * 64;
+    constexpr int P = (M + 255) / 256;            // 256-code passes per row (16 codes per lane)
+    constexpr int U = 8;
+    __shared__ float qf[M];
+    __shared__ float lo_s[CH];
+    __shared__ double sd[CH];
+    __shared__ long long sid[CH];
+    __shared__ int surv[CH];
+    __shared__ int n_surv;
+    __shared__ unsigned int hi_bits;
+    __shared__ float qq_s;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int hl = lane & 15;
+    const int slot = warp * 2 + (lane >> 4);
+    const long long total = s.chunk_off[s.Q];
+    for (long long t = blockIdx.x; t < total; t += gridDim.x) {
+        const int4 tk = s.tasks[t];
+        const int64_t q = tk.x;
+        const int leaf = tk.y;
+        const int64_t lbeg = idx.d_leaf_ptr[leaf], lend = idx.d_leaf_ptr[leaf + 1];
+        const int64_t r0 = lbeg + (int64_t)tk.z * CH;
+        const int nrows = (int)min((int64_t)CH, lend - r0);
+        const double bsf = round_bsf(s, q);
+        const float* qrow = queries + q * M;
+        for (int i = threadIdx.x; i < M; i += SCAN_THREADS) qf[i] = qrow[i];
+        if (threadIdx.x == 0) { n_surv = 0; hi_bits = 0x7f800000u; }
+        __syncthreads();
+        if (warp == 0) {
+            float a = 0.f;
+            for (int i = lane; i < M; i += 32) a = fmaf(qf[i], qf[i], a);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+            if (lane == 0) qq_s = a;
+        }
+        float qv[P][16];
+#pragma unroll
+        for (int p = 0; p < P; ++p)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int d = p * 256 + hl * 16 + i;
+                qv[p][i] = d < M ? qf[d] : 0.f;
+            }
+        __syncthreads();
+        const float qq = qq_s;
+        const int8_t* X8 = idx.d_X8 + r0 * M;
+        float hmin = __int_as_float(0x7f800000);
+        // ---- phase 1: bounds from the int8 codes
+        for (int b0 = 0; b0 < nrows; b0 += 16 * U) {
+            int4 w[U][P];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int r = b0 + slot + 16 * u;
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const bool ok = r < nrows && (p * 256 + hl * 16) < M;
+                    w[u][p] = ok ? __ldg(reinterpret_cast<const int4*>(X8 + (int64_t)r * M + p * 256) + hl)
+                                 : make_int4(0, 0, 0, 0);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                float dot = 0.f;
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const int ws[4] = {w[u][p].x, w[u][p].y, w[u][p].z, w[u][p].w};
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+#pragma unroll
+                        for (int b = 0; b < 4; ++b)
+                            dot = fmaf((float)(int8_t)(ws[c] >> (8 * b)), qv[p][c * 4 + b], dot);
+                }
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+                const int r = b0 + slot + 16 * u;
+                if (r < nrows) {
+                    const float sc = __ldg(idx.d_scale + r0 + r);
+                    const float s2xx = sc * sc * (float)__ldg(idx.d_xx + r0 + r);
+                    const float e = __ldg(idx.d_qerr + r0 + r);
+                    const float d2 = qq + s2xx - 2.f * sc * dot;
+                    const float tol = 1e-5f * (qq + s2xx);
+                    const float lo = (sqrtf(fmaxf(d2 - tol, 0.f)) - e) * (1.f - 1e-6f);
+                    const float hi = (sqrtf(fmaxf(d2 + tol, 0.f)) + e) * (1.f + 1e-6f);
+                    hmin = fminf(hmin, hi);
+                    if (hl == 0) lo_s[r] = lo;
+                }
+            }
+        }
+        if (s.k == 1) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) hmin = fminf(hmin, __shfl_xor_sync(0xffffffffu, hmin, o));
+            if (lane == 0) atomicMin(&hi_bits, __float_as_uint(hmin));
+        }
+        __syncthreads();
+        // ---- phase 2: survivors -> exact fp64 rows
+        {
+            double thr = bsf;
+            if (s.k == 1) thr = fmin(thr, (double)__uint_as_float(hi_bits));
+            const float thr_f = thr < kInf ? __double2float_ru(thr) : __int_as_float(0x7f800000);
+            for (int r = threadIdx.x; r < nrows; r += SCAN_THREADS) {
+                if (lo_s[r] <= thr_f) surv[atomicAdd(&n_surv, 1)] = r;
+                else sd[r] = kInf;
+            }
+        }
+        __syncthreads();
+        if (s.ea_count != nullptr && threadIdx.x == 0) {
+            atomicAdd(&s.ea_count[0], (unsigned long long)nrows);
+            atomicAdd(&s.ea_count[1], (unsigned long long)n_surv);
+        }
+        {
+            const int ns = n_surv;
+            const float* X0 = idx.d_X + r0 * M;
+            for (int b0 = 0; b0 < ns; b0 += 16) {
+                const int jj = b0 + slot;
+                const bool v = jj < ns;
+                const int r = v ? surv[jj] : 0;
+                float4 x[NCH];
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch)
+                    x[ch] = v ? __ldg(reinterpret_cast<const float4*>(X0 + (int64_t)r * M) + ch * 16 + hl)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+                double acc = 0.0;
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch) {
+                    const float* qq4 = qf + ch * 64 + hl * 4;
+                    double d0 = (double)x[ch].x - (double)qq4[0], d1 = (double)x[ch].y - (double)qq4[1];
+                    double d2 = (double)x[ch].z - (double)qq4[2], d3 = (double)x[ch].w - (double)qq4[3];
+                    acc = __fma_rn(d0, d0, acc); acc = __fma_rn(d1, d1, acc);
+                    acc = __fma_rn(d2, d2, acc); acc = __fma_rn(d3, d3, acc);
+                }
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (v && hl == 0) sd[r] = sqrt(acc);
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+            double* cd = s.cand_d + t * s.kc;
+            long long* ci = s.cand_i + t * s.kc;
+            for (int i = lane; i < nrows; i += 32) {
+                sid[i] = idx.d_row_id[r0 + i];
+                if (!(sd[i] <= bsf)) sd[i] = kInf;
+            }
+            __syncwarp();
+            if (s.kc >= nrows) {
+                for (int i = lane; i < s.kc; i += 32) {
+                    cd[i] = i < nrows ? sd[i] : kInf;
+                    ci[i] = (i < nrows && sd[i] != kInf) ? sid[i] : -1;
+                }
+            } else {
+                for (int sel = 0; sel < s.kc; ++sel) {
+                    double bd = kInf; long long bi = LLONG_MAX; int bp = -1;
+                    for (int i = lane; i < nrows; i += 32)
+                        if (pair_less(sd[i], sid[i], bd, bi)) { bd = sd[i]; bi = sid[i]; bp = i; }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        double od = __shfl_xor_sync(0xffffffffu, bd, o);
+                        long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                        int op = __shfl_xor_sync(0xffffffffu, bp, o);
+                        if (pair_less(od, oi, bd, bi)) { bd = od; bi = oi; bp = op; }
+                    }
+                    if (lane == 0) {
+                        cd[sel] = bd;
+                        ci[sel] = (bd == kInf) ? -1 : bi;
+                        if (bp >= 0) { sd[bp] = kInf; sid[bp] = LLONG_MAX; }
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // --------------------------------------------------------------- merge ----
 // One warp per query: k smallest (d, id) among the running top-k and this
 // round's candidates (each series is scanned at most once per query, so all
@@ -1056,13 +1243,18 @@ __global__ void finish_kernel(RoundState s, int64_t* out_ids, double* out_d) {
 // Scan variant (experiments): LF_SCAN_VARIANT = ea2 (default) | ea3 | full.
 static int scan_variant() {
     const char* e = getenv("LF_SCAN_VARIANT");
-    return (e && strcmp(e, "ea3") == 0) ? 3 : (e && strcmp(e, "full") == 0) ? 0 : 2;
+    if (e && strcmp(e, "ea3") == 0) return 3;
+    if (e && strcmp(e, "full") == 0) return 0;
+    if (e && strcmp(e, "ea2") == 0) return 2;
+    return 8;                                      // default: int8-bounded scan when the shadow exists
 }
 
 template <int NCH>
 static cudaError_t launch_scan_ea(const RoundState& s, const lf_index& idx, const float* q, int sms,
                                   cudaStream_t st) {
-    if (scan_variant() == 3)
+    if (scan_variant() == 8 && idx.d_X8 != nullptr)
+        scan_q8_kernel<NCH><<<sms * 4, SCAN_THREADS, 0, st>>>(s, idx, q);
+    else if (scan_variant() == 3)
         scan_ea3_kernel<NCH><<<sms * 4, SCAN_THREADS, 0, st>>>(s, idx, q);
     else
         scan_ea2_kernel<NCH><<<sms * 3, SCAN_THREADS, 0, st>>>(s, idx, q);

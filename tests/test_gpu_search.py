@@ -321,3 +321,28 @@ def test_large_tree_unfused_order():
         o = lo.search(ot, q, 2)
         assert res.ids[i].tolist() == [a for a, _ in o.results]
         assert res.stats[i].tolist() == [o.stats[s] for s in lo.STAT_KEYS]
+
+
+@pytest.mark.parametrize("variant", ["q8", "ea2", "ea3", "full"])
+@pytest.mark.parametrize("k", [1, 4])
+def test_scan_variants_agree(variant, k, monkeypatch):
+    """Every scan variant (int8-bounded, early-abandon v2/v3, full) returns the same
+    ids and exact distances; counters are identical (whole leaves are counted)."""
+    from paper_2502_01836_b200 import build_index, search_batch
+
+    data = lo.randwalk(15000, 128, 31)
+    t = build_index(data, 600)
+    Q = np.concatenate([lo.noisy_queries(data, 12, nz, 70 + int(10 * nz)) for nz in (0.1, 0.25, 0.4)])
+    monkeypatch.setenv("LF_SCAN_VARIANT", "full")
+    ref = search_batch(t, Q, k)
+    monkeypatch.setenv("LF_SCAN_VARIANT", variant if variant != "q8" else "q8")
+    got = search_batch(t, Q, k)
+    np.testing.assert_array_equal(got.ids, ref.ids)
+    np.testing.assert_allclose(got.dists, ref.dists, rtol=1e-14)
+    np.testing.assert_array_equal(got.stats, ref.stats)
+    seq = search_batch(t, Q, k, sequential=True)
+    ot = lo.build_tree(data, 600)
+    for i in range(0, Q.shape[0], 5):
+        o = lo.search(ot, Q[i], k)
+        assert seq.ids[i].tolist() == [a for a, _ in o.results]
+        assert seq.stats[i].tolist() == [o.stats[s_] for s_ in lo.STAT_KEYS]

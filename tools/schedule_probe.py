@@ -23,8 +23,8 @@ args = argparse.Namespace(n=a.n, m=256, leaf_cap=a.leaf_cap, queries=1000, targe
                           n_local=500, calibration=300, max_epochs=a.max_epochs)
 w = bench.setup_workload(args, torch.device("cuda", 0))
 e, Q = w["eidx"], w["Q"]
-configs = [("ea2", dict(max_round_leaves=64)), ("ea3", dict(max_round_leaves=64)), ("full", dict(max_round_leaves=64)),
-           ("ea2", dict(max_round_leaves=16)), ("ea2", dict(max_round_leaves=8)), ("ea2", dict(sequential=True))]
+configs = [("q8", dict(max_round_leaves=64)), ("ea2", dict(max_round_leaves=64)), ("full", dict(max_round_leaves=64)),
+           ("q8", dict(max_round_leaves=16)), ("q8", dict(max_round_leaves=256))]
 for var, kw in configs:
     os.environ["LF_SCAN_VARIANT"] = var
     search_queries(e, Q, 1, target=0.99, **kw)
