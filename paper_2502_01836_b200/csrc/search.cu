@@ -968,11 +968,13 @@ __global__ void __launch_bounds__(SCAN_THREADS, 4) scan_ea3_kernel(RoundState s,
 
 // Bounded scan over the int8 shadow (lf_quantize_rows): 1/4 of the bytes of
 // every row decide whether the exact fp32 row must be read at all.
-//   phase 1: half a warp per row, 8 rows in flight: dot = code . q (fp32),
-//            d^2 ~= |q|^2 + s^2 xx - 2 s dot, with its fp32 rounding bounded by
-//            tol = 1e-5 (|q|^2 + s^2 xx); the true distance then lies in
-//            [lo, hi] = [sqrt(d^2 - tol) - qerr, sqrt(d^2 + tol) + qerr] (both
-//            widened by 1e-6 for the sqrt rounding);
+//   phase 1: the query is quantised the same way (codes cq, scale sq, error
+//            eq = ||sq cq - q||, exact fp64, rounded up); half a warp per row,
+//            8 rows in flight, D = cx . cq with DP4A (exact int32);
+//            ||x^ - q^||^2 = sx^2 xx + sq^2 qq - 2 sx sq D (fp32, rounding
+//            bounded by tol = 1e-5 (sx^2 xx + sq^2 qq)), and by the triangle
+//            inequality the true distance lies in
+//            [sqrt(.. - tol) - ex - eq, sqrt(.. + tol) + ex + eq] (widened 1e-6);
 //   phase 2: for k = 1 the task's best row is within min_r hi_r, so a row whose
 //            lo exceeds min(bsf, min hi) can never be the answer; every other
 //            row (the few that remain) is re-read whole and summed EXACTLY in
@@ -984,13 +986,15 @@ __global__ void __launch_bounds__(SCAN_THREADS, 4) scan_q8_kernel(RoundState s, 
     constexpr int P = (M + 255) / 256;            // 256-code passes per row (16 codes per lane)
     constexpr int U = 8;
     __shared__ float qf[M];
+    __shared__ __align__(16) int8_t qc[P * 256];
     __shared__ float lo_s[CH];
     __shared__ double sd[CH];
     __shared__ long long sid[CH];
     __shared__ int surv[CH];
     __shared__ int n_surv;
     __shared__ unsigned int hi_bits;
-    __shared__ float qq_s;
+    __shared__ float qscale_s, qerr_s;
+    __shared__ int qq_s;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int hl = lane & 15;
     const int slot = warp * 2 + (lane >> 4);
@@ -1007,23 +1011,44 @@ __global__ void __launch_bounds__(SCAN_THREADS, 4) scan_q8_kernel(RoundState s, 
         for (int i = threadIdx.x; i < M; i += SCAN_THREADS) qf[i] = qrow[i];
         if (threadIdx.x == 0) { n_surv = 0; hi_bits = 0x7f800000u; }
         __syncthreads();
-        if (warp == 0) {
-            float a = 0.f;
-            for (int i = lane; i < M; i += 32) a = fmaf(qf[i], qf[i], a);
+        if (warp == 0) {                                   // quantise the query like the rows
+            float mx = 0.f;
+            for (int i = lane; i < M; i += 32) mx = fmaxf(mx, fabsf(qf[i]));
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-            if (lane == 0) qq_s = a;
-        }
-        float qv[P][16];
-#pragma unroll
-        for (int p = 0; p < P; ++p)
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int d = p * 256 + hl * 16 + i;
-                qv[p][i] = d < M ? qf[d] : 0.f;
+            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            const float sq = mx > 0.f ? mx / 127.f : 1.f;
+            int qq = 0;
+            double err = 0.0;
+            for (int i = lane; i < P * 256; i += 32) {
+                int c = 0;
+                if (i < M) {
+                    c = (int)fminf(fmaxf(rintf(qf[i] / sq), -127.f), 127.f);
+                    const double e = (double)sq * (double)c - (double)qf[i];
+                    err = __fma_rn(e, e, err);
+                }
+                qc[i] = (int8_t)c;
+                qq += c * c;
             }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                qq += __shfl_xor_sync(0xffffffffu, qq, o);
+                err += __shfl_xor_sync(0xffffffffu, err, o);
+            }
+            if (lane == 0) {
+                qscale_s = sq;
+                qq_s = qq;
+                qerr_s = __double2float_ru(sqrt(err) * (1.0 + 1e-9) + 1e-30);
+            }
+        }
         __syncthreads();
-        const float qq = qq_s;
+        int qw[P][4];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const int4 v = reinterpret_cast<const int4*>(qc + p * 256)[hl];
+            qw[p][0] = v.x; qw[p][1] = v.y; qw[p][2] = v.z; qw[p][3] = v.w;
+        }
+        const float sq = qscale_s, eq = qerr_s;
+        const float sq2qq = sq * sq * (float)qq_s;
         const int8_t* X8 = idx.d_X8 + r0 * M;
         float hmin = __int_as_float(0x7f800000);
         // ---- phase 1: bounds from the int8 codes
@@ -1041,25 +1066,23 @@ __global__ void __launch_bounds__(SCAN_THREADS, 4) scan_q8_kernel(RoundState s, 
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                float dot = 0.f;
+                int dot = 0;
 #pragma unroll
                 for (int p = 0; p < P; ++p) {
-                    const int ws[4] = {w[u][p].x, w[u][p].y, w[u][p].z, w[u][p].w};
-#pragma unroll
-                    for (int c = 0; c < 4; ++c)
-#pragma unroll
-                        for (int b = 0; b < 4; ++b)
-                            dot = fmaf((float)(int8_t)(ws[c] >> (8 * b)), qv[p][c * 4 + b], dot);
+                    dot = __dp4a(w[u][p].x, qw[p][0], dot);
+                    dot = __dp4a(w[u][p].y, qw[p][1], dot);
+                    dot = __dp4a(w[u][p].z, qw[p][2], dot);
+                    dot = __dp4a(w[u][p].w, qw[p][3], dot);
                 }
 #pragma unroll
                 for (int o = 8; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
                 const int r = b0 + slot + 16 * u;
                 if (r < nrows) {
-                    const float sc = __ldg(idx.d_scale + r0 + r);
-                    const float s2xx = sc * sc * (float)__ldg(idx.d_xx + r0 + r);
-                    const float e = __ldg(idx.d_qerr + r0 + r);
-                    const float d2 = qq + s2xx - 2.f * sc * dot;
-                    const float tol = 1e-5f * (qq + s2xx);
+                    const float sx = __ldg(idx.d_scale + r0 + r);
+                    const float sx2xx = sx * sx * (float)__ldg(idx.d_xx + r0 + r);
+                    const float e = __ldg(idx.d_qerr + r0 + r) + eq;
+                    const float d2 = sx2xx + sq2qq - 2.f * (sx * sq) * (float)dot;
+                    const float tol = 1e-5f * (sx2xx + sq2qq);
                     const float lo = (sqrtf(fmaxf(d2 - tol, 0.f)) - e) * (1.f - 1e-6f);
                     const float hi = (sqrtf(fmaxf(d2 + tol, 0.f)) + e) * (1.f + 1e-6f);
                     hmin = fminf(hmin, hi);
