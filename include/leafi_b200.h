@@ -53,9 +53,8 @@ typedef struct lf_index {
     const int32_t* d_leaf_filter;/* [n_leaves] filter slot or -1 (may be NULL) */
     /* optional int8 shadow of X for the bounded scan (lf_quantize_rows); all NULL = unused */
     const int8_t* d_X8;          /* [n_series][m] round(x / scale) */
-    const float* d_scale;        /* [n_series] per-row scale = max|x| / 127 */
-    const int32_t* d_xx;         /* [n_series] sum of squared int8 codes */
-    const float* d_qerr;         /* [n_series] ||scale * code - x||_2, rounded up */
+    const float* d_qmeta;        /* [n_series][4] per row: scale = max|x| / 127, sum of squared
+                                    codes (exact in fp32), ||scale * code - x||_2 rounded up, 0 */
 } lf_index;
 
 /* Options of one batched search (tree.py:220-229 search_engine keyword args). */
@@ -237,10 +236,12 @@ int lf_paa_device(const float* d_values, int64_t n, int32_t m, int32_t n_seg, do
 
 /* Build the int8 shadow used by the bounded leaf scan: per row r, scale_r =
  * max|x| / 127, code = rint(x / scale_r), xx_r = sum code^2, and the exact
- * quantisation error norm qerr_r = ||scale_r * code - x||_2 (fp64, rounded up).
- * Then for any query, | ||x - q|| - ||scale*code - q|| | <= qerr_r. */
-int lf_quantize_rows(const float* d_X, int64_t n, int32_t m, int8_t* d_X8, float* d_scale,
-                     int32_t* d_xx, float* d_qerr, void* stream);
+ * quantisation error norm qerr_r = ||scale_r * code - x||_2 (fp64, rounded up),
+ * packed as d_qmeta[r] = {scale_r, xx_r, qerr_r, 0} (16 B per row, so one bulk
+ * copy stages a block of rows).  Then for any query,
+ * | ||x - q|| - ||scale*code - q|| | <= qerr_r. */
+int lf_quantize_rows(const float* d_X, int64_t n, int32_t m, int8_t* d_X8, float* d_qmeta,
+                     void* stream);
 
 /* Segment means for host rows (summarize_matrix, summarize.py:52-56), numpy order. */
 int lf_paa_host(const float* h_values, int64_t n, int32_t m, int32_t n_seg, double* h_out,

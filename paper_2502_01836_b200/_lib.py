@@ -36,9 +36,7 @@ class LfIndex(C.Structure):
         ("d_env_max", C.c_void_p),
         ("d_leaf_filter", C.c_void_p),
         ("d_X8", C.c_void_p),
-        ("d_scale", C.c_void_p),
-        ("d_xx", C.c_void_p),
-        ("d_qerr", C.c_void_p),
+        ("d_qmeta", C.c_void_p),
     ]
 
 
@@ -104,7 +102,7 @@ SIGNATURES = {
     "lf_paa_host": (C.c_int, [_P, _I64, _I32, _I32, _P, _I32]),
     "lf_tree_build_from_summaries": (_P, [_P, _I64, _I32, _I64]),
     "lf_paa_device": (C.c_int, [_P, _I64, _I32, _I32, _P, _P]),
-    "lf_quantize_rows": (C.c_int, [_P, _I64, _I32, _P, _P, _P, _P, _P]),
+    "lf_quantize_rows": (C.c_int, [_P, _I64, _I32, _P, _P, _P]),
 }
 
 _lib = None

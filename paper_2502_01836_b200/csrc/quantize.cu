@@ -11,7 +11,7 @@
 namespace lf {
 
 __global__ void quantize_kernel(const float* __restrict__ X, int64_t n, int m, int8_t* __restrict__ X8,
-                                float* __restrict__ scale, int32_t* __restrict__ xx, float* __restrict__ qerr) {
+                                float4* __restrict__ meta) {
     const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (r >= n) return;
@@ -37,21 +37,18 @@ __global__ void quantize_kernel(const float* __restrict__ X, int64_t n, int m, i
         sq += __shfl_xor_sync(0xffffffffu, sq, o);
         err += __shfl_xor_sync(0xffffffffu, err, o);
     }
-    if (lane == 0) {
-        scale[r] = s;
-        xx[r] = sq;
-        qerr[r] = __double2float_ru(sqrt(err) * (1.0 + 1e-9) + 1e-30);
-    }
+    if (lane == 0)    // sq <= 512 * 127^2 < 2^24: exact in fp32
+        meta[r] = make_float4(s, (float)sq, __double2float_ru(sqrt(err) * (1.0 + 1e-9) + 1e-30), 0.f);
 }
 
 }  // namespace lf
 
-extern "C" int lf_quantize_rows(const float* d_X, int64_t n, int32_t m, int8_t* d_X8, float* d_scale,
-                                int32_t* d_xx, float* d_qerr, void* stream) {
+extern "C" int lf_quantize_rows(const float* d_X, int64_t n, int32_t m, int8_t* d_X8, float* d_qmeta,
+                                void* stream) {
     LF_REQUIRE(n >= 0 && m >= 1, "bad sizes");
     if (n == 0) return LF_OK;
-    lf::quantize_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, lf::as_stream(stream)>>>(d_X, n, m, d_X8, d_scale,
-                                                                                           d_xx, d_qerr);
+    lf::quantize_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, lf::as_stream(stream)>>>(
+        d_X, n, m, d_X8, reinterpret_cast<float4*>(d_qmeta));
     LF_CUDA(cudaGetLastError());
     return LF_OK;
 }

@@ -966,158 +966,264 @@ __global__ void __launch_bounds__(SCAN_THREADS, 4) scan_ea3_kernel(RoundState s,
     }
 }
 
+// ------------------------------------------------------------ q8 scan ----
 // Bounded scan over the int8 shadow (lf_quantize_rows): 1/4 of the bytes of
 // every row decide whether the exact fp32 row must be read at all.
-//   phase 1: the query is quantised the same way (codes cq, scale sq, error
-//            eq = ||sq cq - q||, exact fp64, rounded up); half a warp per row,
-//            8 rows in flight, D = cx . cq with DP4A (exact int32);
-//            ||x^ - q^||^2 = sx^2 xx + sq^2 qq - 2 sx sq D (fp32, rounding
-//            bounded by tol = 1e-5 (sx^2 xx + sq^2 qq)), and by the triangle
-//            inequality the true distance lies in
-//            [sqrt(.. - tol) - ex - eq, sqrt(.. + tol) + ex + eq] (widened 1e-6);
-//   phase 2: for k = 1 the task's best row is within min_r hi_r, so a row whose
-//            lo exceeds min(bsf, min hi) can never be the answer; every other
-//            row (the few that remain) is re-read whole and summed EXACTLY in
-//            fp64 -- kept distances are exact, dropped rows provably worse.
+//
+// Pipeline (one CTA = 1 producer warp + 8 consumer warps, 2 CTAs per SM,
+// persistent over the round's task list):
+//   producer : one elected lane streams each task's rows in stages of 64 rows
+//              (64 x m int8 codes + 64 x 16 B row metadata) into a ring of
+//              shared-memory stages with cp.async.bulk (TMA bulk copies,
+//              L2 evict-first), completion signalled on a full mbarrier;
+//              it runs ahead across task boundaries, so HBM streaming never
+//              waits for a task's serial tail;
+//   consumers: half a warp per row, 16 codes per lane from shared memory,
+//              D = cx . cq with DP4A (exact int32; the query codes cq were
+//              quantised once per batch by quantize_queries_kernel);
+//              ||x^ - q^||^2 = sx^2 xx + sq^2 qq - 2 sx sq D (fp32, rounding
+//              bounded by tol = 1e-5 (sx^2 xx + sq^2 qq)), and by the triangle
+//              inequality the true distance lies in
+//              [sqrt(.. - tol) - ex - eq, sqrt(.. + tol) + ex + eq] (widened 1e-6);
+//              the stage is released to the producer with one arrive per warp.
+//   tail     : for k = 1 the task's best row is within min_r hi_r, so a row whose
+//              lo exceeds min(bsf, min hi) can never be the answer; every other
+//              row (the few that remain) is re-read whole from HBM and summed
+//              EXACTLY in fp64 -- kept distances are exact, dropped rows
+//              provably worse.
+constexpr int Q8_ROWS = 64;
+constexpr int Q8_CONS_WARPS = 8;
+constexpr int Q8_CONS = 32 * Q8_CONS_WARPS;
+constexpr int Q8_THREADS = Q8_CONS + 32;
+
 template <int NCH>
-__global__ void __launch_bounds__(SCAN_THREADS, 4) scan_q8_kernel(RoundState s, lf_index idx,
-                                                                  const float* __restrict__ queries) {
-    constexpr int M = NCH * 64;
-    constexpr int P = (M + 255) / 256;            // 256-code passes per row (16 codes per lane)
-    constexpr int U = 8;
-    __shared__ float qf[M];
-    __shared__ __align__(16) int8_t qc[P * 256];
-    __shared__ float lo_s[CH];
-    __shared__ double sd[CH];
-    __shared__ long long sid[CH];
-    __shared__ int surv[CH];
-    __shared__ int n_surv;
-    __shared__ unsigned int hi_bits;
-    __shared__ float qscale_s, qerr_s;
-    __shared__ int qq_s;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int hl = lane & 15;
-    const int slot = warp * 2 + (lane >> 4);
+struct Q8Cfg {
+    static constexpr int M = NCH * 64;
+    static constexpr int P = (M + 255) / 256;              // 256-code passes per row (16 codes per lane)
+    static constexpr int CODE_BYTES = Q8_ROWS * M;
+    static constexpr int STAGE_BYTES = CODE_BYTES + Q8_ROWS * 16;
+    static constexpr int STAGES = (81920 / CODE_BYTES) < 2 ? 2 : ((81920 / CODE_BYTES) > 8 ? 8 : 81920 / CODE_BYTES);
+    static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+    static constexpr int LO_OFF = BAR_OFF + 2 * STAGES * 8;
+    static constexpr int SR_OFF = LO_OFF + CH * 4;
+    static constexpr int SD_OFF = SR_OFF + CH * 4;
+    static constexpr int MISC_OFF = SD_OFF + CH * 8;
+    static constexpr int SMEM = MISC_OFF + 16;
+};
+
+__device__ __forceinline__ uint32_t q8_su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void q8_bar_init(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(q8_su32(b)), "r"(n));
+}
+__device__ __forceinline__ void q8_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(q8_su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void q8_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(q8_su32(b)) : "memory");
+}
+__device__ __forceinline__ void q8_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "LF_Q8W_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra LF_Q8W_%=;\n}" ::"r"(q8_su32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void q8_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            q8_su32(dst)),
+        "l"(src), "r"(bytes), "r"(q8_su32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void q8_cons_sync() { asm volatile("bar.sync 1, %0;" ::"n"(Q8_CONS) : "memory"); }
+
+// Query codes, quantised once per batch exactly like the rows (quantize.cu):
+// codes [Q][MP] (zero-padded to MP = 256-multiple), meta [Q] = {scale, qq, err, 0}.
+__global__ void quantize_queries_kernel(const float* __restrict__ queries, int64_t Q, int M, int MP,
+                                        int8_t* __restrict__ qc, float4* __restrict__ qm) {
+    const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (q >= Q) return;
+    const float* x = queries + q * M;
+    float mx = 0.f;
+    for (int i = lane; i < M; i += 32) mx = fmaxf(mx, fabsf(x[i]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const float sq = mx > 0.f ? mx / 127.f : 1.f;
+    int qq = 0;
+    double err = 0.0;
+    for (int i = lane; i < MP; i += 32) {
+        int c = 0;
+        if (i < M) {
+            c = (int)fminf(fmaxf(rintf(x[i] / sq), -127.f), 127.f);
+            const double e = (double)sq * (double)c - (double)x[i];
+            err = __fma_rn(e, e, err);
+        }
+        qc[q * MP + i] = (int8_t)c;
+        qq += c * c;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        qq += __shfl_xor_sync(0xffffffffu, qq, o);
+        err += __shfl_xor_sync(0xffffffffu, err, o);
+    }
+    if (lane == 0) qm[q] = make_float4(sq, (float)qq, __double2float_ru(sqrt(err) * (1.0 + 1e-9) + 1e-30), 0.f);
+}
+
+template <int NCH>
+__global__ void __launch_bounds__(Q8_THREADS, 2) scan_q8_kernel(RoundState s, lf_index idx,
+                                                                const float* __restrict__ queries,
+                                                                const int8_t* __restrict__ qcodes,
+                                                                const float4* __restrict__ qmeta) {
+    using Cfg = Q8Cfg<NCH>;
+    constexpr int M = Cfg::M, P = Cfg::P, S = Cfg::STAGES;
+    extern __shared__ __align__(128) unsigned char q8_smem[];
+    unsigned char* stages = q8_smem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(q8_smem + Cfg::BAR_OFF);
+    uint64_t* empty = full + S;
+    float* lo_s = reinterpret_cast<float*>(q8_smem + Cfg::LO_OFF);
+    int* surv_r = reinterpret_cast<int*>(q8_smem + Cfg::SR_OFF);
+    double* surv_d = reinterpret_cast<double*>(q8_smem + Cfg::SD_OFF);
+    unsigned int* hi_bits = reinterpret_cast<unsigned int*>(q8_smem + Cfg::MISC_OFF);   // [2], by task parity
+    int* n_surv = reinterpret_cast<int*>(hi_bits + 2);                                 // [2]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            q8_bar_init(&full[i], 1);
+            q8_bar_init(&empty[i], Q8_CONS_WARPS);
+        }
+        hi_bits[0] = hi_bits[1] = 0x7f800000u;
+        n_surv[0] = n_surv[1] = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
     const long long total = s.chunk_off[s.Q];
-    for (long long t = blockIdx.x; t < total; t += gridDim.x) {
-        const int4 tk = s.tasks[t];
-        const int64_t q = tk.x;
-        const int leaf = tk.y;
-        const int64_t lbeg = idx.d_leaf_ptr[leaf], lend = idx.d_leaf_ptr[leaf + 1];
-        const int64_t r0 = lbeg + (int64_t)tk.z * CH;
-        const int nrows = (int)min((int64_t)CH, lend - r0);
-        const double bsf = round_bsf(s, q);
-        const float* qrow = queries + q * M;
-        for (int i = threadIdx.x; i < M; i += SCAN_THREADS) qf[i] = qrow[i];
-        if (threadIdx.x == 0) { n_surv = 0; hi_bits = 0x7f800000u; }
-        __syncthreads();
-        if (warp == 0) {                                   // quantise the query like the rows
-            float mx = 0.f;
-            for (int i = lane; i < M; i += 32) mx = fmaxf(mx, fabsf(qf[i]));
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            const float sq = mx > 0.f ? mx / 127.f : 1.f;
-            int qq = 0;
-            double err = 0.0;
-            for (int i = lane; i < P * 256; i += 32) {
-                int c = 0;
-                if (i < M) {
-                    c = (int)fminf(fmaxf(rintf(qf[i] / sq), -127.f), 127.f);
-                    const double e = (double)sq * (double)c - (double)qf[i];
-                    err = __fma_rn(e, e, err);
+
+    if (warp == 0) {   // ---------------------------------------------- producer
+        if (lane == 0) {
+            uint64_t pol;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+            int slot = 0;
+            uint32_t ph = 0;
+            for (long long t = blockIdx.x; t < total; t += gridDim.x) {
+                const int4 tk = s.tasks[t];
+                const int64_t lend = idx.d_leaf_ptr[tk.y + 1];
+                const int64_t r0 = idx.d_leaf_ptr[tk.y] + (int64_t)tk.z * CH;
+                const int nrows = (int)min((int64_t)CH, lend - r0);
+                for (int j = 0; j < nrows; j += Q8_ROWS) {
+                    const int rows = min(Q8_ROWS, nrows - j);
+                    q8_wait(&empty[slot], ph ^ 1);
+                    unsigned char* dst = stages + slot * Cfg::STAGE_BYTES;
+                    q8_expect_tx(&full[slot], (uint32_t)(rows * (M + 16)));
+                    q8_bulk(dst, idx.d_X8 + (r0 + j) * M, (uint32_t)(rows * M), &full[slot], pol);
+                    q8_bulk(dst + Cfg::CODE_BYTES, idx.d_qmeta + (r0 + j) * 4, (uint32_t)(rows * 16), &full[slot], pol);
+                    if (++slot == S) { slot = 0; ph ^= 1; }
                 }
-                qc[i] = (int8_t)c;
-                qq += c * c;
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                qq += __shfl_xor_sync(0xffffffffu, qq, o);
-                err += __shfl_xor_sync(0xffffffffu, err, o);
-            }
-            if (lane == 0) {
-                qscale_s = sq;
-                qq_s = qq;
-                qerr_s = __double2float_ru(sqrt(err) * (1.0 + 1e-9) + 1e-30);
             }
         }
-        __syncthreads();
+        return;
+    }
+
+    // ------------------------------------------------------------ consumers
+    const int cw = warp - 1;
+    const int ctid = threadIdx.x - 32;
+    const int hl = lane & 15;
+    const int hslot = cw * 2 + (lane >> 4);        // 16 half-warps
+    int slot = 0;
+    uint32_t ph = 0;
+    int par = 0;
+    for (long long t = blockIdx.x; t < total; t += gridDim.x, par ^= 1) {
+        const int4 tk = s.tasks[t];
+        const int64_t q = tk.x;
+        const int64_t lend = idx.d_leaf_ptr[tk.y + 1];
+        const int64_t r0 = idx.d_leaf_ptr[tk.y] + (int64_t)tk.z * CH;
+        const int nrows = (int)min((int64_t)CH, lend - r0);
+        const double bsf = round_bsf(s, q);
         int qw[P][4];
 #pragma unroll
         for (int p = 0; p < P; ++p) {
-            const int4 v = reinterpret_cast<const int4*>(qc + p * 256)[hl];
+            int4 v = make_int4(0, 0, 0, 0);
+            if (p * 256 + hl * 16 < M) v = __ldg(reinterpret_cast<const int4*>(qcodes + q * (P * 256) + p * 256) + hl);
             qw[p][0] = v.x; qw[p][1] = v.y; qw[p][2] = v.z; qw[p][3] = v.w;
         }
-        const float sq = qscale_s, eq = qerr_s;
-        const float sq2qq = sq * sq * (float)qq_s;
-        const int8_t* X8 = idx.d_X8 + r0 * M;
+        const float4 qmv = __ldg(qmeta + q);
+        const float sq = qmv.x, eq = qmv.z;
+        const float sq2qq = sq * sq * qmv.y;
         float hmin = __int_as_float(0x7f800000);
-        // ---- phase 1: bounds from the int8 codes
-        for (int b0 = 0; b0 < nrows; b0 += 16 * U) {
-            int4 w[U][P];
+        // ---- bounds from the int8 codes, stage by stage
+        for (int j = 0; j < nrows; j += Q8_ROWS) {
+            const int rows = min(Q8_ROWS, nrows - j);
+            q8_wait(&full[slot], ph);
+            const unsigned char* stg = stages + slot * Cfg::STAGE_BYTES;
+            const float4* mt = reinterpret_cast<const float4*>(stg + Cfg::CODE_BYTES);
+            int dots[Q8_ROWS / 16];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int r = b0 + slot + 16 * u;
-#pragma unroll
-                for (int p = 0; p < P; ++p) {
-                    const bool ok = r < nrows && (p * 256 + hl * 16) < M;
-                    w[u][p] = ok ? __ldg(reinterpret_cast<const int4*>(X8 + (int64_t)r * M + p * 256) + hl)
-                                 : make_int4(0, 0, 0, 0);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
+            for (int u = 0; u < Q8_ROWS / 16; ++u) {
+                const int r = hslot + 16 * u;
                 int dot = 0;
 #pragma unroll
                 for (int p = 0; p < P; ++p) {
-                    dot = __dp4a(w[u][p].x, qw[p][0], dot);
-                    dot = __dp4a(w[u][p].y, qw[p][1], dot);
-                    dot = __dp4a(w[u][p].z, qw[p][2], dot);
-                    dot = __dp4a(w[u][p].w, qw[p][3], dot);
+                    if (r < rows && p * 256 + hl * 16 < M) {
+                        const int4 w = *reinterpret_cast<const int4*>(stg + r * M + p * 256 + hl * 16);
+                        dot = __dp4a(w.x, qw[p][0], dot);
+                        dot = __dp4a(w.y, qw[p][1], dot);
+                        dot = __dp4a(w.z, qw[p][2], dot);
+                        dot = __dp4a(w.w, qw[p][3], dot);
+                    }
                 }
+                dots[u] = dot;
+            }
 #pragma unroll
-                for (int o = 8; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-                const int r = b0 + slot + 16 * u;
-                if (r < nrows) {
-                    const float sx = __ldg(idx.d_scale + r0 + r);
-                    const float sx2xx = sx * sx * (float)__ldg(idx.d_xx + r0 + r);
-                    const float e = __ldg(idx.d_qerr + r0 + r) + eq;
-                    const float d2 = sx2xx + sq2qq - 2.f * (sx * sq) * (float)dot;
-                    const float tol = 1e-5f * (sx2xx + sq2qq);
-                    const float lo = (sqrtf(fmaxf(d2 - tol, 0.f)) - e) * (1.f - 1e-6f);
-                    const float hi = (sqrtf(fmaxf(d2 + tol, 0.f)) + e) * (1.f + 1e-6f);
-                    hmin = fminf(hmin, hi);
-                    if (hl == 0) lo_s[r] = lo;
+            for (int u = 0; u < Q8_ROWS / 16; ++u) {
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1) dots[u] += __shfl_xor_sync(0xffffffffu, dots[u], o);
+            }
+            if (hl == 0) {
+#pragma unroll
+                for (int u = 0; u < Q8_ROWS / 16; ++u) {
+                    const int r = hslot + 16 * u;
+                    if (r < rows) {
+                        const float4 mr = mt[r];
+                        const float sx2xx = mr.x * mr.x * mr.y;
+                        const float e = mr.z + eq;
+                        const float d2 = sx2xx + sq2qq - 2.f * (mr.x * sq) * (float)dots[u];
+                        const float tol = 1e-5f * (sx2xx + sq2qq);
+                        const float lo = (sqrtf(fmaxf(d2 - tol, 0.f)) - e) * (1.f - 1e-6f);
+                        const float hi = (sqrtf(fmaxf(d2 + tol, 0.f)) + e) * (1.f + 1e-6f);
+                        hmin = fminf(hmin, hi);
+                        lo_s[j + r] = lo;
+                    }
                 }
             }
+            __syncwarp();
+            if (lane == 0) q8_arrive(&empty[slot]);
+            if (++slot == S) { slot = 0; ph ^= 1; }
         }
         if (s.k == 1) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) hmin = fminf(hmin, __shfl_xor_sync(0xffffffffu, hmin, o));
-            if (lane == 0) atomicMin(&hi_bits, __float_as_uint(hmin));
+            if (lane == 0) atomicMin(&hi_bits[par], __float_as_uint(hmin));
         }
-        __syncthreads();
-        // ---- phase 2: survivors -> exact fp64 rows
+        q8_cons_sync();
+        // ---- survivors
         {
             double thr = bsf;
-            if (s.k == 1) thr = fmin(thr, (double)__uint_as_float(hi_bits));
+            if (s.k == 1) thr = fmin(thr, (double)__uint_as_float(hi_bits[par]));
             const float thr_f = thr < kInf ? __double2float_ru(thr) : __int_as_float(0x7f800000);
-            for (int r = threadIdx.x; r < nrows; r += SCAN_THREADS) {
-                if (lo_s[r] <= thr_f) surv[atomicAdd(&n_surv, 1)] = r;
-                else sd[r] = kInf;
-            }
+            for (int r = ctid; r < nrows; r += Q8_CONS)
+                if (lo_s[r] <= thr_f) surv_r[atomicAdd(&n_surv[par], 1)] = r;
         }
-        __syncthreads();
-        if (s.ea_count != nullptr && threadIdx.x == 0) {
-            atomicAdd(&s.ea_count[0], (unsigned long long)nrows);
-            atomicAdd(&s.ea_count[1], (unsigned long long)n_surv);
-        }
-        {
-            const int ns = n_surv;
+        q8_cons_sync();
+        const int ns = n_surv[par];
+        {   // exact fp64 direct-form distances of the survivors (series.py:142-146)
             const float* X0 = idx.d_X + r0 * M;
+            const float* qrow = queries + q * M;
             for (int b0 = 0; b0 < ns; b0 += 16) {
-                const int jj = b0 + slot;
+                const int jj = b0 + hslot;
                 const bool v = jj < ns;
-                const int r = v ? surv[jj] : 0;
+                const int r = v ? surv_r[jj] : 0;
                 float4 x[NCH];
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch)
@@ -1126,56 +1232,56 @@ __global__ void __launch_bounds__(SCAN_THREADS, 4) scan_q8_kernel(RoundState s, 
                 double acc = 0.0;
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch) {
-                    const float* qq4 = qf + ch * 64 + hl * 4;
-                    double d0 = (double)x[ch].x - (double)qq4[0], d1 = (double)x[ch].y - (double)qq4[1];
-                    double d2 = (double)x[ch].z - (double)qq4[2], d3 = (double)x[ch].w - (double)qq4[3];
+                    const float4 qv = __ldg(reinterpret_cast<const float4*>(qrow) + ch * 16 + hl);
+                    const double d0 = (double)x[ch].x - (double)qv.x, d1 = (double)x[ch].y - (double)qv.y;
+                    const double d2 = (double)x[ch].z - (double)qv.z, d3 = (double)x[ch].w - (double)qv.w;
                     acc = __fma_rn(d0, d0, acc); acc = __fma_rn(d1, d1, acc);
                     acc = __fma_rn(d2, d2, acc); acc = __fma_rn(d3, d3, acc);
                 }
 #pragma unroll
                 for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                if (v && hl == 0) sd[r] = sqrt(acc);
+                if (v && hl == 0) surv_d[jj] = sqrt(acc);
             }
         }
-        __syncthreads();
-        if (warp == 0) {
+        q8_cons_sync();
+        if (ctid == 0) {
+            if (s.ea_count != nullptr) {
+                atomicAdd(&s.ea_count[0], (unsigned long long)nrows);
+                atomicAdd(&s.ea_count[1], (unsigned long long)ns);
+            }
+            hi_bits[par] = 0x7f800000u;          // reused by the task after next
+            n_surv[par] = 0;
+        }
+        if (cw == 0) {   // per-task candidates from the survivors only
             double* cd = s.cand_d + t * s.kc;
             long long* ci = s.cand_i + t * s.kc;
-            for (int i = lane; i < nrows; i += 32) {
-                sid[i] = idx.d_row_id[r0 + i];
-                if (!(sd[i] <= bsf)) sd[i] = kInf;
-            }
-            __syncwarp();
-            if (s.kc >= nrows) {
-                for (int i = lane; i < s.kc; i += 32) {
-                    cd[i] = i < nrows ? sd[i] : kInf;
-                    ci[i] = (i < nrows && sd[i] != kInf) ? sid[i] : -1;
+            double last_d = -1.0;
+            long long last_i = -1;
+            for (int sel = 0; sel < s.kc; ++sel) {
+                double bd = kInf;
+                long long bi = LLONG_MAX;
+                for (int i = lane; i < ns; i += 32) {
+                    const double d = surv_d[i];
+                    if (!(d <= bsf)) continue;
+                    const long long id = idx.d_row_id[r0 + surv_r[i]];
+                    if (pair_less(last_d, last_i, d, id) && pair_less(d, id, bd, bi)) { bd = d; bi = id; }
                 }
-            } else {
-                for (int sel = 0; sel < s.kc; ++sel) {
-                    double bd = kInf; long long bi = LLONG_MAX; int bp = -1;
-                    for (int i = lane; i < nrows; i += 32)
-                        if (pair_less(sd[i], sid[i], bd, bi)) { bd = sd[i]; bi = sid[i]; bp = i; }
 #pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) {
-                        double od = __shfl_xor_sync(0xffffffffu, bd, o);
-                        long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                        int op = __shfl_xor_sync(0xffffffffu, bp, o);
-                        if (pair_less(od, oi, bd, bi)) { bd = od; bi = oi; bp = op; }
-                    }
-                    if (lane == 0) {
-                        cd[sel] = bd;
-                        ci[sel] = (bd == kInf) ? -1 : bi;
-                        if (bp >= 0) { sd[bp] = kInf; sid[bp] = LLONG_MAX; }
-                    }
-                    __syncwarp();
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+                    const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                    if (pair_less(od, oi, bd, bi)) { bd = od; bi = oi; }
                 }
+                if (lane == 0) {
+                    cd[sel] = bd;
+                    ci[sel] = (bi == LLONG_MAX) ? -1 : bi;
+                }
+                last_d = bd;
+                last_i = bi;
             }
         }
-        __syncthreads();
     }
 }
-
 // --------------------------------------------------------------- merge ----
 // One warp per query: k smallest (d, id) among the running top-k and this
 // round's candidates (each series is scanned at most once per query, so all
@@ -1273,11 +1379,18 @@ static int scan_variant() {
 }
 
 template <int NCH>
-static cudaError_t launch_scan_ea(const RoundState& s, const lf_index& idx, const float* q, int sms,
-                                  cudaStream_t st) {
-    if (scan_variant() == 8 && idx.d_X8 != nullptr)
-        scan_q8_kernel<NCH><<<sms * 4, SCAN_THREADS, 0, st>>>(s, idx, q);
-    else if (scan_variant() == 3)
+static cudaError_t launch_scan_ea(const RoundState& s, const lf_index& idx, const float* q, const int8_t* qc8,
+                                  const float4* qm8, int sms, cudaStream_t st) {
+    if (qc8 != nullptr) {
+        static bool attr = false;       // one instantiation per NCH
+        if (!attr) {
+            cudaError_t e = cudaFuncSetAttribute(scan_q8_kernel<NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 Q8Cfg<NCH>::SMEM);
+            if (e != cudaSuccess) return e;
+            attr = true;
+        }
+        scan_q8_kernel<NCH><<<sms * 2, Q8_THREADS, Q8Cfg<NCH>::SMEM, st>>>(s, idx, q, qc8, qm8);
+    } else if (scan_variant() == 3)
         scan_ea3_kernel<NCH><<<sms * 4, SCAN_THREADS, 0, st>>>(s, idx, q);
     else
         scan_ea2_kernel<NCH><<<sms * 3, SCAN_THREADS, 0, st>>>(s, idx, q);
@@ -1304,7 +1417,8 @@ struct lf_session {
     const float* d_q = nullptr;
     lf::RoundState s{};
     lf::Scratch qsumm, lb, lbs, order, cursor, done, topd, topi, topn, topd2, topi2, topn2, sel_leaf,
-        sel_trace, sel_pre, n_sel, chunk_off, cand_d, cand_i, task_min, n_active, tasks, ea_count;
+        sel_trace, sel_pre, n_sel, chunk_off, cand_d, cand_i, task_min, n_active, tasks, ea_count, qc8, qm8;
+    bool q8 = false;                 // int8-bounded scan (query codes quantised once in begin)
     int* h_active = nullptr;
     int round = 0;
     long long kernels = 0;
@@ -1404,6 +1518,17 @@ static int session_begin(lf_session* ss) {
     init_state_kernel<<<(unsigned)((Q + 127) / 128), 128, 0, st>>>(s);
     LF_CUDA(cudaGetLastError());
     ++ss->kernels;
+    ss->q8 = idx.d_X8 != nullptr && idx.d_qmeta != nullptr && o.early_abandon && !s.want_trace &&
+             (idx.m % 64) == 0 && idx.m <= 512 && scan_variant() == 8;
+    if (ss->q8) {
+        const int MP = (idx.m + 255) / 256 * 256;
+        LF_CUDA(ss->qc8.alloc((size_t)Q * MP, st));
+        LF_CUDA(ss->qm8.alloc(sizeof(float4) * Q, st));
+        quantize_queries_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(
+            ss->d_q, Q, idx.m, MP, ss->qc8.as<int8_t>(), ss->qm8.as<float4>());
+        LF_CUDA(cudaGetLastError());
+        ++ss->kernels;
+    }
     if (ss->prof) LF_CUDA(cudaEventRecord(ss->ev[1], st));
     return LF_OK;
 }
@@ -1439,15 +1564,17 @@ static int session_round(lf_session* ss, const double* d_bound, double* d_bsf_ou
     const bool ea = o.early_abandon && !s.want_trace && (idx.m % 64) == 0 && idx.m <= 512 && scan_variant() != 0;
     if (ea) {
         const int g3 = sm_count();                // launch_scan_ea sizes the grid to the variant's residency
+        const int8_t* qc8 = ss->q8 ? ss->qc8.as<int8_t>() : nullptr;
+        const float4* qm8 = ss->q8 ? ss->qm8.as<float4>() : nullptr;
         switch (idx.m / 64) {
-            case 1: ce = launch_scan_ea<1>(s, idx, ss->d_q, g3, st); break;
-            case 2: ce = launch_scan_ea<2>(s, idx, ss->d_q, g3, st); break;
-            case 3: ce = launch_scan_ea<3>(s, idx, ss->d_q, g3, st); break;
-            case 4: ce = launch_scan_ea<4>(s, idx, ss->d_q, g3, st); break;
-            case 5: ce = launch_scan_ea<5>(s, idx, ss->d_q, g3, st); break;
-            case 6: ce = launch_scan_ea<6>(s, idx, ss->d_q, g3, st); break;
-            case 7: ce = launch_scan_ea<7>(s, idx, ss->d_q, g3, st); break;
-            default: ce = launch_scan_ea<8>(s, idx, ss->d_q, g3, st); break;
+            case 1: ce = launch_scan_ea<1>(s, idx, ss->d_q, qc8, qm8, g3, st); break;
+            case 2: ce = launch_scan_ea<2>(s, idx, ss->d_q, qc8, qm8, g3, st); break;
+            case 3: ce = launch_scan_ea<3>(s, idx, ss->d_q, qc8, qm8, g3, st); break;
+            case 4: ce = launch_scan_ea<4>(s, idx, ss->d_q, qc8, qm8, g3, st); break;
+            case 5: ce = launch_scan_ea<5>(s, idx, ss->d_q, qc8, qm8, g3, st); break;
+            case 6: ce = launch_scan_ea<6>(s, idx, ss->d_q, qc8, qm8, g3, st); break;
+            case 7: ce = launch_scan_ea<7>(s, idx, ss->d_q, qc8, qm8, g3, st); break;
+            default: ce = launch_scan_ea<8>(s, idx, ss->d_q, qc8, qm8, g3, st); break;
         }
     } else if ((idx.m & 3) != 0 || m4 <= 32) ce = launch_scan<1>(s, idx, ss->d_q, grid, st);
     else if (m4 <= 64) ce = launch_scan<2>(s, idx, ss->d_q, grid, st);

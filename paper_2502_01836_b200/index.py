@@ -299,16 +299,13 @@ class DeviceIndex:
             self.env_min = torch.from_numpy(np.ascontiguousarray(t.env_min.T)).to(dev)
             self.env_max = torch.from_numpy(np.ascontiguousarray(t.env_max.T)).to(dev)
             # int8 shadow for the bounded scan (scan_q8_kernel), when the layout allows it
-            self.X8 = self.scale = self.xx = self.qerr = None
+            self.X8 = self.qmeta = None
             n_rows, m = int(self.X.shape[0]), int(self.X.shape[1])
             if m % 64 == 0 and m <= 512 and n_rows:
                 self.X8 = torch.empty((n_rows, m), dtype=torch.int8, device=dev)
-                self.scale = torch.empty(n_rows, dtype=torch.float32, device=dev)
-                self.xx = torch.empty(n_rows, dtype=torch.int32, device=dev)
-                self.qerr = torch.empty(n_rows, dtype=torch.float32, device=dev)
+                self.qmeta = torch.empty((n_rows, 4), dtype=torch.float32, device=dev)
                 _lib.check(_lib.lib().lf_quantize_rows(self.X.data_ptr(), n_rows, m, self.X8.data_ptr(),
-                                                       self.scale.data_ptr(), self.xx.data_ptr(),
-                                                       self.qerr.data_ptr(), _lib.stream_ptr()))
+                                                       self.qmeta.data_ptr(), _lib.stream_ptr()))
         self.leaf_ids = leaf_ids
         self.leaf_ptr_host = leaf_ptr
         self.slot_of_leaf = {int(l): j for j, l in enumerate(leaf_ids)}
@@ -338,6 +335,5 @@ class DeviceIndex:
         s.d_env_max = self.env_max.data_ptr()
         s.d_leaf_filter = None if leaf_filter is None else leaf_filter.data_ptr()
         if self.X8 is not None:
-            s.d_X8, s.d_scale = self.X8.data_ptr(), self.scale.data_ptr()
-            s.d_xx, s.d_qerr = self.xx.data_ptr(), self.qerr.data_ptr()
+            s.d_X8, s.d_qmeta = self.X8.data_ptr(), self.qmeta.data_ptr()
         return s

@@ -346,3 +346,29 @@ def test_scan_variants_agree(variant, k, monkeypatch):
         o = lo.search(ot, Q[i], k)
         assert seq.ids[i].tolist() == [a for a, _ in o.results]
         assert seq.stats[i].tolist() == [o.stats[s_] for s_ in lo.STAT_KEYS]
+
+
+@pytest.mark.parametrize("m", [64, 192, 256, 320, 512])
+@pytest.mark.parametrize("k", [1, 3])
+def test_q8_pipeline_exact(m, k, monkeypatch):
+    """The TMA-pipelined int8-bounded scan (several stage counts / passes per row)
+    equals the full fp64 scan: ids, distances and counters.  The collection holds
+    exact duplicates (ties broken by id), an all-zero row (scale fallback) and
+    queries that ARE collection rows (distance exactly 0)."""
+    from paper_2502_01836_b200 import build_index, search_batch
+
+    data = lo.randwalk(9000, m, 40 + m)
+    data[100:110] = data[7]                       # 11 identical rows
+    data[200] = 0.0
+    t = build_index(data, 700)
+    Q = np.concatenate([lo.noisy_queries(data, 10, nz, 90 + int(10 * nz)) for nz in (0.1, 0.3)]
+                       + [data[[7, 200, 4321]].astype(np.float64)])
+    monkeypatch.setenv("LF_SCAN_VARIANT", "full")
+    ref = search_batch(t, Q, k)
+    monkeypatch.setenv("LF_SCAN_VARIANT", "q8")
+    got = search_batch(t, Q, k)
+    np.testing.assert_array_equal(got.ids, ref.ids)
+    np.testing.assert_allclose(got.dists, ref.dists, rtol=1e-14)
+    np.testing.assert_array_equal(got.stats, ref.stats)
+    assert got.ids[-3, 0] == 7 and got.dists[-3, 0] == 0.0
+    assert got.ids[-1, 0] == 4321 and got.dists[-1, 0] == 0.0
