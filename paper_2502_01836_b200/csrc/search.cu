@@ -973,19 +973,24 @@ __global__ void __launch_bounds__(SCAN_THREADS, 4) scan_ea3_kernel(RoundState s,
 // Pipeline (one CTA = 1 producer warp + 8 consumer warps, 2 CTAs per SM,
 // persistent over the round's task list):
 //   producer : one elected lane streams each task's rows in stages of 64 rows
-//              (64 x m int8 codes + 64 x 16 B row metadata) into a ring of
-//              shared-memory stages with cp.async.bulk (TMA bulk copies,
-//              L2 evict-first), completion signalled on a full mbarrier;
-//              it runs ahead across task boundaries, so HBM streaming never
-//              waits for a task's serial tail;
-//   consumers: half a warp per row, 16 codes per lane from shared memory,
-//              D = cx . cq with DP4A (exact int32; the query codes cq were
-//              quantised once per batch by quantize_queries_kernel);
+//              (64 x m int8 codes + 64 x 16 B row metadata; the first stage of
+//              a task also carries the query's codes and a task header) into a
+//              ring of shared-memory stages with cp.async.bulk (TMA bulk
+//              copies, L2 evict-first), completion on a full mbarrier.  It runs
+//              ahead across task boundaries, so HBM streaming never waits for a
+//              task's serial tail, and consumers never wait on a global load to
+//              learn what they are scanning.
+//   consumers: a warp takes 8 rows of a stage, half a warp per 4 rows, 16 codes
+//              per lane per 256-code pass: D = cx . cq with DP4A (exact int32;
+//              the query codes cq were quantised once per batch by
+//              quantize_queries_kernel).  A transposing butterfly (5 shuffles
+//              for 4 rows) leaves every lane with one full row dot, so the bound
+//              arithmetic runs once per row on all lanes instead of serially:
 //              ||x^ - q^||^2 = sx^2 xx + sq^2 qq - 2 sx sq D (fp32, rounding
 //              bounded by tol = 1e-5 (sx^2 xx + sq^2 qq)), and by the triangle
 //              inequality the true distance lies in
-//              [sqrt(.. - tol) - ex - eq, sqrt(.. + tol) + ex + eq] (widened 1e-6);
-//              the stage is released to the producer with one arrive per warp.
+//              [sqrt(.. - tol) - ex - eq, sqrt(.. + tol) + ex + eq] (widened 1e-6).
+//              One arrive per warp releases the stage to the producer.
 //   tail     : for k = 1 the task's best row is within min_r hi_r, so a row whose
 //              lo exceeds min(bsf, min hi) can never be the answer; every other
 //              row (the few that remain) is re-read whole from HBM and summed
@@ -995,13 +1000,18 @@ constexpr int Q8_ROWS = 64;
 constexpr int Q8_CONS_WARPS = 8;
 constexpr int Q8_CONS = 32 * Q8_CONS_WARPS;
 constexpr int Q8_THREADS = Q8_CONS + 32;
+static_assert(Q8_ROWS == 8 * Q8_CONS_WARPS, "8 rows per consumer warp per stage");
 
 template <int NCH>
 struct Q8Cfg {
     static constexpr int M = NCH * 64;
     static constexpr int P = (M + 255) / 256;              // 256-code passes per row (16 codes per lane)
     static constexpr int CODE_BYTES = Q8_ROWS * M;
-    static constexpr int STAGE_BYTES = CODE_BYTES + Q8_ROWS * 16;
+    static constexpr int META_OFF = CODE_BYTES;             // 64 x float4 row metadata
+    static constexpr int QC_OFF = META_OFF + Q8_ROWS * 16;  // query codes (first stage of a task)
+    static constexpr int QM_OFF = QC_OFF + P * 256;         // query metadata float4
+    static constexpr int HDR_OFF = QM_OFF + 16;             // {r0 (i64), q (i32), nrows (i32)}
+    static constexpr int STAGE_BYTES = (HDR_OFF + 16 + 127) / 128 * 128;
     static constexpr int STAGES = (81920 / CODE_BYTES) < 2 ? 2 : ((81920 / CODE_BYTES) > 8 ? 8 : 81920 / CODE_BYTES);
     static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
     static constexpr int LO_OFF = BAR_OFF + 2 * STAGES * 8;
@@ -1107,8 +1117,11 @@ __global__ void __launch_bounds__(Q8_THREADS, 2) scan_q8_kernel(RoundState s, lf
             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
             int slot = 0;
             uint32_t ph = 0;
-            for (long long t = blockIdx.x; t < total; t += gridDim.x) {
-                const int4 tk = s.tasks[t];
+            long long t = blockIdx.x;
+            int4 tk = t < total ? s.tasks[t] : make_int4(0, 0, 0, 0);
+            for (; t < total; t += gridDim.x) {
+                const long long tn = t + gridDim.x;
+                const int4 tk_next = tn < total ? s.tasks[tn] : make_int4(0, 0, 0, 0);   // prefetch
                 const int64_t lend = idx.d_leaf_ptr[tk.y + 1];
                 const int64_t r0 = idx.d_leaf_ptr[tk.y] + (int64_t)tk.z * CH;
                 const int nrows = (int)min((int64_t)CH, lend - r0);
@@ -1116,11 +1129,22 @@ __global__ void __launch_bounds__(Q8_THREADS, 2) scan_q8_kernel(RoundState s, lf
                     const int rows = min(Q8_ROWS, nrows - j);
                     q8_wait(&empty[slot], ph ^ 1);
                     unsigned char* dst = stages + slot * Cfg::STAGE_BYTES;
-                    q8_expect_tx(&full[slot], (uint32_t)(rows * (M + 16)));
+                    uint32_t bytes = (uint32_t)(rows * (M + 16));
+                    if (j == 0) {
+                        *reinterpret_cast<long long*>(dst + Cfg::HDR_OFF) = r0;
+                        *reinterpret_cast<int2*>(dst + Cfg::HDR_OFF + 8) = make_int2(tk.x, nrows);
+                        bytes += P * 256 + 16;
+                    }
+                    q8_expect_tx(&full[slot], bytes);    // release: orders the header stores
                     q8_bulk(dst, idx.d_X8 + (r0 + j) * M, (uint32_t)(rows * M), &full[slot], pol);
-                    q8_bulk(dst + Cfg::CODE_BYTES, idx.d_qmeta + (r0 + j) * 4, (uint32_t)(rows * 16), &full[slot], pol);
+                    q8_bulk(dst + Cfg::META_OFF, idx.d_qmeta + (r0 + j) * 4, (uint32_t)(rows * 16), &full[slot], pol);
+                    if (j == 0) {
+                        q8_bulk(dst + Cfg::QC_OFF, qcodes + (int64_t)tk.x * (P * 256), P * 256, &full[slot], pol);
+                        q8_bulk(dst + Cfg::QM_OFF, qmeta + tk.x, 16, &full[slot], pol);
+                    }
                     if (++slot == S) { slot = 0; ph ^= 1; }
                 }
+                tk = tk_next;
             }
         }
         return;
@@ -1130,38 +1154,40 @@ __global__ void __launch_bounds__(Q8_THREADS, 2) scan_q8_kernel(RoundState s, lf
     const int cw = warp - 1;
     const int ctid = threadIdx.x - 32;
     const int hl = lane & 15;
-    const int hslot = cw * 2 + (lane >> 4);        // 16 half-warps
+    const int rbase = cw * 8 + (lane >> 4) * 4;        // this half-warp's 4 rows of a stage
+    const bool b8 = (hl & 8) != 0, b4 = (hl & 4) != 0;
+    const int myrow = rbase + (b8 ? 2 : 0) + (b4 ? 1 : 0);   // row whose total this lane ends with
     int slot = 0;
     uint32_t ph = 0;
     int par = 0;
     for (long long t = blockIdx.x; t < total; t += gridDim.x, par ^= 1) {
-        const int4 tk = s.tasks[t];
-        const int64_t q = tk.x;
-        const int64_t lend = idx.d_leaf_ptr[tk.y + 1];
-        const int64_t r0 = idx.d_leaf_ptr[tk.y] + (int64_t)tk.z * CH;
-        const int nrows = (int)min((int64_t)CH, lend - r0);
-        const double bsf = round_bsf(s, q);
+        // first stage of the task: header + query codes
+        q8_wait(&full[slot], ph);
+        const unsigned char* st0 = stages + slot * Cfg::STAGE_BYTES;
+        const int64_t r0 = *reinterpret_cast<const long long*>(st0 + Cfg::HDR_OFF);
+        const int2 hq = *reinterpret_cast<const int2*>(st0 + Cfg::HDR_OFF + 8);
+        const int64_t q = hq.x;
+        const int nrows = hq.y;
+        const double bsf = round_bsf(s, q);                  // consumed in the tail only
         int qw[P][4];
 #pragma unroll
         for (int p = 0; p < P; ++p) {
-            int4 v = make_int4(0, 0, 0, 0);
-            if (p * 256 + hl * 16 < M) v = __ldg(reinterpret_cast<const int4*>(qcodes + q * (P * 256) + p * 256) + hl);
+            const int4 v = *reinterpret_cast<const int4*>(st0 + Cfg::QC_OFF + p * 256 + hl * 16);
             qw[p][0] = v.x; qw[p][1] = v.y; qw[p][2] = v.z; qw[p][3] = v.w;
         }
-        const float4 qmv = __ldg(qmeta + q);
+        const float4 qmv = *reinterpret_cast<const float4*>(st0 + Cfg::QM_OFF);
         const float sq = qmv.x, eq = qmv.z;
         const float sq2qq = sq * sq * qmv.y;
         float hmin = __int_as_float(0x7f800000);
         // ---- bounds from the int8 codes, stage by stage
         for (int j = 0; j < nrows; j += Q8_ROWS) {
+            if (j > 0) q8_wait(&full[slot], ph);
             const int rows = min(Q8_ROWS, nrows - j);
-            q8_wait(&full[slot], ph);
             const unsigned char* stg = stages + slot * Cfg::STAGE_BYTES;
-            const float4* mt = reinterpret_cast<const float4*>(stg + Cfg::CODE_BYTES);
-            int dots[Q8_ROWS / 16];
+            int d[4];
 #pragma unroll
-            for (int u = 0; u < Q8_ROWS / 16; ++u) {
-                const int r = hslot + 16 * u;
+            for (int u = 0; u < 4; ++u) {
+                const int r = rbase + u;
                 int dot = 0;
 #pragma unroll
                 for (int p = 0; p < P; ++p) {
@@ -1173,29 +1199,29 @@ __global__ void __launch_bounds__(Q8_THREADS, 2) scan_q8_kernel(RoundState s, lf
                         dot = __dp4a(w.w, qw[p][3], dot);
                     }
                 }
-                dots[u] = dot;
+                d[u] = dot;
             }
-#pragma unroll
-            for (int u = 0; u < Q8_ROWS / 16; ++u) {
-#pragma unroll
-                for (int o = 8; o > 0; o >>= 1) dots[u] += __shfl_xor_sync(0xffffffffu, dots[u], o);
+            // transposing butterfly over the 16 lanes of the half: 4 row partials -> 1 row total
+            {
+                const int s0 = b8 ? d[0] : d[2], s1 = b8 ? d[1] : d[3];
+                const int k0 = b8 ? d[2] : d[0], k1 = b8 ? d[3] : d[1];
+                const int e0 = k0 + __shfl_xor_sync(0xffffffffu, s0, 8);
+                const int e1 = k1 + __shfl_xor_sync(0xffffffffu, s1, 8);
+                int v = (b4 ? e1 : e0) + __shfl_xor_sync(0xffffffffu, b4 ? e0 : e1, 4);
+                v += __shfl_xor_sync(0xffffffffu, v, 2);
+                v += __shfl_xor_sync(0xffffffffu, v, 1);
+                d[0] = v;
             }
-            if (hl == 0) {
-#pragma unroll
-                for (int u = 0; u < Q8_ROWS / 16; ++u) {
-                    const int r = hslot + 16 * u;
-                    if (r < rows) {
-                        const float4 mr = mt[r];
-                        const float sx2xx = mr.x * mr.x * mr.y;
-                        const float e = mr.z + eq;
-                        const float d2 = sx2xx + sq2qq - 2.f * (mr.x * sq) * (float)dots[u];
-                        const float tol = 1e-5f * (sx2xx + sq2qq);
-                        const float lo = (sqrtf(fmaxf(d2 - tol, 0.f)) - e) * (1.f - 1e-6f);
-                        const float hi = (sqrtf(fmaxf(d2 + tol, 0.f)) + e) * (1.f + 1e-6f);
-                        hmin = fminf(hmin, hi);
-                        lo_s[j + r] = lo;
-                    }
-                }
+            if (myrow < rows) {
+                const float4 mr = *reinterpret_cast<const float4*>(stg + Cfg::META_OFF + myrow * 16);
+                const float sx2xx = mr.x * mr.x * mr.y;
+                const float e = mr.z + eq;
+                const float d2 = sx2xx + sq2qq - 2.f * (mr.x * sq) * (float)d[0];
+                const float tol = 1e-5f * (sx2xx + sq2qq);
+                const float lo = (sqrtf(fmaxf(d2 - tol, 0.f)) - e) * (1.f - 1e-6f);
+                const float hi = (sqrtf(fmaxf(d2 + tol, 0.f)) + e) * (1.f + 1e-6f);
+                hmin = fminf(hmin, hi);
+                if ((hl & 3) == 0) lo_s[j + myrow] = lo;
             }
             __syncwarp();
             if (lane == 0) q8_arrive(&empty[slot]);
@@ -1220,6 +1246,7 @@ __global__ void __launch_bounds__(Q8_THREADS, 2) scan_q8_kernel(RoundState s, lf
         {   // exact fp64 direct-form distances of the survivors (series.py:142-146)
             const float* X0 = idx.d_X + r0 * M;
             const float* qrow = queries + q * M;
+            const int hslot = cw * 2 + (lane >> 4);
             for (int b0 = 0; b0 < ns; b0 += 16) {
                 const int jj = b0 + hslot;
                 const bool v = jj < ns;
@@ -1261,10 +1288,10 @@ __global__ void __launch_bounds__(Q8_THREADS, 2) scan_q8_kernel(RoundState s, lf
                 double bd = kInf;
                 long long bi = LLONG_MAX;
                 for (int i = lane; i < ns; i += 32) {
-                    const double d = surv_d[i];
-                    if (!(d <= bsf)) continue;
+                    const double dd = surv_d[i];
+                    if (!(dd <= bsf)) continue;
                     const long long id = idx.d_row_id[r0 + surv_r[i]];
-                    if (pair_less(last_d, last_i, d, id) && pair_less(d, id, bd, bi)) { bd = d; bi = id; }
+                    if (pair_less(last_d, last_i, dd, id) && pair_less(dd, id, bd, bi)) { bd = dd; bi = id; }
                 }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {

@@ -1,18 +1,23 @@
 #!/bin/bash
-# ncu evidence for profiles/ (run under gpurun, ONE GPU).  Two passes over the
-# real bench workload (25M x 256, cap 10K, 1000 queries); the profiling range is
-# the timed steps only (bench.py --ncu -> cudaProfilerStart/Stop).
-#  1) launch list: every kernel of the timed steps with its device time
+# ncu evidence for profiles/ (run under gpurun, ONE GPU).  Passes over the real
+# bench workload (25M x 256, cap 10K, 1000 queries); the profiling range is the
+# timed step only (bench.py --ncu -> cudaProfilerStart/Stop).
+#  1) launch list: every kernel of the timed step with its device time
 #     (cold-cache, serialised: compare shares, not absolutes);
-#  2) --set full on the filter kernel and the first leaf-scan rounds.
+#  2) DRAM bytes of every leaf-scan launch of the step (-> roofline.traffic);
+#  3) --set full on selected scan launches and the filter kernel.
 OUT=${OUT:-gpurun_out}
 EXTRA=${EXTRA:-}
+B="python bench.py --ncu --steps 1 --warmup 3 --no-cpu-baseline --tdg-queries 0 $EXTRA"
 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
-    --log-file $OUT/launches.csv python bench.py --ncu --steps 1 --warmup 3 --no-cpu-baseline $EXTRA \
-    > $OUT/ncu_bench.json 2> $OUT/ncu_bench.log
+    --log-file $OUT/launches.csv $B > $OUT/ncu_launches_bench.json 2> $OUT/ncu_launches.log
 echo "launch list rc=$?"
+ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+    --profile-from-start off -k regex:"${SCAN_REGEX:-scan_q8_kernel}" --csv --log-file $OUT/scan_dram.csv \
+    $B > $OUT/ncu_dram_bench.json 2> $OUT/ncu_dram.log
+echo "scan dram rc=$?"
 ncu --set full --clock-control none --import-source on --profile-from-start off \
-    -k regex:"${KREGEX:-scan_ea2_kernel|filter_tc_kernel}" -c ${KCOUNT:-5} -o $OUT/prof_full \
-    python bench.py --ncu --steps 1 --warmup 3 --no-cpu-baseline $EXTRA > $OUT/ncu_full.log 2>&1
+    -k regex:"${KREGEX:-scan_q8_kernel|filter_tc_kernel}" --launch-skip ${KSKIP:-0} -c ${KCOUNT:-6} \
+    -o $OUT/prof_full $B > $OUT/ncu_full.log 2>&1
 echo "full set rc=$?"
 ls -la $OUT
