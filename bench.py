@@ -328,7 +328,7 @@ def run_ours(args, rank, world, device):
     if args.ncu:
         torch.cuda.cudart().cudaProfilerStart()
     scan_ms, scan_launches, kernels = 0.0, 0, 0
-    ea_rows, ea_surv = 0.0, 0.0
+    ea_rows, ea_surv, refills = 0.0, 0.0, 0.0
     with ClockSampler(torch.cuda.current_device()) as clk:
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
@@ -339,6 +339,7 @@ def run_ours(args, rank, world, device):
             scan_launches += int(prof[4])
             ea_rows += prof[8]
             ea_surv += prof[9]
+            refills += prof[7]
             kernels += int(prof[5]) + 1          # + the filter-inference launch
         ev1.record(stream)
         torch.cuda.synchronize()
@@ -440,6 +441,11 @@ def run_ours(args, rank, world, device):
         "leaves_pruned_pct": 100.0 * leaves_pruned,
         "series_pruning_ratio": series_pruned,
         "per_noise": per_noise,
+        "counters_per_query": {name: {"mean": float(np.mean(chk.stats[:, j])), "max": int(np.max(chk.stats[:, j]))}
+                               for j, name in enumerate(("leaves_visited", "leaves_searched", "leaves_lb_pruned",
+                                                         "leaves_filter_pruned", "filter_inferences",
+                                                         "series_scanned"))},
+        "visit_order_refills_per_step": refills / args.steps,
         "clocks": clocks,
         "e2e": e2e,
         "gpu_launches": kernels,

@@ -85,6 +85,7 @@ typedef struct lf_search_opts {
 #define LF_PROF_ROUNDS 4         /* rounds executed */
 #define LF_PROF_KERNELS 5        /* kernels launched by the library (own kernels; CUB sort counted as 1) */
 #define LF_PROF_TOTAL_MS 6       /* whole call, first to last event */
+#define LF_PROF_REFILLS 7        /* queries whose sorted visit-order prefix was completed */
 #define LF_PROF_EA_ROWS 8        /* rows tested by the early-abandon scan */
 #define LF_PROF_EA_SURVIVORS 9   /* rows that survived the first 64-dim test */
 

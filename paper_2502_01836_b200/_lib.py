@@ -57,7 +57,7 @@ class LfSearchOpts(C.Structure):
 
 
 N_PROF = 10
-PROF_NAMES = ("bounds_ms", "plan_ms", "scan_ms", "merge_ms", "rounds", "kernels", "total_ms", "unused",
+PROF_NAMES = ("bounds_ms", "plan_ms", "scan_ms", "merge_ms", "rounds", "kernels", "total_ms", "refills",
               "ea_rows", "ea_survivors")
 
 

@@ -7,6 +7,9 @@
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 
+#include <algorithm>
+#include <climits>
+
 #include "bounds.cuh"
 #include "common.cuh"
 
@@ -84,81 +87,300 @@ __global__ void iota_rows_kernel(int* __restrict__ v, int64_t Q, int n, int* __r
     if (t <= Q) offs[t] = (int)(t * n);
 }
 
-// Fused K1 + K2 for trees of up to 8192 nodes: one CTA per query computes every
-// node's search bound (lb_kernel<0> formula) straight into registers and sorts
-// the (lb, node id) pairs with a stable block radix sort in shared memory --
-// the bound matrix never round-trips through HBM before sorting.
+// One visit-order record: node, its bound, its leaf slot (+ filter flag) and the
+// filter operand pred - offset (tree.py:277-286), exactly as the plan evaluates it.
+__device__ inline void put_record(const OrderArgs& o, const lf_index& idx, int64_t q, int Nn, int p, double lb,
+                                  int node) {
+    const int64_t at = q * Nn + p;
+    o.lbs[at] = lb;
+    o.order[at] = node;
+    const int leaf = idx.d_node_leaf[node];
+    int rec = leaf;
+    double a = -kInf;
+    if (leaf >= 0 && idx.d_leaf_filter != nullptr && (o.pred != nullptr || o.pred64 != nullptr)) {
+        const int fs = idx.d_leaf_filter[leaf];
+        if (fs >= 0) {
+            rec |= LF_REC_HASF;
+            const double pv = o.pred64 != nullptr ? o.pred64[q * o.F + fs] : (double)o.pred[q * o.F + fs];
+            a = pv - o.offset[fs];
+        }
+    }
+    o.leafo[at] = rec;
+    o.adj[at] = a;
+}
+
+__device__ inline double node_bound(const double* qs, const double* ws, int ns, const double* env_min,
+                                    const double* env_max, int n_env, int node) {
+    double acc = 0.0;
+    for (int sg = 0; sg < ns; ++sg) {                  // lb_kernel<0>: np.dot(widths*gap, gap)
+        const double mn = env_min[(int64_t)sg * n_env + node];
+        const double mx = env_max[(int64_t)sg * n_env + node];
+        double g = fmax(mn - qs[sg], qs[sg] - mx);
+        g = fmax(g, 0.0);
+        acc = __fma_rn(__dmul_rn(ws[sg], g), g, acc);
+    }
+    return sqrt(acc);
+}
+
+// Fused K1 + K2 for trees of up to 8192 nodes, FULL order: one CTA per query
+// computes every node's search bound straight into registers and sorts the
+// nodes in shared memory -- the bound matrix never round-trips through HBM.
+// The sort key is the HIGH 32 bits of the non-negative fp64 bound (they order
+// like the doubles): a stable 4-pass 8-bit block radix sort instead of a 16-pass
+// sort of 64-bit keys.  Equal high words are then put in exact (lb, node id)
+// order by sorting each run on the low words (runs are rare and short; equal
+// bounds keep ascending ids from the stable sort), so the result is the exact
+// (lb, id) order of tree.py:256-275.
 constexpr int FS_THREADS = 512;
 
-template <int ITEMS>
-__global__ void __launch_bounds__(FS_THREADS) bounds_sort_kernel(const double* __restrict__ qsumm, lf_index idx,
-                                                                 const double* __restrict__ env_min,
-                                                                 const double* __restrict__ env_max, int n_env,
-                                                                 double* __restrict__ lbs, int* __restrict__ order) {
-    using Sort = cub::BlockRadixSort<double, FS_THREADS, ITEMS, int>;
+template <int ITEMS, int RB>
+struct FsSmem {
+    using Sort = cub::BlockRadixSort<unsigned, FS_THREADS, ITEMS, int, RB>;
+    unsigned lo[FS_THREADS * ITEMS];                   // low word of each node's bound, by node id
+    union {
+        typename Sort::TempStorage sort;
+        struct {
+            unsigned key[FS_THREADS * ITEMS];          // sorted high words
+            int node[FS_THREADS * ITEMS];              // sorted node ids
+        } out;
+    } u;
+};
+
+template <int ITEMS, int RB>
+__global__ void __launch_bounds__(FS_THREADS, 1) bounds_sort_kernel(const double* __restrict__ qsumm, lf_index idx,
+                                                                 int n_env, OrderArgs o) {
+    using Sm = FsSmem<ITEMS, RB>;
     extern __shared__ __align__(16) uint8_t fs_smem[];
-    auto& tmp = *reinterpret_cast<typename Sort::TempStorage*>(fs_smem);
+    Sm& sm = *reinterpret_cast<Sm*>(fs_smem);
     __shared__ double qs[LF_MAX_SEG];
     __shared__ double ws[LF_MAX_SEG];
     const int64_t q = blockIdx.x;
+    if (o.only != nullptr && o.only[q] == 0) return;
     const int ns = idx.n_seg;
     if (threadIdx.x < ns) {
         qs[threadIdx.x] = qsumm[q * ns + threadIdx.x];
         ws[threadIdx.x] = (double)idx.seg_width[threadIdx.x];
     }
     __syncthreads();
-    double keys[ITEMS];
+    unsigned keys[ITEMS];
     int vals[ITEMS];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         const int node = threadIdx.x * ITEMS + i;          // blocked arrangement: stable sort keeps id order
         if (node < n_env) {
-            double acc = 0.0;
-            for (int sg = 0; sg < ns; ++sg) {
-                const double mn = env_min[(int64_t)sg * n_env + node];
-                const double mx = env_max[(int64_t)sg * n_env + node];
-                double g = fmax(mn - qs[sg], qs[sg] - mx);
-                g = fmax(g, 0.0);
-                acc = __fma_rn(__dmul_rn(ws[sg], g), g, acc);
-            }
-            keys[i] = sqrt(acc);
+            const double lb = node_bound(qs, ws, ns, idx.d_env_min, idx.d_env_max, n_env, node);
+            keys[i] = (unsigned)__double2hiint(lb);
+            sm.lo[node] = (unsigned)__double2loint(lb);
             vals[i] = node;
         } else {
-            keys[i] = kInf;                                // padding sorts last
+            keys[i] = 0xFFFFFFFFu;                         // padding sorts last (real keys <= +inf's 0x7FF00000)
             vals[i] = INT_MAX;
         }
     }
-    Sort(tmp).Sort(keys, vals);
+    typename Sm::Sort(sm.u.sort).Sort(keys, vals);
+    __syncthreads();                                       // temp storage is reused below
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-        const int pos = threadIdx.x * ITEMS + i;
-        if (pos < n_env) {
-            lbs[q * n_env + pos] = keys[i];
-            order[q * n_env + pos] = vals[i];
+        sm.u.out.key[threadIdx.x * ITEMS + i] = keys[i];
+        sm.u.out.node[threadIdx.x * ITEMS + i] = vals[i];
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < n_env; p += FS_THREADS) {   // exact order inside runs of equal high words
+        const unsigned kp = sm.u.out.key[p];
+        if ((p == 0 || sm.u.out.key[p - 1] != kp) && p + 1 < n_env && sm.u.out.key[p + 1] == kp) {
+            int e = p + 1;
+            while (e < n_env && sm.u.out.key[e] == kp) ++e;
+            for (int a = p + 1; a < e; ++a) {              // insertion sort by (low word, id)
+                const int na = sm.u.out.node[a];
+                const unsigned la = sm.lo[na];
+                int b = a - 1;
+                while (b >= p) {
+                    const int nb = sm.u.out.node[b];
+                    const unsigned lbw = sm.lo[nb];
+                    if (lbw < la || (lbw == la && nb < na)) break;
+                    sm.u.out.node[b + 1] = nb;
+                    --b;
+                }
+                sm.u.out.node[b + 1] = na;
+            }
         }
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < n_env; p += FS_THREADS) {
+        const int node = sm.u.out.node[p];
+        put_record(o, idx, q, n_env, p, __hiloint2double((int)sm.u.out.key[p], (int)sm.lo[node]), node);
+    }
+    if (threadIdx.x == 0) {
+        o.olen[q] = n_env;
+        if (o.only != nullptr) o.only[q] = 0;
     }
 }
 
-template <int ITEMS>
-static int launch_fused(const double* d_qsumm, int64_t Q, const lf_index& idx, int n, double* lbs, int* order,
+// Fused K1 + K2, PREFIX of the order (trees of up to 8192 nodes).  A search
+// only ever walks the head of its visit order (it stops at the first node with
+// lb > bsf * f), so sorting all n_nodes pairs per query is mostly wasted work.
+// One CTA per query: bounds into registers; radix-select (4 byte passes over
+// the high 32 bits of the non-negative fp64 bound, which order like the
+// doubles) the key T of the PF_K-th smallest; compact every node with key <= T
+// (or < T if that overflows PF_CAP) -- exactly the head of the (lb, id) order --
+// and bitonic-sort it by (lb, id) in shared memory.  A query whose walk reaches
+// the end of its prefix is refilled with the full order (refill_order).
+constexpr int PF_THREADS = 512;
+constexpr int PF_ITEMS = 16;
+constexpr int PF_K = 1024;
+constexpr int PF_CAP = 2048;
+
+__global__ void __launch_bounds__(PF_THREADS, 1) prefix_order_kernel(const double* __restrict__ qsumm, lf_index idx,
+                                                                  int Nn, OrderArgs o) {
+    __shared__ double qs[LF_MAX_SEG];
+    __shared__ double ws[LF_MAX_SEG];
+    __shared__ double sk[PF_CAP];
+    __shared__ int sv[PF_CAP];
+    __shared__ int hist[256];
+    __shared__ unsigned s_prefix;
+    __shared__ int s_rem, s_lt, s_le, s_cnt;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t q = blockIdx.x;
+    const int ns = idx.n_seg;
+    if (tid < ns) {
+        qs[tid] = qsumm[q * ns + tid];
+        ws[tid] = (double)idx.seg_width[tid];
+    }
+    if (tid == 0) { s_lt = 0; s_le = 0; s_cnt = 0; }
+    __syncthreads();
+    double key[PF_ITEMS];
+    unsigned k32[PF_ITEMS];
+#pragma unroll
+    for (int i = 0; i < PF_ITEMS; ++i) {
+        const int node = tid * PF_ITEMS + i;
+        if (node < Nn) {
+            key[i] = node_bound(qs, ws, ns, idx.d_env_min, idx.d_env_max, Nn, node);
+            k32[i] = (unsigned)__double2hiint(key[i]);     // lb >= 0: monotone in lb
+        } else {
+            key[i] = kInf;
+            k32[i] = 0xFFFFFFFFu;                          // never selected
+        }
+    }
+    unsigned T = 0xFFFFFFFEu;                              // Nn <= PF_CAP: everything
+    bool take = true;
+    if (Nn > PF_CAP) {
+        unsigned prefix = 0, mask = 0;
+        int rem = PF_K;
+        for (int shift = 24; shift >= 0; shift -= 8) {
+            if (tid < 256) hist[tid] = 0;
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < PF_ITEMS; ++i)
+                if (k32[i] != 0xFFFFFFFFu && (k32[i] & mask) == prefix) atomicAdd(&hist[(k32[i] >> shift) & 255], 1);
+            __syncthreads();
+            if (warp == 0) {
+                int c[8], sum = 0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) { c[j] = hist[lane * 8 + j]; sum += c[j]; }
+                int incl = sum;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, incl, d);
+                    if (lane >= d) incl += v;
+                }
+                const int excl = incl - sum;
+                if (excl < rem && rem <= incl) {
+                    int acc = excl, b = 7;
+                    for (int j = 0; j < 8; ++j) {
+                        if (acc + c[j] >= rem) { b = j; break; }
+                        acc += c[j];
+                    }
+                    s_prefix = prefix | ((unsigned)(lane * 8 + b) << shift);
+                    s_rem = rem - acc;
+                }
+            }
+            __syncthreads();
+            prefix = s_prefix;
+            rem = s_rem;
+            mask |= 255u << shift;
+        }
+        T = prefix;                                        // key of the PF_K-th smallest bound
+        int lt = 0, le = 0;
+#pragma unroll
+        for (int i = 0; i < PF_ITEMS; ++i) {
+            lt += k32[i] < T;
+            le += k32[i] <= T;
+        }
+        atomicAdd(&s_lt, lt);
+        atomicAdd(&s_le, le);
+        __syncthreads();
+        if (s_le > PF_CAP) {                               // take only keys < T (count < PF_K); none
+            if (s_lt == 0) take = false;                   // at all -> the plan refills at once
+            else T -= 1;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < PF_ITEMS; ++i)
+        if (take && k32[i] <= T) {
+            const int pos = atomicAdd(&s_cnt, 1);
+            sk[pos] = key[i];
+            sv[pos] = tid * PF_ITEMS + i;
+        }
+    __syncthreads();
+    const int cnt = s_cnt;
+    int N = 64;
+    while (N < cnt) N <<= 1;
+    for (int i = cnt + tid; i < N; i += PF_THREADS) { sk[i] = kInf; sv[i] = INT_MAX; }
+    __syncthreads();
+    for (int k = 2; k <= N; k <<= 1) {                     // bitonic sort by (lb, node id)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = tid; i < N; i += PF_THREADS) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const double a = sk[i], b = sk[ixj];
+                    const int va = sv[i], vb = sv[ixj];
+                    const bool gt = a > b || (a == b && va > vb);
+                    if (gt == ((i & k) == 0)) { sk[i] = b; sk[ixj] = a; sv[i] = vb; sv[ixj] = va; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int p = tid; p < cnt; p += PF_THREADS) put_record(o, idx, q, Nn, p, sk[p], sv[p]);
+    if (tid == 0) o.olen[q] = cnt;
+}
+
+__global__ void records_kernel(const double* __restrict__ lb_sorted, const int* __restrict__ order, lf_index idx,
+                               int64_t Q, int Nn, OrderArgs o) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < Q * Nn) {
+        const int64_t q = t / Nn;
+        put_record(o, idx, q, Nn, (int)(t - q * Nn), lb_sorted[t], order[t]);
+    }
+    if (t < Q) o.olen[t] = Nn;
+}
+
+template <int ITEMS, int RB = 4>
+static int launch_fused(const double* d_qsumm, int64_t Q, const lf_index& idx, int n, const OrderArgs& oa,
                         cudaStream_t st) {
-    using Sort = cub::BlockRadixSort<double, FS_THREADS, ITEMS, int>;
-    const int bytes = (int)sizeof(typename Sort::TempStorage);
+    const int bytes = (int)sizeof(FsSmem<ITEMS, RB>);
     static bool attr = false;
     if (!attr) {
-        LF_CUDA(cudaFuncSetAttribute(bounds_sort_kernel<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        LF_CUDA(cudaFuncSetAttribute(bounds_sort_kernel<ITEMS, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
         attr = true;
     }
-    bounds_sort_kernel<ITEMS><<<(unsigned)Q, FS_THREADS, bytes, st>>>(d_qsumm, idx, idx.d_env_min, idx.d_env_max, n,
-                                                                      lbs, order);
+    bounds_sort_kernel<ITEMS, RB><<<(unsigned)Q, FS_THREADS, bytes, st>>>(d_qsumm, idx, n, oa);
     LF_CUDA(cudaGetLastError());
     return LF_OK;
 }
 
-// Segment means + bounds + per-query visit order in as few passes as the tree
-// size allows: fused block sort up to 8192 nodes, else bounds kernel + CUB.
+static int launch_full_fused(const double* d_qsumm, int64_t Q, const lf_index& idx, int n, const OrderArgs& oa,
+                             cudaStream_t st) {
+    if (n <= FS_THREADS * 4) return launch_fused<4>(d_qsumm, Q, idx, n, oa, st);
+    if (n <= FS_THREADS * 8) return launch_fused<8>(d_qsumm, Q, idx, n, oa, st);
+    return launch_fused<16>(d_qsumm, Q, idx, n, oa, st);
+}
+
+// Segment means + bounds + per-query visit-order records in as few passes as the
+// tree size allows: fused prefix / block sort up to 8192 nodes, else bounds
+// kernel + CUB segmented sort + record gather.
 int bounds_and_order(const float* d_q, int64_t Q, const lf_index& idx, double* d_qsumm, double* d_lb_scratch,
-                     double* d_lbs, int* d_order, cudaStream_t st, int* kernels) {
+                     const OrderArgs& oa, bool prefix, cudaStream_t st, int* kernels) {
     const int n = idx.n_nodes;
     if (Q == 0 || n == 0) return LF_OK;
     if (n <= FS_THREADS * 16 && Q <= 0x7fffffff) {
@@ -167,19 +389,36 @@ int bounds_and_order(const float* d_q, int64_t Q, const lf_index& idx, double* d
             paa_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(d_q, Q, idx, d_qsumm);
             LF_CUDA(cudaGetLastError());
         }
-        int rc;
-        if (n <= FS_THREADS * 4) rc = launch_fused<4>(d_qsumm, Q, idx, n, d_lbs, d_order, st);
-        else if (n <= FS_THREADS * 8) rc = launch_fused<8>(d_qsumm, Q, idx, n, d_lbs, d_order, st);
-        else rc = launch_fused<16>(d_qsumm, Q, idx, n, d_lbs, d_order, st);
         if (kernels) *kernels += 2;
-        return rc;
+        if (prefix && n > PF_CAP) {
+            prefix_order_kernel<<<(unsigned)Q, PF_THREADS, 0, st>>>(d_qsumm, idx, n, oa);
+            LF_CUDA(cudaGetLastError());
+            return LF_OK;
+        }
+        OrderArgs all = oa;
+        all.only = nullptr;
+        return launch_full_fused(d_qsumm, Q, idx, n, all, st);
     }
     int rc = launch_bounds(d_q, Q, idx, idx.d_env_min, idx.d_env_max, n, 0, d_qsumm, d_lb_scratch, st);
     if (rc) return rc;
-    if (kernels) *kernels += 4;
-    return sort_visit_order(d_lb_scratch, Q, n, d_lbs, d_order, st);
+    if (kernels) *kernels += 5;
+    rc = sort_visit_order(d_lb_scratch, Q, n, oa.lbs, oa.order, st);
+    if (rc) return rc;
+    const int64_t tot = std::max<int64_t>(Q * n, Q);
+    records_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(oa.lbs, oa.order, idx, Q, n, oa);
+    LF_CUDA(cudaGetLastError());
+    return LF_OK;
 }
 
+int refill_order(const float* d_q, int64_t Q, const lf_index& idx, const double* d_qsumm, double* d_lb_scratch,
+                 const OrderArgs& oa, cudaStream_t st, int* kernels) {
+    (void)d_q;
+    (void)d_lb_scratch;
+    const int n = idx.n_nodes;
+    LF_REQUIRE(n <= FS_THREADS * 16, "refill is only needed for prefix orders (<= 8192 nodes)");
+    if (kernels) *kernels += 1;
+    return launch_full_fused(d_qsumm, Q, idx, n, oa, st);
+}
 // Per-query stable sort of (lb, node id): the heap pop order of tree.py:256-275
 // (child lb >= parent lb and child id > parent id, so the heap is a sort).
 int sort_visit_order(const double* d_lb, int64_t Q, int n, double* d_lb_sorted, int* d_order,

@@ -33,8 +33,13 @@ struct RoundState {
     int k, kc;                   // kc = candidates kept per task = min(k, CH)
     int R, Rcap;                 // leaves per query this round, and the buffer stride
     double f;                    // bsf_factor
-    const int* order;            // [Q][Nn]
+    const int* order;            // [Q][Nn] visit-order records (bounds.cuh OrderArgs)
     const double* lbs;           // [Q][Nn]
+    const int* leafo;            // [Q][Nn] leaf slot | LF_REC_HASF, -1 internal
+    const double* adj;           // [Q][Nn] pred - offset of the leaf's filter
+    const int* olen;             // [Q] valid (sorted) entries of the order
+    int* refill;                 // [Q] set when the walk reached olen < Nn
+    int* n_refill;               // queries flagged this round (= n_active + 1)
     int* cursor;                 // [Q]
     int* done;                   // [Q]
     double* top_d;               // [Q][k]   running top-k (round-start state)
@@ -78,87 +83,12 @@ __device__ inline double round_bsf(const RoundState& s, int64_t q) {
 }
 
 // ---------------------------------------------------------------- plan ----
-__global__ void plan_kernel(RoundState s, lf_index idx) {
-    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= s.Q) return;
-    const int Nn = idx.n_nodes;
-    int ns = 0, nch = 0;
-    int* pre = s.sel_pre + q * (s.Rcap + 1);
-    if (!s.done[q]) {
-        const double bsf = round_bsf(s, q);
-        const double thr = bsf * s.f;
-        const int* ord = s.order + q * Nn;
-        const double* lbs = s.lbs + q * Nn;
-        long long* st = s.stats + q * LF_N_STATS;
-        int cur = s.cursor[q];
-        bool fin = false;
-        int tl = s.want_trace ? s.tr.d_len[q] : 0;
-        const int64_t tbase = q * (int64_t)idx.n_leaves;
-        while (cur < Nn) {
-            const int node = ord[cur];
-            const double lb = lbs[cur];
-            const int leaf = idx.d_node_leaf[node];
-            if (lb > thr) {                      // tree.py:261
-                if (leaf >= 0) {
-                    st[0]++; st[2]++;
-                    if (s.want_trace) {
-                        s.tr.d_leaf[tbase + tl] = node; s.tr.d_lb[tbase + tl] = lb;
-                        s.tr.d_searched[tbase + tl] = 0; s.tr.d_leaf_nn[tbase + tl] = __longlong_as_double(0x7ff8000000000000LL);
-                        s.tr.d_bsf_before[tbase + tl] = bsf; ++tl;
-                    }
-                }
-                fin = true;
-                break;
-            }
-            ++cur;
-            if (leaf < 0) continue;              // internal: children follow in order
-            st[0]++;
-            const int fs = (idx.d_leaf_filter != nullptr && (s.pred != nullptr || s.pred64 != nullptr))
-                               ? idx.d_leaf_filter[leaf] : -1;
-            if (fs >= 0) {                        // tree.py:279-286
-                st[4]++;
-                const double pv = s.pred64 != nullptr ? s.pred64[q * s.F + fs] : (double)s.pred[q * s.F + fs];
-                const double p = pv - s.offset[fs];
-                if (p > thr) {
-                    st[3]++;
-                    if (s.want_trace) {
-                        s.tr.d_leaf[tbase + tl] = node; s.tr.d_lb[tbase + tl] = lb;
-                        s.tr.d_searched[tbase + tl] = 0; s.tr.d_leaf_nn[tbase + tl] = __longlong_as_double(0x7ff8000000000000LL);
-                        s.tr.d_bsf_before[tbase + tl] = bsf; ++tl;
-                    }
-                    continue;
-                }
-            }
-            const int64_t rows = idx.d_leaf_ptr[leaf + 1] - idx.d_leaf_ptr[leaf];
-            st[1]++; st[5] += rows;              // tree.py:290-291: whole leaves
-            s.sel_leaf[q * s.Rcap + ns] = leaf;
-            if (s.want_trace) {
-                s.sel_trace[q * s.Rcap + ns] = tl;
-                s.tr.d_leaf[tbase + tl] = node; s.tr.d_lb[tbase + tl] = lb;
-                s.tr.d_searched[tbase + tl] = 1; s.tr.d_bsf_before[tbase + tl] = bsf; ++tl;
-            }
-            pre[ns] = nch;
-            nch += (int)((rows + CH - 1) / CH);
-            ++ns;
-            if (ns == s.R) break;
-        }
-        if (cur >= Nn) fin = true;
-        s.cursor[q] = cur;
-        if (s.want_trace) s.tr.d_len[q] = tl;
-        if (fin) s.done[q] = 1;
-        else atomicAdd(s.n_active, 1);
-    }
-    pre[ns] = nch;
-    s.n_sel[q] = ns;
-    s.chunk_off[q + 1] = nch;   // counts; turned into offsets by offsets_kernel
-}
-
 // Warp-parallel plan: one warp per query evaluates 32 consecutive visit-order
 // entries at a time.  Within a round every decision uses the round-start bsf,
 // so the entries are independent; ballots locate the first break (lb > bsf*f)
 // and the R-th selected leaf, and prefix counts place selections and trace
-// entries in visit order.  Counters, selections and traces are identical to
-// plan_kernel's serial walk.
+// entries in visit order.  Counters, selections and traces are identical to a
+// serial walk of the same entries (tree.py:256-297 with the round-start bsf).
 __global__ void plan_warp_kernel(RoundState s, lf_index idx) {
     const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -172,31 +102,28 @@ __global__ void plan_warp_kernel(RoundState s, lf_index idx) {
         const double thr = bsf * s.f;
         const int* ord = s.order + q * Nn;
         const double* lbs = s.lbs + q * Nn;
+        const int* lrec = s.leafo + q * Nn;
+        const double* adj = s.adj + q * Nn;
+        const int len = s.olen[q];
         long long* st = s.stats + q * LF_N_STATS;
         int cur = s.cursor[q];
-        bool fin = false;
+        bool fin = false, quota_hit = false;
         int tl = s.want_trace ? s.tr.d_len[q] : 0;
         const int64_t tbase = q * (int64_t)idx.n_leaves;
         long long c_vis = 0, c_srch = 0, c_lbp = 0, c_fp = 0, c_inf = 0, c_rows = 0;
-        while (!fin && cur < Nn) {
+        while (!fin && cur < len) {
             const int i = cur + lane;
-            const bool valid = i < Nn;
-            const int node = valid ? ord[i] : -1;
+            const bool valid = i < len;
+            const int node = (valid && s.want_trace) ? ord[i] : -1;
             const double lb = valid ? lbs[i] : kInf;
-            const int leaf = valid ? idx.d_node_leaf[node] : -1;
+            const int rec = valid ? lrec[i] : -1;
+            const int leaf = rec >= 0 ? (rec & LF_REC_LEAF) : -1;
             const bool brk = valid && lb > thr;
             const unsigned bmask = __ballot_sync(0xffffffffu, brk);
             const int first_brk = bmask ? __ffs(bmask) - 1 : 32;
             const bool visit = valid && leaf >= 0 && lane < first_brk;
-            int fs = -1;
-            bool fpr = false;
-            if (visit && idx.d_leaf_filter != nullptr && (s.pred != nullptr || s.pred64 != nullptr)) {
-                fs = idx.d_leaf_filter[leaf];
-                if (fs >= 0) {
-                    const double pv = s.pred64 != nullptr ? s.pred64[q * s.F + fs] : (double)s.pred[q * s.F + fs];
-                    fpr = (pv - s.offset[fs]) > thr;
-                }
-            }
+            const int fs = (visit && (rec & LF_REC_HASF)) ? 0 : -1;
+            const bool fpr = fs >= 0 && adj[i] > thr;      // (pred - offset) > bsf * f, tree.py:282
             const bool scan = visit && !fpr;
             const unsigned smask = __ballot_sync(0xffffffffu, scan);
             const int need = s.R - ns;
@@ -208,7 +135,7 @@ __global__ void plan_warp_kernel(RoundState s, lf_index idx) {
                 end = __ffs(mm);                                   // include the need-th selected lane
                 quota = true;
             } else {
-                end = min(first_brk, Nn - cur);
+                end = min(first_brk, len - cur);
             }
             const bool in = lane < end;
             const bool v_in = visit && in;
@@ -257,7 +184,8 @@ __global__ void plan_warp_kernel(RoundState s, lf_index idx) {
             nch += __shfl_sync(0xffffffffu, incl, 31);
             if (quota) {
                 cur += end;
-            } else if (first_brk < 32 && first_brk < Nn - cur) {
+                quota_hit = true;
+            } else if (first_brk < 32 && first_brk < len - cur) {
                 // the break entry: a leaf counts as visited + lb-pruned (tree.py:261-269)
                 const int bnode = __shfl_sync(0xffffffffu, node, first_brk);
                 const int bleaf = __shfl_sync(0xffffffffu, leaf, first_brk);
@@ -288,6 +216,10 @@ __global__ void plan_warp_kernel(RoundState s, lf_index idx) {
             if (s.want_trace) s.tr.d_len[q] = tl;
             if (fin) s.done[q] = 1;
             else atomicAdd(s.n_active, 1);
+            if (!fin && !quota_hit && cur >= len) {        // walked off the sorted prefix
+                s.refill[q] = 1;
+                atomicAdd(s.n_refill, 1);
+            }
         }
     }
     if (lane == 0) {
@@ -458,127 +390,6 @@ __global__ void __launch_bounds__(SCAN_THREADS) scan_kernel(RoundState s, lf_ind
                     for (int i = lane; i < nrows; i += 32) {
                         if (pair_less(sd[i], sid[i], bd, bi)) { bd = sd[i]; bi = sid[i]; bp = i; }
                     }
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) {
-                        double od = __shfl_xor_sync(0xffffffffu, bd, o);
-                        long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                        int op = __shfl_xor_sync(0xffffffffu, bp, o);
-                        if (pair_less(od, oi, bd, bi)) { bd = od; bi = oi; bp = op; }
-                    }
-                    if (lane == 0) {
-                        cd[sel] = bd;
-                        ci[sel] = (bd == kInf) ? -1 : bi;
-                        if (bp >= 0) { sd[bp] = kInf; sid[bp] = LLONG_MAX; }
-                    }
-                    __syncwarp();
-                }
-            }
-        }
-        __syncthreads();
-    }
-}
-
-// Early-abandoning scan (m % 64 == 0).  Half a warp owns a row; each row is
-// read in 256-byte pieces (64 dims = one float4 per lane).  After every piece
-// the half-warp reduces its running squared distance and drops the row once it
-// exceeds the threshold, so the rest of the row is never fetched from HBM.
-// Threshold: the round-start k-th best (tree.py:207 keeps d <= bsf) and, for
-// k = 1, the best full distance this half-warp has seen; both with a 1e-12
-// relative margin so a dropped row is strictly worse after the sqrt.  Whole
-// leaves still count in series_scanned (F4).
-template <int NCH, int U>
-__global__ void __launch_bounds__(SCAN_THREADS) scan_ea_kernel(RoundState s, lf_index idx,
-                                                               const float* __restrict__ queries) {
-    __shared__ double sd[CH];
-    __shared__ long long sid[CH];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int hl = lane & 15;
-    const int slot = warp * 2 + (lane >> 4);          // 16 half-warps per CTA
-    const long long total = s.chunk_off[s.Q];
-    const int m = idx.m;
-    constexpr double kMargin = 1.0 + 1e-12;
-    for (long long t = blockIdx.x; t < total; t += gridDim.x) {
-        const int4 tk = s.tasks[t];             // (query, leaf slot, chunk) from expand_tasks_kernel
-        const int64_t q = tk.x;
-        const int leaf = tk.y;
-        const int c = tk.z;
-        const int64_t lbeg = idx.d_leaf_ptr[leaf], lend = idx.d_leaf_ptr[leaf + 1];
-        const int64_t r0 = lbeg + (int64_t)c * CH;
-        const int nrows = (int)min((int64_t)CH, lend - r0);
-        const double bsf = round_bsf(s, q);
-        const double bsf2 = bsf == kInf ? kInf : bsf * bsf * kMargin;
-        const float* qrow = queries + q * m;
-        double qv[NCH][4];
-#pragma unroll
-        for (int ch = 0; ch < NCH; ++ch) {
-            float4 x = reinterpret_cast<const float4*>(qrow + ch * 64)[hl];
-            qv[ch][0] = x.x; qv[ch][1] = x.y; qv[ch][2] = x.z; qv[ch][3] = x.w;
-        }
-        double best2 = kInf;                                   // k == 1: best full d^2 seen here
-        // warp-uniform trip count: both half-warps run every iteration (the
-        // half-warp reductions below use full-warp shuffles)
-        for (int b0 = 0; b0 < nrows; b0 += 16 * U) {
-            const int base = b0 + slot;
-            double acc[U];
-            bool alive[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) { acc[u] = 0.0; alive[u] = base + 16 * u < nrows; }
-            double p[U];
-#pragma unroll
-            for (int ch = 0; ch < NCH; ++ch) {
-                float4 x[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const float4* rp = reinterpret_cast<const float4*>(idx.d_X + (r0 + base + 16 * u) * m + ch * 64);
-                    x[u] = alive[u] ? __ldcs(rp + hl) : make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    double d0 = (double)x[u].x - qv[ch][0], d1 = (double)x[u].y - qv[ch][1];
-                    double d2 = (double)x[u].z - qv[ch][2], d3 = (double)x[u].w - qv[ch][3];
-                    acc[u] = __fma_rn(d0, d0, acc[u]);
-                    acc[u] = __fma_rn(d1, d1, acc[u]);
-                    acc[u] = __fma_rn(d2, d2, acc[u]);
-                    acc[u] = __fma_rn(d3, d3, acc[u]);
-                    double v = acc[u];
-#pragma unroll
-                    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                    p[u] = v;
-                }
-                const double thr2 = s.k == 1 ? fmin(bsf2, best2 * kMargin) : bsf2;
-#pragma unroll
-                for (int u = 0; u < U; ++u)
-                    if (alive[u] && p[u] > thr2) alive[u] = false;
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int r = base + 16 * u;
-                if (r < nrows) {
-                    if (alive[u] && s.k == 1) best2 = fmin(best2, p[u]);
-                    if (hl == 0) {
-                        sd[r] = alive[u] ? sqrt(p[u]) : kInf;
-                        sid[r] = idx.d_row_id[r0 + r];
-                    }
-                }
-            }
-        }
-        __syncthreads();
-        if (warp == 0) {
-            double* cd = s.cand_d + t * s.kc;
-            long long* ci = s.cand_i + t * s.kc;
-            for (int i = lane; i < nrows; i += 32)
-                if (!(sd[i] <= bsf)) sd[i] = kInf;
-            __syncwarp();
-            if (s.kc >= nrows) {
-                for (int i = lane; i < s.kc; i += 32) {
-                    cd[i] = i < nrows ? sd[i] : kInf;
-                    ci[i] = (i < nrows && sd[i] != kInf) ? sid[i] : -1;
-                }
-            } else {
-                for (int sel = 0; sel < s.kc; ++sel) {
-                    double bd = kInf; long long bi = LLONG_MAX; int bp = -1;
-                    for (int i = lane; i < nrows; i += 32)
-                        if (pair_less(sd[i], sid[i], bd, bi)) { bd = sd[i]; bi = sid[i]; bp = i; }
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) {
                         double od = __shfl_xor_sync(0xffffffffu, bd, o);
@@ -1396,7 +1207,16 @@ __global__ void finish_kernel(RoundState s, int64_t* out_ids, double* out_d) {
     out_d[t] = ok ? s.top_d[t] : kInf;
 }
 
-// Scan variant (experiments): LF_SCAN_VARIANT = ea2 (default) | ea3 | full.
+// Visit orders as full per-query sorts (default) or sorted prefixes + refill
+// (LF_FULL_ORDER=0).  LeaFi walks deep into the order -- its filters prune most
+// visited leaves (bench: 281 leaves visited per query, 1,202 at most), so a
+// 1,024-entry prefix sends ~27% of the queries to a refill and the full sort wins.
+static bool prefix_orders() {
+    const char* e = getenv("LF_FULL_ORDER");
+    return e && e[0] == '0';
+}
+
+// Scan variant (experiments): LF_SCAN_VARIANT = q8 (default) | ea2 | ea3 | full.
 static int scan_variant() {
     const char* e = getenv("LF_SCAN_VARIANT");
     if (e && strcmp(e, "ea3") == 0) return 3;
@@ -1444,8 +1264,11 @@ struct lf_session {
     const float* d_q = nullptr;
     lf::RoundState s{};
     lf::Scratch qsumm, lb, lbs, order, cursor, done, topd, topi, topn, topd2, topi2, topn2, sel_leaf,
-        sel_trace, sel_pre, n_sel, chunk_off, cand_d, cand_i, task_min, n_active, tasks, ea_count, qc8, qm8;
+        sel_trace, sel_pre, n_sel, chunk_off, cand_d, cand_i, task_min, n_active, tasks, ea_count, qc8, qm8,
+        leafo, adj, olen, refill;
+    lf::OrderArgs oa{};
     bool q8 = false;                 // int8-bounded scan (query codes quantised once in begin)
+    long long refills = 0;           // queries whose visit order was completed after the prefix
     int* h_active = nullptr;
     int round = 0;
     long long kernels = 0;
@@ -1482,6 +1305,11 @@ static int session_begin(lf_session* ss) {
     LF_CUDA(ss->lb.alloc(Nn > 8192 ? sizeof(double) * Q * Nn : 16, st));   // only the unfused path uses it
     LF_CUDA(ss->lbs.alloc(sizeof(double) * Q * Nn, st));
     LF_CUDA(ss->order.alloc(sizeof(int) * Q * Nn, st));
+    LF_CUDA(ss->leafo.alloc(sizeof(int) * Q * Nn, st));
+    LF_CUDA(ss->adj.alloc(sizeof(double) * Q * Nn, st));
+    LF_CUDA(ss->olen.alloc(sizeof(int) * Q, st));
+    LF_CUDA(ss->refill.alloc(sizeof(int) * Q, st));
+    LF_CUDA(cudaMemsetAsync(ss->refill.p, 0, sizeof(int) * Q, st));
     LF_CUDA(ss->cursor.alloc(sizeof(int) * Q, st));
     LF_CUDA(ss->done.alloc(sizeof(int) * Q, st));
     LF_CUDA(ss->topd.alloc(sizeof(double) * Q * s.k, st));
@@ -1498,13 +1326,13 @@ static int session_begin(lf_session* ss) {
     LF_CUDA(ss->cand_d.alloc(sizeof(double) * max_tasks * s.kc, st));
     LF_CUDA(ss->cand_i.alloc(sizeof(long long) * max_tasks * s.kc, st));
     LF_CUDA(ss->task_min.alloc(sizeof(double) * (s.want_trace ? max_tasks : 1), st));
-    LF_CUDA(ss->n_active.alloc(sizeof(int), st));
+    LF_CUDA(ss->n_active.alloc(sizeof(int) * 2, st));   // [active, refill requests]
     LF_CUDA(ss->tasks.alloc(sizeof(int4) * max_tasks, st));
     LF_CUDA(ss->ea_count.alloc(sizeof(unsigned long long) * 2, st));
     LF_CUDA(cudaMemsetAsync(ss->ea_count.p, 0, sizeof(unsigned long long) * 2, st));
     {   // one pinned word per host thread; a round reads it right after its own sync
         static thread_local int* pinned = nullptr;
-        if (pinned == nullptr) LF_CUDA(cudaMallocHost(&pinned, sizeof(int)));
+        if (pinned == nullptr) LF_CUDA(cudaMallocHost(&pinned, sizeof(int) * 2));
         ss->h_active = pinned;
     }
 
@@ -1515,13 +1343,29 @@ static int session_begin(lf_session* ss) {
         LF_CUDA(cudaEventRecord(ss->ev[0], st));
     }
     int nk = 0;
-    int rc = bounds_and_order(ss->d_q, Q, idx, ss->qsumm.as<double>(), ss->lb.as<double>(), ss->lbs.as<double>(),
-                              ss->order.as<int>(), st, &nk);
+    OrderArgs& oa = ss->oa;
+    oa.lbs = ss->lbs.as<double>();
+    oa.order = ss->order.as<int>();
+    oa.leafo = ss->leafo.as<int>();
+    oa.adj = ss->adj.as<double>();
+    oa.olen = ss->olen.as<int>();
+    oa.pred = o.d_pred;
+    oa.pred64 = o.d_pred_f64;
+    oa.offset = o.d_offset;
+    oa.F = o.n_filters;
+    oa.only = nullptr;
+    int rc = bounds_and_order(ss->d_q, Q, idx, ss->qsumm.as<double>(), ss->lb.as<double>(), oa, prefix_orders(),
+                              st, &nk);
     if (rc) return rc;
     ss->kernels += nk;
 
     s.order = ss->order.as<int>();
     s.lbs = ss->lbs.as<double>();
+    s.leafo = ss->leafo.as<int>();
+    s.adj = ss->adj.as<double>();
+    s.olen = ss->olen.as<int>();
+    s.refill = ss->refill.as<int>();
+    s.n_refill = ss->n_active.as<int>() + 1;
     s.cursor = ss->cursor.as<int>();
     s.done = ss->done.as<int>();
     s.top_d = ss->topd.as<double>();
@@ -1579,7 +1423,7 @@ static int session_round(lf_session* ss, const double* d_bound, double* d_bsf_ou
     const int64_t Q = ss->Q;
     s.bound = d_bound;
     s.R = o.sequential ? 1 : (int)std::min<int64_t>(s.Rcap, (int64_t)1 << std::min(ss->round, 30));
-    LF_CUDA(cudaMemsetAsync(s.n_active, 0, sizeof(int), st));
+    LF_CUDA(cudaMemsetAsync(s.n_active, 0, sizeof(int) * 2, st));
     if (ss->prof) cudaEventRecord(ss->ev[2], st);
     plan_warp_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s, idx);
     offsets_kernel<<<1, 1024, 0, st>>>(s.chunk_off, Q);
@@ -1622,8 +1466,17 @@ static int session_round(lf_session* ss, const double* d_bound, double* d_bsf_ou
         LF_CUDA(cudaGetLastError());
         ++ss->kernels;
     }
-    LF_CUDA(cudaMemcpyAsync(ss->h_active, s.n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+    LF_CUDA(cudaMemcpyAsync(ss->h_active, s.n_active, sizeof(int) * 2, cudaMemcpyDeviceToHost, st));
     LF_CUDA(cudaStreamSynchronize(st));
+    if (ss->h_active[1] > 0) {      // some walks reached the end of their sorted prefix
+        OrderArgs oa = ss->oa;
+        oa.only = s.refill;
+        int nk = 0;
+        int rc = refill_order(ss->d_q, Q, idx, ss->qsumm.as<double>(), ss->lb.as<double>(), oa, st, &nk);
+        if (rc) return rc;
+        ss->kernels += nk;
+        ss->refills += ss->h_active[1];
+    }
     if (ss->prof) {
         double* p = o.h_profile;
         if (ss->round == 0) p[LF_PROF_BOUNDS_MS] = ev_ms(ss->ev[0], ss->ev[1]);
@@ -1651,6 +1504,7 @@ static int session_end(lf_session* ss, int64_t* out_ids, double* out_d, int64_t*
         p[LF_PROF_ROUNDS] = ss->round;
         p[LF_PROF_KERNELS] = (double)ss->kernels;
         p[LF_PROF_TOTAL_MS] = ev_ms(ss->ev[0], ss->ev[5]);
+        p[LF_PROF_REFILLS] = (double)ss->refills;
         unsigned long long c[2] = {0, 0};
         cudaMemcpy(c, ss->ea_count.p, sizeof(c), cudaMemcpyDeviceToHost);
         p[LF_PROF_EA_ROWS] = (double)c[0];

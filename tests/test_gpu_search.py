@@ -372,3 +372,67 @@ def test_q8_pipeline_exact(m, k, monkeypatch):
     np.testing.assert_array_equal(got.stats, ref.stats)
     assert got.ids[-3, 0] == 7 and got.dists[-3, 0] == 0.0
     assert got.ids[-1, 0] == 4321 and got.dists[-1, 0] == 0.0
+
+
+def _prefix_tree():
+    """2048 < nodes <= 8192: the visit order is built as a sorted prefix + refills."""
+    from paper_2502_01836_b200 import build_index
+
+    data = lo.randwalk(40000, 64, 77)
+    t = build_index(data, 24)
+    assert 2048 < t.n_nodes <= 8192, t.n_nodes
+    return data, t
+
+
+def test_prefix_order_sequential_matches_oracle(monkeypatch):
+    """Sequential exact search over prefix orders (with refills): ids, distances and
+    every counter equal the reference traversal."""
+    from paper_2502_01836_b200 import search_batch
+
+    monkeypatch.setenv("LF_FULL_ORDER", "0")
+    data, t = _prefix_tree()
+    Q = np.concatenate([lo.noisy_queries(data, 6, nz, 50 + int(10 * nz)) for nz in (0.1, 0.5, 1.5)])
+    prof = np.zeros(16)
+    res = search_batch(t, Q, 3, sequential=True, profile=prof)
+    assert prof[7] > 0, "the wide queries must have needed a refill"
+    ot = lo.build_tree(data, 24)
+    for i, q in enumerate(Q):
+        o = lo.search(ot, q, 3)
+        assert res.ids[i].tolist() == [a for a, _ in o.results], i
+        np.testing.assert_allclose(res.dists[i], [b for _, b in o.results], rtol=DIST_RTOL)
+        assert res.stats[i].tolist() == [o.stats[s_] for s_ in lo.STAT_KEYS], i
+
+
+def test_prefix_order_batched_equals_full_order(monkeypatch):
+    """Batched exact search: prefix orders + refills give the same neighbours as
+    full per-query sorts (LF_FULL_ORDER=1)."""
+    from paper_2502_01836_b200 import search_batch
+
+    data, t = _prefix_tree()
+    Q = np.concatenate([lo.noisy_queries(data, 16, nz, 60 + int(10 * nz)) for nz in (0.1, 0.4, 1.0)])
+    for k in (1, 4):
+        monkeypatch.setenv("LF_FULL_ORDER", "1")
+        ref = search_batch(t, Q, k)
+        monkeypatch.setenv("LF_FULL_ORDER", "0")
+        got = search_batch(t, Q, k)
+        np.testing.assert_array_equal(got.ids, ref.ids)
+        np.testing.assert_array_equal(got.dists, ref.dists)
+
+
+def test_prefix_order_filtered_sequential_matches_oracle(monkeypatch):
+    """Sequential filtered search over prefix orders: results and counters equal the
+    reference cascade fed the same predictions (host callables, fp64)."""
+    from paper_2502_01836_b200 import search_engine
+
+    monkeypatch.setenv("LF_FULL_ORDER", "0")
+    data, t = _prefix_tree()
+    rng = np.random.default_rng(5)
+    leaves = [int(l) for l in t.leaf_ids]
+    preds = {l: (lambda q, v=float(rng.uniform(0.0, 6.0)): v) for l in leaves[::3]}
+    offs = {l: float(rng.uniform(0.0, 1.0)) for l in preds}
+    ot = lo.build_tree(data, 24)
+    for i, q in enumerate(lo.noisy_queries(data, 8, 0.6, 88)):
+        out = search_engine(t, q, 2, predictors=preds, offsets=offs)
+        o = lo.search(ot, q, 2, predictors=preds, offsets=offs)
+        assert [a for a, _ in out.results] == [a for a, _ in o.results], i
+        assert [getattr(out.stats, s_) for s_ in lo.STAT_KEYS] == [o.stats[s_] for s_ in lo.STAT_KEYS], i
