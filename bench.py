@@ -239,6 +239,11 @@ def peaks() -> tuple:
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def bf16_peak() -> float:
+    p = ROOT / "MEASURED_PEAKS.json"
+    return float(json.loads(p.read_text())["bf16_tflops"]) if p.exists() else 1590.0
+
+
 def tf32_peak() -> float:
     p = ROOT / "MEASURED_PEAKS.json"
     bf16 = json.loads(p.read_text())["bf16_tflops"] if p.exists() else 1590.0
@@ -360,7 +365,7 @@ def run_ours(args, rank, world, device):
     tdg = None
     if args.tdg_queries > 0:
         from paper_2502_01836_b200.synth import queries_device
-        from paper_2502_01836_b200.targets import leaf_min_distances
+        from paper_2502_01836_b200.targets import default_path, leaf_min_distances
 
         Xq = w["di"].X
         gq = torch.cat([queries_device(Xq, args.tdg_queries // 4, nz, args.seed + 77 + i)
@@ -377,10 +382,19 @@ def run_ours(args, rank, world, device):
         t_ms = te0.elapsed_time(te1)
         pairs = gq.shape[0] * tree.n
         flops = 2.0 * pairs * tree.m
+        path = default_path(tree, w["di"])
+        if path == "q8":
+            pk, pk_src = 2.0 * bf16_peak(), "dense int8 = 2 x measured bf16 (MEASURED_PEAKS.json bf16_tflops)"
+            desc = "tcgen05 kind::i8 GEMM over the int8 shadow + exact fp64 re-check (lf_leaf_min_dist_q8)"
+        else:
+            pk, pk_src = tf32_peak(), "dense tf32 = 1/2 of measured bf16 (MEASURED_PEAKS.json bf16_tflops)"
+            desc = "tcgen05 tf32 GEMM + exact fp64 re-check (lf_leaf_min_dist_tc)"
         tdg = {"queries": int(gq.shape[0]), "leaves": tree.n_leaves, "series": tree.n, "ms": t_ms,
                "pairs_per_s": pairs / (t_ms / 1e3), "algorithmic_tflops": flops / (t_ms / 1e3) / 1e12,
-               "tensor_peak_tflops": tf32_peak(), "frac_of_tf32_peak": flops / (t_ms / 1e3) / 1e12 / tf32_peak(),
-               "path": "tcgen05 tf32 GEMM + exact fp64 re-check (lf_leaf_min_dist_tc)",
+               "algorithmic_flops_definition": "2 x queries x series x m (each pair's dot product once)",
+               "tensor_peak_tops": pk, "peak_source": pk_src,
+               "frac_of_peak": flops / (t_ms / 1e3) / 1e12 / pk,
+               "path": desc,
                "exact_zero_check": bool(torch.isfinite(dl).all().item()),
                "reference_cpu_pairs_per_s_per_core": "1.0-1.3e6 (BASELINE.md, collect_targets at C1)"}
         del dl, gq
@@ -541,7 +555,7 @@ def main():
     ap.add_argument("--max-epochs", type=int, default=1000, help="filter training cap (setup speed)")
     ap.add_argument("--sharded", action="store_true",
                     help="use the leaf-sharded round driver even on one GPU (what N>1 runs)")
-    ap.add_argument("--tdg-queries", type=int, default=2000,
+    ap.add_argument("--tdg-queries", type=int, default=10000,
                     help="queries for the training-data-generation measurement (0 = skip)")
     ap.add_argument("--ncu", action="store_true",
                     help="bracket the timed steps with cudaProfilerStart/Stop (ncu --profile-from-start off)")

@@ -202,6 +202,20 @@ int lf_local_min_dist_tc(const float* d_queries, const lf_index* idx, const int6
                          const int32_t* h_group_leaf, int32_t n_groups, double* d_dl, void* stream);
 
 /*
+ * Same two calls on the INT8 tensor cores (tcgen05.mma.kind::i8) over the
+ * collection's int8 shadow (lf_quantize_rows; m in {128, 256}): exact int32 code
+ * dot products give a rigorous interval for every (query, row) distance, and only
+ * rows that can still be a leaf minimum are re-checked EXACTLY in fp64 from the
+ * fp32 rows -- results are the exact fp64 direct-form minima (same terms as
+ * lf_leaf_min_dist, another summation order, so equal to ~1 ulp).
+ */
+int lf_leaf_min_dist_q8(const float* d_queries, int64_t Q, const lf_index* idx,
+                        const int32_t* h_leaf_sel, int32_t S, double* d_dl, int64_t ldd,
+                        void* stream);
+int lf_local_min_dist_q8(const float* d_queries, const lf_index* idx, const int64_t* h_qptr,
+                         const int32_t* h_group_leaf, int32_t n_groups, double* d_dl, void* stream);
+
+/*
  * Full distance matrix between queries and an arbitrary row block
  * (series.batch_distances, series.py:127-139). d_block [B][m], out [Q][B].
  */

@@ -95,6 +95,8 @@ SIGNATURES = {
     "lf_batch_distances": (C.c_int, [_P, _I64, _P, _I64, _I32, _P, _P]),
     "lf_leaf_min_dist_tc": (C.c_int, [_P, _I64, C.POINTER(LfIndex), _P, _I32, _P, _I64, _P]),
     "lf_local_min_dist_tc": (C.c_int, [_P, C.POINTER(LfIndex), _P, _P, _I32, _P, _P]),
+    "lf_leaf_min_dist_q8": (C.c_int, [_P, _I64, C.POINTER(LfIndex), _P, _I32, _P, _I64, _P]),
+    "lf_local_min_dist_q8": (C.c_int, [_P, C.POINTER(LfIndex), _P, _P, _I32, _P, _P]),
     "lf_tree_build": (_P, [_P, _I64, _I32, _I32, _I64, _I32]),
     "lf_tree_info": (C.c_int, [_P, C.POINTER(_I32), C.POINTER(_I32)]),
     "lf_tree_export": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),

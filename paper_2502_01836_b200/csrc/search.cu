@@ -21,6 +21,7 @@
 
 #include "bounds.cuh"
 #include "common.cuh"
+#include "tc.cuh"
 
 namespace lf {
 
@@ -860,39 +861,6 @@ __device__ __forceinline__ void q8_bulk(void* dst, const void* src, uint32_t byt
 }
 __device__ __forceinline__ void q8_cons_sync() { asm volatile("bar.sync 1, %0;" ::"n"(Q8_CONS) : "memory"); }
 
-// Query codes, quantised once per batch exactly like the rows (quantize.cu):
-// codes [Q][MP] (zero-padded to MP = 256-multiple), meta [Q] = {scale, qq, err, 0}.
-__global__ void quantize_queries_kernel(const float* __restrict__ queries, int64_t Q, int M, int MP,
-                                        int8_t* __restrict__ qc, float4* __restrict__ qm) {
-    const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (q >= Q) return;
-    const float* x = queries + q * M;
-    float mx = 0.f;
-    for (int i = lane; i < M; i += 32) mx = fmaxf(mx, fabsf(x[i]));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const float sq = mx > 0.f ? mx / 127.f : 1.f;
-    int qq = 0;
-    double err = 0.0;
-    for (int i = lane; i < MP; i += 32) {
-        int c = 0;
-        if (i < M) {
-            c = (int)fminf(fmaxf(rintf(x[i] / sq), -127.f), 127.f);
-            const double e = (double)sq * (double)c - (double)x[i];
-            err = __fma_rn(e, e, err);
-        }
-        qc[q * MP + i] = (int8_t)c;
-        qq += c * c;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        qq += __shfl_xor_sync(0xffffffffu, qq, o);
-        err += __shfl_xor_sync(0xffffffffu, err, o);
-    }
-    if (lane == 0) qm[q] = make_float4(sq, (float)qq, __double2float_ru(sqrt(err) * (1.0 + 1e-9) + 1e-30), 0.f);
-}
-
 template <int NCH>
 __global__ void __launch_bounds__(Q8_THREADS, 2) scan_q8_kernel(RoundState s, lf_index idx,
                                                                 const float* __restrict__ queries,
@@ -1395,9 +1363,8 @@ static int session_begin(lf_session* ss) {
         const int MP = (idx.m + 255) / 256 * 256;
         LF_CUDA(ss->qc8.alloc((size_t)Q * MP, st));
         LF_CUDA(ss->qm8.alloc(sizeof(float4) * Q, st));
-        quantize_queries_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(
-            ss->d_q, Q, idx.m, MP, ss->qc8.as<int8_t>(), ss->qm8.as<float4>());
-        LF_CUDA(cudaGetLastError());
+        int rq = quantize_queries(ss->d_q, Q, idx.m, MP, ss->qc8.as<int8_t>(), ss->qm8.as<float4>(), st);
+        if (rq) return rq;
         ++ss->kernels;
     }
     if (ss->prof) LF_CUDA(cudaEventRecord(ss->ev[1], st));

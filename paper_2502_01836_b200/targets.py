@@ -77,15 +77,24 @@ def tc_ok(m: int) -> bool:
     return m % 32 == 0 and 32 <= m <= 256
 
 
+def default_path(t, di) -> str:
+    """int8 tensor cores over the int8 shadow when it exists (m in {128, 256}), else
+    tf32 tensor cores (m in {32, ..., 256}), else fp64 CUDA cores."""
+    if getattr(di, "X8", None) is not None and t.m in (128, 256):
+        return "q8"
+    return "tc" if tc_ok(t.m) else "simt"
+
+
 def leaf_min_distances(index, queries, leaf_slots, path: str | None = None) -> "torch.Tensor":
     """Device fp64 [Q, S]: exact min distance from each query to each leaf slot.
 
-    path "tc" (default when m allows): lf_leaf_min_dist_tc; "simt": lf_leaf_min_dist
-    (fp64 CUDA cores).  Both return the same bits."""
+    path "q8" (default when the int8 shadow exists): lf_leaf_min_dist_q8; "tc":
+    lf_leaf_min_dist_tc (tf32); "simt": lf_leaf_min_dist (fp64 CUDA cores).  All
+    return the exact fp64 minima (to ~1 ulp: different summation orders)."""
     torch = _lib.require_cuda()
     t = as_tree(index)
     di = t.device()
-    path = path or ("tc" if tc_ok(t.m) else "simt")
+    path = path or default_path(t, di)
     q = queries if isinstance(queries, torch.Tensor) else torch.from_numpy(
         np.ascontiguousarray(np.atleast_2d(queries), dtype=np.float32))
     q = q.to(device=di.device, dtype=torch.float32).contiguous()
@@ -93,10 +102,10 @@ def leaf_min_distances(index, queries, leaf_slots, path: str | None = None) -> "
     Q, S = q.shape[0], sel.shape[0]
     out = torch.empty((Q, S), dtype=torch.float64, device=di.device)
     st = di.struct(None)
-    if path == "tc" and Q and S:
+    if path in ("tc", "q8") and Q and S:
         hsel = np.ascontiguousarray(np.asarray(leaf_slots, dtype=np.int32))
-        _lib.check(_lib.lib().lf_leaf_min_dist_tc(q.data_ptr(), Q, st, _lib.ptr(hsel), S, out.data_ptr(), S,
-                                                  _lib.stream_ptr()))
+        fn = _lib.lib().lf_leaf_min_dist_q8 if path == "q8" else _lib.lib().lf_leaf_min_dist_tc
+        _lib.check(fn(q.data_ptr(), Q, st, _lib.ptr(hsel), S, out.data_ptr(), S, _lib.stream_ptr()))
         return out
     for s0 in range(0, S, 65535):
         s1 = min(S, s0 + 65535)
@@ -221,8 +230,9 @@ def local_targets_all(index, queries_by_leaf: dict, path: str | None = None) -> 
     torch = _lib.require_cuda()
     t = as_tree(index)
     di = t.device()
-    path = path or ("tc" if tc_ok(t.m) else "simt")
-    fn = _lib.lib().lf_local_min_dist_tc if path == "tc" else _lib.lib().lf_local_min_dist
+    path = path or default_path(t, di)
+    fn = {"q8": _lib.lib().lf_local_min_dist_q8, "tc": _lib.lib().lf_local_min_dist_tc}.get(
+        path, _lib.lib().lf_local_min_dist)
     leaves = list(queries_by_leaf)
     out = {}
     for g0 in range(0, len(leaves), 65535):
