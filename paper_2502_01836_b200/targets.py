@@ -20,6 +20,7 @@ import numpy as np
 
 from . import _lib
 from .engine import as_tree
+from .index import shard_leaf_ranges
 
 
 @dataclass
@@ -85,15 +86,16 @@ def default_path(t, di) -> str:
     return "tc" if tc_ok(t.m) else "simt"
 
 
-def leaf_min_distances(index, queries, leaf_slots, path: str | None = None) -> "torch.Tensor":
+def leaf_min_distances(index, queries, leaf_slots, path: str | None = None, dindex=None) -> "torch.Tensor":
     """Device fp64 [Q, S]: exact min distance from each query to each leaf slot.
 
     path "q8" (default when the int8 shadow exists): lf_leaf_min_dist_q8; "tc":
     lf_leaf_min_dist_tc (tf32); "simt": lf_leaf_min_dist (fp64 CUDA cores).  All
-    return the exact fp64 minima (to ~1 ulp: different summation orders)."""
+    return the exact fp64 minima (to ~1 ulp: different summation orders).
+    dindex: a DeviceIndex (e.g. a leaf shard) whose slots `leaf_slots` refer to."""
     torch = _lib.require_cuda()
     t = as_tree(index)
-    di = t.device()
+    di = dindex if dindex is not None else t.device()
     path = path or default_path(t, di)
     q = queries if isinstance(queries, torch.Tensor) else torch.from_numpy(
         np.ascontiguousarray(np.atleast_2d(queries), dtype=np.float32))
@@ -115,6 +117,35 @@ def leaf_min_distances(index, queries, leaf_slots, path: str | None = None) -> "
                 q[q0:q1].data_ptr(), q1 - q0, st, sel[s0:s1].data_ptr(), s1 - s0,
                 out[q0:q1, s0:s1].data_ptr(), S, _lib.stream_ptr()))
     return out
+
+
+def sharded_leaf_min_distances(index, queries, rank: int, world: int, *, gather: bool = True, group=None,
+                               path: str | None = None):
+    """Training-data generation sharded like the search: this rank
+    computes the min distances to ITS leaf shard only (contiguous leaves balanced by
+    series count, queries replicated); with gather=True the columns of every rank are
+    all-gathered into the full [Q, n_leaves] matrix (leaf slots in ascending node id).
+    Returns (local [Q, L_r], full or None, (a, b) = this rank's leaf-slot range)."""
+    torch = _lib.require_cuda()
+    import torch.distributed as dist
+
+    t = as_tree(index)
+    di = t.shard(rank, world)
+    a, b = di.leaf_range
+    local = leaf_min_distances(t, queries, list(range(b - a)), path=path, dindex=di)
+    if not gather:
+        return local, None, (a, b)
+    if world == 1:
+        return local, local, (a, b)
+    sizes = t.size[t.leaf_ids]
+    ranges = shard_leaf_ranges(sizes, world)
+    width = max(r1 - r0 for r0, r1 in ranges)
+    pad = torch.full((local.shape[0], width), float("inf"), dtype=local.dtype, device=local.device)
+    pad[:, :b - a] = local
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    full = torch.cat([parts[r][:, :r1 - r0] for r, (r0, r1) in enumerate(ranges)], dim=1)
+    return local, full, (a, b)
 
 
 def leaf_bounds(index, queries, mode: int = 1):

@@ -218,3 +218,27 @@ def test_mindist_q8_exact(m, cap):
     tb = local_targets_all(t, qs, path="simt")
     for l in lids:
         np.testing.assert_allclose(ta[l][0], tb[l][0], rtol=1e-13, atol=0)
+
+
+def test_sharded_tdg_columns_concatenate():
+    """Training-data generation on leaf shards: the ranks' local column blocks, in
+    rank order, are exactly the unsharded [Q, n_leaves] min-distance matrix."""
+    import torch
+    from paper_2502_01836_b200 import build_index
+    from paper_2502_01836_b200.targets import leaf_min_distances, sharded_leaf_min_distances
+
+    data = lo.randwalk(15000, 128, 17)
+    t = build_index(data, 400)
+    Q = np.concatenate([lo.noisy_queries(data, 100, 0.3, 8), data[5:9]])
+    full = leaf_min_distances(t, Q, list(range(t.n_leaves))).cpu().numpy()
+    for world in (2, 3):
+        parts, prev = [], 0
+        for r in range(world):
+            loc, _, (a, b) = sharded_leaf_min_distances(t, Q, r, world, gather=False)
+            assert a == prev and loc.shape == (Q.shape[0], b - a)
+            parts.append(loc.cpu().numpy())
+            prev = b
+        assert prev == t.n_leaves
+        np.testing.assert_array_equal(np.concatenate(parts, axis=1), full)
+    _, g1, _ = sharded_leaf_min_distances(t, Q, 0, 1)
+    np.testing.assert_array_equal(g1.cpu().numpy(), full)
