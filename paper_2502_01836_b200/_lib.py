@@ -37,6 +37,8 @@ class LfIndex(C.Structure):
         ("d_leaf_filter", C.c_void_p),
         ("d_X8", C.c_void_p),
         ("d_qmeta", C.c_void_p),
+        ("d_X8b", C.c_void_p),
+        ("d_qmeta2", C.c_void_p),
     ]
 
 
@@ -105,6 +107,7 @@ SIGNATURES = {
     "lf_tree_build_from_summaries": (_P, [_P, _I64, _I32, _I64]),
     "lf_paa_device": (C.c_int, [_P, _I64, _I32, _I32, _P, _P]),
     "lf_quantize_rows": (C.c_int, [_P, _I64, _I32, _P, _P, _P]),
+    "lf_quantize_rows2": (C.c_int, [_P, _I64, _I32, _P, _P, _P, _P, _P]),
 }
 
 _lib = None

@@ -195,8 +195,9 @@ def test_mindist_tc_bit_identical(m, cap):
         np.testing.assert_allclose(ta[l][0], tb[l][0], rtol=1e-13, atol=0)
 
 
+@pytest.mark.parametrize("path", ["q8", "q82"])
 @pytest.mark.parametrize("m,cap", [(128, 300), (256, 700), (256, 3000)])
-def test_mindist_q8_exact(m, cap):
+def test_mindist_q8_exact(m, cap, path):
     """int8 tensor-core bound + exact fp64 re-check == fp64 SIMT kernel (rel 1e-13),
     with ragged leaves (partial 256-row chunks), partial 128-query tiles, member
     queries (exact zeros), far queries and the local (grouped) variant."""
@@ -208,13 +209,13 @@ def test_mindist_q8_exact(m, cap):
     assert t.device().X8 is not None
     Q = np.concatenate([lo.noisy_queries(data, 150, 0.2, 5), lo.noisy_queries(data, 40, 2.0, 6), data[:37]])
     slots = list(range(t.n_leaves))
-    a = leaf_min_distances(t, Q, slots, path="q8").cpu().numpy()
+    a = leaf_min_distances(t, Q, slots, path=path).cpu().numpy()
     b = leaf_min_distances(t, Q, slots, path="simt").cpu().numpy()
     np.testing.assert_allclose(a, b, rtol=1e-13, atol=0)
     assert (a[190:].min(axis=1) == 0.0).all()
     lids = [int(l) for l in t.leaf_ids[:6]]
     qs = {l: lo.noisy_queries(data, 130 + l % 3, 0.3, l) for l in lids}
-    ta = local_targets_all(t, qs, path="q8")
+    ta = local_targets_all(t, qs, path=path)
     tb = local_targets_all(t, qs, path="simt")
     for l in lids:
         np.testing.assert_allclose(ta[l][0], tb[l][0], rtol=1e-13, atol=0)

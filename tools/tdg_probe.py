@@ -13,7 +13,7 @@ from paper_2502_01836_b200.targets import leaf_min_distances
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 2_000_000
 nq = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
-paths = sys.argv[3].split(",") if len(sys.argv) > 3 else ["q8", "tc", "simt"]
+paths = sys.argv[3].split(",") if len(sys.argv) > 3 else ["q8", "q82", "tc", "simt"]
 X = randwalk_device(n, 256, 3)
 t = build_index_device(X, 10000)
 t.device()
@@ -23,13 +23,13 @@ ref = None
 for path in paths:
     leaf_min_distances(t, Q[:128], slots, path=path)
     torch.cuda.synchronize()
-    if path == "q8":
+    if path.startswith("q8"):
         torch.cuda.cudart().cudaProfilerStart()
     t0 = time.perf_counter()
     out = leaf_min_distances(t, Q, slots, path=path)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    if path == "q8":
+    if path.startswith("q8"):
         torch.cuda.cudart().cudaProfilerStop()
     if ref is None:
         ref = out.clone()
