@@ -275,10 +275,10 @@ def run_ours(args, rank, world, device):
 
     if world == 1 and not args.sharded:
         def step(profile=None):
-            return search_queries(eidx, Q, 1, target=args.target, copy_out=False, profile=profile)
+            return search_queries(eidx, Q, 1, target=args.target, copy_out=False, profile=profile, lazy=args.lazy)
 
         def checked(queries):
-            return search_queries(eidx, queries, 1, target=args.target)
+            return search_queries(eidx, queries, 1, target=args.target, lazy=args.lazy)
     else:
         # leaf-sharded: this rank's leaves, rows and filters; one MIN-allreduce per round
         from paper_2502_01836_b200.filters import FilterPack
@@ -292,10 +292,11 @@ def run_ours(args, rank, world, device):
 
         def step(profile=None):
             return search_sharded(tree, Q, 1, rank=rank, world=world, pack=lpack, offsets=loffs,
-                                  copy_out=False, profile=profile)
+                                  copy_out=False, profile=profile, lazy=args.lazy)
 
         def checked(queries):
-            return search_sharded(tree, queries, 1, rank=rank, world=world, pack=lpack, offsets=loffs)
+            return search_sharded(tree, queries, 1, rank=rank, world=world, pack=lpack, offsets=loffs,
+                                  lazy=args.lazy)
 
     for _ in range(args.warmup):
         step()
@@ -333,7 +334,7 @@ def run_ours(args, rank, world, device):
     if args.ncu:
         torch.cuda.cudart().cudaProfilerStart()
     scan_ms, scan_launches, kernels = 0.0, 0, 0
-    ea_rows, ea_surv, refills = 0.0, 0.0, 0.0
+    ea_rows, ea_surv, refills, pred_ms, lazy_pairs, pred_steps = 0.0, 0.0, 0.0, 0.0, 0.0, 0.0
     with ClockSampler(torch.cuda.current_device()) as clk:
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
@@ -345,7 +346,10 @@ def run_ours(args, rank, world, device):
             ea_rows += prof[8]
             ea_surv += prof[9]
             refills += prof[7]
-            kernels += int(prof[5]) + 1          # + the filter-inference launch
+            pred_ms += prof[10]
+            lazy_pairs += prof[11]
+            pred_steps += prof[12]
+            kernels += int(prof[5]) + (0 if args.lazy else 1)    # + the dense filter pass
         ev1.record(stream)
         torch.cuda.synchronize()
     if args.ncu:
@@ -483,14 +487,24 @@ def run_ours(args, rank, world, device):
             "reference_equivalent_GBps": ref_equiv,
             "reference_equivalent_definition": "series_scanned x m x 4 B (every scanned series read in fp32) / scan time",
             "scan_ms_per_step": scan_ms / args.steps, "scan_launches_per_step": scan_launches / args.steps,
-            "phase_ms_last_step": {"filter_inference": filter_ms, "bounds+sort": prof[0], "plan": prof[1],
+            "phase_ms_last_step": {"filter_inference": prof[10] if args.lazy else filter_ms,
+                                   "bounds+sort": prof[0], "plan": prof[1],
                                    "scan": prof[2], "merge": prof[3], "lf_search_total": prof[6]},
         },
-        "filter_kernel": {
-            "path": eidx.pack.path, "bound": "tensor", "ms": filter_ms, "achieved": filter_tflops,
-            "unit": "TFLOP/s", "peak": tf32_peak(), "frac": filter_tflops / tf32_peak(),
-            "flops_per_launch": 2.0 * nQ * F * tree.m * (tree.m + 1),
-            "peak_source": "dense tf32 = 1/2 of measured bf16 (MEASURED_PEAKS.json bf16_tflops)",
+        "filter_inference": {
+            "mode": ("lazy, inside lf_search: windows of the reachable (query, leaf) pairs predicted by a "
+                     "tcgen05 tf32 pair GEMM, bit-identical to the dense kernel") if args.lazy else
+                    "dense: one tcgen05 tf32 pass over every (query, filter) pair before lf_search",
+            "pairs_per_step": lazy_pairs / args.steps, "dense_pairs_per_step": nQ * F,
+            "ms_per_step": pred_ms / args.steps, "passes_per_step": pred_steps / args.steps,
+            "pair_flops_per_step": 2.0 * (lazy_pairs / args.steps) * tree.m * (tree.m + 1),
+            "dense_kernel": {
+                "path": eidx.pack.path, "bound": "tensor", "ms": filter_ms, "achieved": filter_tflops,
+                "unit": "TFLOP/s", "peak": tf32_peak(), "frac": filter_tflops / tf32_peak(),
+                "flops_per_launch": 2.0 * nQ * F * tree.m * (tree.m + 1),
+                "peak_source": "dense tf32 = 1/2 of measured bf16 (MEASURED_PEAKS.json bf16_tflops)",
+                "note": "every (query, filter) pair; used for calibration, timed here for reference",
+            },
         },
         "setup_s": w["setup_s"],
         "train_data_gen": tdg,
@@ -566,6 +580,8 @@ def main():
                     help="use the leaf-sharded round driver even on one GPU (what N>1 runs)")
     ap.add_argument("--tdg-queries", type=int, default=10000,
                     help="queries for the training-data-generation measurement (0 = skip)")
+    ap.add_argument("--lazy", action="store_true",
+                    help="lazy filter inference inside lf_search instead of the dense pass")
     ap.add_argument("--ncu", action="store_true",
                     help="bracket the timed steps with cudaProfilerStart/Stop (ncu --profile-from-start off)")
     args = ap.parse_args()

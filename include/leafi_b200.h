@@ -79,9 +79,19 @@ typedef struct lf_search_opts {
                                     tracing; needs m % 64 == 0) */
     double* h_profile;           /* optional host array[LF_N_PROF]: CUDA-event times (ms)
                                     accumulated per phase, see LF_PROF_* */
+    /* Lazy filter inference (used when d_pred and d_pred_f64 are NULL and d_W1T is
+       set): the filter pack itself -- W1T [F][m][m] (hidden-major, as for
+       lf_filter_predict_tc), b1 [F][m], W2 [F][m], b2 [F], m in {32, ..., 256}.  After
+       the first round, predictions are computed on the tensor cores only for the
+       (query, leaf) pairs the walk can still reach (leaves with lb <= bsf * f),
+       bit-identical to lf_filter_predict_tc's. */
+    const float* d_W1T;
+    const float* d_b1;
+    const float* d_W2;
+    const float* d_b2;
 } lf_search_opts;
 
-#define LF_N_PROF 10
+#define LF_N_PROF 13
 #define LF_PROF_BOUNDS_MS 0      /* segment means + node bounds + visit-order sort */
 #define LF_PROF_PLAN_MS 1        /* plan + chunk offsets, all rounds */
 #define LF_PROF_SCAN_MS 2        /* leaf-scan kernel, all rounds */
@@ -92,6 +102,9 @@ typedef struct lf_search_opts {
 #define LF_PROF_REFILLS 7        /* queries whose sorted visit-order prefix was completed */
 #define LF_PROF_EA_ROWS 8        /* rows tested by the early-abandon scan */
 #define LF_PROF_EA_SURVIVORS 9   /* rows that survived the first 64-dim test */
+#define LF_PROF_PREDICT_MS 10    /* lazy filter inference (pairs, gather, tensor-core GEMM) */
+#define LF_PROF_PAIRS 11         /* (query, leaf) predictions computed lazily */
+#define LF_PROF_PREDICT_STEPS 12 /* lazy inference passes (one after round 0, then on request) */
 
 /* Optional per-query trace (tree.py:77-83 TraceEntry), capacity n_leaves per query. */
 typedef struct lf_trace {
@@ -170,6 +183,17 @@ int lf_filter_predict(const float* d_queries, int64_t Q, int32_t m,
 int lf_filter_predict_tc(const float* d_queries, int64_t Q, int32_t m,
                          const float* d_W1T, const float* d_b1, const float* d_W2,
                          const float* d_b2, int32_t F, float* d_pred, void* stream);
+
+/*
+ * Predictions for an explicit list of (query, filter) pairs on the tensor cores:
+ * pairs are bucketed by filter, their query rows gathered, and one tcgen05 tile
+ * list evaluates them -- bit-identical to the same pairs of lf_filter_predict_tc.
+ * This is the kernel lf_search uses for lazy inference.  d_out [P] (fp64 of the
+ * fp32 prediction).
+ */
+int lf_filter_predict_pairs_tc(const float* d_queries, int32_t m, const float* d_W1T, const float* d_b1,
+                               const float* d_W2, const float* d_b2, int32_t F, const int32_t* d_pair_q,
+                               const int32_t* d_pair_f, int64_t P, double* d_out, void* stream);
 
 /*
  * Exact query x leaf minimum distance (direct form, fp64 accumulation).

@@ -55,12 +55,16 @@ class LfSearchOpts(C.Structure):
         ("want_trace", C.c_int32),
         ("early_abandon", C.c_int32),
         ("h_profile", C.c_void_p),
+        ("d_W1T", C.c_void_p),
+        ("d_b1", C.c_void_p),
+        ("d_W2", C.c_void_p),
+        ("d_b2", C.c_void_p),
     ]
 
 
-N_PROF = 10
+N_PROF = 13
 PROF_NAMES = ("bounds_ms", "plan_ms", "scan_ms", "merge_ms", "rounds", "kernels", "total_ms", "refills",
-              "ea_rows", "ea_survivors")
+              "ea_rows", "ea_survivors", "predict_ms", "pairs", "predict_steps")
 
 
 class LfTrace(C.Structure):
@@ -92,6 +96,7 @@ SIGNATURES = {
     "lf_search_free": (None, [_P]),
     "lf_filter_predict": (C.c_int, [_P, _I64, _I32, _P, _P, _P, _P, _I32, _P, _P]),
     "lf_filter_predict_tc": (C.c_int, [_P, _I64, _I32, _P, _P, _P, _P, _I32, _P, _P]),
+    "lf_filter_predict_pairs_tc": (C.c_int, [_P, _I32, _P, _P, _P, _P, _I32, _P, _P, _I64, _P, _P]),
     "lf_leaf_min_dist": (C.c_int, [_P, _I64, C.POINTER(LfIndex), _P, _I32, _P, _I64, _P]),
     "lf_local_min_dist": (C.c_int, [_P, C.POINTER(LfIndex), _P, _P, _I32, _P, _P]),
     "lf_batch_distances": (C.c_int, [_P, _I64, _P, _I64, _I32, _P, _P]),

@@ -97,12 +97,16 @@ __device__ inline void put_record(const OrderArgs& o, const lf_index& idx, int64
     const int leaf = idx.d_node_leaf[node];
     int rec = leaf;
     double a = -kInf;
-    if (leaf >= 0 && idx.d_leaf_filter != nullptr && (o.pred != nullptr || o.pred64 != nullptr)) {
+    if (leaf >= 0 && idx.d_leaf_filter != nullptr && (o.pred != nullptr || o.pred64 != nullptr || o.lazy)) {
         const int fs = idx.d_leaf_filter[leaf];
         if (fs >= 0) {
             rec |= LF_REC_HASF;
-            const double pv = o.pred64 != nullptr ? o.pred64[q * o.F + fs] : (double)o.pred[q * o.F + fs];
-            a = pv - o.offset[fs];
+            if (o.lazy) {
+                a = __longlong_as_double(0x7ff8000000000000LL);    // filled by the lazy inference
+            } else {
+                const double pv = o.pred64 != nullptr ? o.pred64[q * o.F + fs] : (double)o.pred[q * o.F + fs];
+                a = pv - o.offset[fs];
+            }
         }
     }
     o.leafo[at] = rec;

@@ -25,6 +25,7 @@ struct OrderArgs {
     const double* offset;        // [F]
     int F;
     int* only;                   // refill: queries with only[q] != 0 (cleared when done); NULL = all
+    int lazy;                    // predictions computed later (lazy inference): flag filters, adj = NaN
 };
 // prefix = true: sort only the first ~PF_K entries of each order (olen[q] < n_nodes
 // possible); the plan asks for the rest with refill_order when it gets there.

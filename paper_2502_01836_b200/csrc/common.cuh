@@ -96,4 +96,10 @@ __device__ inline bool pair_less(double da, long long ia, double db, long long i
 
 constexpr double kInf = __builtin_huge_val();
 
+// Lazy filter inference on the tensor cores (filters_tc.cu): predictions for gathered
+// query rows bucketed by filter, written as pred - offset into visit-order records.
+int filter_pairs_tc(const float* d_rows, int64_t P, int m, const float* d_W1T, const float* d_b1,
+                    const float* d_W2, const float* d_b2, int F, const int4* d_tiles, const int* d_ntiles,
+                    const int2* d_dst, const double* d_offset, double* d_adj, int Nn, cudaStream_t st);
+
 }  // namespace lf

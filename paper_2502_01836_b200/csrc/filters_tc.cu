@@ -103,10 +103,26 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
           "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                                               \
         : "r"(taddr))
 
+// PAIRS = false: every (query, filter) pair, tiles (f, 128-query block), dense pred [Q][F].
+// PAIRS = true : a device tile list (f, first row, rows) over GATHERED query rows
+//                (one row per (query, visit-order position) pair, grouped by filter);
+//                the epilogue writes adj[q][pos] = pred - offset[f] straight into the
+//                search's visit-order records.  Same MMA K order and epilogue order
+//                as the dense kernel, so every prediction is bit-identical to it.
+struct PairArgs {
+    const int4* tiles;           // (filter, first gathered row, rows, 0)
+    const int* n_tiles;          // device count
+    const int2* dst;             // per gathered row: (query, visit-order position)
+    const double* offset;        // [F]
+    double* adj;                 // [Q][Nn]
+    int Nn;
+};
+
+template <bool PAIRS>
 __global__ void __launch_bounds__(THREADS, 1)
 filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
                  int64_t Q, int m, int F, const float* __restrict__ b1, const float* __restrict__ W2,
-                 const float* __restrict__ b2, float* __restrict__ pred) {
+                 const float* __restrict__ b2, float* __restrict__ pred, PairArgs pa) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -117,7 +133,7 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_mb = (int)((Q + BM - 1) / BM);
-    const int64_t n_tiles = (int64_t)F * n_mb;
+    const int64_t n_tiles = PAIRS ? (int64_t)*pa.n_tiles : (int64_t)F * n_mb;
     const int n_kb = m / BK;
     const uint32_t b_bytes = (uint32_t)m * BK * 4;
 
@@ -143,13 +159,21 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
             int stage = 0;
             uint32_t phase = 0;
             for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-                const int f = (int)(t / n_mb), mb = (int)(t % n_mb);
+                int f, row0;
+                if (PAIRS) {
+                    const int4 tl = pa.tiles[t];
+                    f = tl.x;
+                    row0 = tl.y;
+                } else {
+                    f = (int)(t / n_mb);
+                    row0 = (int)(t % n_mb) * BM;
+                }
                 for (int kb = 0; kb < n_kb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * STAGE_BYTES;
                     uint8_t* sb = sa + A_BYTES;
                     mbar_expect_tx(&full[stage], A_BYTES + b_bytes);
-                    tma_2d(&map_x, &full[stage], sa, kb * BK, mb * BM);
+                    tma_2d(&map_x, &full[stage], sa, kb * BK, row0);
                     tma_2d(&map_w, &full[stage], sb, kb * BK, f * m);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -188,7 +212,17 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-            const int f = (int)(t / n_mb), mb = (int)(t % n_mb);
+            int f, row0, nrows;
+            if (PAIRS) {
+                const int4 tl = pa.tiles[t];
+                f = tl.x;
+                row0 = tl.y;
+                nrows = tl.z;
+            } else {
+                f = (int)(t / n_mb);
+                row0 = (int)(t % n_mb) * BM;
+                nrows = BM;
+            }
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const float* b1f = b1 + (int64_t)f * m;
@@ -208,8 +242,16 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
-            const int64_t q = (int64_t)mb * BM + row;
-            if (q < Q) pred[q * F + f] = __fadd_rn(part, b2[f]);
+            if (PAIRS) {
+                if (row < nrows) {
+                    const int2 d = pa.dst[row0 + row];
+                    const double pv = (double)__fadd_rn(part, b2[f]);
+                    pa.adj[(int64_t)d.x * pa.Nn + d.y] = pa.offset != nullptr ? pv - pa.offset[f] : pv;
+                }
+            } else {
+                const int64_t q = (int64_t)row0 + row;
+                if (q < Q) pred[q * F + f] = __fadd_rn(part, b2[f]);
+            }
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
     }
@@ -266,14 +308,95 @@ extern "C" int lf_filter_predict_tc(const float* d_queries, int64_t Q, int32_t m
     if (rc) return rc;
     static bool attr_set = false;
     if (!attr_set) {
-        LF_CUDA(cudaFuncSetAttribute(tc::filter_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        LF_CUDA(cudaFuncSetAttribute(tc::filter_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      tc::SMEM_BYTES));
         attr_set = true;
     }
     const int64_t tiles = (int64_t)F * ((Q + tc::BM - 1) / tc::BM);
     const int grid = (int)std::min<int64_t>(tiles, sm_count());
-    tc::filter_tc_kernel<<<grid, tc::THREADS, tc::SMEM_BYTES, as_stream(stream)>>>(mx, mw, Q, m, F, d_b1, d_W2,
-                                                                                    d_b2, d_pred);
+    tc::filter_tc_kernel<false><<<grid, tc::THREADS, tc::SMEM_BYTES, as_stream(stream)>>>(
+        mx, mw, Q, m, F, d_b1, d_W2, d_b2, d_pred, tc::PairArgs{});
     LF_CUDA(cudaGetLastError());
     return LF_OK;
+}
+
+namespace lf {
+// Predictions for gathered (query, position) rows grouped by filter (lazy inference
+// inside lf_search): d_rows [P][m], tile list and count on the device.
+int filter_pairs_tc(const float* d_rows, int64_t P, int m, const float* d_W1T, const float* d_b1,
+                    const float* d_W2, const float* d_b2, int F, const int4* d_tiles, const int* d_ntiles,
+                    const int2* d_dst, const double* d_offset, double* d_adj, int Nn, cudaStream_t st) {
+    if (P == 0 || F == 0) return LF_OK;
+    CUtensorMap mx, mw;
+    int rc = tc::make_map(&mx, d_rows, P, m, tc::BM);
+    if (rc) return rc;
+    rc = tc::make_map(&mw, d_W1T, (int64_t)F * m, m, m);
+    if (rc) return rc;
+    static bool attr_set = false;
+    if (!attr_set) {
+        LF_CUDA(cudaFuncSetAttribute(tc::filter_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     tc::SMEM_BYTES));
+        attr_set = true;
+    }
+    tc::PairArgs pa{d_tiles, d_ntiles, d_dst, d_offset, d_adj, Nn};
+    tc::filter_tc_kernel<true><<<sm_count(), tc::THREADS, tc::SMEM_BYTES, st>>>(mx, mw, P, m, F, d_b1, d_W2, d_b2,
+                                                                               nullptr, pa);
+    LF_CUDA(cudaGetLastError());
+    return LF_OK;
+}
+}  // namespace lf
+
+// ---------------------------------------------------------------------------
+// Explicit (query, filter) pair list: bucket by filter, gather, pair GEMM.
+namespace lf {
+namespace tc {
+__global__ void pair_hist_kernel(const int32_t* __restrict__ pf, int64_t P, int* __restrict__ hist) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < P) atomicAdd(&hist[pf[i]], 1);
+}
+__global__ void pair_bucket_kernel(const float* __restrict__ queries, int m, const int32_t* __restrict__ pq,
+                                   const int32_t* __restrict__ pf, int64_t P, int* __restrict__ fcur,
+                                   int2* __restrict__ dst, float* __restrict__ rows) {
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= P) return;
+    int slot = 0;
+    if (lane == 0) {
+        slot = atomicAdd(&fcur[pf[i]], 1);
+        dst[slot] = make_int2((int)i, 0);
+    }
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    const float* src = queries + (int64_t)pq[i] * m;
+    for (int c = lane; c < m; c += 32) rows[(int64_t)slot * m + c] = src[c];
+}
+}  // namespace tc
+int pair_tiles(const int* d_hist, int F, int* d_fcur, int4* d_tiles, int* d_ntiles, cudaStream_t st);
+}  // namespace lf
+
+extern "C" int lf_filter_predict_pairs_tc(const float* d_queries, int32_t m, const float* d_W1T, const float* d_b1,
+                                          const float* d_W2, const float* d_b2, int32_t F, const int32_t* d_pair_q,
+                                          const int32_t* d_pair_f, int64_t P, double* d_out, void* stream) {
+    using namespace lf;
+    LF_REQUIRE(m >= 32 && m <= 256 && m % 32 == 0, "tensor-core filter path needs m in {32, 64, ..., 256}");
+    LF_REQUIRE(P >= 0 && F >= 1, "bad sizes");
+    if (P == 0) return LF_OK;
+    cudaStream_t st = as_stream(stream);
+    Scratch hist, fcur, tiles, ntiles, dst, rows;
+    LF_CUDA(hist.alloc(sizeof(int) * F, st));
+    LF_CUDA(fcur.alloc(sizeof(int) * F, st));
+    LF_CUDA(tiles.alloc(sizeof(int4) * (size_t)(P / 128 + F + 1), st));
+    LF_CUDA(ntiles.alloc(sizeof(int), st));
+    LF_CUDA(dst.alloc(sizeof(int2) * (size_t)P, st));
+    LF_CUDA(rows.alloc(sizeof(float) * (size_t)P * m, st));
+    LF_CUDA(cudaMemsetAsync(hist.p, 0, sizeof(int) * F, st));
+    tc::pair_hist_kernel<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(d_pair_f, P, hist.as<int>());
+    LF_CUDA(cudaGetLastError());
+    int rc = pair_tiles(hist.as<int>(), F, fcur.as<int>(), tiles.as<int4>(), ntiles.as<int>(), st);
+    if (rc) return rc;
+    tc::pair_bucket_kernel<<<(unsigned)((P * 32 + 255) / 256), 256, 0, st>>>(d_queries, m, d_pair_q, d_pair_f, P,
+                                                                            fcur.as<int>(), dst.as<int2>(),
+                                                                            rows.as<float>());
+    LF_CUDA(cudaGetLastError());
+    return filter_pairs_tc(rows.as<float>(), P, m, d_W1T, d_b1, d_W2, d_b2, F, tiles.as<int4>(), ntiles.as<int>(),
+                           dst.as<int2>(), nullptr, d_out, 1, st);
 }

@@ -41,6 +41,11 @@ struct RoundState {
     const int* olen;             // [Q] valid (sorted) entries of the order
     int* refill;                 // [Q] set when the walk reached olen < Nn
     int* n_refill;               // queries flagged this round (= n_active + 1)
+    int lazy;                    // lazy filter inference: adj valid for positions < pcount[q]
+    const int* pcount;           // [Q]
+    int* preq;                   // [Q] set when the walk stopped at pcount (more predictions needed)
+    int* pwin;                   // [Q] positions the next prediction pass covers (doubles per pass)
+    int* n_predict;              // walks that reached pcount with a finite bsf (= n_active + 2)
     int* cursor;                 // [Q]
     int* done;                   // [Q]
     double* top_d;               // [Q][k]   running top-k (round-start state)
@@ -105,7 +110,9 @@ __global__ void plan_warp_kernel(RoundState s, lf_index idx) {
         const double* lbs = s.lbs + q * Nn;
         const int* lrec = s.leafo + q * Nn;
         const double* adj = s.adj + q * Nn;
-        const int len = s.olen[q];
+        const int olen = s.olen[q];
+        // lazy inference: with a finite bsf the filter rule needs adj, valid below pcount
+        const int len = (s.lazy && thr < kInf) ? min(olen, s.pcount[q]) : olen;
         long long* st = s.stats + q * LF_N_STATS;
         int cur = s.cursor[q];
         bool fin = false, quota_hit = false;
@@ -217,9 +224,14 @@ __global__ void plan_warp_kernel(RoundState s, lf_index idx) {
             if (s.want_trace) s.tr.d_len[q] = tl;
             if (fin) s.done[q] = 1;
             else atomicAdd(s.n_active, 1);
-            if (!fin && !quota_hit && cur >= len) {        // walked off the sorted prefix
-                s.refill[q] = 1;
-                atomicAdd(s.n_refill, 1);
+            if (!fin && !quota_hit && cur >= len) {
+                if (len < olen) {                          // needs predictions further down
+                    s.preq[q] = 1;
+                    atomicAdd(s.n_predict, 1);
+                } else {                                   // walked off the sorted prefix
+                    s.refill[q] = 1;
+                    atomicAdd(s.n_refill, 1);
+                }
             }
         }
     }
@@ -268,6 +280,160 @@ __global__ void expand_tasks_kernel(RoundState s) {
         const int c0 = pre[j], n = pre[j + 1] - c0;
         for (int c = lane; c < n; c += 32) s.tasks[base + c0 + c] = make_int4((int)q, leaf, c, j);
     }
+}
+
+// ------------------------------------------------------- lazy inference ----
+// After a round, a query with a finite bsf can only ever reach the visit-order
+// positions [pcount, pend), pend = the first position whose bound exceeds bsf * f
+// (bsf only decreases).  The leaves with a filter in that range are the (query,
+// leaf) pairs whose prediction the cascade may need (tree.py:277-286 evaluates a
+// subset of exactly these).  pass 1 counts them per filter, a single-CTA scan
+// turns the counts into filter buckets and a 128-row tile list, pass 2 fills the
+// buckets and gathers the query rows, and filter_pairs_tc (tcgen05, the same
+// arithmetic as the dense filter kernel) writes pred - offset into the records.
+constexpr int PRED_WINDOW = 1024;   // visit-order positions of a query's first prediction pass
+
+__global__ void fill_int_kernel(int* p, int64_t n, int v) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+__global__ void pairs_count_kernel(RoundState s, int* pend, int* fhist, unsigned long long* total, lf_index idx,
+                                   int all) {
+    const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (q >= s.Q) return;
+    const int start = s.pcount[q];
+    const double thr = round_bsf(s, q) * s.f;
+    const bool want = all || s.preq[q];
+    __syncwarp();
+    if (lane == 0) s.preq[q] = 0;
+    if (s.done[q] || !(thr < kInf) || !want) {
+        if (lane == 0) pend[q] = start;
+        return;
+    }
+    const int Nn = idx.n_nodes;
+    // a window of the order at a time (doubling per pass): LeaFi's filters stop most
+    // walks long before the bound does (281 of 4,096 leaves visited per query on the
+    // bench workload), so predicting every leaf under the bound would be ~15x the work
+    const int win = s.pwin[q];
+    const int len = min(s.olen[q], start + win);
+    const double* lbs = s.lbs + q * Nn;
+    const int* lrec = s.leafo + q * Nn;
+    int i = start, cnt = 0;
+    bool broke = false;
+    while (i < len) {                                  // 128 positions per pass, loads in flight together
+        double lbv[4];
+        int recv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int k = i + 32 * u + lane;
+            lbv[u] = k < len ? lbs[k] : kInf;
+            recv[u] = k < len ? lrec[k] : -1;
+        }
+        bool stop = false;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (stop) break;
+            const int k = i + 32 * u + lane;
+            const bool valid = k < len;
+            const bool brk = valid && lbv[u] > thr;
+            const unsigned bmask = __ballot_sync(0xffffffffu, brk);
+            const int first = bmask ? __ffs(bmask) - 1 : 32;
+            const int rec = (valid && lane < first) ? recv[u] : -1;
+            const bool has = rec >= 0 && (rec & LF_REC_HASF);
+            if (has) atomicAdd(&fhist[idx.d_leaf_filter[rec & LF_REC_LEAF]], 1);
+            cnt += __popc(__ballot_sync(0xffffffffu, has));
+            if (bmask) { i += 32 * u + first; broke = true; stop = true; }
+        }
+        if (stop) break;
+        i += 128;
+    }
+    if (lane == 0) s.pwin[q] = win * 2;
+    if (lane == 0) {
+        // the break entry itself stays walkable (its bound alone decides), so the walk
+        // can finish there instead of asking for predictions again
+        pend[q] = broke ? i + 1 : min(i, len);
+        if (cnt) atomicAdd(total, (unsigned long long)cnt);
+    }
+}
+
+// Filter buckets (exclusive scan of the per-filter counts) and the tile list
+// (filter, first row, rows <= 128) in one CTA.
+__global__ void pair_tiles_kernel(const int* __restrict__ fhist, int F, int* __restrict__ fcur, int4* __restrict__ tiles,
+                                  int* __restrict__ ntiles) {
+    __shared__ int sp[1024], st[1024];
+    __shared__ int carry_p, carry_t;
+    if (threadIdx.x == 0) { carry_p = 0; carry_t = 0; }
+    __syncthreads();
+    for (int base = 0; base < F; base += blockDim.x) {
+        const int f = base + threadIdx.x;
+        const int h = f < F ? fhist[f] : 0;
+        sp[threadIdx.x] = h;
+        st[threadIdx.x] = (h + 127) / 128;
+        __syncthreads();
+        for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+            const int ap = threadIdx.x >= (unsigned)o ? sp[threadIdx.x - o] : 0;
+            const int at = threadIdx.x >= (unsigned)o ? st[threadIdx.x - o] : 0;
+            __syncthreads();
+            sp[threadIdx.x] += ap;
+            st[threadIdx.x] += at;
+            __syncthreads();
+        }
+        if (f < F) {
+            const int p0 = carry_p + sp[threadIdx.x] - h;
+            const int nt = (h + 127) / 128;
+            const int t0 = carry_t + st[threadIdx.x] - nt;
+            fcur[f] = p0;
+            for (int t = 0; t < nt; ++t) tiles[t0 + t] = make_int4(f, p0 + 128 * t, min(128, h - 128 * t), 0);
+        }
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) { carry_p += sp[threadIdx.x]; carry_t += st[threadIdx.x]; }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *ntiles = carry_t;
+}
+
+int pair_tiles(const int* d_hist, int F, int* d_fcur, int4* d_tiles, int* d_ntiles, cudaStream_t st) {
+    pair_tiles_kernel<<<1, 1024, 0, st>>>(d_hist, F, d_fcur, d_tiles, d_ntiles);
+    LF_CUDA(cudaGetLastError());
+    return LF_OK;
+}
+
+// Bucket the pairs by filter (slot order inside a bucket is irrelevant: every row's
+// prediction depends on that row alone) and gather their query rows.
+__global__ void pairs_fill_kernel(RoundState s, lf_index idx, const float* __restrict__ queries, int m, int* pcount,
+                                  const int* __restrict__ pend, int* fcur, int2* __restrict__ dst,
+                                  float* __restrict__ rows) {
+    const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (q >= s.Q) return;
+    const int start = pcount[q], end = pend[q];
+    const int Nn = idx.n_nodes;
+    const int* lrec = s.leafo + q * Nn;
+    const double* lbs = s.lbs + q * Nn;
+    const double thr = round_bsf(s, q) * s.f;       // same bound as pass 1: skips its break entry
+    for (int i = start; i < end; i += 32) {
+        const int k = i + lane;
+        const int rec = (k < end && lbs[k] <= thr) ? lrec[k] : -1;
+        const bool has = rec >= 0 && (rec & LF_REC_HASF);
+        if (has) {
+            const int slot = atomicAdd(&fcur[idx.d_leaf_filter[rec & LF_REC_LEAF]], 1);
+            dst[slot] = make_int2((int)q, k);
+        }
+    }
+    if (lane == 0) pcount[q] = end;
+}
+
+// Gather the query row of every bucketed pair (warp per pair, 128-bit copies).
+__global__ void pairs_gather_kernel(const float* __restrict__ queries, int m, const int2* __restrict__ dst, int64_t P,
+                                    float* __restrict__ rows) {
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= P) return;
+    const float4* src = reinterpret_cast<const float4*>(queries + (int64_t)dst[i].x * m);
+    float4* out = reinterpret_cast<float4*>(rows + i * m);
+    for (int c = lane; c < m / 4; c += 32) out[c] = __ldg(src + c);
 }
 
 // ---------------------------------------------------------------- scan ----
@@ -1233,8 +1399,12 @@ struct lf_session {
     lf::RoundState s{};
     lf::Scratch qsumm, lb, lbs, order, cursor, done, topd, topi, topn, topd2, topi2, topn2, sel_leaf,
         sel_trace, sel_pre, n_sel, chunk_off, cand_d, cand_i, task_min, n_active, tasks, ea_count, qc8, qm8,
-        leafo, adj, olen, refill;
+        leafo, adj, olen, refill, pcount, pend, preq, pwin, fhist, fcur, ntiles, ptotal;
     lf::OrderArgs oa{};
+    bool lazy = false;               // lazy filter inference (opts.d_W1T instead of predictions)
+    long long pairs = 0;             // predictions computed lazily
+    int predict_steps = 0;
+    double predict_ms = 0.0;
     bool q8 = false;                 // int8-bounded scan (query codes quantised once in begin)
     long long refills = 0;           // queries whose visit order was completed after the prefix
     int* h_active = nullptr;
@@ -1294,13 +1464,28 @@ static int session_begin(lf_session* ss) {
     LF_CUDA(ss->cand_d.alloc(sizeof(double) * max_tasks * s.kc, st));
     LF_CUDA(ss->cand_i.alloc(sizeof(long long) * max_tasks * s.kc, st));
     LF_CUDA(ss->task_min.alloc(sizeof(double) * (s.want_trace ? max_tasks : 1), st));
-    LF_CUDA(ss->n_active.alloc(sizeof(int) * 2, st));   // [active, refill requests]
+    LF_CUDA(ss->n_active.alloc(sizeof(int) * 3, st));   // [active, refill requests, predict requests]
+    ss->lazy = o.d_pred == nullptr && o.d_pred_f64 == nullptr && o.d_W1T != nullptr;
+    if (ss->lazy) {
+        LF_CUDA(ss->pcount.alloc(sizeof(int) * Q, st));
+        LF_CUDA(cudaMemsetAsync(ss->pcount.p, 0, sizeof(int) * Q, st));
+        LF_CUDA(ss->pend.alloc(sizeof(int) * Q, st));
+        LF_CUDA(ss->preq.alloc(sizeof(int) * Q, st));
+        LF_CUDA(cudaMemsetAsync(ss->preq.p, 0, sizeof(int) * Q, st));
+        LF_CUDA(ss->pwin.alloc(sizeof(int) * Q, st));
+        fill_int_kernel<<<(unsigned)((Q + 255) / 256), 256, 0, st>>>(ss->pwin.as<int>(), Q, PRED_WINDOW);
+        LF_CUDA(cudaGetLastError());
+        LF_CUDA(ss->fhist.alloc(sizeof(int) * std::max(1, o.n_filters), st));
+        LF_CUDA(ss->fcur.alloc(sizeof(int) * std::max(1, o.n_filters), st));
+        LF_CUDA(ss->ntiles.alloc(sizeof(int), st));
+        LF_CUDA(ss->ptotal.alloc(sizeof(unsigned long long), st));
+    }
     LF_CUDA(ss->tasks.alloc(sizeof(int4) * max_tasks, st));
     LF_CUDA(ss->ea_count.alloc(sizeof(unsigned long long) * 2, st));
     LF_CUDA(cudaMemsetAsync(ss->ea_count.p, 0, sizeof(unsigned long long) * 2, st));
     {   // one pinned word per host thread; a round reads it right after its own sync
         static thread_local int* pinned = nullptr;
-        if (pinned == nullptr) LF_CUDA(cudaMallocHost(&pinned, sizeof(int) * 2));
+        if (pinned == nullptr) LF_CUDA(cudaMallocHost(&pinned, sizeof(int) * 4));
         ss->h_active = pinned;
     }
 
@@ -1322,6 +1507,7 @@ static int session_begin(lf_session* ss) {
     oa.offset = o.d_offset;
     oa.F = o.n_filters;
     oa.only = nullptr;
+    oa.lazy = ss->lazy ? 1 : 0;
     int rc = bounds_and_order(ss->d_q, Q, idx, ss->qsumm.as<double>(), ss->lb.as<double>(), oa, prefix_orders(),
                               st, &nk);
     if (rc) return rc;
@@ -1334,6 +1520,11 @@ static int session_begin(lf_session* ss) {
     s.olen = ss->olen.as<int>();
     s.refill = ss->refill.as<int>();
     s.n_refill = ss->n_active.as<int>() + 1;
+    s.n_predict = ss->n_active.as<int>() + 2;
+    s.lazy = ss->lazy ? 1 : 0;
+    s.pcount = ss->lazy ? ss->pcount.as<int>() : nullptr;
+    s.preq = ss->lazy ? ss->preq.as<int>() : nullptr;
+    s.pwin = ss->lazy ? ss->pwin.as<int>() : nullptr;
     s.cursor = ss->cursor.as<int>();
     s.done = ss->done.as<int>();
     s.top_d = ss->topd.as<double>();
@@ -1382,6 +1573,65 @@ __global__ void bsf_out_kernel(RoundState s, double* out) {
     if (q < s.Q) out[q] = query_bsf(s, q);
 }
 
+// Lazy filter inference for every query with a finite bsf (see pairs_count_kernel).
+static int predict_step(lf_session* ss) {
+    RoundState& s = ss->s;
+    const lf_index& idx = ss->idx;
+    const lf_search_opts& o = ss->opts;
+    cudaStream_t st = ss->st;
+    const int64_t Q = ss->Q;
+    const int F = o.n_filters;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ss->prof) {
+        LF_CUDA(cudaEventCreate(&e0));
+        LF_CUDA(cudaEventCreate(&e1));
+        LF_CUDA(cudaEventRecord(e0, st));
+    }
+    LF_CUDA(cudaMemsetAsync(ss->fhist.p, 0, sizeof(int) * std::max(1, F), st));
+    LF_CUDA(cudaMemsetAsync(ss->ptotal.p, 0, sizeof(unsigned long long), st));
+    const unsigned wgrid = (unsigned)((Q * 32 + 255) / 256);
+    pairs_count_kernel<<<wgrid, 256, 0, st>>>(s, ss->pend.as<int>(), ss->fhist.as<int>(),
+                                              ss->ptotal.as<unsigned long long>(), idx, ss->round == 0 ? 1 : 0);
+    LF_CUDA(cudaGetLastError());
+    unsigned long long total = 0;
+    LF_CUDA(cudaMemcpyAsync(&total, ss->ptotal.p, sizeof(total), cudaMemcpyDeviceToHost, st));
+    LF_CUDA(cudaStreamSynchronize(st));
+    ss->kernels += 1;
+    if (total == 0) {
+        LF_CUDA(cudaMemcpyAsync(ss->pcount.p, ss->pend.p, sizeof(int) * Q, cudaMemcpyDeviceToDevice, st));
+    } else {
+        const int64_t P = (int64_t)total;
+        Scratch rows, dst, tiles;
+        LF_CUDA(rows.alloc(sizeof(float) * (size_t)P * idx.m, st));
+        LF_CUDA(dst.alloc(sizeof(int2) * (size_t)P, st));
+        LF_CUDA(tiles.alloc(sizeof(int4) * (size_t)(P / 128 + F + 1), st));
+        pair_tiles_kernel<<<1, 1024, 0, st>>>(ss->fhist.as<int>(), F, ss->fcur.as<int>(), tiles.as<int4>(),
+                                              ss->ntiles.as<int>());
+        LF_CUDA(cudaGetLastError());
+        pairs_fill_kernel<<<wgrid, 256, 0, st>>>(s, idx, ss->d_q, idx.m, ss->pcount.as<int>(), ss->pend.as<int>(),
+                                                 ss->fcur.as<int>(), dst.as<int2>(), rows.as<float>());
+        LF_CUDA(cudaGetLastError());
+        pairs_gather_kernel<<<(unsigned)((P * 32 + 255) / 256), 256, 0, st>>>(ss->d_q, idx.m, dst.as<int2>(), P,
+                                                                             rows.as<float>());
+        LF_CUDA(cudaGetLastError());
+        int rc = filter_pairs_tc(rows.as<float>(), P, idx.m, o.d_W1T, o.d_b1, o.d_W2, o.d_b2, F, tiles.as<int4>(),
+                                 ss->ntiles.as<int>(), dst.as<int2>(), o.d_offset, ss->adj.as<double>(), idx.n_nodes,
+                                 st);
+        if (rc) return rc;
+        ss->kernels += 4;
+        ss->pairs += P;
+        ++ss->predict_steps;
+    }
+    if (ss->prof) {
+        LF_CUDA(cudaEventRecord(e1, st));
+        LF_CUDA(cudaEventSynchronize(e1));
+        ss->predict_ms += ev_ms(e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
+    return LF_OK;
+}
+
 static int session_round(lf_session* ss, const double* d_bound, double* d_bsf_out, int* active_out) {
     RoundState& s = ss->s;
     const lf_index& idx = ss->idx;
@@ -1390,7 +1640,7 @@ static int session_round(lf_session* ss, const double* d_bound, double* d_bsf_ou
     const int64_t Q = ss->Q;
     s.bound = d_bound;
     s.R = o.sequential ? 1 : (int)std::min<int64_t>(s.Rcap, (int64_t)1 << std::min(ss->round, 30));
-    LF_CUDA(cudaMemsetAsync(s.n_active, 0, sizeof(int) * 2, st));
+    LF_CUDA(cudaMemsetAsync(s.n_active, 0, sizeof(int) * 3, st));
     if (ss->prof) cudaEventRecord(ss->ev[2], st);
     plan_warp_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s, idx);
     offsets_kernel<<<1, 1024, 0, st>>>(s.chunk_off, Q);
@@ -1433,8 +1683,12 @@ static int session_round(lf_session* ss, const double* d_bound, double* d_bsf_ou
         LF_CUDA(cudaGetLastError());
         ++ss->kernels;
     }
-    LF_CUDA(cudaMemcpyAsync(ss->h_active, s.n_active, sizeof(int) * 2, cudaMemcpyDeviceToHost, st));
+    LF_CUDA(cudaMemcpyAsync(ss->h_active, s.n_active, sizeof(int) * 3, cudaMemcpyDeviceToHost, st));
     LF_CUDA(cudaStreamSynchronize(st));
+    if (ss->lazy && ss->h_active[0] > 0 && (ss->round == 0 || ss->h_active[2] > 0)) {
+        int rc = predict_step(ss);     // after round 0 every bsf is finite: predict what is reachable
+        if (rc) return rc;
+    }
     if (ss->h_active[1] > 0) {      // some walks reached the end of their sorted prefix
         OrderArgs oa = ss->oa;
         oa.only = s.refill;
@@ -1472,6 +1726,9 @@ static int session_end(lf_session* ss, int64_t* out_ids, double* out_d, int64_t*
         p[LF_PROF_KERNELS] = (double)ss->kernels;
         p[LF_PROF_TOTAL_MS] = ev_ms(ss->ev[0], ss->ev[5]);
         p[LF_PROF_REFILLS] = (double)ss->refills;
+        p[LF_PROF_PREDICT_MS] = ss->predict_ms;
+        p[LF_PROF_PAIRS] = (double)ss->pairs;
+        p[LF_PROF_PREDICT_STEPS] = (double)ss->predict_steps;
         unsigned long long c[2] = {0, 0};
         cudaMemcpy(c, ss->ea_count.p, sizeof(c), cudaMemcpyDeviceToHost);
         p[LF_PROF_EA_ROWS] = (double)c[0];
@@ -1492,9 +1749,13 @@ static int check_args(const lf_index* idx, int64_t Q, const lf_search_opts* opts
     LF_REQUIRE(Q >= 0, "negative query count");
     LF_REQUIRE(opts->k >= 1 && opts->k <= idx->n_series, "k must be in [1, n]");
     LF_REQUIRE(idx->n_seg >= 1 && idx->n_seg <= LF_MAX_SEG, "bad segment count");
-    LF_REQUIRE((opts->d_pred == nullptr && opts->d_pred_f64 == nullptr) ||
+    LF_REQUIRE((opts->d_pred == nullptr && opts->d_pred_f64 == nullptr && opts->d_W1T == nullptr) ||
                    (opts->d_offset != nullptr && idx->d_leaf_filter != nullptr),
                "filter predictions need offsets and a leaf->filter map");
+    LF_REQUIRE(opts->d_W1T == nullptr || opts->d_pred != nullptr || opts->d_pred_f64 != nullptr ||
+                   (opts->d_b1 != nullptr && opts->d_W2 != nullptr && opts->d_b2 != nullptr && idx->m % 32 == 0 &&
+                    idx->m >= 32 && idx->m <= 256 && opts->n_filters >= 1),
+               "lazy filter inference needs W1T, b1, W2, b2 and m in {32, 64, ..., 256}");
     LF_REQUIRE(opts->sequential || opts->max_round_leaves >= 1, "max_round_leaves must be >= 1");
     return LF_OK;
 }

@@ -152,12 +152,16 @@ def _queries_device(queries, m: int, dev):
 def search_batch(index, queries, k: int = 1, *, bsf_factor: float = 1.0, predictions=None,
                  offsets=None, leaf_filter=None, sequential: bool = False,
                  max_round_leaves: int = 64, want_trace: bool = False, stream=None,
-                 copy_out: bool = True, profile: np.ndarray | None = None, early_abandon: bool = True):
+                 copy_out: bool = True, profile: np.ndarray | None = None, early_abandon: bool = True,
+                 filters=None):
     """Search a batch of queries in one lf_search call.
 
     predictions: device fp32 [Q, F] filter outputs (FilterPack.predict), with
     offsets [F] (fp64) and leaf_filter int32 [n_leaves] (filter slot per leaf
     slot, -1 for unfiltered leaves).
+    filters: a tensor-core FilterPack INSTEAD of predictions (lazy inference inside
+    lf_search: only the (query, leaf) pairs the walk can reach are predicted, with the
+    same kernel arithmetic, so results equal the predictions path bit for bit).
     """
     torch = _lib.require_cuda()
     t = as_tree(index)
@@ -179,7 +183,24 @@ def search_batch(index, queries, k: int = 1, *, bsf_factor: float = 1.0, predict
             raise ValueError("profile must be a float64 array of at least N_PROF entries")
         opts.h_profile = profile.ctypes.data
     keep = []
-    if predictions is not None:
+    if filters is not None:
+        if predictions is not None:
+            raise ValueError("pass predictions or filters, not both")
+        if offsets is None or leaf_filter is None:
+            raise ValueError("filters need offsets and a leaf->filter map")
+        if filters.path != "tc":
+            raise ValueError("lazy filter inference needs the tensor-core filter path")
+        off = torch.as_tensor(np.asarray(offsets, dtype=np.float64) if not isinstance(offsets, torch.Tensor)
+                              else offsets, dtype=torch.float64).to(dev).contiguous()
+        lf = leaf_filter.to(device=dev, dtype=torch.int32).contiguous()
+        if off.shape[0] != filters.n_filters or lf.shape != (di.n_leaves,):
+            raise ValueError("filter / offset / leaf map shapes do not agree")
+        keep += [off, lf]
+        opts.d_W1T, opts.d_b1 = filters.W1T.data_ptr(), filters.b1.data_ptr()
+        opts.d_W2, opts.d_b2 = filters.W2.data_ptr(), filters.b2.data_ptr()
+        opts.d_offset, opts.n_filters = off.data_ptr(), int(off.shape[0])
+        ist = di.struct(lf)
+    elif predictions is not None:
         if offsets is None or leaf_filter is None:
             raise ValueError("filter predictions need offsets and a leaf->filter map")
         pdt = torch.float64 if predictions.dtype == torch.float64 else torch.float32

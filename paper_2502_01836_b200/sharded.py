@@ -32,7 +32,7 @@ class GpuRoundEngine:
 
     def __init__(self, dindex, queries, k: int, *, predictions=None, offsets=None, leaf_filter=None,
                  bsf_factor: float = 1.0, max_round_leaves: int = 64, early_abandon: bool = True,
-                 stream=None, profile=None):
+                 stream=None, profile=None, filters=None):
         import torch
 
         self.torch = torch
@@ -49,7 +49,15 @@ class GpuRoundEngine:
         o.max_round_leaves = int(max_round_leaves)
         o.early_abandon = 1 if early_abandon else 0
         lf = None
-        if predictions is not None:
+        if filters is not None:                      # lazy inference inside the session
+            off = torch.as_tensor(offsets, dtype=torch.float64).to(self.device).contiguous()
+            lf = leaf_filter.to(device=self.device, dtype=torch.int32).contiguous()
+            self._keep += [off, lf, filters]
+            o.d_W1T, o.d_b1 = filters.W1T.data_ptr(), filters.b1.data_ptr()
+            o.d_W2, o.d_b2 = filters.W2.data_ptr(), filters.b2.data_ptr()
+            o.d_offset = off.data_ptr()
+            o.n_filters = int(off.shape[0])
+        elif predictions is not None:
             pr = predictions.to(self.device).contiguous()
             off = torch.as_tensor(offsets, dtype=torch.float64).to(self.device).contiguous()
             lf = leaf_filter.to(device=self.device, dtype=torch.int32).contiguous()
@@ -151,7 +159,7 @@ class ShardedResult:
 
 def search_sharded(tree, queries, k: int = 1, *, rank: int, world: int, pack=None, offsets=None,
                    bsf_factor: float = 1.0, max_round_leaves: int = 64, group=None, copy_out: bool = True,
-                   profile=None):
+                   profile=None, lazy: bool = False):
     """Leaf-sharded batched search on this rank's GPU (call on every rank).
 
     pack: this rank's FilterPack (its local filters only) with `offsets` in pack
@@ -164,7 +172,10 @@ def search_sharded(tree, queries, k: int = 1, *, rank: int, world: int, pack=Non
     q = q.to(device=di.device, dtype=torch.float32).contiguous()
     kw = {}
     if pack is not None and pack.n_filters:
-        kw = dict(predictions=pack.predict(q), offsets=offsets, leaf_filter=pack.leaf_filter(di))
+        if lazy and pack.path == "tc":
+            kw = dict(filters=pack, offsets=offsets, leaf_filter=pack.leaf_filter(di))
+        else:
+            kw = dict(predictions=pack.predict(q), offsets=offsets, leaf_filter=pack.leaf_filter(di))
     eng = GpuRoundEngine(di, q, k, bsf_factor=bsf_factor, max_round_leaves=max_round_leaves, profile=profile, **kw)
     ids, d, stats, rounds = run_rounds(eng, group)
     if not copy_out:

@@ -436,3 +436,55 @@ def test_prefix_order_filtered_sequential_matches_oracle(monkeypatch):
         o = lo.search(ot, q, 2, predictors=preds, offsets=offs)
         assert [a for a, _ in out.results] == [a for a, _ in o.results], i
         assert [getattr(out.stats, s_) for s_ in lo.STAT_KEYS] == [o.stats[s_] for s_ in lo.STAT_KEYS], i
+
+
+@pytest.mark.parametrize("k,seq", [(1, False), (3, False), (1, True), (2, True)])
+def test_lazy_filter_inference_identical(k, seq):
+    """Lazy inference inside lf_search (tensor-core GEMM over only the reachable
+    (query, leaf) pairs) gives exactly the results and counters of the dense
+    predictions path, sequential and batched schedules."""
+    import torch
+    from paper_2502_01836_b200 import build_index, search_batch
+    from paper_2502_01836_b200.filters import FilterPack
+
+    data = lo.randwalk(30000, 64, 91)
+    t = build_index(data, 150)
+    rng = np.random.default_rng(3)
+    leaves = [int(l) for l in t.leaf_ids]
+    sel = leaves[::2] + leaves[1::7]
+    sel = sorted(set(sel))
+    F, m = len(sel), 64
+    pack = FilterPack(sel, rng.normal(0, 0.08, (F, m, m)), rng.normal(0, 0.05, (F, m)),
+                      rng.normal(0, 0.08, (F, m)), rng.uniform(1.0, 9.0, F), path="tc")
+    Q = np.concatenate([lo.noisy_queries(data, 70, nz, 40 + int(10 * nz)) for nz in (0.1, 0.3, 0.6)])
+    qd = torch.from_numpy(Q.astype(np.float32)).cuda()
+    di = t.device()
+    offs = rng.uniform(0.0, 1.5, F)
+    lf = pack.leaf_filter(di)
+    dense = search_batch(t, qd, k, predictions=pack.predict(qd), offsets=offs, leaf_filter=lf, sequential=seq)
+    prof = np.zeros(16)
+    lazy = search_batch(t, qd, k, filters=pack, offsets=offs, leaf_filter=lf, sequential=seq, profile=prof)
+    np.testing.assert_array_equal(lazy.ids, dense.ids)
+    np.testing.assert_array_equal(lazy.dists, dense.dists)
+    np.testing.assert_array_equal(lazy.stats, dense.stats)
+    assert dense.stats[:, 3].sum() > 0, "the random filters must prune something"
+    assert 0 < prof[11] < Q.shape[0] * F, "lazy inference computes a strict subset of the pairs"
+
+
+def test_pair_predictions_bit_identical():
+    """lf_filter_predict_pairs_tc (bucketed, gathered rows) == the dense tensor-core
+    predictions of the same (query, filter) pairs, bit for bit, in any pair order."""
+    import torch
+    from paper_2502_01836_b200.filters import FilterPack
+
+    rng = np.random.default_rng(11)
+    F, m, Q = 37, 128, 300
+    pack = FilterPack(list(range(F)), rng.normal(0, 0.08, (F, m, m)), rng.normal(0, 0.05, (F, m)),
+                      rng.normal(0, 0.08, (F, m)), rng.uniform(1.0, 9.0, F), path="tc")
+    qd = torch.from_numpy(rng.normal(0, 1, (Q, m)).astype(np.float32)).cuda()
+    dense = pack.predict(qd).cpu().numpy().astype(np.float64)
+    pq = rng.integers(0, Q, 5000)
+    pf = rng.integers(0, F, 5000)
+    pf[:400] = 5                                   # one filter with several 128-row tiles
+    got = pack.predict_pairs(qd, pq, pf).cpu().numpy()
+    np.testing.assert_array_equal(got, dense[pq, pf])
