@@ -119,19 +119,33 @@ __global__ void plan_warp_kernel(RoundState s, lf_index idx) {
         int tl = s.want_trace ? s.tr.d_len[q] : 0;
         const int64_t tbase = q * (int64_t)idx.n_leaves;
         long long c_vis = 0, c_srch = 0, c_lbp = 0, c_fp = 0, c_inf = 0, c_rows = 0;
+        // records of the current 32 entries, and the next 32 prefetched while these are
+        // decided (a walk that neither breaks nor fills its quota moves on by exactly 32)
+        auto load = [&](int at, double& l_, int& r_, double& a_) {
+            const int k = at + lane;
+            l_ = k < len ? lbs[k] : kInf;
+            r_ = k < len ? lrec[k] : -1;
+            a_ = k < len ? adj[k] : 0.0;
+        };
+        double lb_c, ad_c;
+        int rec_c;
+        load(cur, lb_c, rec_c, ad_c);
         while (!fin && cur < len) {
+            double lb_n, ad_n;
+            int rec_n;
+            load(cur + 32, lb_n, rec_n, ad_n);
             const int i = cur + lane;
             const bool valid = i < len;
             const int node = (valid && s.want_trace) ? ord[i] : -1;
-            const double lb = valid ? lbs[i] : kInf;
-            const int rec = valid ? lrec[i] : -1;
+            const double lb = lb_c;
+            const int rec = rec_c;
             const int leaf = rec >= 0 ? (rec & LF_REC_LEAF) : -1;
             const bool brk = valid && lb > thr;
             const unsigned bmask = __ballot_sync(0xffffffffu, brk);
             const int first_brk = bmask ? __ffs(bmask) - 1 : 32;
             const bool visit = valid && leaf >= 0 && lane < first_brk;
             const int fs = (visit && (rec & LF_REC_HASF)) ? 0 : -1;
-            const bool fpr = fs >= 0 && adj[i] > thr;      // (pred - offset) > bsf * f, tree.py:282
+            const bool fpr = fs >= 0 && ad_c > thr;        // (pred - offset) > bsf * f, tree.py:282
             const bool scan = visit && !fpr;
             const unsigned smask = __ballot_sync(0xffffffffu, scan);
             const int need = s.R - ns;
@@ -216,6 +230,11 @@ __global__ void plan_warp_kernel(RoundState s, lf_index idx) {
                 cur += end;
             }
             if (quota) break;
+            if (end == 32) {
+                lb_c = lb_n; rec_c = rec_n; ad_c = ad_n;
+            } else {
+                load(cur, lb_c, rec_c, ad_c);
+            }
         }
         if (cur >= Nn) fin = true;
         if (lane == 0) {
