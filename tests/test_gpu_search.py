@@ -488,3 +488,25 @@ def test_pair_predictions_bit_identical():
     pf[:400] = 5                                   # one filter with several 128-row tiles
     got = pack.predict_pairs(qd, pq, pf).cpu().numpy()
     np.testing.assert_array_equal(got, dense[pq, pf])
+
+
+@pytest.mark.parametrize("k", [1, 5])
+def test_grouped_scan_identical(k, monkeypatch):
+    """The round's tasks grouped by (leaf, chunk) -- one pass over a chunk serves every
+    query scanning it, groups split at 8 -- give exactly the per-task scan's results
+    and counters.  Queries are clustered so that groups of 1..20 queries form."""
+    from paper_2502_01836_b200 import build_index, search_batch
+
+    data = lo.randwalk(40000, 128, 61)
+    t = build_index(data, 900)
+    base = lo.noisy_queries(data, 6, 0.05, 3)
+    rng = np.random.default_rng(4)
+    Q = np.concatenate([np.stack([base[i % 6] + rng.normal(0, 0.05, base.shape[1]) for i in range(90)]),
+                        lo.noisy_queries(data, 30, 0.4, 5)])
+    monkeypatch.setenv("LF_SCAN_GROUP", "0")
+    ref = search_batch(t, Q, k)
+    monkeypatch.setenv("LF_SCAN_GROUP", "1")
+    got = search_batch(t, Q, k)
+    np.testing.assert_array_equal(got.ids, ref.ids)
+    np.testing.assert_array_equal(got.dists, ref.dists)
+    np.testing.assert_array_equal(got.stats, ref.stats)
