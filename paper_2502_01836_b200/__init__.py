@@ -23,6 +23,7 @@ from .engine import (
     search_engine,
 )
 from .filters import FilterPack
+from .isax import build_isax_index
 
 __version__ = "0.1.0"
 
@@ -37,6 +38,7 @@ __all__ = [
     "batch_distances",
     "build_index",
     "build_index_device",
+    "build_isax_index",
     "DeviceRows",
     "epsilon_search",
     "exact_search",

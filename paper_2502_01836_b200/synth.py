@@ -110,3 +110,48 @@ def queries_device(values, count: int, noise_level: float, seed: int):
     src = torch.randint(0, values.shape[0], (count,), generator=g, device=values.device)
     noise = torch.randn((count, values.shape[1]), generator=g, device=values.device, dtype=torch.float64)
     return (values[src].to(torch.float64) + noise * noise_level).to(torch.float32)
+
+
+# --------------------------------------------------------------------------
+# BASELINE config 5 (Deep1B-shaped): Gaussian-mixture vectors.  No reference
+# generator exists (parity unpinned): K centers ~ N(0, 1)^m,
+# points = center + N(0, sigma^2)^m, rounded to fp32.  Fixed seed.
+# --------------------------------------------------------------------------
+def gaussian_mixture(n: int, m: int, seed: int, n_centers: int = 1000, sigma: float = 0.25,
+                     chunk_rows: int = 1 << 16) -> np.ndarray:
+    """Host fp64 (fp32-exact) [n, m] Gaussian mixture."""
+    if n < 1 or m < 2 or n_centers < 1:
+        raise ValueError(f"need n >= 1, m >= 2, n_centers >= 1, got {n}, {m}, {n_centers}")
+    rng = np.random.default_rng(seed)
+    centers = rng.standard_normal((n_centers, m))
+    out = np.empty((n, m), dtype=np.float64)
+    for r0 in range(0, n, chunk_rows):
+        r1 = min(n, r0 + chunk_rows)
+        c = rng.integers(0, n_centers, size=r1 - r0)
+        out[r0:r1] = _f32_exact(centers[c] + sigma * rng.standard_normal((r1 - r0, m)))
+    return out
+
+
+def gaussian_mixture_device(n: int, m: int, seed: int, n_centers: int = 1000, sigma: float = 0.25,
+                            device="cuda", chunk_rows: int = 1 << 22):
+    """GPU Gaussian mixture (same law as gaussian_mixture, torch Philox stream)."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    centers = torch.randn((n_centers, m), generator=g, device=device, dtype=torch.float32)
+    out = torch.empty((n, m), dtype=torch.float32, device=device)
+    for r0 in range(0, n, chunk_rows):
+        r1 = min(n, r0 + chunk_rows)
+        c = torch.randint(0, n_centers, (r1 - r0,), generator=g, device=device)
+        out[r0:r1] = centers[c] + sigma * torch.randn((r1 - r0, m), generator=g, device=device)
+    return out
+
+
+def recall_at_k(ids: np.ndarray, exact_ids: np.ndarray) -> np.ndarray:
+    """Per-query recall@k = |returned ids ∩ exact top-k ids| / k (the reference defines
+    recall@1 only, cli.py:83-88; this is its k-NN generalisation for config 5)."""
+    ids = np.atleast_2d(ids)
+    exact_ids = np.atleast_2d(exact_ids)
+    k = exact_ids.shape[1]
+    return np.array([len(set(a.tolist()) & set(b.tolist())) / k for a, b in zip(ids, exact_ids)])
