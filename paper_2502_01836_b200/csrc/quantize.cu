@@ -17,6 +17,7 @@ __global__ void quantize_kernel(const float* __restrict__ X, int64_t n, int m, i
     const int lane = threadIdx.x & 31;
     if (r >= n) return;
     const float* x = X + r * m;
+    const int m8 = (m + 63) / 64 * 64;            // code rows are zero-padded to a multiple of 64
     float mx = 0.f;
     for (int i = lane; i < m; i += 32) mx = fmaxf(mx, fabsf(x[i]));
 #pragma unroll
@@ -28,11 +29,12 @@ __global__ void quantize_kernel(const float* __restrict__ X, int64_t n, int m, i
         float c = rintf(x[i] / s);
         c = fminf(fmaxf(c, -127.f), 127.f);
         const int ci = (int)c;
-        X8[r * m + i] = (int8_t)ci;
+        X8[r * m8 + i] = (int8_t)ci;
         sq += ci * ci;
         const double e = (double)s * (double)ci - (double)x[i];
         err = __fma_rn(e, e, err);
     }
+    for (int i = m + lane; i < m8; i += 32) X8[r * m8 + i] = 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         sq += __shfl_xor_sync(0xffffffffu, sq, o);
@@ -164,7 +166,7 @@ extern "C" int lf_quantize_rows(const float* d_X, int64_t n, int32_t m, int8_t* 
 
 extern "C" int lf_quantize_rows2(const float* d_X, int64_t n, int32_t m, const int8_t* d_X8, const float* d_qmeta,
                                  int8_t* d_X8b, float* d_qmeta2, void* stream) {
-    LF_REQUIRE(n >= 0 && m >= 1, "bad sizes");
+    LF_REQUIRE(n >= 0 && m >= 1 && m % 64 == 0, "second-level codes need m % 64 == 0");
     return lf::quantize_level2(d_X, n, m, m, d_X8, reinterpret_cast<const float4*>(d_qmeta), d_X8b,
                                reinterpret_cast<float4*>(d_qmeta2), lf::as_stream(stream));
 }

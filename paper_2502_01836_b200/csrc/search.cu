@@ -1212,9 +1212,11 @@ __global__ void __launch_bounds__(Q8_THREADS, 2) scan_q8_kernel(RoundState s, lf
         }
         q8_cons_sync();
         const int ns = n_surv[par];
-        {   // exact fp64 direct-form distances of the survivors (series.py:142-146)
-            const float* X0 = idx.d_X + r0 * M;
-            const float* qrow = queries + q * M;
+        {   // exact fp64 direct-form distances of the survivors (series.py:142-146); fp32 rows
+            // have stride m (the int8 codes are zero-padded to M)
+            const int mr = idx.m;
+            const float* X0 = idx.d_X + r0 * mr;
+            const float* qrow = queries + q * mr;
             const int hslot = cw * 2 + (lane >> 4);
             for (int b0 = 0; b0 < ns; b0 += 16) {
                 const int jj = b0 + hslot;
@@ -1223,12 +1225,15 @@ __global__ void __launch_bounds__(Q8_THREADS, 2) scan_q8_kernel(RoundState s, lf
                 float4 x[NCH];
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch)
-                    x[ch] = v ? __ldg(reinterpret_cast<const float4*>(X0 + (int64_t)r * M) + ch * 16 + hl)
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
+                    x[ch] = (v && ch * 64 + hl * 4 < mr)
+                                ? __ldg(reinterpret_cast<const float4*>(X0 + (int64_t)r * mr) + ch * 16 + hl)
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
                 double acc = 0.0;
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch) {
-                    const float4 qv = __ldg(reinterpret_cast<const float4*>(qrow) + ch * 16 + hl);
+                    const float4 qv = ch * 64 + hl * 4 < mr
+                                          ? __ldg(reinterpret_cast<const float4*>(qrow) + ch * 16 + hl)
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
                     const double d0 = (double)x[ch].x - (double)qv.x, d1 = (double)x[ch].y - (double)qv.y;
                     const double d2 = (double)x[ch].z - (double)qv.z, d3 = (double)x[ch].w - (double)qv.w;
                     acc = __fma_rn(d0, d0, acc); acc = __fma_rn(d1, d1, acc);
@@ -1342,25 +1347,27 @@ __device__ __forceinline__ void q8_tail_sync() { asm volatile("bar.sync 2, %0;" 
 template <int NCH>
 __device__ __forceinline__ void q8g_exact(const lf_index& idx, const float* __restrict__ queries, const int* gq,
                                           int64_t r0, const int* surv_r, double* surv_d, int ns, int tw, int lane) {
-    constexpr int M = NCH * 64;
+    const int mr = idx.m;                      // fp32 row stride (codes are padded to NCH * 64)
     const int hl = lane & 15;
-    const float* X0 = idx.d_X + r0 * M;
+    const float* X0 = idx.d_X + r0 * mr;
     const int hslot = tw * 2 + (lane >> 4);
     for (int b0 = 0; b0 < ns; b0 += 2 * GT_WARPS) {
         const int jj = b0 + hslot;
         const bool v = jj < ns;
         const int ent = v ? surv_r[jj] : 0;
         const int r = ent & 0xffff;
-        const float* qrow = queries + (int64_t)gq[ent >> 16] * M;
+        const float* qrow = queries + (int64_t)gq[ent >> 16] * mr;
         float4 x[NCH];
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch)
-            x[ch] = v ? __ldg(reinterpret_cast<const float4*>(X0 + (int64_t)r * M) + ch * 16 + hl)
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
+            x[ch] = (v && ch * 64 + hl * 4 < mr)
+                        ? __ldg(reinterpret_cast<const float4*>(X0 + (int64_t)r * mr) + ch * 16 + hl)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
         double acc = 0.0;
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) {
-            const float4 qv = __ldg(reinterpret_cast<const float4*>(qrow) + ch * 16 + hl);
+            const float4 qv = ch * 64 + hl * 4 < mr ? __ldg(reinterpret_cast<const float4*>(qrow) + ch * 16 + hl)
+                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
             const double d0 = (double)x[ch].x - (double)qv.x, d1 = (double)x[ch].y - (double)qv.y;
             const double d2 = (double)x[ch].z - (double)qv.z, d3 = (double)x[ch].w - (double)qv.w;
             acc = __fma_rn(d0, d0, acc); acc = __fma_rn(d1, d1, acc);
@@ -2071,7 +2078,7 @@ static int session_begin(lf_session* ss) {
     LF_CUDA(cudaGetLastError());
     ++ss->kernels;
     ss->q8 = idx.d_X8 != nullptr && idx.d_qmeta != nullptr && o.early_abandon && !s.want_trace &&
-             (idx.m % 64) == 0 && idx.m <= 512 && scan_variant() == 8;
+             (idx.m % 4) == 0 && idx.m <= 512 && scan_variant() == 8;
     if (ss->q8) {
         // grouping by (leaf, chunk) reads ~1/3 fewer int8 bytes on the bench workload but its
         // round overhead (~30 us) eats the gain there (scan 3.95 -> 3.82 ms, +0.27 ms grouping),
@@ -2192,7 +2199,11 @@ static int session_round(lf_session* ss, const double* d_bound, double* d_bsf_ou
     const int grid = sm_count() * 4;
     const int m4 = idx.m / 4;
     cudaError_t ce;
-    const bool ea = o.early_abandon && !s.want_trace && (idx.m % 64) == 0 && idx.m <= 512 && scan_variant() != 0;
+    // the int8-bounded scan takes m % 4 == 0 (codes zero-padded to a multiple of 64); the fp32
+    // early-abandon variants need m % 64 == 0
+    const bool ea = o.early_abandon && !s.want_trace && idx.m <= 512 && scan_variant() != 0 &&
+                    ((idx.m % 64) == 0 || (ss->q8 && (idx.m % 4) == 0));
+    const int nch = (idx.m + 63) / 64;
     if (ea && ss->q8 && ss->grouped) {
         // group the round's tasks by (leaf, chunk), then one pass per chunk serves them all
         const int64_t max_tasks = std::max<int64_t>(
@@ -2215,7 +2226,7 @@ static int session_round(lf_session* ss, const double* d_bound, double* d_bsf_ou
         ss->kernels += 6;
         if (ss->prof) cudaEventRecord(ss->ev[3], st);     // grouping counts as planning
         const int sms = sm_count();
-        switch (idx.m / 64) {
+        switch (nch) {
 #define LF_GROUPED(N)                                                                                          \
     case N: {                                                                                                 \
         static bool attr = false;                                                                             \
@@ -2239,7 +2250,7 @@ static int session_round(lf_session* ss, const double* d_bound, double* d_bsf_ou
         const int g3 = sm_count();                // launch_scan_ea sizes the grid to the variant's residency
         const int8_t* qc8 = ss->q8 ? ss->qc8.as<int8_t>() : nullptr;
         const float4* qm8 = ss->q8 ? ss->qm8.as<float4>() : nullptr;
-        switch (idx.m / 64) {
+        switch (nch) {
             case 1: ce = launch_scan_ea<1>(s, idx, ss->d_q, qc8, qm8, g3, st); break;
             case 2: ce = launch_scan_ea<2>(s, idx, ss->d_q, qc8, qm8, g3, st); break;
             case 3: ce = launch_scan_ea<3>(s, idx, ss->d_q, qc8, qm8, g3, st); break;

@@ -301,8 +301,8 @@ class DeviceIndex:
             # int8 shadow for the bounded scan (scan_q8_kernel), when the layout allows it
             self.X8 = self.qmeta = None
             n_rows, m = int(self.X.shape[0]), int(self.X.shape[1])
-            if m % 64 == 0 and m <= 512 and n_rows:
-                self.X8 = torch.empty((n_rows, m), dtype=torch.int8, device=dev)
+            if m % 4 == 0 and m <= 512 and n_rows:     # codes zero-padded to a multiple of 64
+                self.X8 = torch.empty((n_rows, (m + 63) // 64 * 64), dtype=torch.int8, device=dev)
                 self.qmeta = torch.empty((n_rows, 4), dtype=torch.float32, device=dev)
                 _lib.check(_lib.lib().lf_quantize_rows(self.X.data_ptr(), n_rows, m, self.X8.data_ptr(),
                                                        self.qmeta.data_ptr(), _lib.stream_ptr()))
@@ -320,7 +320,7 @@ class DeviceIndex:
         + 16 B per row).  Returns False when the first level does not exist."""
         import torch
 
-        if self.X8 is None:
+        if self.X8 is None or self.X.shape[1] % 64:
             return False
         if getattr(self, "X8b", None) is None:
             n_rows, m = int(self.X.shape[0]), int(self.X.shape[1])

@@ -348,7 +348,7 @@ def test_scan_variants_agree(variant, k, monkeypatch):
         assert seq.stats[i].tolist() == [o.stats[s_] for s_ in lo.STAT_KEYS]
 
 
-@pytest.mark.parametrize("m", [64, 192, 256, 320, 512])
+@pytest.mark.parametrize("m", [36, 64, 96, 100, 192, 256, 320, 512])
 @pytest.mark.parametrize("k", [1, 3])
 def test_q8_pipeline_exact(m, k, monkeypatch):
     """The TMA-pipelined int8-bounded scan (several stage counts / passes per row)
