@@ -49,6 +49,18 @@ FIXED = dict(t_series=2e-7, t_filter=6e-6)       # injected constants (reference
 NOISE_LEVELS = (0.1, 0.2, 0.3, 0.4)
 
 
+HEADLINE = "1-NN queries/sec at 99% recall, 25M x 256 random-walk series; leaves pruned %"
+
+
+def metric_name(args) -> str:
+    """BASELINE.json's metric for the default workload; the analogous name for configs 3 / 5."""
+    if args.k == 1 and args.dataset == "randwalk" and args.index == "dstree" and args.target == 0.99:
+        return HEADLINE
+    data = "Gaussian-mixture vectors" if args.dataset == "gmm" else "random-walk series"
+    return (f"{args.k}-NN queries/sec at {args.target:.0%} target, {args.n} x {args.m} {data} "
+            f"({'iSAX' if args.index == 'isax' else 'DSTree'}); leaves pruned %")
+
+
 def log(*a):
     print("[bench]", *a, file=sys.stderr, flush=True)
 
@@ -118,11 +130,21 @@ def setup_workload(args, device):
     from paper_2502_01836_b200.training import TrainConfig
 
     t0 = time.perf_counter()
-    X = randwalk_device(args.n, args.m, args.seed, device=device)
+    if args.dataset == "gmm":       # BASELINE config 5 (Deep1B-shaped Gaussian mixture)
+        from paper_2502_01836_b200.synth import gaussian_mixture_device
+
+        X = gaussian_mixture_device(args.n, args.m, args.seed, device=device)
+    else:
+        X = randwalk_device(args.n, args.m, args.seed, device=device)
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t0
     t0 = time.perf_counter()
-    tree = build_index_device(X, max_leaf_size=args.leaf_cap, segments=8)
+    if args.index == "isax":        # BASELINE config 3
+        from paper_2502_01836_b200.isax import build_isax_index
+
+        tree = build_isax_index(X, max_leaf_size=args.leaf_cap, segments=8)
+    else:
+        tree = build_index_device(X, max_leaf_size=args.leaf_cap, segments=8)
     di = tree.device(device)
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
@@ -144,7 +166,7 @@ def setup_workload(args, device):
     del X
     torch.cuda.empty_cache()
     t0 = time.perf_counter()
-    exact = search_batch(tree, Q, 1)
+    exact = search_batch(tree, Q, args.k)
     t_exact = time.perf_counter() - t0
     log(f"exact ground truth for {Q.shape[0]} queries in {t_exact:.2f}s "
         f"(pruning {np.mean(exact.pruning_ratios()):.4f})")
@@ -153,7 +175,7 @@ def setup_workload(args, device):
 
 
 def recall_of(res, exact) -> float:
-    """cli.py:83-88: id match, or distance within 1e-6 relative."""
+    """cli.py:83-88: id match, or distance within 1e-6 relative (recall@1)."""
     rid, rd = res.ids[:, 0], res.dists[:, 0]
     oid, od = exact.ids[:, 0], exact.dists[:, 0]
     ok = (rid == oid) | (np.abs(rd - od) <= 1e-6 * np.maximum(od, 1e-300))
@@ -170,7 +192,7 @@ def _oracle_worker(qi_list):
     t, preds, offs, Qh = _OR["tree"], _OR["preds"], _OR["offs"], _OR["Q"]
     out = []
     for qi in qi_list:
-        o = lo.search(t, Qh[qi], 1, predictors=preds, offsets=offs)
+        o = lo.search(t, Qh[qi], _OR.get("k", 1), predictors=preds, offsets=offs)
         out.append((qi, o.results[0][0], o.stats["series_scanned"]))
     return out
 
@@ -203,7 +225,7 @@ def oracle_setup(w) -> None:
     filt = eidx.filters
     preds = {l: (lambda x, f=filt[l]: lo.mlp_forward(f.W1, f.b1, f.W2, f.b2, x)) for l in filt}
     offs = eidx.tuned_offsets(w["target"])
-    _OR.update(tree=ot, preds=preds, offs=offs, Q=w["Q"].cpu().numpy().astype(np.float64))
+    _OR.update(tree=ot, preds=preds, offs=offs, Q=w["Q"].cpu().numpy().astype(np.float64), k=w.get("k", 1))
 
 
 def oracle_time(sample_idx, workers: int) -> tuple:
@@ -268,6 +290,7 @@ def run_ours(args, rank, world, device):
 
     w = setup_workload(args, device)
     w["target"] = args.target
+    w["k"] = args.k
     eidx, Q, exact, tree = w["eidx"], w["Q"], w["exact"], w["tree"]
     nQ = Q.shape[0]
     stream = torch.cuda.current_stream()
@@ -275,10 +298,11 @@ def run_ours(args, rank, world, device):
 
     if world == 1 and not args.sharded:
         def step(profile=None):
-            return search_queries(eidx, Q, 1, target=args.target, copy_out=False, profile=profile, lazy=args.lazy)
+            return search_queries(eidx, Q, args.k, target=args.target, copy_out=False, profile=profile,
+                                  lazy=args.lazy)
 
         def checked(queries):
-            return search_queries(eidx, queries, 1, target=args.target, lazy=args.lazy)
+            return search_queries(eidx, queries, args.k, target=args.target, lazy=args.lazy)
     else:
         # leaf-sharded: this rank's leaves, rows and filters; one MIN-allreduce per round
         from paper_2502_01836_b200.filters import FilterPack
@@ -291,11 +315,11 @@ def run_ours(args, rank, world, device):
         loffs = np.array([offs_all[l] for l in local], dtype=np.float64)
 
         def step(profile=None):
-            return search_sharded(tree, Q, 1, rank=rank, world=world, pack=lpack, offsets=loffs,
+            return search_sharded(tree, Q, args.k, rank=rank, world=world, pack=lpack, offsets=loffs,
                                   copy_out=False, profile=profile, lazy=args.lazy)
 
         def checked(queries):
-            return search_sharded(tree, queries, 1, rank=rank, world=world, pack=lpack, offsets=loffs,
+            return search_sharded(tree, queries, args.k, rank=rank, world=world, pack=lpack, offsets=loffs,
                                   lazy=args.lazy)
 
     for _ in range(args.warmup):
@@ -304,6 +328,11 @@ def run_ours(args, rank, world, device):
     # one checked run: recall and pruning of the exact workload being timed
     chk = checked(Q)
     recall = recall_of(chk, exact)
+    recall_k = None
+    if args.k > 1:
+        from paper_2502_01836_b200.synth import recall_at_k
+
+        recall_k = float(np.mean(recall_at_k(chk.ids, exact.ids)))
     per_noise = {}
     per = nQ // len(NOISE_LEVELS)
     for i, nz in enumerate(NOISE_LEVELS):
@@ -444,7 +473,7 @@ def run_ours(args, rank, world, device):
     ref_equiv = ref_bytes / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else None
     traffic, _ = ncu_traffic()
     line = {
-        "metric": "1-NN queries/sec at 99% recall, 25M x 256 random-walk series; leaves pruned %",
+        "metric": metric_name(args),
         "value": value,
         "unit": "queries/s",
         "n_gpus": world,
@@ -457,14 +486,16 @@ def run_ours(args, rank, world, device):
         "dtype": "f64-accumulated f32 series (scan/bounds), f32 filters",
         "data": "synthetic random walk generated on device (reference law, Philox stream), 25.6 GB >> L2: no flush needed",
         "config": {
-            "workload": f"DSTree+LeaFi {args.n}x{args.m}, leaf cap {args.leaf_cap}, {nQ} queries "
-                        f"(noise {'/'.join(map(str, NOISE_LEVELS))}), 1-NN, target {args.target}",
+            "workload": f"{'iSAX' if args.index == 'isax' else 'DSTree'}+LeaFi {args.n}x{args.m} "
+                        f"{'Gaussian mixture' if args.dataset == 'gmm' else 'random walk'}, leaf cap {args.leaf_cap}, "
+                        f"{nQ} queries (noise {'/'.join(map(str, NOISE_LEVELS))}), {args.k}-NN, target {args.target}",
             "n_series": args.n, "length": args.m, "leaf_cap": args.leaf_cap, "leaves": tree.n_leaves,
-            "filters": len(eidx.filters), "queries_per_step": nQ, "k": 1, "recall_target": args.target,
+            "filters": len(eidx.filters), "queries_per_step": nQ, "k": args.k, "recall_target": args.target,
             "parallelism": f"leaf-sharded x{world}" if world > 1 else "1 GPU",
             "l2": "inputs larger than L2 (25.6 GB collection)",
         },
         "recall_at_1": recall,
+        **({f"recall_at_{args.k}": recall_k} if args.k > 1 else {}),
         "leaves_pruned_pct": 100.0 * leaves_pruned,
         "series_pruning_ratio": series_pruned,
         "per_noise": per_noise,
@@ -528,6 +559,7 @@ def run_reference(args, rank, world, device):
     """The reference arm: the CPU oracle (restated reference algorithm) on the box's cores."""
     w = setup_workload(args, device)
     w["target"] = args.target
+    w["k"] = args.k
     workers = os.cpu_count() or 1
     oracle_setup(w)
     nQ = w["Q"].shape[0]
@@ -544,7 +576,7 @@ def run_reference(args, rank, world, device):
     value = n_done / sum(times)
     return {
         "impl": "reference",
-        "metric": "1-NN queries/sec at 99% recall, 25M x 256 random-walk series; leaves pruned %",
+        "metric": metric_name(args),
         "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64 (numpy oracle)", "data": "same synthetic workload as the ours arm",
@@ -580,6 +612,11 @@ def main():
                     help="use the leaf-sharded round driver even on one GPU (what N>1 runs)")
     ap.add_argument("--tdg-queries", type=int, default=10000,
                     help="queries for the training-data-generation measurement (0 = skip)")
+    ap.add_argument("--dataset", choices=("randwalk", "gmm"), default="randwalk",
+                    help="gmm = BASELINE config 5's Gaussian mixture (use with --m 96 --k 10)")
+    ap.add_argument("--index", choices=("dstree", "isax"), default="dstree",
+                    help="isax = BASELINE config 3's index family")
+    ap.add_argument("--k", type=int, default=1)
     ap.add_argument("--lazy", action="store_true",
                     help="lazy filter inference inside lf_search instead of the dense pass")
     ap.add_argument("--ncu", action="store_true",
