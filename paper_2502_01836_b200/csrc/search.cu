@@ -1936,8 +1936,11 @@ struct lf_session {
     lf::Scratch cbase, ghist, gcur, gsorted, glist, gcount, gbsum, ginfo;
     int n_keys = 0;
     long long refills = 0;           // queries whose visit order was completed after the prefix
-    int* h_active = nullptr;
-    int round = 0;
+    int* h_active = nullptr;         // pinned [2 slots][4]: active, refill, predict requests
+    int round = 0;                   // rounds enqueued
+    int harvested = 0;               // rounds whose counts were read back
+    cudaEvent_t rev[2][4] = {};      // per slot: plan start, scan start, merge start, merge end
+    cudaEvent_t done_ev[2] = {};     // per slot: counts copied back
     long long kernels = 0;
     cudaEvent_t ev[6] = {};
     bool prof = false;
@@ -1993,7 +1996,12 @@ static int session_begin(lf_session* ss) {
     LF_CUDA(ss->cand_d.alloc(sizeof(double) * max_tasks * s.kc, st));
     LF_CUDA(ss->cand_i.alloc(sizeof(long long) * max_tasks * s.kc, st));
     LF_CUDA(ss->task_min.alloc(sizeof(double) * (s.want_trace ? max_tasks : 1), st));
-    LF_CUDA(ss->n_active.alloc(sizeof(int) * 3, st));   // [active, refill requests, predict requests]
+    LF_CUDA(ss->n_active.alloc(sizeof(int) * 8, st));   // [2 slots][active, refill, predict requests, -]
+    for (int sl = 0; sl < 2; ++sl) {
+        LF_CUDA(cudaEventCreateWithFlags(&ss->done_ev[sl], cudaEventDisableTiming));
+        if (o.h_profile)
+            for (auto& e : ss->rev[sl]) LF_CUDA(cudaEventCreate(&e));
+    }
     ss->lazy = o.d_pred == nullptr && o.d_pred_f64 == nullptr && o.d_W1T != nullptr;
     if (ss->lazy) {
         LF_CUDA(ss->pcount.alloc(sizeof(int) * Q, st));
@@ -2014,7 +2022,7 @@ static int session_begin(lf_session* ss) {
     LF_CUDA(cudaMemsetAsync(ss->ea_count.p, 0, sizeof(unsigned long long) * 2, st));
     {   // one pinned word per host thread; a round reads it right after its own sync
         static thread_local int* pinned = nullptr;
-        if (pinned == nullptr) LF_CUDA(cudaMallocHost(&pinned, sizeof(int) * 4));
+        if (pinned == nullptr) LF_CUDA(cudaMallocHost(&pinned, sizeof(int) * 8));
         ss->h_active = pinned;
     }
 
@@ -2182,20 +2190,28 @@ static int predict_step(lf_session* ss) {
     return LF_OK;
 }
 
-static int session_round(lf_session* ss, const double* d_bound, double* d_bsf_out, int* active_out) {
+// Enqueue one round (plan, scan, merge) into count slot round & 1; the counts are
+// copied back asynchronously (done_ev).  session_harvest reads them.
+static int session_enqueue(lf_session* ss, const double* d_bound, double* d_bsf_out) {
     RoundState& s = ss->s;
     const lf_index& idx = ss->idx;
     const lf_search_opts& o = ss->opts;
     cudaStream_t st = ss->st;
     const int64_t Q = ss->Q;
+    const int slot = ss->round & 1;
+    int* counts = ss->n_active.as<int>() + 4 * slot;
+    s.n_active = counts;
+    s.n_refill = counts + 1;
+    s.n_predict = counts + 2;
+    cudaEvent_t* ev = ss->rev[slot];
     s.bound = d_bound;
     s.R = o.sequential ? 1 : (int)std::min<int64_t>(s.Rcap, (int64_t)1 << std::min(ss->round, 30));
-    LF_CUDA(cudaMemsetAsync(s.n_active, 0, sizeof(int) * 3, st));
-    if (ss->prof) cudaEventRecord(ss->ev[2], st);
+    LF_CUDA(cudaMemsetAsync(counts, 0, sizeof(int) * 3, st));
+    if (ss->prof) cudaEventRecord(ev[0], st);
     plan_warp_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s, idx);
     offsets_kernel<<<1, 1024, 0, st>>>(s.chunk_off, Q);
     expand_tasks_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s);
-    if (ss->prof) cudaEventRecord(ss->ev[3], st);
+    if (ss->prof) cudaEventRecord(ev[1], st);
     const int grid = sm_count() * 4;
     const int m4 = idx.m / 4;
     cudaError_t ce;
@@ -2224,7 +2240,7 @@ static int session_round(lf_session* ss, const double* d_bound, double* d_bsf_ou
                                                  ss->gcount.as<int>(), ss->ginfo.as<GroupInfo>());
         LF_CUDA(cudaGetLastError());
         ss->kernels += 6;
-        if (ss->prof) cudaEventRecord(ss->ev[3], st);     // grouping counts as planning
+        if (ss->prof) cudaEventRecord(ev[1], st);          // grouping counts as planning
         const int sms = sm_count();
         switch (nch) {
 #define LF_GROUPED(N)                                                                                          \
@@ -2266,10 +2282,10 @@ static int session_round(lf_session* ss, const double* d_bound, double* d_bsf_ou
     else if (m4 <= 256) ce = launch_scan<8>(s, idx, ss->d_q, grid, st);
     else return fail(LF_EINVAL, "series length > 1024 not supported");
     if (ce != cudaSuccess) return fail(LF_ECUDA, cudaGetErrorString(ce));
-    if (ss->prof) cudaEventRecord(ss->ev[4], st);
+    if (ss->prof) cudaEventRecord(ev[2], st);
     merge_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s);
     LF_CUDA(cudaGetLastError());
-    if (ss->prof) cudaEventRecord(ss->ev[5], st);
+    if (ss->prof) cudaEventRecord(ev[3], st);
     ss->kernels += 5;
     std::swap(s.top_d, s.top_d_out);
     std::swap(s.top_i, s.top_i_out);
@@ -2279,31 +2295,54 @@ static int session_round(lf_session* ss, const double* d_bound, double* d_bsf_ou
         LF_CUDA(cudaGetLastError());
         ++ss->kernels;
     }
-    LF_CUDA(cudaMemcpyAsync(ss->h_active, s.n_active, sizeof(int) * 3, cudaMemcpyDeviceToHost, st));
-    LF_CUDA(cudaStreamSynchronize(st));
-    if (ss->lazy && ss->h_active[0] > 0 && (ss->round == 0 || ss->h_active[2] > 0)) {
+    LF_CUDA(cudaMemcpyAsync(ss->h_active + 4 * slot, counts, sizeof(int) * 3, cudaMemcpyDeviceToHost, st));
+    LF_CUDA(cudaEventRecord(ss->done_ev[slot], st));
+    ++ss->round;
+    return LF_OK;
+}
+
+// Wait for the oldest enqueued round's counts, run the host-decided follow-ups
+// (lazy prediction pass, order refill) and accumulate its profile.
+static int session_harvest(lf_session* ss, int* active_out) {
+    RoundState& s = ss->s;
+    const lf_index& idx = ss->idx;
+    const lf_search_opts& o = ss->opts;
+    cudaStream_t st = ss->st;
+    const int64_t Q = ss->Q;
+    const int r = ss->harvested;
+    const int slot = r & 1;
+    int* h = ss->h_active + 4 * slot;
+    LF_CUDA(cudaEventSynchronize(ss->done_ev[slot]));
+    if (ss->lazy && h[0] > 0 && (r == 0 || h[2] > 0)) {
         int rc = predict_step(ss);     // after round 0 every bsf is finite: predict what is reachable
         if (rc) return rc;
     }
-    if (ss->h_active[1] > 0) {      // some walks reached the end of their sorted prefix
+    if (h[1] > 0) {                    // some walks reached the end of their sorted prefix
         OrderArgs oa = ss->oa;
         oa.only = s.refill;
         int nk = 0;
         int rc = refill_order(ss->d_q, Q, idx, ss->qsumm.as<double>(), ss->lb.as<double>(), oa, st, &nk);
         if (rc) return rc;
         ss->kernels += nk;
-        ss->refills += ss->h_active[1];
+        ss->refills += h[1];
     }
     if (ss->prof) {
         double* p = o.h_profile;
-        if (ss->round == 0) p[LF_PROF_BOUNDS_MS] = ev_ms(ss->ev[0], ss->ev[1]);
-        p[LF_PROF_PLAN_MS] += ev_ms(ss->ev[2], ss->ev[3]);
-        p[LF_PROF_SCAN_MS] += ev_ms(ss->ev[3], ss->ev[4]);
-        p[LF_PROF_MERGE_MS] += ev_ms(ss->ev[4], ss->ev[5]);
+        cudaEvent_t* ev = ss->rev[slot];
+        if (r == 0) p[LF_PROF_BOUNDS_MS] = ev_ms(ss->ev[0], ss->ev[1]);
+        p[LF_PROF_PLAN_MS] += ev_ms(ev[0], ev[1]);
+        p[LF_PROF_SCAN_MS] += ev_ms(ev[1], ev[2]);
+        p[LF_PROF_MERGE_MS] += ev_ms(ev[2], ev[3]);
     }
-    ++ss->round;
-    *active_out = *ss->h_active;
+    ++ss->harvested;
+    *active_out = h[0];
     return LF_OK;
+}
+
+static int session_round(lf_session* ss, const double* d_bound, double* d_bsf_out, int* active_out) {
+    int rc = session_enqueue(ss, d_bound, d_bsf_out);
+    if (rc) return rc;
+    return session_harvest(ss, active_out);
 }
 
 static int session_end(lf_session* ss, int64_t* out_ids, double* out_d, int64_t* out_stats) {
@@ -2318,7 +2357,7 @@ static int session_end(lf_session* ss, int64_t* out_ids, double* out_d, int64_t*
         double* p = ss->opts.h_profile;
         cudaEventRecord(ss->ev[5], st);
         cudaEventSynchronize(ss->ev[5]);
-        p[LF_PROF_ROUNDS] = ss->round;
+        p[LF_PROF_ROUNDS] = ss->harvested;
         p[LF_PROF_KERNELS] = (double)ss->kernels;
         p[LF_PROF_TOTAL_MS] = ev_ms(ss->ev[0], ss->ev[5]);
         p[LF_PROF_REFILLS] = (double)ss->refills;
@@ -2337,6 +2376,11 @@ static void session_free(lf_session* ss) {
     if (!ss) return;
     for (auto& e : ss->ev)
         if (e) cudaEventDestroy(e);
+    for (int sl = 0; sl < 2; ++sl) {
+        if (ss->done_ev[sl]) cudaEventDestroy(ss->done_ev[sl]);
+        for (auto& e : ss->rev[sl])
+            if (e) cudaEventDestroy(e);
+    }
     delete ss;   // Scratch members free their device buffers stream-ordered
 }
 
@@ -2415,10 +2459,23 @@ int lf_search(const lf_index* idx, const float* d_queries, int64_t Q, const lf_s
         return rc;
     }
     int active = 0;
-    do {
-        rc = lf_search_round(ss, nullptr, nullptr, &active);
-        if (rc) break;
-    } while (active > 0);
+    if (ss->lazy || lf::prefix_orders()) {
+        do {   // host decisions after every round (prediction passes, refills): no pipelining
+            rc = lf_search_round(ss, nullptr, nullptr, &active);
+            if (rc) break;
+        } while (active > 0);
+    } else {
+        // one round in flight ahead of the count read-back: the host never idles the GPU
+        // between rounds; a round enqueued after the last active one finds every query done
+        // and changes nothing
+        rc = lf::session_enqueue(ss, nullptr, nullptr);
+        while (rc == LF_OK) {
+            rc = lf::session_enqueue(ss, nullptr, nullptr);
+            if (rc) break;
+            rc = lf::session_harvest(ss, &active);
+            if (rc || active == 0) break;
+        }
+    }
     if (rc == LF_OK) rc = lf_search_end(ss, d_out_ids, d_out_dists);
     lf_search_free(ss);
     return rc;
