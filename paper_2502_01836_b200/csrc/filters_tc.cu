@@ -21,6 +21,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace lf {
@@ -306,13 +308,14 @@ extern "C" int lf_filter_predict_tc(const float* d_queries, int64_t Q, int32_t m
     if (rc) return rc;
     rc = tc::make_map(&mw, d_W1T, (int64_t)F * m, m, m);
     if (rc) return rc;
+    const int n_mb = (int)((Q + tc::BM - 1) / tc::BM);
     static bool attr_set = false;
     if (!attr_set) {
         LF_CUDA(cudaFuncSetAttribute(tc::filter_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      tc::SMEM_BYTES));
         attr_set = true;
     }
-    const int64_t tiles = (int64_t)F * ((Q + tc::BM - 1) / tc::BM);
+    const int64_t tiles = (int64_t)F * n_mb;
     const int grid = (int)std::min<int64_t>(tiles, sm_count());
     tc::filter_tc_kernel<false><<<grid, tc::THREADS, tc::SMEM_BYTES, as_stream(stream)>>>(
         mx, mw, Q, m, F, d_b1, d_W2, d_b2, d_pred, tc::PairArgs{});
