@@ -364,6 +364,7 @@ def run_ours(args, rank, world, device):
         torch.cuda.cudart().cudaProfilerStart()
     scan_ms, scan_launches, kernels = 0.0, 0, 0
     ea_rows, ea_surv, refills, pred_ms, lazy_pairs, pred_steps = 0.0, 0.0, 0.0, 0.0, 0.0, 0.0
+    stream_b, exact_b = 0.0, 0.0
     with ClockSampler(torch.cuda.current_device()) as clk:
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
@@ -378,6 +379,8 @@ def run_ours(args, rank, world, device):
             pred_ms += prof[10]
             lazy_pairs += prof[11]
             pred_steps += prof[12]
+            stream_b += prof[13]
+            exact_b += prof[14]
             kernels += int(prof[5]) + (0 if args.lazy else 1)    # + the dense filter pass
         ev1.record(stream)
         torch.cuda.synchronize()
@@ -463,9 +466,11 @@ def run_ours(args, rank, world, device):
     # quantisation error) for every scanned series, plus the exact fp32 row (4 B/dim) for
     # the survivors of the bound; the reference reads 4 B/dim for every scanned series.
     ref_bytes = scanned_per_step * tree.m * 4 * args.steps
-    if w["di"].X8 is not None and ea_rows > 0:
-        alg_bytes = ea_rows * (tree.m + 12) + ea_surv * tree.m * 4
-        bytes_def = "series_scanned x (m x 1 B int8 + 12 B) + survivors x m x 4 B"
+    if stream_b > 0:
+        alg_bytes = stream_b + exact_b
+        bytes_def = ("bytes the scan kernels must move, counted in the kernels: per tested row its codes + 16 B "
+                     "metadata (round 0: int8 shadow, m bytes; later rounds: projected shadow, pca_k bytes), plus "
+                     "m x 4 B for every surviving row re-read exactly")
     else:
         alg_bytes = ref_bytes
         bytes_def = "series_scanned x m x 4 B"
@@ -508,7 +513,10 @@ def run_ours(args, rank, world, device):
         "e2e": e2e,
         "gpu_launches": kernels,
         "roofline": {
-            "kernel": "leaf scan (scan_q8_kernel: int8-bounded, exact fp64 survivors)", "bound": "hbm",
+            "kernel": ("leaf scan (scan_q8_kernel round 0, then scan_pq_kernel + survivor_exact_kernel: "
+                       "int8 / projected-int8 bounds, exact fp64 survivors)") if os.environ.get("LF_SCAN_VARIANT") == "pq"
+                      else "leaf scan (scan_q8_kernel: TMA-pipelined int8-bounded scan, exact fp64 survivors)",
+            "bound": "hbm",
             "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
             "peak_source": peak_src,

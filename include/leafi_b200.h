@@ -59,6 +59,15 @@ typedef struct lf_index {
        generation; NULL = unused */
     const int8_t* d_X8b;         /* [n_series][m] rint((x - s1 c1) / (s1 / 128)) */
     const float* d_qmeta2;       /* [n_series][4] |x^|^2, ||c2||, ||x^ - x|| rounded up, 0 */
+    /* optional projected shadow for the two-stage scan (NULL = unused): an orthonormal
+       basis P of pca_k directions (fp64, rows orthonormal), the mean mu, and per row the
+       int8 codes of y = P (x - mu) with {scale, sum code^2, ||scale*code - y|| rounded up,
+       ||(x - mu) - P^T y||} -- ||x - q||^2 = ||y - y_q||^2 + ||r - r_q||^2 */
+    int32_t pca_k;               /* 32 or 64 (0 = no projected shadow) */
+    const double* d_P;           /* [pca_k][m] */
+    const double* d_mu;          /* [m] */
+    const int8_t* d_Xp;          /* [n_series][pca_k] */
+    const float* d_pmeta;        /* [n_series][4] */
 } lf_index;
 
 /* Options of one batched search (tree.py:220-229 search_engine keyword args). */
@@ -91,7 +100,7 @@ typedef struct lf_search_opts {
     const float* d_b2;
 } lf_search_opts;
 
-#define LF_N_PROF 13
+#define LF_N_PROF 15
 #define LF_PROF_BOUNDS_MS 0      /* segment means + node bounds + visit-order sort */
 #define LF_PROF_PLAN_MS 1        /* plan + chunk offsets, all rounds */
 #define LF_PROF_SCAN_MS 2        /* leaf-scan kernel, all rounds */
@@ -105,6 +114,8 @@ typedef struct lf_search_opts {
 #define LF_PROF_PREDICT_MS 10    /* lazy filter inference (pairs, gather, tensor-core GEMM) */
 #define LF_PROF_PAIRS 11         /* (query, leaf) predictions computed lazily */
 #define LF_PROF_PREDICT_STEPS 12 /* lazy inference passes (one after round 0, then on request) */
+#define LF_PROF_SCAN_STREAM_BYTES 13 /* bytes the scans streamed (codes + row metadata, or fp32 rows) */
+#define LF_PROF_SCAN_EXACT_BYTES 14  /* fp32 bytes re-read for exact distances of surviving rows */
 
 /* Optional per-query trace (tree.py:77-83 TraceEntry), capacity n_leaves per query. */
 typedef struct lf_trace {

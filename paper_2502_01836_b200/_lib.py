@@ -39,6 +39,11 @@ class LfIndex(C.Structure):
         ("d_qmeta", C.c_void_p),
         ("d_X8b", C.c_void_p),
         ("d_qmeta2", C.c_void_p),
+        ("pca_k", C.c_int32),
+        ("d_P", C.c_void_p),
+        ("d_mu", C.c_void_p),
+        ("d_Xp", C.c_void_p),
+        ("d_pmeta", C.c_void_p),
     ]
 
 
@@ -62,9 +67,10 @@ class LfSearchOpts(C.Structure):
     ]
 
 
-N_PROF = 13
+N_PROF = 15
 PROF_NAMES = ("bounds_ms", "plan_ms", "scan_ms", "merge_ms", "rounds", "kernels", "total_ms", "refills",
-              "ea_rows", "ea_survivors", "predict_ms", "pairs", "predict_steps")
+              "ea_rows", "ea_survivors", "predict_ms", "pairs", "predict_steps", "scan_stream_bytes",
+              "scan_exact_bytes")
 
 
 class LfTrace(C.Structure):

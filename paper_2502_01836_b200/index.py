@@ -20,6 +20,7 @@ tree.build_index, tree.py:164-189) or adopted from a reference Index object
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -306,6 +307,10 @@ class DeviceIndex:
                 self.qmeta = torch.empty((n_rows, 4), dtype=torch.float32, device=dev)
                 _lib.check(_lib.lib().lf_quantize_rows(self.X.data_ptr(), n_rows, m, self.X8.data_ptr(),
                                                        self.qmeta.data_ptr(), _lib.stream_ptr()))
+            self.pca_k = 0
+            self.P = self.mu = self.Xp = self.pmeta = None
+            if m % 4 == 0 and 64 <= m <= 512 and n_rows >= 256 and os.environ.get("LF_SCAN_VARIANT") == "pq":
+                self.ensure_pca(int(os.environ.get("LF_PCA_K", "32")))      # opt-in two-stage scan
         self.leaf_ids = leaf_ids
         self.leaf_ptr_host = leaf_ptr
         self.slot_of_leaf = {int(l): j for j, l in enumerate(leaf_ids)}
@@ -314,6 +319,43 @@ class DeviceIndex:
     @property
     def n_leaves(self) -> int:
         return int(self.leaf_ids.shape[0])
+
+    def ensure_pca(self, k: int = 32, sample: int = 200_000, seed: int = 0) -> None:
+        """Projected shadow for the two-stage scan (lf_index.d_Xp): the top-k principal
+        directions of a row sample (fp64 SVD, orthonormal rows), and per row the int8
+        codes of y = P (x - mu) with {scale, sum code^2, code error (rounded up),
+        residual norm}.  Index-build plumbing in torch; the search reads it in the
+        scan kernel."""
+        import torch
+
+        if k not in (32, 64):
+            raise ValueError("pca_k must be 32 or 64")
+        X = self.X
+        n, m = int(X.shape[0]), int(X.shape[1])
+        with torch.cuda.device(self.device):
+            g = torch.Generator(device=self.device)
+            g.manual_seed(seed)
+            pick = torch.randint(0, n, (min(sample, n),), generator=g, device=self.device)
+            S = X[pick].double()
+            mu = S.mean(0)
+            _, _, V = torch.linalg.svd(S - mu, full_matrices=False)
+            P = V[:k].contiguous()
+            codes = torch.empty((n, k), dtype=torch.int8, device=self.device)
+            meta = torch.empty((n, 4), dtype=torch.float32, device=self.device)
+            inf32 = torch.tensor(float("inf"), dtype=torch.float32, device=self.device)
+            for r0 in range(0, n, 1 << 20):
+                A = X[r0:r0 + (1 << 20)].double() - mu
+                y = A @ P.T
+                r = (A - y @ P).norm(dim=1)
+                s32 = (y.abs().amax(1) / 127).float()
+                s32 = torch.where(s32 > 0, s32, torch.ones_like(s32))
+                c = torch.round(y / s32.double()[:, None]).clamp(-127, 127)
+                e = ((c * s32.double()[:, None] - y).norm(dim=1) * (1 + 1e-9) + 1e-30)
+                e32 = e.float()
+                e32 = torch.where(e32.double() < e, torch.nextafter(e32, inf32), e32)      # rounded up
+                codes[r0:r0 + (1 << 20)] = c.to(torch.int8)
+                meta[r0:r0 + (1 << 20)] = torch.stack([s32, (c * c).sum(1).float(), e32, r.float()], dim=1)
+        self.pca_k, self.P, self.mu, self.Xp, self.pmeta = k, P, mu.contiguous(), codes, meta
 
     def ensure_level2(self) -> bool:
         """Build the second-level residual codes (training-data generation only; m x 1 B
@@ -358,4 +400,8 @@ class DeviceIndex:
             s.d_X8, s.d_qmeta = self.X8.data_ptr(), self.qmeta.data_ptr()
         if getattr(self, "X8b", None) is not None:
             s.d_X8b, s.d_qmeta2 = self.X8b.data_ptr(), self.qmeta2.data_ptr()
+        if getattr(self, "Xp", None) is not None:
+            s.pca_k = self.pca_k
+            s.d_P, s.d_mu = self.P.data_ptr(), self.mu.data_ptr()
+            s.d_Xp, s.d_pmeta = self.Xp.data_ptr(), self.pmeta.data_ptr()
         return s

@@ -517,3 +517,32 @@ def test_grouped_scan_identical(k, monkeypatch):
     np.testing.assert_array_equal(got.ids, ref.ids)
     np.testing.assert_array_equal(got.dists, ref.dists)
     np.testing.assert_array_equal(got.stats, ref.stats)
+
+
+@pytest.mark.parametrize("m,pk", [(64, 32), (96, 32), (256, 32), (256, 64), (320, 64)])
+@pytest.mark.parametrize("k", [1, 3])
+def test_projected_scan_exact(m, pk, k, monkeypatch):
+    """Two-stage scan over the projected shadow (int8 codes of the top principal
+    coordinates + residual norms) == the full fp64 scan: ids, distances, counters;
+    with duplicate rows, an all-zero row and queries equal to rows."""
+    from paper_2502_01836_b200 import build_index, search_batch
+
+    data = lo.randwalk(9000, m, 140 + m)
+    data[100:110] = data[7]
+    data[200] = 0.0
+    t = build_index(data, 700)
+    di = t.device()
+    if pk != di.pca_k:
+        di.ensure_pca(pk)
+    assert di.pca_k == pk
+    Q = np.concatenate([lo.noisy_queries(data, 10, nz, 90 + int(10 * nz)) for nz in (0.1, 0.3)]
+                       + [data[[7, 200, 4321]].astype(np.float64)])
+    monkeypatch.setenv("LF_SCAN_VARIANT", "full")
+    ref = search_batch(t, Q, k)
+    monkeypatch.setenv("LF_SCAN_VARIANT", "pq")
+    prof = np.zeros(16)
+    got = search_batch(t, Q, k, profile=prof)
+    np.testing.assert_array_equal(got.ids, ref.ids)
+    np.testing.assert_allclose(got.dists, ref.dists, rtol=1e-14)
+    np.testing.assert_array_equal(got.stats, ref.stats)
+    assert prof[8] > 0 and prof[9] < prof[8], "the projected bound must run and drop rows"

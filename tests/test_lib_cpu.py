@@ -41,7 +41,7 @@ def test_struct_layouts_match_header():
     import ctypes as C
     from paper_2502_01836_b200 import _lib
 
-    assert C.sizeof(_lib.LfIndex) == 8 + 4 * 4 + 8 + 2 * 4 * 64 + 11 * 8
+    assert C.sizeof(_lib.LfIndex) == 8 + 4 * 4 + 8 + 2 * 4 * 64 + 11 * 8 + 8 + 4 * 8
     assert C.sizeof(_lib.LfTrace) == 6 * 8
 
 

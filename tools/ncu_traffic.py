@@ -35,15 +35,20 @@ for k, v in per.items():
 b = json.loads([l for l in open(bench_path) if l.startswith("{")][-1])
 alg = b["roofline"]["algorithmic_bytes_per_step"]
 n = len(launches)
+# one scan phase per round: its streaming kernel (scan_q8 / scan_pq) plus, after scan_pq,
+# the survivor_exact kernel -- bench.py's "achieved" and "traffic" are per phase
+rounds = sum(1 for x in launches if "survivor_exact" not in x["kernel"])
 tot = sum(x["dram_read_bytes"] + x["dram_write_bytes"] for x in launches)
 out = {
     "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum, every scan "
               "launch of one timed bench step (tools/ncu_capture.sh)",
     "launches_per_step": n,
+    "scan_phases_per_step": rounds,
     "dram_bytes_per_step": tot,
-    "dram_bytes_per_launch": tot / max(n, 1),
+    "dram_bytes_per_launch": tot / max(rounds, 1),
+    "dram_bytes_per_launch_definition": "per scan phase (round): streaming kernel + survivor re-check kernel",
     "algorithmic_bytes_per_step": alg,
-    "algorithmic_bytes_per_launch": alg / max(n, 1),
+    "algorithmic_bytes_per_launch": alg / max(rounds, 1),
     "traffic_over_algorithmic": tot / alg if alg else None,
     "scan_ns_serialised_per_step": sum(x["ns"] for x in launches),
     "launches": launches,
