@@ -1032,8 +1032,10 @@ struct Q8Cfg {
     static constexpr int LO_OFF = BAR_OFF + 2 * STAGES * 8;
     static constexpr int SR_OFF = LO_OFF + CH * 4;
     static constexpr int SD_OFF = SR_OFF + CH * 4;
-    static constexpr int MISC_OFF = SD_OFF + CH * 8;
-    static constexpr int SMEM = MISC_OFF + 16;
+    static constexpr int HI_OFF = SD_OFF + CH * 8;                   // upper ends (k > 1)
+    static constexpr int HIST_OFF = HI_OFF + CH * 4;                 // 256-bin radix-select histogram
+    static constexpr int MISC_OFF = HIST_OFF + 256 * 4;
+    static constexpr int SMEM = MISC_OFF + 32;
 };
 
 __device__ __forceinline__ uint32_t q8_su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -1080,6 +1082,9 @@ __global__ void __launch_bounds__(Q8_THREADS, 2) scan_q8_kernel(RoundState s, lf
     double* surv_d = reinterpret_cast<double*>(q8_smem + Cfg::SD_OFF);
     unsigned int* hi_bits = reinterpret_cast<unsigned int*>(q8_smem + Cfg::MISC_OFF);   // [2], by task parity
     int* n_surv = reinterpret_cast<int*>(hi_bits + 2);                                 // [2]
+    unsigned int* sel = reinterpret_cast<unsigned int*>(n_surv + 2);                  // [2] radix-select state
+    float* hi_s = reinterpret_cast<float*>(q8_smem + Cfg::HI_OFF);
+    int* hist = reinterpret_cast<int*>(q8_smem + Cfg::HIST_OFF);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
@@ -1203,7 +1208,10 @@ __global__ void __launch_bounds__(Q8_THREADS, 2) scan_q8_kernel(RoundState s, lf
                 const float lo = (sqrtf(fmaxf(d2 - tol, 0.f)) - e) * (1.f - 1e-6f);
                 const float hi = (sqrtf(fmaxf(d2 + tol, 0.f)) + e) * (1.f + 1e-6f);
                 hmin = fminf(hmin, hi);
-                if ((hl & 3) == 0) lo_s[j + myrow] = lo;
+                if ((hl & 3) == 0) {
+                    lo_s[j + myrow] = lo;
+                    if (s.k > 1) hi_s[j + myrow] = hi;
+                }
             }
             __syncwarp();
             if (lane == 0) q8_arrive(&empty[slot]);
@@ -1215,10 +1223,53 @@ __global__ void __launch_bounds__(Q8_THREADS, 2) scan_q8_kernel(RoundState s, lf
             if (lane == 0) atomicMin(&hi_bits[par], __float_as_uint(hmin));
         }
         q8_cons_sync();
+        float kth_hi = __int_as_float(0x7f800000);
+        if (s.k > 1 && s.kc <= nrows && !(bsf < kInf)) {
+            // no k-th best yet: the task's kc-th smallest upper end bounds its kc-th best distance
+            // (radix select over the upper ends' bits, which order like the non-negative floats)
+            unsigned prefix = 0, mask = 0;
+            int rem = s.kc;
+            for (int shift = 24; shift >= 0; shift -= 8) {
+                hist[ctid] = 0;
+                q8_cons_sync();
+                for (int r = ctid; r < nrows; r += Q8_CONS) {
+                    const unsigned key = __float_as_uint(hi_s[r]);
+                    if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
+                }
+                q8_cons_sync();
+                if (cw == 0) {
+                    int c[8], sum = 0;
+#pragma unroll
+                    for (int jj = 0; jj < 8; ++jj) { c[jj] = hist[lane * 8 + jj]; sum += c[jj]; }
+                    int incl = sum;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const int v = __shfl_up_sync(0xffffffffu, incl, d);
+                        if (lane >= d) incl += v;
+                    }
+                    const int excl = incl - sum;
+                    if (excl < rem && rem <= incl) {
+                        int acc = excl, b = 7;
+                        for (int jj = 0; jj < 8; ++jj) {
+                            if (acc + c[jj] >= rem) { b = jj; break; }
+                            acc += c[jj];
+                        }
+                        sel[0] = prefix | ((unsigned)(lane * 8 + b) << shift);
+                        sel[1] = (unsigned)(rem - acc);
+                    }
+                }
+                q8_cons_sync();
+                prefix = sel[0];
+                rem = (int)sel[1];
+                mask |= 255u << shift;
+            }
+            kth_hi = __uint_as_float(prefix);
+        }
         // ---- survivors
         {
             double thr = bsf;
             if (s.k == 1) thr = fmin(thr, (double)__uint_as_float(hi_bits[par]));
+            else thr = fmin(thr, (double)kth_hi);
             const float thr_f = thr < kInf ? __double2float_ru(thr) : __int_as_float(0x7f800000);
             for (int r = ctid; r < nrows; r += Q8_CONS)
                 if (lo_s[r] <= thr_f) surv_r[atomicAdd(&n_surv[par], 1)] = r;
