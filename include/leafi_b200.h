@@ -307,6 +307,17 @@ int lf_quantize_rows(const float* d_X, int64_t n, int32_t m, int8_t* d_X8, float
 int lf_quantize_rows2(const float* d_X, int64_t n, int32_t m, const int8_t* d_X8, const float* d_qmeta,
                       int8_t* d_X8b, float* d_qmeta2, void* stream);
 
+/*
+ * Conformal auto-tuner fitting (conformal.py:171-198 simulate_search, for R offset
+ * vectors at once): the calibration skeleton in visit order -- bounds, leaf minimum
+ * distances, predictions (NaN: no filter), filter slots (-1: none), all [nq][L] --
+ * and offsets [R][F]; out [R][nq] = the distance each calibration query's filtered
+ * search reaches.  Bit-identical to the host replay (comparisons and minima only).
+ */
+int lf_replay_offsets(const double* d_lb, const double* d_dl, const double* d_pred, const int32_t* d_slot,
+                      int64_t nq, int32_t L, const double* d_offsets, int64_t R, int32_t F, double* d_out,
+                      void* stream);
+
 /* Segment means for host rows (summarize_matrix, summarize.py:52-56), numpy order. */
 int lf_paa_host(const float* h_values, int64_t n, int32_t m, int32_t n_seg, double* h_out,
                 int32_t n_threads);

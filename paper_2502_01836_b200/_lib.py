@@ -118,6 +118,7 @@ SIGNATURES = {
     "lf_tree_build_from_summaries": (_P, [_P, _I64, _I32, _I64]),
     "lf_paa_device": (C.c_int, [_P, _I64, _I32, _I32, _P, _P]),
     "lf_quantize_rows": (C.c_int, [_P, _I64, _I32, _P, _P, _P]),
+    "lf_replay_offsets": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _P, _I64, _I32, _P, _P]),
     "lf_quantize_rows2": (C.c_int, [_P, _I64, _I32, _P, _P, _P, _P, _P]),
 }
 

@@ -28,7 +28,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .calibration import build_skeleton, compute_alphas, fit_auto_tuners, tune
+from .calibration import DeviceReplay, build_skeleton, compute_alphas, fit_auto_tuners, tune
 from .engine import SearchOutcome, as_tree, search_batch
 from .filters import FilterPack
 from .synth import generate_global_queries, generate_local_queries
@@ -347,7 +347,7 @@ def enhance(index, plan: SplitPlan, budget: SelectionBudget, seed: int, *,
         alphas = {lid: compute_alphas(preds[lid], gts.dl_selected[pool:, s]) for s, lid in enumerate(selected)}
         sk = build_skeleton(gts.lb_matrix[pool:], gts.dl_calib_full, gts.visit_order[pool:],
                             gts.nn_distance[pool:], gts.leaf_ids, selected, preds)
-        curves = fit_auto_tuners(sk, alphas)
+        curves = fit_auto_tuners(sk, alphas, replay=DeviceReplay(sk))          # GPU replay, SURVEY §8(f)1
         begin("done")
         e = EnhancedIndex(t, filters, curves, plan, budget, constants, report, reports, pack=pack)
         e.global_set = gts

@@ -243,3 +243,27 @@ def test_sharded_tdg_columns_concatenate():
         np.testing.assert_array_equal(np.concatenate(parts, axis=1), full)
     _, g1, _ = sharded_leaf_min_distances(t, Q, 0, 1)
     np.testing.assert_array_equal(g1.cpu().numpy(), full)
+
+
+def test_device_replay_bit_identical():
+    """lf_replay_offsets == the host replay (conformal.py:171-198 twin) for many offset
+    vectors (including an all-infinite one), and GPU-fitted curves equal host-fitted ones."""
+    from paper_2502_01836_b200 import calibration as cal
+
+    rng = np.random.default_rng(0)
+    nq, L, F = 60, 40, 12
+    lb = np.sort(rng.uniform(0, 5, (nq, L)), axis=1)
+    dl = lb + rng.uniform(0, 3, (nq, L))
+    slot = rng.integers(-1, F, (nq, L)).astype(np.int32)
+    pred = np.where(slot >= 0, dl + rng.normal(0, 1, (nq, L)), np.nan)
+    sk = cal.CalibrationSkeleton(lb, dl, pred, slot, dl.min(axis=1))
+    rows = rng.uniform(0, 2, (97, F))
+    rows[3] = np.inf
+    dev = cal.DeviceReplay(sk)
+    np.testing.assert_array_equal(dev(rows), cal.replay_many(sk, rows))
+    alphas = {l: np.sort(rng.uniform(0, 2, nq))[::-1] for l in range(F)}
+    a = cal.fit_auto_tuners(sk, alphas)
+    b = cal.fit_auto_tuners(sk, alphas, replay=dev)
+    for l in a:
+        np.testing.assert_array_equal(a[l].knot_quality, b[l].knot_quality)
+        np.testing.assert_array_equal(a[l].knot_offset, b[l].knot_offset)
