@@ -603,7 +603,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--n", type=int, default=25_000_000)
+    ap.add_argument("--n", "--rows", dest="n", type=int, default=25_000_000)
     ap.add_argument("--m", type=int, default=256)
     ap.add_argument("--leaf-cap", type=int, default=10_000)
     ap.add_argument("--queries", type=int, default=1000)
@@ -640,10 +640,15 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    device = torch.device("cuda", local)
+    dev_index = local % max(1, torch.cuda.device_count())     # > 1 rank per GPU only in functional tests
+    torch.cuda.set_device(dev_index)
+    device = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        backend = os.environ.get("LF_DIST_BACKEND", "nccl")   # gloo: functional test of N ranks on one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
     if args.impl == "reference":
         if rank != 0:
             if world > 1:
