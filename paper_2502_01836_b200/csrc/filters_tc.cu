@@ -36,7 +36,7 @@ constexpr int A_BYTES = BM * BK * 4;          // 16 KiB
 constexpr int B_BYTES_MAX = 256 * BK * 4;     // 32 KiB (N = m <= 256)
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES_MAX;
 constexpr int TMEM_COLS = 512;                // 2 accumulator buffers x 256 columns
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + 4096 /*b1, W2 x 2*/;
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -126,7 +126,7 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
                  int64_t Q, int m, int F, const float* __restrict__ b1, const float* __restrict__ W2,
                  const float* __restrict__ b2, float* __restrict__ pred, PairArgs pa) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
@@ -209,12 +209,14 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
             }
         }
     } else {                                                 // ---- epilogue (warps 2..5)
+        // b1[f] / W2[f] (2 x m floats) are staged in shared memory one tile ahead with
+        // cp.async by the 128 epilogue threads: each tile is a new filter for this CTA,
+        // so reading them with per-column global loads paid an L2 round trip per chunk.
+        const int et = threadIdx.x - 64;                     // 0..127
         const int quarter = warp & 3;                        // TMEM lanes [32*quarter, +32)
         const int row = quarter * 32 + lane;
-        int acc = 0;
-        uint32_t acc_phase = 0;
-        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-            int f, row0, nrows;
+        float* pbuf = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);   // [2][2][256]
+        auto tile_filter = [&](int64_t t, int& f, int& row0, int& nrows) {
             if (PAIRS) {
                 const int4 tl = pa.tiles[t];
                 f = tl.x;
@@ -225,10 +227,35 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
                 row0 = (int)(t % n_mb) * BM;
                 nrows = BM;
             }
+        };
+        auto stage_params = [&](int64_t t, int slot) {
+            if (t < n_tiles) {
+                int f, r0, nr;
+                tile_filter(t, f, r0, nr);
+                const int chunks = m >> 2;                   // 16-byte chunks per vector
+                if (et < 2 * chunks) {
+                    const float* src = (et < chunks ? b1 + (int64_t)f * m + et * 4
+                                                    : W2 + (int64_t)f * m + (et - chunks) * 4);
+                    float* dst = pbuf + slot * 512 + (et < chunks ? et * 4 : 256 + (et - chunks) * 4);
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(su32(dst)), "l"(src) : "memory");
+                }
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        int slot = 0;
+        stage_params(blockIdx.x, 0);
+        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+            int f, row0, nrows;
+            tile_filter(t, f, row0, nrows);
+            stage_params(t + gridDim.x, slot ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+            asm volatile("bar.sync 1, 128;" ::: "memory");   // this tile's parameters visible
+            const float4* b1s = reinterpret_cast<const float4*>(pbuf + slot * 512);
+            const float4* w2s = reinterpret_cast<const float4*>(pbuf + slot * 512 + 256);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            const float* b1f = b1 + (int64_t)f * m;
-            const float* w2f = W2 + (int64_t)f * m;
             float part = 0.f;
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * 256);
             for (int c0 = 0; c0 < m; c0 += 32) {
@@ -236,9 +263,16 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
                 LF_TMEM_LD32(taddr + (uint32_t)c0, r);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const float h = fmaxf(__fadd_rn(__uint_as_float(r[j]), __ldg(b1f + c0 + j)), 0.f);
-                    part = __fmaf_rn(h, __ldg(w2f + c0 + j), part);
+                for (int j4 = 0; j4 < 8; ++j4) {
+                    const float4 bb = b1s[(c0 >> 2) + j4];
+                    const float4 ww = w2s[(c0 >> 2) + j4];
+                    const float bv[4] = {bb.x, bb.y, bb.z, bb.w};
+                    const float wv[4] = {ww.x, ww.y, ww.z, ww.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const float h = fmaxf(__fadd_rn(__uint_as_float(r[j4 * 4 + u]), bv[u]), 0.f);
+                        part = __fmaf_rn(h, wv[u], part);
+                    }
                 }
             }
             tc_fence_before();
@@ -254,8 +288,11 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
                 const int64_t q = (int64_t)row0 + row;
                 if (q < Q) pred[q * F + f] = __fadd_rn(part, b2[f]);
             }
+            asm volatile("bar.sync 1, 128;" ::: "memory");   // slot free for the tile after next
+            slot ^= 1;
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     tc_fence_before();
     __syncthreads();
@@ -301,7 +338,9 @@ extern "C" int lf_filter_predict_tc(const float* d_queries, int64_t Q, int32_t m
     using namespace lf;
     LF_REQUIRE(Q >= 0 && F >= 0, "bad sizes");
     LF_REQUIRE(m >= 32 && m <= 256 && m % 32 == 0, "tensor-core filter path needs m in {32, 64, ..., 256}");
-    LF_REQUIRE(((uintptr_t)d_queries & 15) == 0 && ((uintptr_t)d_W1T & 15) == 0, "operands must be 16-byte aligned");
+    LF_REQUIRE(((uintptr_t)d_queries & 15) == 0 && ((uintptr_t)d_W1T & 15) == 0 && ((uintptr_t)d_b1 & 15) == 0 &&
+                   ((uintptr_t)d_W2 & 15) == 0,
+               "operands must be 16-byte aligned");
     if (Q == 0 || F == 0) return LF_OK;
     CUtensorMap mx, mw;
     int rc = tc::make_map(&mx, d_queries, Q, m, tc::BM);
@@ -382,6 +421,7 @@ extern "C" int lf_filter_predict_pairs_tc(const float* d_queries, int32_t m, con
     using namespace lf;
     LF_REQUIRE(m >= 32 && m <= 256 && m % 32 == 0, "tensor-core filter path needs m in {32, 64, ..., 256}");
     LF_REQUIRE(P >= 0 && F >= 1, "bad sizes");
+    LF_REQUIRE(((uintptr_t)d_b1 & 15) == 0 && ((uintptr_t)d_W2 & 15) == 0, "b1 / W2 must be 16-byte aligned");
     if (P == 0) return LF_OK;
     cudaStream_t st = as_stream(stream);
     Scratch hist, fcur, tiles, ntiles, dst, rows;

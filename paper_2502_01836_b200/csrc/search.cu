@@ -971,8 +971,9 @@ static int check_args(const lf_index* idx, int64_t Q, const lf_search_opts* opts
                "filter predictions need offsets and a leaf->filter map");
     LF_REQUIRE(opts->d_W1T == nullptr || opts->d_pred != nullptr || opts->d_pred_f64 != nullptr ||
                    (opts->d_b1 != nullptr && opts->d_W2 != nullptr && opts->d_b2 != nullptr && idx->m % 32 == 0 &&
-                    idx->m >= 32 && idx->m <= 256 && opts->n_filters >= 1),
-               "lazy filter inference needs W1T, b1, W2, b2 and m in {32, 64, ..., 256}");
+                    idx->m >= 32 && idx->m <= 256 && opts->n_filters >= 1 && ((uintptr_t)opts->d_b1 & 15) == 0 &&
+                    ((uintptr_t)opts->d_W2 & 15) == 0),
+               "lazy filter inference needs W1T, b1, W2, b2 (16-byte aligned) and m in {32, 64, ..., 256}");
     LF_REQUIRE(opts->sequential || opts->max_round_leaves >= 1, "max_round_leaves must be >= 1");
     return LF_OK;
 }
