@@ -477,6 +477,10 @@ def run_ours(args, rank, world, device):
     achieved = alg_bytes / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else None
     ref_equiv = ref_bytes / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else None
     traffic, _ = ncu_traffic()
+    di = w.get("di")
+    pca_k = int(getattr(di, "pca_k", 0) or 0)
+    pca_energy = getattr(di, "pca_energy", None)
+    pq_on = pca_k > 0 and os.environ.get("LF_SCAN_VARIANT") in (None, "", "pq")
     line = {
         "metric": metric_name(args),
         "value": value,
@@ -513,9 +517,11 @@ def run_ours(args, rank, world, device):
         "e2e": e2e,
         "gpu_launches": kernels,
         "roofline": {
-            "kernel": ("leaf scan (scan_q8_kernel round 0, then scan_pq_kernel + survivor_exact_kernel: "
-                       "int8 / projected-int8 bounds, exact fp64 survivors)") if os.environ.get("LF_SCAN_VARIANT") == "pq"
+            "kernel": ("leaf scan (scan_q8_kernel round 0, then scan_pq_kernel -> pq_over_exact_kernel -> "
+                       "pq_select_kernel: int8 / projected-int8 bounds, exact fp64 survivors)") if pq_on
                       else "leaf scan (scan_q8_kernel: TMA-pipelined int8-bounded scan, exact fp64 survivors)",
+            "projected_shadow": {"pca_k": pca_k, "energy": pca_energy,
+                                 "used": pq_on} if pca_k or pca_energy is not None else None,
             "bound": "hbm",
             "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
@@ -597,7 +603,7 @@ def run_reference(args, rank, world, device):
     }
 
 
-def main():
+def make_parser():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -629,7 +635,11 @@ def main():
                     help="lazy filter inference inside lf_search instead of the dense pass")
     ap.add_argument("--ncu", action="store_true",
                     help="bracket the timed steps with cudaProfilerStart/Stop (ncu --profile-from-start off)")
-    args = ap.parse_args()
+    return ap
+
+
+def main():
+    args = make_parser().parse_args()
     if args.warmup < 3:
         log("warmup raised to 3 (timing rule)")
         args.warmup = 3

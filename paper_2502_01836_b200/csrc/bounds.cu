@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "bounds.cuh"
 #include "common.cuh"
@@ -126,6 +127,87 @@ __device__ inline double node_bound(const double* qs, const double* ws, int ns, 
     return sqrt(acc);
 }
 
+// ITEMS bounds per thread for nodes first, first + stride, ... (striped, so each
+// warp load is 256 contiguous bytes of one segment's envelope row).  Segments
+// are the OUTER loop: all 2 x ITEMS loads of a segment are in flight together
+// instead of one dependent L2 round trip per (node, segment).  Each node's FMA
+// chain still runs over segments in order -- bit-identical to node_bound.
+template <int ITEMS>
+__device__ __forceinline__ void node_bounds_striped(const double* qs, const double* ws, int ns,
+                                                    const double* __restrict__ env_min,
+                                                    const double* __restrict__ env_max, int n_env, int first,
+                                                    int stride, double (&lb)[ITEMS]) {
+    double acc[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) acc[i] = 0.0;
+    for (int sg = 0; sg < ns; ++sg) {
+        const double qv = qs[sg], wv = ws[sg];
+        const double* mnp = env_min + (int64_t)sg * n_env;
+        const double* mxp = env_max + (int64_t)sg * n_env;
+        double mn[ITEMS], mx[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const int node = first + i * stride;
+            mn[i] = node < n_env ? __ldg(mnp + node) : 0.0;
+            mx[i] = node < n_env ? __ldg(mxp + node) : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            double g = fmax(mn[i] - qv, qv - mx[i]);
+            g = fmax(g, 0.0);
+            acc[i] = __fma_rn(__dmul_rn(wv, g), g, acc[i]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) lb[i] = sqrt(acc[i]);
+}
+
+// put_record for ITEMS visit positions per thread (p = first + i * stride), the
+// dependent loads (node -> leaf -> filter -> prediction, offset) issued level by
+// level across all ITEMS positions so their latencies overlap.
+template <int ITEMS>
+__device__ __forceinline__ void put_records_striped(const OrderArgs& o, const lf_index& idx, int64_t q, int Nn,
+                                                    int first, int stride, const unsigned* key_hi,
+                                                    const int* node_at, const unsigned* lo_by_node) {
+    int node[ITEMS], leaf[ITEMS], fs[ITEMS];
+    const bool filt = idx.d_leaf_filter != nullptr && (o.pred != nullptr || o.pred64 != nullptr || o.lazy);
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const int p = first + i * stride;
+        node[i] = p < Nn ? node_at[p] : -1;
+    }
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) leaf[i] = node[i] >= 0 ? __ldg(idx.d_node_leaf + node[i]) : -1;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) fs[i] = (filt && leaf[i] >= 0) ? __ldg(idx.d_leaf_filter + leaf[i]) : -1;
+    double pv[ITEMS], off[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        pv[i] = 0.0;
+        off[i] = 0.0;
+        if (fs[i] >= 0 && !o.lazy) {
+            pv[i] = o.pred64 != nullptr ? o.pred64[q * o.F + fs[i]] : (double)o.pred[q * o.F + fs[i]];
+            off[i] = o.offset[fs[i]];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const int p = first + i * stride;
+        if (p >= Nn) continue;
+        const int64_t at = q * Nn + p;
+        o.lbs[at] = __hiloint2double((int)key_hi[p], (int)lo_by_node[node[i]]);
+        o.order[at] = node[i];
+        int rec = leaf[i];
+        double a = -kInf;
+        if (fs[i] >= 0) {
+            rec |= LF_REC_HASF;
+            a = o.lazy ? __longlong_as_double(0x7ff8000000000000LL) : pv[i] - off[i];
+        }
+        o.leafo[at] = rec;
+        o.adj[at] = a;
+    }
+}
+
 // Fused K1 + K2 for trees of up to 8192 nodes, FULL order: one CTA per query
 // computes every node's search bound straight into registers and sorts the
 // nodes in shared memory -- the bound matrix never round-trips through HBM.
@@ -166,27 +248,41 @@ __global__ void __launch_bounds__(FS_THREADS, 1) bounds_sort_kernel(const double
         ws[threadIdx.x] = (double)idx.seg_width[threadIdx.x];
     }
     __syncthreads();
+    {
+        double lb[ITEMS];
+        node_bounds_striped<ITEMS>(qs, ws, ns, idx.d_env_min, idx.d_env_max, n_env, threadIdx.x, FS_THREADS, lb);
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const int node = i * FS_THREADS + threadIdx.x;
+            if (node < n_env) {
+                sm.u.out.key[node] = (unsigned)__double2hiint(lb[i]);
+                sm.lo[node] = (unsigned)__double2loint(lb[i]);
+            }
+        }
+    }
+    __syncthreads();
     unsigned keys[ITEMS];
     int vals[ITEMS];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         const int node = threadIdx.x * ITEMS + i;          // blocked arrangement: stable sort keeps id order
         if (node < n_env) {
-            const double lb = node_bound(qs, ws, ns, idx.d_env_min, idx.d_env_max, n_env, node);
-            keys[i] = (unsigned)__double2hiint(lb);
-            sm.lo[node] = (unsigned)__double2loint(lb);
+            keys[i] = sm.u.out.key[node];
             vals[i] = node;
         } else {
             keys[i] = 0xFFFFFFFFu;                         // padding sorts last (real keys <= +inf's 0x7FF00000)
             vals[i] = INT_MAX;
         }
     }
-    typename Sm::Sort(sm.u.sort).Sort(keys, vals);
+    __syncthreads();                                       // the sort's temp storage overlays out.key
+    // Bit 31 (the sign of a non-negative bound) is always 0 -- padding's 0x7FFFFFFF in
+    // the low 31 bits still sorts after +inf's 0x7FF00000.  Striped output: conflict-free stores.
+    typename Sm::Sort(sm.u.sort).SortBlockedToStriped(keys, vals, 0, 31);
     __syncthreads();                                       // temp storage is reused below
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-        sm.u.out.key[threadIdx.x * ITEMS + i] = keys[i];
-        sm.u.out.node[threadIdx.x * ITEMS + i] = vals[i];
+        sm.u.out.key[i * FS_THREADS + threadIdx.x] = keys[i];
+        sm.u.out.node[i * FS_THREADS + threadIdx.x] = vals[i];
     }
     __syncthreads();
     for (int p = threadIdx.x; p < n_env; p += FS_THREADS) {   // exact order inside runs of equal high words
@@ -210,10 +306,7 @@ __global__ void __launch_bounds__(FS_THREADS, 1) bounds_sort_kernel(const double
         }
     }
     __syncthreads();
-    for (int p = threadIdx.x; p < n_env; p += FS_THREADS) {
-        const int node = sm.u.out.node[p];
-        put_record(o, idx, q, n_env, p, __hiloint2double((int)sm.u.out.key[p], (int)sm.lo[node]), node);
-    }
+    put_records_striped<ITEMS>(o, idx, q, n_env, threadIdx.x, FS_THREADS, sm.u.out.key, sm.u.out.node, sm.lo);
     if (threadIdx.x == 0) {
         o.olen[q] = n_env;
         if (o.only != nullptr) o.only[q] = 0;
@@ -254,11 +347,11 @@ __global__ void __launch_bounds__(PF_THREADS, 1) prefix_order_kernel(const doubl
     __syncthreads();
     double key[PF_ITEMS];
     unsigned k32[PF_ITEMS];
+    node_bounds_striped<PF_ITEMS>(qs, ws, ns, idx.d_env_min, idx.d_env_max, Nn, tid, PF_THREADS, key);
 #pragma unroll
     for (int i = 0; i < PF_ITEMS; ++i) {
-        const int node = tid * PF_ITEMS + i;
+        const int node = i * PF_THREADS + tid;             // striped; the bitonic sort orders by (lb, id)
         if (node < Nn) {
-            key[i] = node_bound(qs, ws, ns, idx.d_env_min, idx.d_env_max, Nn, node);
             k32[i] = (unsigned)__double2hiint(key[i]);     // lb >= 0: monotone in lb
         } else {
             key[i] = kInf;
@@ -323,7 +416,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) prefix_order_kernel(const doubl
         if (take && k32[i] <= T) {
             const int pos = atomicAdd(&s_cnt, 1);
             sk[pos] = key[i];
-            sv[pos] = tid * PF_ITEMS + i;
+            sv[pos] = i * PF_THREADS + tid;
         }
     __syncthreads();
     const int cnt = s_cnt;
@@ -373,11 +466,28 @@ static int launch_fused(const double* d_qsumm, int64_t Q, const lf_index& idx, i
     return LF_OK;
 }
 
+static int sort_radix_bits() {                         // LF_SORT_RB: digit width of the block sort (4..7)
+    const char* e = std::getenv("LF_SORT_RB");
+    const int rb = e != nullptr ? std::atoi(e) : 5;
+    return rb >= 4 && rb <= 7 ? rb : 5;
+}
+
+template <int ITEMS>
+static int launch_fused_rb(const double* d_qsumm, int64_t Q, const lf_index& idx, int n, const OrderArgs& oa,
+                           cudaStream_t st) {
+    switch (sort_radix_bits()) {
+        case 5: return launch_fused<ITEMS, 5>(d_qsumm, Q, idx, n, oa, st);
+        case 6: return launch_fused<ITEMS, 6>(d_qsumm, Q, idx, n, oa, st);
+        case 7: return launch_fused<ITEMS, 7>(d_qsumm, Q, idx, n, oa, st);
+        default: return launch_fused<ITEMS, 4>(d_qsumm, Q, idx, n, oa, st);
+    }
+}
+
 static int launch_full_fused(const double* d_qsumm, int64_t Q, const lf_index& idx, int n, const OrderArgs& oa,
                              cudaStream_t st) {
-    if (n <= FS_THREADS * 4) return launch_fused<4>(d_qsumm, Q, idx, n, oa, st);
-    if (n <= FS_THREADS * 8) return launch_fused<8>(d_qsumm, Q, idx, n, oa, st);
-    return launch_fused<16>(d_qsumm, Q, idx, n, oa, st);
+    if (n <= FS_THREADS * 4) return launch_fused_rb<4>(d_qsumm, Q, idx, n, oa, st);
+    if (n <= FS_THREADS * 8) return launch_fused_rb<8>(d_qsumm, Q, idx, n, oa, st);
+    return launch_fused_rb<16>(d_qsumm, Q, idx, n, oa, st);
 }
 
 // Segment means + bounds + per-query visit-order records in as few passes as the

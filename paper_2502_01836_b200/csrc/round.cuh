@@ -165,11 +165,19 @@ cudaError_t launch_chunk_base(const lf_index& idx, int* cbase, cudaStream_t st);
 cudaError_t launch_grouped_scan(const RoundState& s, const lf_index& idx, const float* q, const int8_t* qc8,
                                 const float4* qm8, const GroupScratch& g, int64_t max_tasks, cudaStream_t st);
 // scan_pq.cu: projected two-stage scan
-constexpr int PQ_SQ = 64;                     // survivors of a task handed to survivor_exact_kernel
 cudaError_t launch_project_queries(const float* q, int64_t Q, const lf_index& idx, int8_t* qc, float4* qm,
                                    cudaStream_t st);
+// Survivors of the projected scan: (task, row) entries, re-read row-parallel.
+struct PQOverflow {
+    int2* ent;                                // [cap] (task, row in chunk); task < 0: unused slot
+    double* dist;                             // [cap] exact distances
+    int* n;                                   // entries claimed this launch (device counter)
+    int* base;                                // [max_tasks] first entry of an overflowing task
+    int cap;
+};
+constexpr int PQ_OVER_CAP = 8 << 20;          // 8M entries (128 MB)
 cudaError_t launch_scan_pq(const RoundState& s, const lf_index& idx, const float* q, const int8_t* qc,
-                           const float4* qm, int* surv_cnt, unsigned short* surv_rows, int64_t max_tasks,
+                           const float4* qm, int* surv_cnt, const PQOverflow& ov, int64_t max_tasks,
                            cudaStream_t st);
 
 }  // namespace lf

@@ -1,4 +1,5 @@
 // K4 variant (LF_SCAN_VARIANT=pq): the projected two-stage scan.
+#include <algorithm>
 #include <climits>
 
 #include "common.cuh"
@@ -19,26 +20,29 @@ namespace lf {
 // A row costs pca_k + 16 bytes instead of m + 16 (random walks keep ~98% of their
 // energy in 32 directions); rows whose lo reaches min(bsf, min hi) are re-read
 // whole and summed EXACTLY in fp64, so results equal the full scan.
-// Same TMA bulk-copy pipeline as scan_q8_kernel: 1 producer warp, 8 consumer warps.
-constexpr int PQ_ROWS = 256;                  // rows per stage
+// One WARP per task (no CTA barriers): at pca_k + 16 = 48 bytes a 512-row chunk is
+// only 24 KB, so the per-task barriers of the CTA-pipelined q8 scan would dominate.
+// Each warp streams its own tasks through a private ring of PQW_NS shared-memory
+// slots of PQW_STG rows, filled by cp.async.bulk (lane 0 issues, an mbarrier per
+// slot completes on the bytes): the refill of a slot is issued as soon as the warp
+// has read it, so PQW_NS - 1 pieces per warp are always in flight.  Lane i owns rows
+// i, i + 32, ... of a piece; lo / hi live in registers, min hi is a warp reduction
+// and survivors are compacted by ballot.
+constexpr int PQW_STG = 128;                  // rows per ring slot
+constexpr int PQW_NS = 3;                     // ring slots per warp
+constexpr int PQ_PIECES = CH / PQW_STG;       // slots per task (max)
+constexpr int PQ_SLOTS = CH / 32;             // rows per lane per task
 
 template <int KP>
-struct PQCfg {
-    static constexpr int L = KP / 16;         // lanes per row (16 codes each)
-    static constexpr int RPW = 32 / L;        // rows per warp instruction
-    static constexpr int CODE_BYTES = PQ_ROWS * KP;
-    static constexpr int STAGE_BYTES = (CODE_BYTES + PQ_ROWS * 16 + 127) / 128 * 128;
-    static constexpr int STAGES = KP == 32 ? 6 : 4;
-    static constexpr int QC_OFF = CODE_BYTES + PQ_ROWS * 16;         // query codes (first stage of a task)
-    static constexpr int QM_OFF = QC_OFF + KP;                       // query meta float4
-    static constexpr int HDR_OFF = QM_OFF + 16;                       // r0 i64, q, nrows
-    static constexpr int STAGE_TOTAL = (HDR_OFF + 16 + 127) / 128 * 128;
-    static constexpr int BAR_OFF = STAGES * STAGE_TOTAL;
-    static constexpr int LO_OFF = BAR_OFF + 2 * STAGES * 8;
-    static constexpr int SR_OFF = LO_OFF + CH * 4;
-    static constexpr int SD_OFF = SR_OFF + CH * 4;
-    static constexpr int MISC_OFF = SD_OFF + CH * 8;
-    static constexpr int SMEM = MISC_OFF + 16;
+struct PQW {
+    static constexpr int WARPS = KP == 32 ? 8 : 5;
+    static constexpr int CODE = PQW_STG * KP;
+    static constexpr int STAGE = CODE + PQW_STG * 16;
+    static constexpr int RING = WARPS * PQW_NS * STAGE;
+    static constexpr int BAR_OFF = RING;
+    static constexpr int ROWS_OFF = BAR_OFF + WARPS * PQW_NS * 8;
+    static constexpr int DIST_OFF = (ROWS_OFF + WARPS * CH * 2 + 15) / 16 * 16;
+    static constexpr int SMEM = DIST_OFF + WARPS * CH * 8;
 };
 
 // Query projection: y_q = P (q - mu) in fp64, residual norm, int8 codes (same
@@ -88,270 +92,11 @@ __global__ void project_queries_kernel(const float* __restrict__ queries, int64_
 }
 
 
-template <int KP>
-__global__ void __launch_bounds__(Q8_THREADS, 2) scan_pq_kernel(RoundState s, lf_index idx,
-                                                                const float* __restrict__ queries,
-                                                                const int8_t* __restrict__ qcodes,
-                                                                const float4* __restrict__ qmeta,
-                                                                int* __restrict__ surv_cnt,
-                                                                unsigned short* __restrict__ surv_rows) {
-    using Cfg = PQCfg<KP>;
-    constexpr int S = Cfg::STAGES, L = Cfg::L, RPW = Cfg::RPW;
-    extern __shared__ __align__(128) unsigned char pq_smem[];
-    unsigned char* stages = pq_smem;
-    uint64_t* full = reinterpret_cast<uint64_t*>(pq_smem + Cfg::BAR_OFF);
-    uint64_t* empty = full + S;
-    float* lo_s = reinterpret_cast<float*>(pq_smem + Cfg::LO_OFF);
-    int* surv_r = reinterpret_cast<int*>(pq_smem + Cfg::SR_OFF);
-    double* surv_d = reinterpret_cast<double*>(pq_smem + Cfg::SD_OFF);
-    unsigned int* hi_bits = reinterpret_cast<unsigned int*>(pq_smem + Cfg::MISC_OFF);   // [2]
-    int* n_surv = reinterpret_cast<int*>(hi_bits + 2);                                 // [2]
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < S; ++i) {
-            q8_bar_init(&full[i], 1);
-            q8_bar_init(&empty[i], Q8_CONS_WARPS);
-        }
-        hi_bits[0] = hi_bits[1] = 0x7f800000u;
-        n_surv[0] = n_surv[1] = 0;
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const long long total = s.chunk_off[s.Q];
-
-    if (warp == 0) {   // ---------------------------------------------- producer
-        if (lane == 0) {
-            uint64_t pol;
-            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-            int slot = 0;
-            uint32_t ph = 0;
-            constexpr int PF = 4;                        // task records in flight ahead
-            int4 ring[PF];
-#pragma unroll
-            for (int i = 0; i < PF; ++i) {
-                const long long ti = blockIdx.x + (long long)i * gridDim.x;
-                ring[i] = ti < total ? s.task_rows[ti] : make_int4(0, 0, 0, 0);
-            }
-            int head = 0;
-            for (long long t = blockIdx.x; t < total; t += gridDim.x) {
-                int4 tr = ring[0];
-#pragma unroll
-                for (int i = 0; i < PF; ++i)
-                    if (i == head) tr = ring[i];
-                const long long tf = t + (long long)PF * gridDim.x;
-                const int4 nx = tf < total ? s.task_rows[tf] : make_int4(0, 0, 0, 0);
-#pragma unroll
-                for (int i = 0; i < PF; ++i)
-                    if (i == head) ring[i] = nx;
-                head = head + 1 == PF ? 0 : head + 1;
-                const int4 tk = make_int4(tr.w, 0, 0, 0);
-                const int64_t r0 = (int64_t)(unsigned)tr.x | ((int64_t)tr.y << 32);
-                const int nrows = tr.z;
-                for (int j = 0; j < nrows; j += PQ_ROWS) {
-                    const int rows = min(PQ_ROWS, nrows - j);
-                    q8_wait(&empty[slot], ph ^ 1);
-                    unsigned char* dst = stages + slot * Cfg::STAGE_TOTAL;
-                    uint32_t bytes = (uint32_t)(rows * (KP + 16));
-                    if (j == 0) {
-                        *reinterpret_cast<long long*>(dst + Cfg::HDR_OFF) = r0;
-                        *reinterpret_cast<int2*>(dst + Cfg::HDR_OFF + 8) = make_int2(tk.x, nrows);
-                        bytes += KP + 16;
-                    }
-                    q8_expect_tx(&full[slot], bytes);
-                    q8_bulk(dst, idx.d_Xp + (r0 + j) * KP, (uint32_t)(rows * KP), &full[slot], pol);
-                    q8_bulk(dst + Cfg::CODE_BYTES, idx.d_pmeta + (r0 + j) * 4, (uint32_t)(rows * 16), &full[slot], pol);
-                    if (j == 0) {
-                        q8_bulk(dst + Cfg::QC_OFF, qcodes + (int64_t)tk.x * KP, KP, &full[slot], pol);
-                        q8_bulk(dst + Cfg::QM_OFF, qmeta + tk.x, 16, &full[slot], pol);
-                    }
-                    if (++slot == S) { slot = 0; ph ^= 1; }
-                }
-            }
-        }
-        return;
-    }
-
-    // ------------------------------------------------------------ consumers
-    const int cw = warp - 1;
-    const int ctid = threadIdx.x - 32;
-    const int sub = lane % L;                       // this lane's 16-code slice of its row
-    const int rw = lane / L;                        // row within the warp instruction
-    const int m = idx.m;
-    int slot = 0;
-    uint32_t ph = 0;
-    int par = 0;
-    for (long long t = blockIdx.x; t < total; t += gridDim.x, par ^= 1) {
-        q8_wait(&full[slot], ph);
-        const unsigned char* st0 = stages + slot * Cfg::STAGE_TOTAL;
-        const int64_t r0 = *reinterpret_cast<const long long*>(st0 + Cfg::HDR_OFF);
-        const int2 hq = *reinterpret_cast<const int2*>(st0 + Cfg::HDR_OFF + 8);
-        const int64_t q = hq.x;
-        const int nrows = hq.y;
-        const double bsf = round_bsf(s, q);
-        const int4 qw = *reinterpret_cast<const int4*>(st0 + Cfg::QC_OFF + sub * 16);
-        const float4 qmv = *reinterpret_cast<const float4*>(st0 + Cfg::QM_OFF);
-        const float sq = qmv.x, eq = qmv.z, rq = qmv.w;
-        const float sq2qq = sq * sq * qmv.y;
-        float hmin = __int_as_float(0x7f800000);
-        for (int j = 0; j < nrows; j += PQ_ROWS) {
-            if (j > 0) q8_wait(&full[slot], ph);
-            const int rows = min(PQ_ROWS, nrows - j);
-            const unsigned char* stg = stages + slot * Cfg::STAGE_TOTAL;
-#pragma unroll
-            for (int it = 0; it < PQ_ROWS / (Q8_CONS_WARPS * RPW); ++it) {
-                const int r = (it * Q8_CONS_WARPS + cw) * RPW + rw;
-                const bool v = r < rows;
-                const int4 w = v ? *reinterpret_cast<const int4*>(stg + r * KP + sub * 16) : make_int4(0, 0, 0, 0);
-                int dot = __dp4a(w.x, qw.x, 0);
-                dot = __dp4a(w.y, qw.y, dot);
-                dot = __dp4a(w.z, qw.z, dot);
-                dot = __dp4a(w.w, qw.w, dot);
-#pragma unroll
-                for (int o = L / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-                if (v) {
-                    const float4 mr = *reinterpret_cast<const float4*>(stg + Cfg::CODE_BYTES + r * 16);
-                    const float sx2xx = mr.x * mr.x * mr.y;
-                    const float e = mr.z + eq;
-                    const float a2 = sx2xx + sq2qq - 2.f * (mr.x * sq) * (float)dot;
-                    const float tol = 1e-5f * (sx2xx + sq2qq);
-                    const float alo = fmaxf(sqrtf(fmaxf(a2 - tol, 0.f)) - e, 0.f);
-                    const float ahi = sqrtf(fmaxf(a2 + tol, 0.f)) + e;
-                    const float blo = fmaxf(fabsf(mr.w - rq) - 1e-6f * (mr.w + rq), 0.f);
-                    const float bhi = (mr.w + rq) * (1.f + 1e-6f);
-                    const float lo = sqrtf(fmaf(alo, alo, blo * blo)) * (1.f - 1e-5f);
-                    const float hi = sqrtf(fmaf(ahi, ahi, bhi * bhi)) * (1.f + 1e-5f);
-                    hmin = fminf(hmin, hi);
-                    if (sub == 0) lo_s[j + r] = lo;
-                }
-            }
-            __syncwarp();
-            if (lane == 0) q8_arrive(&empty[slot]);
-            if (++slot == S) { slot = 0; ph ^= 1; }
-        }
-        if (s.k == 1) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) hmin = fminf(hmin, __shfl_xor_sync(0xffffffffu, hmin, o));
-            if (lane == 0) atomicMin(&hi_bits[par], __float_as_uint(hmin));
-        }
-        q8_cons_sync();
-        {
-            double thr = bsf;
-            if (s.k == 1) thr = fmin(thr, (double)__uint_as_float(hi_bits[par]));
-            const float thr_f = thr < kInf ? __double2float_ru(thr) : __int_as_float(0x7f800000);
-            for (int r = ctid; r < nrows; r += Q8_CONS)
-                if (lo_s[r] <= thr_f) surv_r[atomicAdd(&n_surv[par], 1)] = r;
-        }
-        q8_cons_sync();
-        const int ns = n_surv[par];
-        if (ns <= PQ_SQ) {
-            // the common case: hand the few survivors to survivor_exact_kernel (no global
-            // loads on this CTA's critical path); the candidates are written there
-            for (int i = ctid; i < ns; i += Q8_CONS) surv_rows[t * PQ_SQ + i] = (unsigned short)surv_r[i];
-            if (ctid == 0) {
-                surv_cnt[t] = ns;
-                if (s.ea_count != nullptr) {
-                    atomicAdd(&s.ea_count[0], (unsigned long long)nrows);
-                    atomicAdd(&s.ea_count[1], (unsigned long long)ns);
-                    atomicAdd(&s.ea_count[2], (unsigned long long)((long long)nrows * (KP + 16)));
-                    atomicAdd(&s.ea_count[3], (unsigned long long)((long long)ns * m * 4));
-                }
-            }
-            q8_cons_sync();
-            if (ctid == 0) {
-                hi_bits[par] = 0x7f800000u;
-                n_surv[par] = 0;
-            }
-            continue;
-        }
-        if (ctid == 0) surv_cnt[t] = -1;                 // candidates written below
-        {   // exact fp64 direct-form distances of the survivors (series.py:142-146), half a warp each
-            const float* X0 = idx.d_X + r0 * m;
-            const float* qrow = queries + q * m;
-            const int hl = lane & 15;
-            const int hslot = cw * 2 + (lane >> 4);
-            for (int b0 = 0; b0 < ns; b0 += 16) {
-                const int jj = b0 + hslot;
-                const bool v = jj < ns;
-                const int r = v ? surv_r[jj] : 0;
-                double acc = 0.0;
-                for (int c = hl * 4; c < m; c += 64) {
-                    float4 xv = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (v) xv = __ldg(reinterpret_cast<const float4*>(X0 + (int64_t)r * m + c));
-                    const float4 qv = __ldg(reinterpret_cast<const float4*>(qrow + c));
-                    const double d0 = (double)xv.x - (double)qv.x, d1 = (double)xv.y - (double)qv.y;
-                    const double d2 = (double)xv.z - (double)qv.z, d3 = (double)xv.w - (double)qv.w;
-                    acc = __fma_rn(d0, d0, acc); acc = __fma_rn(d1, d1, acc);
-                    acc = __fma_rn(d2, d2, acc); acc = __fma_rn(d3, d3, acc);
-                }
-#pragma unroll
-                for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                if (v && hl == 0) surv_d[jj] = sqrt(acc);
-            }
-        }
-        q8_cons_sync();
-        if (ctid == 0) {
-            if (s.ea_count != nullptr) {
-                atomicAdd(&s.ea_count[0], (unsigned long long)nrows);
-                atomicAdd(&s.ea_count[1], (unsigned long long)ns);
-                atomicAdd(&s.ea_count[2], (unsigned long long)((long long)nrows * (KP + 16)));
-                atomicAdd(&s.ea_count[3], (unsigned long long)((long long)ns * m * 4));
-            }
-            hi_bits[par] = 0x7f800000u;
-            n_surv[par] = 0;
-        }
-        if (cw == 0) {
-            double* cd = s.cand_d + t * s.kc;
-            long long* ci = s.cand_i + t * s.kc;
-            double last_d = -1.0;
-            long long last_i = -1;
-            for (int sel = 0; sel < s.kc; ++sel) {
-                double bd = kInf;
-                long long bi = LLONG_MAX;
-                for (int i = lane; i < ns; i += 32) {
-                    const double dd = surv_d[i];
-                    if (!(dd <= bsf)) continue;
-                    const long long id = idx.d_row_id[r0 + surv_r[i]];
-                    if (pair_less(last_d, last_i, dd, id) && pair_less(dd, id, bd, bi)) { bd = dd; bi = id; }
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const double od = __shfl_xor_sync(0xffffffffu, bd, o);
-                    const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                    if (pair_less(od, oi, bd, bi)) { bd = od; bi = oi; }
-                }
-                if (lane == 0) {
-                    cd[sel] = bd;
-                    ci[sel] = (bi == LLONG_MAX) ? -1 : bi;
-                }
-                last_d = bd;
-                last_i = bi;
-            }
-        }
-    }
-}
-
-// Exact fp64 re-read of the projected scan's survivors (series.py:142-146), one warp
-// per task, 4 rows in flight per iteration; then the task's kc best (d, id) with
-// d <= bsf (tree.py:207) as its candidates.  Tasks the scan finished itself have
-// surv_cnt = -1.
-__global__ void survivor_exact_kernel(RoundState s, lf_index idx, const float* __restrict__ queries,
-                                      const int* __restrict__ surv_cnt,
-                                      const unsigned short* __restrict__ surv_rows) {
-    const long long t = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (t >= s.chunk_off[s.Q]) return;
-    const int ns = surv_cnt[t];
-    if (ns < 0) return;
-    const int4 tk = s.tasks[t];
-    const int64_t q = tk.x;
-    const int64_t r0 = idx.d_leaf_ptr[tk.y] + (int64_t)tk.z * CH;
-    const int m = idx.m;
-    const double bsf = round_bsf(s, q);
-    const float* qrow = queries + q * m;
-    const unsigned short* rl = surv_rows + t * PQ_SQ;
-    double dist_mine = kInf;                          // lane i keeps row i's distance (ns <= 64: two slots)
-    double dist_mine2 = kInf;
-    constexpr int RF = 8;                             // rows in flight per warp
+// Exact fp64 distances of rows rl[0 .. ns) of a task, one warp, RF rows in flight;
+// dist[i] (shared memory) = sqrt(sum (x - q)^2) in the direct form of series.py:142-146.
+__device__ __forceinline__ void pq_exact_rows(const float* __restrict__ X0, const float* __restrict__ qrow, int m,
+                                              const unsigned short* rl, int ns, double* dist, int lane) {
+    constexpr int RF = 8;
     for (int b = 0; b < ns; b += RF) {
         double acc[RF];
 #pragma unroll
@@ -361,7 +106,7 @@ __global__ void survivor_exact_kernel(RoundState s, lf_index idx, const float* _
             float4 xv[RF];
 #pragma unroll
             for (int u = 0; u < RF; ++u)
-                xv[u] = b + u < ns ? __ldg(reinterpret_cast<const float4*>(idx.d_X + (r0 + rl[b + u]) * m + c))
+                xv[u] = b + u < ns ? __ldg(reinterpret_cast<const float4*>(X0 + (int64_t)rl[b + u] * m + c))
                                    : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
             for (int u = 0; u < RF; ++u) {
@@ -375,44 +120,325 @@ __global__ void survivor_exact_kernel(RoundState s, lf_index idx, const float* _
         for (int u = 0; u < RF; ++u) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
-            const int i = b + u;
-            if (i < ns) {
-                if (lane == (i & 31)) {
-                    if (i < 32) dist_mine = sqrt(acc[u]);
-                    else dist_mine2 = sqrt(acc[u]);
-                }
-            }
+            if (lane == 0 && b + u < ns) dist[b + u] = sqrt(acc[u]);
         }
     }
-    long long id_mine = lane < ns ? idx.d_row_id[r0 + rl[lane]] : LLONG_MAX;
-    long long id_mine2 = lane + 32 < ns ? idx.d_row_id[r0 + rl[lane + 32]] : LLONG_MAX;
-    if (!(dist_mine <= bsf)) { dist_mine = kInf; id_mine = LLONG_MAX; }
-    if (!(dist_mine2 <= bsf)) { dist_mine2 = kInf; id_mine2 = LLONG_MAX; }
-    double* cd = s.cand_d + t * s.kc;
-    long long* ci = s.cand_i + t * s.kc;
-    double last_d = -1.0;
-    long long last_i = -1;
-    for (int sel = 0; sel < s.kc; ++sel) {
-        double bd = kInf;
-        long long bi = LLONG_MAX;
-        if (pair_less(last_d, last_i, dist_mine, id_mine) && pair_less(dist_mine, id_mine, bd, bi)) {
-            bd = dist_mine; bi = id_mine;
+    __syncwarp();
+}
+
+template <int KP>
+__global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState s, lf_index idx,
+                                                                      const float* __restrict__ queries,
+                                                                      const int8_t* __restrict__ qcodes,
+                                                                      const float4* __restrict__ qmeta,
+                                                                      int* __restrict__ surv_cnt,
+                                                                      PQOverflow ov) {
+    using C = PQW<KP>;
+    constexpr int V = KP / 16;                        // int4 code vectors per row
+    constexpr int RPL = PQW_STG / 32;                 // rows per lane per slot
+    extern __shared__ __align__(128) unsigned char pqw_smem[];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long gw = (long long)blockIdx.x * C::WARPS + wib;
+    const long long nw = (long long)gridDim.x * C::WARPS;
+    const long long total = s.chunk_off[s.Q];
+    const int m = idx.m;
+    unsigned char* ring = pqw_smem + wib * PQW_NS * C::STAGE;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(pqw_smem + C::BAR_OFF) + wib * PQW_NS;
+    unsigned short* rows_w = reinterpret_cast<unsigned short*>(pqw_smem + C::ROWS_OFF) + wib * CH;
+    double* dist_w = reinterpret_cast<double*>(pqw_smem + C::DIST_OFF) + wib * CH;
+    if (lane == 0) {
+        for (int i = 0; i < PQW_NS; ++i) q8_bar_init(&bars[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+
+    // issue cursor: (task, piece) NS pieces ahead of the consumer (lane 0 issues)
+    long long it = gw;
+    int ip = 0, inrows = 0;
+    int64_t ir0 = 0;
+    if (it < total) {
+        const int4 tr = s.task_rows[it];
+        ir0 = (int64_t)(unsigned)tr.x | ((int64_t)tr.y << 32);
+        inrows = tr.z;
+    }
+    auto issue = [&](int slot) {
+        if (it >= total) return;
+        const int rows = min(PQW_STG, inrows - ip * PQW_STG);
+        if (lane == 0) {
+            unsigned char* dst = ring + slot * C::STAGE;
+            const int64_t rr = ir0 + (int64_t)ip * PQW_STG;
+            q8_expect_tx(&bars[slot], (uint32_t)(rows > 0 ? rows * (KP + 16) : 0));
+            if (rows > 0) {
+                q8_bulk(dst, idx.d_Xp + rr * KP, (uint32_t)(rows * KP), &bars[slot], pol);
+                q8_bulk(dst + C::CODE, idx.d_pmeta + rr * 4, (uint32_t)(rows * 16), &bars[slot], pol);
+            }
         }
-        if (pair_less(last_d, last_i, dist_mine2, id_mine2) && pair_less(dist_mine2, id_mine2, bd, bi)) {
-            bd = dist_mine2; bi = id_mine2;
+        if (++ip * PQW_STG >= inrows) {
+            ip = 0;
+            it += nw;
+            if (it < total) {
+                const int4 tr = s.task_rows[it];
+                ir0 = (int64_t)(unsigned)tr.x | ((int64_t)tr.y << 32);
+                inrows = tr.z;
+            }
+        }
+    };
+#pragma unroll
+    for (int i = 0; i < PQW_NS; ++i) issue(i);
+    int cslot = 0;
+    uint32_t cph = 0;
+    unsigned long long c_rows = 0, c_surv = 0;
+    for (long long t = gw; t < total; t += nw) {
+        const int4 tr = s.task_rows[t];
+        const int64_t r0 = (int64_t)(unsigned)tr.x | ((int64_t)tr.y << 32);
+        const int nrows = tr.z;
+        const int64_t q = tr.w;
+        const int pieces = nrows > 0 ? (nrows + PQW_STG - 1) / PQW_STG : 1;
+        const double bsf = round_bsf(s, q);
+        int4 qw[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) qw[v] = __ldg(reinterpret_cast<const int4*>(qcodes + q * KP) + v);
+        const float4 qmv = __ldg(qmeta + q);
+        const float sq = qmv.x, eq = qmv.z, rq = qmv.w;
+        const float sq2qq = sq * sq * qmv.y;
+        float lo[PQ_SLOTS];
+        float hmin = __int_as_float(0x7f800000);
+#pragma unroll
+        for (int p = 0; p < PQ_PIECES; ++p) {
+            if (p < pieces) {
+                q8_wait(&bars[cslot], cph);
+                const unsigned char* stg = ring + cslot * C::STAGE;
+#pragma unroll
+                for (int u = 0; u < RPL; ++u) {
+                    const int ri = u * 32 + lane;
+                    const bool v = p * PQW_STG + ri < nrows;
+                    int4 w[V];
+#pragma unroll
+                    for (int c = 0; c < V; ++c)
+                        w[c] = v ? *reinterpret_cast<const int4*>(stg + ri * KP + c * 16) : make_int4(0, 0, 0, 0);
+                    const float4 mr = v ? *reinterpret_cast<const float4*>(stg + C::CODE + ri * 16)
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+                    int dot = 0;
+#pragma unroll
+                    for (int c = 0; c < V; ++c) {
+                        dot = __dp4a(w[c].x, qw[c].x, dot);
+                        dot = __dp4a(w[c].y, qw[c].y, dot);
+                        dot = __dp4a(w[c].z, qw[c].z, dot);
+                        dot = __dp4a(w[c].w, qw[c].w, dot);
+                    }
+                    const float sx2xx = mr.x * mr.x * mr.y;
+                    const float e = mr.z + eq;
+                    const float a2 = sx2xx + sq2qq - 2.f * (mr.x * sq) * (float)dot;
+                    const float tol = 1e-5f * (sx2xx + sq2qq);
+                    const float alo = fmaxf(sqrtf(fmaxf(a2 - tol, 0.f)) - e, 0.f);
+                    const float ahi = sqrtf(fmaxf(a2 + tol, 0.f)) + e;
+                    const float blo = fmaxf(fabsf(mr.w - rq) - 1e-6f * (mr.w + rq), 0.f);
+                    const float bhi = (mr.w + rq) * (1.f + 1e-6f);
+                    lo[p * RPL + u] = v ? sqrtf(fmaf(alo, alo, blo * blo)) * (1.f - 1e-5f) : __int_as_float(0x7f800000);
+                    if (v) hmin = fminf(hmin, sqrtf(fmaf(ahi, ahi, bhi * bhi)) * (1.f + 1e-5f));
+                }
+                __syncwarp();                            // every lane has read the slot
+                issue(cslot);                            // refill it NS pieces ahead
+                if (++cslot == PQW_NS) { cslot = 0; cph ^= 1; }
+            } else {
+#pragma unroll
+                for (int u = 0; u < RPL; ++u) lo[p * RPL + u] = __int_as_float(0x7f800000);
+            }
+        }
+        double thr = bsf;
+        if (s.k == 1) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) hmin = fminf(hmin, __shfl_xor_sync(0xffffffffu, hmin, o));
+            thr = fmin(thr, (double)hmin);
+        }
+        const float thr_f = thr < kInf ? __double2float_ru(thr) : __int_as_float(0x7f800000);
+        unsigned bal[PQ_SLOTS];
+        int ns = 0;
+#pragma unroll
+        for (int g = 0; g < PQ_SLOTS; ++g) {
+            bal[g] = __ballot_sync(0xffffffffu, lo[g] <= thr_f);
+            ns += __popc(bal[g]);
+        }
+        c_rows += (unsigned long long)nrows;
+        c_surv += (unsigned long long)ns;
+        if (ns == 0) {
+            if (lane == 0) surv_cnt[t] = 0;
+            continue;
+        }
+        // survivors -> (task, row) entries for the row-parallel re-read (pq_over_exact_kernel)
+        int base = 0;
+        if (lane == 0) base = atomicAdd(ov.n, ns);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        const bool fits = (long long)base + ns <= (long long)ov.cap;
+        const unsigned below = (1u << lane) - 1u;
+        int off = 0;
+#pragma unroll
+        for (int g = 0; g < PQ_SLOTS; ++g) {
+            if ((bal[g] >> lane) & 1u) {
+                const int pos = off + __popc(bal[g] & below);
+                if (fits) {
+                    ov.ent[base + pos] = make_int2((int)t, g * 32 + lane);
+                } else {
+                    if ((long long)base + pos < (long long)ov.cap) ov.ent[base + pos] = make_int2(-1, 0);
+                    rows_w[pos] = (unsigned short)(g * 32 + lane);
+                }
+            }
+            off += __popc(bal[g]);
+        }
+        if (fits) {
+            if (lane == 0) {
+                surv_cnt[t] = ns;
+                ov.base[t] = base;
+            }
+            continue;
+        }
+        __syncwarp();
+        if (lane == 0) surv_cnt[t] = -1;                 // entry list full: re-read and select here
+        pq_exact_rows(idx.d_X + r0 * m, queries + q * m, m, rows_w, ns, dist_w, lane);
+        double* cd = s.cand_d + t * s.kc;
+        long long* ci = s.cand_i + t * s.kc;
+        double last_d = -1.0;
+        long long last_i = -1;
+        for (int sel = 0; sel < s.kc; ++sel) {
+            double bd = kInf;
+            long long bi = LLONG_MAX;
+            for (int i = lane; i < ns; i += 32) {
+                const double dd = dist_w[i];
+                if (!(dd <= bsf)) continue;
+                const long long id = idx.d_row_id[r0 + rows_w[i]];
+                if (pair_less(last_d, last_i, dd, id) && pair_less(dd, id, bd, bi)) { bd = dd; bi = id; }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+                const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (pair_less(od, oi, bd, bi)) { bd = od; bi = oi; }
+            }
+            if (lane == 0) {
+                cd[sel] = bd;
+                ci[sel] = (bi == LLONG_MAX) ? -1 : bi;
+            }
+            last_d = bd;
+            last_i = bi;
+        }
+        __syncwarp();
+    }
+    if (s.ea_count != nullptr && lane == 0 && c_rows > 0) {
+        atomicAdd(&s.ea_count[0], c_rows);
+        atomicAdd(&s.ea_count[1], c_surv);
+        atomicAdd(&s.ea_count[2], c_rows * (unsigned long long)(KP + 16));
+        atomicAdd(&s.ea_count[3], c_surv * (unsigned long long)m * 4ull);
+    }
+}
+
+// Row-parallel exact fp64 distances of the survivor entries (series.py:142-146 direct
+// form): 8 lanes per row, 2 rows per 8-lane group, 8 rows per warp iteration; each lane
+// keeps 2 x m / 32 float4 loads in flight.
+__global__ void __launch_bounds__(256) pq_over_exact_kernel(RoundState s, lf_index idx,
+                                                            const float* __restrict__ queries, PQOverflow ov) {
+    constexpr int R = 2;
+    const int lane = threadIdx.x & 31, sl = lane & 7, grp = lane >> 3;
+    const long long n = min((long long)*ov.n, (long long)ov.cap);
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    const int m = idx.m;
+    for (long long w0 = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (4 * R); w0 < n;
+         w0 += nw * 4 * R) {
+        const float* xr[R];
+        const float* qr[R];
+        bool v[R];
+        long long ii[R];
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+            ii[u] = w0 + u * 4 + grp;
+            int2 e = make_int2(-1, 0);
+            if (ii[u] < n) e = ov.ent[ii[u]];
+            v[u] = e.x >= 0;
+            xr[u] = queries;
+            qr[u] = queries;
+            if (v[u]) {
+                const int4 tk = s.tasks[e.x];
+                xr[u] = idx.d_X + (idx.d_leaf_ptr[tk.y] + (int64_t)tk.z * CH + e.y) * m;
+                qr[u] = queries + (int64_t)tk.x * m;
+            }
+        }
+        double acc[R];
+#pragma unroll
+        for (int u = 0; u < R; ++u) acc[u] = 0.0;
+#pragma unroll 4
+        for (int c = sl * 4; c < m; c += 32) {
+            float4 xv[R], qv[R];
+#pragma unroll
+            for (int u = 0; u < R; ++u) {
+                xv[u] = v[u] ? __ldcs(reinterpret_cast<const float4*>(xr[u] + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                qv[u] = v[u] ? __ldg(reinterpret_cast<const float4*>(qr[u] + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < R; ++u) {
+                const double d0 = (double)xv[u].x - (double)qv[u].x, d1 = (double)xv[u].y - (double)qv[u].y;
+                const double d2 = (double)xv[u].z - (double)qv[u].z, d3 = (double)xv[u].w - (double)qv[u].w;
+                acc[u] = __fma_rn(d0, d0, acc[u]); acc[u] = __fma_rn(d1, d1, acc[u]);
+                acc[u] = __fma_rn(d2, d2, acc[u]); acc[u] = __fma_rn(d3, d3, acc[u]);
+            }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double od = __shfl_xor_sync(0xffffffffu, bd, o);
-            const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (pair_less(od, oi, bd, bi)) { bd = od; bi = oi; }
+        for (int u = 0; u < R; ++u) {
+            acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], 4);
+            acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], 2);
+            acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], 1);
+            if (v[u] && sl == 0) ov.dist[ii[u]] = sqrt(acc[u]);
         }
-        if (lane == 0) {
-            cd[sel] = bd;
-            ci[sel] = (bi == LLONG_MAX || bd == kInf) ? -1 : bi;
+    }
+}
+
+// Per task: its kc best (d, id) with d <= bsf (tree.py:207) from the re-read
+// distances, as the task's candidates.  Tasks the scan finished itself have
+// surv_cnt = -1; tasks without survivors get empty candidates.
+__global__ void pq_select_kernel(RoundState s, lf_index idx, const int* __restrict__ surv_cnt, PQOverflow ov) {
+    const int lane = threadIdx.x & 31;
+    const long long total = s.chunk_off[s.Q];
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long t = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < total; t += nw) {
+        const int ns = surv_cnt[t];
+        if (ns < 0) continue;
+        double* cd = s.cand_d + t * s.kc;
+        long long* ci = s.cand_i + t * s.kc;
+        if (ns == 0) {
+            for (int i = lane; i < s.kc; i += 32) {
+                cd[i] = kInf;
+                ci[i] = -1;
+            }
+            continue;
         }
-        last_d = bd;
-        last_i = bi;
+        const int4 tk = s.tasks[t];
+        const int64_t r0 = idx.d_leaf_ptr[tk.y] + (int64_t)tk.z * CH;
+        const double bsf = round_bsf(s, tk.x);
+        const int base = ov.base[t];
+        double last_d = -1.0;
+        long long last_i = -1;
+        for (int sel = 0; sel < s.kc; ++sel) {
+            double bd = kInf;
+            long long bi = LLONG_MAX;
+            for (int i = lane; i < ns; i += 32) {
+                const double dd = ov.dist[base + i];
+                if (!(dd <= bsf)) continue;
+                const long long id = idx.d_row_id[r0 + ov.ent[base + i].y];
+                if (pair_less(last_d, last_i, dd, id) && pair_less(dd, id, bd, bi)) { bd = dd; bi = id; }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+                const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (pair_less(od, oi, bd, bi)) { bd = od; bi = oi; }
+            }
+            if (lane == 0) {
+                cd[sel] = bd;
+                ci[sel] = (bi == LLONG_MAX) ? -1 : bi;
+            }
+            last_d = bd;
+            last_i = bi;
+        }
     }
 }
 
@@ -425,25 +451,31 @@ cudaError_t launch_project_queries(const float* q, int64_t Q, const lf_index& id
 
 template <int KP>
 static cudaError_t launch_pq_kp(const RoundState& s, const lf_index& idx, const float* q, const int8_t* qc,
-                                const float4* qm, int* surv_cnt, unsigned short* surv_rows, cudaStream_t st) {
+                                const float4* qm, int* surv_cnt, const PQOverflow& ov, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(scan_pq_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             PQCfg<KP>::SMEM);
+                                             PQW<KP>::SMEM);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    scan_pq_kernel<KP><<<sm_count() * 2, Q8_THREADS, PQCfg<KP>::SMEM, st>>>(s, idx, q, qc, qm, surv_cnt, surv_rows);
+    scan_pq_kernel<KP><<<sm_count(), PQW<KP>::WARPS * 32, PQW<KP>::SMEM, st>>>(s, idx, q, qc, qm, surv_cnt, ov);
     return cudaGetLastError();
 }
 
 cudaError_t launch_scan_pq(const RoundState& s, const lf_index& idx, const float* q, const int8_t* qc,
-                           const float4* qm, int* surv_cnt, unsigned short* surv_rows, int64_t max_tasks,
+                           const float4* qm, int* surv_cnt, const PQOverflow& ov, int64_t max_tasks,
                            cudaStream_t st) {
-    cudaError_t e = idx.pca_k == 32 ? launch_pq_kp<32>(s, idx, q, qc, qm, surv_cnt, surv_rows, st)
-                                    : launch_pq_kp<64>(s, idx, q, qc, qm, surv_cnt, surv_rows, st);
+    cudaError_t e = cudaMemsetAsync(ov.n, 0, sizeof(int), st);
     if (e != cudaSuccess) return e;
-    survivor_exact_kernel<<<(unsigned)((max_tasks * 32 + 255) / 256), 256, 0, st>>>(s, idx, q, surv_cnt, surv_rows);
+    e = idx.pca_k == 32 ? launch_pq_kp<32>(s, idx, q, qc, qm, surv_cnt, ov, st)
+                        : launch_pq_kp<64>(s, idx, q, qc, qm, surv_cnt, ov, st);
+    if (e != cudaSuccess) return e;
+    pq_over_exact_kernel<<<sm_count() * 8, 256, 0, st>>>(s, idx, q, ov);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const long long warps = std::min<long long>(max_tasks, (long long)sm_count() * 64);
+    pq_select_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(s, idx, surv_cnt, ov);
     return cudaGetLastError();
 }
 

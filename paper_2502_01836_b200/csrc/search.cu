@@ -501,18 +501,16 @@ static bool prefix_orders() {
     return e && e[0] == '0';
 }
 
-// Scan variant (experiments): LF_SCAN_VARIANT = q8 (default) | ea2 | ea3 | full.
-// Scan variant: LF_SCAN_VARIANT = q8 (default: full-length int8 shadow, at the HBM
-// roofline) | pq (projected shadow after round 0: ~3x fewer bytes, but latency-bound
-// on the survivor re-reads -- measured 0.96-1.05x of q8 depending on the box) |
-// ea2 | ea3 | full.
+// Scan variant: LF_SCAN_VARIANT unset / pq (default: the full-length int8 shadow in
+// round 0, then the projected shadow -- 48 instead of 272 bytes per row -- wherever the
+// index carries one) | q8 (int8 shadow only) | ea2 | ea3 | full.
 static int scan_variant() {
     const char* e = getenv("LF_SCAN_VARIANT");
-    if (e && strcmp(e, "pq") == 0) return 8;       // projected stage when the shadow exists
-    if (!e || strcmp(e, "q8") == 0) return 9;      // int8 shadow only
-    if (e && strcmp(e, "ea3") == 0) return 3;
-    if (e && strcmp(e, "full") == 0) return 0;
-    if (e && strcmp(e, "ea2") == 0) return 2;
+    if (!e || e[0] == 0 || strcmp(e, "pq") == 0) return 8;   // projected stage when the shadow exists
+    if (strcmp(e, "q8") == 0) return 9;            // int8 shadow only
+    if (strcmp(e, "ea3") == 0) return 3;
+    if (strcmp(e, "full") == 0) return 0;
+    if (strcmp(e, "ea2") == 0) return 2;
     return 8;                                      // default: int8-bounded scan when the shadow exists
 }
 
@@ -539,7 +537,7 @@ struct lf_session {
     bool q8 = false;                 // int8-bounded scan (query codes quantised once in begin)
     bool grouped = false;            // q8 scan with the round's tasks grouped by (leaf, chunk)
     bool pq = false;                 // two-stage scan over the projected shadow (d_Xp)
-    lf::Scratch qcp, qmp, pq_cnt, pq_rows, pq_trows;
+    lf::Scratch qcp, qmp, pq_cnt, pq_trows, pq_oent, pq_odist, pq_on, pq_obase;
     lf::Scratch cbase, ghist, gcur, gsorted, glist, gcount, gbsum, ginfo;
     int n_keys = 0;
     long long refills = 0;           // queries whose visit order was completed after the prefix
@@ -702,7 +700,10 @@ static int session_begin(lf_session* ss) {
         LF_CUDA(ss->pq_cnt.alloc(sizeof(int) * max_tasks, st));
         LF_CUDA(ss->pq_trows.alloc(sizeof(int4) * max_tasks, st));
         s.task_rows = ss->pq_trows.as<int4>();
-        LF_CUDA(ss->pq_rows.alloc(sizeof(unsigned short) * PQ_SQ * max_tasks, st));
+        LF_CUDA(ss->pq_oent.alloc(sizeof(int2) * PQ_OVER_CAP, st));
+        LF_CUDA(ss->pq_odist.alloc(sizeof(double) * PQ_OVER_CAP, st));
+        LF_CUDA(ss->pq_on.alloc(sizeof(int), st));
+        LF_CUDA(ss->pq_obase.alloc(sizeof(int) * max_tasks, st));
         LF_CUDA(launch_project_queries(ss->d_q, Q, idx, ss->qcp.as<int8_t>(), ss->qmp.as<float4>(), st));
         ++ss->kernels;
     }
@@ -840,9 +841,11 @@ static int session_enqueue(lf_session* ss, const double* d_bound, double* d_bsf_
     if (ea && ss->pq && !(ss->round == 0 && ss->q8)) {
         // round 0 has no best-so-far yet: the projected bound's loose upper end would let
         // most rows through, so the first round runs the full-length int8 scan
-        ce = launch_scan_pq(s, idx, ss->d_q, ss->qcp.as<int8_t>(), ss->qmp.as<float4>(), ss->pq_cnt.as<int>(),
-                            ss->pq_rows.as<unsigned short>(), max_tasks, st);
-        ++ss->kernels;
+        const PQOverflow ov{ss->pq_oent.as<int2>(), ss->pq_odist.as<double>(), ss->pq_on.as<int>(),
+                            ss->pq_obase.as<int>(), PQ_OVER_CAP};
+        ce = launch_scan_pq(s, idx, ss->d_q, ss->qcp.as<int8_t>(), ss->qmp.as<float4>(), ss->pq_cnt.as<int>(), ov,
+                            max_tasks, st);
+        ss->kernels += 3;
     } else if (ea && ss->q8 && ss->grouped) {
         GroupScratch g{ss->cbase.as<int>(), ss->ghist.as<int>(), ss->gcur.as<int>(), ss->gsorted.as<int>(),
                        ss->glist.as<int2>(), ss->gcount.as<int>(), ss->gbsum.as<int2>(), ss->ginfo.p, ss->n_keys};

@@ -53,6 +53,9 @@ def as_f32_rows(values) -> np.ndarray:
     return v32
 
 
+
+PCA_MIN_ENERGY = 0.9     # default projected-shadow gate (random walks: ~0.98 in 32 directions)
+
 class DeviceRows:
     """Row access to a device-resident collection with numpy semantics (rows -> host fp32)."""
 
@@ -309,8 +312,13 @@ class DeviceIndex:
                                                        self.qmeta.data_ptr(), _lib.stream_ptr()))
             self.pca_k = 0
             self.P = self.mu = self.Xp = self.pmeta = None
-            if m % 4 == 0 and 64 <= m <= 512 and n_rows >= 256 and os.environ.get("LF_SCAN_VARIANT") == "pq":
-                self.ensure_pca(int(os.environ.get("LF_PCA_K", "32")))      # opt-in two-stage scan
+            self.pca_energy = None
+            variant = os.environ.get("LF_SCAN_VARIANT") or None
+            if m % 4 == 0 and 64 <= m <= 512 and n_rows >= 256 and variant in (None, "pq"):
+                # projected shadow for the two-stage scan: by default only when the leading
+                # directions hold most of the energy (else the projected bound prunes little)
+                self.ensure_pca(int(os.environ.get("LF_PCA_K", "32")),
+                                min_energy=None if variant == "pq" else PCA_MIN_ENERGY)
         self.leaf_ids = leaf_ids
         self.leaf_ptr_host = leaf_ptr
         self.slot_of_leaf = {int(l): j for j, l in enumerate(leaf_ids)}
@@ -320,12 +328,14 @@ class DeviceIndex:
     def n_leaves(self) -> int:
         return int(self.leaf_ids.shape[0])
 
-    def ensure_pca(self, k: int = 32, sample: int = 200_000, seed: int = 0) -> None:
+    def ensure_pca(self, k: int = 32, sample: int = 200_000, seed: int = 0, min_energy: float | None = None) -> bool:
         """Projected shadow for the two-stage scan (lf_index.d_Xp): the top-k principal
         directions of a row sample (fp64 SVD, orthonormal rows), and per row the int8
         codes of y = P (x - mu) with {scale, sum code^2, code error (rounded up),
         residual norm}.  Index-build plumbing in torch; the search reads it in the
-        scan kernel."""
+        scan kernel.  With min_energy, the shadow is built only when the k directions
+        hold at least that fraction of the sample's centred energy (self.pca_energy).
+        Returns whether the shadow exists."""
         import torch
 
         if k not in (32, 64):
@@ -338,7 +348,11 @@ class DeviceIndex:
             pick = torch.randint(0, n, (min(sample, n),), generator=g, device=self.device)
             S = X[pick].double()
             mu = S.mean(0)
-            _, _, V = torch.linalg.svd(S - mu, full_matrices=False)
+            _, sv, V = torch.linalg.svd(S - mu, full_matrices=False)
+            e2 = sv * sv
+            self.pca_energy = float(e2[:k].sum() / e2.sum()) if float(e2.sum()) > 0 else 1.0
+            if min_energy is not None and self.pca_energy < min_energy:
+                return False
             P = V[:k].contiguous()
             codes = torch.empty((n, k), dtype=torch.int8, device=self.device)
             meta = torch.empty((n, 4), dtype=torch.float32, device=self.device)
@@ -356,6 +370,7 @@ class DeviceIndex:
                 codes[r0:r0 + (1 << 20)] = c.to(torch.int8)
                 meta[r0:r0 + (1 << 20)] = torch.stack([s32, (c * c).sum(1).float(), e32, r.float()], dim=1)
         self.pca_k, self.P, self.mu, self.Xp, self.pmeta = k, P, mu.contiguous(), codes, meta
+        return True
 
     def ensure_level2(self) -> bool:
         """Build the second-level residual codes (training-data generation only; m x 1 B

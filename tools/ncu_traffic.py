@@ -36,8 +36,8 @@ b = json.loads([l for l in open(bench_path) if l.startswith("{")][-1])
 alg = b["roofline"]["algorithmic_bytes_per_step"]
 n = len(launches)
 # one scan phase per round: its streaming kernel (scan_q8 / scan_pq) plus, after scan_pq,
-# the survivor_exact kernel -- bench.py's "achieved" and "traffic" are per phase
-rounds = sum(1 for x in launches if "survivor_exact" not in x["kernel"])
+# the survivor re-read and selection kernels -- bench.py's "achieved" and "traffic" are per phase
+rounds = sum(1 for x in launches if "scan_q8" in x["kernel"] or "scan_pq" in x["kernel"])
 tot = sum(x["dram_read_bytes"] + x["dram_write_bytes"] for x in launches)
 out = {
     "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum, every scan "
@@ -46,7 +46,7 @@ out = {
     "scan_phases_per_step": rounds,
     "dram_bytes_per_step": tot,
     "dram_bytes_per_launch": tot / max(rounds, 1),
-    "dram_bytes_per_launch_definition": "per scan phase (round): streaming kernel + survivor re-check kernel",
+    "dram_bytes_per_launch_definition": "per scan phase (round): streaming kernel + survivor re-read / selection kernels",
     "algorithmic_bytes_per_step": alg,
     "algorithmic_bytes_per_launch": alg / max(rounds, 1),
     "traffic_over_algorithmic": tot / alg if alg else None,

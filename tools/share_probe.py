@@ -20,8 +20,7 @@ ap.add_argument("--n", type=int, default=25_000_000)
 ap.add_argument("--leaf-cap", type=int, default=10_000)
 ap.add_argument("--max-epochs", type=int, default=1000)
 a = ap.parse_args()
-args = argparse.Namespace(n=a.n, m=256, leaf_cap=a.leaf_cap, queries=1000, target=0.99, seed=1234, n_global=1500,
-                          n_local=500, calibration=300, max_epochs=a.max_epochs)
+args = bench.make_parser().parse_args(["--n", str(a.n), "--leaf-cap", str(a.leaf_cap), "--max-epochs", str(a.max_epochs)])
 w = bench.setup_workload(args, torch.device("cuda", 0))
 e, Q, tree = w["eidx"], w["Q"], w["tree"]
 di = tree.device()
