@@ -167,15 +167,23 @@ cudaError_t launch_grouped_scan(const RoundState& s, const lf_index& idx, const 
 // scan_pq.cu: projected two-stage scan
 cudaError_t launch_project_queries(const float* q, int64_t Q, const lf_index& idx, int8_t* qc, float4* qm,
                                    cudaStream_t st);
-// Survivors of the projected scan: (task, row) entries, re-read row-parallel.
+// Survivors of the projected scan: (task, row) entries, contiguous per task, for pq_tail_kernel.
 struct PQOverflow {
     int2* ent;                                // [cap] (task, row in chunk); task < 0: unused slot
-    double* dist;                             // [cap] exact distances
     int* n;                                   // entries claimed this launch (device counter)
-    int* base;                                // [max_tasks] first entry of an overflowing task
+    int* base;                                // [max_tasks] first entry of a task
     int cap;
+    unsigned short* wrows;                    // [scan warps][CH] rows / distances of a task whose
+    double* wdist;                            //   entries did not fit (re-read in the scan warp)
+    // second stage: the full-length int8 interval of every entry (nullptr qc8: no stage)
+    const int8_t* qc8;                        // [Q][mp] query codes (quantize_queries)
+    const float4* qm8;                        // [Q] query code metadata
+    int mp;
+    float* lo8;                               // [cap] int8 lower bound of each entry
+    unsigned* thr;                            // [max_tasks] the projected stage's threshold (float bits)
 };
-constexpr int PQ_OVER_CAP = 8 << 20;          // 8M entries (128 MB)
+int pq_scan_warps();                          // warps of one scan_pq_kernel launch
+constexpr int PQ_OVER_CAP = 8 << 20;          // 8M entries (64 MB)
 cudaError_t launch_scan_pq(const RoundState& s, const lf_index& idx, const float* q, const int8_t* qc,
                            const float4* qm, int* surv_cnt, const PQOverflow& ov, int64_t max_tasks,
                            cudaStream_t st);

@@ -28,21 +28,19 @@ namespace lf {
 // has read it, so PQW_NS - 1 pieces per warp are always in flight.  Lane i owns rows
 // i, i + 32, ... of a piece; lo / hi live in registers, min hi is a warp reduction
 // and survivors are compacted by ballot.
-constexpr int PQW_STG = 128;                  // rows per ring slot
-constexpr int PQW_NS = 3;                     // ring slots per warp
+constexpr int PQW_STG = 64;                   // rows per ring slot
+constexpr int PQW_NS = 4;                     // ring slots per warp
 constexpr int PQ_PIECES = CH / PQW_STG;       // slots per task (max)
 constexpr int PQ_SLOTS = CH / 32;             // rows per lane per task
 
 template <int KP>
 struct PQW {
-    static constexpr int WARPS = KP == 32 ? 8 : 5;
+    static constexpr int WARPS = KP == 32 ? 16 : 8;
     static constexpr int CODE = PQW_STG * KP;
     static constexpr int STAGE = CODE + PQW_STG * 16;
     static constexpr int RING = WARPS * PQW_NS * STAGE;
     static constexpr int BAR_OFF = RING;
-    static constexpr int ROWS_OFF = BAR_OFF + WARPS * PQW_NS * 8;
-    static constexpr int DIST_OFF = (ROWS_OFF + WARPS * CH * 2 + 15) / 16 * 16;
-    static constexpr int SMEM = DIST_OFF + WARPS * CH * 8;
+    static constexpr int SMEM = BAR_OFF + WARPS * PQW_NS * 8;
 };
 
 // Query projection: y_q = P (q - mu) in fp64, residual norm, int8 codes (same
@@ -126,6 +124,39 @@ __device__ __forceinline__ void pq_exact_rows(const float* __restrict__ X0, cons
     __syncwarp();
 }
 
+// The task's kc best (d, id) with d <= bsf (tree.py:207) over ns survivors, as its
+// candidates; dist(i) / id(i) give survivor i's exact distance and row id (NaN: pruned).
+template <class DistF, class IdF>
+__device__ __forceinline__ void pq_select(const RoundState& s, long long t, int lane, int ns, double bsf, DistF dist,
+                                          IdF id_of) {
+    double* cd = s.cand_d + t * s.kc;
+    long long* ci = s.cand_i + t * s.kc;
+    double last_d = -1.0;
+    long long last_i = -1;
+    for (int sel = 0; sel < s.kc; ++sel) {
+        double bd = kInf;
+        long long bi = LLONG_MAX;
+        for (int i = lane; i < ns; i += 32) {
+            const double dd = dist(i);
+            if (!(dd <= bsf)) continue;
+            const long long id = id_of(i);
+            if (pair_less(last_d, last_i, dd, id) && pair_less(dd, id, bd, bi)) { bd = dd; bi = id; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+            const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (pair_less(od, oi, bd, bi)) { bd = od; bi = oi; }
+        }
+        if (lane == 0) {
+            cd[sel] = bd;
+            ci[sel] = (bi == LLONG_MAX) ? -1 : bi;
+        }
+        last_d = bd;
+        last_i = bi;
+    }
+}
+
 template <int KP>
 __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState s, lf_index idx,
                                                                       const float* __restrict__ queries,
@@ -144,8 +175,8 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
     const int m = idx.m;
     unsigned char* ring = pqw_smem + wib * PQW_NS * C::STAGE;
     uint64_t* bars = reinterpret_cast<uint64_t*>(pqw_smem + C::BAR_OFF) + wib * PQW_NS;
-    unsigned short* rows_w = reinterpret_cast<unsigned short*>(pqw_smem + C::ROWS_OFF) + wib * CH;
-    double* dist_w = reinterpret_cast<double*>(pqw_smem + C::DIST_OFF) + wib * CH;
+    unsigned short* rows_w = ov.wrows + gw * CH;      // fallback scratch (entry list full), global
+    double* dist_w = ov.wdist + gw * CH;
     if (lane == 0) {
         for (int i = 0; i < PQW_NS; ++i) q8_bar_init(&bars[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -189,7 +220,7 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
     for (int i = 0; i < PQW_NS; ++i) issue(i);
     int cslot = 0;
     uint32_t cph = 0;
-    unsigned long long c_rows = 0, c_surv = 0;
+    unsigned long long c_rows = 0, c_surv = 0, c_fall = 0;
     for (long long t = gw; t < total; t += nw) {
         const int4 tr = s.task_rows[t];
         const int64_t r0 = (int64_t)(unsigned)tr.x | ((int64_t)tr.y << 32);
@@ -291,153 +322,171 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
             if (lane == 0) {
                 surv_cnt[t] = ns;
                 ov.base[t] = base;
+                ov.thr[t] = __float_as_uint(thr_f);
             }
             continue;
         }
         __syncwarp();
         if (lane == 0) surv_cnt[t] = -1;                 // entry list full: re-read and select here
         pq_exact_rows(idx.d_X + r0 * m, queries + q * m, m, rows_w, ns, dist_w, lane);
-        double* cd = s.cand_d + t * s.kc;
-        long long* ci = s.cand_i + t * s.kc;
-        double last_d = -1.0;
-        long long last_i = -1;
-        for (int sel = 0; sel < s.kc; ++sel) {
-            double bd = kInf;
-            long long bi = LLONG_MAX;
-            for (int i = lane; i < ns; i += 32) {
-                const double dd = dist_w[i];
-                if (!(dd <= bsf)) continue;
-                const long long id = idx.d_row_id[r0 + rows_w[i]];
-                if (pair_less(last_d, last_i, dd, id) && pair_less(dd, id, bd, bi)) { bd = dd; bi = id; }
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double od = __shfl_xor_sync(0xffffffffu, bd, o);
-                const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                if (pair_less(od, oi, bd, bi)) { bd = od; bi = oi; }
-            }
-            if (lane == 0) {
-                cd[sel] = bd;
-                ci[sel] = (bi == LLONG_MAX) ? -1 : bi;
-            }
-            last_d = bd;
-            last_i = bi;
-        }
+        if (ov.qc8 != nullptr) c_fall += (unsigned long long)ns;
+        pq_select(s, t, lane, ns, bsf, [&](int i) { return dist_w[i]; },
+                  [&](int i) { return idx.d_row_id[r0 + rows_w[i]]; });
         __syncwarp();
     }
     if (s.ea_count != nullptr && lane == 0 && c_rows > 0) {
         atomicAdd(&s.ea_count[0], c_rows);
-        atomicAdd(&s.ea_count[1], c_surv);
         atomicAdd(&s.ea_count[2], c_rows * (unsigned long long)(KP + 16));
-        atomicAdd(&s.ea_count[3], c_surv * (unsigned long long)m * 4ull);
+        if (ov.qc8 == nullptr) {                      // else the int8 stage / re-read count theirs
+            atomicAdd(&s.ea_count[1], c_surv);
+            atomicAdd(&s.ea_count[3], c_surv * (unsigned long long)m * 4ull);
+        } else if (c_fall > 0) {
+            atomicAdd(&s.ea_count[1], c_fall);
+            atomicAdd(&s.ea_count[3], c_fall * (unsigned long long)m * 4ull);
+        }
     }
 }
 
-// Row-parallel exact fp64 distances of the survivor entries (series.py:142-146 direct
-// form): 8 lanes per row, 2 rows per 8-lane group, 8 rows per warp iteration; each lane
-// keeps 2 x m / 32 float4 loads in flight.
-__global__ void __launch_bounds__(256) pq_over_exact_kernel(RoundState s, lf_index idx,
-                                                            const float* __restrict__ queries, PQOverflow ov) {
+// int8 stage of the projected scan's survivor entries, row-parallel: the full-length
+// int8 interval of each entry (the bound of scan_q8_kernel; 8 lanes per row, 16 code
+// bytes per lane per load, 2 rows per 8-lane group).  lo is kept per entry; for k = 1
+// the task threshold is min'ed with every entry's upper bound -- the task's best row
+// survives both stages, so no row whose lower bound exceeds it can be the nearest.
+__global__ void __launch_bounds__(256) pq_q8_bound_kernel(RoundState s, lf_index idx, PQOverflow ov) {
     constexpr int R = 2;
     const int lane = threadIdx.x & 31, sl = lane & 7, grp = lane >> 3;
     const long long n = min((long long)*ov.n, (long long)ov.cap);
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-    const int m = idx.m;
+    const int M8 = (idx.m + 63) / 64 * 64;
+    unsigned long long cnt = 0;
     for (long long w0 = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (4 * R); w0 < n;
          w0 += nw * 4 * R) {
-        const float* xr[R];
-        const float* qr[R];
-        bool v[R];
         long long ii[R];
+        int2 e[R];
+        int64_t row[R];
+        int64_t qq[R];
 #pragma unroll
         for (int u = 0; u < R; ++u) {
             ii[u] = w0 + u * 4 + grp;
-            int2 e = make_int2(-1, 0);
-            if (ii[u] < n) e = ov.ent[ii[u]];
-            v[u] = e.x >= 0;
-            xr[u] = queries;
-            qr[u] = queries;
-            if (v[u]) {
-                const int4 tk = s.tasks[e.x];
-                xr[u] = idx.d_X + (idx.d_leaf_ptr[tk.y] + (int64_t)tk.z * CH + e.y) * m;
-                qr[u] = queries + (int64_t)tk.x * m;
+            e[u] = ii[u] < n ? ov.ent[ii[u]] : make_int2(-1, 0);
+            row[u] = 0;
+            qq[u] = 0;
+            if (e[u].x >= 0) {
+                const int4 tk = s.tasks[e[u].x];
+                row[u] = idx.d_leaf_ptr[tk.y] + (int64_t)tk.z * CH + e[u].y;
+                qq[u] = tk.x;
             }
         }
-        double acc[R];
+        int dot[R];
 #pragma unroll
-        for (int u = 0; u < R; ++u) acc[u] = 0.0;
-#pragma unroll 4
-        for (int c = sl * 4; c < m; c += 32) {
-            float4 xv[R], qv[R];
+        for (int u = 0; u < R; ++u) dot[u] = 0;
+        for (int c = sl * 16; c < M8; c += 128) {
+            int4 w[R], qv[R];
 #pragma unroll
             for (int u = 0; u < R; ++u) {
-                xv[u] = v[u] ? __ldcs(reinterpret_cast<const float4*>(xr[u] + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
-                qv[u] = v[u] ? __ldg(reinterpret_cast<const float4*>(qr[u] + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                const bool v = e[u].x >= 0;
+                w[u] = v ? __ldcs(reinterpret_cast<const int4*>(idx.d_X8 + row[u] * M8 + c)) : make_int4(0, 0, 0, 0);
+                qv[u] = v ? __ldg(reinterpret_cast<const int4*>(ov.qc8 + qq[u] * ov.mp + c)) : make_int4(0, 0, 0, 0);
             }
 #pragma unroll
             for (int u = 0; u < R; ++u) {
-                const double d0 = (double)xv[u].x - (double)qv[u].x, d1 = (double)xv[u].y - (double)qv[u].y;
-                const double d2 = (double)xv[u].z - (double)qv[u].z, d3 = (double)xv[u].w - (double)qv[u].w;
-                acc[u] = __fma_rn(d0, d0, acc[u]); acc[u] = __fma_rn(d1, d1, acc[u]);
-                acc[u] = __fma_rn(d2, d2, acc[u]); acc[u] = __fma_rn(d3, d3, acc[u]);
+                dot[u] = __dp4a(w[u].x, qv[u].x, dot[u]);
+                dot[u] = __dp4a(w[u].y, qv[u].y, dot[u]);
+                dot[u] = __dp4a(w[u].z, qv[u].z, dot[u]);
+                dot[u] = __dp4a(w[u].w, qv[u].w, dot[u]);
             }
         }
 #pragma unroll
         for (int u = 0; u < R; ++u) {
-            acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], 4);
-            acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], 2);
-            acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], 1);
-            if (v[u] && sl == 0) ov.dist[ii[u]] = sqrt(acc[u]);
+            dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], 4);
+            dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], 2);
+            dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], 1);
+            if (e[u].x >= 0 && sl == 0) {
+                const float4 mr = __ldcs(reinterpret_cast<const float4*>(idx.d_qmeta) + row[u]);
+                const float4 qmv = __ldg(ov.qm8 + qq[u]);
+                const float sq = qmv.x, eq = qmv.z;
+                const float sq2qq = sq * sq * qmv.y;
+                const float sx2xx = mr.x * mr.x * mr.y;
+                const float ee = mr.z + eq;
+                const float d2 = sx2xx + sq2qq - 2.f * (mr.x * sq) * (float)dot[u];
+                const float tol = 1e-5f * (sx2xx + sq2qq);
+                ov.lo8[ii[u]] = (sqrtf(fmaxf(d2 - tol, 0.f)) - ee) * (1.f - 1e-6f);
+                ++cnt;
+                if (s.k == 1)
+                    atomicMin(&ov.thr[e[u].x], __float_as_uint((sqrtf(fmaxf(d2 + tol, 0.f)) + ee) * (1.f + 1e-6f)));
+            }
         }
+    }
+    if (s.ea_count != nullptr) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (lane == 0 && cnt > 0) atomicAdd(&s.ea_count[2], cnt * (unsigned long long)(M8 + 16));
     }
 }
 
-// Per task: its kc best (d, id) with d <= bsf (tree.py:207) from the re-read
-// distances, as the task's candidates.  Tasks the scan finished itself have
-// surv_cnt = -1; tasks without survivors get empty candidates.
-__global__ void pq_select_kernel(RoundState s, lf_index idx, const int* __restrict__ surv_cnt, PQOverflow ov) {
-    const int lane = threadIdx.x & 31;
+// Tail of the projected scan, one warp per task with survivors (entries
+// [base, base + ns) of the entry list, contiguous per task): the rows whose int8
+// lower bound (pq_q8_bound_kernel) reaches the task threshold are re-read exactly in
+// fp64 (series.py:142-146), RF rows in flight, and the task's kc candidates written.
+// Without the int8 shadow (qc8 == nullptr) every entry is re-read.
+constexpr int PQT_WARPS = 8;
+__global__ void __launch_bounds__(PQT_WARPS * 32) pq_tail_kernel(RoundState s, lf_index idx,
+                                                                 const float* __restrict__ queries,
+                                                                 const int* __restrict__ surv_cnt, PQOverflow ov) {
+    __shared__ unsigned short s_rows[PQT_WARPS][CH];
+    __shared__ double s_dist[PQT_WARPS][CH];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long total = s.chunk_off[s.Q];
-    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-    for (long long t = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < total; t += nw) {
+    const long long nw = (long long)gridDim.x * PQT_WARPS;
+    const int m = idx.m;
+    unsigned short* rows_w = s_rows[wib];
+    double* dist_w = s_dist[wib];
+    unsigned long long c_exact = 0;
+    for (long long t = (long long)blockIdx.x * PQT_WARPS + wib; t < total; t += nw) {
         const int ns = surv_cnt[t];
-        if (ns < 0) continue;
-        double* cd = s.cand_d + t * s.kc;
-        long long* ci = s.cand_i + t * s.kc;
+        if (ns < 0) continue;                          // the scan warp finished this task
         if (ns == 0) {
             for (int i = lane; i < s.kc; i += 32) {
-                cd[i] = kInf;
-                ci[i] = -1;
+                s.cand_d[t * s.kc + i] = kInf;
+                s.cand_i[t * s.kc + i] = -1;
             }
             continue;
         }
         const int4 tk = s.tasks[t];
+        const int64_t q = tk.x;
         const int64_t r0 = idx.d_leaf_ptr[tk.y] + (int64_t)tk.z * CH;
-        const double bsf = round_bsf(s, tk.x);
+        const double bsf = round_bsf(s, q);
         const int base = ov.base[t];
-        double last_d = -1.0;
-        long long last_i = -1;
-        for (int sel = 0; sel < s.kc; ++sel) {
-            double bd = kInf;
-            long long bi = LLONG_MAX;
-            for (int i = lane; i < ns; i += 32) {
-                const double dd = ov.dist[base + i];
-                if (!(dd <= bsf)) continue;
-                const long long id = idx.d_row_id[r0 + ov.ent[base + i].y];
-                if (pair_less(last_d, last_i, dd, id) && pair_less(dd, id, bd, bi)) { bd = dd; bi = id; }
+        const int2* ent = ov.ent + base;
+        int nx = 0;                                    // rows for the exact re-read
+        if (ov.qc8 != nullptr) {                       // int8 stage done by pq_q8_bound_kernel
+            const float thr8 = __uint_as_float(ov.thr[t]);
+            for (int b = 0; b < ns; b += 32) {
+                const int i = b + lane;
+                const bool sv = i < ns && ov.lo8[base + i] <= thr8;
+                const unsigned bal = __ballot_sync(0xffffffffu, sv);
+                if (sv) rows_w[nx + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)ent[i].y;
+                nx += __popc(bal);
             }
+        } else {
+            for (int i = lane; i < ns; i += 32) rows_w[i] = (unsigned short)ent[i].y;
+            nx = ns;
+        }
+        __syncwarp();
+        c_exact += (unsigned long long)nx;
+        pq_exact_rows(idx.d_X + r0 * m, queries + q * m, m, rows_w, nx, dist_w, lane);
+        pq_select(s, t, lane, nx, bsf, [&](int i) { return dist_w[i]; },
+                  [&](int i) { return idx.d_row_id[r0 + rows_w[i]]; });
+        __syncwarp();
+    }
+    if (s.ea_count != nullptr) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double od = __shfl_xor_sync(0xffffffffu, bd, o);
-                const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                if (pair_less(od, oi, bd, bi)) { bd = od; bi = oi; }
+        for (int o = 16; o > 0; o >>= 1) c_exact += __shfl_xor_sync(0xffffffffu, c_exact, o);
+        if (lane == 0) {
+            if (c_exact) {
+                atomicAdd(&s.ea_count[1], c_exact);
+                atomicAdd(&s.ea_count[3], c_exact * (unsigned long long)m * 4ull);
             }
-            if (lane == 0) {
-                cd[sel] = bd;
-                ci[sel] = (bi == LLONG_MAX) ? -1 : bi;
-            }
-            last_d = bd;
-            last_i = bi;
         }
     }
 }
@@ -463,6 +512,8 @@ static cudaError_t launch_pq_kp(const RoundState& s, const lf_index& idx, const 
     return cudaGetLastError();
 }
 
+int pq_scan_warps() { return sm_count() * PQW<32>::WARPS; }   // >= PQW<64>: 16 vs 8 per SM
+
 cudaError_t launch_scan_pq(const RoundState& s, const lf_index& idx, const float* q, const int8_t* qc,
                            const float4* qm, int* surv_cnt, const PQOverflow& ov, int64_t max_tasks,
                            cudaStream_t st) {
@@ -471,11 +522,13 @@ cudaError_t launch_scan_pq(const RoundState& s, const lf_index& idx, const float
     e = idx.pca_k == 32 ? launch_pq_kp<32>(s, idx, q, qc, qm, surv_cnt, ov, st)
                         : launch_pq_kp<64>(s, idx, q, qc, qm, surv_cnt, ov, st);
     if (e != cudaSuccess) return e;
-    pq_over_exact_kernel<<<sm_count() * 8, 256, 0, st>>>(s, idx, q, ov);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    if (ov.qc8 != nullptr) {
+        pq_q8_bound_kernel<<<sm_count() * 8, 256, 0, st>>>(s, idx, ov);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
     const long long warps = std::min<long long>(max_tasks, (long long)sm_count() * 64);
-    pq_select_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(s, idx, surv_cnt, ov);
+    pq_tail_kernel<<<(unsigned)((warps + PQT_WARPS - 1) / PQT_WARPS), PQT_WARPS * 32, 0, st>>>(s, idx, q, surv_cnt, ov);
     return cudaGetLastError();
 }
 
