@@ -479,9 +479,7 @@ __global__ void __launch_bounds__(PQT_WARPS * 32) pq_tail_kernel(RoundState s, l
                   [&](int i) { return idx.d_row_id[r0 + rows_w[i]]; });
         __syncwarp();
     }
-    if (s.ea_count != nullptr) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) c_exact += __shfl_xor_sync(0xffffffffu, c_exact, o);
+    if (s.ea_count != nullptr) {                         // c_exact is warp-uniform
         if (lane == 0) {
             if (c_exact) {
                 atomicAdd(&s.ea_count[1], c_exact);
