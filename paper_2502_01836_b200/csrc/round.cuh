@@ -169,7 +169,7 @@ cudaError_t launch_project_queries(const float* q, int64_t Q, const lf_index& id
                                    cudaStream_t st);
 // Survivors of the projected scan: (task, row) entries, contiguous per task, for pq_tail_kernel.
 struct PQOverflow {
-    int2* ent;                                // [cap] (task, row in chunk); task < 0: unused slot
+    int4* ent;                                // [cap] (task, query, absolute row lo, hi); task < 0: unused
     int* n;                                   // entries claimed this launch (device counter)
     int* base;                                // [max_tasks] first entry of a task
     int cap;
@@ -183,7 +183,7 @@ struct PQOverflow {
     unsigned* thr;                            // [max_tasks] the projected stage's threshold (float bits)
 };
 int pq_scan_warps();                          // warps of one scan_pq_kernel launch
-constexpr int PQ_OVER_CAP = 8 << 20;          // 8M entries (64 MB)
+constexpr int PQ_OVER_CAP = 8 << 20;          // 8M entries (128 MB + lo8)
 cudaError_t launch_scan_pq(const RoundState& s, const lf_index& idx, const float* q, const int8_t* qc,
                            const float4* qm, int* surv_cnt, const PQOverflow& ov, int64_t max_tasks,
                            cudaStream_t st);

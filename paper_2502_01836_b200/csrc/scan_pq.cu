@@ -310,9 +310,10 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
             if ((bal[g] >> lane) & 1u) {
                 const int pos = off + __popc(bal[g] & below);
                 if (fits) {
-                    ov.ent[base + pos] = make_int2((int)t, g * 32 + lane);
+                    const int64_t ar = r0 + g * 32 + lane;      // absolute row
+                    ov.ent[base + pos] = make_int4((int)t, (int)q, (int)(unsigned)ar, (int)(ar >> 32));
                 } else {
-                    if ((long long)base + pos < (long long)ov.cap) ov.ent[base + pos] = make_int2(-1, 0);
+                    if ((long long)base + pos < (long long)ov.cap) ov.ent[base + pos] = make_int4(-1, 0, 0, 0);
                     rows_w[pos] = (unsigned short)(g * 32 + lane);
                 }
             }
@@ -362,20 +363,15 @@ __global__ void __launch_bounds__(256) pq_q8_bound_kernel(RoundState s, lf_index
     for (long long w0 = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (4 * R); w0 < n;
          w0 += nw * 4 * R) {
         long long ii[R];
-        int2 e[R];
+        int4 e[R];
         int64_t row[R];
         int64_t qq[R];
 #pragma unroll
         for (int u = 0; u < R; ++u) {
             ii[u] = w0 + u * 4 + grp;
-            e[u] = ii[u] < n ? ov.ent[ii[u]] : make_int2(-1, 0);
-            row[u] = 0;
-            qq[u] = 0;
-            if (e[u].x >= 0) {
-                const int4 tk = s.tasks[e[u].x];
-                row[u] = idx.d_leaf_ptr[tk.y] + (int64_t)tk.z * CH + e[u].y;
-                qq[u] = tk.x;
-            }
+            e[u] = ii[u] < n ? ov.ent[ii[u]] : make_int4(-1, 0, 0, 0);
+            row[u] = (int64_t)(unsigned)e[u].z | ((int64_t)e[u].w << 32);
+            qq[u] = e[u].y;
         }
         int dot[R];
 #pragma unroll
@@ -424,6 +420,8 @@ __global__ void __launch_bounds__(256) pq_q8_bound_kernel(RoundState s, lf_index
     }
 }
 
+__device__ __forceinline__ int64_t ent_row(int4 e) { return (int64_t)(unsigned)e.z | ((int64_t)e.w << 32); }
+
 // Tail of the projected scan, one warp per task with survivors (entries
 // [base, base + ns) of the entry list, contiguous per task): the rows whose int8
 // lower bound (pq_q8_bound_kernel) reaches the task threshold are re-read exactly in
@@ -457,7 +455,7 @@ __global__ void __launch_bounds__(PQT_WARPS * 32) pq_tail_kernel(RoundState s, l
         const int64_t r0 = idx.d_leaf_ptr[tk.y] + (int64_t)tk.z * CH;
         const double bsf = round_bsf(s, q);
         const int base = ov.base[t];
-        const int2* ent = ov.ent + base;
+        const int4* ent = ov.ent + base;
         int nx = 0;                                    // rows for the exact re-read
         if (ov.qc8 != nullptr) {                       // int8 stage done by pq_q8_bound_kernel
             const float thr8 = __uint_as_float(ov.thr[t]);
@@ -465,11 +463,11 @@ __global__ void __launch_bounds__(PQT_WARPS * 32) pq_tail_kernel(RoundState s, l
                 const int i = b + lane;
                 const bool sv = i < ns && ov.lo8[base + i] <= thr8;
                 const unsigned bal = __ballot_sync(0xffffffffu, sv);
-                if (sv) rows_w[nx + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)ent[i].y;
+                if (sv) rows_w[nx + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)(ent_row(ent[i]) - r0);
                 nx += __popc(bal);
             }
         } else {
-            for (int i = lane; i < ns; i += 32) rows_w[i] = (unsigned short)ent[i].y;
+            for (int i = lane; i < ns; i += 32) rows_w[i] = (unsigned short)(ent_row(ent[i]) - r0);
             nx = ns;
         }
         __syncwarp();

@@ -700,7 +700,7 @@ static int session_begin(lf_session* ss) {
         LF_CUDA(ss->pq_cnt.alloc(sizeof(int) * max_tasks, st));
         LF_CUDA(ss->pq_trows.alloc(sizeof(int4) * max_tasks, st));
         s.task_rows = ss->pq_trows.as<int4>();
-        LF_CUDA(ss->pq_oent.alloc(sizeof(int2) * PQ_OVER_CAP, st));
+        LF_CUDA(ss->pq_oent.alloc(sizeof(int4) * PQ_OVER_CAP, st));
         LF_CUDA(ss->pq_on.alloc(sizeof(int), st));
         LF_CUDA(ss->pq_obase.alloc(sizeof(int) * max_tasks, st));
         LF_CUDA(ss->pq_wrows.alloc(sizeof(unsigned short) * CH * pq_scan_warps(), st));
@@ -844,7 +844,7 @@ static int session_enqueue(lf_session* ss, const double* d_bound, double* d_bsf_
     if (ea && ss->pq && !(ss->round == 0 && ss->q8)) {
         // round 0 has no best-so-far yet: the projected bound's loose upper end would let
         // most rows through, so the first round runs the full-length int8 scan
-        const PQOverflow ov{ss->pq_oent.as<int2>(), ss->pq_on.as<int>(),
+        const PQOverflow ov{ss->pq_oent.as<int4>(), ss->pq_on.as<int>(),
                             ss->pq_obase.as<int>(), PQ_OVER_CAP, ss->pq_wrows.as<unsigned short>(),
                             ss->pq_wdist.as<double>(), ss->q8 ? ss->qc8.as<int8_t>() : nullptr,
                             ss->q8 ? ss->qm8.as<float4>() : nullptr, (idx.m + 255) / 256 * 256,
