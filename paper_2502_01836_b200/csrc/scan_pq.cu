@@ -43,6 +43,12 @@ struct PQW {
     static constexpr int SMEM = BAR_OFF + WARPS * PQW_NS * 8;
 };
 
+__device__ __forceinline__ float sqrt_approx(float x) {   // MUFU.SQRT, denormals kept
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // Query projection: y_q = P (q - mu) in fp64, residual norm, int8 codes (same
 // scheme as the rows).  Warp per query.  codes [Q][KP], meta [Q] = {s, qq, e, r}.
 __global__ void project_queries_kernel(const float* __restrict__ queries, int64_t Q, int m, int k, int KP,
@@ -234,8 +240,11 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
         const float4 qmv = __ldg(qmeta + q);
         const float sq = qmv.x, eq = qmv.z, rq = qmv.w;
         const float sq2qq = sq * sq * qmv.y;
-        float lo[PQ_SLOTS];
-        float hmin = __int_as_float(0x7f800000);
+        const float sq2 = 2.f * sq;
+        // lo2 / hi2: squares of the interval ends before their (1 -+ 1e-5) factors; the
+        // comparisons below run in the squared domain (one sqrt per task, not two per row)
+        float lo2[PQ_SLOTS];
+        float hmin2 = __int_as_float(0x7f800000);
 #pragma unroll
         for (int p = 0; p < PQ_PIECES; ++p) {
             if (p < pieces) {
@@ -245,12 +254,11 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
                 for (int u = 0; u < RPL; ++u) {
                     const int ri = u * 32 + lane;
                     const bool v = p * PQW_STG + ri < nrows;
+                    // rows past the chunk's end read stale slot bytes; their result is masked
                     int4 w[V];
 #pragma unroll
-                    for (int c = 0; c < V; ++c)
-                        w[c] = v ? *reinterpret_cast<const int4*>(stg + ri * KP + c * 16) : make_int4(0, 0, 0, 0);
-                    const float4 mr = v ? *reinterpret_cast<const float4*>(stg + C::CODE + ri * 16)
-                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (int c = 0; c < V; ++c) w[c] = *reinterpret_cast<const int4*>(stg + ri * KP + c * 16);
+                    const float4 mr = *reinterpret_cast<const float4*>(stg + C::CODE + ri * 16);
                     int dot = 0;
 #pragma unroll
                     for (int c = 0; c < V; ++c) {
@@ -259,37 +267,43 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
                         dot = __dp4a(w[c].z, qw[c].z, dot);
                         dot = __dp4a(w[c].w, qw[c].w, dot);
                     }
-                    const float sx2xx = mr.x * mr.x * mr.y;
+                    const float nn = mr.y + sq2qq;               // ||x_c||^2 + ||q_c||^2
+                    const float a2 = fmaf(-(mr.x * sq2), (float)dot, nn);
+                    const float tol = 1e-5f * nn;
                     const float e = mr.z + eq;
-                    const float a2 = sx2xx + sq2qq - 2.f * (mr.x * sq) * (float)dot;
-                    const float tol = 1e-5f * (sx2xx + sq2qq);
-                    const float alo = fmaxf(sqrtf(fmaxf(a2 - tol, 0.f)) - e, 0.f);
-                    const float ahi = sqrtf(fmaxf(a2 + tol, 0.f)) + e;
-                    const float blo = fmaxf(fabsf(mr.w - rq) - 1e-6f * (mr.w + rq), 0.f);
-                    const float bhi = (mr.w + rq) * (1.f + 1e-6f);
-                    lo[p * RPL + u] = v ? sqrtf(fmaf(alo, alo, blo * blo)) * (1.f - 1e-5f) : __int_as_float(0x7f800000);
-                    if (v) hmin = fminf(hmin, sqrtf(fmaf(ahi, ahi, bhi * bhi)) * (1.f + 1e-5f));
+                    // sqrt.approx (rel err < 2^-22): the tol slack (>= 2.5e-6 sqrt(a2)) and the
+                    // final 1 -+ 1e-5 factors cover it, so both ends stay rigorous
+                    const float alo = fmaxf(sqrt_approx(fmaxf(a2 - tol, 0.f)) - e, 0.f);
+                    const float ahi = sqrt_approx(fmaxf(a2 + tol, 0.f)) + e;
+                    const float rs = mr.w + rq;
+                    const float blo = fmaxf(fmaf(-1e-6f, rs, fabsf(mr.w - rq)), 0.f);
+                    const float bhi = rs * (1.f + 1e-6f);
+                    lo2[p * RPL + u] = v ? fmaf(alo, alo, blo * blo) : __int_as_float(0x7f800000);
+                    hmin2 = fminf(hmin2, v ? fmaf(ahi, ahi, bhi * bhi) : __int_as_float(0x7f800000));
                 }
                 __syncwarp();                            // every lane has read the slot
                 issue(cslot);                            // refill it NS pieces ahead
                 if (++cslot == PQW_NS) { cslot = 0; cph ^= 1; }
             } else {
 #pragma unroll
-                for (int u = 0; u < RPL; ++u) lo[p * RPL + u] = __int_as_float(0x7f800000);
+                for (int u = 0; u < RPL; ++u) lo2[p * RPL + u] = __int_as_float(0x7f800000);
             }
         }
         double thr = bsf;
         if (s.k == 1) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) hmin = fminf(hmin, __shfl_xor_sync(0xffffffffu, hmin, o));
-            thr = fmin(thr, (double)hmin);
+            for (int o = 16; o > 0; o >>= 1) hmin2 = fminf(hmin2, __shfl_xor_sync(0xffffffffu, hmin2, o));
+            thr = fmin(thr, (double)(sqrtf(hmin2) * (1.f + 1e-5f)));
         }
         const float thr_f = thr < kInf ? __double2float_ru(thr) : __int_as_float(0x7f800000);
+        // keep iff sqrt(lo2) (1 - 1e-5) <= thr  <=>  lo2 <= (thr / (1 - 1e-5))^2, rounded up
+        const float thr2 = thr < kInf ? __double2float_ru((thr / (1.0 - 1e-5)) * (thr / (1.0 - 1e-5)))
+                                      : __int_as_float(0x7f800000);
         unsigned bal[PQ_SLOTS];
         int ns = 0;
 #pragma unroll
         for (int g = 0; g < PQ_SLOTS; ++g) {
-            bal[g] = __ballot_sync(0xffffffffu, lo[g] <= thr_f);
+            bal[g] = __ballot_sync(0xffffffffu, lo2[g] <= thr2);
             ns += __popc(bal[g]);
         }
         c_rows += (unsigned long long)nrows;

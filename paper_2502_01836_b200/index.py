@@ -331,8 +331,8 @@ class DeviceIndex:
     def ensure_pca(self, k: int = 32, sample: int = 200_000, seed: int = 0, min_energy: float | None = None) -> bool:
         """Projected shadow for the two-stage scan (lf_index.d_Xp): the top-k principal
         directions of a row sample (fp64 SVD, orthonormal rows), and per row the int8
-        codes of y = P (x - mu) with {scale, sum code^2, code error (rounded up),
-        residual norm}.  Index-build plumbing in torch; the search reads it in the
+        codes of y = P (x - mu) with {scale, ||scale * code||^2, code error (rounded
+        up), residual norm}.  Index-build plumbing in torch; the search reads it in the
         scan kernel.  With min_energy, the shadow is built only when the k directions
         hold at least that fraction of the sample's centred energy (self.pca_energy).
         Returns whether the shadow exists."""
@@ -368,7 +368,8 @@ class DeviceIndex:
                 e32 = e.float()
                 e32 = torch.where(e32.double() < e, torch.nextafter(e32, inf32), e32)      # rounded up
                 codes[r0:r0 + (1 << 20)] = c.to(torch.int8)
-                meta[r0:r0 + (1 << 20)] = torch.stack([s32, (c * c).sum(1).float(), e32, r.float()], dim=1)
+                xx = (s32.double() ** 2 * (c * c).sum(1)).float()      # ||scale * code||^2
+                meta[r0:r0 + (1 << 20)] = torch.stack([s32, xx, e32, r.float()], dim=1)
         self.pca_k, self.P, self.mu, self.Xp, self.pmeta = k, P, mu.contiguous(), codes, meta
         return True
 
