@@ -196,6 +196,22 @@ int lf_filter_predict_tc(const float* d_queries, int64_t Q, int32_t m,
                          const float* d_b2, int32_t F, float* d_pred, void* stream);
 
 /*
+ * The same GEMM with fp16 operands (tcgen05.mma kind::f16, twice the tf32 rate).
+ * Every operand row is stored scaled by a power of two so its max |value| lies in
+ * [2^13, 2^14): fp16 then keeps tf32's 10-bit mantissa with no overflow, and the
+ * epilogue undoes the scaling exactly.  d_W1T_h [F][hidden][in] fp16 bits with
+ * per-filter exponents d_wexp [F] (lf_filter_rows_to_f16 over W1T viewed as F x m*m
+ * rows); the queries are converted inside the call.  m in {64, 128, 192, 256}.
+ */
+int lf_filter_predict_f16(const float* d_queries, int64_t Q, int32_t m,
+                          const uint16_t* d_W1T_h, const int32_t* d_wexp, const float* d_b1,
+                          const float* d_W2, const float* d_b2, int32_t F, float* d_pred,
+                          void* stream);
+/* fp32 rows [rows][m] -> fp16 bits scaled by 2^-exps[r] (max |value| in [2^13, 2^14)). */
+int lf_filter_rows_to_f16(const float* d_X, int64_t rows, int32_t m, uint16_t* d_out,
+                          int32_t* d_exps, void* stream);
+
+/*
  * Predictions for an explicit list of (query, filter) pairs on the tensor cores:
  * pairs are bucketed by filter, their query rows gathered, and one tcgen05 tile
  * list evaluates them -- bit-identical to the same pairs of lf_filter_predict_tc.

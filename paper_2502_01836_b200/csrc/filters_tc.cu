@@ -12,14 +12,15 @@
 // epilogue warps read their accumulator row with tcgen05.ld and fold bias,
 // rectifier and the W2 dot product in registers -- H never leaves the SM.
 //
-// Warp roles (192 threads, one persistent CTA per SM):
-//   warp 0: TMA producer    warp 1: TMEM owner + MMA issuer    warps 2-5: epilogue
+// Warp roles (320 threads, one persistent CTA per SM):
+//   warp 0: TMA producer    warp 1: TMEM owner + MMA issuer    warps 2-9: epilogue
 //
 // Batch invariance: an output's K order (k-blocks, then the four
 // K=8 MMAs inside a block) and its j order in the epilogue depend only on m,
 // never on Q or on the tile a query falls in.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cuda_fp16.h>
 
 #include <cstdlib>
 
@@ -29,14 +30,15 @@ namespace lf {
 namespace tc {
 
 constexpr int BM = 128;          // queries per tile (UMMA M)
-constexpr int BK = 32;           // fp32 elements per 128-byte swizzle row
+constexpr int BK = 32;           // fp32 elements per 128-byte swizzle row (fp16: 64)
 constexpr int STAGES = 4;
-constexpr int THREADS = 192;
+constexpr int THREADS = 320;          // producer, MMA issuer, 8 epilogue warps
 constexpr int A_BYTES = BM * BK * 4;          // 16 KiB
-constexpr int B_BYTES_MAX = 256 * BK * 4;     // 32 KiB (N = m <= 256)
+constexpr int B_BYTES_MAX = 256 * 128;        // 32 KiB (N = m <= 256, 128-byte rows)
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES_MAX;
 constexpr int TMEM_COLS = 512;                // 2 accumulator buffers x 256 columns
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + 4096 /*b1, W2 x 2*/;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + 4096 /*b1, W2 x 2*/ +
+                           1024 /*half-row partials x 2*/;
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -94,6 +96,20 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// Instruction descriptor: D f32, A/B f16, both K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+    return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
 #define LF_TMEM_LD32(taddr, r)                                                                                 \
     asm volatile(                                                                                              \
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"      \
@@ -120,11 +136,21 @@ struct PairArgs {
     int Nn;
 };
 
-template <bool PAIRS>
+// fp16 operands (F16 = true): each X row and each filter's W1 is stored scaled by a
+// power of two (max |value| in [2^13, 2^14), exact), so fp16 keeps tf32's 10-bit
+// mantissa without overflow; the epilogue multiplies the accumulator back by
+// 2^(xexp[row] + wexp[f]) -- exact -- before the bias.
+struct F16Args {
+    const int* xexp;             // per X row (dense: query; pairs: gathered row)
+    const int* wexp;             // per filter
+};
+
+template <bool PAIRS, bool F16>
 __global__ void __launch_bounds__(THREADS, 1)
 filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
                  int64_t Q, int m, int F, const float* __restrict__ b1, const float* __restrict__ W2,
-                 const float* __restrict__ b2, float* __restrict__ pred, PairArgs pa) {
+                 const float* __restrict__ b2, float* __restrict__ pred, PairArgs pa, F16Args fa) {
+    constexpr int BKE = F16 ? 64 : BK;               // elements per 128-byte K block
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -136,12 +162,12 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_mb = (int)((Q + BM - 1) / BM);
     const int64_t n_tiles = PAIRS ? (int64_t)*pa.n_tiles : (int64_t)F * n_mb;
-    const int n_kb = m / BK;
-    const uint32_t b_bytes = (uint32_t)m * BK * 4;
+    const int n_kb = m / BKE;
+    const uint32_t b_bytes = (uint32_t)m * 128;
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
+        for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 8); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
@@ -175,15 +201,15 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
                     uint8_t* sa = smem + stage * STAGE_BYTES;
                     uint8_t* sb = sa + A_BYTES;
                     mbar_expect_tx(&full[stage], A_BYTES + b_bytes);
-                    tma_2d(&map_x, &full[stage], sa, kb * BK, row0);
-                    tma_2d(&map_w, &full[stage], sb, kb * BK, f * m);
+                    tma_2d(&map_x, &full[stage], sa, kb * BKE, row0);
+                    tma_2d(&map_w, &full[stage], sb, kb * BKE, f * m);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {                                     // ---- MMA issuer (single thread)
-            const uint32_t idesc = idesc_tf32(BM, m);
+            const uint32_t idesc = F16 ? idesc_f16(BM, m) : idesc_tf32(BM, m);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -198,9 +224,14 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
                     const uint32_t sa = su32(smem + stage * STAGE_BYTES);
                     const uint32_t sb = sa + A_BYTES;
 #pragma unroll
-                    for (int kk = 0; kk < BK / 8; ++kk)          // K = 8 tf32 = 32 bytes per MMA
-                        mma_tf32(d, sw128_desc(sa + kk * 32), sw128_desc(sb + kk * 32), idesc,
-                                 (kb | kk) != 0 ? 1u : 0u);
+                    for (int kk = 0; kk < 4; ++kk) {             // K = 8 tf32 / 16 f16 = 32 bytes per MMA
+                        if (F16)
+                            mma_f16(d, sw128_desc(sa + kk * 32), sw128_desc(sb + kk * 32), idesc,
+                                    (kb | kk) != 0 ? 1u : 0u);
+                        else
+                            mma_tf32(d, sw128_desc(sa + kk * 32), sw128_desc(sb + kk * 32), idesc,
+                                     (kb | kk) != 0 ? 1u : 0u);
+                    }
                     mma_commit(&empty[stage]);                  // smem slot free once these MMAs retire
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -208,14 +239,21 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
         }
-    } else {                                                 // ---- epilogue (warps 2..5)
+    } else {                                                 // ---- epilogue (warps 2..9)
         // b1[f] / W2[f] (2 x m floats) are staged in shared memory one tile ahead with
-        // cp.async by the 128 epilogue threads: each tile is a new filter for this CTA,
+        // cp.async by the epilogue threads: each tile is a new filter for this CTA,
         // so reading them with per-column global loads paid an L2 round trip per chunk.
-        const int et = threadIdx.x - 64;                     // 0..127
+        // Two warps per TMEM lane quarter: half 0 (warps 2-5) folds columns [0, hc),
+        // half 1 (warps 6-9) columns [hc, m); half 1 hands its partial to half 0 through
+        // shared memory (double-buffered by tile parity, one named barrier per pair).
+        const int et = threadIdx.x - 64;                     // 0..255
         const int quarter = warp & 3;                        // TMEM lanes [32*quarter, +32)
+        const int half = (warp - 2) >> 2;
         const int row = quarter * 32 + lane;
+        const int hc = ((m >> 1) + 31) & ~31;                // half 0's columns
+        const int c_begin = half ? hc : 0, c_end = half ? m : hc;
         float* pbuf = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);   // [2][2][256]
+        float* xbuf = pbuf + 2 * 512;                                               // [2][128]
         auto tile_filter = [&](int64_t t, int& f, int& row0, int& nrows) {
             if (PAIRS) {
                 const int4 tl = pa.tiles[t];
@@ -251,14 +289,20 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
             tile_filter(t, f, row0, nrows);
             stage_params(t + gridDim.x, slot ^ 1);
             asm volatile("cp.async.wait_group 1;" ::: "memory");
-            asm volatile("bar.sync 1, 128;" ::: "memory");   // this tile's parameters visible
+            asm volatile("bar.sync 1, 256;" ::: "memory");   // this tile's parameters visible
             const float4* b1s = reinterpret_cast<const float4*>(pbuf + slot * 512);
             const float4* w2s = reinterpret_cast<const float4*>(pbuf + slot * 512 + 256);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             float part = 0.f;
+            float sc = 1.f;                                  // F16: undo the operands' scaling
+            if (F16) {
+                const int64_t xr = (int64_t)row0 + row;
+                const int ex = (PAIRS ? row < nrows : xr < Q) ? fa.xexp[xr] : 0;
+                sc = scalbnf(1.f, ex + fa.wexp[f]);
+            }
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * 256);
-            for (int c0 = 0; c0 < m; c0 += 32) {
+            for (int c0 = c_begin; c0 < c_end; c0 += 32) {
                 uint32_t r[32];
                 LF_TMEM_LD32(taddr + (uint32_t)c0, r);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -270,7 +314,9 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
                     const float wv[4] = {ww.x, ww.y, ww.z, ww.w};
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        const float h = fmaxf(__fadd_rn(__uint_as_float(r[j4 * 4 + u]), bv[u]), 0.f);
+                        const float a = F16 ? __fmul_rn(__uint_as_float(r[j4 * 4 + u]), sc)
+                                            : __uint_as_float(r[j4 * 4 + u]);
+                        const float h = fmaxf(__fadd_rn(a, bv[u]), 0.f);
                         part = __fmaf_rn(h, wv[u], part);
                     }
                 }
@@ -278,17 +324,22 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
-            if (PAIRS) {
-                if (row < nrows) {
-                    const int2 d = pa.dst[row0 + row];
-                    const double pv = (double)__fadd_rn(part, b2[f]);
-                    pa.adj[(int64_t)d.x * pa.Nn + d.y] = pa.offset != nullptr ? pv - pa.offset[f] : pv;
+            if (half) xbuf[slot * 128 + row] = part;
+            asm volatile("bar.sync %0, 64;" ::"r"(2 + quarter) : "memory");   // the quarter's two warps
+            if (half == 0) {
+                part = __fadd_rn(part, xbuf[slot * 128 + row]);
+                if (PAIRS) {
+                    if (row < nrows) {
+                        const int2 d = pa.dst[row0 + row];
+                        const double pv = (double)__fadd_rn(part, b2[f]);
+                        pa.adj[(int64_t)d.x * pa.Nn + d.y] = pa.offset != nullptr ? pv - pa.offset[f] : pv;
+                    }
+                } else {
+                    const int64_t q = (int64_t)row0 + row;
+                    if (q < Q) pred[q * F + f] = __fadd_rn(part, b2[f]);
                 }
-            } else {
-                const int64_t q = (int64_t)row0 + row;
-                if (q < Q) pred[q * F + f] = __fadd_rn(part, b2[f]);
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");   // slot free for the tile after next
+            asm volatile("bar.sync 1, 256;" ::: "memory");   // slot free for the tile after next
             slot ^= 1;
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
@@ -315,14 +366,16 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-static int make_map(CUtensorMap* map, const float* base, int64_t rows, int cols, int box_rows) {
+static int make_map(CUtensorMap* map, const void* base, int64_t rows, int cols, int box_rows, bool f16 = false) {
     auto fn = encode_fn();
     if (!fn) return fail(LF_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    const int esize = f16 ? 2 : 4;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(float)};
-    cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * esize};
+    cuuint32_t box[2] = {(cuuint32_t)(128 / esize), (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+    CUresult r = fn(map, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                    const_cast<void*>(base), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(LF_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
@@ -350,14 +403,14 @@ extern "C" int lf_filter_predict_tc(const float* d_queries, int64_t Q, int32_t m
     const int n_mb = (int)((Q + tc::BM - 1) / tc::BM);
     static bool attr_set = false;
     if (!attr_set) {
-        LF_CUDA(cudaFuncSetAttribute(tc::filter_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        LF_CUDA(cudaFuncSetAttribute(tc::filter_tc_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      tc::SMEM_BYTES));
         attr_set = true;
     }
     const int64_t tiles = (int64_t)F * n_mb;
     const int grid = (int)std::min<int64_t>(tiles, sm_count());
-    tc::filter_tc_kernel<false><<<grid, tc::THREADS, tc::SMEM_BYTES, as_stream(stream)>>>(
-        mx, mw, Q, m, F, d_b1, d_W2, d_b2, d_pred, tc::PairArgs{});
+    tc::filter_tc_kernel<false, false><<<grid, tc::THREADS, tc::SMEM_BYTES, as_stream(stream)>>>(
+        mx, mw, Q, m, F, d_b1, d_W2, d_b2, d_pred, tc::PairArgs{}, tc::F16Args{});
     LF_CUDA(cudaGetLastError());
     return LF_OK;
 }
@@ -376,13 +429,14 @@ int filter_pairs_tc(const float* d_rows, int64_t P, int m, const float* d_W1T, c
     if (rc) return rc;
     static bool attr_set = false;
     if (!attr_set) {
-        LF_CUDA(cudaFuncSetAttribute(tc::filter_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        LF_CUDA(cudaFuncSetAttribute(tc::filter_tc_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      tc::SMEM_BYTES));
         attr_set = true;
     }
     tc::PairArgs pa{d_tiles, d_ntiles, d_dst, d_offset, d_adj, Nn};
-    tc::filter_tc_kernel<true><<<sm_count(), tc::THREADS, tc::SMEM_BYTES, st>>>(mx, mw, P, m, F, d_b1, d_W2, d_b2,
-                                                                               nullptr, pa);
+    tc::filter_tc_kernel<true, false><<<sm_count(), tc::THREADS, tc::SMEM_BYTES, st>>>(mx, mw, P, m, F, d_b1, d_W2,
+                                                                                      d_b2, nullptr, pa,
+                                                                                      tc::F16Args{});
     LF_CUDA(cudaGetLastError());
     return LF_OK;
 }
@@ -442,4 +496,75 @@ extern "C" int lf_filter_predict_pairs_tc(const float* d_queries, int32_t m, con
     LF_CUDA(cudaGetLastError());
     return filter_pairs_tc(rows.as<float>(), P, m, d_W1T, d_b1, d_W2, d_b2, F, tiles.as<int4>(), ntiles.as<int>(),
                            dst.as<int2>(), nullptr, d_out, 1, st);
+}
+
+// ---------------------------------------------------------------------------
+// fp16 operands: rows scaled by a power of two into fp16 (exact scaling, RN to
+// fp16's 10-bit mantissa -- tf32's precision), kind::f16 MMAs at twice the tf32 rate.
+namespace lf {
+namespace tc {
+__global__ void rows_to_f16_kernel(const float* __restrict__ X, int64_t rows, int m, __half* __restrict__ out,
+                                   int* __restrict__ exps) {
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    const float* x = X + r * m;
+    float amax = 0.f;
+    for (int c = lane; c < m; c += 32) amax = fmaxf(amax, fabsf(x[c]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    const int e = amax > 0.f ? ilogbf(amax) - 13 : 0;    // max |x| 2^-e in [2^13, 2^14)
+    for (int c = lane; c < m; c += 32) out[r * m + c] = __float2half_rn(scalbnf(x[c], -e));
+    if (lane == 0) exps[r] = e;
+}
+}  // namespace tc
+
+int rows_to_f16(const float* d_X, int64_t rows, int m, __half* d_out, int* d_exps, cudaStream_t st) {
+    if (rows == 0) return LF_OK;
+    tc::rows_to_f16_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, st>>>(d_X, rows, m, d_out, d_exps);
+    LF_CUDA(cudaGetLastError());
+    return LF_OK;
+}
+}  // namespace lf
+
+extern "C" int lf_filter_rows_to_f16(const float* d_X, int64_t rows, int32_t m, uint16_t* d_out, int32_t* d_exps,
+                                     void* stream) {
+    using namespace lf;
+    LF_REQUIRE(rows >= 0 && m >= 1, "bad sizes");
+    return rows_to_f16(d_X, rows, m, reinterpret_cast<__half*>(d_out), d_exps, as_stream(stream));
+}
+
+extern "C" int lf_filter_predict_f16(const float* d_queries, int64_t Q, int32_t m, const uint16_t* d_W1T_h,
+                                     const int32_t* d_wexp, const float* d_b1, const float* d_W2, const float* d_b2,
+                                     int32_t F, float* d_pred, void* stream) {
+    using namespace lf;
+    LF_REQUIRE(Q >= 0 && F >= 0, "bad sizes");
+    LF_REQUIRE(m >= 64 && m <= 256 && m % 64 == 0, "fp16 filter path needs m in {64, 128, 192, 256}");
+    LF_REQUIRE(((uintptr_t)d_W1T_h & 15) == 0 && ((uintptr_t)d_b1 & 15) == 0 && ((uintptr_t)d_W2 & 15) == 0,
+               "operands must be 16-byte aligned");
+    if (Q == 0 || F == 0) return LF_OK;
+    cudaStream_t st = as_stream(stream);
+    Scratch xh, xe;
+    LF_CUDA(xh.alloc(sizeof(__half) * (size_t)Q * m, st));
+    LF_CUDA(xe.alloc(sizeof(int) * (size_t)Q, st));
+    int rc = rows_to_f16(d_queries, Q, m, xh.as<__half>(), xe.as<int>(), st);
+    if (rc) return rc;
+    CUtensorMap mx, mw;
+    rc = tc::make_map(&mx, xh.p, Q, m, tc::BM, true);
+    if (rc) return rc;
+    rc = tc::make_map(&mw, d_W1T_h, (int64_t)F * m, m, m, true);
+    if (rc) return rc;
+    const int n_mb = (int)((Q + tc::BM - 1) / tc::BM);
+    static bool attr_set = false;
+    if (!attr_set) {
+        LF_CUDA(cudaFuncSetAttribute(tc::filter_tc_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     tc::SMEM_BYTES));
+        attr_set = true;
+    }
+    const int64_t tiles = (int64_t)F * n_mb;
+    const int grid = (int)std::min<int64_t>(tiles, sm_count());
+    tc::filter_tc_kernel<false, true><<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(
+        mx, mw, Q, m, F, d_b1, d_W2, d_b2, d_pred, tc::PairArgs{}, tc::F16Args{xe.as<int>(), d_wexp});
+    LF_CUDA(cudaGetLastError());
+    return LF_OK;
 }

@@ -364,9 +364,10 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
 
 // int8 stage of the projected scan's survivor entries, row-parallel: the full-length
 // int8 interval of each entry (the bound of scan_q8_kernel; 8 lanes per row, 16 code
-// bytes per lane per load, 2 rows per 8-lane group).  lo is kept per entry; for k = 1
-// the task threshold is min'ed with every entry's upper bound -- the task's best row
-// survives both stages, so no row whose lower bound exceeds it can be the nearest.
+// bytes per lane per load, 2 rows per 8-lane group, row metadata loaded up front).
+// lo is kept per entry; for k = 1 the task threshold is min'ed with every entry's
+// upper bound -- the task's best row survives both stages, so no row whose lower
+// bound exceeds it can be the nearest.
 __global__ void __launch_bounds__(256) pq_q8_bound_kernel(RoundState s, lf_index idx, PQOverflow ov) {
     constexpr int R = 2;
     const int lane = threadIdx.x & 31, sl = lane & 7, grp = lane >> 3;
@@ -380,6 +381,7 @@ __global__ void __launch_bounds__(256) pq_q8_bound_kernel(RoundState s, lf_index
         int4 e[R];
         int64_t row[R];
         int64_t qq[R];
+        float4 mr[R], qmv[R];
 #pragma unroll
         for (int u = 0; u < R; ++u) {
             ii[u] = w0 + u * 4 + grp;
@@ -389,7 +391,12 @@ __global__ void __launch_bounds__(256) pq_q8_bound_kernel(RoundState s, lf_index
         }
         int dot[R];
 #pragma unroll
-        for (int u = 0; u < R; ++u) dot[u] = 0;
+        for (int u = 0; u < R; ++u) {
+            dot[u] = 0;
+            const bool v = e[u].x >= 0 && sl == 0;          // metadata with the first code loads
+            mr[u] = v ? __ldcs(reinterpret_cast<const float4*>(idx.d_qmeta) + row[u]) : make_float4(0.f, 0.f, 0.f, 0.f);
+            qmv[u] = v ? __ldg(ov.qm8 + qq[u]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
         for (int c = sl * 16; c < M8; c += 128) {
             int4 w[R], qv[R];
 #pragma unroll
@@ -412,13 +419,11 @@ __global__ void __launch_bounds__(256) pq_q8_bound_kernel(RoundState s, lf_index
             dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], 2);
             dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], 1);
             if (e[u].x >= 0 && sl == 0) {
-                const float4 mr = __ldcs(reinterpret_cast<const float4*>(idx.d_qmeta) + row[u]);
-                const float4 qmv = __ldg(ov.qm8 + qq[u]);
-                const float sq = qmv.x, eq = qmv.z;
-                const float sq2qq = sq * sq * qmv.y;
-                const float sx2xx = mr.x * mr.x * mr.y;
-                const float ee = mr.z + eq;
-                const float d2 = sx2xx + sq2qq - 2.f * (mr.x * sq) * (float)dot[u];
+                const float sq = qmv[u].x, eq = qmv[u].z;
+                const float sq2qq = sq * sq * qmv[u].y;
+                const float sx2xx = mr[u].x * mr[u].x * mr[u].y;
+                const float ee = mr[u].z + eq;
+                const float d2 = sx2xx + sq2qq - 2.f * (mr[u].x * sq) * (float)dot[u];
                 const float tol = 1e-5f * (sx2xx + sq2qq);
                 ov.lo8[ii[u]] = (sqrtf(fmaxf(d2 - tol, 0.f)) - ee) * (1.f - 1e-6f);
                 ++cnt;

@@ -11,15 +11,20 @@ ones used to search are bit-identical (enhanced.py:283-285).
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import _lib
 
 
 class FilterPack:
-    """path: "tc" (tcgen05 tf32, default when m is a multiple of 32 up to 256) or
-    "simt" (fp32 CUDA-core FFMA).  Calibration and search must use the same pack
-    (same path) -- predictions are then bit-identical (F6)."""
+    """path: "tc16" (tcgen05 kind::f16 over power-of-two-scaled fp16 operands --
+    tf32's mantissa at twice its rate; default when m is a multiple of 64 up to 256),
+    "tc" (tcgen05 tf32; default for other multiples of 32; the lazy in-search
+    inference runs on it) or "simt" (fp32 CUDA-core FFMA).  LF_FILTER_PATH overrides
+    the default.  Calibration and search must use the same pack (same path) --
+    predictions are then bit-identical (F6)."""
 
     def __init__(self, leaf_ids, W1, b1, W2, b2, device=None, path: str | None = None):
         torch = _lib.require_cuda()
@@ -45,11 +50,19 @@ class FilterPack:
         self.device = dev
         self._slot_maps = {}
         tc_ok = F > 0 and m % 32 == 0 and 32 <= m <= 256
-        self.path = path or ("tc" if tc_ok else "simt")
-        if self.path == "tc":
+        tc16_ok = tc_ok and m % 64 == 0
+        self.path = path or os.environ.get("LF_FILTER_PATH") or ("tc16" if tc16_ok else "tc" if tc_ok else "simt")
+        if self.path in ("tc", "tc16"):
             if not tc_ok:
                 raise ValueError("tensor-core filter path needs m in {32, 64, ..., 256}")
+            if self.path == "tc16" and not tc16_ok:
+                raise ValueError("fp16 tensor-core filter path needs m in {64, 128, 192, 256}")
             self.W1T = self.W1.transpose(1, 2).contiguous()     # K-major B operand [F][hidden][in]
+            if self.path == "tc16":
+                self.W1T_h = torch.empty((F, m, m), dtype=torch.float16, device=dev)
+                self.wexp = torch.empty(F, dtype=torch.int32, device=dev)
+                _lib.check(_lib.lib().lf_filter_rows_to_f16(self.W1T.data_ptr(), F, m * m, self.W1T_h.data_ptr(),
+                                                           self.wexp.data_ptr(), _lib.stream_ptr()))
         elif self.path != "simt":
             raise ValueError(f"unknown filter path {self.path!r}")
 
@@ -81,6 +94,12 @@ class FilterPack:
         if Q and self.n_filters:
             if q.shape[1] != self.m:
                 raise ValueError(f"input shape {tuple(q.shape)} does not match model dim {self.m}")
+            if self.path == "tc16":
+                _lib.check(_lib.lib().lf_filter_predict_f16(q.data_ptr(), Q, self.m, self.W1T_h.data_ptr(),
+                                                            self.wexp.data_ptr(), self.b1.data_ptr(),
+                                                            self.W2.data_ptr(), self.b2.data_ptr(), self.n_filters,
+                                                            out.data_ptr(), _lib.stream_ptr(stream)))
+                return out
             fn = _lib.lib().lf_filter_predict_tc if self.path == "tc" else _lib.lib().lf_filter_predict
             w = self.W1T if self.path == "tc" else self.W1
             _lib.check(fn(q.data_ptr(), Q, self.m, w.data_ptr(), self.b1.data_ptr(), self.W2.data_ptr(),

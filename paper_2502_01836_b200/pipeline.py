@@ -244,7 +244,9 @@ def search_queries(eidx, queries, k: int = 1, *, target: float | None = None, ex
     q = queries if isinstance(queries, torch.Tensor) else torch.from_numpy(
         np.ascontiguousarray(np.atleast_2d(queries), dtype=np.float32))
     q = q.to(device=di.device, dtype=torch.float32)
-    if lazy and pk.path == "tc":
+    if lazy and pk.path != "tc":
+        raise ValueError("lazy filter inference runs on the tf32 pack (FilterPack path 'tc', LF_FILTER_PATH=tc)")
+    if lazy:
         return search_batch(e.base, q.contiguous(), k, filters=pk, offsets=e.offset_vector(target, device=True),
                             leaf_filter=pk.leaf_filter(di), sequential=sequential,
                             max_round_leaves=max_round_leaves, want_trace=want_trace, stream=stream,

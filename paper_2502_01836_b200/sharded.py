@@ -172,7 +172,9 @@ def search_sharded(tree, queries, k: int = 1, *, rank: int, world: int, pack=Non
     q = q.to(device=di.device, dtype=torch.float32).contiguous()
     kw = {}
     if pack is not None and pack.n_filters:
-        if lazy and pack.path == "tc":
+        if lazy:
+            if pack.path != "tc":
+                raise ValueError("lazy filter inference runs on the tf32 pack (FilterPack path 'tc')")
             kw = dict(filters=pack, offsets=offsets, leaf_filter=pack.leaf_filter(di))
         else:
             kw = dict(predictions=pack.predict(q), offsets=offsets, leaf_filter=pack.leaf_filter(di))

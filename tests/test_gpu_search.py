@@ -158,20 +158,25 @@ def _pack(g, path=None):
 
 # tolerances: fp32 FFMA (simt) differs from OpenBLAS only in summation order;
 # tcgen05 kind::tf32 multiplies 10-bit-mantissa operands (fp32 accumulate).
-PRED_TOL = {"simt": dict(rtol=2e-5, atol=2e-5), "tc": dict(rtol=5e-3, atol=5e-3)}
+PRED_TOL = {"simt": dict(rtol=2e-5, atol=2e-5), "tc": dict(rtol=5e-3, atol=5e-3),
+            "tc16": dict(rtol=5e-3, atol=5e-3)}     # fp16 operands keep tf32's 10-bit mantissa
 
 
-@pytest.mark.parametrize("path", ["simt", "tc"])
+@pytest.mark.parametrize("path", ["simt", "tc", "tc16"])
 def test_filter_predictions_vs_reference(pipeline_golden, path):
     g = pipeline_golden
+    if path == "tc16" and np.shape(g["W1"])[-1] % 64:
+        pytest.skip("fp16 path needs m % 64 == 0")
     pred = _pack(g, path).predict(g["queries"]).cpu().numpy().astype(np.float64)
     np.testing.assert_allclose(pred, g["pred_queries"], **PRED_TOL[path])
 
 
-@pytest.mark.parametrize("path", ["simt", "tc"])
+@pytest.mark.parametrize("path", ["simt", "tc", "tc16"])
 def test_filter_predictions_batch_invariant(pipeline_golden, path):
     """F6: a query's predictions do not depend on the batch it is in."""
     g = pipeline_golden
+    if path == "tc16" and np.shape(g["W1"])[-1] % 64:
+        pytest.skip("fp16 path needs m % 64 == 0")
     pk = _pack(g, path)
     full = pk.predict(g["queries"]).cpu().numpy()
     for lo_, hi in ((0, 1), (7, 8), (5, 60), (33, 47)):
@@ -197,13 +202,37 @@ def test_filter_tc_vs_fp64(m):
     simt = FilterPack(list(range(F)), W1, b1, W2, b2, path="simt").predict(X).cpu().numpy()
     np.testing.assert_allclose(simt, ref, rtol=1e-5, atol=1e-5)
     np.testing.assert_allclose(tc, ref, rtol=5e-3, atol=5e-3)
+    if m % 64 == 0:
+        tc16 = FilterPack(list(range(F)), W1, b1, W2, b2, path="tc16").predict(X).cpu().numpy()
+        np.testing.assert_allclose(tc16, ref, rtol=5e-3, atol=5e-3)
+
+
+@pytest.mark.parametrize("m", [64, 256])
+def test_filter_f16_power_of_two_scaling(m):
+    """fp16 operands are stored scaled by powers of two: inputs and weights far outside
+    fp16's range (1e12, 1e-12) give the same predictions, bit for bit, as the same
+    problem rescaled by exact powers of two."""
+    from paper_2502_01836_b200 import FilterPack
+
+    rng = np.random.default_rng(7 + m)
+    F, Q = 9, 200
+    W1 = (rng.uniform(-1, 1, (F, m, m)) / np.sqrt(m)).astype(np.float32)
+    b1 = (rng.standard_normal((F, m)) * 0.1).astype(np.float32)
+    W2 = (rng.uniform(-1, 1, (F, m)) / np.sqrt(m)).astype(np.float32)
+    b2 = rng.standard_normal(F).astype(np.float32)
+    X = lo.randwalk(Q, m, 5).astype(np.float32)
+    base = FilterPack(list(range(F)), W1, b1, W2, b2, path="tc16").predict(X).cpu().numpy()
+    big = FilterPack(list(range(F)), W1 * np.float32(2.0 ** -40), b1, W2, b2, path="tc16")
+    got = big.predict(X * np.float32(2.0 ** 40)).cpu().numpy()
+    np.testing.assert_array_equal(got, base)
+    assert np.isfinite(base).all()
 
 
 def test_filter_known_answers(knowns):
     from paper_2502_01836_b200 import FilterPack
 
     for m in (32, 256):
-        for path in ("simt", "tc"):
+        for path in ("simt", "tc") + (("tc16",) if m % 64 == 0 else ()):
             pk = FilterPack([0], knowns[f"mlp_{m}_W1"][None], knowns[f"mlp_{m}_b1"][None],
                             knowns[f"mlp_{m}_W2"][None], knowns[f"mlp_{m}_b2"].reshape(1), path=path)
             got = pk.predict(knowns[f"mlp_{m}_x"]).cpu().numpy()[:, 0]
