@@ -381,7 +381,7 @@ def run_ours(args, rank, world, device):
             pred_steps += prof[12]
             stream_b += prof[13]
             exact_b += prof[14]
-            kernels += int(prof[5]) + (0 if args.lazy else 1)    # + the dense filter pass
+            kernels += int(prof[5]) + (0 if args.lazy else 2 if eidx.pack.path == "tc16" else 1)   # + dense pass
         ev1.record(stream)
         torch.cuda.synchronize()
     if args.ncu:
@@ -521,8 +521,8 @@ def run_ours(args, rank, world, device):
         "e2e": e2e,
         "gpu_launches": kernels,
         "roofline": {
-            "kernel": ("leaf scan (scan_q8_kernel round 0, then scan_pq_kernel -> pq_over_exact_kernel -> "
-                       "pq_select_kernel: int8 / projected-int8 bounds, exact fp64 survivors)") if pq_on
+            "kernel": ("leaf scan (scan_q8_kernel round 0, then scan_pq_kernel -> pq_q8_bound_kernel -> "
+                       "pq_tail_kernel: projected-int8 / int8 bounds, exact fp64 survivors)") if pq_on
                       else "leaf scan (scan_q8_kernel: TMA-pipelined int8-bounded scan, exact fp64 survivors)",
             "projected_shadow": {"pca_k": pca_k, "energy": pca_energy,
                                  "used": pq_on} if pca_k or pca_energy is not None else None,

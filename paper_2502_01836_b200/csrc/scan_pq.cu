@@ -50,49 +50,74 @@ __device__ __forceinline__ float sqrt_approx(float x) {   // MUFU.SQRT, denormal
 }
 
 // Query projection: y_q = P (q - mu) in fp64, residual norm, int8 codes (same
-// scheme as the rows).  Warp per query.  codes [Q][KP], meta [Q] = {s, qq, e, r}.
-__global__ void project_queries_kernel(const float* __restrict__ queries, int64_t Q, int m, int k, int KP,
-                                       const double* __restrict__ P, const double* __restrict__ mu,
-                                       int8_t* __restrict__ qc, float4* __restrict__ qm) {
-    const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (q >= Q) return;
+// scheme as the rows).  One CTA of 8 warps per query, each warp k / 8 directions;
+// the residual norm is sqrt(max(||q - mu||^2 - ||y_q||^2, 0)) (P has orthonormal
+// rows; fp64 keeps the cancellation far below the bound's 1e-6 slack).
+// codes [Q][KP], meta [Q] = {s, qq, e, r}.
+constexpr int PJ_WARPS = 8;
+__global__ void __launch_bounds__(PJ_WARPS * 32) project_queries_kernel(const float* __restrict__ queries, int64_t Q,
+                                                                       int m, int k, int KP,
+                                                                       const double* __restrict__ P,
+                                                                       const double* __restrict__ mu,
+                                                                       int8_t* __restrict__ qc,
+                                                                       float4* __restrict__ qm) {
+    __shared__ double y[64];
+    __shared__ double part[PJ_WARPS];
+    const int64_t q = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const float* x = queries + q * m;
-    double y[64];
-#pragma unroll
-    for (int j = 0; j < 64; ++j) y[j] = 0.0;
-    for (int j = 0; j < k; ++j) {
+    for (int j = warp; j < k; j += PJ_WARPS) {
         double acc = 0.0;
         for (int i = lane; i < m; i += 32) acc = __fma_rn(P[(int64_t)j * m + i], (double)x[i] - mu[i], acc);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        y[j < 64 ? j : 63] = acc;
+        if (lane == 0) y[j] = acc;
     }
-    double rr = 0.0;
-    for (int i = lane; i < m; i += 32) {
-        double v = (double)x[i] - mu[i];
-        for (int j = 0; j < k; ++j) v -= P[(int64_t)j * m + i] * y[j];
-        rr = __fma_rn(v, v, rr);
+    double xx = 0.0;
+    for (int i = threadIdx.x; i < m; i += PJ_WARPS * 32) {
+        const double v = (double)x[i] - mu[i];
+        xx = __fma_rn(v, v, xx);
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) rr += __shfl_xor_sync(0xffffffffu, rr, o);
+    for (int o = 16; o > 0; o >>= 1) xx += __shfl_xor_sync(0xffffffffu, xx, o);
+    if (lane == 0) part[warp] = xx;
+    __syncthreads();
+    if (warp != 0) return;
+    xx = lane < PJ_WARPS ? part[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) xx += __shfl_xor_sync(0xffffffffu, xx, o);
+    double yy = 0.0;
     float mx = 0.f;
-    for (int j = 0; j < k; ++j) mx = fmaxf(mx, (float)fabs(y[j]));
+    for (int j = lane; j < k; j += 32) {
+        yy = __fma_rn(y[j], y[j], yy);
+        mx = fmaxf(mx, (float)fabs(y[j]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        yy += __shfl_xor_sync(0xffffffffu, yy, o);
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
     const float s = mx > 0.f ? mx / 127.f : 1.f;
     double err = 0.0;
     int qq = 0;
-    for (int j = 0; j < KP; ++j) {
+    for (int j = lane; j < KP; j += 32) {
         int c = 0;
         if (j < k) {
             c = (int)fmin(fmax(rint(y[j] / (double)s), -127.0), 127.0);
             const double e = (double)s * c - y[j];
             err = __fma_rn(e, e, err);
         }
-        if (lane == 0) qc[q * KP + j] = (int8_t)c;
+        qc[q * KP + j] = (int8_t)c;
         qq += c * c;
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        qq += __shfl_xor_sync(0xffffffffu, qq, o);
+        err += __shfl_xor_sync(0xffffffffu, err, o);
+    }
     if (lane == 0)
-        qm[q] = make_float4(s, (float)qq, __double2float_ru(sqrt(err) * (1.0 + 1e-9) + 1e-30), (float)sqrt(rr));
+        qm[q] = make_float4(s, (float)qq, __double2float_ru(sqrt(err) * (1.0 + 1e-9) + 1e-30),
+                            (float)sqrt(fmax(xx - yy, 0.0)));
 }
 
 
@@ -105,20 +130,27 @@ __device__ __forceinline__ void pq_exact_rows(const float* __restrict__ X0, cons
         double acc[RF];
 #pragma unroll
         for (int u = 0; u < RF; ++u) acc[u] = 0.0;
-        for (int c = lane * 4; c < m; c += 128) {
-            const float4 qv = __ldg(reinterpret_cast<const float4*>(qrow + c));
-            float4 xv[RF];
+        for (int c0 = lane * 4; c0 < m; c0 += 256) {      // two 512-byte column blocks in flight
+            float4 qv[2], xv[2][RF];
 #pragma unroll
-            for (int u = 0; u < RF; ++u)
-                xv[u] = b + u < ns ? __ldg(reinterpret_cast<const float4*>(X0 + (int64_t)rl[b + u] * m + c))
+            for (int h = 0; h < 2; ++h) {
+                const int c = c0 + h * 128;
+                qv[h] = c < m ? __ldg(reinterpret_cast<const float4*>(qrow + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int u = 0; u < RF; ++u)
+                    xv[h][u] = (b + u < ns && c < m)
+                                   ? __ldg(reinterpret_cast<const float4*>(X0 + (int64_t)rl[b + u] * m + c))
                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-            for (int u = 0; u < RF; ++u) {
-                const double d0 = (double)xv[u].x - (double)qv.x, d1 = (double)xv[u].y - (double)qv.y;
-                const double d2 = (double)xv[u].z - (double)qv.z, d3 = (double)xv[u].w - (double)qv.w;
-                acc[u] = __fma_rn(d0, d0, acc[u]); acc[u] = __fma_rn(d1, d1, acc[u]);
-                acc[u] = __fma_rn(d2, d2, acc[u]); acc[u] = __fma_rn(d3, d3, acc[u]);
             }
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int u = 0; u < RF; ++u) {
+                    const double d0 = (double)xv[h][u].x - (double)qv[h].x, d1 = (double)xv[h][u].y - (double)qv[h].y;
+                    const double d2 = (double)xv[h][u].z - (double)qv[h].z, d3 = (double)xv[h][u].w - (double)qv[h].w;
+                    acc[u] = __fma_rn(d0, d0, acc[u]); acc[u] = __fma_rn(d1, d1, acc[u]);
+                    acc[u] = __fma_rn(d2, d2, acc[u]); acc[u] = __fma_rn(d3, d3, acc[u]);
+                }
         }
 #pragma unroll
         for (int u = 0; u < RF; ++u) {
@@ -397,21 +429,29 @@ __global__ void __launch_bounds__(256) pq_q8_bound_kernel(RoundState s, lf_index
             mr[u] = v ? __ldcs(reinterpret_cast<const float4*>(idx.d_qmeta) + row[u]) : make_float4(0.f, 0.f, 0.f, 0.f);
             qmv[u] = v ? __ldg(ov.qm8 + qq[u]) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        for (int c = sl * 16; c < M8; c += 128) {
-            int4 w[R], qv[R];
+        // both 128-byte halves of a 256-byte row in flight together (longer rows loop)
+        for (int c0 = sl * 16; c0 < M8; c0 += 256) {
+            int4 w[R][2], qv[R][2];
 #pragma unroll
-            for (int u = 0; u < R; ++u) {
-                const bool v = e[u].x >= 0;
-                w[u] = v ? __ldcs(reinterpret_cast<const int4*>(idx.d_X8 + row[u] * M8 + c)) : make_int4(0, 0, 0, 0);
-                qv[u] = v ? __ldg(reinterpret_cast<const int4*>(ov.qc8 + qq[u] * ov.mp + c)) : make_int4(0, 0, 0, 0);
-            }
+            for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int u = 0; u < R; ++u) {
-                dot[u] = __dp4a(w[u].x, qv[u].x, dot[u]);
-                dot[u] = __dp4a(w[u].y, qv[u].y, dot[u]);
-                dot[u] = __dp4a(w[u].z, qv[u].z, dot[u]);
-                dot[u] = __dp4a(w[u].w, qv[u].w, dot[u]);
-            }
+                for (int u = 0; u < R; ++u) {
+                    const int c = c0 + h * 128;
+                    const bool v = e[u].x >= 0 && c < M8;
+                    w[u][h] = v ? __ldcs(reinterpret_cast<const int4*>(idx.d_X8 + row[u] * M8 + c))
+                                : make_int4(0, 0, 0, 0);
+                    qv[u][h] = v ? __ldg(reinterpret_cast<const int4*>(ov.qc8 + qq[u] * ov.mp + c))
+                                 : make_int4(0, 0, 0, 0);
+                }
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int u = 0; u < R; ++u) {
+                    dot[u] = __dp4a(w[u][h].x, qv[u][h].x, dot[u]);
+                    dot[u] = __dp4a(w[u][h].y, qv[u][h].y, dot[u]);
+                    dot[u] = __dp4a(w[u][h].z, qv[u][h].z, dot[u]);
+                    dot[u] = __dp4a(w[u][h].w, qv[u][h].w, dot[u]);
+                }
         }
 #pragma unroll
         for (int u = 0; u < R; ++u) {
@@ -508,8 +548,8 @@ __global__ void __launch_bounds__(PQT_WARPS * 32) pq_tail_kernel(RoundState s, l
 
 cudaError_t launch_project_queries(const float* q, int64_t Q, const lf_index& idx, int8_t* qc, float4* qm,
                                    cudaStream_t st) {
-    project_queries_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(q, Q, idx.m, idx.pca_k, idx.pca_k,
-                                                                             idx.d_P, idx.d_mu, qc, qm);
+    project_queries_kernel<<<(unsigned)Q, PJ_WARPS * 32, 0, st>>>(q, Q, idx.m, idx.pca_k, idx.pca_k, idx.d_P,
+                                                                  idx.d_mu, qc, qm);
     return cudaGetLastError();
 }
 
