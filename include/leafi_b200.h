@@ -80,8 +80,9 @@ typedef struct lf_search_opts {
     int32_t n_filters;
     int32_t sequential;          /* 1: one scanned leaf per query per round (exact
                                     reference semantics, every counter identical);
-                                    0: doubling rounds 1,2,4,..,max_round_leaves */
-    int32_t max_round_leaves;    /* cap of the doubling schedule (>= 1) */
+                                    0: growing rounds 1,4,16,..,max_round_leaves leaves per
+                                       query (x4 per round; LF_ROUND_GROWTH_LOG2 overrides) */
+    int32_t max_round_leaves;    /* cap of the round schedule (>= 1; the Python API uses 256) */
     int32_t want_trace;          /* fill the trace buffers below */
     int32_t early_abandon;       /* 1: abandon a row once its partial distance exceeds the
                                     threshold (HBM bytes saved; results identical; off when

@@ -504,6 +504,16 @@ static bool prefix_orders() {
 // Scan variant: LF_SCAN_VARIANT unset / pq (default: the full-length int8 shadow in
 // round 0, then the projected shadow -- 48 instead of 272 bytes per row -- wherever the
 // index carries one) | q8 (int8 shadow only) | ea2 | ea3 | full.
+// Leaves per query per round grow as 2^(round * g): LF_ROUND_GROWTH_LOG2 = g (default 2:
+// 1, 4, 16, ... up to max_round_leaves).  Measured on the bench workload (1K queries,
+// tools/growth_probe.py): x2 / cap 64 -> 9 rounds, 3.47 ms; x4 / cap 256 -> 5 rounds,
+// 3.12 ms, 2% more series scanned -- fewer rounds of fixed per-round latency.
+static int round_growth_log2() {
+    const char* e = getenv("LF_ROUND_GROWTH_LOG2");
+    const int g = e ? atoi(e) : 2;
+    return g >= 1 && g <= 6 ? g : 2;
+}
+
 static int scan_variant() {
     const char* e = getenv("LF_SCAN_VARIANT");
     if (!e || e[0] == 0 || strcmp(e, "pq") == 0) return 8;   // projected stage when the shadow exists
@@ -827,7 +837,8 @@ static int session_enqueue(lf_session* ss, const double* d_bound, double* d_bsf_
     s.n_predict = counts + 2;
     cudaEvent_t* ev = ss->rev[slot];
     s.bound = d_bound;
-    s.R = o.sequential ? 1 : (int)std::min<int64_t>(s.Rcap, (int64_t)1 << std::min(ss->round, 30));
+    s.R = o.sequential ? 1
+                       : (int)std::min<int64_t>(s.Rcap, (int64_t)1 << std::min(ss->round * round_growth_log2(), 30));
     LF_CUDA(cudaMemsetAsync(counts, 0, sizeof(int) * 3, st));
     if (ss->prof) cudaEventRecord(ev[0], st);
     plan_warp_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s, idx);

@@ -13,7 +13,7 @@ Two schedules:
 * ``sequential=True``: one scanned leaf per query per round.  Bit-for-bit the
   reference traversal (same results, counters and trace); used by the
   single-query seam.
-* ``sequential=False`` (batch default): rounds of 1, 2, 4, ... leaves per
+* ``sequential=False`` (batch default): rounds of 1, 4, 16, ... leaves per
   query.  Same exact-mode answers; the best-so-far is refreshed
   between rounds only, so a query may scan a few extra leaves (F3).
 """
@@ -151,7 +151,7 @@ def _queries_device(queries, m: int, dev):
 
 def search_batch(index, queries, k: int = 1, *, bsf_factor: float = 1.0, predictions=None,
                  offsets=None, leaf_filter=None, sequential: bool = False,
-                 max_round_leaves: int = 64, want_trace: bool = False, stream=None,
+                 max_round_leaves: int = 256, want_trace: bool = False, stream=None,
                  copy_out: bool = True, profile: np.ndarray | None = None, early_abandon: bool = True,
                  filters=None):
     """Search a batch of queries in one lf_search call.

@@ -224,7 +224,7 @@ def _as_enhanced(eidx) -> EnhancedIndex:
 
 
 def search_queries(eidx, queries, k: int = 1, *, target: float | None = None, exact: bool = False,
-                   sequential: bool = False, max_round_leaves: int = 64, want_trace: bool = False,
+                   sequential: bool = False, max_round_leaves: int = 256, want_trace: bool = False,
                    stream=None, copy_out: bool = True, profile=None, lazy: bool = False):
     """Batched LeaFi search in one lf_search call.  lazy=False (default): one
     lf_filter_predict over every (query, filter) pair first; lazy=True (tensor-core

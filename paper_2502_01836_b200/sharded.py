@@ -31,7 +31,7 @@ class GpuRoundEngine:
     """lf_search session over one device (leaf shard) index."""
 
     def __init__(self, dindex, queries, k: int, *, predictions=None, offsets=None, leaf_filter=None,
-                 bsf_factor: float = 1.0, max_round_leaves: int = 64, early_abandon: bool = True,
+                 bsf_factor: float = 1.0, max_round_leaves: int = 256, early_abandon: bool = True,
                  stream=None, profile=None, filters=None):
         import torch
 
@@ -158,7 +158,7 @@ class ShardedResult:
 
 
 def search_sharded(tree, queries, k: int = 1, *, rank: int, world: int, pack=None, offsets=None,
-                   bsf_factor: float = 1.0, max_round_leaves: int = 64, group=None, copy_out: bool = True,
+                   bsf_factor: float = 1.0, max_round_leaves: int = 256, group=None, copy_out: bool = True,
                    profile=None, lazy: bool = False):
     """Leaf-sharded batched search on this rank's GPU (call on every rank).
 

@@ -14,11 +14,11 @@ ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start o
     --log-file $OUT/launches.csv $B > $OUT/ncu_launches_bench.json 2> $OUT/ncu_launches.log
 echo "launch list rc=$?"
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
-    --profile-from-start off -k regex:"${SCAN_REGEX:-scan_q8_kernel|scan_pq_kernel|pq_over_exact_kernel|pq_select_kernel}" --csv --log-file $OUT/scan_dram.csv \
+    --profile-from-start off -k regex:"${SCAN_REGEX:-scan_q8_kernel|scan_pq_kernel|pq_q8_bound_kernel|pq_tail_kernel}" --csv --log-file $OUT/scan_dram.csv \
     $B > $OUT/ncu_dram_bench.json 2> $OUT/ncu_dram.log
 echo "scan dram rc=$?"
 ncu --set full --clock-control none --import-source on --profile-from-start off \
-    -k regex:"${KREGEX:-scan_q8_kernel|scan_pq_kernel|pq_over_exact_kernel|filter_tc_kernel|bounds_sort_kernel|plan_warp_kernel}" \
+    -k regex:"${KREGEX:-scan_q8_kernel|scan_pq_kernel|pq_q8_bound_kernel|pq_tail_kernel|filter_tc_kernel|bounds_sort_kernel|plan_warp_kernel}" \
     --launch-skip ${KSKIP:-0} -c ${KCOUNT:-8} -o $OUT/prof_full $B > $OUT/ncu_full.log 2>&1
 echo "full set rc=$?"
 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:mindist_q8 -c 1 \
