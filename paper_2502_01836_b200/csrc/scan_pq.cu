@@ -400,7 +400,10 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
 // lo is kept per entry; for k = 1 the task threshold is min'ed with every entry's
 // upper bound -- the task's best row survives both stages, so no row whose lower
 // bound exceeds it can be the nearest.
-__global__ void __launch_bounds__(256) pq_q8_bound_kernel(RoundState s, lf_index idx, PQOverflow ov) {
+#ifndef LF_PQB_MINB
+#define LF_PQB_MINB 3                           // resident CTAs per SM the register budget targets (sweep: 2 / 3 / 4 / 6 -> scan 1.55 / 1.46 / 1.48 / 1.60 ms)
+#endif
+__global__ void __launch_bounds__(256, LF_PQB_MINB) pq_q8_bound_kernel(RoundState s, lf_index idx, PQOverflow ov) {
     constexpr int R = 2;
     const int lane = threadIdx.x & 31, sl = lane & 7, grp = lane >> 3;
     const long long n = min((long long)*ov.n, (long long)ov.cap);

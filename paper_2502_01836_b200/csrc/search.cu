@@ -236,11 +236,12 @@ __global__ void expand_tasks_kernel(RoundState s, const int64_t* __restrict__ le
     const int ns = s.n_sel[q];
     const long long base = s.chunk_off[q];
     const int* pre = s.sel_pre + q * (s.Rcap + 1);
-    for (int j = 0; j < ns; ++j) {
+    // lane per selected leaf (up to 32 leaves' loads in flight), its chunks in order
+    for (int j = lane; j < ns; j += 32) {
         const int leaf = s.sel_leaf[q * s.Rcap + j];
         const int c0 = pre[j], n = pre[j + 1] - c0;
         const long long lb = leaf_ptr[leaf], le = leaf_ptr[leaf + 1];
-        for (int c = lane; c < n; c += 32) {
+        for (int c = 0; c < n; ++c) {
             s.tasks[base + c0 + c] = make_int4((int)q, leaf, c, j);
             if (s.task_rows != nullptr) {   // row range of the task, so a producer needs no dependent loads
                 const long long r0 = lb + (long long)c * CH;
