@@ -28,14 +28,25 @@ namespace lf {
 // has read it, so PQW_NS - 1 pieces per warp are always in flight.  Lane i owns rows
 // i, i + 32, ... of a piece; lo / hi live in registers, min hi is a warp reduction
 // and survivors are compacted by ballot.
-constexpr int PQW_STG = 64;                   // rows per ring slot
-constexpr int PQW_NS = 4;                     // ring slots per warp
+// ring geometry (tools/pq_sweep.sh: 64 rows x 4 slots x 16 warps, 64 x 3 x 20 and a
+// next-task prefetch all within 1%; 32-row slots are slower)
+#ifndef LF_PQW_STG
+#define LF_PQW_STG 64
+#endif
+#ifndef LF_PQW_NS
+#define LF_PQW_NS 4
+#endif
+#ifndef LF_PQW_WARPS32
+#define LF_PQW_WARPS32 16
+#endif
+constexpr int PQW_STG = LF_PQW_STG;           // rows per ring slot
+constexpr int PQW_NS = LF_PQW_NS;             // ring slots per warp
 constexpr int PQ_PIECES = CH / PQW_STG;       // slots per task (max)
 constexpr int PQ_SLOTS = CH / 32;             // rows per lane per task
 
 template <int KP>
 struct PQW {
-    static constexpr int WARPS = KP == 32 ? 16 : 8;
+    static constexpr int WARPS = KP == 32 ? LF_PQW_WARPS32 : 8;
     static constexpr int CODE = PQW_STG * KP;
     static constexpr int STAGE = CODE + PQW_STG * 16;
     static constexpr int RING = WARPS * PQW_NS * STAGE;
@@ -261,15 +272,15 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
     unsigned long long c_rows = 0, c_surv = 0, c_fall = 0;
     for (long long t = gw; t < total; t += nw) {
         const int4 tr = s.task_rows[t];
+        const double bsf = round_bsf(s, tr.w);
+        int4 qw[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) qw[v] = __ldg(reinterpret_cast<const int4*>(qcodes + (int64_t)tr.w * KP) + v);
+        const float4 qmv = __ldg(qmeta + tr.w);
         const int64_t r0 = (int64_t)(unsigned)tr.x | ((int64_t)tr.y << 32);
         const int nrows = tr.z;
         const int64_t q = tr.w;
         const int pieces = nrows > 0 ? (nrows + PQW_STG - 1) / PQW_STG : 1;
-        const double bsf = round_bsf(s, q);
-        int4 qw[V];
-#pragma unroll
-        for (int v = 0; v < V; ++v) qw[v] = __ldg(reinterpret_cast<const int4*>(qcodes + q * KP) + v);
-        const float4 qmv = __ldg(qmeta + q);
         const float sq = qmv.x, eq = qmv.z, rq = qmv.w;
         const float sq2qq = sq * sq * qmv.y;
         const float sq2 = 2.f * sq;
@@ -401,7 +412,9 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
 // upper bound -- the task's best row survives both stages, so no row whose lower
 // bound exceeds it can be the nearest.
 #ifndef LF_PQB_MINB
-#define LF_PQB_MINB 3                           // resident CTAs per SM the register budget targets (sweep: 2 / 3 / 4 / 6 -> scan 1.55 / 1.46 / 1.48 / 1.60 ms)
+// resident CTAs per SM the register budget targets (bench sweep 2 / 3 / 4 / 6: scan phase
+// 1.55 / 1.46 / 1.48 / 1.60 ms per batch)
+#define LF_PQB_MINB 3
 #endif
 __global__ void __launch_bounds__(256, LF_PQB_MINB) pq_q8_bound_kernel(RoundState s, lf_index idx, PQOverflow ov) {
     constexpr int R = 2;
