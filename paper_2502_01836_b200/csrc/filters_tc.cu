@@ -314,9 +314,9 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
                     const float wv[4] = {ww.x, ww.y, ww.z, ww.w};
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        const float a = F16 ? __fmul_rn(__uint_as_float(r[j4 * 4 + u]), sc)
-                                            : __uint_as_float(r[j4 * 4 + u]);
-                        const float h = fmaxf(__fadd_rn(a, bv[u]), 0.f);
+                        // F16: acc * 2^e is exact, so one FFMA rounds exactly like FMUL + FADD
+                        const float h = F16 ? fmaxf(__fmaf_rn(__uint_as_float(r[j4 * 4 + u]), sc, bv[u]), 0.f)
+                                            : fmaxf(__fadd_rn(__uint_as_float(r[j4 * 4 + u]), bv[u]), 0.f);
                         part = __fmaf_rn(h, wv[u], part);
                     }
                 }
