@@ -549,6 +549,7 @@ struct lf_session {
     bool grouped = false;            // q8 scan with the round's tasks grouped by (leaf, chunk)
     bool pq = false;                 // two-stage scan over the projected shadow (d_Xp)
     lf::Scratch qcp, qmp, pq_cnt, pq_trows, pq_oent, pq_on, pq_obase, pq_wrows, pq_wdist, pq_lo8, pq_thr;
+    int pq_cap = lf::PQ_OVER_CAP;    // survivor entry capacity (LF_PQ_OVER_CAP: tests of the full-list path)
     lf::Scratch cbase, ghist, gcur, gsorted, glist, gcount, gbsum, ginfo;
     int n_keys = 0;
     long long refills = 0;           // queries whose visit order was completed after the prefix
@@ -711,12 +712,13 @@ static int session_begin(lf_session* ss) {
         LF_CUDA(ss->pq_cnt.alloc(sizeof(int) * max_tasks, st));
         LF_CUDA(ss->pq_trows.alloc(sizeof(int4) * max_tasks, st));
         s.task_rows = ss->pq_trows.as<int4>();
-        LF_CUDA(ss->pq_oent.alloc(sizeof(int4) * PQ_OVER_CAP, st));
+        if (const char* e = getenv("LF_PQ_OVER_CAP")) ss->pq_cap = std::max(1, std::min(PQ_OVER_CAP, atoi(e)));
+        LF_CUDA(ss->pq_oent.alloc(sizeof(int4) * ss->pq_cap, st));
         LF_CUDA(ss->pq_on.alloc(sizeof(int), st));
         LF_CUDA(ss->pq_obase.alloc(sizeof(int) * max_tasks, st));
         LF_CUDA(ss->pq_wrows.alloc(sizeof(unsigned short) * CH * pq_scan_warps(), st));
         LF_CUDA(ss->pq_wdist.alloc(sizeof(double) * CH * pq_scan_warps(), st));
-        LF_CUDA(ss->pq_lo8.alloc(sizeof(float) * PQ_OVER_CAP, st));
+        LF_CUDA(ss->pq_lo8.alloc(sizeof(float) * ss->pq_cap, st));
         LF_CUDA(ss->pq_thr.alloc(sizeof(unsigned) * max_tasks, st));
         LF_CUDA(launch_project_queries(ss->d_q, Q, idx, ss->qcp.as<int8_t>(), ss->qmp.as<float4>(), st));
         ++ss->kernels;
@@ -857,7 +859,7 @@ static int session_enqueue(lf_session* ss, const double* d_bound, double* d_bsf_
         // round 0 has no best-so-far yet: the projected bound's loose upper end would let
         // most rows through, so the first round runs the full-length int8 scan
         const PQOverflow ov{ss->pq_oent.as<int4>(), ss->pq_on.as<int>(),
-                            ss->pq_obase.as<int>(), PQ_OVER_CAP, ss->pq_wrows.as<unsigned short>(),
+                            ss->pq_obase.as<int>(), ss->pq_cap, ss->pq_wrows.as<unsigned short>(),
                             ss->pq_wdist.as<double>(), ss->q8 ? ss->qc8.as<int8_t>() : nullptr,
                             ss->q8 ? ss->qm8.as<float4>() : nullptr, (idx.m + 255) / 256 * 256,
                             ss->pq_lo8.as<float>(), ss->pq_thr.as<unsigned>()};

@@ -548,9 +548,10 @@ def test_grouped_scan_identical(k, monkeypatch):
     np.testing.assert_array_equal(got.stats, ref.stats)
 
 
-@pytest.mark.parametrize("m,pk", [(64, 32), (96, 32), (256, 32), (256, 64), (320, 64)])
+@pytest.mark.parametrize("m,pk,cap", [(64, 32, None), (96, 32, None), (256, 32, None), (256, 64, None),
+                                      (320, 64, None), (256, 32, "40")])
 @pytest.mark.parametrize("k", [1, 3])
-def test_projected_scan_exact(m, pk, k, monkeypatch):
+def test_projected_scan_exact(m, pk, cap, k, monkeypatch):
     """Two-stage scan over the projected shadow (int8 codes of the top principal
     coordinates + residual norms) == the full fp64 scan: ids, distances, counters;
     with duplicate rows, an all-zero row and queries equal to rows."""
@@ -569,6 +570,8 @@ def test_projected_scan_exact(m, pk, k, monkeypatch):
     monkeypatch.setenv("LF_SCAN_VARIANT", "full")
     ref = search_batch(t, Q, k)
     monkeypatch.setenv("LF_SCAN_VARIANT", "pq")
+    if cap is not None:      # a tiny survivor entry list: tasks that do not fit re-read in the scan warp
+        monkeypatch.setenv("LF_PQ_OVER_CAP", cap)
     prof = np.zeros(16)
     got = search_batch(t, Q, k, profile=prof)
     np.testing.assert_array_equal(got.ids, ref.ids)
