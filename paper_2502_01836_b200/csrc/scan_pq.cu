@@ -1,4 +1,5 @@
-// K4 variant (LF_SCAN_VARIANT=pq): the projected two-stage scan.
+// K4b-d (default from round 1 on; LF_SCAN_VARIANT=q8 disables): the projected scan
+// cascade.
 #include <algorithm>
 #include <climits>
 
@@ -9,17 +10,19 @@
 namespace lf {
 
 // ----------------------------------------------------------- projected scan ----
-// Two-stage bounded scan over a PROJECTED int8 shadow (lf_index.d_Xp): per row the
-// int8 codes of y = P (x - mu) for an orthonormal basis P of pca_k directions (the
-// collection's leading principal directions) plus {scale, sum code^2, code error e,
+// Bounded scan over a PROJECTED int8 shadow (lf_index.d_Xp): per row the int8 codes
+// of y = P (x - mu) for an orthonormal basis P of pca_k directions (the collection's
+// leading principal directions) plus {scale, ||scale * code||^2, code error e,
 // residual norm r = ||(x - mu) - P^T y||}.  Because P has orthonormal rows,
 //     ||x - q||^2 = ||y - y_q||^2 + ||r_vec - r_vec_q||^2,
 // the int8 codes give ||y - y_q|| within e + e_q (triangle inequality, fp32
 // rounding covered by tol) and | r - r_q | <= ||r_vec - r_vec_q|| <= r + r_q, so
 //     lo = sqrt(A_lo^2 + (r - r_q)^2),  hi = sqrt(A_hi^2 + (r + r_q)^2).
-// A row costs pca_k + 16 bytes instead of m + 16 (random walks keep ~98% of their
-// energy in 32 directions); rows whose lo reaches min(bsf, min hi) are re-read
-// whole and summed EXACTLY in fp64, so results equal the full scan.
+// A row costs pca_k + 16 bytes instead of m + 16 (random walks keep ~97% of their
+// energy in 32 directions).  Rows whose lo reaches min(bsf, min hi) -- 2% on the
+// bench workload -- get the full-length int8 interval (pq_q8_bound_kernel), and the
+// ones that survive that are re-read whole and summed EXACTLY in fp64
+// (pq_tail_kernel), so results equal the full scan.
 // One WARP per task (no CTA barriers): at pca_k + 16 = 48 bytes a 512-row chunk is
 // only 24 KB, so the per-task barriers of the CTA-pipelined q8 scan would dominate.
 // Each warp streams its own tasks through a private ring of PQW_NS shared-memory
@@ -355,7 +358,7 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
             if (lane == 0) surv_cnt[t] = 0;
             continue;
         }
-        // survivors -> (task, row) entries for the row-parallel re-read (pq_over_exact_kernel)
+        // survivors -> (task, query, row) entries for the int8 stage (pq_q8_bound_kernel)
         int base = 0;
         if (lane == 0) base = atomicAdd(ov.n, ns);
         base = __shfl_sync(0xffffffffu, base, 0);
