@@ -496,7 +496,9 @@ def run_ours(args, rank, world, device):
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "f64-accumulated f32 series (scan/bounds), f32 filters",
+        "dtype": "f64-accumulated f32 series (scan/bounds), " + (
+            "filters on fp16 operands (power-of-two scaled, tf32 mantissa) with f32 accumulation"
+            if eidx.pack.path == "tc16" else "tf32 filters" if eidx.pack.path == "tc" else "f32 filters"),
         "data": "synthetic random walk generated on device (reference law, Philox stream), 25.6 GB >> L2: no flush needed",
         "config": {
             "workload": f"{'iSAX' if args.index == 'isax' else 'DSTree'}+LeaFi {args.n}x{args.m} "
