@@ -302,22 +302,29 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
                 sc = scalbnf(1.f, ex + fa.wexp[f]);
             }
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * 256);
-            for (int c0 = c_begin; c0 < c_end; c0 += 32) {
-                uint32_t r[32];
-                LF_TMEM_LD32(taddr + (uint32_t)c0, r);
+            for (int c0 = c_begin; c0 < c_end; c0 += 64) {     // two 32-column loads per wait
+                uint32_t r[2][32];
+                const bool two = c0 + 32 < c_end;                 // warp-uniform
+                LF_TMEM_LD32(taddr + (uint32_t)c0, r[0]);
+                if (two) LF_TMEM_LD32(taddr + (uint32_t)(c0 + 32), r[1]);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                for (int j4 = 0; j4 < 8; ++j4) {
-                    const float4 bb = b1s[(c0 >> 2) + j4];
-                    const float4 ww = w2s[(c0 >> 2) + j4];
-                    const float bv[4] = {bb.x, bb.y, bb.z, bb.w};
-                    const float wv[4] = {ww.x, ww.y, ww.z, ww.w};
+                for (int hh = 0; hh < 2; ++hh) {
+                    if (hh == 1 && !two) break;
+                    const int cb = c0 + hh * 32;
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        // F16: acc * 2^e is exact, so one FFMA rounds exactly like FMUL + FADD
-                        const float h = F16 ? fmaxf(__fmaf_rn(__uint_as_float(r[j4 * 4 + u]), sc, bv[u]), 0.f)
-                                            : fmaxf(__fadd_rn(__uint_as_float(r[j4 * 4 + u]), bv[u]), 0.f);
-                        part = __fmaf_rn(h, wv[u], part);
+                    for (int j4 = 0; j4 < 8; ++j4) {
+                        const float4 bb = b1s[(cb >> 2) + j4];
+                        const float4 ww = w2s[(cb >> 2) + j4];
+                        const float bv[4] = {bb.x, bb.y, bb.z, bb.w};
+                        const float wv[4] = {ww.x, ww.y, ww.z, ww.w};
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            // F16: acc * 2^e is exact, so one FFMA rounds exactly like FMUL + FADD
+                            const float a = __uint_as_float(r[hh][j4 * 4 + u]);
+                            const float h = F16 ? fmaxf(__fmaf_rn(a, sc, bv[u]), 0.f) : fmaxf(__fadd_rn(a, bv[u]), 0.f);
+                            part = __fmaf_rn(h, wv[u], part);
+                        }
                     }
                 }
             }
