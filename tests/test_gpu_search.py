@@ -578,3 +578,25 @@ def test_projected_scan_exact(m, pk, cap, k, monkeypatch):
     np.testing.assert_allclose(got.dists, ref.dists, rtol=1e-14)
     np.testing.assert_array_equal(got.stats, ref.stats)
     assert prof[8] > 0 and prof[9] < prof[8], "the projected bound must run and drop rows"
+
+
+def test_projected_shadow_energy_gate(monkeypatch):
+    """The index build keeps the projected shadow only when 32 principal directions
+    hold >= 90% of the energy: yes for random walks, no for a 96-d Gaussian mixture
+    (whose searches then run the int8 scan in every round, with the same results)."""
+    from paper_2502_01836_b200 import build_index, search_batch
+    from paper_2502_01836_b200.synth import gaussian_mixture
+
+    monkeypatch.delenv("LF_SCAN_VARIANT", raising=False)
+    rw = build_index(lo.randwalk(6000, 128, 5), 400).device()
+    assert rw.pca_k == 32 and rw.pca_energy >= 0.9
+    g = gaussian_mixture(6000, 96, 9, n_centers=200).astype(np.float32)
+    t = build_index(g, 400)
+    di = t.device()
+    assert di.pca_k == 0 and di.pca_energy < 0.9
+    Q = g[[3, 77, 4000]].astype(np.float64) + 0.01
+    got = search_batch(t, Q, 2)
+    monkeypatch.setenv("LF_SCAN_VARIANT", "full")
+    ref = search_batch(t, Q, 2)
+    np.testing.assert_array_equal(got.ids, ref.ids)
+    np.testing.assert_allclose(got.dists, ref.dists, rtol=1e-14)
