@@ -1,7 +1,10 @@
 // Error state and device queries for the C-ABI (include/leafi_b200.h).
 #include <cuda_runtime.h>
 
+#include <mutex>
+#include <set>
 #include <string>
+#include <tuple>
 
 #include "common.cuh"
 
@@ -35,6 +38,24 @@ int sm_count() {
     cached_dev = dev;
     cached = n;
     return n;
+}
+
+cudaError_t smem_optin_impl(const void* fn, int bytes) {
+    static std::mutex mu;
+    static std::set<std::tuple<const void*, int, int>> done;   // (kernel, device, bytes)
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const auto key = std::make_tuple(fn, dev, bytes);
+    {
+        std::lock_guard<std::mutex> g(mu);
+        if (done.count(key)) return cudaSuccess;
+    }
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(mu);
+    done.insert(key);
+    return cudaSuccess;
 }
 
 }  // namespace lf

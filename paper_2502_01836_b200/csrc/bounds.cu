@@ -456,11 +456,7 @@ template <int ITEMS, int RB = 4>
 static int launch_fused(const double* d_qsumm, int64_t Q, const lf_index& idx, int n, const OrderArgs& oa,
                         cudaStream_t st) {
     const int bytes = (int)sizeof(FsSmem<ITEMS, RB>);
-    static bool attr = false;
-    if (!attr) {
-        LF_CUDA(cudaFuncSetAttribute(bounds_sort_kernel<ITEMS, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-        attr = true;
-    }
+    LF_CUDA(smem_optin(bounds_sort_kernel<ITEMS, RB>, bytes));
     bounds_sort_kernel<ITEMS, RB><<<(unsigned)Q, FS_THREADS, bytes, st>>>(d_qsumm, idx, n, oa);
     LF_CUDA(cudaGetLastError());
     return LF_OK;

@@ -28,6 +28,13 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 int sm_count();
 
+// Opt a kernel into more than 48 KB of dynamic shared memory.  The attribute
+// belongs to the device context, so it is set once per (kernel, device, size),
+// not once per process: one process driving several GPUs sets it on each.
+cudaError_t smem_optin_impl(const void* fn, int bytes);
+template <class F>
+inline cudaError_t smem_optin(F* fn, int bytes) { return smem_optin_impl(reinterpret_cast<const void*>(fn), bytes); }
+
 // Keep the stream-ordered allocator's pool warm across calls: by default the
 // pool trims to zero at every synchronisation, which turns each search call's
 // scratch into fresh cudaMalloc/cudaFree (and implicit syncs).

@@ -408,12 +408,7 @@ extern "C" int lf_filter_predict_tc(const float* d_queries, int64_t Q, int32_t m
     rc = tc::make_map(&mw, d_W1T, (int64_t)F * m, m, m);
     if (rc) return rc;
     const int n_mb = (int)((Q + tc::BM - 1) / tc::BM);
-    static bool attr_set = false;
-    if (!attr_set) {
-        LF_CUDA(cudaFuncSetAttribute(tc::filter_tc_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     tc::SMEM_BYTES));
-        attr_set = true;
-    }
+    LF_CUDA(smem_optin(tc::filter_tc_kernel<false, false>, tc::SMEM_BYTES));
     const int64_t tiles = (int64_t)F * n_mb;
     const int grid = (int)std::min<int64_t>(tiles, sm_count());
     tc::filter_tc_kernel<false, false><<<grid, tc::THREADS, tc::SMEM_BYTES, as_stream(stream)>>>(
@@ -434,12 +429,7 @@ int filter_pairs_tc(const float* d_rows, int64_t P, int m, const float* d_W1T, c
     if (rc) return rc;
     rc = tc::make_map(&mw, d_W1T, (int64_t)F * m, m, m);
     if (rc) return rc;
-    static bool attr_set = false;
-    if (!attr_set) {
-        LF_CUDA(cudaFuncSetAttribute(tc::filter_tc_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     tc::SMEM_BYTES));
-        attr_set = true;
-    }
+    LF_CUDA(smem_optin(tc::filter_tc_kernel<true, false>, tc::SMEM_BYTES));
     tc::PairArgs pa{d_tiles, d_ntiles, d_dst, d_offset, d_adj, Nn};
     tc::filter_tc_kernel<true, false><<<sm_count(), tc::THREADS, tc::SMEM_BYTES, st>>>(mx, mw, P, m, F, d_b1, d_W2,
                                                                                       d_b2, nullptr, pa,
@@ -562,12 +552,7 @@ extern "C" int lf_filter_predict_f16(const float* d_queries, int64_t Q, int32_t 
     rc = tc::make_map(&mw, d_W1T_h, (int64_t)F * m, m, m, true);
     if (rc) return rc;
     const int n_mb = (int)((Q + tc::BM - 1) / tc::BM);
-    static bool attr_set = false;
-    if (!attr_set) {
-        LF_CUDA(cudaFuncSetAttribute(tc::filter_tc_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     tc::SMEM_BYTES));
-        attr_set = true;
-    }
+    LF_CUDA(smem_optin(tc::filter_tc_kernel<false, true>, tc::SMEM_BYTES));
     const int64_t tiles = (int64_t)F * n_mb;
     const int grid = (int)std::min<int64_t>(tiles, sm_count());
     tc::filter_tc_kernel<false, true><<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(

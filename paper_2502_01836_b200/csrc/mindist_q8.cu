@@ -705,11 +705,7 @@ static int run(const float* d_q, int64_t Q, const lf_index& idx, const std::vect
     if (rc) return rc;
     rc = encode_map_2d(&mx, CU_TENSOR_MAP_DATA_TYPE_UINT8, idx.d_X8, idx.n_series, idx.m, idx.m, KBB, BN);
     if (rc) return rc;
-    static bool attr = false;
-    if (!attr) {
-        LF_CUDA(cudaFuncSetAttribute(mindist_q8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-        attr = true;
-    }
+    LF_CUDA(smem_optin(mindist_q8_kernel, SMEM_BYTES));
     const int grid = (int)std::min<size_t>(items.size(), (size_t)sm_count());
     if (idx.d_X8b != nullptr && idx.d_qmeta2 != nullptr) {
         Scratch qc2, qm2;
@@ -725,11 +721,7 @@ static int run(const float* d_q, int64_t Q, const lf_index& idx, const std::vect
             return rc;
         if ((rc = encode_map_2d(&mx2, CU_TENSOR_MAP_DATA_TYPE_UINT8, idx.d_X8b, idx.n_series, idx.m, idx.m, KBB, BN2)))
             return rc;
-        static bool attr2 = false;
-        if (!attr2) {
-            LF_CUDA(cudaFuncSetAttribute(mindist_q82_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES));
-            attr2 = true;
-        }
+        LF_CUDA(smem_optin(mindist_q82_kernel, SMEM2_BYTES));
         mindist_q82_kernel<<<grid, THREADS, SMEM2_BYTES, st>>>(mq1, mq2, mx1, mx2, d_items.as<Item>(),
                                                                (int)items.size(), idx, d_q, qm.as<float4>(),
                                                                qm2.as<float4>(),

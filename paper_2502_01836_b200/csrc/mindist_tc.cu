@@ -407,11 +407,7 @@ static int run(const float* d_q, int64_t Q, const lf_index& idx, const std::vect
     if (rc) return rc;
     rc = make_map(&mx, idx.d_X, idx.n_series, idx.m, BN);
     if (rc) return rc;
-    static bool attr = false;
-    if (!attr) {
-        LF_CUDA(cudaFuncSetAttribute(mindist_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-        attr = true;
-    }
+    LF_CUDA(smem_optin(mindist_tc_kernel, SMEM_BYTES));
     const int grid = (int)std::min<size_t>(items.size(), (size_t)sm_count());
     mindist_tc_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(mq, mx, d_items.as<Item>(), (int)items.size(), idx, d_q,
                                                          qn.as<double>(), xn.as<double>(),

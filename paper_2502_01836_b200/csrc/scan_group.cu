@@ -525,13 +525,7 @@ cudaError_t launch_chunk_base(const lf_index& idx, int* cbase, cudaStream_t st) 
 template <int N>
 static cudaError_t launch_q8g_nch(const RoundState& s, const lf_index& idx, const float* q, const int8_t* qc8,
                                   const float4* qm8, const GroupScratch& g, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(scan_q8g_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             Q8GCfg<N>::SMEM);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (cudaError_t e = smem_optin(scan_q8g_kernel<N>, Q8GCfg<N>::SMEM); e != cudaSuccess) return e;
     scan_q8g_kernel<N><<<sm_count(), G_THREADS, Q8GCfg<N>::SMEM, st>>>(
         s, idx, q, qc8, qm8, g.sorted, static_cast<const GroupInfo*>(g.info), g.count);
     return cudaGetLastError();

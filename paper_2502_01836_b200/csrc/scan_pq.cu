@@ -575,13 +575,7 @@ cudaError_t launch_project_queries(const float* q, int64_t Q, const lf_index& id
 template <int KP>
 static cudaError_t launch_pq_kp(const RoundState& s, const lf_index& idx, const float* q, const int8_t* qc,
                                 const float4* qm, int* surv_cnt, const PQOverflow& ov, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(scan_pq_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             PQW<KP>::SMEM);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (cudaError_t e = smem_optin(scan_pq_kernel<KP>, PQW<KP>::SMEM); e != cudaSuccess) return e;
     scan_pq_kernel<KP><<<sm_count(), PQW<KP>::WARPS * 32, PQW<KP>::SMEM, st>>>(s, idx, q, qc, qm, surv_cnt, ov);
     return cudaGetLastError();
 }

@@ -319,13 +319,7 @@ __global__ void __launch_bounds__(Q8_THREADS, 2) scan_q8_kernel(RoundState s, lf
 template <int NCH>
 static cudaError_t launch_q8_nch(const RoundState& s, const lf_index& idx, const float* q, const int8_t* qc8,
                                  const float4* qm8, cudaStream_t st) {
-    static bool attr = false;       // one instantiation per NCH
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(scan_q8_kernel<NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             Q8Cfg<NCH>::SMEM);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (cudaError_t e = smem_optin(scan_q8_kernel<NCH>, Q8Cfg<NCH>::SMEM); e != cudaSuccess) return e;
     scan_q8_kernel<NCH><<<sm_count() * 2, Q8_THREADS, Q8Cfg<NCH>::SMEM, st>>>(s, idx, q, qc8, qm8);
     return cudaGetLastError();
 }

@@ -12,6 +12,7 @@ ones used to search are bit-identical (enhanced.py:283-285).
 from __future__ import annotations
 
 import os
+import weakref
 
 import numpy as np
 
@@ -48,7 +49,7 @@ class FilterPack:
         self.W2 = t(W2, (F, m))
         self.b2 = t(b2, (F,))
         self.device = dev
-        self._slot_maps = {}
+        self._slot_maps = weakref.WeakKeyDictionary()   # DeviceIndex -> leaf->filter map
         tc_ok = F > 0 and m % 32 == 0 and 32 <= m <= 256
         tc16_ok = tc_ok and m % 64 == 0
         self.path = path or os.environ.get("LF_FILTER_PATH") or ("tc16" if tc16_ok else "tc" if tc_ok else "simt")
@@ -126,7 +127,7 @@ class FilterPack:
     def leaf_filter(self, dindex):
         """int32 [n_leaves]: filter slot of each leaf slot of a DeviceIndex, -1 if none."""
         torch = _lib.require_cuda()
-        key = id(dindex)
+        key = dindex
         if key not in self._slot_maps:
             m = np.full(dindex.n_leaves, -1, dtype=np.int32)
             for s, lid in enumerate(self.leaf_ids):

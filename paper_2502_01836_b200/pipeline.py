@@ -25,6 +25,9 @@ import math
 import time
 from dataclasses import dataclass, field
 
+import warnings
+import weakref
+
 import numpy as np
 
 from . import _lib
@@ -170,7 +173,16 @@ class EnhancedIndex:
 
     @classmethod
     def adopt(cls, ref_eidx) -> "EnhancedIndex":
-        """Wrap a reference enhanced.EnhancedIndex (duck-typed)."""
+        """Wrap a reference enhanced.EnhancedIndex (duck-typed).
+
+        The reference's conformal curves were fitted on its numpy fp32 forward;
+        searches here predict with the tensor-core pack, so the calibration rule
+        "calibrate on the search's own predictor" (enhanced.py:280-283) holds only
+        approximately for an adopted index.  Re-run enhance() on the adopted base
+        index for a guaranteed recall target."""
+        warnings.warn("adopted reference EnhancedIndex: its curves were calibrated on the numpy forward, "
+                      "the GPU search predicts on the tensor-core pack -- the recall target is approximate "
+                      "(re-run pipeline.enhance for a calibrated index)", RuntimeWarning, stacklevel=2)
         filters = {int(l): FilterModel(np.asarray(m.W1), np.asarray(m.b1), np.asarray(m.W2), float(m.b2))
                    for l, m in ref_eidx.filters.items()}
         return cls(ref_eidx.base, filters, dict(ref_eidx.curves), ref_eidx.plan, ref_eidx.budget,
@@ -209,18 +221,20 @@ class EnhancedIndex:
         return got
 
 
-_adopted_eidx = {}
+_adopted_eidx = weakref.WeakKeyDictionary()   # reference EnhancedIndex -> wrapper (dies with it)
 
 
 def _as_enhanced(eidx) -> EnhancedIndex:
     if isinstance(eidx, EnhancedIndex):
         return eidx
-    key = id(eidx)
-    got = _adopted_eidx.get(key)
-    if got is None or got[0] is not eidx:
-        got = (eidx, EnhancedIndex.adopt(eidx))
-        _adopted_eidx[key] = got
-    return got[1]
+    try:
+        got = _adopted_eidx.get(eidx)
+    except TypeError:                             # not weak-referenceable: adopt per call
+        return EnhancedIndex.adopt(eidx)
+    if got is None:
+        got = EnhancedIndex.adopt(eidx)
+        _adopted_eidx[eidx] = got
+    return got
 
 
 def search_queries(eidx, queries, k: int = 1, *, target: float | None = None, exact: bool = False,
@@ -308,7 +322,7 @@ def enhance(index, plan: SplitPlan, budget: SelectionBudget, seed: int, *,
         gq, _ = generate_global_queries(t.values, plan.n_global, noise_range, derive_seed(seed, 2))
 
         begin("collect-targets")
-        gts = collect_targets(t, selected, gq, plan.calibration)
+        gts = collect_targets(t, selected, gq, plan.calibration, train_nn=False)   # only nn[pool:] is read
 
         begin("local-queries")
         local_q = {}

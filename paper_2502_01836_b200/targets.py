@@ -185,8 +185,13 @@ def leaf_bounds(index, queries, mode: int = 1):
     return qs, lb
 
 
-def collect_targets(index, selected_leaves, queries, calibration_count: int) -> GlobalTrainSet:
-    """GPU twin of traingen.collect_targets (traingen.py:147-220)."""
+def collect_targets(index, selected_leaves, queries, calibration_count: int, *,
+                    train_nn: bool = True) -> GlobalTrainSet:
+    """GPU twin of traingen.collect_targets (traingen.py:147-220).
+
+    train_nn=False skips the pass-2 walk for the training rows (nn_distance[:c0]
+    is then NaN): enhance() reads only the calibration rows' nn_distance, and the
+    walk needs distances to every non-selected leaf it reaches."""
     torch = _lib.require_cuda()
     t = as_tree(index)
     di = t.device()
@@ -224,7 +229,9 @@ def collect_targets(index, selected_leaves, queries, calibration_count: int) -> 
     nn = np.empty(n_q)
     dcal_h = dcal.cpu().numpy()
     nn[c0:] = dcal_h.min(axis=1)
-    if c0 > 0:
+    if c0 > 0 and not train_nn:
+        nn[:c0] = np.nan
+    elif c0 > 0:
         d_other = None
         if other_pos:
             d_other = np.full((c0, L), np.inf)
