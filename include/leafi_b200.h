@@ -55,10 +55,6 @@ typedef struct lf_index {
     const int8_t* d_X8;          /* [n_series][roundup(m, 64)] round(x / scale), zero-padded */
     const float* d_qmeta;        /* [n_series][4] per row: scale = max|x| / 127, sum of squared
                                     codes (exact in fp32), ||scale * code - x||_2 rounded up, 0 */
-    /* optional second-level residual codes (lf_quantize_rows2), used by training-data
-       generation; NULL = unused */
-    const int8_t* d_X8b;         /* [n_series][m] rint((x - s1 c1) / (s1 / 128)) */
-    const float* d_qmeta2;       /* [n_series][4] |x^|^2, ||c2||, ||x^ - x|| rounded up, 0 */
     /* optional projected shadow for the two-stage scan (NULL = unused): an orthonormal
        basis P of pca_k directions (fp64, rows orthonormal), the mean mu, and per row the
        int8 codes of y = P (x - mu) with {scale, sum code^2, ||scale*code - y|| rounded up,
@@ -131,6 +127,15 @@ typedef struct lf_trace {
 const char* lf_last_error(void);
 int lf_version(void);
 int lf_device_sm_count(int device);
+
+/*
+ * Struct layout as this library was compiled, for bindings that mirror the
+ * structs above (ctypes, cgo, JNA): lf_abi_sizeof("lf_index") is sizeof, and
+ * lf_abi_offsetof("lf_index", "d_X") the field's offsetof; -1 for an unknown
+ * struct or field.  Types: "lf_index", "lf_search_opts", "lf_trace".
+ */
+int64_t lf_abi_sizeof(const char* type_name);
+int64_t lf_abi_offsetof(const char* type_name, const char* field_name);
 
 /*
  * Query segment means and node lower bounds.
@@ -265,10 +270,6 @@ int lf_local_min_dist_tc(const float* d_queries, const lf_index* idx, const int6
  * fp32 rows -- results are the exact fp64 direct-form minima (same terms as
  * lf_leaf_min_dist, another summation order, so equal to ~1 ulp).
  */
-/* With the second level present (d_X8b / d_qmeta2) the _q8 calls run the two-level
- * kernel: three int8 MMAs per tile (c1.d1 and c1.d2 + c2.d1 into two s32
- * accumulators), an interval ~128x narrower, and about one exact re-check per
- * (query, leaf) instead of dozens. */
 int lf_leaf_min_dist_q8(const float* d_queries, int64_t Q, const lf_index* idx,
                         const int32_t* h_leaf_sel, int32_t S, double* d_dl, int64_t ldd,
                         void* stream);
@@ -318,11 +319,6 @@ int lf_paa_device(const float* d_values, int64_t n, int32_t m, int32_t n_seg, do
 int lf_quantize_rows(const float* d_X, int64_t n, int32_t m, int8_t* d_X8, float* d_qmeta,
                      void* stream);
 
-/* Second level of the shadow: x^ = s1 c1 + (s1 / 128) c2 (|c2| <= 64), so ||x^ - x||
- * is ~128x below the first level's; d_qmeta2[r] = {|x^|^2, ||c2||, ||x^ - x|| rounded
- * up, 0}.  Needs the first level (lf_quantize_rows) in d_X8 / d_qmeta. */
-int lf_quantize_rows2(const float* d_X, int64_t n, int32_t m, const int8_t* d_X8, const float* d_qmeta,
-                      int8_t* d_X8b, float* d_qmeta2, void* stream);
 
 /*
  * Conformal auto-tuner fitting (conformal.py:171-198 simulate_search, for R offset

@@ -37,8 +37,6 @@ class LfIndex(C.Structure):
         ("d_leaf_filter", C.c_void_p),
         ("d_X8", C.c_void_p),
         ("d_qmeta", C.c_void_p),
-        ("d_X8b", C.c_void_p),
-        ("d_qmeta2", C.c_void_p),
         ("pca_k", C.c_int32),
         ("d_P", C.c_void_p),
         ("d_mu", C.c_void_p),
@@ -93,6 +91,8 @@ SIGNATURES = {
     "lf_last_error": (C.c_char_p, []),
     "lf_version": (C.c_int, []),
     "lf_device_sm_count": (C.c_int, [C.c_int]),
+    "lf_abi_sizeof": (C.c_int64, [C.c_char_p]),
+    "lf_abi_offsetof": (C.c_int64, [C.c_char_p, C.c_char_p]),
     "lf_bounds": (C.c_int, [_P, _I64, C.POINTER(LfIndex), _P, _P, _I32, _I32, _P, _P, _P]),
     "lf_search": (C.c_int, [C.POINTER(LfIndex), _P, _I64, C.POINTER(LfSearchOpts), _P, _P, _P,
                             C.POINTER(LfTrace), _P]),
@@ -121,7 +121,6 @@ SIGNATURES = {
     "lf_paa_device": (C.c_int, [_P, _I64, _I32, _I32, _P, _P]),
     "lf_quantize_rows": (C.c_int, [_P, _I64, _I32, _P, _P, _P]),
     "lf_replay_offsets": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _P, _I64, _I32, _P, _P]),
-    "lf_quantize_rows2": (C.c_int, [_P, _I64, _I32, _P, _P, _P, _P, _P]),
 }
 
 _lib = None
@@ -141,7 +140,25 @@ def lib():
             fn.restype = res
             fn.argtypes = args
         _lib = h
+        check_abi()          # a stale library with another struct layout fails here, not in a kernel
     return _lib
+
+
+STRUCTS = {"lf_index": LfIndex, "lf_search_opts": LfSearchOpts, "lf_trace": LfTrace}
+
+
+def check_abi() -> None:
+    """Assert that every ctypes mirror matches the compiled struct: sizeof and the
+    offset of each field (lf_abi_sizeof / lf_abi_offsetof)."""
+    h = lib()
+    for name, cls in STRUCTS.items():
+        size = h.lf_abi_sizeof(name.encode())
+        if size != C.sizeof(cls):
+            raise RuntimeError(f"{name}: ctypes sizeof {C.sizeof(cls)} != compiled {size}")
+        for fname, _ in cls._fields_:
+            off = h.lf_abi_offsetof(name.encode(), fname.encode())
+            if off != getattr(cls, fname).offset:
+                raise RuntimeError(f"{name}.{fname}: ctypes offset {getattr(cls, fname).offset} != compiled {off}")
 
 
 def check(rc: int) -> None:

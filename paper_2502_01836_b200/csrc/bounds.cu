@@ -59,6 +59,53 @@ __global__ void lb_kernel(const double* __restrict__ qsumm, int64_t Q, int n_seg
     }
 }
 
+// lb[q][node] for QT queries x 128 nodes per CTA: each thread holds its node's
+// envelope (n_seg <= 8) in registers and reuses it for QT queries, so the
+// envelopes are read from L2 once per QT queries instead of once per query.
+// Same arithmetic as lb_kernel (bit-identical bounds).
+constexpr int LBT_NODES = 128;
+constexpr int LBT_Q = 16;
+constexpr int LBT_SEG = 8;
+
+template <int MODE>
+__global__ void __launch_bounds__(LBT_NODES) lb_tile_kernel(const double* __restrict__ qsumm, int64_t Q, int ns,
+                                                            lf_index idx, const double* __restrict__ env_min,
+                                                            const double* __restrict__ env_max, int n_env,
+                                                            double* __restrict__ lb) {
+    __shared__ double qs[LBT_Q][LBT_SEG];
+    __shared__ double ws[LBT_SEG];
+    const int node = blockIdx.x * LBT_NODES + threadIdx.x;
+    const int64_t q0 = (int64_t)blockIdx.y * LBT_Q;
+    for (int i = threadIdx.x; i < LBT_Q * ns; i += LBT_NODES) {
+        const int qq = i / ns, sg = i - qq * ns;
+        qs[qq][sg] = q0 + qq < Q ? qsumm[(q0 + qq) * ns + sg] : 0.0;
+    }
+    if (threadIdx.x < ns) ws[threadIdx.x] = (double)idx.seg_width[threadIdx.x];
+    __syncthreads();
+    if (node >= n_env) return;
+    double mn[LBT_SEG], mx[LBT_SEG];
+#pragma unroll
+    for (int sg = 0; sg < LBT_SEG; ++sg) {
+        mn[sg] = sg < ns ? __ldg(env_min + (int64_t)sg * n_env + node) : 0.0;
+        mx[sg] = sg < ns ? __ldg(env_max + (int64_t)sg * n_env + node) : 0.0;
+    }
+    const int qn = (int)min((int64_t)LBT_Q, Q - q0);
+    for (int qq = 0; qq < qn; ++qq) {
+        double acc = 0.0;
+#pragma unroll
+        for (int sg = 0; sg < LBT_SEG; ++sg) {
+            if (sg < ns) {
+                const double qv = qs[qq][sg];
+                double g = fmax(mn[sg] - qv, qv - mx[sg]);
+                g = fmax(g, 0.0);
+                if (MODE == 0) acc = __fma_rn(__dmul_rn(ws[sg], g), g, acc);
+                else acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(g, g), ws[sg]));
+            }
+        }
+        lb[(q0 + qq) * n_env + node] = sqrt(acc);
+    }
+}
+
 int launch_bounds(const float* d_q, int64_t Q, const lf_index& idx, const double* env_min,
                   const double* env_max, int n_env, int mode, double* d_qsumm, double* d_lb,
                   cudaStream_t st) {
@@ -70,6 +117,15 @@ int launch_bounds(const float* d_q, int64_t Q, const lf_index& idx, const double
         LF_CUDA(cudaGetLastError());
     }
     if (n_env == 0) return LF_OK;
+    if (idx.n_seg <= LBT_SEG && (Q + LBT_Q - 1) / LBT_Q <= 65535) {
+        dim3 grid((unsigned)((n_env + LBT_NODES - 1) / LBT_NODES), (unsigned)((Q + LBT_Q - 1) / LBT_Q));
+        if (mode == 0)
+            lb_tile_kernel<0><<<grid, LBT_NODES, 0, st>>>(d_qsumm, Q, idx.n_seg, idx, env_min, env_max, n_env, d_lb);
+        else
+            lb_tile_kernel<1><<<grid, LBT_NODES, 0, st>>>(d_qsumm, Q, idx.n_seg, idx, env_min, env_max, n_env, d_lb);
+        LF_CUDA(cudaGetLastError());
+        return LF_OK;
+    }
     dim3 block(256);
     dim3 grid((unsigned)((n_env + 255) / 256), (unsigned)(Q < 65535 ? Q : 65535));
     if (mode == 0)
@@ -88,96 +144,19 @@ __global__ void iota_rows_kernel(int* __restrict__ v, int64_t Q, int n, int* __r
     if (t <= Q) offs[t] = (int)(t * n);
 }
 
-// One visit-order record: node, its bound, its leaf slot (+ filter flag) and the
-// filter operand pred - offset (tree.py:277-286), exactly as the plan evaluates it.
-__device__ inline void put_record(const OrderArgs& o, const lf_index& idx, int64_t q, int Nn, int p, double lb,
-                                  int node) {
-    const int64_t at = q * Nn + p;
-    o.lbs[at] = lb;
-    o.order[at] = node;
-    const int leaf = idx.d_node_leaf[node];
-    int rec = leaf;
-    double a = -kInf;
-    if (leaf >= 0 && idx.d_leaf_filter != nullptr && (o.pred != nullptr || o.pred64 != nullptr || o.lazy)) {
-        const int fs = idx.d_leaf_filter[leaf];
-        if (fs >= 0) {
-            rec |= LF_REC_HASF;
-            if (o.lazy) {
-                a = __longlong_as_double(0x7ff8000000000000LL);    // filled by the lazy inference
-            } else {
-                const double pv = o.pred64 != nullptr ? o.pred64[q * o.F + fs] : (double)o.pred[q * o.F + fs];
-                a = pv - o.offset[fs];
-            }
-        }
-    }
-    o.leafo[at] = rec;
-    o.adj[at] = a;
-}
-
-__device__ inline double node_bound(const double* qs, const double* ws, int ns, const double* env_min,
-                                    const double* env_max, int n_env, int node) {
-    double acc = 0.0;
-    for (int sg = 0; sg < ns; ++sg) {                  // lb_kernel<0>: np.dot(widths*gap, gap)
-        const double mn = env_min[(int64_t)sg * n_env + node];
-        const double mx = env_max[(int64_t)sg * n_env + node];
-        double g = fmax(mn - qs[sg], qs[sg] - mx);
-        g = fmax(g, 0.0);
-        acc = __fma_rn(__dmul_rn(ws[sg], g), g, acc);
-    }
-    return sqrt(acc);
-}
-
-// ITEMS bounds per thread for nodes first, first + stride, ... (striped, so each
-// warp load is 256 contiguous bytes of one segment's envelope row).  Segments
-// are the OUTER loop: all 2 x ITEMS loads of a segment are in flight together
-// instead of one dependent L2 round trip per (node, segment).  Each node's FMA
-// chain still runs over segments in order -- bit-identical to node_bound.
+// ------------------------------------------------------------ leaf order ----
+// The record of visit position p of query q (bounds.cuh): its bound, the gap
+// bound before it, leaf slot | filter flag, and pred - offset of the filter.
+// ITEMS positions per thread, the dependent loads (node -> leaf -> filter ->
+// prediction, offset) issued level by level so their latencies overlap.
 template <int ITEMS>
-__device__ __forceinline__ void node_bounds_striped(const double* qs, const double* ws, int ns,
-                                                    const double* __restrict__ env_min,
-                                                    const double* __restrict__ env_max, int n_env, int first,
-                                                    int stride, double (&lb)[ITEMS]) {
-    double acc[ITEMS];
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) acc[i] = 0.0;
-    for (int sg = 0; sg < ns; ++sg) {
-        const double qv = qs[sg], wv = ws[sg];
-        const double* mnp = env_min + (int64_t)sg * n_env;
-        const double* mxp = env_max + (int64_t)sg * n_env;
-        double mn[ITEMS], mx[ITEMS];
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            const int node = first + i * stride;
-            mn[i] = node < n_env ? __ldg(mnp + node) : 0.0;
-            mx[i] = node < n_env ? __ldg(mxp + node) : 0.0;
-        }
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            double g = fmax(mn[i] - qv, qv - mx[i]);
-            g = fmax(g, 0.0);
-            acc[i] = __fma_rn(__dmul_rn(wv, g), g, acc[i]);
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) lb[i] = sqrt(acc[i]);
-}
-
-// put_record for ITEMS visit positions per thread (p = first + i * stride), the
-// dependent loads (node -> leaf -> filter -> prediction, offset) issued level by
-// level across all ITEMS positions so their latencies overlap.
-template <int ITEMS>
-__device__ __forceinline__ void put_records_striped(const OrderArgs& o, const lf_index& idx, int64_t q, int Nn,
-                                                    int first, int stride, const unsigned* key_hi,
-                                                    const int* node_at, const unsigned* lo_by_node) {
-    int node[ITEMS], leaf[ITEMS], fs[ITEMS];
+__device__ __forceinline__ void put_records(const OrderArgs& o, const lf_index& idx, int64_t q, int Lr, int L,
+                                            const int (&p)[ITEMS], const int (&node)[ITEMS],
+                                            const double (&lbv)[ITEMS], const double (&gapv)[ITEMS]) {
     const bool filt = idx.d_leaf_filter != nullptr && (o.pred != nullptr || o.pred64 != nullptr || o.lazy);
+    int leaf[ITEMS], fs[ITEMS];
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        const int p = first + i * stride;
-        node[i] = p < Nn ? node_at[p] : -1;
-    }
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) leaf[i] = node[i] >= 0 ? __ldg(idx.d_node_leaf + node[i]) : -1;
+    for (int i = 0; i < ITEMS; ++i) leaf[i] = p[i] < L ? __ldg(idx.d_node_leaf + node[i]) : -1;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) fs[i] = (filt && leaf[i] >= 0) ? __ldg(idx.d_leaf_filter + leaf[i]) : -1;
     double pv[ITEMS], off[ITEMS];
@@ -192,343 +171,324 @@ __device__ __forceinline__ void put_records_striped(const OrderArgs& o, const lf
     }
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-        const int p = first + i * stride;
-        if (p >= Nn) continue;
-        const int64_t at = q * Nn + p;
-        o.lbs[at] = __hiloint2double((int)key_hi[p], (int)lo_by_node[node[i]]);
-        o.order[at] = node[i];
+        if (p[i] >= L) continue;
+        const int64_t at = q * Lr + p[i];
         int rec = leaf[i];
         double a = -kInf;
         if (fs[i] >= 0) {
             rec |= LF_REC_HASF;
             a = o.lazy ? __longlong_as_double(0x7ff8000000000000LL) : pv[i] - off[i];
         }
+        o.lbs[at] = lbv[i];
+        o.gap[at] = gapv[i];
         o.leafo[at] = rec;
         o.adj[at] = a;
+        if (o.order != nullptr) o.order[at] = node[i];
     }
 }
 
-// Fused K1 + K2 for trees of up to 8192 nodes, FULL order: one CTA per query
-// computes every node's search bound straight into registers and sorts the
-// nodes in shared memory -- the bound matrix never round-trips through HBM.
-// The sort key is the HIGH 32 bits of the non-negative fp64 bound (they order
-// like the doubles): a stable 4-pass 8-bit block radix sort instead of a 16-pass
-// sort of 64-bit keys.  Equal high words are then put in exact (lb, node id)
-// order by sorting each run on the low words (runs are rare and short; equal
-// bounds keep ascending ids from the stable sort), so the result is the exact
-// (lb, id) order of tree.py:256-275.
-constexpr int FS_THREADS = 512;
+// One CTA per query (trees of <= 8192 nodes, <= 4096 leaf slots): the node
+// bounds come from the L2-resident bound matrix (lb_tile_kernel); the leaves are
+// compacted in node-id order (warp ballots + one scan of the per-(item, warp)
+// counts), sorted by a 16-bit key -- floor(lb * 65000 / max lb), monotone in lb --
+// with a stable block radix sort (4 passes), and runs of equal keys are put in
+// exact (lb, node id) order by insertion sort (compact index order is node id
+// order, so the stable sort leaves each run nearly sorted).  Every non-leaf node
+// then finds by binary search the first leaf after it in (lb, id) order and
+// raises that leaf's gap bound to its own (atomicMax on the bits: bounds are
+// non-negative doubles).
+constexpr int LO_THREADS = 512;
+constexpr int LO_WARPS = LO_THREADS / 32;
+constexpr int LO_LEAF_ITEMS = 8;
+constexpr int LO_MAX_LEAVES = LO_THREADS * LO_LEAF_ITEMS;
+constexpr int LO_MAX_NI = 16;                            // node items per thread: <= 8192 nodes
+constexpr double LO_KEY_SPAN = 65000.0;
 
-template <int ITEMS, int RB>
-struct FsSmem {
-    using Sort = cub::BlockRadixSort<unsigned, FS_THREADS, ITEMS, int, RB>;
-    unsigned lo[FS_THREADS * ITEMS];                   // low word of each node's bound, by node id
+template <int RB>
+struct LoSmem {
+    using Sort = cub::BlockRadixSort<unsigned short, LO_THREADS, LO_LEAF_ITEMS, short, RB>;
+    double lb[LO_MAX_LEAVES];     // compact leaf bounds (node-id order); sorted after step 6
+    int node[LO_MAX_LEAVES];      // compact leaf node ids; sorted after step 6
     union {
         typename Sort::TempStorage sort;
         struct {
-            unsigned key[FS_THREADS * ITEMS];          // sorted high words
-            int node[FS_THREADS * ITEMS];              // sorted node ids
-        } out;
+            unsigned short key[LO_MAX_LEAVES];     // sorted keys
+            short perm[LO_MAX_LEAVES];             // compact index at each sorted position
+        } s;
+        unsigned long long gap[LO_MAX_LEAVES];     // bits of the gap bound before each position
     } u;
+    int wcnt[LO_MAX_NI][LO_WARPS];                 // leaves per (item, warp) -> exclusive offsets
+    double wmax[LO_WARPS];
+    double vmax;
+    int total;
 };
 
-template <int ITEMS, int RB>
-__global__ void __launch_bounds__(FS_THREADS, 1) bounds_sort_kernel(const double* __restrict__ qsumm, lf_index idx,
-                                                                 int n_env, OrderArgs o) {
-    using Sm = FsSmem<ITEMS, RB>;
-    extern __shared__ __align__(16) uint8_t fs_smem[];
-    Sm& sm = *reinterpret_cast<Sm*>(fs_smem);
-    __shared__ double qs[LF_MAX_SEG];
-    __shared__ double ws[LF_MAX_SEG];
+template <int NI, int RB>
+__global__ void __launch_bounds__(LO_THREADS, 2) leaf_order_kernel(const double* __restrict__ lb, lf_index idx,
+                                                                   OrderArgs o) {
+    using Sm = LoSmem<RB>;
+    extern __shared__ __align__(16) uint8_t lo_smem[];
+    Sm& sm = *reinterpret_cast<Sm*>(lo_smem);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned below = (1u << lane) - 1u;
     const int64_t q = blockIdx.x;
-    if (o.only != nullptr && o.only[q] == 0) return;
-    const int ns = idx.n_seg;
-    if (threadIdx.x < ns) {
-        qs[threadIdx.x] = qsumm[q * ns + threadIdx.x];
-        ws[threadIdx.x] = (double)idx.seg_width[threadIdx.x];
+    const int Nn = idx.n_nodes;
+    const int Lr = idx.n_leaves;
+    const double* lbq = lb + q * Nn;
+
+    // 1. local-leaf flags, leaves per (item, warp), largest leaf bound
+    unsigned flags = 0;
+    double vmax = 0.0;
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+        const int node = i * LO_THREADS + tid;
+        const bool isl = node < Nn && __ldg(idx.d_node_leaf + node) >= 0;
+        const unsigned b = __ballot_sync(0xffffffffu, isl);
+        if (isl) {
+            flags |= 1u << i;
+            vmax = fmax(vmax, lbq[node]);
+        }
+        if (lane == 0) sm.wcnt[i][warp] = __popc(b);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, off));
+    if (lane == 0) sm.wmax[warp] = vmax;
+    __syncthreads();
+    // 2. exclusive scan of the counts in (item, warp) order = node-id order
+    if (warp == 0) {
+        constexpr int NC = NI * LO_WARPS;                // <= 256 = 32 lanes x 8
+        int c[8], sum = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int k = lane * 8 + j;
+            c[j] = k < NC ? sm.wcnt[k / LO_WARPS][k % LO_WARPS] : 0;
+            sum += c[j];
+        }
+        int incl = sum;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += v;
+        }
+        int run = incl - sum;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int k = lane * 8 + j;
+            if (k < NC) sm.wcnt[k / LO_WARPS][k % LO_WARPS] = run;
+            run += c[j];
+        }
+        if (lane == 31) sm.total = incl;
+        double m = lane < LO_WARPS ? sm.wmax[lane] : 0.0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+        if (lane == 0) sm.vmax = m;
     }
     __syncthreads();
+    const int L = sm.total;
+    // 3. compact the leaves in node-id order
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+        const bool isl = (flags >> i) & 1u;
+        const unsigned b = __ballot_sync(0xffffffffu, isl);
+        if (isl) {
+            const int node = i * LO_THREADS + tid;
+            const int pos = sm.wcnt[i][warp] + __popc(b & below);
+            sm.lb[pos] = lbq[node];
+            sm.node[pos] = node;
+        }
+    }
+    __syncthreads();
+    // 4. stable sort of the 16-bit keys (blocked input = node-id order)
     {
-        double lb[ITEMS];
-        node_bounds_striped<ITEMS>(qs, ws, ns, idx.d_env_min, idx.d_env_max, n_env, threadIdx.x, FS_THREADS, lb);
+        const double vm = sm.vmax;
+        const double scale = (vm > 0.0 && vm < kInf) ? LO_KEY_SPAN / vm : 0.0;
+        unsigned short keys[LO_LEAF_ITEMS];
+        short vals[LO_LEAF_ITEMS];
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            const int node = i * FS_THREADS + threadIdx.x;
-            if (node < n_env) {
-                sm.u.out.key[node] = (unsigned)__double2hiint(lb[i]);
-                sm.lo[node] = (unsigned)__double2loint(lb[i]);
+        for (int e = 0; e < LO_LEAF_ITEMS; ++e) {
+            const int j = tid * LO_LEAF_ITEMS + e;
+            if (j < L) {
+                keys[e] = (unsigned short)fmin(floor(sm.lb[j] * scale), LO_KEY_SPAN);
+            } else {
+                keys[e] = 0xFFFFu;                       // padding sorts last (real keys <= 65000)
             }
+            vals[e] = (short)j;
+        }
+        typename Sm::Sort(sm.u.sort).SortBlockedToStriped(keys, vals, 0, 16);
+        __syncthreads();                                 // temp storage is reused below
+#pragma unroll
+        for (int e = 0; e < LO_LEAF_ITEMS; ++e) {
+            const int r = e * LO_THREADS + tid;
+            sm.u.s.key[r] = keys[e];
+            sm.u.s.perm[r] = vals[e];
         }
     }
     __syncthreads();
-    unsigned keys[ITEMS];
-    int vals[ITEMS];
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        const int node = threadIdx.x * ITEMS + i;          // blocked arrangement: stable sort keeps id order
-        if (node < n_env) {
-            keys[i] = sm.u.out.key[node];
-            vals[i] = node;
-        } else {
-            keys[i] = 0xFFFFFFFFu;                         // padding sorts last (real keys <= +inf's 0x7FF00000)
-            vals[i] = INT_MAX;
-        }
-    }
-    __syncthreads();                                       // the sort's temp storage overlays out.key
-    // Bit 31 (the sign of a non-negative bound) is always 0 -- padding's 0x7FFFFFFF in
-    // the low 31 bits still sorts after +inf's 0x7FF00000.  Striped output: conflict-free stores.
-    typename Sm::Sort(sm.u.sort).SortBlockedToStriped(keys, vals, 0, 31);
-    __syncthreads();                                       // temp storage is reused below
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        sm.u.out.key[i * FS_THREADS + threadIdx.x] = keys[i];
-        sm.u.out.node[i * FS_THREADS + threadIdx.x] = vals[i];
-    }
-    __syncthreads();
-    for (int p = threadIdx.x; p < n_env; p += FS_THREADS) {   // exact order inside runs of equal high words
-        const unsigned kp = sm.u.out.key[p];
-        if ((p == 0 || sm.u.out.key[p - 1] != kp) && p + 1 < n_env && sm.u.out.key[p + 1] == kp) {
+    // 5. exact (lb, node id) order inside runs of equal keys
+    for (int p = tid; p < L; p += LO_THREADS) {
+        const unsigned short kp = sm.u.s.key[p];
+        if ((p == 0 || sm.u.s.key[p - 1] != kp) && p + 1 < L && sm.u.s.key[p + 1] == kp) {
             int e = p + 1;
-            while (e < n_env && sm.u.out.key[e] == kp) ++e;
-            for (int a = p + 1; a < e; ++a) {              // insertion sort by (low word, id)
-                const int na = sm.u.out.node[a];
-                const unsigned la = sm.lo[na];
+            while (e < L && sm.u.s.key[e] == kp) ++e;
+            for (int a = p + 1; a < e; ++a) {
+                const int ja = sm.u.s.perm[a];
+                const double la = sm.lb[ja];
                 int b = a - 1;
                 while (b >= p) {
-                    const int nb = sm.u.out.node[b];
-                    const unsigned lbw = sm.lo[nb];
-                    if (lbw < la || (lbw == la && nb < na)) break;
-                    sm.u.out.node[b + 1] = nb;
+                    const int jb = sm.u.s.perm[b];
+                    const double lbb = sm.lb[jb];
+                    if (lbb < la || (lbb == la && jb < ja)) break;
+                    sm.u.s.perm[b + 1] = (short)jb;
                     --b;
                 }
-                sm.u.out.node[b + 1] = na;
+                sm.u.s.perm[b + 1] = (short)ja;
             }
         }
     }
     __syncthreads();
-    put_records_striped<ITEMS>(o, idx, q, n_env, threadIdx.x, FS_THREADS, sm.u.out.key, sm.u.out.node, sm.lo);
-    if (threadIdx.x == 0) {
-        o.olen[q] = n_env;
-        if (o.only != nullptr) o.only[q] = 0;
-    }
-}
-
-// Fused K1 + K2, PREFIX of the order (trees of up to 8192 nodes).  A search
-// only ever walks the head of its visit order (it stops at the first node with
-// lb > bsf * f), so sorting all n_nodes pairs per query is mostly wasted work.
-// One CTA per query: bounds into registers; radix-select (4 byte passes over
-// the high 32 bits of the non-negative fp64 bound, which order like the
-// doubles) the key T of the PF_K-th smallest; compact every node with key <= T
-// (or < T if that overflows PF_CAP) -- exactly the head of the (lb, id) order --
-// and bitonic-sort it by (lb, id) in shared memory.  A query whose walk reaches
-// the end of its prefix is refilled with the full order (refill_order).
-constexpr int PF_THREADS = 512;
-constexpr int PF_ITEMS = 16;
-constexpr int PF_K = 1024;
-constexpr int PF_CAP = 2048;
-
-__global__ void __launch_bounds__(PF_THREADS, 1) prefix_order_kernel(const double* __restrict__ qsumm, lf_index idx,
-                                                                  int Nn, OrderArgs o) {
-    __shared__ double qs[LF_MAX_SEG];
-    __shared__ double ws[LF_MAX_SEG];
-    __shared__ double sk[PF_CAP];
-    __shared__ int sv[PF_CAP];
-    __shared__ int hist[256];
-    __shared__ unsigned s_prefix;
-    __shared__ int s_rem, s_lt, s_le, s_cnt;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t q = blockIdx.x;
-    const int ns = idx.n_seg;
-    if (tid < ns) {
-        qs[tid] = qsumm[q * ns + tid];
-        ws[tid] = (double)idx.seg_width[tid];
-    }
-    if (tid == 0) { s_lt = 0; s_le = 0; s_cnt = 0; }
-    __syncthreads();
-    double key[PF_ITEMS];
-    unsigned k32[PF_ITEMS];
-    node_bounds_striped<PF_ITEMS>(qs, ws, ns, idx.d_env_min, idx.d_env_max, Nn, tid, PF_THREADS, key);
+    // 6. materialise the sorted order in place
+    {
+        double slb[LO_LEAF_ITEMS];
+        int snode[LO_LEAF_ITEMS];
 #pragma unroll
-    for (int i = 0; i < PF_ITEMS; ++i) {
-        const int node = i * PF_THREADS + tid;             // striped; the bitonic sort orders by (lb, id)
-        if (node < Nn) {
-            k32[i] = (unsigned)__double2hiint(key[i]);     // lb >= 0: monotone in lb
-        } else {
-            key[i] = kInf;
-            k32[i] = 0xFFFFFFFFu;                          // never selected
-        }
-    }
-    unsigned T = 0xFFFFFFFEu;                              // Nn <= PF_CAP: everything
-    bool take = true;
-    if (Nn > PF_CAP) {
-        unsigned prefix = 0, mask = 0;
-        int rem = PF_K;
-        for (int shift = 24; shift >= 0; shift -= 8) {
-            if (tid < 256) hist[tid] = 0;
-            __syncthreads();
-#pragma unroll
-            for (int i = 0; i < PF_ITEMS; ++i)
-                if (k32[i] != 0xFFFFFFFFu && (k32[i] & mask) == prefix) atomicAdd(&hist[(k32[i] >> shift) & 255], 1);
-            __syncthreads();
-            if (warp == 0) {
-                int c[8], sum = 0;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) { c[j] = hist[lane * 8 + j]; sum += c[j]; }
-                int incl = sum;
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const int v = __shfl_up_sync(0xffffffffu, incl, d);
-                    if (lane >= d) incl += v;
-                }
-                const int excl = incl - sum;
-                if (excl < rem && rem <= incl) {
-                    int acc = excl, b = 7;
-                    for (int j = 0; j < 8; ++j) {
-                        if (acc + c[j] >= rem) { b = j; break; }
-                        acc += c[j];
-                    }
-                    s_prefix = prefix | ((unsigned)(lane * 8 + b) << shift);
-                    s_rem = rem - acc;
-                }
+        for (int e = 0; e < LO_LEAF_ITEMS; ++e) {
+            const int r = e * LO_THREADS + tid;
+            if (r < L) {
+                const int j = sm.u.s.perm[r];
+                slb[e] = sm.lb[j];
+                snode[e] = sm.node[j];
             }
-            __syncthreads();
-            prefix = s_prefix;
-            rem = s_rem;
-            mask |= 255u << shift;
         }
-        T = prefix;                                        // key of the PF_K-th smallest bound
-        int lt = 0, le = 0;
-#pragma unroll
-        for (int i = 0; i < PF_ITEMS; ++i) {
-            lt += k32[i] < T;
-            le += k32[i] <= T;
-        }
-        atomicAdd(&s_lt, lt);
-        atomicAdd(&s_le, le);
         __syncthreads();
-        if (s_le > PF_CAP) {                               // take only keys < T (count < PF_K); none
-            if (s_lt == 0) take = false;                   // at all -> the plan refills at once
-            else T -= 1;
-        }
-    }
 #pragma unroll
-    for (int i = 0; i < PF_ITEMS; ++i)
-        if (take && k32[i] <= T) {
-            const int pos = atomicAdd(&s_cnt, 1);
-            sk[pos] = key[i];
-            sv[pos] = i * PF_THREADS + tid;
-        }
-    __syncthreads();
-    const int cnt = s_cnt;
-    int N = 64;
-    while (N < cnt) N <<= 1;
-    for (int i = cnt + tid; i < N; i += PF_THREADS) { sk[i] = kInf; sv[i] = INT_MAX; }
-    __syncthreads();
-    for (int k = 2; k <= N; k <<= 1) {                     // bitonic sort by (lb, node id)
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = tid; i < N; i += PF_THREADS) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
-                    const double a = sk[i], b = sk[ixj];
-                    const int va = sv[i], vb = sv[ixj];
-                    const bool gt = a > b || (a == b && va > vb);
-                    if (gt == ((i & k) == 0)) { sk[i] = b; sk[ixj] = a; sv[i] = vb; sv[ixj] = va; }
-                }
+        for (int e = 0; e < LO_LEAF_ITEMS; ++e) {
+            const int r = e * LO_THREADS + tid;
+            if (r < L) {
+                sm.lb[r] = slb[e];
+                sm.node[r] = snode[e];
+                sm.u.gap[r] = 0ull;                      // key / perm are dead
             }
-            __syncthreads();
         }
     }
-    for (int p = tid; p < cnt; p += PF_THREADS) put_record(o, idx, q, Nn, p, sk[p], sv[p]);
-    if (tid == 0) o.olen[q] = cnt;
-}
-
-__global__ void records_kernel(const double* __restrict__ lb_sorted, const int* __restrict__ order, lf_index idx,
-                               int64_t Q, int Nn, OrderArgs o) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < Q * Nn) {
-        const int64_t q = t / Nn;
-        put_record(o, idx, q, Nn, (int)(t - q * Nn), lb_sorted[t], order[t]);
+    __syncthreads();
+    // 7. gap bounds: each non-leaf node raises the gap of the first leaf after it
+#pragma unroll 4
+    for (int i = 0; i < NI; ++i) {
+        const int node = i * LO_THREADS + tid;
+        if (node >= Nn || ((flags >> i) & 1u)) continue;
+        const double v = lbq[node];
+        int lo = 0, hi = L;
+        while (lo < hi) {                                // first position with (lb, id) > (v, node)
+            const int mid = (lo + hi) >> 1;
+            const double a = sm.lb[mid];
+            if (a > v || (a == v && sm.node[mid] > node)) hi = mid;
+            else lo = mid + 1;
+        }
+        if (lo < L) atomicMax(&sm.u.gap[lo], (unsigned long long)__double_as_longlong(v));
     }
-    if (t < Q) o.olen[t] = Nn;
+    __syncthreads();
+    // 8. records, 4 positions per thread at a time
+#pragma unroll
+    for (int h = 0; h < LO_LEAF_ITEMS; h += 4) {
+        int p[4], node[4];
+        double lbv[4], gv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            p[e] = (h + e) * LO_THREADS + tid;
+            const bool ok = p[e] < L;
+            node[e] = ok ? sm.node[p[e]] : 0;
+            lbv[e] = ok ? sm.lb[p[e]] : 0.0;
+            gv[e] = ok ? __longlong_as_double((long long)sm.u.gap[p[e]]) : 0.0;
+        }
+        put_records<4>(o, idx, q, Lr, L, p, node, lbv, gv);
+    }
+    if (tid == 0) o.olen[q] = L;
 }
 
-template <int ITEMS, int RB = 4>
-static int launch_fused(const double* d_qsumm, int64_t Q, const lf_index& idx, int n, const OrderArgs& oa,
-                        cudaStream_t st) {
-    const int bytes = (int)sizeof(FsSmem<ITEMS, RB>);
-    LF_CUDA(smem_optin(bounds_sort_kernel<ITEMS, RB>, bytes));
-    bounds_sort_kernel<ITEMS, RB><<<(unsigned)Q, FS_THREADS, bytes, st>>>(d_qsumm, idx, n, oa);
+// Any tree size: one warp per query walks the FULL sorted (lb, node id) order
+// (CUB segmented sort of the bound matrix), keeps the local leaves in order and
+// carries the largest non-leaf bound seen since the previous leaf.
+__global__ void leaf_records_kernel(const double* __restrict__ slb, const int* __restrict__ sorder, lf_index idx,
+                                    int64_t Q, OrderArgs o) {
+    const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (q >= Q) return;
+    const unsigned below = (1u << lane) - 1u;
+    const int Nn = idx.n_nodes, Lr = idx.n_leaves;
+    const double* lbs = slb + q * Nn;
+    const int* ord = sorder + q * Nn;
+    double carry = 0.0;                                  // largest non-leaf bound after the last leaf
+    int outp = 0;
+    for (int base = 0; base < Nn; base += 32) {
+        const int i = base + lane;
+        const bool valid = i < Nn;
+        const int node = valid ? ord[i] : 0;
+        const double v = valid ? lbs[i] : 0.0;
+        const int leaf = valid ? __ldg(idx.d_node_leaf + node) : -1;
+        const bool isl = valid && leaf >= 0;
+        const bool isn = valid && leaf < 0;
+        const unsigned ml = __ballot_sync(0xffffffffu, isl);
+        const unsigned mn = __ballot_sync(0xffffffffu, isn);
+        const unsigned nl = mn & below, ll = ml & below;
+        const int hn = nl ? 31 - __clz(nl) : -1;
+        const int hl = ll ? 31 - __clz(ll) : -1;
+        const double vn = __shfl_sync(0xffffffffu, v, hn >= 0 ? hn : 0);
+        const double g = hn > hl ? vn : (hl >= 0 ? 0.0 : carry);
+        const int lastn = mn ? 31 - __clz(mn) : -1;
+        const int lastl = ml ? 31 - __clz(ml) : -1;
+        const double vlast = __shfl_sync(0xffffffffu, v, lastn >= 0 ? lastn : 0);
+        if (isl) {
+            const int p1[1] = {outp + __popc(ll)};
+            const int n1[1] = {node};
+            const double l1[1] = {v}, g1[1] = {g};
+            put_records<1>(o, idx, q, Lr, Lr, p1, n1, l1, g1);
+        }
+        outp += __popc(ml);
+        if (lastn > lastl) carry = vlast;
+        else if (lastl >= 0) carry = 0.0;
+    }
+    if (lane == 0) o.olen[q] = outp;
+}
+
+template <int NI>
+static int launch_leaf_order(const double* d_lb, int64_t Q, const lf_index& idx, const OrderArgs& oa,
+                             cudaStream_t st) {
+    constexpr int RB = 4;
+    const int bytes = (int)sizeof(LoSmem<RB>);
+    LF_CUDA(smem_optin(leaf_order_kernel<NI, RB>, bytes));
+    leaf_order_kernel<NI, RB><<<(unsigned)Q, LO_THREADS, bytes, st>>>(d_lb, idx, oa);
     LF_CUDA(cudaGetLastError());
     return LF_OK;
 }
 
-static int sort_radix_bits() {                         // LF_SORT_RB: digit width of the block sort (4..7)
-    const char* e = std::getenv("LF_SORT_RB");
-    const int rb = e != nullptr ? std::atoi(e) : 5;
-    return rb >= 4 && rb <= 7 ? rb : 5;
-}
-
-template <int ITEMS>
-static int launch_fused_rb(const double* d_qsumm, int64_t Q, const lf_index& idx, int n, const OrderArgs& oa,
-                           cudaStream_t st) {
-    switch (sort_radix_bits()) {
-        case 5: return launch_fused<ITEMS, 5>(d_qsumm, Q, idx, n, oa, st);
-        case 6: return launch_fused<ITEMS, 6>(d_qsumm, Q, idx, n, oa, st);
-        case 7: return launch_fused<ITEMS, 7>(d_qsumm, Q, idx, n, oa, st);
-        default: return launch_fused<ITEMS, 4>(d_qsumm, Q, idx, n, oa, st);
-    }
-}
-
-static int launch_full_fused(const double* d_qsumm, int64_t Q, const lf_index& idx, int n, const OrderArgs& oa,
-                             cudaStream_t st) {
-    if (n <= FS_THREADS * 4) return launch_fused_rb<4>(d_qsumm, Q, idx, n, oa, st);
-    if (n <= FS_THREADS * 8) return launch_fused_rb<8>(d_qsumm, Q, idx, n, oa, st);
-    return launch_fused_rb<16>(d_qsumm, Q, idx, n, oa, st);
-}
-
-// Segment means + bounds + per-query visit-order records in as few passes as the
-// tree size allows: fused prefix / block sort up to 8192 nodes, else bounds
-// kernel + CUB segmented sort + record gather.
-int bounds_and_order(const float* d_q, int64_t Q, const lf_index& idx, double* d_qsumm, double* d_lb_scratch,
-                     const OrderArgs& oa, bool prefix, cudaStream_t st, int* kernels) {
+// Segment means + node bounds + per-query leaf records: the bound matrix
+// (lb_tile_kernel) feeds the per-query leaf sort when the tree fits one CTA
+// (<= 8192 nodes, <= 4096 leaf slots), else CUB's segmented sort of all nodes
+// and the warp-per-query record walk.
+int bounds_and_order(const float* d_q, int64_t Q, const lf_index& idx, double* d_qsumm, double* d_lb,
+                     const OrderArgs& oa, cudaStream_t st, int* kernels) {
     const int n = idx.n_nodes;
     if (Q == 0 || n == 0) return LF_OK;
-    if (n <= FS_THREADS * 16 && Q <= 0x7fffffff) {
-        {
-            int64_t tot = Q * idx.n_seg;
-            paa_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(d_q, Q, idx, d_qsumm);
-            LF_CUDA(cudaGetLastError());
-        }
-        if (kernels) *kernels += 2;
-        if (prefix && n > PF_CAP) {
-            prefix_order_kernel<<<(unsigned)Q, PF_THREADS, 0, st>>>(d_qsumm, idx, n, oa);
-            LF_CUDA(cudaGetLastError());
-            return LF_OK;
-        }
-        OrderArgs all = oa;
-        all.only = nullptr;
-        return launch_full_fused(d_qsumm, Q, idx, n, all, st);
+    int rc = launch_bounds(d_q, Q, idx, idx.d_env_min, idx.d_env_max, n, 0, d_qsumm, d_lb, st);
+    if (rc) return rc;
+    if (kernels) *kernels += 3;
+    if (n <= LO_THREADS * LO_MAX_NI && idx.n_leaves <= LO_MAX_LEAVES && Q <= 0x7fffffff) {
+        if (n <= LO_THREADS * 4) return launch_leaf_order<4>(d_lb, Q, idx, oa, st);
+        if (n <= LO_THREADS * 8) return launch_leaf_order<8>(d_lb, Q, idx, oa, st);
+        return launch_leaf_order<16>(d_lb, Q, idx, oa, st);
     }
-    int rc = launch_bounds(d_q, Q, idx, idx.d_env_min, idx.d_env_max, n, 0, d_qsumm, d_lb_scratch, st);
+    Scratch slb, sord;
+    LF_CUDA(slb.alloc(sizeof(double) * Q * n, st));
+    LF_CUDA(sord.alloc(sizeof(int) * Q * n, st));
+    rc = sort_visit_order(d_lb, Q, n, slb.as<double>(), sord.as<int>(), st);
     if (rc) return rc;
-    if (kernels) *kernels += 5;
-    rc = sort_visit_order(d_lb_scratch, Q, n, oa.lbs, oa.order, st);
-    if (rc) return rc;
-    const int64_t tot = std::max<int64_t>(Q * n, Q);
-    records_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(oa.lbs, oa.order, idx, Q, n, oa);
+    if (kernels) *kernels += 2;
+    leaf_records_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(slb.as<double>(), sord.as<int>(), idx, Q,
+                                                                          oa);
     LF_CUDA(cudaGetLastError());
     return LF_OK;
 }
 
-int refill_order(const float* d_q, int64_t Q, const lf_index& idx, const double* d_qsumm, double* d_lb_scratch,
-                 const OrderArgs& oa, cudaStream_t st, int* kernels) {
-    (void)d_q;
-    (void)d_lb_scratch;
-    const int n = idx.n_nodes;
-    LF_REQUIRE(n <= FS_THREADS * 16, "refill is only needed for prefix orders (<= 8192 nodes)");
-    if (kernels) *kernels += 1;
-    return launch_full_fused(d_qsumm, Q, idx, n, oa, st);
-}
 // Per-query stable sort of (lb, node id): the heap pop order of tree.py:256-275
 // (child lb >= parent lb and child id > parent id, so the heap is a sort).
 int sort_visit_order(const double* d_lb, int64_t Q, int n, double* d_lb_sorted, int* d_order,

@@ -7,16 +7,27 @@ namespace lf {
 int launch_bounds(const float* d_q, int64_t Q, const lf_index& idx, const double* env_min,
                   const double* env_max, int n_env, int mode, double* d_qsumm, double* d_lb,
                   cudaStream_t st);
-// Per-query visit-order records [Q][n_nodes] in (lb, node id) order; only the
-// first olen[q] entries are valid (a sorted PREFIX of the full order, or all of
-// it).  leafo = leaf slot | LF_REC_HASF when the leaf has a filter, -1 for an
-// internal node; adj = prediction - offset of that filter (the exact operand of
-// the filter rule, tree.py:282), gathered once so the plan never chases it.
+
+// Per-query visit-order records [Q][L] over the L LEAF slots of the index, in
+// (lb, node id) order -- the pop order of tree.py:256-275 restricted to the
+// leaves.  Internal nodes (and, on a leaf shard, the other shards' leaves) are
+// not records: the only thing they decide is where the walk stops.  The walk
+// stops at the first popped node with lb > bsf * f (tree.py:261); an internal
+// node there ends the walk WITHOUT counting a leaf (tree.py:262-265), a leaf
+// counts as visited + lb-pruned.  Because bounds are popped in ascending order,
+// "some non-leaf node between leaf i-1 and leaf i has lb > thr" is the same as
+// gap[i] > thr, gap[i] = the largest such bound (0 if none): the walk at leaf i
+// stops uncounted if gap[i] > thr, else counted if lb[i] > thr.
+//   leafo = leaf slot | LF_REC_HASF when the leaf has a filter;
+//   adj   = prediction - offset of that filter (the exact operand of the filter
+//           rule, tree.py:282), gathered once so the plan never chases it;
+//   order = node id (written only when `order` is non-NULL: traces).
 constexpr int LF_REC_HASF = 1 << 30;
 constexpr int LF_REC_LEAF = LF_REC_HASF - 1;
 struct OrderArgs {
     double* lbs;
-    int* order;
+    double* gap;
+    int* order;                  // may be NULL
     int* leafo;
     double* adj;
     int* olen;
@@ -24,17 +35,12 @@ struct OrderArgs {
     const double* pred64;        // [Q][F] or NULL
     const double* offset;        // [F]
     int F;
-    int* only;                   // refill: queries with only[q] != 0 (cleared when done); NULL = all
     int lazy;                    // predictions computed later (lazy inference): flag filters, adj = NaN
 };
-// prefix = true: sort only the first ~PF_K entries of each order (olen[q] < n_nodes
-// possible); the plan asks for the rest with refill_order when it gets there.
-int bounds_and_order(const float* d_q, int64_t Q, const lf_index& idx, double* d_qsumm, double* d_lb_scratch,
-                     const OrderArgs& oa, bool prefix, cudaStream_t st, int* kernels);
-// Full order for the queries flagged in oa.only (the first olen[q] entries are
-// unchanged: the prefix is the head of the full order).
-int refill_order(const float* d_q, int64_t Q, const lf_index& idx, const double* d_qsumm, double* d_lb_scratch,
-                 const OrderArgs& oa, cudaStream_t st, int* kernels);
+// Segment means (d_qsumm [Q][n_seg]), node bounds (d_lb [Q][n_nodes], the search
+// bound of summarize.py:97-107) and the leaf records above.
+int bounds_and_order(const float* d_q, int64_t Q, const lf_index& idx, double* d_qsumm, double* d_lb,
+                     const OrderArgs& oa, cudaStream_t st, int* kernels);
 int sort_visit_order(const double* d_lb, int64_t Q, int n, double* d_lb_sorted, int* d_order,
                      cudaStream_t st);
 }  // namespace lf

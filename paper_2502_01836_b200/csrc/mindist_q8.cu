@@ -381,295 +381,6 @@ mindist_q8_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_consta
     }
 }
 
-// ---------------------------------------------------------------------------
-// Two-level variant: x^ = s1 (c1 + c2 / 128), q^ = t1 (d1 + d2 / 128).
-//     x^ . q^ = s1 t1 (T1 + T2 / 128 + (c2 . d2) / 16384),
-//     T1 = c1 . d1  and  T2 = c1 . d2 + c2 . d1   (two s32 TMEM accumulators, three
-//     int8 MMAs per K step); the dropped c2 . d2 term is bounded by ||c2|| ||d2||.
-// The interval half-width e2_x + e2_q is ~128x narrower than the one-level kernel's,
-// so on far leaves (where many rows sit within the one-level error band of the
-// minimum) the exact re-checks drop from dozens to about one per (query, leaf).
-// Tiles: 128 queries x 128 rows x m; 2 query stages (d1 + d2 k-blocks), double-
-// buffered row chunks (c1 + c2 k-blocks), 2 x (2 x 128) TMEM columns.
-constexpr int BN2 = 128;
-constexpr int T_BYTES = 128 * KBB;                 // one 128 x 128 B operand tile
-constexpr int A2_STAGE = 2 * T_BYTES;              // d1 + d2
-constexpr int STAGES2 = 2;
-constexpr int B2_BUF = MAX_KB * 2 * T_BYTES;       // per chunk: (c1, c2) x k-blocks
-constexpr int O2_B = 0;
-constexpr int O2_A = O2_B + 2 * B2_BUF;
-constexpr int O2_META = O2_A + STAGES2 * A2_STAGE;
-constexpr int O2_EMAX = O2_META + 2 * BN2 * 16;
-constexpr int O2_BAR = O2_EMAX + 16;
-constexpr int N2_BAR = 2 * STAGES2 + 8;
-constexpr int O2_TMEM = O2_BAR + N2_BAR * 8;
-constexpr int O2_LIST = O2_TMEM + 16;
-constexpr int O2_SBEST = O2_LIST + EPI_WARPS * 64 * 4;
-constexpr int SMEM2_BYTES = O2_SBEST + EPI_WARPS * 32 * 8 + 1024;
-
-__global__ void __launch_bounds__(THREADS, 1)
-mindist_q82_kernel(const __grid_constant__ CUtensorMap map_q1, const __grid_constant__ CUtensorMap map_q2,
-                   const __grid_constant__ CUtensorMap map_x1, const __grid_constant__ CUtensorMap map_x2,
-                   const Item* __restrict__ items, int n_items, lf_index idx, const float* __restrict__ Qf,
-                   const float4* __restrict__ qmeta1, const float4* __restrict__ qmeta2,
-                   unsigned long long* __restrict__ out, long long ldo) {
-    extern __shared__ uint8_t smem_raw[];
-    // 1024-B alignment for the SW128 tiles, by offsetting the __shared__ array itself so the
-    // compiler keeps the shared address space (LDS, not generic loads)
-    uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
-    uint8_t* Bs = smem + O2_B;
-    uint8_t* As = smem + O2_A;
-    float4* meta = reinterpret_cast<float4*>(smem + O2_META);         // [2][BN2] {|x^|^2, s1, e2, s1 ||c2||}
-    float* emax_s = reinterpret_cast<float*>(smem + O2_EMAX);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + O2_BAR);
-    uint64_t* empty = full + STAGES2;
-    uint64_t* bfull = empty + STAGES2;
-    uint64_t* bempty = bfull + 2;
-    uint64_t* tfull = bempty + 2;
-    uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + O2_TMEM);
-    int* cand_all = reinterpret_cast<int*>(smem + O2_LIST);
-    unsigned long long* sbest_all = reinterpret_cast<unsigned long long*>(smem + O2_SBEST);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m = idx.m;
-    const int n_kb = m / KBB;
-    if (warp == 0 && lane == 0) {
-        for (int s = 0; s < STAGES2; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&bfull[s], 1);
-            mbar_init(&bempty[s], 1 + EPI_WARPS);
-            mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], EPI_WARPS);
-        }
-        mbar_fence_init();
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
-                     "r"(TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    tc_before();
-    __syncthreads();
-    tc_after();
-    const uint32_t tmem_base = *tmem_slot;
-
-    if (warp == 0) {                                            // ---- producer
-        const float4* rm1 = reinterpret_cast<const float4*>(idx.d_qmeta);
-        const float4* rm2 = reinterpret_cast<const float4*>(idx.d_qmeta2);
-        int stage = 0;
-        uint32_t phase = 0;
-        long long chunk = 0;
-        for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-            const Item item = items[it];
-            const long long lb = idx.d_leaf_ptr[item.leaf], le = idx.d_leaf_ptr[item.leaf + 1];
-            const int n_qb = (int)((item.q1 - item.q0 + BM - 1) / BM);
-            for (long long r0 = lb; r0 < le; r0 += BN2, ++chunk) {
-                const int bb = (int)(chunk & 1);
-                __syncwarp();
-                mbar_wait(&bempty[bb], (uint32_t)((chunk >> 1) & 1) ^ 1u);
-                float em = 0.f;
-                for (int i = lane; i < BN2; i += 32) {
-                    const long long r = r0 + i;
-                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (r < le) {
-                        const float s1 = __ldg(rm1 + r).x;
-                        const float4 b = __ldg(rm2 + r);
-                        v = make_float4(b.x, s1, b.z, s1 * b.y * (1.f + 1e-6f));
-                        em = fmaxf(em, b.z);
-                    }
-                    meta[bb * BN2 + i] = v;
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) em = fmaxf(em, __shfl_xor_sync(0xffffffffu, em, o));
-                if (lane == 0) emax_s[bb] = em;
-                __syncwarp();
-                if (lane == 0) {
-                    mbar_expect_tx(&bfull[bb], (uint32_t)(n_kb * 2 * T_BYTES));
-                    for (int kb = 0; kb < n_kb; ++kb) {
-                        uint8_t* dst = Bs + bb * B2_BUF + kb * 2 * T_BYTES;
-                        tma_2d(&map_x1, &bfull[bb], dst, kb * KBB, (int)r0);
-                        tma_2d(&map_x2, &bfull[bb], dst + T_BYTES, kb * KBB, (int)r0);
-                    }
-                }
-                for (int qb = 0; qb < n_qb; ++qb) {
-                    for (int kb = 0; kb < n_kb; ++kb) {
-                        if (lane == 0) {
-                            mbar_wait(&empty[stage], phase ^ 1);
-                            mbar_expect_tx(&full[stage], A2_STAGE);
-                            uint8_t* dst = As + stage * A2_STAGE;
-                            const int qrow = (int)(item.q0 + qb * BM);
-                            tma_2d(&map_q1, &full[stage], dst, kb * KBB, qrow);
-                            tma_2d(&map_q2, &full[stage], dst + T_BYTES, kb * KBB, qrow);
-                        }
-                        if (++stage == STAGES2) { stage = 0; phase ^= 1; }
-                    }
-                }
-            }
-        }
-    } else if (warp == 1) {                                     // ---- MMA issuer
-        if (lane == 0) {
-            const uint32_t idesc = idesc_s8(BM, BN2);
-            int stage = 0, acc = 0;
-            uint32_t phase = 0, acc_phase = 0;
-            long long chunk = 0;
-            for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-                const Item item = items[it];
-                const long long lb = idx.d_leaf_ptr[item.leaf], le = idx.d_leaf_ptr[item.leaf + 1];
-                const int n_qb = (int)((item.q1 - item.q0 + BM - 1) / BM);
-                for (long long r0 = lb; r0 < le; r0 += BN2, ++chunk) {
-                    const int bb = (int)(chunk & 1);
-                    mbar_wait(&bfull[bb], (uint32_t)((chunk >> 1) & 1));
-                    tc_after();
-                    const uint32_t bs = su32(Bs + bb * B2_BUF);
-                    for (int qb = 0; qb < n_qb; ++qb) {
-                        mbar_wait(&tempty[acc], acc_phase ^ 1);
-                        tc_after();
-                        const uint32_t d1 = tmem_base + (uint32_t)(acc * 256);
-                        const uint32_t d2 = d1 + 128;
-                        for (int kb = 0; kb < n_kb; ++kb) {
-                            mbar_wait(&full[stage], phase);
-                            tc_after();
-                            const uint32_t a1 = su32(As + stage * A2_STAGE), a2 = a1 + T_BYTES;
-                            const uint32_t b1 = bs + kb * 2 * T_BYTES, b2 = b1 + T_BYTES;
-#pragma unroll
-                            for (int kk = 0; kk < KBB / 32; ++kk) {
-                                const uint32_t first = (kb | kk) != 0 ? 1u : 0u;
-                                mma_i8(d1, sw128_desc(a1 + kk * 32), sw128_desc(b1 + kk * 32), idesc, first);
-                                mma_i8(d2, sw128_desc(a1 + kk * 32), sw128_desc(b2 + kk * 32), idesc, first);
-                                mma_i8(d2, sw128_desc(a2 + kk * 32), sw128_desc(b1 + kk * 32), idesc, 1u);
-                            }
-                            mma_commit(&empty[stage]);
-                            if (++stage == STAGES2) { stage = 0; phase ^= 1; }
-                        }
-                        mma_commit(&tfull[acc]);
-                        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-                    }
-                    mma_commit(&bempty[bb]);
-                }
-            }
-        }
-    } else {                                                    // ---- epilogue (warps 2..9)
-        const int quarter = warp & 3;
-        const int grp = (warp - 2) >> 2;                        // column half (64 rows each)
-        const int row = quarter * 32 + lane;
-        int* list = cand_all + (warp - 2) * 64;
-        unsigned long long* sbest = sbest_all + (warp - 2) * 32;
-        int acc = 0;
-        uint32_t acc_phase = 0;
-        long long chunk = 0;
-        for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-            const Item item = items[it];
-            const long long lb = idx.d_leaf_ptr[item.leaf], le = idx.d_leaf_ptr[item.leaf + 1];
-            const int n_qb = (int)((item.q1 - item.q0 + BM - 1) / BM);
-            for (long long r0 = lb; r0 < le; r0 += BN2, ++chunk) {
-                const int bb = (int)(chunk & 1);
-                const int nrows = (int)min((long long)BN2, le - r0);
-                mbar_wait(&bfull[bb], (uint32_t)((chunk >> 1) & 1));
-                const float4* mt = meta + bb * BN2 + grp * 64;
-                const int ncols = max(0, min(64, nrows - grp * 64));
-                const float emax_rows = emax_s[bb];
-                for (int qb = 0; qb < n_qb; ++qb) {
-                    const long long q = item.q0 + (long long)qb * BM + row;
-                    const bool qv = q < item.q1;
-                    unsigned long long* dst = out + (qv ? q : 0) * ldo + item.col;
-                    double best = qv ? __longlong_as_double((long long)*(volatile unsigned long long*)dst) : 0.0;
-                    const float4 qa = qv ? __ldg(qmeta1 + q) : make_float4(1.f, 0.f, 0.f, 0.f);
-                    const float4 qb2 = qv ? __ldg(qmeta2 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-                    const float Rq = qb2.x, cq2 = 2.f * qa.x;
-                    const float hq = cq2 * qb2.y * (1.f / 16384.f) * (1.f + 1e-6f);   // dropped c2.d2 term
-                    const float emax = emax_rows + qb2.z;
-                    mbar_wait(&tfull[acc], acc_phase);
-                    tc_after();
-                    const uint32_t t1 =
-                        tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * 256 + grp * 64);
-                    const uint32_t t2 = t1 + 128;
-                    float U = best < kInf ? __double2float_ru(sqrt(best)) : __int_as_float(0x7f800000);
-                    if (__any_sync(0xffffffffu, !(best < kInf))) {
-                        float v = __int_as_float(0x7f800000);
-                        for (int c0 = 0; c0 < ncols; c0 += 32) {
-                            uint32_t r1[32], r2[32];
-                            LF_TMEM_LD32X(t1 + (uint32_t)c0, r1);
-                            LF_TMEM_LD32X(t2 + (uint32_t)c0, r2);
-                            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) {
-                                if (c0 + j < ncols) {
-                                    const float4 mr = mt[c0 + j];
-                                    const float c1 = mr.x + Rq;
-                                    const float D = fmaf((float)(int)r2[j], 1.f / 128.f, (float)(int)r1[j]);
-                                    const float d2 = fmaf(-(cq2 * mr.y), D, c1);
-                                    v = fminf(v, d2 + fmaf(mr.w, hq, 1e-5f * c1));
-                                }
-                            }
-                        }
-                        if (!(best < kInf)) U = (sqrtf(fmaxf(v, 0.f)) + emax) * (1.f + 1e-6f);
-                    }
-                    const float V = (U + qb2.z) * (1.f + 1e-6f);
-                    const long long qbase = item.q0 + (long long)qb * BM + quarter * 32;
-                    sbest[lane] = (unsigned long long)__double_as_longlong(best);
-                    int cnt = 0;
-                    auto flush = [&]() {
-                        __syncwarp();
-                        if (m == 256)
-                            recheck8<256>(list, cnt, lane, Qf, qbase, idx.d_X, r0 + grp * 64, sbest, out, ldo, item.col);
-                        else
-                            recheck8<128>(list, cnt, lane, Qf, qbase, idx.d_X, r0 + grp * 64, sbest, out, ldo, item.col);
-                        __syncwarp();
-                        best = __longlong_as_double((long long)sbest[lane]);
-                        cnt = 0;
-                    };
-                    for (int c0 = 0; c0 < ncols; c0 += 32) {
-                        uint32_t r1[32], r2[32];
-                        LF_TMEM_LD32X(t1 + (uint32_t)c0, r1);
-                        LF_TMEM_LD32X(t2 + (uint32_t)c0, r2);
-                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                        unsigned bits = 0;
-                        if (qv) {
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) {
-                                if (c0 + j < ncols) {
-                                    const float4 mr = mt[c0 + j];
-                                    const float c1 = mr.x + Rq;
-                                    const float D = fmaf((float)(int)r2[j], 1.f / 128.f, (float)(int)r1[j]);
-                                    const float d2 = fmaf(-(cq2 * mr.y), D, c1);
-                                    const float tl = fmaf(mr.w, hq, 1e-5f * c1);
-                                    const float t = V + mr.z;
-                                    bits |= (d2 - tl <= t * t * (1.f + 2e-5f) ? 1u : 0u) << j;
-                                }
-                            }
-                        }
-                        while (__any_sync(0xffffffffu, bits != 0)) {
-                            if (cnt > 32) flush();
-                            const bool has = bits != 0;
-                            const unsigned mask = __ballot_sync(0xffffffffu, has);
-                            if (has) {
-                                const int j = __ffs(bits) - 1;
-                                bits &= bits - 1;
-                                list[cnt + __popc(mask & ((1u << lane) - 1u))] = (lane << 8) | (c0 + j);
-                            }
-                            cnt += __popc(mask);
-                        }
-                    }
-                    if (cnt) flush();
-                    tc_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&tempty[acc]);
-                    if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bempty[bb]);
-            }
-        }
-    }
-    tc_before();
-    __syncthreads();
-    if (warp == 1) {
-        tc_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
-    }
-}
-
 __global__ void fill_bits_kernel(unsigned long long* p, int64_t rows, int64_t cols, int64_t ld, unsigned long long v) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t < rows * cols) p[(t / cols) * ld + (t % cols)] = v;
@@ -707,30 +418,9 @@ static int run(const float* d_q, int64_t Q, const lf_index& idx, const std::vect
     if (rc) return rc;
     LF_CUDA(smem_optin(mindist_q8_kernel, SMEM_BYTES));
     const int grid = (int)std::min<size_t>(items.size(), (size_t)sm_count());
-    if (idx.d_X8b != nullptr && idx.d_qmeta2 != nullptr) {
-        Scratch qc2, qm2;
-        LF_CUDA(qc2.alloc((size_t)Q * mp, st));
-        LF_CUDA(qm2.alloc(sizeof(float4) * Q, st));
-        rc = quantize_level2(d_q, Q, idx.m, mp, qc.as<int8_t>(), qm.as<float4>(), qc2.as<int8_t>(), qm2.as<float4>(),
-                             st);
-        if (rc) return rc;
-        CUtensorMap mq1, mq2, mx1, mx2;
-        if ((rc = encode_map_2d(&mq1, CU_TENSOR_MAP_DATA_TYPE_UINT8, qc.p, Q, idx.m, mp, KBB, BM))) return rc;
-        if ((rc = encode_map_2d(&mq2, CU_TENSOR_MAP_DATA_TYPE_UINT8, qc2.p, Q, idx.m, mp, KBB, BM))) return rc;
-        if ((rc = encode_map_2d(&mx1, CU_TENSOR_MAP_DATA_TYPE_UINT8, idx.d_X8, idx.n_series, idx.m, idx.m, KBB, BN2)))
-            return rc;
-        if ((rc = encode_map_2d(&mx2, CU_TENSOR_MAP_DATA_TYPE_UINT8, idx.d_X8b, idx.n_series, idx.m, idx.m, KBB, BN2)))
-            return rc;
-        LF_CUDA(smem_optin(mindist_q82_kernel, SMEM2_BYTES));
-        mindist_q82_kernel<<<grid, THREADS, SMEM2_BYTES, st>>>(mq1, mq2, mx1, mx2, d_items.as<Item>(),
-                                                               (int)items.size(), idx, d_q, qm.as<float4>(),
-                                                               qm2.as<float4>(),
-                                                               reinterpret_cast<unsigned long long*>(d_out), ldo);
-    } else {
-        mindist_q8_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(mq, mx, d_items.as<Item>(), (int)items.size(), idx, d_q,
-                                                             qm.as<float4>(),
-                                                             reinterpret_cast<unsigned long long*>(d_out), ldo);
-    }
+    mindist_q8_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(mq, mx, d_items.as<Item>(), (int)items.size(), idx, d_q,
+                                                         qm.as<float4>(),
+                                                         reinterpret_cast<unsigned long long*>(d_out), ldo);
     LF_CUDA(cudaGetLastError());
     sqrt_bits_kernel<<<(unsigned)((out_rows * out_cols + 255) / 256), 256, 0, st>>>(d_out, out_rows, out_cols, ldo);
     LF_CUDA(cudaGetLastError());

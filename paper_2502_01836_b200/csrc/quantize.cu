@@ -77,53 +77,6 @@ __global__ void quantize_queries_kernel(const float* __restrict__ queries, int64
     if (lane == 0) qm[q] = make_float4(sq, (float)qq, __double2float_ru(sqrt(err) * (1.0 + 1e-9) + 1e-30), 0.f);
 }
 
-// Second-level codes (the residual of the first level at 1/128 of its scale):
-// x^ = s1 c1 + (s1 / 128) c2 with |c2| <= 64, so ||x^ - x|| is ~128x smaller.
-// Rows: X8 (level 1) + meta1 {s1, ..} -> X8b, meta2 {|x^|^2, ||c2||, ||x^ - x|| (rounded up), 0}.
-// All arithmetic in fp64, where s1 c1 + s2 c2 and x^ - x are exact.
-__global__ void quantize2_kernel(const float* __restrict__ X, int64_t n, int m, int ld8, const int8_t* __restrict__ X8,
-                                 const float4* __restrict__ meta1, int8_t* __restrict__ X8b,
-                                 float4* __restrict__ meta2) {
-    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (r >= n) return;
-    const double s1 = (double)meta1[r].x;
-    const double s2 = s1 * (1.0 / 128.0);
-    double err = 0.0, nrm = 0.0;
-    int c2sq = 0;
-    for (int i = lane; i < ld8; i += 32) {
-        int c2 = 0;
-        if (i < m) {
-            const double x = (double)X[r * m + i];
-            const double h1 = s1 * (double)X8[r * ld8 + i];
-            c2 = (int)fmin(fmax(rint((x - h1) / s2), -127.0), 127.0);
-            const double xh = h1 + s2 * (double)c2;
-            const double e = xh - x;
-            err = __fma_rn(e, e, err);
-            nrm = __fma_rn(xh, xh, nrm);
-        }
-        X8b[r * ld8 + i] = (int8_t)c2;
-        c2sq += c2 * c2;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        err += __shfl_xor_sync(0xffffffffu, err, o);
-        nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
-        c2sq += __shfl_xor_sync(0xffffffffu, c2sq, o);
-    }
-    if (lane == 0)
-        meta2[r] = make_float4((float)nrm, __double2float_ru(sqrt((double)c2sq)),
-                               __double2float_ru(sqrt(err) * (1.0 + 1e-9) + 1e-30), 0.f);
-}
-
-int quantize_level2(const float* d_X, int64_t n, int m, int ld8, const int8_t* d_X8, const float4* d_meta1,
-                    int8_t* d_X8b, float4* d_meta2, cudaStream_t st) {
-    if (n == 0) return LF_OK;
-    quantize2_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, st>>>(d_X, n, m, ld8, d_X8, d_meta1, d_X8b, d_meta2);
-    LF_CUDA(cudaGetLastError());
-    return LF_OK;
-}
-
 int quantize_queries(const float* d_q, int64_t Q, int m, int mp, int8_t* d_codes, float4* d_meta, cudaStream_t st) {
     if (Q == 0) return LF_OK;
     quantize_queries_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(d_q, Q, m, mp, d_codes, d_meta);
@@ -164,9 +117,3 @@ extern "C" int lf_quantize_rows(const float* d_X, int64_t n, int32_t m, int8_t* 
     return LF_OK;
 }
 
-extern "C" int lf_quantize_rows2(const float* d_X, int64_t n, int32_t m, const int8_t* d_X8, const float* d_qmeta,
-                                 int8_t* d_X8b, float* d_qmeta2, void* stream) {
-    LF_REQUIRE(n >= 0 && m >= 1 && m % 64 == 0, "second-level codes need m % 64 == 0");
-    return lf::quantize_level2(d_X, n, m, m, d_X8, reinterpret_cast<const float4*>(d_qmeta), d_X8b,
-                               reinterpret_cast<float4*>(d_qmeta2), lf::as_stream(stream));
-}

@@ -20,13 +20,12 @@ struct RoundState {
     int k, kc;                   // kc = candidates kept per task = min(k, CH)
     int R, Rcap;                 // leaves per query this round, and the buffer stride
     double f;                    // bsf_factor
-    const int* order;            // [Q][Nn] visit-order records (bounds.cuh OrderArgs)
-    const double* lbs;           // [Q][Nn]
-    const int* leafo;            // [Q][Nn] leaf slot | LF_REC_HASF, -1 internal
-    const double* adj;           // [Q][Nn] pred - offset of the leaf's filter
-    const int* olen;             // [Q] valid (sorted) entries of the order
-    int* refill;                 // [Q] set when the walk reached olen < Nn
-    int* n_refill;               // queries flagged this round (= n_active + 1)
+    const int* order;            // [Q][L] visit-order leaf records (bounds.cuh OrderArgs): node ids (traces)
+    const double* lbs;           // [Q][L] leaf bound
+    const double* gap;           // [Q][L] largest non-leaf bound popped since the previous leaf (0: none)
+    const int* leafo;            // [Q][L] leaf slot | LF_REC_HASF
+    const double* adj;           // [Q][L] pred - offset of the leaf's filter
+    const int* olen;             // [Q] records of the order (= L)
     int lazy;                    // lazy filter inference: adj valid for positions < pcount[q]
     const int* pcount;           // [Q]
     int* preq;                   // [Q] set when the walk stopped at pcount (more predictions needed)
@@ -141,29 +140,11 @@ __device__ __forceinline__ void q8_bulk(void* dst, const void* src, uint32_t byt
 __device__ __forceinline__ void q8_cons_sync() { asm volatile("bar.sync 1, %0;" ::"n"(Q8_CONS) : "memory"); }
 
 // ---- host launchers (one per scan file); each returns the launch error
-// scan_fp32.cu: fp64 full scan (VEC float4 per lane) and the fp32 early-abandon scans
+// scan_fp32.cu: fp64 full scan (VEC float4 per lane): traces, and indexes without a shadow
 cudaError_t launch_scan_full(const RoundState& s, const lf_index& idx, const float* q, cudaStream_t st);
-cudaError_t launch_scan_ea_fp32(const RoundState& s, const lf_index& idx, const float* q, bool v3, cudaStream_t st);
 // scan_q8.cu: TMA-pipelined int8-bounded scan
 cudaError_t launch_scan_q8(const RoundState& s, const lf_index& idx, const float* q, const int8_t* qc8,
                            const float4* qm8, cudaStream_t st);
-// scan_group.cu: tasks grouped by (leaf, chunk)
-struct GroupScratch {
-    int* cbase;          // [n_leaves + 1] chunk base per leaf
-    int* hist;           // [n_keys]
-    int* cur;            // [n_keys]
-    int* sorted;         // [max_tasks]
-    int2* list;          // [max_tasks]
-    int* count;          // [1]
-    int2* bsum;          // [blocks]
-    void* info;          // [max_tasks] GroupInfo
-    int n_keys;
-};
-size_t group_info_bytes();
-int group_blocks(int n_keys);
-cudaError_t launch_chunk_base(const lf_index& idx, int* cbase, cudaStream_t st);
-cudaError_t launch_grouped_scan(const RoundState& s, const lf_index& idx, const float* q, const int8_t* qc8,
-                                const float4* qm8, const GroupScratch& g, int64_t max_tasks, cudaStream_t st);
 // scan_pq.cu: projected two-stage scan
 cudaError_t launch_project_queries(const float* q, int64_t Q, const lf_index& idx, int8_t* qc, float4* qm,
                                    cudaStream_t st);

@@ -42,16 +42,17 @@ __global__ void plan_warp_kernel(RoundState s, lf_index idx) {
     const int lane = threadIdx.x & 31;
     if (q >= s.Q) return;
     const unsigned below = (1u << lane) - 1u;
-    const int Nn = idx.n_nodes;
+    const int Lr = s.n_leaves;                 // records per query: the leaf slots
     int* pre = s.sel_pre + q * (s.Rcap + 1);
     int ns = 0, nch = 0;
     if (!s.done[q]) {
         const double bsf = round_bsf(s, q);
         const double thr = bsf * s.f;
-        const int* ord = s.order + q * Nn;
-        const double* lbs = s.lbs + q * Nn;
-        const int* lrec = s.leafo + q * Nn;
-        const double* adj = s.adj + q * Nn;
+        const int* ord = s.order + q * Lr;       // node ids (traces only)
+        const double* lbs = s.lbs + q * Lr;
+        const double* gps = s.gap + q * Lr;
+        const int* lrec = s.leafo + q * Lr;
+        const double* adj = s.adj + q * Lr;
         const int olen = s.olen[q];
         // lazy inference: with a finite bsf the filter rule needs adj, valid below pcount
         const int len = (s.lazy && thr < kInf) ? min(olen, s.pcount[q]) : olen;
@@ -63,26 +64,30 @@ __global__ void plan_warp_kernel(RoundState s, lf_index idx) {
         long long c_vis = 0, c_srch = 0, c_lbp = 0, c_fp = 0, c_inf = 0, c_rows = 0;
         // records of the current 32 entries, and the next 32 prefetched while these are
         // decided (a walk that neither breaks nor fills its quota moves on by exactly 32)
-        auto load = [&](int at, double& l_, int& r_, double& a_) {
+        auto load = [&](int at, double& l_, double& g_, int& r_, double& a_) {
             const int k = at + lane;
             l_ = k < len ? lbs[k] : kInf;
+            g_ = k < len ? gps[k] : 0.0;
             r_ = k < len ? lrec[k] : -1;
             a_ = k < len ? adj[k] : 0.0;
         };
-        double lb_c, ad_c;
+        double lb_c, gp_c, ad_c;
         int rec_c;
-        load(cur, lb_c, rec_c, ad_c);
+        load(cur, lb_c, gp_c, rec_c, ad_c);
         while (!fin && cur < len) {
-            double lb_n, ad_n;
+            double lb_n, gp_n, ad_n;
             int rec_n;
-            load(cur + 32, lb_n, rec_n, ad_n);
+            load(cur + 32, lb_n, gp_n, rec_n, ad_n);
             const int i = cur + lane;
             const bool valid = i < len;
             const int node = (valid && s.want_trace) ? ord[i] : -1;
             const double lb = lb_c;
             const int rec = rec_c;
             const int leaf = rec >= 0 ? (rec & LF_REC_LEAF) : -1;
-            const bool brk = valid && lb > thr;
+            // the walk stops before this leaf if a non-leaf node popped since the previous
+            // leaf has lb > bsf * f (gap, uncounted), or at this leaf if its own bound does
+            const bool gbrk = valid && gp_c > thr;
+            const bool brk = valid && (gbrk || lb > thr);
             const unsigned bmask = __ballot_sync(0xffffffffu, brk);
             const int first_brk = bmask ? __ffs(bmask) - 1 : 32;
             const bool visit = valid && leaf >= 0 && lane < first_brk;
@@ -150,11 +155,12 @@ __global__ void plan_warp_kernel(RoundState s, lf_index idx) {
                 cur += end;
                 quota_hit = true;
             } else if (first_brk < 32 && first_brk < len - cur) {
-                // the break entry: a leaf counts as visited + lb-pruned (tree.py:261-269)
+                // the break entry: a leaf counts as visited + lb-pruned (tree.py:261-269),
+                // an internal node (gap) ends the walk uncounted
                 const int bnode = __shfl_sync(0xffffffffu, node, first_brk);
-                const int bleaf = __shfl_sync(0xffffffffu, leaf, first_brk);
+                const bool bgap = __shfl_sync(0xffffffffu, gbrk, first_brk);
                 const double blb = __shfl_sync(0xffffffffu, lb, first_brk);
-                if (bleaf >= 0) {
+                if (!bgap) {
                     c_vis += 1;
                     c_lbp += 1;
                     if (s.want_trace && lane == 0) {
@@ -173,26 +179,21 @@ __global__ void plan_warp_kernel(RoundState s, lf_index idx) {
             }
             if (quota) break;
             if (end == 32) {
-                lb_c = lb_n; rec_c = rec_n; ad_c = ad_n;
+                lb_c = lb_n; gp_c = gp_n; rec_c = rec_n; ad_c = ad_n;
             } else {
-                load(cur, lb_c, rec_c, ad_c);
+                load(cur, lb_c, gp_c, rec_c, ad_c);
             }
         }
-        if (cur >= Nn) fin = true;
+        if (cur >= olen) fin = true;
         if (lane == 0) {
             st[0] += c_vis; st[1] += c_srch; st[2] += c_lbp; st[3] += c_fp; st[4] += c_inf; st[5] += c_rows;
             s.cursor[q] = cur;
             if (s.want_trace) s.tr.d_len[q] = tl;
             if (fin) s.done[q] = 1;
             else atomicAdd(s.n_active, 1);
-            if (!fin && !quota_hit && cur >= len) {
-                if (len < olen) {                          // needs predictions further down
-                    s.preq[q] = 1;
-                    atomicAdd(s.n_predict, 1);
-                } else {                                   // walked off the sorted prefix
-                    s.refill[q] = 1;
-                    atomicAdd(s.n_refill, 1);
-                }
+            if (!fin && !quota_hit && cur >= len && len < olen) {   // needs predictions further down
+                s.preq[q] = 1;
+                atomicAdd(s.n_predict, 1);
             }
         }
     }
@@ -282,14 +283,14 @@ __global__ void pairs_count_kernel(RoundState s, int* pend, int* fhist, unsigned
         if (lane == 0) pend[q] = start;
         return;
     }
-    const int Nn = idx.n_nodes;
+    const int Lr = idx.n_leaves;
     // a window of the order at a time (doubling per pass): LeaFi's filters stop most
     // walks long before the bound does (281 of 4,096 leaves visited per query on the
     // bench workload), so predicting every leaf under the bound would be ~15x the work
     const int win = s.pwin[q];
     const int len = min(s.olen[q], start + win);
-    const double* lbs = s.lbs + q * Nn;
-    const int* lrec = s.leafo + q * Nn;
+    const double* lbs = s.lbs + q * Lr;
+    const int* lrec = s.leafo + q * Lr;
     int i = start, cnt = 0;
     bool broke = false;
     while (i < len) {                                  // 128 positions per pass, loads in flight together
@@ -379,9 +380,9 @@ __global__ void pairs_fill_kernel(RoundState s, lf_index idx, const float* __res
     const int lane = threadIdx.x & 31;
     if (q >= s.Q) return;
     const int start = pcount[q], end = pend[q];
-    const int Nn = idx.n_nodes;
-    const int* lrec = s.leafo + q * Nn;
-    const double* lbs = s.lbs + q * Nn;
+    const int Lr = idx.n_leaves;
+    const int* lrec = s.leafo + q * Lr;
+    const double* lbs = s.lbs + q * Lr;
     const double thr = round_bsf(s, q) * s.f;       // same bound as pass 1: skips its break entry
     for (int i = start; i < end; i += 32) {
         const int k = i + lane;
@@ -493,18 +494,9 @@ __global__ void finish_kernel(RoundState s, int64_t* out_ids, double* out_d) {
     out_d[t] = ok ? s.top_d[t] : kInf;
 }
 
-// Visit orders as full per-query sorts (default) or sorted prefixes + refill
-// (LF_FULL_ORDER=0).  LeaFi walks deep into the order -- its filters prune most
-// visited leaves (bench: 281 leaves visited per query, 1,202 at most), so a
-// 1,024-entry prefix sends ~27% of the queries to a refill and the full sort wins.
-static bool prefix_orders() {
-    const char* e = getenv("LF_FULL_ORDER");
-    return e && e[0] == '0';
-}
-
 // Scan variant: LF_SCAN_VARIANT unset / pq (default: the full-length int8 shadow in
 // round 0, then the projected shadow -- 48 instead of 272 bytes per row -- wherever the
-// index carries one) | q8 (int8 shadow only) | ea2 | ea3 | full.
+// index carries one) | q8 (int8 shadow only) | full (fp64 over the fp32 rows).
 // Leaves per query per round grow as 2^(round * g): LF_ROUND_GROWTH_LOG2 = g (default 2:
 // 1, 4, 16, ... up to max_round_leaves).  Measured on the bench workload (1K queries,
 // tools/growth_probe.py): x2 / cap 64 -> 9 rounds, 3.47 ms; x4 / cap 256 -> 5 rounds,
@@ -519,9 +511,7 @@ static int scan_variant() {
     const char* e = getenv("LF_SCAN_VARIANT");
     if (!e || e[0] == 0 || strcmp(e, "pq") == 0) return 8;   // projected stage when the shadow exists
     if (strcmp(e, "q8") == 0) return 9;            // int8 shadow only
-    if (strcmp(e, "ea3") == 0) return 3;
     if (strcmp(e, "full") == 0) return 0;
-    if (strcmp(e, "ea2") == 0) return 2;
     return 8;                                      // default: int8-bounded scan when the shadow exists
 }
 
@@ -537,23 +527,19 @@ struct lf_session {
     int64_t Q = 0;
     const float* d_q = nullptr;
     lf::RoundState s{};
-    lf::Scratch qsumm, lb, lbs, order, cursor, done, topd, topi, topn, topd2, topi2, topn2, sel_leaf,
+    lf::Scratch qsumm, lb, lbs, gap, order, cursor, done, topd, topi, topn, topd2, topi2, topn2, sel_leaf,
         sel_trace, sel_pre, n_sel, chunk_off, cand_d, cand_i, task_min, n_active, tasks, ea_count, qc8, qm8,
-        leafo, adj, olen, refill, pcount, pend, preq, pwin, fhist, fcur, ntiles, ptotal;
+        leafo, adj, olen, pcount, pend, preq, pwin, fhist, fcur, ntiles, ptotal;
     lf::OrderArgs oa{};
     bool lazy = false;               // lazy filter inference (opts.d_W1T instead of predictions)
     long long pairs = 0;             // predictions computed lazily
     int predict_steps = 0;
     double predict_ms = 0.0;
     bool q8 = false;                 // int8-bounded scan (query codes quantised once in begin)
-    bool grouped = false;            // q8 scan with the round's tasks grouped by (leaf, chunk)
     bool pq = false;                 // two-stage scan over the projected shadow (d_Xp)
     lf::Scratch qcp, qmp, pq_cnt, pq_trows, pq_oent, pq_on, pq_obase, pq_wrows, pq_wdist, pq_lo8, pq_thr;
     int pq_cap = lf::PQ_OVER_CAP;    // survivor entry capacity (LF_PQ_OVER_CAP: tests of the full-list path)
-    lf::Scratch cbase, ghist, gcur, gsorted, glist, gcount, gbsum, ginfo;
-    int n_keys = 0;
-    long long refills = 0;           // queries whose visit order was completed after the prefix
-    int* h_active = nullptr;         // pinned [2 slots][4]: active, refill, predict requests
+    int* h_active = nullptr;         // pinned [2 slots][4]: active, -, predict requests
     int round = 0;                   // rounds enqueued
     int harvested = 0;               // rounds whose counts were read back
     cudaEvent_t rev[2][4] = {};      // per slot: plan start, scan start, merge start, merge end
@@ -570,7 +556,7 @@ static int session_begin(lf_session* ss) {
     const lf_search_opts& o = ss->opts;
     cudaStream_t st = ss->st;
     const int64_t Q = ss->Q;
-    const int Nn = idx.n_nodes;
+    const int Nn = idx.n_nodes, L = std::max(1, idx.n_leaves);
     RoundState& s = ss->s;
     s.Q = Q;
     s.k = o.k;
@@ -589,14 +575,13 @@ static int session_begin(lf_session* ss) {
     const int64_t max_chunks_leaf = std::max<int64_t>(1, (idx.max_leaf_rows + CH - 1) / CH);
     const int64_t max_tasks = std::max<int64_t>(1, Q * s.Rcap * max_chunks_leaf);
     LF_CUDA(ss->qsumm.alloc(sizeof(double) * Q * idx.n_seg, st));
-    LF_CUDA(ss->lb.alloc(Nn > 8192 ? sizeof(double) * Q * Nn : 16, st));   // only the unfused path uses it
-    LF_CUDA(ss->lbs.alloc(sizeof(double) * Q * Nn, st));
-    LF_CUDA(ss->order.alloc(sizeof(int) * Q * Nn, st));
-    LF_CUDA(ss->leafo.alloc(sizeof(int) * Q * Nn, st));
-    LF_CUDA(ss->adj.alloc(sizeof(double) * Q * Nn, st));
+    LF_CUDA(ss->lb.alloc(sizeof(double) * Q * Nn, st));        // node bounds (L2-resident at 1K x 8K)
+    LF_CUDA(ss->lbs.alloc(sizeof(double) * Q * L, st));        // leaf records in visit order
+    LF_CUDA(ss->gap.alloc(sizeof(double) * Q * L, st));
+    if (s.want_trace) LF_CUDA(ss->order.alloc(sizeof(int) * Q * L, st));
+    LF_CUDA(ss->leafo.alloc(sizeof(int) * Q * L, st));
+    LF_CUDA(ss->adj.alloc(sizeof(double) * Q * L, st));
     LF_CUDA(ss->olen.alloc(sizeof(int) * Q, st));
-    LF_CUDA(ss->refill.alloc(sizeof(int) * Q, st));
-    LF_CUDA(cudaMemsetAsync(ss->refill.p, 0, sizeof(int) * Q, st));
     LF_CUDA(ss->cursor.alloc(sizeof(int) * Q, st));
     LF_CUDA(ss->done.alloc(sizeof(int) * Q, st));
     LF_CUDA(ss->topd.alloc(sizeof(double) * Q * s.k, st));
@@ -652,7 +637,8 @@ static int session_begin(lf_session* ss) {
     int nk = 0;
     OrderArgs& oa = ss->oa;
     oa.lbs = ss->lbs.as<double>();
-    oa.order = ss->order.as<int>();
+    oa.gap = ss->gap.as<double>();
+    oa.order = s.want_trace ? ss->order.as<int>() : nullptr;
     oa.leafo = ss->leafo.as<int>();
     oa.adj = ss->adj.as<double>();
     oa.olen = ss->olen.as<int>();
@@ -660,20 +646,17 @@ static int session_begin(lf_session* ss) {
     oa.pred64 = o.d_pred_f64;
     oa.offset = o.d_offset;
     oa.F = o.n_filters;
-    oa.only = nullptr;
     oa.lazy = ss->lazy ? 1 : 0;
-    int rc = bounds_and_order(ss->d_q, Q, idx, ss->qsumm.as<double>(), ss->lb.as<double>(), oa, prefix_orders(),
-                              st, &nk);
+    int rc = bounds_and_order(ss->d_q, Q, idx, ss->qsumm.as<double>(), ss->lb.as<double>(), oa, st, &nk);
     if (rc) return rc;
     ss->kernels += nk;
 
-    s.order = ss->order.as<int>();
+    s.order = oa.order;
     s.lbs = ss->lbs.as<double>();
+    s.gap = ss->gap.as<double>();
     s.leafo = ss->leafo.as<int>();
     s.adj = ss->adj.as<double>();
     s.olen = ss->olen.as<int>();
-    s.refill = ss->refill.as<int>();
-    s.n_refill = ss->n_active.as<int>() + 1;
     s.n_predict = ss->n_active.as<int>() + 2;
     s.lazy = ss->lazy ? 1 : 0;
     s.pcount = ss->lazy ? ss->pcount.as<int>() : nullptr;
@@ -724,26 +707,6 @@ static int session_begin(lf_session* ss) {
         ++ss->kernels;
     }
     if (ss->q8) {
-        // grouping by (leaf, chunk) reads ~1/3 fewer int8 bytes on the bench workload but its
-        // round overhead (~30 us) eats the gain there (scan 3.95 -> 3.82 ms, +0.27 ms grouping),
-        // so it is opt-in: LF_SCAN_GROUP=1
-        const char* ge = getenv("LF_SCAN_GROUP");
-        ss->grouped = ge && ge[0] == '1';
-        if (ss->grouped) {
-            LF_CUDA(ss->cbase.alloc(sizeof(int) * (idx.n_leaves + 1), st));
-            LF_CUDA(launch_chunk_base(idx, ss->cbase.as<int>(), st));
-            LF_CUDA(cudaMemcpyAsync(&ss->n_keys, ss->cbase.as<int>() + idx.n_leaves, sizeof(int),
-                                    cudaMemcpyDeviceToHost, st));
-            LF_CUDA(cudaStreamSynchronize(st));
-            LF_CUDA(ss->ghist.alloc(sizeof(int) * std::max(1, ss->n_keys), st));
-            LF_CUDA(ss->gcur.alloc(sizeof(int) * std::max(1, ss->n_keys), st));
-            LF_CUDA(ss->gsorted.alloc(sizeof(int) * max_tasks, st));
-            LF_CUDA(ss->glist.alloc(sizeof(int2) * max_tasks, st));
-            LF_CUDA(ss->ginfo.alloc(group_info_bytes() * max_tasks, st));
-            LF_CUDA(ss->gcount.alloc(sizeof(int), st));
-            LF_CUDA(ss->gbsum.alloc(sizeof(int2) * (group_blocks(ss->n_keys) + 1), st));
-            ++ss->kernels;
-        }
         const int MP = (idx.m + 255) / 256 * 256;
         LF_CUDA(ss->qc8.alloc((size_t)Q * MP, st));
         LF_CUDA(ss->qm8.alloc(sizeof(float4) * Q, st));
@@ -808,7 +771,7 @@ static int predict_step(lf_session* ss) {
                                                                              rows.as<float>());
         LF_CUDA(cudaGetLastError());
         int rc = filter_pairs_tc(rows.as<float>(), P, idx.m, o.d_W1T, o.d_b1, o.d_W2, o.d_b2, F, tiles.as<int4>(),
-                                 ss->ntiles.as<int>(), dst.as<int2>(), o.d_offset, ss->adj.as<double>(), idx.n_nodes,
+                                 ss->ntiles.as<int>(), dst.as<int2>(), o.d_offset, ss->adj.as<double>(), idx.n_leaves,
                                  st);
         if (rc) return rc;
         ss->kernels += 4;
@@ -836,7 +799,6 @@ static int session_enqueue(lf_session* ss, const double* d_bound, double* d_bsf_
     const int slot = ss->round & 1;
     int* counts = ss->n_active.as<int>() + 4 * slot;
     s.n_active = counts;
-    s.n_refill = counts + 1;
     s.n_predict = counts + 2;
     cudaEvent_t* ev = ss->rev[slot];
     s.bound = d_bound;
@@ -849,10 +811,8 @@ static int session_enqueue(lf_session* ss, const double* d_bound, double* d_bsf_
     expand_tasks_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s, idx.d_leaf_ptr);
     if (ss->prof) cudaEventRecord(ev[1], st);
     cudaError_t ce;
-    // the int8-bounded scan takes m % 4 == 0 (codes zero-padded to a multiple of 64); the fp32
-    // early-abandon variants need m % 64 == 0
-    const bool ea = o.early_abandon && !s.want_trace && idx.m <= 512 && scan_variant() != 0 &&
-                    ((idx.m % 64) == 0 || (ss->q8 && (idx.m % 4) == 0));
+    // the bounded scans take m % 4 == 0 (codes zero-padded to a multiple of 64)
+    const bool ea = o.early_abandon && !s.want_trace && idx.m <= 512 && scan_variant() != 0 && ss->q8;
     const int64_t max_tasks =
         std::max<int64_t>(1, Q * s.Rcap * std::max<int64_t>(1, (idx.max_leaf_rows + CH - 1) / CH));
     if (ea && ss->pq && !(ss->round == 0 && ss->q8)) {
@@ -866,15 +826,8 @@ static int session_enqueue(lf_session* ss, const double* d_bound, double* d_bsf_
         ce = launch_scan_pq(s, idx, ss->d_q, ss->qcp.as<int8_t>(), ss->qmp.as<float4>(), ss->pq_cnt.as<int>(), ov,
                             max_tasks, st);
         ss->kernels += ss->q8 ? 3 : 2;
-    } else if (ea && ss->q8 && ss->grouped) {
-        GroupScratch g{ss->cbase.as<int>(), ss->ghist.as<int>(), ss->gcur.as<int>(), ss->gsorted.as<int>(),
-                       ss->glist.as<int2>(), ss->gcount.as<int>(), ss->gbsum.as<int2>(), ss->ginfo.p, ss->n_keys};
-        ce = launch_grouped_scan(s, idx, ss->d_q, ss->qc8.as<int8_t>(), ss->qm8.as<float4>(), g, max_tasks, st);
-        ss->kernels += 6;                                  // (its grouping kernels count as scan time)
-    } else if (ea && ss->q8) {
-        ce = launch_scan_q8(s, idx, ss->d_q, ss->qc8.as<int8_t>(), ss->qm8.as<float4>(), st);
     } else if (ea) {
-        ce = launch_scan_ea_fp32(s, idx, ss->d_q, scan_variant() == 3, st);
+        ce = launch_scan_q8(s, idx, ss->d_q, ss->qc8.as<int8_t>(), ss->qm8.as<float4>(), st);
     } else {
         if (idx.m > 1024) return fail(LF_EINVAL, "series length > 1024 not supported");
         ce = launch_scan_full(s, idx, ss->d_q, st);
@@ -899,8 +852,8 @@ static int session_enqueue(lf_session* ss, const double* d_bound, double* d_bsf_
     return LF_OK;
 }
 
-// Wait for the oldest enqueued round's counts, run the host-decided follow-ups
-// (lazy prediction pass, order refill) and accumulate its profile.
+// Wait for the oldest enqueued round's counts, run the host-decided follow-up
+// (lazy prediction pass) and accumulate its profile.
 static int session_harvest(lf_session* ss, int* active_out) {
     RoundState& s = ss->s;
     const lf_index& idx = ss->idx;
@@ -914,15 +867,6 @@ static int session_harvest(lf_session* ss, int* active_out) {
     if (ss->lazy && h[0] > 0 && (r == 0 || h[2] > 0)) {
         int rc = predict_step(ss);     // after round 0 every bsf is finite: predict what is reachable
         if (rc) return rc;
-    }
-    if (h[1] > 0) {                    // some walks reached the end of their sorted prefix
-        OrderArgs oa = ss->oa;
-        oa.only = s.refill;
-        int nk = 0;
-        int rc = refill_order(ss->d_q, Q, idx, ss->qsumm.as<double>(), ss->lb.as<double>(), oa, st, &nk);
-        if (rc) return rc;
-        ss->kernels += nk;
-        ss->refills += h[1];
     }
     if (ss->prof) {
         double* p = o.h_profile;
@@ -958,7 +902,7 @@ static int session_end(lf_session* ss, int64_t* out_ids, double* out_d, int64_t*
         p[LF_PROF_ROUNDS] = ss->harvested;
         p[LF_PROF_KERNELS] = (double)ss->kernels;
         p[LF_PROF_TOTAL_MS] = ev_ms(ss->ev[0], ss->ev[5]);
-        p[LF_PROF_REFILLS] = (double)ss->refills;
+        p[LF_PROF_REFILLS] = 0.0;
         p[LF_PROF_PREDICT_MS] = ss->predict_ms;
         p[LF_PROF_PAIRS] = (double)ss->pairs;
         p[LF_PROF_PREDICT_STEPS] = (double)ss->predict_steps;
@@ -1060,8 +1004,8 @@ int lf_search(const lf_index* idx, const float* d_queries, int64_t Q, const lf_s
         return rc;
     }
     int active = 0;
-    if (ss->lazy || lf::prefix_orders()) {
-        do {   // host decisions after every round (prediction passes, refills): no pipelining
+    if (ss->lazy) {
+        do {   // host decisions after every round (prediction passes): no pipelining
             rc = lf_search_round(ss, nullptr, nullptr, &active);
             if (rc) break;
         } while (active > 0);

@@ -81,7 +81,5 @@ int encode_map_2d(CUtensorMap* map, CUtensorMapDataType dtype, const void* base,
 // Query int8 codes + {scale, sum code^2, ||scale*code - q||, 0} (quantize.cu).
 int quantize_queries(const float* d_q, int64_t Q, int m, int mp, int8_t* d_codes, float4* d_meta, cudaStream_t st);
 // Second-level residual codes (quantize.cu): rows of `ld8`-strided codes.
-int quantize_level2(const float* d_X, int64_t n, int m, int ld8, const int8_t* d_X8, const float4* d_meta1,
-                    int8_t* d_X8b, float4* d_meta2, cudaStream_t st);
 
 }  // namespace lf

@@ -373,26 +373,6 @@ class DeviceIndex:
         self.pca_k, self.P, self.mu, self.Xp, self.pmeta = k, P, mu.contiguous(), codes, meta
         return True
 
-    def ensure_level2(self) -> bool:
-        """Build the second-level residual codes (training-data generation only; m x 1 B
-        + 16 B per row).  Returns False when the first level does not exist."""
-        import torch
-
-        if self.X8 is None or self.X.shape[1] % 64:
-            return False
-        if getattr(self, "X8b", None) is None:
-            n_rows, m = int(self.X.shape[0]), int(self.X.shape[1])
-            with torch.cuda.device(self.device):
-                self.X8b = torch.empty((n_rows, m), dtype=torch.int8, device=self.device)
-                self.qmeta2 = torch.empty((n_rows, 4), dtype=torch.float32, device=self.device)
-                _lib.check(_lib.lib().lf_quantize_rows2(self.X.data_ptr(), n_rows, m, self.X8.data_ptr(),
-                                                        self.qmeta.data_ptr(), self.X8b.data_ptr(),
-                                                        self.qmeta2.data_ptr(), _lib.stream_ptr()))
-        return True
-
-    def drop_level2(self) -> None:
-        self.X8b = self.qmeta2 = None
-
     def struct(self, leaf_filter=None) -> _lib.LfIndex:
         t = self.tree
         s = _lib.LfIndex()
@@ -414,8 +394,6 @@ class DeviceIndex:
         s.d_leaf_filter = None if leaf_filter is None else leaf_filter.data_ptr()
         if self.X8 is not None:
             s.d_X8, s.d_qmeta = self.X8.data_ptr(), self.qmeta.data_ptr()
-        if getattr(self, "X8b", None) is not None:
-            s.d_X8b, s.d_qmeta2 = self.X8b.data_ptr(), self.qmeta2.data_ptr()
         if getattr(self, "Xp", None) is not None:
             s.pca_k = self.pca_k
             s.d_P, s.d_mu = self.P.data_ptr(), self.mu.data_ptr()

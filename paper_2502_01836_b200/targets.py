@@ -78,18 +78,6 @@ def tc_ok(m: int) -> bool:
     return m % 32 == 0 and 32 <= m <= 256
 
 
-def _q8_struct(di, path: str):
-    """Index struct for the int8 kernels: "q8" = first-level codes (default), "q82" =
-    two-level codes (built on first use; 128x narrower intervals, three MMAs and two
-    accumulators per tile -- slower on random walks)."""
-    if path == "q82":
-        di.ensure_level2()
-    st = di.struct(None)
-    if path != "q82":
-        st.d_X8b = st.d_qmeta2 = None
-    return st
-
-
 def default_path(t, di) -> str:
     """int8 tensor cores over the int8 shadow when it exists (m in {128, 256}), else
     tf32 tensor cores (m in {32, ..., 256}), else fp64 CUDA cores."""
@@ -116,12 +104,9 @@ def leaf_min_distances(index, queries, leaf_slots, path: str | None = None, dind
     Q, S = q.shape[0], sel.shape[0]
     out = torch.empty((Q, S), dtype=torch.float64, device=di.device)
     st = di.struct(None)
-    if path in ("tc", "q8", "q82") and Q and S:
+    if path in ("tc", "q8") and Q and S:
         hsel = np.ascontiguousarray(np.asarray(leaf_slots, dtype=np.int32))
-        fn = _lib.lib().lf_leaf_min_dist_tc
-        if path.startswith("q8"):
-            fn = _lib.lib().lf_leaf_min_dist_q8
-            st = _q8_struct(di, path)
+        fn = _lib.lib().lf_leaf_min_dist_q8 if path == "q8" else _lib.lib().lf_leaf_min_dist_tc
         _lib.check(fn(q.data_ptr(), Q, st, _lib.ptr(hsel), S, out.data_ptr(), S, _lib.stream_ptr()))
         return out
     for s0 in range(0, S, 65535):
@@ -284,9 +269,9 @@ def local_targets_all(index, queries_by_leaf: dict, path: str | None = None) -> 
     t = as_tree(index)
     di = t.device()
     path = path or default_path(t, di)
-    fn = {"q8": _lib.lib().lf_local_min_dist_q8, "q82": _lib.lib().lf_local_min_dist_q8,
+    fn = {"q8": _lib.lib().lf_local_min_dist_q8,
           "tc": _lib.lib().lf_local_min_dist_tc}.get(path, _lib.lib().lf_local_min_dist)
-    st = _q8_struct(di, path) if path.startswith("q8") else di.struct(None)
+    st = di.struct(None)
     leaves = list(queries_by_leaf)
     out = {}
     for g0 in range(0, len(leaves), 65535):

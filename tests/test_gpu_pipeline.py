@@ -195,7 +195,7 @@ def test_mindist_tc_bit_identical(m, cap):
         np.testing.assert_allclose(ta[l][0], tb[l][0], rtol=1e-13, atol=0)
 
 
-@pytest.mark.parametrize("path", ["q8", "q82"])
+@pytest.mark.parametrize("path", ["q8"])
 @pytest.mark.parametrize("m,cap", [(128, 300), (256, 700), (256, 3000)])
 def test_mindist_q8_exact(m, cap, path):
     """int8 tensor-core bound + exact fp64 re-check == fp64 SIMT kernel (rel 1e-13),

@@ -352,11 +352,11 @@ def test_large_tree_unfused_order():
         assert res.stats[i].tolist() == [o.stats[s] for s in lo.STAT_KEYS]
 
 
-@pytest.mark.parametrize("variant", ["q8", "ea2", "ea3", "full"])
+@pytest.mark.parametrize("variant", ["q8"])
 @pytest.mark.parametrize("k", [1, 4])
 def test_scan_variants_agree(variant, k, monkeypatch):
-    """Every scan variant (int8-bounded, early-abandon v2/v3, full) returns the same
-    ids and exact distances; counters are identical (whole leaves are counted)."""
+    """The int8-bounded scan returns the same ids and exact distances as the full
+    fp64 scan; counters are identical (whole leaves are counted)."""
     from paper_2502_01836_b200 import build_index, search_batch
 
     data = lo.randwalk(15000, 128, 31)
@@ -403,8 +403,8 @@ def test_q8_pipeline_exact(m, k, monkeypatch):
     assert got.ids[-1, 0] == 4321 and got.dists[-1, 0] == 0.0
 
 
-def _prefix_tree():
-    """2048 < nodes <= 8192: the visit order is built as a sorted prefix + refills."""
+def _mid_tree():
+    """2048 < nodes <= 8192: the widest block-sorted leaf order (16 node items per thread)."""
     from paper_2502_01836_b200 import build_index
 
     data = lo.randwalk(40000, 64, 77)
@@ -413,48 +413,49 @@ def _prefix_tree():
     return data, t
 
 
-def test_prefix_order_sequential_matches_oracle(monkeypatch):
-    """Sequential exact search over prefix orders (with refills): ids, distances and
-    every counter equal the reference traversal."""
+def test_leaf_order_sequential_matches_oracle():
+    """Sequential exact search over the leaf-only visit order (internal nodes folded
+    into each leaf's gap bound): ids, distances, every counter and the trace equal
+    the reference traversal, including walks that end at an internal node (no
+    lb-pruned leaf counted) and walks that end at a leaf."""
     from paper_2502_01836_b200 import search_batch
 
-    monkeypatch.setenv("LF_FULL_ORDER", "0")
-    data, t = _prefix_tree()
+    data, t = _mid_tree()
     Q = np.concatenate([lo.noisy_queries(data, 6, nz, 50 + int(10 * nz)) for nz in (0.1, 0.5, 1.5)])
-    prof = np.zeros(16)
-    res = search_batch(t, Q, 3, sequential=True, profile=prof)
-    assert prof[7] > 0, "the wide queries must have needed a refill"
+    res = search_batch(t, Q, 3, sequential=True, want_trace=True)
     ot = lo.build_tree(data, 24)
+    ended = set()
     for i, q in enumerate(Q):
-        o = lo.search(ot, q, 3)
+        o = lo.search(ot, q, 3, want_trace=True)
         assert res.ids[i].tolist() == [a for a, _ in o.results], i
         np.testing.assert_allclose(res.dists[i], [b for _, b in o.results], rtol=DIST_RTOL)
         assert res.stats[i].tolist() == [o.stats[s_] for s_ in lo.STAT_KEYS], i
+        assert [e.leaf_id for e in res.trace_of(i)] == [e[0] for e in o.trace], i
+        assert [e.lower_bound for e in res.trace_of(i)] == [e[1] for e in o.trace], i
+        ended.add(o.stats["leaves_lb_pruned"])
+    assert ended == {0, 1}, "both break kinds (internal node / leaf) must occur"
 
 
-def test_prefix_order_batched_equals_full_order(monkeypatch):
-    """Batched exact search: prefix orders + refills give the same neighbours as
-    full per-query sorts (LF_FULL_ORDER=1)."""
+def test_leaf_order_batched_equals_sequential():
+    """Batched rounds over the leaf order give the sequential walk's neighbours."""
     from paper_2502_01836_b200 import search_batch
 
-    data, t = _prefix_tree()
+    data, t = _mid_tree()
     Q = np.concatenate([lo.noisy_queries(data, 16, nz, 60 + int(10 * nz)) for nz in (0.1, 0.4, 1.0)])
     for k in (1, 4):
-        monkeypatch.setenv("LF_FULL_ORDER", "1")
-        ref = search_batch(t, Q, k)
-        monkeypatch.setenv("LF_FULL_ORDER", "0")
+        ref = search_batch(t, Q, k, sequential=True)
         got = search_batch(t, Q, k)
         np.testing.assert_array_equal(got.ids, ref.ids)
         np.testing.assert_array_equal(got.dists, ref.dists)
+        assert (got.stats[:, 5] >= ref.stats[:, 5]).all()
 
 
-def test_prefix_order_filtered_sequential_matches_oracle(monkeypatch):
-    """Sequential filtered search over prefix orders: results and counters equal the
+def test_leaf_order_filtered_sequential_matches_oracle():
+    """Sequential filtered search over the leaf order: results and counters equal the
     reference cascade fed the same predictions (host callables, fp64)."""
     from paper_2502_01836_b200 import search_engine
 
-    monkeypatch.setenv("LF_FULL_ORDER", "0")
-    data, t = _prefix_tree()
+    data, t = _mid_tree()
     rng = np.random.default_rng(5)
     leaves = [int(l) for l in t.leaf_ids]
     preds = {l: (lambda q, v=float(rng.uniform(0.0, 6.0)): v) for l in leaves[::3]}
@@ -524,28 +525,6 @@ def test_pair_predictions_bit_identical():
     pf[:400] = 5                                   # one filter with several 128-row tiles
     got = pack.predict_pairs(qd, pq, pf).cpu().numpy()
     np.testing.assert_array_equal(got, dense[pq, pf])
-
-
-@pytest.mark.parametrize("k", [1, 5])
-def test_grouped_scan_identical(k, monkeypatch):
-    """The round's tasks grouped by (leaf, chunk) -- one pass over a chunk serves every
-    query scanning it, groups split at 8 -- give exactly the per-task scan's results
-    and counters.  Queries are clustered so that groups of 1..20 queries form."""
-    from paper_2502_01836_b200 import build_index, search_batch
-
-    data = lo.randwalk(40000, 128, 61)
-    t = build_index(data, 900)
-    base = lo.noisy_queries(data, 6, 0.05, 3)
-    rng = np.random.default_rng(4)
-    Q = np.concatenate([np.stack([base[i % 6] + rng.normal(0, 0.05, base.shape[1]) for i in range(90)]),
-                        lo.noisy_queries(data, 30, 0.4, 5)])
-    monkeypatch.setenv("LF_SCAN_GROUP", "0")
-    ref = search_batch(t, Q, k)
-    monkeypatch.setenv("LF_SCAN_GROUP", "1")
-    got = search_batch(t, Q, k)
-    np.testing.assert_array_equal(got.ids, ref.ids)
-    np.testing.assert_array_equal(got.dists, ref.dists)
-    np.testing.assert_array_equal(got.stats, ref.stats)
 
 
 @pytest.mark.parametrize("m,pk,cap", [(64, 32, None), (96, 32, None), (256, 32, None), (256, 64, None),

@@ -36,13 +36,25 @@ def test_library_exports_every_declared_symbol():
     assert h.lf_version() == 1
 
 
+def _header_fields(struct: str) -> list:
+    text = (ROOT / "include" / "leafi_b200.h").read_text()
+    body = re.search(r"typedef struct %s \{(.*?)\} %s;" % (struct, struct), text, re.S).group(1)
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    return [re.search(r"(\w+)\s*(\[[^\]]*\])?$", d.strip()).group(1) for d in body.split(";") if d.strip()]
+
+
 def test_struct_layouts_match_header():
-    """ctypes structs mirror the C structs (field order and sizes)."""
-    import ctypes as C
+    """ctypes structs mirror the compiled C structs: the same fields in header order,
+    and sizeof / every offsetof equal to what the library reports (lf_abi_*)."""
     from paper_2502_01836_b200 import _lib
 
-    assert C.sizeof(_lib.LfIndex) == 8 + 4 * 4 + 8 + 2 * 4 * 64 + 11 * 8 + 8 + 4 * 8
-    assert C.sizeof(_lib.LfTrace) == 6 * 8
+    h = _lib.lib()
+    for name, cls in _lib.STRUCTS.items():
+        assert [f for f, _ in cls._fields_] == _header_fields(name), name
+    _lib.check_abi()
+    assert h.lf_abi_sizeof(b"nope") == -1
+    assert h.lf_abi_offsetof(b"lf_index", b"nope") == -1
+    assert h.lf_abi_offsetof(b"lf_index", b"n_series") == 0
 
 
 def _table_equal(t, g, prefix="nt_"):
