@@ -197,6 +197,124 @@ def _oracle_worker(qi_list):
     return out
 
 
+def _oracle_exact_worker(qi_list):
+    """Exact search (tree.py:300-302) of the oracle: ids, distances, counters."""
+    from oracle import leafi_oracle as lo
+
+    t, Qh = _OR["tree"], _OR["Q"]
+    out = []
+    for qi in qi_list:
+        o = lo.search(t, Qh[qi], 1)
+        out.append((qi, [a for a, _ in o.results], [d for _, d in o.results], [o.stats[k] for k in lo.STAT_KEYS]))
+    return out
+
+
+def _oracle_injected_worker(qi_list):
+    """The LeaFi cascade of the oracle fed the GPU's own predictions (so any
+    difference is the search, not the filter arithmetic)."""
+    from oracle import leafi_oracle as lo
+
+    t, Qh, P, offs, lids = _OR["tree"], _OR["Q"], _OR["P"], _OR["offs"], _OR["pack_leaves"]
+    out = []
+    for qi in qi_list:
+        preds = {l: (lambda x, v=float(P[qi, j]): v) for j, l in enumerate(lids)}
+        o = lo.search(t, Qh[qi], 1, predictors=preds, offsets=offs)
+        out.append((qi, [a for a, _ in o.results], [d for _, d in o.results], [o.stats[k] for k in lo.STAT_KEYS]))
+    return out
+
+
+def oracle_map(fn, idx, workers: int):
+    import multiprocessing as mp
+
+    chunks = [c for c in (list(idx[i::workers]) for i in range(workers)) if c]
+    with mp.get_context("fork").Pool(len(chunks)) as pool:
+        return sorted((r for part in pool.map(fn, chunks) for r in part), key=lambda r: r[0])
+
+
+def parity_25m(w, workers: int) -> dict:
+    """Parity at the headline configuration (rank 0, after oracle_setup):
+    (1) exact mode, >= 64 queries (16 per noise level): the oracle's exact search
+        (tree.py:300-302) vs the GPU's exact search on the same 25M tree --
+        ids identical, distances within 1e-4 relative (north_star) and, with the
+        sequential schedule, every counter identical;
+    (2) LeaFi cascade: the oracle fed the GPU's own predictions vs the GPU's
+        sequential filtered search -- ids and counters identical;
+    (3) filter arithmetic A/B: the fp32 CUDA-core pack vs the fp16 tensor-core pack
+        on the same trained filters and offsets, all queries: recall, leaves
+        pruned, and the (query, filter) prune decisions against the true 1-NN
+        distance (pred - offset > d*) that agree;
+    (4) training-data generation spot check: exact min distances of sampled
+        (query, leaf) pairs recomputed on the host in fp64."""
+    import torch
+
+    from oracle import leafi_oracle as lo
+    from paper_2502_01836_b200 import search_batch
+    from paper_2502_01836_b200.filters import FilterPack
+
+    tree, eidx, Q, exact, di = w["tree"], w["eidx"], w["Q"], w["exact"], w["di"]
+    nQ = Q.shape[0]
+    per = nQ // len(NOISE_LEVELS)
+    take = max(16, 64 // len(NOISE_LEVELS))
+    idx = np.concatenate([i * per + np.linspace(0, per - 1, take).astype(int) for i in range(len(NOISE_LEVELS))])
+    out = {"queries": int(len(idx)), "sample": f"{take} per noise level, evenly spaced"}
+    # (1) exact mode
+    t0 = time.perf_counter()
+    ores = oracle_map(_oracle_exact_worker, idx, workers)
+    seq = search_batch(tree, Q[idx], 1, sequential=True)
+    oid = np.array([r[1][0] for r in ores])
+    od = np.array([r[2][0] for r in ores])
+    ost = np.array([r[3] for r in ores])
+    rel = np.abs(seq.dists[:, 0] - od) / np.maximum(od, 1e-300)
+    out["exact"] = {"ids_identical": bool((seq.ids[:, 0] == oid).all()),
+                    "batched_ids_identical": bool((exact.ids[idx, 0] == oid).all()),
+                    "max_rel_dist_err": float(rel.max()), "dist_tolerance": 1e-4,
+                    "counters_identical_sequential": bool((seq.stats == ost).all()),
+                    "oracle_s": time.perf_counter() - t0}
+    # (2) LeaFi cascade with identical predictions
+    pack = eidx.pack
+    P = pack.predict(Q)
+    offv = eidx.offset_vector(w["target"], device=True)
+    _OR.update(P=P.cpu().numpy(), pack_leaves=list(pack.leaf_ids))
+    ires = oracle_map(_oracle_injected_worker, idx, workers)
+    fseq = search_batch(tree, Q[idx], 1, predictions=P[torch.as_tensor(idx, device=P.device)], offsets=offv,
+                        leaf_filter=pack.leaf_filter(di), sequential=True)
+    out["leafi_same_predictions"] = {
+        "ids_identical": bool((fseq.ids[:, 0] == np.array([r[1][0] for r in ires])).all()),
+        "counters_identical_sequential": bool((fseq.stats == np.array([r[3] for r in ires])).all())}
+    # (3) fp32 CUDA-core pack vs the fp16 tensor-core pack
+    p32 = FilterPack.from_models(eidx.filters, device=P.device, path="simt")
+    P32 = p32.predict(Q)
+    res16 = search_batch(tree, Q, 1, predictions=P, offsets=offv, leaf_filter=pack.leaf_filter(di))
+    res32 = search_batch(tree, Q, 1, predictions=P32, offsets=offv, leaf_filter=p32.leaf_filter(di))
+    dstar = torch.as_tensor(exact.dists[:, 0], device=P.device)[:, None]
+    off_row = offv[None, :]
+    d16 = (P.double() - off_row) > dstar
+    d32 = (P32.double() - off_row) > dstar
+    diff = (P.double() - P32.double()).abs()
+    out["filter_precision_ab"] = {
+        "recall_fp16_pack": recall_of(res16, exact), "recall_fp32_pack": recall_of(res32, exact),
+        "leaves_pruned_pct_fp16_pack": 100.0 * (1.0 - float(np.mean(res16.stats[:, 1])) / tree.n_leaves),
+        "leaves_pruned_pct_fp32_pack": 100.0 * (1.0 - float(np.mean(res32.stats[:, 1])) / tree.n_leaves),
+        "prune_decisions_agree": float((d16 == d32).double().mean().item()),
+        "prune_decisions": int(d16.numel()),
+        "max_abs_pred_diff": float(diff.max().item()),
+        "max_rel_pred_diff": float((diff / P32.double().abs().clamp_min(1e-30)).max().item()),
+        "definition": "decision per (query, filter): pred - offset > exact 1-NN distance; both packs share "
+                      "the filters and the offsets fitted on the fp16 pack"}
+    del P32, p32
+    # (4) training-data generation spot check
+    if w.get("tdg_sample") is not None:
+        gq, dl, slots = w["tdg_sample"]
+        errs = []
+        for qi, s_ in zip(range(gq.shape[0]), slots):
+            r0, r1 = int(di.leaf_ptr_host[s_]), int(di.leaf_ptr_host[s_ + 1])
+            rows = di.X[r0:r1].cpu().numpy()
+            ref = float(lo.pair_dist(gq[qi:qi + 1], rows).min())
+            errs.append(abs(dl[qi] - ref) / max(ref, 1e-300))
+        out["train_data_gen_spot_check"] = {"pairs": len(errs), "max_rel_err": float(max(errs))}
+    return out
+
+
 def oracle_setup(w) -> None:
     """OracleTree over a host copy of the collection + numpy filter callables."""
     from oracle import leafi_oracle as lo
@@ -420,6 +538,15 @@ def run_ours(args, rank, world, device):
         te1.record(stream)
         torch.cuda.synchronize()
         t_ms = te0.elapsed_time(te1)
+        # member rows as queries: their own leaf's minimum must be exactly 0.0
+        mslots = np.linspace(0, tdi.n_leaves - 1, 16).astype(int)
+        mrows = torch.stack([tdi.X[int(tdi.leaf_ptr_host[s_])] for s_ in mslots]).contiguous()
+        mdl = leaf_min_distances(tree, mrows, slots, dindex=tdi)
+        member_zero = bool((mdl[torch.arange(16), torch.as_tensor(mslots)] == 0.0).all().item())
+        # a sample of (query, leaf) minima for the host fp64 spot check (parity block)
+        samp = np.linspace(0, gq.shape[0] - 1, 8).astype(int)
+        sslots = np.linspace(0, tdi.n_leaves - 1, 8).astype(int)
+        w["tdg_sample"] = (gq[samp].double().cpu().numpy(), dl[samp, sslots].cpu().numpy(), sslots)
         if world > 1:
             tt = torch.tensor([t_ms], dtype=torch.float64, device=device)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -440,7 +567,7 @@ def run_ours(args, rank, world, device):
                "tensor_peak_tops": pk, "peak_source": pk_src,
                "frac_of_peak": flops / (t_ms / 1e3) / 1e12 / pk,
                "path": desc,
-               "exact_zero_check": bool(torch.isfinite(dl).all().item()),
+               "member_rows_exact_zero": member_zero,
                "reference_cpu_pairs_per_s_per_core": "1.0-1.3e6 (BASELINE.md, collect_targets at C1)"}
         del dl, gq
 
@@ -569,6 +696,7 @@ def run_ours(args, rank, world, device):
         idx = np.linspace(0, nQ - 1, n_s).astype(int)
         el, res = oracle_time(idx, workers)
         agree = float(np.mean([chk.ids[qi, 0] == rid for qi, rid, _ in res]))
+        line["parity_25M"] = parity_25m(w, workers)
         line["cpu_baseline"] = {"value": len(idx) / el, "unit": "queries/s", "cores": workers, "kind": "port",
                                 "sample": f"{len(idx)} of the {nQ} benchmark queries (evenly spaced over the 4 noise "
                                           f"levels), oracle/leafi_oracle.search with the same tree, filters and "

@@ -4,7 +4,6 @@
 // bound, np.dot -> one fp64 FMA chain over segments), summarize.py:114-122
 // (batched bound used by traingen, einsum -> sequential sum of (g*g)*w).
 // Both orders are reproduced bit-for-bit so visit orders and counters match.
-#include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 
 #include <algorithm>
@@ -62,19 +61,23 @@ __global__ void lb_kernel(const double* __restrict__ qsumm, int64_t Q, int n_seg
 // lb[q][node] for QT queries x 128 nodes per CTA: each thread holds its node's
 // envelope (n_seg <= 8) in registers and reuses it for QT queries, so the
 // envelopes are read from L2 once per QT queries instead of once per query.
-// Same arithmetic as lb_kernel (bit-identical bounds).
+// Same arithmetic as lb_kernel (bit-identical bounds).  With qmax / qmin set it
+// also records, per query, the range of its leaf bounds as float bits (rounded:
+// the leaf-order kernel only needs it to spread its buckets).
 constexpr int LBT_NODES = 128;
 constexpr int LBT_Q = 16;
 constexpr int LBT_SEG = 8;
 
 template <int MODE>
-__global__ void __launch_bounds__(LBT_NODES) lb_tile_kernel(const double* __restrict__ qsumm, int64_t Q, int ns,
-                                                            lf_index idx, const double* __restrict__ env_min,
-                                                            const double* __restrict__ env_max, int n_env,
-                                                            double* __restrict__ lb) {
+__global__ void __launch_bounds__(LBT_NODES, 4) lb_tile_kernel(const double* __restrict__ qsumm, int64_t Q, int ns,
+                                                               lf_index idx, const double* __restrict__ env_min,
+                                                               const double* __restrict__ env_max, int n_env,
+                                                               double* __restrict__ lb, unsigned* __restrict__ qmax,
+                                                               unsigned* __restrict__ qmin) {
     __shared__ double qs[LBT_Q][LBT_SEG];
     __shared__ double ws[LBT_SEG];
     const int node = blockIdx.x * LBT_NODES + threadIdx.x;
+    const int lane = threadIdx.x & 31;
     const int64_t q0 = (int64_t)blockIdx.y * LBT_Q;
     for (int i = threadIdx.x; i < LBT_Q * ns; i += LBT_NODES) {
         const int qq = i / ns, sg = i - qq * ns;
@@ -82,12 +85,13 @@ __global__ void __launch_bounds__(LBT_NODES) lb_tile_kernel(const double* __rest
     }
     if (threadIdx.x < ns) ws[threadIdx.x] = (double)idx.seg_width[threadIdx.x];
     __syncthreads();
-    if (node >= n_env) return;
+    const bool valid = node < n_env;
+    const bool isl = qmax != nullptr && valid && __ldg(idx.d_node_leaf + node) >= 0;
     double mn[LBT_SEG], mx[LBT_SEG];
 #pragma unroll
     for (int sg = 0; sg < LBT_SEG; ++sg) {
-        mn[sg] = sg < ns ? __ldg(env_min + (int64_t)sg * n_env + node) : 0.0;
-        mx[sg] = sg < ns ? __ldg(env_max + (int64_t)sg * n_env + node) : 0.0;
+        mn[sg] = (valid && sg < ns) ? __ldg(env_min + (int64_t)sg * n_env + node) : 0.0;
+        mx[sg] = (valid && sg < ns) ? __ldg(env_max + (int64_t)sg * n_env + node) : 0.0;
     }
     const int qn = (int)min((int64_t)LBT_Q, Q - q0);
     for (int qq = 0; qq < qn; ++qq) {
@@ -95,20 +99,32 @@ __global__ void __launch_bounds__(LBT_NODES) lb_tile_kernel(const double* __rest
 #pragma unroll
         for (int sg = 0; sg < LBT_SEG; ++sg) {
             if (sg < ns) {
+                // max(mn - q, q - mx, 0) (summarize.py:103-104): mn <= mx, so at most one
+                // of the two differences is positive -- selects instead of fmax
                 const double qv = qs[qq][sg];
-                double g = fmax(mn[sg] - qv, qv - mx[sg]);
-                g = fmax(g, 0.0);
+                const double a = mn[sg] - qv, b = qv - mx[sg];
+                const double g = a > 0.0 ? a : (b > 0.0 ? b : 0.0);
                 if (MODE == 0) acc = __fma_rn(__dmul_rn(ws[sg], g), g, acc);
                 else acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(g, g), ws[sg]));
             }
         }
-        lb[(q0 + qq) * n_env + node] = sqrt(acc);
+        const double v = sqrt(acc);
+        if (valid) lb[(q0 + qq) * n_env + node] = v;
+        if (qmax != nullptr) {
+            const unsigned fb = __float_as_uint((float)v);
+            const unsigned hi = __reduce_max_sync(0xffffffffu, isl ? fb : 0u);
+            const unsigned lo = __reduce_min_sync(0xffffffffu, isl ? fb : 0xffffffffu);
+            if (lane == 0 && lo != 0xffffffffu) {
+                atomicMax(qmax + q0 + qq, hi);
+                atomicMin(qmin + q0 + qq, lo);
+            }
+        }
     }
 }
 
 int launch_bounds(const float* d_q, int64_t Q, const lf_index& idx, const double* env_min,
                   const double* env_max, int n_env, int mode, double* d_qsumm, double* d_lb,
-                  cudaStream_t st) {
+                  cudaStream_t st, unsigned* d_qmax, unsigned* d_qmin) {
     if (Q == 0) return LF_OK;
     {
         int64_t n = Q * idx.n_seg;
@@ -118,11 +134,17 @@ int launch_bounds(const float* d_q, int64_t Q, const lf_index& idx, const double
     }
     if (n_env == 0) return LF_OK;
     if (idx.n_seg <= LBT_SEG && (Q + LBT_Q - 1) / LBT_Q <= 65535) {
+        if (d_qmax != nullptr) {
+            LF_CUDA(cudaMemsetAsync(d_qmax, 0, sizeof(unsigned) * Q, st));
+            LF_CUDA(cudaMemsetAsync(d_qmin, 0xff, sizeof(unsigned) * Q, st));
+        }
         dim3 grid((unsigned)((n_env + LBT_NODES - 1) / LBT_NODES), (unsigned)((Q + LBT_Q - 1) / LBT_Q));
         if (mode == 0)
-            lb_tile_kernel<0><<<grid, LBT_NODES, 0, st>>>(d_qsumm, Q, idx.n_seg, idx, env_min, env_max, n_env, d_lb);
+            lb_tile_kernel<0><<<grid, LBT_NODES, 0, st>>>(d_qsumm, Q, idx.n_seg, idx, env_min, env_max, n_env, d_lb,
+                                                          d_qmax, d_qmin);
         else
-            lb_tile_kernel<1><<<grid, LBT_NODES, 0, st>>>(d_qsumm, Q, idx.n_seg, idx, env_min, env_max, n_env, d_lb);
+            lb_tile_kernel<1><<<grid, LBT_NODES, 0, st>>>(d_qsumm, Q, idx.n_seg, idx, env_min, env_max, n_env, d_lb,
+                                                          d_qmax, d_qmin);
         LF_CUDA(cudaGetLastError());
         return LF_OK;
     }
@@ -187,207 +209,214 @@ __device__ __forceinline__ void put_records(const OrderArgs& o, const lf_index& 
     }
 }
 
-// One CTA per query (trees of <= 8192 nodes, <= 4096 leaf slots): the node
-// bounds come from the L2-resident bound matrix (lb_tile_kernel); the leaves are
-// compacted in node-id order (warp ballots + one scan of the per-(item, warp)
-// counts), sorted by a 16-bit key -- floor(lb * 65000 / max lb), monotone in lb --
-// with a stable block radix sort (4 passes), and runs of equal keys are put in
-// exact (lb, node id) order by insertion sort (compact index order is node id
-// order, so the stable sort leaves each run nearly sorted).  Every non-leaf node
-// then finds by binary search the first leaf after it in (lb, id) order and
-// raises that leaf's gap bound to its own (atomicMax on the bits: bounds are
-// non-negative doubles).
+// One CTA per query (trees of <= 8192 nodes, <= 4096 leaf slots); the node
+// bounds come from the L2-resident bound matrix and the range of the query's
+// leaf bounds from lb_tile_kernel.  A counting sort:
+//   1. every leaf is staged in shared memory (warp-aggregated slots, any order)
+//      and counted in bucket floor((lb - lo) * (NB - 1) / (hi - lo)) -- a map
+//      monotone in lb, so every leaf of a lower bucket precedes every leaf of a
+//      higher one in (lb, id) order;
+//   2. one scan of the counts, an atomic scatter into the buckets;
+//   3. each bucket (about one leaf on average) is put in exact (lb, node id)
+//      order: insertion sort, or -- buckets of more than LO_BIG leaves, bounds
+//      clustered far below their spread -- a warp computes every element's rank
+//      (pairs (lb, id) are distinct, so ranks are a permutation);
+//   4. every non-leaf node finds the first leaf after it in (lb, id) order inside
+//      its own bucket (or at the next bucket's start) and raises that leaf's gap
+//      bound to its own bound (atomicMax on the bits: bounds are non-negative).
+// Global round trips: one for the leaves' bounds, one for the non-leaves', and
+// the record gathers.
 constexpr int LO_THREADS = 512;
 constexpr int LO_WARPS = LO_THREADS / 32;
 constexpr int LO_LEAF_ITEMS = 8;
 constexpr int LO_MAX_LEAVES = LO_THREADS * LO_LEAF_ITEMS;
 constexpr int LO_MAX_NI = 16;                            // node items per thread: <= 8192 nodes
-constexpr double LO_KEY_SPAN = 65000.0;
+constexpr int LO_NB = 4096;                              // buckets of the counting sort
+constexpr int LO_BIG = 32;
+constexpr int LO_BIG_LIST = LO_MAX_LEAVES / (LO_BIG + 1) + 1;
 
-template <int RB>
 struct LoSmem {
-    using Sort = cub::BlockRadixSort<unsigned short, LO_THREADS, LO_LEAF_ITEMS, short, RB>;
-    double lb[LO_MAX_LEAVES];     // compact leaf bounds (node-id order); sorted after step 6
-    int node[LO_MAX_LEAVES];      // compact leaf node ids; sorted after step 6
     union {
-        typename Sort::TempStorage sort;
         struct {
-            unsigned short key[LO_MAX_LEAVES];     // sorted keys
-            short perm[LO_MAX_LEAVES];             // compact index at each sorted position
-        } s;
-        unsigned long long gap[LO_MAX_LEAVES];     // bits of the gap bound before each position
+            double lb[LO_MAX_LEAVES];              // staged leaves (any order)
+            int node[LO_MAX_LEAVES];
+        } st;
+        unsigned long long gap[LO_MAX_LEAVES];     // after the sort: gap bound bits per position
     } u;
-    int wcnt[LO_MAX_NI][LO_WARPS];                 // leaves per (item, warp) -> exclusive offsets
-    double wmax[LO_WARPS];
-    double vmax;
-    int total;
+    double lb[LO_MAX_LEAVES];                      // leaves in (lb, node id) order
+    int node[LO_MAX_LEAVES];
+    int bend[LO_NB];                               // bucket counts -> starts -> ends
+    int big[LO_BIG_LIST];
+    int nstage, nbig;
 };
 
-template <int NI, int RB>
+__device__ __forceinline__ int lo_bucket(double v, double lo, double scale) {
+    const double k = floor((v - lo) * scale);
+    return k <= 0.0 ? 0 : (k >= (double)(LO_NB - 1) ? LO_NB - 1 : (int)k);
+}
+
+__device__ __forceinline__ bool lo_less(double la, int na, double lb_, int nb) {
+    return la < lb_ || (la == lb_ && na < nb);
+}
+
+template <int NI>
 __global__ void __launch_bounds__(LO_THREADS, 2) leaf_order_kernel(const double* __restrict__ lb, lf_index idx,
-                                                                   OrderArgs o) {
-    using Sm = LoSmem<RB>;
+                                                                   const unsigned* __restrict__ qmax,
+                                                                   const unsigned* __restrict__ qmin, OrderArgs o) {
     extern __shared__ __align__(16) uint8_t lo_smem[];
-    Sm& sm = *reinterpret_cast<Sm*>(lo_smem);
+    LoSmem& sm = *reinterpret_cast<LoSmem*>(lo_smem);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned below = (1u << lane) - 1u;
     const int64_t q = blockIdx.x;
     const int Nn = idx.n_nodes;
     const int Lr = idx.n_leaves;
     const double* lbq = lb + q * Nn;
-
-    // 1. local-leaf flags, leaves per (item, warp), largest leaf bound
-    unsigned flags = 0;
-    double vmax = 0.0;
-#pragma unroll
-    for (int i = 0; i < NI; ++i) {
-        const int node = i * LO_THREADS + tid;
-        const bool isl = node < Nn && __ldg(idx.d_node_leaf + node) >= 0;
-        const unsigned b = __ballot_sync(0xffffffffu, isl);
-        if (isl) {
-            flags |= 1u << i;
-            vmax = fmax(vmax, lbq[node]);
-        }
-        if (lane == 0) sm.wcnt[i][warp] = __popc(b);
+    const double lo = (double)__uint_as_float(qmin[q]);
+    const double span = (double)__uint_as_float(qmax[q]) - lo;
+    const double scale = (span > 0.0 && span < kInf) ? (double)(LO_NB - 1) / span : 0.0;
+    for (int b = tid; b < LO_NB; b += LO_THREADS) sm.bend[b] = 0;
+    if (tid == 0) {
+        sm.nstage = 0;
+        sm.nbig = 0;
     }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, off));
-    if (lane == 0) sm.wmax[warp] = vmax;
     __syncthreads();
-    // 2. exclusive scan of the counts in (item, warp) order = node-id order
-    if (warp == 0) {
-        constexpr int NC = NI * LO_WARPS;                // <= 256 = 32 lanes x 8
-        int c[8], sum = 0;
+    // 1. stage the leaves and count them per bucket (loads of 8 items in flight together)
+    unsigned flags = 0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int k = lane * 8 + j;
-            c[j] = k < NC ? sm.wcnt[k / LO_WARPS][k % LO_WARPS] : 0;
+    for (int h = 0; h < NI; h += 8) {
+        int nl[8];
+        double v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int node = (h + e) * LO_THREADS + tid;
+            nl[e] = node < Nn ? __ldg(idx.d_node_leaf + node) : -1;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int node = (h + e) * LO_THREADS + tid;
+            v[e] = nl[e] >= 0 ? lbq[node] : 0.0;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const bool isl = nl[e] >= 0;
+            const unsigned bm = __ballot_sync(0xffffffffu, isl);
+            if (bm == 0) continue;
+            int base = 0;
+            if (lane == 0) base = atomicAdd(&sm.nstage, __popc(bm));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (isl) {
+                flags |= 1u << (h + e);
+                const int pos = base + __popc(bm & below);
+                sm.u.st.lb[pos] = v[e];
+                sm.u.st.node[pos] = (h + e) * LO_THREADS + tid;
+                atomicAdd(&sm.bend[lo_bucket(v[e], lo, scale)], 1);
+            }
+        }
+    }
+    __syncthreads();
+    const int L = sm.nstage;
+    // 2. exclusive scan of the counts (8 consecutive buckets per thread), then scatter
+    {
+        constexpr int PT = LO_NB / LO_THREADS;
+        int c[PT], sum = 0;
+#pragma unroll
+        for (int j = 0; j < PT; ++j) {
+            c[j] = sm.bend[tid * PT + j];
             sum += c[j];
         }
         int incl = sum;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, incl, d);
-            if (lane >= d) incl += v;
+            const int t = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += t;
         }
+        __shared__ int wsum[LO_WARPS];
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
         int run = incl - sum;
+        for (int w = 0; w < warp; ++w) run += wsum[w];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int k = lane * 8 + j;
-            if (k < NC) sm.wcnt[k / LO_WARPS][k % LO_WARPS] = run;
+        for (int j = 0; j < PT; ++j) {
+            sm.bend[tid * PT + j] = run;
             run += c[j];
         }
-        if (lane == 31) sm.total = incl;
-        double m = lane < LO_WARPS ? sm.wmax[lane] : 0.0;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
-        if (lane == 0) sm.vmax = m;
     }
     __syncthreads();
-    const int L = sm.total;
-    // 3. compact the leaves in node-id order
-#pragma unroll
-    for (int i = 0; i < NI; ++i) {
-        const bool isl = (flags >> i) & 1u;
-        const unsigned b = __ballot_sync(0xffffffffu, isl);
-        if (isl) {
-            const int node = i * LO_THREADS + tid;
-            const int pos = sm.wcnt[i][warp] + __popc(b & below);
-            sm.lb[pos] = lbq[node];
-            sm.node[pos] = node;
-        }
-    }
-    __syncthreads();
-    // 4. stable sort of the 16-bit keys (blocked input = node-id order)
-    {
-        const double vm = sm.vmax;
-        const double scale = (vm > 0.0 && vm < kInf) ? LO_KEY_SPAN / vm : 0.0;
-        unsigned short keys[LO_LEAF_ITEMS];
-        short vals[LO_LEAF_ITEMS];
-#pragma unroll
-        for (int e = 0; e < LO_LEAF_ITEMS; ++e) {
-            const int j = tid * LO_LEAF_ITEMS + e;
-            if (j < L) {
-                keys[e] = (unsigned short)fmin(floor(sm.lb[j] * scale), LO_KEY_SPAN);
-            } else {
-                keys[e] = 0xFFFFu;                       // padding sorts last (real keys <= 65000)
-            }
-            vals[e] = (short)j;
-        }
-        typename Sm::Sort(sm.u.sort).SortBlockedToStriped(keys, vals, 0, 16);
-        __syncthreads();                                 // temp storage is reused below
-#pragma unroll
-        for (int e = 0; e < LO_LEAF_ITEMS; ++e) {
-            const int r = e * LO_THREADS + tid;
-            sm.u.s.key[r] = keys[e];
-            sm.u.s.perm[r] = vals[e];
-        }
-    }
-    __syncthreads();
-    // 5. exact (lb, node id) order inside runs of equal keys
     for (int p = tid; p < L; p += LO_THREADS) {
-        const unsigned short kp = sm.u.s.key[p];
-        if ((p == 0 || sm.u.s.key[p - 1] != kp) && p + 1 < L && sm.u.s.key[p + 1] == kp) {
-            int e = p + 1;
-            while (e < L && sm.u.s.key[e] == kp) ++e;
-            for (int a = p + 1; a < e; ++a) {
-                const int ja = sm.u.s.perm[a];
-                const double la = sm.lb[ja];
-                int b = a - 1;
-                while (b >= p) {
-                    const int jb = sm.u.s.perm[b];
-                    const double lbb = sm.lb[jb];
-                    if (lbb < la || (lbb == la && jb < ja)) break;
-                    sm.u.s.perm[b + 1] = (short)jb;
-                    --b;
-                }
-                sm.u.s.perm[b + 1] = (short)ja;
+        const double v = sm.u.st.lb[p];
+        const int pos = atomicAdd(&sm.bend[lo_bucket(v, lo, scale)], 1);   // start -> end
+        sm.lb[pos] = v;
+        sm.node[pos] = sm.u.st.node[p];
+    }
+    __syncthreads();
+    // 3. exact (lb, node id) order inside each bucket
+#pragma unroll
+    for (int j = 0; j < LO_NB / LO_THREADS; ++j) {
+        const int b = j * LO_THREADS + tid;
+        const int s0 = b == 0 ? 0 : sm.bend[b - 1], e0 = sm.bend[b];
+        if (e0 - s0 > LO_BIG) {
+            const int t = atomicAdd(&sm.nbig, 1);
+            if (t < LO_BIG_LIST) sm.big[t] = b;
+            continue;
+        }
+        for (int a = s0 + 1; a < e0; ++a) {
+            const double la = sm.lb[a];
+            const int na = sm.node[a];
+            int c = a - 1;
+            while (c >= s0 && !lo_less(sm.lb[c], sm.node[c], la, na)) {
+                sm.lb[c + 1] = sm.lb[c];
+                sm.node[c + 1] = sm.node[c];
+                --c;
             }
+            sm.lb[c + 1] = la;
+            sm.node[c + 1] = na;
         }
     }
     __syncthreads();
-    // 6. materialise the sorted order in place
-    {
-        double slb[LO_LEAF_ITEMS];
-        int snode[LO_LEAF_ITEMS];
-#pragma unroll
-        for (int e = 0; e < LO_LEAF_ITEMS; ++e) {
-            const int r = e * LO_THREADS + tid;
-            if (r < L) {
-                const int j = sm.u.s.perm[r];
-                slb[e] = sm.lb[j];
-                snode[e] = sm.node[j];
+    if (sm.nbig > 0) {                                   // rare: a warp ranks each big bucket
+        for (int t = warp; t < sm.nbig; t += LO_WARPS) {
+            const int b = sm.big[t];
+            const int s0 = b == 0 ? 0 : sm.bend[b - 1], e0 = sm.bend[b];
+            for (int i = s0 + lane; i < e0; i += 32) {
+                const double li = sm.lb[i];
+                const int ni = sm.node[i];
+                int r = 0;
+                for (int j2 = s0; j2 < e0; ++j2) r += lo_less(sm.lb[j2], sm.node[j2], li, ni);
+                sm.u.st.lb[s0 + r] = li;                 // the staging area is free now
+                sm.u.st.node[s0 + r] = ni;
+            }
+            __syncwarp();
+            for (int i = s0 + lane; i < e0; i += 32) {
+                sm.lb[i] = sm.u.st.lb[i];
+                sm.node[i] = sm.u.st.node[i];
             }
         }
         __syncthreads();
+    }
+    for (int p = tid; p < L; p += LO_THREADS) sm.u.gap[p] = 0ull;
+    __syncthreads();
+    // 4. gap bounds of the non-leaf nodes
 #pragma unroll
-        for (int e = 0; e < LO_LEAF_ITEMS; ++e) {
-            const int r = e * LO_THREADS + tid;
-            if (r < L) {
-                sm.lb[r] = slb[e];
-                sm.node[r] = snode[e];
-                sm.u.gap[r] = 0ull;                      // key / perm are dead
-            }
+    for (int h = 0; h < NI; h += 8) {
+        double v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int node = (h + e) * LO_THREADS + tid;
+            v[e] = (node < Nn && !((flags >> (h + e)) & 1u)) ? lbq[node] : -1.0;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            if (v[e] < 0.0) continue;
+            const int node = (h + e) * LO_THREADS + tid;
+            const int b = lo_bucket(v[e], lo, scale);
+            int p = b == 0 ? 0 : sm.bend[b - 1];
+            const int e0 = sm.bend[b];
+            while (p < e0 && lo_less(sm.lb[p], sm.node[p], v[e], node)) ++p;
+            if (p < L) atomicMax(&sm.u.gap[p], (unsigned long long)__double_as_longlong(v[e]));
         }
     }
     __syncthreads();
-    // 7. gap bounds: each non-leaf node raises the gap of the first leaf after it
-#pragma unroll 4
-    for (int i = 0; i < NI; ++i) {
-        const int node = i * LO_THREADS + tid;
-        if (node >= Nn || ((flags >> i) & 1u)) continue;
-        const double v = lbq[node];
-        int lo = 0, hi = L;
-        while (lo < hi) {                                // first position with (lb, id) > (v, node)
-            const int mid = (lo + hi) >> 1;
-            const double a = sm.lb[mid];
-            if (a > v || (a == v && sm.node[mid] > node)) hi = mid;
-            else lo = mid + 1;
-        }
-        if (lo < L) atomicMax(&sm.u.gap[lo], (unsigned long long)__double_as_longlong(v));
-    }
-    __syncthreads();
-    // 8. records, 4 positions per thread at a time
+    // 5. records, 4 positions per thread at a time
 #pragma unroll
     for (int h = 0; h < LO_LEAF_ITEMS; h += 4) {
         int p[4], node[4];
@@ -451,12 +480,11 @@ __global__ void leaf_records_kernel(const double* __restrict__ slb, const int* _
 }
 
 template <int NI>
-static int launch_leaf_order(const double* d_lb, int64_t Q, const lf_index& idx, const OrderArgs& oa,
-                             cudaStream_t st) {
-    constexpr int RB = 4;
-    const int bytes = (int)sizeof(LoSmem<RB>);
-    LF_CUDA(smem_optin(leaf_order_kernel<NI, RB>, bytes));
-    leaf_order_kernel<NI, RB><<<(unsigned)Q, LO_THREADS, bytes, st>>>(d_lb, idx, oa);
+static int launch_leaf_order(const double* d_lb, int64_t Q, const lf_index& idx, const unsigned* qmax,
+                             const unsigned* qmin, const OrderArgs& oa, cudaStream_t st) {
+    const int bytes = (int)sizeof(LoSmem);
+    LF_CUDA(smem_optin(leaf_order_kernel<NI>, bytes));
+    leaf_order_kernel<NI><<<(unsigned)Q, LO_THREADS, bytes, st>>>(d_lb, idx, qmax, qmin, oa);
     LF_CUDA(cudaGetLastError());
     return LF_OK;
 }
@@ -469,13 +497,19 @@ int bounds_and_order(const float* d_q, int64_t Q, const lf_index& idx, double* d
                      const OrderArgs& oa, cudaStream_t st, int* kernels) {
     const int n = idx.n_nodes;
     if (Q == 0 || n == 0) return LF_OK;
-    int rc = launch_bounds(d_q, Q, idx, idx.d_env_min, idx.d_env_max, n, 0, d_qsumm, d_lb, st);
+    const bool fused = n <= LO_THREADS * LO_MAX_NI && idx.n_leaves <= LO_MAX_LEAVES && idx.n_seg <= LBT_SEG &&
+                       (Q + LBT_Q - 1) / LBT_Q <= 65535 && Q <= 0x7fffffff;
+    Scratch range;
+    if (fused) LF_CUDA(range.alloc(sizeof(unsigned) * 2 * Q, st));
+    unsigned* qmax = fused ? range.as<unsigned>() : nullptr;
+    unsigned* qmin = fused ? qmax + Q : nullptr;
+    int rc = launch_bounds(d_q, Q, idx, idx.d_env_min, idx.d_env_max, n, 0, d_qsumm, d_lb, st, qmax, qmin);
     if (rc) return rc;
-    if (kernels) *kernels += 3;
-    if (n <= LO_THREADS * LO_MAX_NI && idx.n_leaves <= LO_MAX_LEAVES && Q <= 0x7fffffff) {
-        if (n <= LO_THREADS * 4) return launch_leaf_order<4>(d_lb, Q, idx, oa, st);
-        if (n <= LO_THREADS * 8) return launch_leaf_order<8>(d_lb, Q, idx, oa, st);
-        return launch_leaf_order<16>(d_lb, Q, idx, oa, st);
+    if (kernels) *kernels += 2;
+    if (fused) {
+        if (kernels) *kernels += 1;
+        if (n <= LO_THREADS * 8) return launch_leaf_order<8>(d_lb, Q, idx, qmax, qmin, oa, st);
+        return launch_leaf_order<16>(d_lb, Q, idx, qmax, qmin, oa, st);
     }
     Scratch slb, sord;
     LF_CUDA(slb.alloc(sizeof(double) * Q * n, st));

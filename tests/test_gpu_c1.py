@@ -3,9 +3,12 @@ against the reference's own run (tests/golden/c1.*, produced by make_golden.py).
 
 * exact search: ids, distances (rel 1e-12) and every counter identical
   (sequential schedule), and ids identical under the batched round schedule;
-* LeaFi at target 0.99 with filters trained by OUR pipeline: recall >= 0.97
-  per noise level (acceptance criterion 9, test_acceptance.py:306-311) and
-  mean pruning within 1 point of the reference's LeaFi run.
+* LeaFi at target 0.99 with filters trained by OUR pipeline: recall@1 >= 0.99
+  over the 400 queries (BASELINE.md config 1 gate; the reference's own run
+  reaches 0.9975), >= 0.97 per noise level (acceptance criterion 9,
+  test_acceptance.py:306-311), and mean pruning within +-1.5 points of the
+  reference's LeaFi run at every noise level (two-sided: 100 queries per level,
+  the band is the noise between two independently trained filter sets).
 """
 
 import json
@@ -54,12 +57,18 @@ def test_c1_leafi_recall_and_pruning(c1):
                    constants=pl.RuntimeConstants(2e-7, 6e-6, fb), train_cfg=TrainConfig(initial_lr=1e-3))
     ref_rows = {(r["noise"], r["method"]): r for r in c1["doc"]["bench_rows"]}
     assert e.filter_leaf_ids == c1["doc"]["selected"]
+    all_hits, report = [], {}
     for nz in LEVELS:
         Q = c1["queries"][nz]
         ex = search_batch(c1["tree"], Q, 1)
         res = pl.search_queries(e, Q, 1, target=0.99)
         hits = [lo.recall_at_1(res.results(i), int(ex.ids[i, 0]), float(ex.dists[i, 0])) for i in range(len(Q))]
+        all_hits += hits
         ours = float(np.mean(res.pruning_ratios()))
         ref = ref_rows[(nz, "filtered")]["mean_pruning_ratio"]
-        assert np.mean(hits) >= 0.97, (nz, np.mean(hits))
-        assert ours >= ref - 0.01, (nz, ours, ref)
+        report[nz] = (float(np.mean(hits)), ours, ref)
+    print("C1 LeaFi (recall, pruning, reference pruning) per noise level:", report)
+    assert np.mean(all_hits) >= 0.99, report
+    for nz, (rec, ours, ref) in report.items():
+        assert rec >= 0.97, (nz, report)
+        assert abs(ours - ref) <= 0.015, (nz, report)

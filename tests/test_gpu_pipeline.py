@@ -74,6 +74,39 @@ def test_collect_targets_pipeline(pipeline_golden):
     np.testing.assert_allclose(gts.nn_distance, g["tg_nn_distance"], rtol=RTOL)
 
 
+def test_collect_targets_m256_int8_vs_oracle():
+    """Training-data generation at m = 256, where the int8 tensor-core kernel
+    (lf_leaf_min_dist_q8 / lf_local_min_dist_q8) is the default path, against the
+    CPU oracle's collect_targets (traingen.py:147-220) on the same tree: bounds and
+    visit order bit-exact, every minimum distance within 1e-12 relative (fp64 direct
+    form, another summation order), member queries exactly 0."""
+    from paper_2502_01836_b200 import build_index
+    from paper_2502_01836_b200.targets import collect_targets, default_path, local_targets_all
+
+    data = lo.randwalk(24000, 256, 21)
+    t = build_index(data, 600)
+    assert default_path(t, t.device()) == "q8"
+    gq, _ = lo.global_queries(data, 220, (0.1, 0.4), 5)
+    gq = np.concatenate([gq, data[[5, 777, 23000]].astype(np.float64)])    # member queries
+    ot = lo.build_tree(data, 600)
+    sel = [int(l) for l in t.leaf_ids[::2]]
+    got = collect_targets(t, sel, gq, 60)
+    ref = lo.collect_targets(ot, sel, gq, 60)
+    np.testing.assert_array_equal(got.lb_matrix, ref.lb_matrix)
+    np.testing.assert_array_equal(got.visit_order, ref.visit_order)
+    np.testing.assert_allclose(got.dl_selected, ref.dl_selected, rtol=1e-12, atol=0)
+    np.testing.assert_allclose(got.dl_calib_full, ref.dl_calib_full, rtol=1e-12, atol=0)
+    np.testing.assert_allclose(got.nn_distance, ref.nn_distance, rtol=1e-12, atol=0)
+    assert (got.dl_calib_full[-3:].min(axis=1) == 0.0).all()
+    lids = [int(l) for l in t.leaf_ids[:4]]
+    qs = {l: lo.noisy_queries(data[ot.members[l]], 50, 0.2, 30 + l) for l in lids}
+    loc = local_targets_all(t, qs)
+    for l in lids:
+        tg, lbs = lo.local_targets(ot, l, qs[l])
+        np.testing.assert_allclose(loc[l][0], tg, rtol=1e-12, atol=0)
+        np.testing.assert_array_equal(loc[l][1], lbs)
+
+
 # -------------------------------------------------------------- pipeline --
 FIXED = dict(t_series=2e-7, t_filter=6e-6, filter_bytes=5 * 1024)   # reference tests/conftest.py:11
 

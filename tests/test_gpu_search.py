@@ -436,6 +436,25 @@ def test_leaf_order_sequential_matches_oracle():
     assert ended == {0, 1}, "both break kinds (internal node / leaf) must occur"
 
 
+def test_leaf_order_clustered_bounds():
+    """A few far-away rows make one leaf's bound an outlier, so the other leaves
+    crowd into a handful of counting-sort buckets (the warp rank-sort path):
+    ids, counters and traces still equal the reference traversal."""
+    from paper_2502_01836_b200 import build_index, search_batch
+
+    data = lo.randwalk(40000, 64, 78)
+    data[:300] = (data[:300] + 5000.0).astype(np.float32)
+    t = build_index(data, 24)
+    Q = np.concatenate([lo.noisy_queries(data[300:], 8, nz, 51 + int(10 * nz)) for nz in (0.1, 1.0)])
+    res = search_batch(t, Q, 2, sequential=True, want_trace=True)
+    ot = lo.build_tree(data, 24)
+    for i, q in enumerate(Q):
+        o = lo.search(ot, q, 2, want_trace=True)
+        assert res.ids[i].tolist() == [a for a, _ in o.results], i
+        assert res.stats[i].tolist() == [o.stats[s_] for s_ in lo.STAT_KEYS], i
+        assert [e.leaf_id for e in res.trace_of(i)] == [e[0] for e in o.trace], i
+
+
 def test_leaf_order_batched_equals_sequential():
     """Batched rounds over the leaf order give the sequential walk's neighbours."""
     from paper_2502_01836_b200 import search_batch
