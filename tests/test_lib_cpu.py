@@ -57,6 +57,24 @@ def test_struct_layouts_match_header():
     assert h.lf_abi_offsetof(b"lf_index", b"n_series") == 0
 
 
+def test_integration_stub_matches_header():
+    """INTEGRATION.md's ctypes mirrors are the generator's output for the current header."""
+    import sys
+
+    sys.path.insert(0, str(ROOT / "tools"))
+    import gen_ctypes_stub
+
+    assert gen_ctypes_stub.doc_block() in (ROOT / "INTEGRATION.md").read_text()
+    ns = {}
+    exec(gen_ctypes_stub.stub().split("lib = C.CDLL")[0].replace("```python", ""), ns)
+    from paper_2502_01836_b200 import _lib
+    for name, cls in _lib.STRUCTS.items():
+        stub_cls = ns[cls.__name__]
+        assert [f for f, _ in stub_cls._fields_] == [f for f, _ in cls._fields_], name
+        import ctypes as C
+        assert C.sizeof(stub_cls) == _lib.lib().lf_abi_sizeof(name.encode()), name
+
+
 def _table_equal(t, g, prefix="nt_"):
     np.testing.assert_array_equal(t.env_min, g[prefix + "env_min"])
     np.testing.assert_array_equal(t.env_max, g[prefix + "env_max"])
