@@ -120,8 +120,15 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------- setup --
-def setup_workload(args, device):
-    """Collection, tree, filters, query batch and exact ground truth (untimed)."""
+def setup_workload(args, device, rank: int = 0, world: int = 1):
+    """Collection, tree, filters, query batch and exact ground truth (untimed).
+
+    world > 1 (leaf-sharded): every rank generates the collection and
+    builds the same tree from its segment means, then keeps ONLY its leaf shard's
+    rows (the full collection is dropped after enhancement); enhancement is sharded
+    (training-data generation on the rank's leaves + all-gather, each rank trains
+    only its own filters, calibration predictions all-gathered); the exact ground
+    truth is the sharded exact search."""
     import torch
 
     from paper_2502_01836_b200 import build_index_device, search_batch
@@ -145,7 +152,7 @@ def setup_workload(args, device):
         tree = build_isax_index(X, max_leaf_size=args.leaf_cap, segments=8)
     else:
         tree = build_index_device(X, max_leaf_size=args.leaf_cap, segments=8)
-    di = tree.device(device)
+    di = tree.device(device) if world == 1 else tree.shard(rank, world, device)
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
     log(f"collection {args.n}x{args.m} in {t_gen:.1f}s; tree {tree.n_leaves} leaves / {tree.n_nodes} nodes in {t_build:.1f}s")
@@ -154,23 +161,35 @@ def setup_workload(args, device):
     budget = pl.SelectionBudget(capacity_bytes=fbytes * tree.n_leaves, a=2.0)
     timings = {}
     t0 = time.perf_counter()
+    shard = (rank, world, None) if world > 1 else None
     eidx = pl.enhance(tree, pl.SplitPlan(args.n_global, args.n_local, args.calibration), budget, args.seed,
                       constants=consts, train_cfg=TrainConfig(initial_lr=1e-3, max_epochs=args.max_epochs),
-                      timings=timings)
+                      timings=timings, shard=shard)
     torch.cuda.synchronize()
     t_enh = time.perf_counter() - t0
     log(f"enhance {len(eidx.filters)} filters in {t_enh:.1f}s: " +
         ", ".join(f"{k}={v:.1f}s" for k, v in timings.items() if v > 0.05))
     per = args.queries // len(NOISE_LEVELS)
     Q = torch.cat([queries_device(X, per, nz, args.seed + int(10 * nz)) for nz in NOISE_LEVELS]).contiguous()
+    tdg_q = None
+    if args.tdg_queries > 0:
+        tdg_q = torch.cat([queries_device(X, args.tdg_queries // 4, nz, args.seed + 77 + i)
+                           for i, nz in enumerate(NOISE_LEVELS)]).contiguous()
     del X
+    if world > 1:
+        tree.values = None                   # the rank keeps its shard's rows only
     torch.cuda.empty_cache()
     t0 = time.perf_counter()
-    exact = search_batch(tree, Q, args.k)
+    if world > 1:
+        from paper_2502_01836_b200.sharded import search_sharded
+
+        exact = search_sharded(tree, Q, args.k, rank=rank, world=world)
+    else:
+        exact = search_batch(tree, Q, args.k)
     t_exact = time.perf_counter() - t0
     log(f"exact ground truth for {Q.shape[0]} queries in {t_exact:.2f}s "
         f"(pruning {np.mean(exact.pruning_ratios()):.4f})")
-    return {"tree": tree, "eidx": eidx, "Q": Q, "exact": exact, "di": di,
+    return {"tree": tree, "eidx": eidx, "Q": Q, "exact": exact, "di": di, "tdg_q": tdg_q,
             "setup_s": {"generate": t_gen, "build": t_build, "enhance": t_enh, "exact": t_exact, **timings}}
 
 
@@ -406,7 +425,7 @@ def run_ours(args, rank, world, device):
     from paper_2502_01836_b200 import _lib
     from paper_2502_01836_b200.pipeline import search_queries
 
-    w = setup_workload(args, device)
+    w = setup_workload(args, device, rank, world)
     w["target"] = args.target
     w["k"] = args.k
     eidx, Q, exact, tree = w["eidx"], w["Q"], w["exact"], w["tree"]
@@ -428,7 +447,8 @@ def run_ours(args, rank, world, device):
 
         a, b = tree.shard(rank, world).leaf_range
         local = [int(l) for l in tree.leaf_ids[a:b] if int(l) in eidx.filters]
-        lpack = FilterPack.from_models({l: eidx.filters[l] for l in local}) if local else None
+        lpack = (eidx.pack if world > 1 else FilterPack.from_models({l: eidx.filters[l] for l in local})) \
+            if local else None                     # world > 1: enhance() trained this rank's filters only
         offs_all = eidx.tuned_offsets(args.target)
         loffs = np.array([offs_all[l] for l in local], dtype=np.float64)
 
@@ -521,9 +541,7 @@ def run_ours(args, rank, world, device):
         from paper_2502_01836_b200.synth import queries_device
         from paper_2502_01836_b200.targets import default_path, leaf_min_distances
 
-        Xq = w["di"].X
-        gq = torch.cat([queries_device(Xq, args.tdg_queries // 4, nz, args.seed + 77 + i)
-                        for i, nz in enumerate(NOISE_LEVELS)]).contiguous()
+        gq = w["tdg_q"]
         # leaf-sharded like the search: this rank's leaves, all queries
         tdi = tree.shard(rank, world) if world > 1 else w["di"]
         slots = list(range(tdi.n_leaves))
@@ -782,10 +800,26 @@ def main():
         log("warmup raised to 3 (timing rule)")
         args.warmup = 3
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torch.distributed.run
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()),
+               *sys.argv[1:]]
+        log("launching", args.gpus, "ranks:", " ".join(cmd[1:6]))
+        sys.exit(subprocess.call(cmd))
+
     import torch
     import torch.distributed as dist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch with "
+                         f"--nproc-per-node {args.gpus}, or drop WORLD_SIZE and let --gpus spawn the ranks)")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dev_index = local % max(1, torch.cuda.device_count())     # > 1 rank per GPU only in functional tests

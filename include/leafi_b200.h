@@ -177,6 +177,17 @@ lf_session* lf_search_begin(const lf_index* idx, const float* d_queries, int64_t
                             const lf_search_opts* opts, const lf_trace* trace, int64_t* d_stats,
                             void* stream);
 int lf_search_round(lf_session* s, const double* d_bound, double* d_bsf_out, int32_t* h_active);
+/*
+ * The same round without a host synchronisation, so a caller can keep one round
+ * in flight while the bound exchange of the previous one runs (leaf-sharded
+ * search: the ranks' MIN-allreduce of [bsf, -active] is stream-ordered after the
+ * round and before the next).  lf_search_round_async enqueues the round and
+ * writes its active-query count to the DEVICE int *d_active (nullable);
+ * lf_search_round_wait waits for the OLDEST enqueued round and returns its count
+ * in *h_active.  At most two rounds may be in flight; not for lazy inference.
+ */
+int lf_search_round_async(lf_session* s, const double* d_bound, double* d_bsf_out, int32_t* d_active);
+int lf_search_round_wait(lf_session* s, int32_t* h_active);
 int lf_search_end(lf_session* s, int64_t* d_out_ids, double* d_out_dists);
 void lf_search_free(lf_session* s);
 

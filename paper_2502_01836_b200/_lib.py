@@ -98,6 +98,8 @@ SIGNATURES = {
                             C.POINTER(LfTrace), _P]),
     "lf_search_begin": (_P, [C.POINTER(LfIndex), _P, _I64, C.POINTER(LfSearchOpts), C.POINTER(LfTrace), _P, _P]),
     "lf_search_round": (C.c_int, [_P, _P, _P, C.POINTER(_I32)]),
+    "lf_search_round_async": (C.c_int, [_P, _P, _P, _P]),
+    "lf_search_round_wait": (C.c_int, [_P, C.POINTER(_I32)]),
     "lf_search_end": (C.c_int, [_P, _P, _P]),
     "lf_search_free": (None, [_P]),
     "lf_filter_predict": (C.c_int, [_P, _I64, _I32, _P, _P, _P, _P, _I32, _P, _P]),

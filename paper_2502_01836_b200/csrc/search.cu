@@ -972,7 +972,30 @@ lf_session* lf_search_begin(const lf_index* idx, const float* d_queries, int64_t
 
 int lf_search_round(lf_session* ss, const double* d_bound, double* d_bsf_out, int32_t* h_active) {
     LF_REQUIRE(ss != nullptr && h_active != nullptr, "NULL argument");
+    LF_REQUIRE(ss->harvested == ss->round, "rounds in flight: call lf_search_round_wait first");
     return lf::session_round(ss, d_bound, d_bsf_out, h_active);
+}
+
+int lf_search_round_async(lf_session* ss, const double* d_bound, double* d_bsf_out, int32_t* d_active) {
+    LF_REQUIRE(ss != nullptr, "NULL session");
+    LF_REQUIRE(!ss->lazy, "lazy filter inference needs host decisions after each round: use lf_search_round");
+    LF_REQUIRE(ss->round - ss->harvested < 2, "at most two rounds in flight: call lf_search_round_wait first");
+    const int slot = ss->round & 1;
+    int rc = lf::session_enqueue(ss, d_bound, d_bsf_out);
+    if (rc) return rc;
+    if (d_active)
+        LF_CUDA(cudaMemcpyAsync(d_active, ss->n_active.as<int>() + 4 * slot, sizeof(int), cudaMemcpyDeviceToDevice,
+                                ss->st));
+    return LF_OK;
+}
+
+int lf_search_round_wait(lf_session* ss, int32_t* h_active) {
+    LF_REQUIRE(ss != nullptr && h_active != nullptr, "NULL argument");
+    LF_REQUIRE(ss->harvested < ss->round, "no round in flight");
+    int act = 0;
+    int rc = lf::session_harvest(ss, &act);
+    *h_active = act;
+    return rc;
 }
 
 int lf_search_end(lf_session* ss, int64_t* d_out_ids, double* d_out_dists) {

@@ -285,11 +285,26 @@ def search(eidx, req: SearchRequest) -> SearchOutcome:
 # --------------------------------------------------------------- enhance ----
 def enhance(index, plan: SplitPlan, budget: SelectionBudget, seed: int, *,
             constants: RuntimeConstants | None = None, train_cfg: TrainConfig | None = None,
-            noise_range=(0.1, 0.4), record_trajectories: bool = False, timings: dict | None = None
-            ) -> EnhancedIndex:
-    """Build filters and auto-tuners over an index (enhanced.py:189-313), GPU stages."""
+            noise_range=(0.1, 0.4), record_trajectories: bool = False, timings: dict | None = None,
+            shard=None) -> EnhancedIndex:
+    """Build filters and auto-tuners over an index (enhanced.py:189-313), GPU stages.
+
+    shard=(rank, world, group): leaf-sharded enhancement (call on every rank).  The
+    selection, global queries and calibration are global; training-data generation
+    runs on this rank's leaves and all-gathers the columns; each rank trains ONLY the
+    filters of its own leaves; the calibration predictions of every rank's filters are
+    all-gathered, so every rank fits the same curves.  The returned index holds this
+    rank's filters (and every curve)."""
     torch = _lib.require_cuda()
     t = as_tree(index)
+    sharded = shard is not None and shard[1] > 1
+    if sharded:
+        import torch.distributed as dist
+
+        rank, world, group = shard
+        di_loc = t.shard(rank, world)
+        a_loc, b_loc = di_loc.leaf_range
+        own = set(int(l) for l in t.leaf_ids[a_loc:b_loc])
     train_cfg = train_cfg or TrainConfig()
     timings = timings if timings is not None else {}
     stage = "init"
@@ -322,29 +337,33 @@ def enhance(index, plan: SplitPlan, budget: SelectionBudget, seed: int, *,
         gq, _ = generate_global_queries(t.values, plan.n_global, noise_range, derive_seed(seed, 2))
 
         begin("collect-targets")
-        gts = collect_targets(t, selected, gq, plan.calibration, train_nn=False)   # only nn[pool:] is read
+        gts = collect_targets(t, selected, gq, plan.calibration, train_nn=False,   # only nn[pool:] is read
+                              shard=shard)
 
         begin("local-queries")
+        col_of = {lid: c for c, lid in enumerate(selected)}
+        mine = [l for l in selected if l in own] if sharded else selected
         local_q = {}
-        for lid in selected:
+        for lid in mine:
             q, _, _ = generate_local_queries(t, lid, plan.n_local, noise_range, derive_seed(seed, 10_000 + lid))
             local_q[lid] = q
-        local = local_targets_all(t, local_q) if plan.n_local else {l: (np.zeros(0), np.zeros(0)) for l in selected}
+        local = (local_targets_all(t, local_q, dindex=di_loc if sharded else None)
+                 if plan.n_local and mine else {l: (np.zeros(0), np.zeros(0)) for l in mine})
 
         begin("train-filters")
-        m, F, pool = t.m, len(selected), gts.train_pool_size
+        m, F, pool = t.m, len(mine), gts.train_pool_size
         n_all = pool + plan.n_local
         n_tr = (n_all * 4) // 5
-        bank = np.concatenate([gts.queries[:pool]] + [local_q[l] for l in selected]).astype(np.float32)
+        bank = np.concatenate([gts.queries[:pool]] + [local_q[l] for l in mine]).astype(np.float32)
         tr_idx = np.empty((F, n_tr), np.int64)
         va_idx = np.empty((F, n_all - n_tr), np.int64)
         tr_y = np.empty((F, n_tr))
         va_y = np.empty((F, n_all - n_tr))
         W1 = np.empty((F, m, m), np.float32); b1 = np.empty((F, m), np.float32)
         W2 = np.empty((F, m), np.float32); b2 = np.empty(F, np.float32)
-        for s, lid in enumerate(selected):
+        for s, lid in enumerate(mine):
             rows = np.concatenate([np.arange(pool), pool + s * plan.n_local + np.arange(plan.n_local)])
-            y = np.concatenate([gts.dl_selected[:pool, s], local[lid][0]])
+            y = np.concatenate([gts.dl_selected[:pool, col_of[lid]], local[lid][0]])
             perm = np.random.default_rng(derive_seed(seed, 30_000 + lid)).permutation(n_all)
             tr_idx[s], va_idx[s] = rows[perm[:n_tr]], rows[perm[n_tr:]]
             tr_y[s], va_y[s] = y[perm[:n_tr]], y[perm[n_tr:]]
@@ -352,13 +371,24 @@ def enhance(index, plan: SplitPlan, budget: SelectionBudget, seed: int, *,
         dbank = torch.from_numpy(bank).cuda()
         (W1, b1, W2, b2), reps = train_filters(dbank, tr_idx, tr_y, va_idx, va_y, (W1, b1, W2, b2), train_cfg,
                                               seed=derive_seed(seed, 20_000), record_trajectories=record_trajectories)
-        filters = {lid: FilterModel(W1[s], b1[s], W2[s], float(b2[s])) for s, lid in enumerate(selected)}
-        reports = {lid: reps[s] for s, lid in enumerate(selected)}
-        pack = FilterPack(selected, W1, b1, W2, b2)
+        filters = {lid: FilterModel(W1[s], b1[s], W2[s], float(b2[s])) for s, lid in enumerate(mine)}
+        reports = {lid: reps[s] for s, lid in enumerate(mine)}
+        pack = FilterPack(mine, W1, b1, W2, b2, device=di_loc.device if sharded else None)
 
         begin("fit-tuners")
         calib = gts.queries[pool:]
-        cpred = pack.predict(calib).cpu().numpy().astype(np.float64)      # same kernel as search (F6)
+        cp = pack.predict(calib) if mine else torch.zeros((calib.shape[0], 0), dtype=torch.float32,
+                                                          device=di_loc.device)
+        if sharded:          # every rank's filters are a contiguous block of `selected`
+            widths = [0] * world
+            dist.all_gather_object(widths, int(cp.shape[1]), group=group)
+            wmax = max(max(widths), 1)
+            pad = torch.zeros((cp.shape[0], wmax), dtype=cp.dtype, device=cp.device)
+            pad[:, :cp.shape[1]] = cp
+            parts = [torch.empty_like(pad) for _ in range(world)]
+            dist.all_gather(parts, pad, group=group)
+            cp = torch.cat([parts[r][:, :widths[r]] for r in range(world)], dim=1)
+        cpred = cp.cpu().numpy().astype(np.float64)      # same kernel as search (F6)
         preds = {lid: cpred[:, s] for s, lid in enumerate(selected)}
         alphas = {lid: compute_alphas(preds[lid], gts.dl_selected[pool:, s]) for s, lid in enumerate(selected)}
         sk = build_skeleton(gts.lb_matrix[pool:], gts.dl_calib_full, gts.visit_order[pool:],

@@ -84,6 +84,21 @@ class GpuRoundEngine:
         _lib.check(_lib.lib().lf_search_round(self.sess, bound.data_ptr(), bsf_out.data_ptr(), C.byref(act)))
         return int(act.value)
 
+    @property
+    def async_rounds(self) -> bool:
+        return self._opts.d_W1T is None          # lazy inference needs host decisions per round
+
+    def enqueue(self, bound, bsf_out, active_dev) -> None:
+        """Enqueue one round without a host sync; its active count lands in active_dev (int32 [1])."""
+        _lib.check(_lib.lib().lf_search_round_async(self.sess, bound.data_ptr(), bsf_out.data_ptr(),
+                                                    active_dev.data_ptr()))
+
+    def wait(self) -> int:
+        """Wait for the oldest enqueued round; its active count."""
+        act = C.c_int32(0)
+        _lib.check(_lib.lib().lf_search_round_wait(self.sess, C.byref(act)))
+        return int(act.value)
+
     def end(self):
         torch = self.torch
         ids = torch.empty((self.Q, self.k), dtype=torch.int64, device=self.device)
@@ -115,6 +130,8 @@ def run_rounds(engine, group=None, max_rounds: int = 1 << 20) -> tuple:
     import torch.distributed as dist
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world > 1 and getattr(engine, "async_rounds", False):
+        return _run_rounds_pipelined(engine, group, world, max_rounds)
     Q, k, dev = engine.Q, engine.k, engine.device
     buf = torch.full((Q + 1,), math.inf, dtype=torch.float64, device=dev)
     bound = torch.full((Q,), math.inf, dtype=torch.float64, device=dev)
@@ -142,6 +159,63 @@ def run_rounds(engine, group=None, max_rounds: int = 1 << 20) -> tuple:
         dist.all_gather(gd, d, group=group)
         ids, d = merge_topk(torch.cat(gi, dim=1), torch.cat(gd, dim=1), k)
         dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=group)
+    return ids, d, stats, rounds
+
+
+def _finish(engine, group, world: int):
+    import torch
+    import torch.distributed as dist
+
+    ids, d, stats = engine.end()
+    gi = [torch.empty_like(ids) for _ in range(world)]
+    gd = [torch.empty_like(d) for _ in range(world)]
+    dist.all_gather(gi, ids, group=group)
+    dist.all_gather(gd, d, group=group)
+    ids, d = merge_topk(torch.cat(gi, dim=1), torch.cat(gd, dim=1), engine.k)
+    dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=group)
+    return ids, d, stats
+
+
+def _run_rounds_pipelined(engine, group, world: int, max_rounds: int) -> tuple:
+    """One round in flight ahead of the host, like lf_search: round r's exchange
+    (MIN-allreduce of [bsf..., -active], stream-ordered after the round) and round
+    r+1 are enqueued before the host reads round r's global active flag -- ONE
+    host synchronisation per round, and the GPU never idles on it.  A round
+    enqueued after the last active one finds every query done on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    Q, dev = engine.Q, engine.device
+    buf = torch.full((Q + 1,), math.inf, dtype=torch.float64, device=dev)
+    bound = torch.full((Q,), math.inf, dtype=torch.float64, device=dev)
+    locs = [torch.empty((Q,), dtype=torch.float64, device=dev) for _ in range(2)]
+    acts = [torch.zeros((1,), dtype=torch.int32, device=dev) for _ in range(2)]
+    flag = torch.empty((2,), dtype=torch.float64, pin_memory=True)
+    evs = [torch.cuda.Event() for _ in range(2)]
+    engine.enqueue(bound, locs[0], acts[0])
+    inflight, rounds, r = 1, 0, 0
+    while True:
+        s = r & 1
+        buf[:Q].copy_(locs[s])
+        buf[Q:].copy_(acts[s].to(torch.float64).neg_())
+        dist.all_reduce(buf, op=dist.ReduceOp.MIN, group=group)
+        bound.copy_(buf[:Q])
+        flag[s:s + 1].copy_(buf[Q:], non_blocking=True)
+        evs[s].record()
+        rounds += 1
+        if rounds < max_rounds:
+            engine.enqueue(bound, locs[s ^ 1], acts[s ^ 1])
+            inflight += 1
+        engine.wait()
+        inflight -= 1
+        evs[s].synchronize()
+        if float(flag[s]) == 0.0 or rounds >= max_rounds:       # no rank has an active query
+            break
+        r += 1
+    while inflight:
+        engine.wait()
+        inflight -= 1
+    ids, d, stats = _finish(engine, group, world)
     return ids, d, stats, rounds
 
 

@@ -148,11 +148,13 @@ def sharded_leaf_min_distances(index, queries, rank: int, world: int, *, gather:
     return local, full, (a, b)
 
 
-def leaf_bounds(index, queries, mode: int = 1):
-    """(qsumm, lb) of queries against every LEAF envelope, columns in ascending leaf id."""
+def leaf_bounds(index, queries, mode: int = 1, dindex=None):
+    """(qsumm, lb) of queries against every LEAF envelope, columns in ascending leaf id.
+    dindex: the DeviceIndex whose device runs it (a leaf shard is enough: the
+    envelopes of every leaf are host data)."""
     torch = _lib.require_cuda()
     t = as_tree(index)
-    di = t.device()
+    di = dindex if dindex is not None else t.device()
     leaf_ids = t.leaf_ids
     if not hasattr(di, "_leaf_env"):
         di._leaf_env = (torch.from_numpy(np.ascontiguousarray(t.env_min[leaf_ids].T)).to(di.device),
@@ -171,14 +173,21 @@ def leaf_bounds(index, queries, mode: int = 1):
 
 
 def collect_targets(index, selected_leaves, queries, calibration_count: int, *,
-                    train_nn: bool = True) -> GlobalTrainSet:
+                    train_nn: bool = True, shard=None) -> GlobalTrainSet:
     """GPU twin of traingen.collect_targets (traingen.py:147-220).
 
     train_nn=False skips the pass-2 walk for the training rows (nn_distance[:c0]
     is then NaN): enhance() reads only the calibration rows' nn_distance, and the
-    walk needs distances to every non-selected leaf it reaches."""
+    walk needs distances to every non-selected leaf it reaches.
+    shard=(rank, world, group): leaf-sharded -- this rank computes
+    every query's minimum distance to ITS leaves only; the columns of all ranks are
+    all-gathered (same kernel per column, so the matrices equal the unsharded ones)."""
     torch = _lib.require_cuda()
     t = as_tree(index)
+    if shard is not None and shard[1] > 1:
+        if not train_nn:
+            return _collect_targets_sharded(t, selected_leaves, queries, calibration_count, *shard)
+        raise ValueError("the sharded collection computes the calibration rows' nn_distance only (train_nn=False)")
     di = t.device()
     Qh = np.atleast_2d(np.asarray(queries, dtype=np.float64))
     n_q = Qh.shape[0]
@@ -240,6 +249,33 @@ def collect_targets(index, selected_leaves, queries, calibration_count: int, *,
     return GlobalTrainSet(Qh, selected, dsel_h, nn, leaf_ids, lbh, orh, calibration_count, dcal_h)
 
 
+def _collect_targets_sharded(t, selected_leaves, queries, calibration_count: int, rank: int, world: int,
+                             group=None) -> GlobalTrainSet:
+    torch = _lib.require_cuda()
+    di = t.shard(rank, world)
+    Qh = np.atleast_2d(np.asarray(queries, dtype=np.float64))
+    n_q = Qh.shape[0]
+    if not 1 <= calibration_count < n_q:
+        raise ValueError("calibration_count must be in [1, n_queries)")
+    selected = sorted(int(s) for s in selected_leaves)
+    leaf_ids = t.leaf_ids.astype(np.int64)
+    unknown = set(selected) - set(int(i) for i in leaf_ids)
+    if unknown:
+        raise ValueError(f"unknown leaf ids in selection: {sorted(unknown)}")
+    q = torch.from_numpy(Qh.astype(np.float32)).to(di.device)
+    _, lb = leaf_bounds(t, q, mode=1, dindex=di)
+    order = torch.sort(lb, dim=1, stable=True).indices.to(torch.int32)
+    _, full, _ = sharded_leaf_min_distances(t, q, rank, world, gather=True, group=group)
+    sel_cols = np.searchsorted(leaf_ids, np.asarray(selected, dtype=np.int64))
+    c0 = n_q - calibration_count
+    dsel_h = full[:, torch.as_tensor(sel_cols, device=full.device)].cpu().numpy()
+    dcal_h = full[c0:].cpu().numpy()
+    nn = np.full(n_q, np.nan)
+    nn[c0:] = dcal_h.min(axis=1)
+    return GlobalTrainSet(Qh, selected, dsel_h, nn, leaf_ids, lb.cpu().numpy(), order.cpu().numpy(),
+                          calibration_count, dcal_h)
+
+
 def collect_local_targets(index, local: LocalQueries) -> LocalQueries:
     """GPU twin of traingen.collect_local_targets (traingen.py:135-144)."""
     t = as_tree(index)
@@ -263,11 +299,12 @@ def own_leaf_bounds(t, leaf_id: int, queries: np.ndarray) -> np.ndarray:
     return np.sqrt(acc)
 
 
-def local_targets_all(index, queries_by_leaf: dict, path: str | None = None) -> dict:
-    """{leaf_id: queries} -> {leaf_id: (targets, lbs)} in one lf_local_min_dist launch per 65535 leaves."""
+def local_targets_all(index, queries_by_leaf: dict, path: str | None = None, dindex=None) -> dict:
+    """{leaf_id: queries} -> {leaf_id: (targets, lbs)} in one lf_local_min_dist launch per 65535 leaves.
+    dindex: a DeviceIndex (e.g. this rank's leaf shard) holding every leaf asked for."""
     torch = _lib.require_cuda()
     t = as_tree(index)
-    di = t.device()
+    di = dindex if dindex is not None else t.device()
     path = path or default_path(t, di)
     fn = {"q8": _lib.lib().lf_local_min_dist_q8,
           "tc": _lib.lib().lf_local_min_dist_tc}.get(path, _lib.lib().lf_local_min_dist)

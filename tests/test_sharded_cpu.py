@@ -157,12 +157,13 @@ def _run(world, case):
     return sorted(res, key=lambda r: r[0])
 
 
-@pytest.mark.parametrize("k", [1, 4])
-def test_sharded_exact_equals_oracle(k):
-    res = _run(2, {"k": k, "f": 1.0, "filters": False})
-    (_, ids0, d0, st0, _), (_, ids1, d1, st1, _) = res
-    np.testing.assert_array_equal(ids0, ids1)                   # every rank holds the merged answer
-    np.testing.assert_array_equal(st0, st1)
+@pytest.mark.parametrize("k,world", [(1, 2), (4, 2), (1, 4), (3, 4)])
+def test_sharded_exact_equals_oracle(k, world):
+    res = _run(world, {"k": k, "f": 1.0, "filters": False})
+    ids0, d0, st0 = res[0][1], res[0][2], res[0][3]
+    for _, ids1, _, st1, _ in res[1:]:
+        np.testing.assert_array_equal(ids0, ids1)               # every rank holds the merged answer
+        np.testing.assert_array_equal(st0, st1)
     data = lo.randwalk(3000, 32, 5)
     tree = lo.build_tree(data, 100)
     Q = np.concatenate([lo.noisy_queries(data, 8, nz, 40 + int(10 * nz)) for nz in (0.1, 0.3)])
