@@ -177,7 +177,7 @@ def setup_workload(args, device, rank: int = 0, world: int = 1):
                            for i, nz in enumerate(NOISE_LEVELS)]).contiguous()
     del X
     if world > 1:
-        tree.values = None                   # the rank keeps its shard's rows only
+        tree.release_rows()                  # the rank keeps its shard's rows only
     torch.cuda.empty_cache()
     t0 = time.perf_counter()
     if world > 1:
@@ -418,6 +418,25 @@ def ncu_traffic():
     return None, None
 
 
+def bounds_roofline(tree, nQ: int, ms: float, hbm: float, peak_src: str) -> dict:
+    """Roofline entry of the bound + visit-order phase: algorithmic
+    bytes = envelopes once per batch (nodes x 2 l x 8 B) + per query and node its
+    bound and id written and read by the sort (Q x nodes x 12 B); also the bytes
+    this implementation actually moves (bound matrix written and read, 8 B per
+    (query, node) each way, leaf records 28 B per (query, leaf))."""
+    nodes, L, l = tree.n_nodes, tree.n_leaves, tree.n_seg
+    alg = nodes * 2 * l * 8 + nQ * nodes * 12
+    moved = nodes * 2 * l * 8 + nQ * nodes * 16 + nQ * L * 28
+    return {"kernels": "paa_kernel + lb_tile_kernel (bound matrix, L2-resident) + leaf_order_kernel (counting sort "
+                       "of the leaves, gap bounds of the internal nodes, leaf records)",
+            "bound": "latency (one CTA per query; see profiles/r02)", "ms": ms,
+            "algorithmic_bytes": alg, "achieved": alg / (ms / 1e3) / 1e9 if ms > 0 else None,
+            "peak": hbm, "unit": "GB/s", "frac": alg / (ms / 1e3) / 1e9 / hbm if ms > 0 else None,
+            "peak_source": peak_src,
+            "moved_bytes": moved, "moved_GBps": moved / (ms / 1e3) / 1e9 if ms > 0 else None,
+            "definition": "algorithmic: nodes x 2 x segments x 8 B + queries x nodes x (8 B bound + 4 B id)"}
+
+
 def run_ours(args, rank, world, device):
     import torch
     import torch.distributed as dist
@@ -500,7 +519,7 @@ def run_ours(args, rank, world, device):
     torch.cuda.synchronize()
     if args.ncu:
         torch.cuda.cudart().cudaProfilerStart()
-    scan_ms, scan_launches, kernels = 0.0, 0, 0
+    scan_ms, scan_launches, kernels, bounds_ms = 0.0, 0, 0, 0.0
     ea_rows, ea_surv, refills, pred_ms, lazy_pairs, pred_steps = 0.0, 0.0, 0.0, 0.0, 0.0, 0.0
     stream_b, exact_b = 0.0, 0.0
     with ClockSampler(torch.cuda.current_device()) as clk:
@@ -510,6 +529,7 @@ def run_ours(args, rank, world, device):
         for _ in range(args.steps):
             step(prof)
             scan_ms += prof[2]
+            bounds_ms += prof[0]
             scan_launches += int(prof[4])
             ea_rows += prof[8]
             ea_surv += prof[9]
@@ -687,6 +707,7 @@ def run_ours(args, rank, world, device):
                                    "bounds+sort": prof[0], "plan": prof[1],
                                    "scan": prof[2], "merge": prof[3], "lf_search_total": prof[6]},
         },
+        "bounds_roofline": bounds_roofline(tree, nQ, bounds_ms / args.steps, hbm, peak_src),
         "filter_inference": {
             "mode": ("lazy, inside lf_search: windows of the reachable (query, leaf) pairs predicted by a "
                      "tcgen05 tf32 pair GEMM, bit-identical to the dense kernel") if args.lazy else

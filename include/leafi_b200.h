@@ -98,14 +98,14 @@ typedef struct lf_search_opts {
 } lf_search_opts;
 
 #define LF_N_PROF 15
-#define LF_PROF_BOUNDS_MS 0      /* segment means + node bounds + visit-order sort */
+#define LF_PROF_BOUNDS_MS 0      /* segment means + node bounds + leaf visit orders (records) */
 #define LF_PROF_PLAN_MS 1        /* plan + chunk offsets, all rounds */
 #define LF_PROF_SCAN_MS 2        /* leaf-scan kernel, all rounds */
 #define LF_PROF_MERGE_MS 3       /* top-k merge, all rounds */
 #define LF_PROF_ROUNDS 4         /* rounds executed */
 #define LF_PROF_KERNELS 5        /* kernels launched by the library (own kernels; CUB sort counted as 1) */
 #define LF_PROF_TOTAL_MS 6       /* whole call, first to last event */
-#define LF_PROF_REFILLS 7        /* queries whose sorted visit-order prefix was completed */
+#define LF_PROF_REFILLS 7        /* reserved (0) */
 #define LF_PROF_EA_ROWS 8        /* rows tested by the early-abandon scan */
 #define LF_PROF_EA_SURVIVORS 9   /* rows that survived the first 64-dim test */
 #define LF_PROF_PREDICT_MS 10    /* lazy filter inference (pairs, gather, tensor-core GEMM) */

@@ -649,6 +649,7 @@ static int session_begin(lf_session* ss) {
     oa.lazy = ss->lazy ? 1 : 0;
     int rc = bounds_and_order(ss->d_q, Q, idx, ss->qsumm.as<double>(), ss->lb.as<double>(), oa, st, &nk);
     if (rc) return rc;
+    if (ss->prof) LF_CUDA(cudaEventRecord(ss->ev[1], st));     // LF_PROF_BOUNDS_MS: means + bounds + order
     ss->kernels += nk;
 
     s.order = oa.order;
@@ -714,7 +715,7 @@ static int session_begin(lf_session* ss) {
         if (rq) return rq;
         ++ss->kernels;
     }
-    if (ss->prof) LF_CUDA(cudaEventRecord(ss->ev[1], st));
+    if (ss->prof) LF_CUDA(cudaEventRecord(ss->ev[2], st));
     return LF_OK;
 }
 

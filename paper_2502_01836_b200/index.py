@@ -74,6 +74,21 @@ class DeviceRows:
         return self.shape[0]
 
 
+class ReleasedRows:
+    """Stand-in for a collection whose rows were dropped (a leaf-sharded rank keeps
+    only its shard's rows): the shape stays known, any row access raises."""
+
+    def __init__(self, shape):
+        self.shape = tuple(shape)
+        self.dtype = np.float32
+
+    def __getitem__(self, ids):
+        raise RuntimeError("the collection rows were released on this rank (leaf shard only)")
+
+    def __len__(self) -> int:
+        return self.shape[0]
+
+
 @dataclass
 class TreeIndex:
     values: object                  # fp32 [n, m] host ndarray, or DeviceRows (original row order)
@@ -91,6 +106,11 @@ class TreeIndex:
     member_ptr: np.ndarray          # int64 [nodes + 1]; internal nodes have empty ranges
     members: np.ndarray             # int64 [n]
     _device: dict = field(default_factory=dict, repr=False, compare=False)
+
+    def release_rows(self) -> None:
+        """Drop the full collection (e.g. after a rank built its leaf shard); the
+        device images already built keep their own rows."""
+        self.values = ReleasedRows(self.values.shape)
 
     # ------------------------------------------------------------- shape --
     @property

@@ -86,9 +86,11 @@ def _enhance_worker(rank, world, port, q):
                "exd": ex.dists, "d": res.dists, "shard": t.shard(rank, world).leaf_range}
         if rank == 0:          # the unsharded collection of the same queries, for comparison
             ref = collect_targets(t, g.selected_leaves, g.queries, 60, train_nn=False)
-            out["eq"] = all(np.array_equal(a, b) for a, b in (
-                (g.lb_matrix, ref.lb_matrix), (g.visit_order, ref.visit_order), (g.dl_selected, ref.dl_selected),
-                (g.dl_calib_full, ref.dl_calib_full), (g.nn_distance[60:], ref.nn_distance[60:])))
+            out["eq"] = {name: (bool(np.array_equal(a, b)), float(np.nanmax(np.abs(a - b))) if a.shape == b.shape
+                                else str((a.shape, b.shape))) for name, a, b in (
+                ("lb", g.lb_matrix, ref.lb_matrix), ("order", g.visit_order, ref.visit_order),
+                ("dsel", g.dl_selected, ref.dl_selected), ("dcal", g.dl_calib_full, ref.dl_calib_full),
+                ("nn", g.nn_distance[-60:], ref.nn_distance[-60:]))}
             out["selected"] = list(g.selected_leaves)
             out["leaf_ids"] = [int(l) for l in t.leaf_ids]
         q.put(out)
@@ -117,7 +119,7 @@ def test_sharded_enhance_two_ranks_gloo():
         p.join(timeout=60)
         assert p.exitcode == 0
     o0, o1 = outs
-    assert o0["eq"], "sharded training-data generation must equal the unsharded collection"
+    assert all(v[0] for v in o0["eq"].values()), o0["eq"]
     assert o0["offs"] == o1["offs"]
     for o in outs:
         a, b = o["shard"]
