@@ -64,6 +64,11 @@ typedef struct lf_index {
     const double* d_mu;          /* [m] */
     const int8_t* d_Xp;          /* [n_series][pca_k] */
     const float* d_pmeta;        /* [n_series][4] */
+    /* optional EAPCA envelopes (NULL = the reference's mean-only bound): per node the
+       [min, max] of its members' segment standard deviations, SoA [n_seg][n_nodes];
+       with them the search bound is the EAPCA bound (lf_bounds_eapca) */
+    const double* d_sd_min;
+    const double* d_sd_max;
 } lf_index;
 
 /* Options of one batched search (tree.py:220-229 search_engine keyword args). */
@@ -148,6 +153,20 @@ int64_t lf_abi_offsetof(const char* type_name, const char* field_name);
 int lf_bounds(const float* d_queries, int64_t Q, const lf_index* idx,
               const double* d_env_min, const double* d_env_max, int32_t n_env,
               int32_t lb_mode, double* d_qsumm, double* d_lb, void* stream);
+
+/*
+ * EAPCA bound (DSTree's mean + standard deviation summary; no reference code --
+ * the reference envelope keeps means only, summarize.py:59-107): per segment the
+ * reference mean and sd = sqrt(sum (x_t - mean)^2 / w) (left-to-right fp64 sum),
+ * lb = sqrt(sum_i w_i (gm_i^2 + gs_i^2)) with gm / gs the gaps of the query's
+ * mean / sd to the node's [min, max] (summarize.py:97-107 shape).  d_qsumm
+ * [Q][2 n_seg] receives the query means then sds; d_lb [Q][n_env].
+ */
+int lf_bounds_eapca(const float* d_queries, int64_t Q, const lf_index* idx, const double* d_env_min,
+                    const double* d_env_max, const double* d_sd_min, const double* d_sd_max, int32_t n_env,
+                    double* d_qsumm, double* d_lb, void* stream);
+/* Per-row EAPCA summaries of device rows: d_out [n][2 n_seg] = means then sds. */
+int lf_eapca_device(const float* d_values, int64_t n, int32_t m, int32_t n_seg, double* d_out, void* stream);
 
 /*
  * Batched best-first search: bounds, per-query (lb, node id) visit order,

@@ -128,6 +128,78 @@ def lb_matrix(qsumms: np.ndarray, mins: np.ndarray, maxs: np.ndarray, widths: np
 
 
 # ---------------------------------------------------------------------------
+# EAPCA bound (north_star "EAPCA/SAX summarisation bounds").
+# PARITY UNPINNED: the reference has no EAPCA code (its envelopes keep segment
+# means only, summarize.py:59-107).  This is the repository's
+# own CPU restatement of the DSTree EAPCA bound in the shape of
+# summarize.py:97-107, defined so the GPU can reproduce it bit for bit:
+#   per segment i (start s_i, width w_i):
+#     mean_i = the reference segment mean (paa: np.add.reduceat / w_i);
+#     sd_i   = sqrt(S_i / w_i), S_i = sum over t of (x_t - mean_i)^2 added LEFT
+#              TO RIGHT in fp64 (population stdev);
+#   node envelope: [min, max] of the members' means (the reference envelope)
+#   and of their sds;
+#   lb^2 = sum_i w_i * (gm_i^2 + gs_i^2), left to right, no fused multiply-add,
+#   gm_i = max(mean_min - mu_q, mu_q - mean_max, 0), gs_i likewise for sd.
+# Sound: per segment, ||q - x||^2 = w (mu_q - mu_x)^2 + ||q~ - x~||^2 and
+# ||q~ - x~|| >= | ||q~|| - ||x~|| | = sqrt(w) |sd_q - sd_x|.
+# ---------------------------------------------------------------------------
+
+def eapca(values: np.ndarray, starts: np.ndarray, widths: np.ndarray) -> tuple:
+    """(means, sds), each [n, l] (or [l] for one series)."""
+    v = np.asarray(values, dtype=np.float64)
+    one = v.ndim == 1
+    v = np.atleast_2d(v)
+    mu = paa(v, starts, widths)
+    sd = np.empty_like(mu)
+    for i, (s, w) in enumerate(zip(starts, widths)):
+        acc = np.zeros(v.shape[0])
+        for t in range(int(s), int(s + w)):
+            d = v[:, t] - mu[:, i]
+            acc = acc + d * d
+        sd[:, i] = np.sqrt(acc / float(w))
+    return (mu[0], sd[0]) if one else (mu, sd)
+
+
+def eapca_envelopes(t: "OracleTree") -> tuple:
+    """Per node [min, max] of the members' segment sds (internal nodes: all descendants)."""
+    _, sd = eapca(t.values, t.starts, t.widths)
+    l = t.widths.shape[0]
+    smin = [np.full(l, math.inf) for _ in range(t.n_nodes)]
+    smax = [np.full(l, -math.inf) for _ in range(t.n_nodes)]
+    for nid in reversed(range(t.n_nodes)):          # children have larger ids than parents
+        if t.is_leaf(nid):
+            ids = t.members[nid]
+            if ids.size:
+                smin[nid] = sd[ids].min(axis=0)
+                smax[nid] = sd[ids].max(axis=0)
+        else:
+            for c in (t.left[nid], t.right[nid]):
+                smin[nid] = np.minimum(smin[nid], smin[c])
+                smax[nid] = np.maximum(smax[nid], smax[c])
+    return smin, smax
+
+
+def node_lb_eapca(qmu, qsd, mn, mx, smn, smx, widths) -> float:
+    """The EAPCA bound of one node (definition above)."""
+    return float(lb_matrix_eapca(np.atleast_2d(qmu), np.atleast_2d(qsd), np.atleast_2d(mn), np.atleast_2d(mx),
+                                 np.atleast_2d(smn), np.atleast_2d(smx), widths)[0, 0])
+
+
+def lb_matrix_eapca(qmu, qsd, mins, maxs, smins, smaxs, widths) -> np.ndarray:
+    """All (query, node) EAPCA bounds [Q, nodes]."""
+    qmu, qsd = np.atleast_2d(qmu), np.atleast_2d(qsd)
+    acc = np.zeros((qmu.shape[0], mins.shape[0]))
+    for i in range(widths.shape[0]):
+        gm = np.maximum(mins[None, :, i] - qmu[:, None, i], qmu[:, None, i] - maxs[None, :, i])
+        gm = np.maximum(gm, 0.0)
+        gs = np.maximum(smins[None, :, i] - qsd[:, None, i], qsd[:, None, i] - smaxs[None, :, i])
+        gs = np.maximum(gs, 0.0)
+        acc = acc + float(widths[i]) * (gm * gm + gs * gs)
+    return np.sqrt(acc)
+
+
+# ---------------------------------------------------------------------------
 # distances (series.py)
 # ---------------------------------------------------------------------------
 
@@ -325,8 +397,10 @@ class OracleOutcome:
 
 
 def search(t: OracleTree, q, k: int = 1, bsf_factor: float = 1.0, predictors=None,
-           offsets=None, want_trace: bool = False) -> OracleOutcome:
-    """tree.py:220-297: best-first traversal, cascade lb -> filter -> scan."""
+           offsets=None, want_trace: bool = False, eapca_env=None) -> OracleOutcome:
+    """tree.py:220-297: best-first traversal, cascade lb -> filter -> scan.
+    eapca_env=(sd_min, sd_max) (eapca_envelopes): the EAPCA bound replaces the
+    reference's mean-only bound (same traversal, unpinned extension)."""
     q = np.ascontiguousarray(q, dtype=np.float64)
     if q.ndim != 1 or q.shape[0] != t.values.shape[1]:
         raise ValueError("query length mismatch")
@@ -337,10 +411,19 @@ def search(t: OracleTree, q, k: int = 1, bsf_factor: float = 1.0, predictors=Non
     if any(lid not in offsets for lid in predictors):
         raise ValueError("missing offsets")
     qs = paa(q, t.starts, t.widths)
+    if eapca_env is not None:
+        qmu, qsd = eapca(q, t.starts, t.widths)
+
+        def bound(nid):
+            return node_lb_eapca(qmu, qsd, t.env_min[nid], t.env_max[nid], eapca_env[0][nid], eapca_env[1][nid],
+                                 t.widths)
+    else:
+        def bound(nid):
+            return node_lb(qs, t.env_min[nid], t.env_max[nid], t.widths)
     best = KBest(k)
     st = dict.fromkeys(STAT_KEYS, 0)
     trace = [] if want_trace else None
-    heap = [(node_lb(qs, t.env_min[0], t.env_max[0], t.widths), 0)]
+    heap = [(bound(0), 0)]
     while heap:
         lb, nid = heapq.heappop(heap)
         bsf = best.bsf
@@ -354,7 +437,7 @@ def search(t: OracleTree, q, k: int = 1, bsf_factor: float = 1.0, predictors=Non
             break
         if not leaf:
             for c in (t.left[nid], t.right[nid]):
-                heapq.heappush(heap, (node_lb(qs, t.env_min[c], t.env_max[c], t.widths), c))
+                heapq.heappush(heap, (bound(c), c))
             continue
         st["leaves_visited"] += 1
         f = predictors.get(nid)

@@ -42,6 +42,8 @@ class LfIndex(C.Structure):
         ("d_mu", C.c_void_p),
         ("d_Xp", C.c_void_p),
         ("d_pmeta", C.c_void_p),
+        ("d_sd_min", C.c_void_p),
+        ("d_sd_max", C.c_void_p),
     ]
 
 
@@ -121,6 +123,8 @@ SIGNATURES = {
     "lf_paa_host": (C.c_int, [_P, _I64, _I32, _I32, _P, _I32]),
     "lf_tree_build_from_summaries": (_P, [_P, _I64, _I32, _I64]),
     "lf_paa_device": (C.c_int, [_P, _I64, _I32, _I32, _P, _P]),
+    "lf_eapca_device": (C.c_int, [_P, _I64, _I32, _I32, _P, _P]),
+    "lf_bounds_eapca": (C.c_int, [_P, _I64, C.POINTER(LfIndex), _P, _P, _P, _P, _I32, _P, _P, _P]),
     "lf_quantize_rows": (C.c_int, [_P, _I64, _I32, _P, _P, _P]),
     "lf_replay_offsets": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _P, _I64, _I32, _P, _P]),
 }

@@ -25,33 +25,61 @@ __global__ void paa_kernel(const float* __restrict__ q, int64_t Q, lf_index idx,
     qsumm[t] = segment_mean(q + qi * idx.m, idx.seg_start[s], idx.seg_width[s]);
 }
 
-// lb[q][node] for nodes of one query row; segment means staged in smem.
+// One thread per (query, segment): EAPCA summary, means then sds ([Q][2 n_seg]).
+__global__ void eapca_kernel(const float* __restrict__ q, int64_t Q, lf_index idx, double* __restrict__ out) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= Q * idx.n_seg) return;
+    const int64_t qi = t / idx.n_seg;
+    const int s = (int)(t - qi * idx.n_seg);
+    const float* row = q + qi * idx.m;
+    const double mu = segment_mean(row, idx.seg_start[s], idx.seg_width[s]);
+    out[qi * 2 * idx.n_seg + s] = mu;
+    out[qi * 2 * idx.n_seg + idx.n_seg + s] = segment_sd(row, idx.seg_start[s], idx.seg_width[s], mu);
+}
+
+// max(mn - q, q - mx, 0) (summarize.py:103-104): mn <= mx, so at most one of the
+// two differences is positive -- selects instead of fmax, bit-identical.
+__device__ __forceinline__ double env_gap(double mn, double mx, double q) {
+    const double a = mn - q, b = q - mx;
+    return a > 0.0 ? a : (b > 0.0 ? b : 0.0);
+}
+
+// The per-segment term of each bound mode, folded into acc:
+//   0: np.dot(widths * gap, gap) -- one FMA chain (search path, summarize.py:107)
+//   1: einsum("qns,qns,s")        -- sequential (g * g) * w (traingen, summarize.py:114-122)
+//   2: EAPCA                      -- acc + w * (gm^2 + gs^2), no FMA (oracle eapca definition)
+template <int MODE>
+__device__ __forceinline__ double bound_term(double acc, double w, double gm, double gs) {
+    if (MODE == 0) return __fma_rn(__dmul_rn(w, gm), gm, acc);
+    if (MODE == 1) return __dadd_rn(acc, __dmul_rn(__dmul_rn(gm, gm), w));
+    return __dadd_rn(acc, __dmul_rn(w, __dadd_rn(__dmul_rn(gm, gm), __dmul_rn(gs, gs))));
+}
+
+// lb[q][node] for nodes of one query row; query summaries staged in smem
+// (any n_seg; MODE 2 reads means then sds, [2 n_seg] per query).
 template <int MODE>
 __global__ void lb_kernel(const double* __restrict__ qsumm, int64_t Q, int n_seg, lf_index idx,
                           const double* __restrict__ env_min, const double* __restrict__ env_max,
+                          const double* __restrict__ sd_min, const double* __restrict__ sd_max,
                           int n_env, double* __restrict__ lb) {
-    __shared__ double qs[LF_MAX_SEG];
+    __shared__ double qs[2 * LF_MAX_SEG];
     __shared__ double ws[LF_MAX_SEG];
+    const int qw = MODE == 2 ? 2 * n_seg : n_seg;
     for (int64_t qi = blockIdx.y; qi < Q; qi += gridDim.y) {
         __syncthreads();
-        if (threadIdx.x < n_seg) {
-            qs[threadIdx.x] = qsumm[qi * n_seg + threadIdx.x];
-            ws[threadIdx.x] = (double)idx.seg_width[threadIdx.x];
-        }
+        if (threadIdx.x < qw) qs[threadIdx.x] = qsumm[qi * qw + threadIdx.x];
+        if (threadIdx.x < n_seg) ws[threadIdx.x] = (double)idx.seg_width[threadIdx.x];
         __syncthreads();
         for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < n_env;
              node += gridDim.x * blockDim.x) {
             double acc = 0.0;
             for (int s = 0; s < n_seg; ++s) {
-                double mn = env_min[(int64_t)s * n_env + node];
-                double mx = env_max[(int64_t)s * n_env + node];
-                double g = fmax(mn - qs[s], qs[s] - mx);
-                g = fmax(g, 0.0);
-                if (MODE == 0) {
-                    acc = __fma_rn(__dmul_rn(ws[s], g), g, acc);          // np.dot(widths*gap, gap)
-                } else {
-                    acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(g, g), ws[s]));  // einsum qns,qns,s
-                }
+                const double gm = env_gap(env_min[(int64_t)s * n_env + node], env_max[(int64_t)s * n_env + node],
+                                          qs[s]);
+                const double gs = MODE == 2 ? env_gap(sd_min[(int64_t)s * n_env + node],
+                                                      sd_max[(int64_t)s * n_env + node], qs[n_seg + s])
+                                            : 0.0;
+                acc = bound_term<MODE>(acc, ws[s], gm, gs);
             }
             lb[qi * n_env + node] = sqrt(acc);
         }
@@ -69,29 +97,36 @@ constexpr int LBT_Q = 16;
 constexpr int LBT_SEG = 8;
 
 template <int MODE>
-__global__ void __launch_bounds__(LBT_NODES, 4) lb_tile_kernel(const double* __restrict__ qsumm, int64_t Q, int ns,
-                                                               lf_index idx, const double* __restrict__ env_min,
-                                                               const double* __restrict__ env_max, int n_env,
-                                                               double* __restrict__ lb, unsigned* __restrict__ qmax,
-                                                               unsigned* __restrict__ qmin) {
-    __shared__ double qs[LBT_Q][LBT_SEG];
+__global__ void __launch_bounds__(LBT_NODES, MODE == 2 ? 2 : 4)
+    lb_tile_kernel(const double* __restrict__ qsumm, int64_t Q, int ns, lf_index idx,
+                   const double* __restrict__ env_min, const double* __restrict__ env_max,
+                   const double* __restrict__ sd_min, const double* __restrict__ sd_max, int n_env,
+                   double* __restrict__ lb, unsigned* __restrict__ qmax, unsigned* __restrict__ qmin) {
+    constexpr int QW = MODE == 2 ? 2 * LBT_SEG : LBT_SEG;
+    __shared__ double qs[LBT_Q][QW];
     __shared__ double ws[LBT_SEG];
     const int node = blockIdx.x * LBT_NODES + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const int64_t q0 = (int64_t)blockIdx.y * LBT_Q;
-    for (int i = threadIdx.x; i < LBT_Q * ns; i += LBT_NODES) {
-        const int qq = i / ns, sg = i - qq * ns;
-        qs[qq][sg] = q0 + qq < Q ? qsumm[(q0 + qq) * ns + sg] : 0.0;
+    const int qw = MODE == 2 ? 2 * ns : ns;
+    for (int i = threadIdx.x; i < LBT_Q * qw; i += LBT_NODES) {
+        const int qq = i / qw, sg = i - qq * qw;
+        const int col = MODE == 2 && sg >= ns ? LBT_SEG + (sg - ns) : sg;
+        qs[qq][col] = q0 + qq < Q ? qsumm[(q0 + qq) * qw + sg] : 0.0;
     }
     if (threadIdx.x < ns) ws[threadIdx.x] = (double)idx.seg_width[threadIdx.x];
     __syncthreads();
     const bool valid = node < n_env;
     const bool isl = qmax != nullptr && valid && __ldg(idx.d_node_leaf + node) >= 0;
-    double mn[LBT_SEG], mx[LBT_SEG];
+    double mn[LBT_SEG], mx[LBT_SEG], smn[MODE == 2 ? LBT_SEG : 1], smx[MODE == 2 ? LBT_SEG : 1];
 #pragma unroll
     for (int sg = 0; sg < LBT_SEG; ++sg) {
         mn[sg] = (valid && sg < ns) ? __ldg(env_min + (int64_t)sg * n_env + node) : 0.0;
         mx[sg] = (valid && sg < ns) ? __ldg(env_max + (int64_t)sg * n_env + node) : 0.0;
+        if constexpr (MODE == 2) {
+            smn[sg] = (valid && sg < ns) ? __ldg(sd_min + (int64_t)sg * n_env + node) : 0.0;
+            smx[sg] = (valid && sg < ns) ? __ldg(sd_max + (int64_t)sg * n_env + node) : 0.0;
+        }
     }
     const int qn = (int)min((int64_t)LBT_Q, Q - q0);
     for (int qq = 0; qq < qn; ++qq) {
@@ -99,13 +134,10 @@ __global__ void __launch_bounds__(LBT_NODES, 4) lb_tile_kernel(const double* __r
 #pragma unroll
         for (int sg = 0; sg < LBT_SEG; ++sg) {
             if (sg < ns) {
-                // max(mn - q, q - mx, 0) (summarize.py:103-104): mn <= mx, so at most one
-                // of the two differences is positive -- selects instead of fmax
-                const double qv = qs[qq][sg];
-                const double a = mn[sg] - qv, b = qv - mx[sg];
-                const double g = a > 0.0 ? a : (b > 0.0 ? b : 0.0);
-                if (MODE == 0) acc = __fma_rn(__dmul_rn(ws[sg], g), g, acc);
-                else acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(g, g), ws[sg]));
+                const double gm = env_gap(mn[sg], mx[sg], qs[qq][sg]);
+                double gs = 0.0;
+                if constexpr (MODE == 2) gs = env_gap(smn[sg], smx[sg], qs[qq][LBT_SEG + sg]);
+                acc = bound_term<MODE>(acc, ws[sg], gm, gs);
             }
         }
         const double v = sqrt(acc);
@@ -124,12 +156,16 @@ __global__ void __launch_bounds__(LBT_NODES, 4) lb_tile_kernel(const double* __r
 
 int launch_bounds(const float* d_q, int64_t Q, const lf_index& idx, const double* env_min,
                   const double* env_max, int n_env, int mode, double* d_qsumm, double* d_lb,
-                  cudaStream_t st, unsigned* d_qmax, unsigned* d_qmin) {
+                  cudaStream_t st, unsigned* d_qmax, unsigned* d_qmin, const double* sd_min,
+                  const double* sd_max) {
     if (Q == 0) return LF_OK;
     {
         int64_t n = Q * idx.n_seg;
         int thr = 256;
-        paa_kernel<<<(unsigned)((n + thr - 1) / thr), thr, 0, st>>>(d_q, Q, idx, d_qsumm);
+        if (mode == 2)
+            eapca_kernel<<<(unsigned)((n + thr - 1) / thr), thr, 0, st>>>(d_q, Q, idx, d_qsumm);
+        else
+            paa_kernel<<<(unsigned)((n + thr - 1) / thr), thr, 0, st>>>(d_q, Q, idx, d_qsumm);
         LF_CUDA(cudaGetLastError());
     }
     if (n_env == 0) return LF_OK;
@@ -139,23 +175,24 @@ int launch_bounds(const float* d_q, int64_t Q, const lf_index& idx, const double
             LF_CUDA(cudaMemsetAsync(d_qmin, 0xff, sizeof(unsigned) * Q, st));
         }
         dim3 grid((unsigned)((n_env + LBT_NODES - 1) / LBT_NODES), (unsigned)((Q + LBT_Q - 1) / LBT_Q));
-        if (mode == 0)
-            lb_tile_kernel<0><<<grid, LBT_NODES, 0, st>>>(d_qsumm, Q, idx.n_seg, idx, env_min, env_max, n_env, d_lb,
-                                                          d_qmax, d_qmin);
-        else
-            lb_tile_kernel<1><<<grid, LBT_NODES, 0, st>>>(d_qsumm, Q, idx.n_seg, idx, env_min, env_max, n_env, d_lb,
-                                                          d_qmax, d_qmin);
+#define LF_TILE(M) lb_tile_kernel<M><<<grid, LBT_NODES, 0, st>>>(d_qsumm, Q, idx.n_seg, idx, env_min, env_max, \
+                                                                sd_min, sd_max, n_env, d_lb, d_qmax, d_qmin)
+        if (mode == 0) LF_TILE(0);
+        else if (mode == 1) LF_TILE(1);
+        else LF_TILE(2);
+#undef LF_TILE
         LF_CUDA(cudaGetLastError());
         return LF_OK;
     }
+    LF_REQUIRE(d_qmax == nullptr, "leaf bound ranges need n_seg <= 8");
     dim3 block(256);
     dim3 grid((unsigned)((n_env + 255) / 256), (unsigned)(Q < 65535 ? Q : 65535));
-    if (mode == 0)
-        lb_kernel<0><<<grid, block, 0, st>>>(d_qsumm, Q, idx.n_seg, idx, env_min, env_max,
-                                             n_env, d_lb);
-    else
-        lb_kernel<1><<<grid, block, 0, st>>>(d_qsumm, Q, idx.n_seg, idx, env_min, env_max,
-                                             n_env, d_lb);
+#define LF_GEN(M) lb_kernel<M><<<grid, block, 0, st>>>(d_qsumm, Q, idx.n_seg, idx, env_min, env_max, sd_min, sd_max, \
+                                                     n_env, d_lb)
+    if (mode == 0) LF_GEN(0);
+    else if (mode == 1) LF_GEN(1);
+    else LF_GEN(2);
+#undef LF_GEN
     LF_CUDA(cudaGetLastError());
     return LF_OK;
 }
@@ -503,7 +540,9 @@ int bounds_and_order(const float* d_q, int64_t Q, const lf_index& idx, double* d
     if (fused) LF_CUDA(range.alloc(sizeof(unsigned) * 2 * Q, st));
     unsigned* qmax = fused ? range.as<unsigned>() : nullptr;
     unsigned* qmin = fused ? qmax + Q : nullptr;
-    int rc = launch_bounds(d_q, Q, idx, idx.d_env_min, idx.d_env_max, n, 0, d_qsumm, d_lb, st, qmax, qmin);
+    const bool eapca = idx.d_sd_min != nullptr && idx.d_sd_max != nullptr;
+    int rc = launch_bounds(d_q, Q, idx, idx.d_env_min, idx.d_env_max, n, eapca ? 2 : 0, d_qsumm, d_lb, st, qmax, qmin,
+                           idx.d_sd_min, idx.d_sd_max);
     if (rc) return rc;
     if (kernels) *kernels += 2;
     if (fused) {
@@ -556,6 +595,33 @@ extern "C" int lf_bounds(const float* d_queries, int64_t Q, const lf_index* idx,
     LF_REQUIRE(lb_mode == 0 || lb_mode == 1, "lb_mode must be 0 or 1");
     return lf::launch_bounds(d_queries, Q, *idx, d_env_min, d_env_max, n_env, lb_mode, d_qsumm,
                              d_lb, lf::as_stream(stream));
+}
+
+extern "C" int lf_bounds_eapca(const float* d_queries, int64_t Q, const lf_index* idx, const double* d_env_min,
+                               const double* d_env_max, const double* d_sd_min, const double* d_sd_max,
+                               int32_t n_env, double* d_qsumm, double* d_lb, void* stream) {
+    LF_REQUIRE(idx != nullptr && d_sd_min != nullptr && d_sd_max != nullptr, "NULL argument");
+    LF_REQUIRE(idx->n_seg >= 1 && idx->n_seg <= LF_MAX_SEG, "bad segment count");
+    return lf::launch_bounds(d_queries, Q, *idx, d_env_min, d_env_max, n_env, 2, d_qsumm, d_lb,
+                             lf::as_stream(stream), nullptr, nullptr, d_sd_min, d_sd_max);
+}
+
+extern "C" int lf_eapca_device(const float* d_values, int64_t n, int32_t m, int32_t n_seg, double* d_out,
+                               void* stream) {
+    LF_REQUIRE(n_seg >= 1 && n_seg <= m && n_seg <= LF_MAX_SEG, "num_segments must be in [1, length]");
+    if (n == 0) return LF_OK;
+    lf_index idx{};
+    idx.m = m;
+    idx.n_seg = n_seg;
+    const int base = m / n_seg, rem = m % n_seg;
+    for (int i = 0, s = 0; i < n_seg; ++i) {
+        idx.seg_width[i] = base + (i < rem ? 1 : 0);
+        idx.seg_start[i] = s;
+        s += idx.seg_width[i];
+    }
+    lf::eapca_kernel<<<(unsigned)((n * n_seg + 255) / 256), 256, 0, lf::as_stream(stream)>>>(d_values, n, idx, d_out);
+    LF_CUDA(cudaGetLastError());
+    return LF_OK;
 }
 
 extern "C" int lf_paa_device(const float* d_values, int64_t n, int32_t m, int32_t n_seg, double* d_out,

@@ -4,10 +4,12 @@
 #include "../../include/leafi_b200.h"
 
 namespace lf {
+// mode 0 / 1: the reference's search / traingen bound; 2: EAPCA (sd_min / sd_max).
 // d_qmax / d_qmin (nullable, [Q]): per query the range of its leaf bounds as float bits.
 int launch_bounds(const float* d_q, int64_t Q, const lf_index& idx, const double* env_min,
                   const double* env_max, int n_env, int mode, double* d_qsumm, double* d_lb,
-                  cudaStream_t st, unsigned* d_qmax = nullptr, unsigned* d_qmin = nullptr);
+                  cudaStream_t st, unsigned* d_qmax = nullptr, unsigned* d_qmin = nullptr,
+                  const double* sd_min = nullptr, const double* sd_max = nullptr);
 
 // Per-query visit-order records [Q][L] over the L LEAF slots of the index, in
 // (lb, node id) order -- the pop order of tree.py:256-275 restricted to the

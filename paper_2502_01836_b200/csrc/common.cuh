@@ -90,6 +90,21 @@ __device__ __host__ inline double segment_mean(const float* row, int start, int 
     return s / (double)width;
 }
 
+// Segment standard deviation of the EAPCA summary (oracle/leafi_oracle.py eapca):
+// sqrt(sum (x_t - mean)^2 / w), the squares added left to right, no FMA.
+__device__ __host__ inline double segment_sd(const float* row, int start, int width, double mean) {
+    double acc = 0.0;
+    for (int t = start; t < start + width; ++t) {
+        const double d = (double)row[t] - mean;
+#ifdef __CUDA_ARCH__
+        acc = __dadd_rn(acc, __dmul_rn(d, d));
+#else
+        acc = acc + d * d;
+#endif
+    }
+    return sqrt(acc / (double)width);
+}
+
 __device__ inline double warp_sum_f64(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

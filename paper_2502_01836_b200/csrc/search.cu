@@ -574,7 +574,7 @@ static int session_begin(lf_session* ss) {
 
     const int64_t max_chunks_leaf = std::max<int64_t>(1, (idx.max_leaf_rows + CH - 1) / CH);
     const int64_t max_tasks = std::max<int64_t>(1, Q * s.Rcap * max_chunks_leaf);
-    LF_CUDA(ss->qsumm.alloc(sizeof(double) * Q * idx.n_seg, st));
+    LF_CUDA(ss->qsumm.alloc(sizeof(double) * Q * idx.n_seg * (idx.d_sd_min != nullptr ? 2 : 1), st));
     LF_CUDA(ss->lb.alloc(sizeof(double) * Q * Nn, st));        // node bounds (L2-resident at 1K x 8K)
     LF_CUDA(ss->lbs.alloc(sizeof(double) * Q * L, st));        // leaf records in visit order
     LF_CUDA(ss->gap.alloc(sizeof(double) * Q * L, st));

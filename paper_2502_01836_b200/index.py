@@ -106,6 +106,46 @@ class TreeIndex:
     member_ptr: np.ndarray          # int64 [nodes + 1]; internal nodes have empty ranges
     members: np.ndarray             # int64 [n]
     _device: dict = field(default_factory=dict, repr=False, compare=False)
+    sd_min: np.ndarray | None = None  # fp64 [nodes, segments]: EAPCA envelopes (use_eapca), else None
+    sd_max: np.ndarray | None = None
+
+    def use_eapca(self) -> "TreeIndex":
+        """Switch the index to the EAPCA bound (mean + stdev per segment,
+        include/leafi_b200.h lf_bounds_eapca): per node the [min, max] of its members'
+        segment stdevs, computed on the GPU (lf_eapca_device) in row chunks.  The tree
+        (the reference's mean-based splits) is unchanged; search and training-data
+        generation then use the EAPCA bound.  Call before the first device image."""
+        torch = _lib.require_cuda()
+        if self.sd_min is not None:
+            return self
+        if self._device:
+            raise RuntimeError("use_eapca() must precede the first device image of the index")
+        n, l = self.n, self.n_seg
+        sd = np.empty((n, l))
+        src = self.values.tensor if isinstance(self.values, DeviceRows) else None
+        step = 1 << 20
+        for r0 in range(0, n, step):
+            r1 = min(n, r0 + step)
+            x = src[r0:r1] if src is not None else torch.from_numpy(
+                np.ascontiguousarray(self.values[r0:r1], dtype=np.float32)).cuda()
+            out = torch.empty((r1 - r0, 2 * l), dtype=torch.float64, device=x.device)
+            _lib.check(_lib.lib().lf_eapca_device(x.data_ptr(), r1 - r0, self.m, l, out.data_ptr(), _lib.stream_ptr()))
+            sd[r0:r1] = out[:, l:].cpu().numpy()
+        nn = self.n_nodes
+        smin = np.full((nn, l), np.inf)
+        smax = np.full((nn, l), -np.inf)
+        for nid in range(nn - 1, -1, -1):                 # children have larger ids than parents
+            if self.left[nid] < 0:
+                ids = self.members[self.member_ptr[nid]:self.member_ptr[nid + 1]]
+                if ids.size:
+                    smin[nid] = sd[ids].min(axis=0)
+                    smax[nid] = sd[ids].max(axis=0)
+            else:
+                for c in (self.left[nid], self.right[nid]):
+                    np.minimum(smin[nid], smin[c], out=smin[nid])
+                    np.maximum(smax[nid], smax[c], out=smax[nid])
+        self.sd_min, self.sd_max = smin, smax
+        return self
 
     def release_rows(self) -> None:
         """Drop the full collection (e.g. after a rank built its leaf shard); the
@@ -322,6 +362,10 @@ class DeviceIndex:
             self.node_leaf = torch.from_numpy(node_leaf).to(dev)
             self.env_min = torch.from_numpy(np.ascontiguousarray(t.env_min.T)).to(dev)
             self.env_max = torch.from_numpy(np.ascontiguousarray(t.env_max.T)).to(dev)
+            self.sd_min = self.sd_max = None
+            if t.sd_min is not None:                  # EAPCA envelopes, SoA like the means
+                self.sd_min = torch.from_numpy(np.ascontiguousarray(t.sd_min.T)).to(dev)
+                self.sd_max = torch.from_numpy(np.ascontiguousarray(t.sd_max.T)).to(dev)
             # int8 shadow for the bounded scan (scan_q8_kernel), when the layout allows it
             self.X8 = self.qmeta = None
             n_rows, m = int(self.X.shape[0]), int(self.X.shape[1])
@@ -414,6 +458,8 @@ class DeviceIndex:
         s.d_leaf_filter = None if leaf_filter is None else leaf_filter.data_ptr()
         if self.X8 is not None:
             s.d_X8, s.d_qmeta = self.X8.data_ptr(), self.qmeta.data_ptr()
+        if self.sd_min is not None:
+            s.d_sd_min, s.d_sd_max = self.sd_min.data_ptr(), self.sd_max.data_ptr()
         if getattr(self, "Xp", None) is not None:
             s.pca_k = self.pca_k
             s.d_P, s.d_mu = self.P.data_ptr(), self.mu.data_ptr()

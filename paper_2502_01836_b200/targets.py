@@ -156,19 +156,26 @@ def leaf_bounds(index, queries, mode: int = 1, dindex=None):
     t = as_tree(index)
     di = dindex if dindex is not None else t.device()
     leaf_ids = t.leaf_ids
+    eapca = t.sd_min is not None                  # the index searches with the EAPCA bound: so does TDG
     if not hasattr(di, "_leaf_env"):
-        di._leaf_env = (torch.from_numpy(np.ascontiguousarray(t.env_min[leaf_ids].T)).to(di.device),
-                        torch.from_numpy(np.ascontiguousarray(t.env_max[leaf_ids].T)).to(di.device))
-    mn, mx = di._leaf_env
+        env = [t.env_min, t.env_max] + ([t.sd_min, t.sd_max] if eapca else [])
+        di._leaf_env = tuple(torch.from_numpy(np.ascontiguousarray(a[leaf_ids].T)).to(di.device) for a in env)
+    mn, mx = di._leaf_env[:2]
     q = queries if isinstance(queries, torch.Tensor) else torch.from_numpy(
         np.ascontiguousarray(np.atleast_2d(queries), dtype=np.float32))
     q = q.to(device=di.device, dtype=torch.float32).contiguous()
     Q = q.shape[0]
-    qs = torch.empty((Q, t.n_seg), dtype=torch.float64, device=di.device)
+    qs = torch.empty((Q, t.n_seg * (2 if eapca else 1)), dtype=torch.float64, device=di.device)
     lb = torch.empty((Q, leaf_ids.shape[0]), dtype=torch.float64, device=di.device)
-    _lib.check(_lib.lib().lf_bounds(q.data_ptr(), Q, di.struct(None), mn.data_ptr(), mx.data_ptr(),
-                                    leaf_ids.shape[0], mode, qs.data_ptr(), lb.data_ptr(),
-                                    _lib.stream_ptr()))
+    if eapca:
+        smn, smx = di._leaf_env[2:]
+        _lib.check(_lib.lib().lf_bounds_eapca(q.data_ptr(), Q, di.struct(None), mn.data_ptr(), mx.data_ptr(),
+                                              smn.data_ptr(), smx.data_ptr(), leaf_ids.shape[0], qs.data_ptr(),
+                                              lb.data_ptr(), _lib.stream_ptr()))
+    else:
+        _lib.check(_lib.lib().lf_bounds(q.data_ptr(), Q, di.struct(None), mn.data_ptr(), mx.data_ptr(),
+                                        leaf_ids.shape[0], mode, qs.data_ptr(), lb.data_ptr(),
+                                        _lib.stream_ptr()))
     return qs, lb
 
 
