@@ -30,6 +30,7 @@ extern "C" {
 #define LF_EINVAL 1     /* bad argument (maps to ValueError in Python) */
 #define LF_ECUDA 2      /* CUDA runtime error (maps to RuntimeError) */
 #define LF_ENOMEM 3
+#define LF_EFORMAT 4    /* malformed LEAF file (maps to FormatError, series.py:25-31) */
 
 #define LF_MAX_SEG 64
 #define LF_N_STATS 6    /* visited, searched, lb_pruned, filter_pruned, inferences, series_scanned */
@@ -339,6 +340,28 @@ lf_tree* lf_tree_build_from_summaries(const double* h_summs, int64_t n, int32_t 
 /* Segment means of device rows (summarize_matrix, summarize.py:52-56), numpy order. */
 int lf_paa_device(const float* d_values, int64_t n, int32_t m, int32_t n_seg, double* d_out,
                   void* stream);
+
+/*
+ * Memory-lean LEAF-format loader (series.py:190-215 _save_matrix / _load_matrix;
+ * SURVEY §8(f)3).  The payload streams through a few pinned host buffers into HBM
+ * (pread by n_threads host threads, H2D, per-chunk kernels); host memory stays
+ * O(n_threads x 32 MB) instead of the reference's fp32 + fp64 copies (F7).
+ *   lf_leaf_header   -- _load_matrix's header checks; LF_EFORMAT with the
+ *                       reference's message and *err_offset (FormatError.offset)
+ *   lf_leaf_paa_file -- pass 1: segment means [n][n_seg] (lf_paa_device order) into
+ *                       d_summ; the rows are not kept
+ *   lf_leaf_load     -- pass 2: row i -> d_X[d_pos[i]] (d_pos NULL = identity,
+ *                       d_pos[i] < 0 = skipped: another rank's leaf), i.e. straight
+ *                       into the leaf-contiguous layout of lf_index.d_X
+ *   lf_leaf_save     -- write device rows [n][m] as a LEAF file (series.py:190-195)
+ * The loaders reject non-finite values (series.py:65-66) with LF_EINVAL.
+ */
+int lf_leaf_header(const char* path, int64_t* n, int32_t* m, int64_t* err_offset);
+int lf_leaf_paa_file(const char* path, int64_t n, int32_t m, int32_t n_seg, double* d_summ,
+                     int32_t n_threads, void* stream);
+int lf_leaf_load(const char* path, int64_t n, int32_t m, const int64_t* d_pos, float* d_X,
+                 int32_t n_threads, void* stream);
+int lf_leaf_save(const char* path, const float* d_X, int64_t n, int32_t m, void* stream);
 
 /* Build the int8 shadow used by the bounded leaf scan: per row r, scale_r =
  * max|x| / 127, code = rint(x / scale_r), xx_r = sum code^2, and the exact

@@ -24,13 +24,16 @@ from .engine import (
 )
 from .filters import FilterPack
 from .isax import build_isax_index
+from .leafio import FileRows, FormatError, load_dataset_device, load_index, read_header, save_dataset
 
 __version__ = "0.1.0"
 
 __all__ = [
     "BatchResult",
     "DeviceIndex",
+    "FileRows",
     "FilterPack",
+    "FormatError",
     "SearchOutcome",
     "SearchStats",
     "TraceEntry",
@@ -43,7 +46,11 @@ __all__ = [
     "epsilon_search",
     "exact_search",
     "linear_scan",
+    "load_dataset_device",
+    "load_index",
     "pruning_ratio",
+    "read_header",
+    "save_dataset",
     "search_batch",
     "search_engine",
     "segment_layout",

@@ -15,7 +15,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libleafi_b200.so"
 MAX_SEG = 64
 N_STATS = 6
 
-LF_OK, LF_EINVAL, LF_ECUDA, LF_ENOMEM = 0, 1, 2, 3
+LF_OK, LF_EINVAL, LF_ECUDA, LF_ENOMEM, LF_EFORMAT = 0, 1, 2, 3, 4
 
 
 class LfIndex(C.Structure):
@@ -125,6 +125,10 @@ SIGNATURES = {
     "lf_paa_device": (C.c_int, [_P, _I64, _I32, _I32, _P, _P]),
     "lf_eapca_device": (C.c_int, [_P, _I64, _I32, _I32, _P, _P]),
     "lf_bounds_eapca": (C.c_int, [_P, _I64, C.POINTER(LfIndex), _P, _P, _P, _P, _I32, _P, _P, _P]),
+    "lf_leaf_header": (C.c_int, [C.c_char_p, C.POINTER(_I64), C.POINTER(_I32), C.POINTER(_I64)]),
+    "lf_leaf_paa_file": (C.c_int, [C.c_char_p, _I64, _I32, _I32, _P, _I32, _P]),
+    "lf_leaf_load": (C.c_int, [C.c_char_p, _I64, _I32, _P, _P, _I32, _P]),
+    "lf_leaf_save": (C.c_int, [C.c_char_p, _P, _I64, _I32, _P]),
     "lf_quantize_rows": (C.c_int, [_P, _I64, _I32, _P, _P, _P]),
     "lf_replay_offsets": (C.c_int, [_P, _P, _P, _P, _I64, _I32, _P, _I64, _I32, _P, _P]),
 }

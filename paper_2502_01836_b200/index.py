@@ -351,8 +351,16 @@ class DeviceIndex:
         node_leaf[leaf_ids] = np.arange(leaf_ids.shape[0], dtype=np.int32)
         with torch.cuda.device(dev):
             rid = torch.from_numpy(order).to(dev)
+            from .leafio import FileRows, load_rows_to
+
             if isinstance(t.values, DeviceRows):
                 self.X = t.values.tensor.index_select(0, rid).contiguous()
+            elif isinstance(t.values, FileRows):
+                # LEAF file: rows streamed straight into their leaf-contiguous slots
+                pos = np.full(t.n, -1, dtype=np.int64)
+                pos[order] = np.arange(order.shape[0], dtype=np.int64)
+                self.X = torch.empty((order.shape[0], t.m), dtype=torch.float32, device=dev)
+                load_rows_to(t.values, torch.from_numpy(pos).to(dev), self.X)
             else:
                 src = torch.from_numpy(t.values).to(dev)
                 self.X = src.index_select(0, rid).contiguous()
