@@ -91,13 +91,17 @@ typedef struct lf_search_opts {
                                     tracing; needs m % 64 == 0) */
     double* h_profile;           /* optional host array[LF_N_PROF]: CUDA-event times (ms)
                                     accumulated per phase, see LF_PROF_* */
-    /* Lazy filter inference (used when d_pred and d_pred_f64 are NULL and d_W1T is
-       set): the filter pack itself -- W1T [F][m][m] (hidden-major, as for
-       lf_filter_predict_tc), b1 [F][m], W2 [F][m], b2 [F], m in {32, ..., 256}.  After
-       the first round, predictions are computed on the tensor cores only for the
-       (query, leaf) pairs the walk can still reach (leaves with lb <= bsf * f),
-       bit-identical to lf_filter_predict_tc's. */
-    const float* d_W1T;
+    /* In-search filter inference (used when d_pred and d_pred_f64 are NULL and d_W1T_h
+       is set): the fp16 filter pack -- W1T_h [F][hidden][in] fp16 bits with per-filter
+       power-of-two exponents d_wexp (lf_filter_predict_f16's operands), b1 [F][m],
+       W2 [F][m], b2 [F]; m in {64, 128, 192, 256}.  Round 0 needs no prediction (bsf is
+       +inf); right after it ONE tensor-core pass predicts exactly the (query, filtered
+       leaf) pairs with lb <= bsf0 * f -- every pair the walk can still reach, since bsf
+       only decreases -- bit-identical to lf_filter_predict_f16's predictions.  (A query
+       whose bsf is still +inf after round 0, k > first leaf's size, gets its pass when
+       it asks for one.) */
+    const uint16_t* d_W1T_h;
+    const int32_t* d_wexp;
     const float* d_b1;
     const float* d_W2;
     const float* d_b2;
@@ -114,9 +118,9 @@ typedef struct lf_search_opts {
 #define LF_PROF_REFILLS 7        /* reserved (0) */
 #define LF_PROF_EA_ROWS 8        /* rows tested by the early-abandon scan */
 #define LF_PROF_EA_SURVIVORS 9   /* rows that survived the first 64-dim test */
-#define LF_PROF_PREDICT_MS 10    /* lazy filter inference (pairs, gather, tensor-core GEMM) */
-#define LF_PROF_PAIRS 11         /* (query, leaf) predictions computed lazily */
-#define LF_PROF_PREDICT_STEPS 12 /* lazy inference passes (one after round 0, then on request) */
+#define LF_PROF_PREDICT_MS 10    /* in-search filter inference (pair lists + tensor-core GEMM) */
+#define LF_PROF_PAIRS 11         /* (query, leaf) predictions computed in the search */
+#define LF_PROF_PREDICT_STEPS 12 /* in-search inference passes (one after round 0, then on request) */
 #define LF_PROF_SCAN_STREAM_BYTES 13 /* bytes the scans streamed (codes + row metadata, or fp32 rows) */
 #define LF_PROF_SCAN_EXACT_BYTES 14  /* fp32 bytes re-read for exact distances of surviving rows */
 

@@ -60,7 +60,8 @@ class LfSearchOpts(C.Structure):
         ("want_trace", C.c_int32),
         ("early_abandon", C.c_int32),
         ("h_profile", C.c_void_p),
-        ("d_W1T", C.c_void_p),
+        ("d_W1T_h", C.c_void_p),
+        ("d_wexp", C.c_void_p),
         ("d_b1", C.c_void_p),
         ("d_W2", C.c_void_p),
         ("d_b2", C.c_void_p),

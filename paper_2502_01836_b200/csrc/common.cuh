@@ -1,6 +1,7 @@
 // Shared helpers for the sm_100a LeaFi kernels.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -123,5 +124,14 @@ constexpr double kInf = __builtin_huge_val();
 int filter_pairs_tc(const float* d_rows, int64_t P, int m, const float* d_W1T, const float* d_b1,
                     const float* d_W2, const float* d_b2, int F, const int4* d_tiles, const int* d_ntiles,
                     const int2* d_dst, const double* d_offset, double* d_adj, int Nn, cudaStream_t st);
+
+// In-search filter inference (filters_tc.cu): the fp16 pack over query rows gathered
+// with TMA gather4 from d_xh (fp16 [Q][m], power-of-two exponents d_xexp).
+int filter_reach_f16(const __half* d_xh, const int* d_xexp, int64_t Q, int m, const uint16_t* d_W1T_h,
+                     const int* d_wexp, const float* d_b1, const float* d_W2, const float* d_b2, int F,
+                     const int4* d_tiles, const int* d_ntiles, const int2* d_dst, const double* d_offset,
+                     double* d_adj, int Nn, cudaStream_t st);
+// fp32 rows -> power-of-two-scaled fp16 rows + exponents (filters_tc.cu).
+int rows_to_f16(const float* d_X, int64_t rows, int m, __half* d_out, int* d_exps, cudaStream_t st);
 
 }  // namespace lf

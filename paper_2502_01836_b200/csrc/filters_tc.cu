@@ -141,11 +141,25 @@ struct PairArgs {
 // mantissa without overflow; the epilogue multiplies the accumulator back by
 // 2^(xexp[row] + wexp[f]) -- exact -- before the bias.
 struct F16Args {
-    const int* xexp;             // per X row (dense: query; pairs: gathered row)
+    const int* xexp;             // per X row (dense: query; pairs: gathered row; GATHER: query)
     const int* wexp;             // per filter
 };
 
-template <bool PAIRS, bool F16>
+// GATHER (with PAIRS and F16): the A operand is not a materialised row list but the
+// batch's fp16 query matrix; the producer warp gathers each tile's 128 query rows
+// straight into the SW128 stage with TMA tile::gather4 (4 rows per instruction, one
+// instruction per lane), so in-search inference reads each filter's W1 once and the
+// queries from L2.
+__device__ __forceinline__ void tma_gather4(const CUtensorMap* map, uint64_t* bar, void* dst, int col, int r0, int r1,
+                                            int r2, int r3) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(su32(dst)),
+        "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(su32(bar))
+        : "memory");
+}
+
+template <bool PAIRS, bool F16, bool GATHER = false>
 __global__ void __launch_bounds__(THREADS, 1)
 filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
                  int64_t Q, int m, int F, const float* __restrict__ b1, const float* __restrict__ W2,
@@ -182,7 +196,52 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp == 0) {
+    if (GATHER && warp == 0) {                               // ---- TMA producer, gathered A
+        // Each tile is (usually) a new filter whose W1 (m x m fp16, 128 KiB) comes from
+        // DRAM: the next tiles' W1 is prefetched into L2 one and two tiles ahead, and the
+        // next tile's gather rows are loaded while this tile's stages are issued, so the
+        // smem ring only ever waits on L2.
+        int stage = 0;
+        uint32_t phase = 0;
+        auto prefetch_w = [&](int64_t tt) {
+            if (lane == 0 && tt < n_tiles) {
+                const int ff = pa.tiles[tt].x;
+                for (int kb = 0; kb < n_kb; ++kb)
+                    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(&map_w),
+                                 "r"(kb * BKE), "r"(ff * m)
+                                 : "memory");
+            }
+        };
+        auto rows_of = [&](int64_t tt, int* q4) {
+            if (tt < n_tiles) {
+                const int4 tl = pa.tiles[tt];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) q4[i] = pa.dst[tl.y + min(4 * lane + i, tl.z - 1)].x;
+            }
+        };
+        int qi[4], qn[4] = {0, 0, 0, 0};
+        prefetch_w(blockIdx.x);
+        prefetch_w((int64_t)blockIdx.x + gridDim.x);
+        rows_of(blockIdx.x, qi);
+        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+            const int f = pa.tiles[t].x;
+            prefetch_w(t + 2 * (int64_t)gridDim.x);
+            rows_of(t + gridDim.x, qn);                      // in flight while this tile is issued
+            for (int kb = 0; kb < n_kb; ++kb) {
+                if (lane == 0) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], A_BYTES + b_bytes);
+                }
+                __syncwarp();
+                uint8_t* sa = smem + stage * STAGE_BYTES;
+                tma_gather4(&map_x, &full[stage], sa + lane * 4 * 128, kb * BKE, qi[0], qi[1], qi[2], qi[3]);
+                if (lane == 0) tma_2d(&map_w, &full[stage], sa + A_BYTES, kb * BKE, f * m);
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) qi[i] = qn[i];
+        }
+    } else if (warp == 0) {
         if (lane == 0) {                                     // ---- TMA producer
             int stage = 0;
             uint32_t phase = 0;
@@ -298,7 +357,7 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
             float sc = 1.f;                                  // F16: undo the operands' scaling
             if (F16) {
                 const int64_t xr = (int64_t)row0 + row;
-                const int ex = (PAIRS ? row < nrows : xr < Q) ? fa.xexp[xr] : 0;
+                const int ex = !(PAIRS ? row < nrows : xr < Q) ? 0 : GATHER ? fa.xexp[pa.dst[xr].x] : fa.xexp[xr];
                 sc = scalbnf(1.f, ex + fa.wexp[f]);
             }
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * 256);
@@ -560,3 +619,26 @@ extern "C" int lf_filter_predict_f16(const float* d_queries, int64_t Q, int32_t 
     LF_CUDA(cudaGetLastError());
     return LF_OK;
 }
+
+namespace lf {
+// In-search filter inference over gathered query rows (lf_search with d_W1T_h): tile
+// list (filter, first pair, pairs) and per-pair (query, visit-order position) on the
+// device; adj[q][pos] = pred - offset.  Bit-identical to lf_filter_predict_f16.
+int filter_reach_f16(const __half* d_xh, const int* d_xexp, int64_t Q, int m, const uint16_t* d_W1T_h,
+                     const int* d_wexp, const float* d_b1, const float* d_W2, const float* d_b2, int F,
+                     const int4* d_tiles, const int* d_ntiles, const int2* d_dst, const double* d_offset,
+                     double* d_adj, int Nn, cudaStream_t st) {
+    if (Q == 0 || F == 0) return LF_OK;
+    CUtensorMap mx, mw;
+    int rc = tc::make_map(&mx, d_xh, Q, m, 1, true);            // gather4: one row per box
+    if (rc) return rc;
+    rc = tc::make_map(&mw, d_W1T_h, (int64_t)F * m, m, m, true);
+    if (rc) return rc;
+    LF_CUDA(smem_optin(tc::filter_tc_kernel<true, true, true>, tc::SMEM_BYTES));
+    tc::PairArgs pa{d_tiles, d_ntiles, d_dst, d_offset, d_adj, Nn};
+    tc::filter_tc_kernel<true, true, true><<<sm_count(), tc::THREADS, tc::SMEM_BYTES, st>>>(
+        mx, mw, Q, m, F, d_b1, d_W2, d_b2, nullptr, pa, tc::F16Args{d_xexp, d_wexp});
+    LF_CUDA(cudaGetLastError());
+    return LF_OK;
+}
+}  // namespace lf

@@ -26,10 +26,9 @@ struct RoundState {
     const int* leafo;            // [Q][L] leaf slot | LF_REC_HASF
     const double* adj;           // [Q][L] pred - offset of the leaf's filter
     const int* olen;             // [Q] records of the order (= L)
-    int lazy;                    // lazy filter inference: adj valid for positions < pcount[q]
+    int lazy;                    // in-search filter inference: adj valid for positions < pcount[q]
     const int* pcount;           // [Q]
     int* preq;                   // [Q] set when the walk stopped at pcount (more predictions needed)
-    int* pwin;                   // [Q] positions the next prediction pass covers (doubles per pass)
     int* n_predict;              // walks that reached pcount with a finite bsf (= n_active + 2)
     int* cursor;                 // [Q]
     int* done;                   // [Q]

@@ -253,84 +253,84 @@ __global__ void expand_tasks_kernel(RoundState s, const int64_t* __restrict__ le
     }
 }
 
-// ------------------------------------------------------- lazy inference ----
-// After a round, a query with a finite bsf can only ever reach the visit-order
-// positions [pcount, pend), pend = the first position whose bound exceeds bsf * f
-// (bsf only decreases).  The leaves with a filter in that range are the (query,
-// leaf) pairs whose prediction the cascade may need (tree.py:277-286 evaluates a
-// subset of exactly these).  pass 1 counts them per filter, a single-CTA scan
-// turns the counts into filter buckets and a 128-row tile list, pass 2 fills the
-// buckets and gathers the query rows, and filter_pairs_tc (tcgen05, the same
-// arithmetic as the dense filter kernel) writes pred - offset into the records.
-constexpr int PRED_WINDOW = 1024;   // visit-order positions of a query's first prediction pass
-
-__global__ void fill_int_kernel(int* p, int64_t n, int v) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) p[i] = v;
-}
-
-__global__ void pairs_count_kernel(RoundState s, int* pend, int* fhist, unsigned long long* total, lf_index idx,
-                                   int all) {
-    const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
+// ------------------------------------------------- in-search inference ----
+// Round 0 needs no prediction (bsf = +inf: the filter rule never fires).  After it,
+// a query with a finite bsf0 can only ever reach the visit-order positions
+// [pcount, pend), pend = one past the first position whose bound exceeds bsf0 * f
+// (bsf only decreases, so every later break comes no later).  The leaves with a
+// filter in that range are a superset of the (query, leaf) pairs whose prediction
+// the cascade may evaluate (tree.py:277-286).  One pass predicts them all: pass 1
+// counts them per filter, a single-CTA scan turns the counts into filter buckets and
+// a 128-pair tile list, pass 2 fills the buckets, and filter_reach_f16 (tcgen05
+// kind::f16, the dense kernel's arithmetic, query rows gathered with TMA gather4)
+// writes pred - offset into the records.  On the bench workload that is 0.42M pairs
+// instead of the 4.1M of a dense pass.  All on the device: rounds stay pipelined.
+// Thread per query: the range of the visit order the walk can still reach.  The
+// order is sorted by (lb, node id), so the first position whose bound exceeds
+// bsf * f is a binary search; pairs are [pstart, pair_end), and the walk may go up to
+// pend = pair_end + 1 (the break entry itself: its bound alone decides).
+__global__ void pairs_range_kernel(RoundState s, int* __restrict__ pcount, int* __restrict__ pstart,
+                                   int* __restrict__ pair_end, int all) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= s.Q) return;
-    const int start = s.pcount[q];
+    const int start = max(pcount[q], s.cursor[q]);      // the walk never goes back
     const double thr = round_bsf(s, q) * s.f;
     const bool want = all || s.preq[q];
-    __syncwarp();
-    if (lane == 0) s.preq[q] = 0;
-    if (s.done[q] || !(thr < kInf) || !want) {
-        if (lane == 0) pend[q] = start;
-        return;
-    }
-    const int Lr = idx.n_leaves;
-    // a window of the order at a time (doubling per pass): LeaFi's filters stop most
-    // walks long before the bound does (281 of 4,096 leaves visited per query on the
-    // bench workload), so predicting every leaf under the bound would be ~15x the work
-    const int win = s.pwin[q];
-    const int len = min(s.olen[q], start + win);
-    const double* lbs = s.lbs + q * Lr;
-    const int* lrec = s.leafo + q * Lr;
-    int i = start, cnt = 0;
-    bool broke = false;
-    while (i < len) {                                  // 128 positions per pass, loads in flight together
-        double lbv[4];
-        int recv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int k = i + 32 * u + lane;
-            lbv[u] = k < len ? lbs[k] : kInf;
-            recv[u] = k < len ? lrec[k] : -1;
+    s.preq[q] = 0;
+    int pe = start, walk = start;
+    if (!s.done[q] && thr < kInf && want) {
+        const double* lbs = s.lbs + q * s.n_leaves;
+        const int len = s.olen[q];
+        int lo = start, hi = len;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (lbs[mid] > thr) hi = mid;
+            else lo = mid + 1;
         }
-        bool stop = false;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            if (stop) break;
-            const int k = i + 32 * u + lane;
-            const bool valid = k < len;
-            const bool brk = valid && lbv[u] > thr;
-            const unsigned bmask = __ballot_sync(0xffffffffu, brk);
-            const int first = bmask ? __ffs(bmask) - 1 : 32;
-            const int rec = (valid && lane < first) ? recv[u] : -1;
-            const bool has = rec >= 0 && (rec & LF_REC_HASF);
-            if (has) atomicAdd(&fhist[idx.d_leaf_filter[rec & LF_REC_LEAF]], 1);
-            cnt += __popc(__ballot_sync(0xffffffffu, has));
-            if (bmask) { i += 32 * u + first; broke = true; stop = true; }
-        }
-        if (stop) break;
-        i += 128;
+        pe = lo;
+        walk = lo < len ? lo + 1 : len;
     }
-    if (lane == 0) s.pwin[q] = win * 2;
-    if (lane == 0) {
-        // the break entry itself stays walkable (its bound alone decides), so the walk
-        // can finish there instead of asking for predictions again
-        pend[q] = broke ? i + 1 : min(i, len);
-        if (cnt) atomicAdd(total, (unsigned long long)cnt);
+    pstart[q] = start;
+    pair_end[q] = pe;
+    pcount[q] = max(pcount[q], walk);
+}
+
+// Warp per (query, 256 positions): FILL = 0 counts the filtered leaves of the
+// reachable range per filter, FILL = 1 places each (query, position) pair in its
+// filter's bucket.
+constexpr int PAIR_SPAN = 256;
+template <bool FILL>
+__global__ void pairs_pos_kernel(int64_t Q, int Lr, const int* __restrict__ pstart, const int* __restrict__ pair_end,
+                                 const int* __restrict__ leafo, const int* __restrict__ leaf_filter,
+                                 int* __restrict__ cnt, int2* __restrict__ dst, unsigned long long* total) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int spans = (Lr + PAIR_SPAN - 1) / PAIR_SPAN;
+    const int64_t q = w / spans;
+    if (q >= Q) return;
+    const int c0 = (int)(w % spans) * PAIR_SPAN;
+    const int a = max(pstart[q], c0), b = min(pair_end[q], c0 + PAIR_SPAN);
+    if (a >= b) return;
+    const int* lrec = leafo + q * Lr;
+    int n = 0;
+    for (int k = a + lane; k < b; k += 32) {
+        const int rec = lrec[k];
+        if (rec >= 0 && (rec & LF_REC_HASF)) {
+            const int f = leaf_filter[rec & LF_REC_LEAF];
+            if (FILL) dst[atomicAdd(&cnt[f], 1)] = make_int2((int)q, k);
+            else atomicAdd(&cnt[f], 1);
+            ++n;
+        }
+    }
+    if (!FILL && total) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+        if (lane == 0 && n) atomicAdd(total, (unsigned long long)n);
     }
 }
 
 // Filter buckets (exclusive scan of the per-filter counts) and the tile list
-// (filter, first row, rows <= 128) in one CTA.
+// (filter, first pair, pairs <= 128) in one CTA.
 __global__ void pair_tiles_kernel(const int* __restrict__ fhist, int F, int* __restrict__ fcur, int4* __restrict__ tiles,
                                   int* __restrict__ ntiles) {
     __shared__ int sp[1024], st[1024];
@@ -369,42 +369,6 @@ int pair_tiles(const int* d_hist, int F, int* d_fcur, int4* d_tiles, int* d_ntil
     pair_tiles_kernel<<<1, 1024, 0, st>>>(d_hist, F, d_fcur, d_tiles, d_ntiles);
     LF_CUDA(cudaGetLastError());
     return LF_OK;
-}
-
-// Bucket the pairs by filter (slot order inside a bucket is irrelevant: every row's
-// prediction depends on that row alone) and gather their query rows.
-__global__ void pairs_fill_kernel(RoundState s, lf_index idx, const float* __restrict__ queries, int m, int* pcount,
-                                  const int* __restrict__ pend, int* fcur, int2* __restrict__ dst,
-                                  float* __restrict__ rows) {
-    const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (q >= s.Q) return;
-    const int start = pcount[q], end = pend[q];
-    const int Lr = idx.n_leaves;
-    const int* lrec = s.leafo + q * Lr;
-    const double* lbs = s.lbs + q * Lr;
-    const double thr = round_bsf(s, q) * s.f;       // same bound as pass 1: skips its break entry
-    for (int i = start; i < end; i += 32) {
-        const int k = i + lane;
-        const int rec = (k < end && lbs[k] <= thr) ? lrec[k] : -1;
-        const bool has = rec >= 0 && (rec & LF_REC_HASF);
-        if (has) {
-            const int slot = atomicAdd(&fcur[idx.d_leaf_filter[rec & LF_REC_LEAF]], 1);
-            dst[slot] = make_int2((int)q, k);
-        }
-    }
-    if (lane == 0) pcount[q] = end;
-}
-
-// Gather the query row of every bucketed pair (warp per pair, 128-bit copies).
-__global__ void pairs_gather_kernel(const float* __restrict__ queries, int m, const int2* __restrict__ dst, int64_t P,
-                                    float* __restrict__ rows) {
-    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (i >= P) return;
-    const float4* src = reinterpret_cast<const float4*>(queries + (int64_t)dst[i].x * m);
-    float4* out = reinterpret_cast<float4*>(rows + i * m);
-    for (int c = lane; c < m / 4; c += 32) out[c] = __ldg(src + c);
 }
 
 // --------------------------------------------------------------- merge ----
@@ -529,12 +493,12 @@ struct lf_session {
     lf::RoundState s{};
     lf::Scratch qsumm, lb, lbs, gap, order, cursor, done, topd, topi, topn, topd2, topi2, topn2, sel_leaf,
         sel_trace, sel_pre, n_sel, chunk_off, cand_d, cand_i, task_min, n_active, tasks, ea_count, qc8, qm8,
-        leafo, adj, olen, pcount, pend, preq, pwin, fhist, fcur, ntiles, ptotal;
+        leafo, adj, olen, pcount, pstart, pend, preq, fhist, fcur, ntiles, ptotal, pdst, ptiles, xh, xexp;
     lf::OrderArgs oa{};
-    bool lazy = false;               // lazy filter inference (opts.d_W1T instead of predictions)
-    long long pairs = 0;             // predictions computed lazily
+    bool lazy = false;               // in-search filter inference (opts.d_W1T_h instead of predictions)
+    bool predict_pending = false;    // a harvested round asked for predictions (bsf was +inf after round 0)
     int predict_steps = 0;
-    double predict_ms = 0.0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pev;   // profiling: per prediction pass
     bool q8 = false;                 // int8-bounded scan (query codes quantised once in begin)
     bool pq = false;                 // two-stage scan over the projected shadow (d_Xp)
     lf::Scratch qcp, qmp, pq_cnt, pq_trows, pq_oent, pq_on, pq_obase, pq_wrows, pq_wdist, pq_lo8, pq_thr;
@@ -604,20 +568,28 @@ static int session_begin(lf_session* ss) {
         if (o.h_profile)
             for (auto& e : ss->rev[sl]) LF_CUDA(cudaEventCreate(&e));
     }
-    ss->lazy = o.d_pred == nullptr && o.d_pred_f64 == nullptr && o.d_W1T != nullptr;
+    ss->lazy = o.d_pred == nullptr && o.d_pred_f64 == nullptr && o.d_W1T_h != nullptr;
     if (ss->lazy) {
+        const int F = std::max(1, o.n_filters);
         LF_CUDA(ss->pcount.alloc(sizeof(int) * Q, st));
         LF_CUDA(cudaMemsetAsync(ss->pcount.p, 0, sizeof(int) * Q, st));
+        LF_CUDA(ss->pstart.alloc(sizeof(int) * Q, st));
         LF_CUDA(ss->pend.alloc(sizeof(int) * Q, st));
         LF_CUDA(ss->preq.alloc(sizeof(int) * Q, st));
         LF_CUDA(cudaMemsetAsync(ss->preq.p, 0, sizeof(int) * Q, st));
-        LF_CUDA(ss->pwin.alloc(sizeof(int) * Q, st));
-        fill_int_kernel<<<(unsigned)((Q + 255) / 256), 256, 0, st>>>(ss->pwin.as<int>(), Q, PRED_WINDOW);
-        LF_CUDA(cudaGetLastError());
-        LF_CUDA(ss->fhist.alloc(sizeof(int) * std::max(1, o.n_filters), st));
-        LF_CUDA(ss->fcur.alloc(sizeof(int) * std::max(1, o.n_filters), st));
+        LF_CUDA(ss->fhist.alloc(sizeof(int) * F, st));
+        LF_CUDA(ss->fcur.alloc(sizeof(int) * F, st));
         LF_CUDA(ss->ntiles.alloc(sizeof(int), st));
         LF_CUDA(ss->ptotal.alloc(sizeof(unsigned long long), st));
+        LF_CUDA(cudaMemsetAsync(ss->ptotal.p, 0, sizeof(unsigned long long), st));
+        const int64_t max_pairs = Q * (int64_t)L;     // every (query, leaf) pair, worst case
+        LF_CUDA(ss->pdst.alloc(sizeof(int2) * max_pairs, st));
+        LF_CUDA(ss->ptiles.alloc(sizeof(int4) * (max_pairs / 128 + F + 1), st));
+        LF_CUDA(ss->xh.alloc(sizeof(__half) * Q * idx.m, st));
+        LF_CUDA(ss->xexp.alloc(sizeof(int) * Q, st));
+        int rc = rows_to_f16(ss->d_q, Q, idx.m, ss->xh.as<__half>(), ss->xexp.as<int>(), st);
+        if (rc) return rc;
+        ++ss->kernels;
     }
     LF_CUDA(ss->tasks.alloc(sizeof(int4) * max_tasks, st));
     LF_CUDA(ss->ea_count.alloc(sizeof(unsigned long long) * 4, st));
@@ -662,7 +634,6 @@ static int session_begin(lf_session* ss) {
     s.lazy = ss->lazy ? 1 : 0;
     s.pcount = ss->lazy ? ss->pcount.as<int>() : nullptr;
     s.preq = ss->lazy ? ss->preq.as<int>() : nullptr;
-    s.pwin = ss->lazy ? ss->pwin.as<int>() : nullptr;
     s.cursor = ss->cursor.as<int>();
     s.done = ss->done.as<int>();
     s.top_d = ss->topd.as<double>();
@@ -730,8 +701,10 @@ __global__ void bsf_out_kernel(RoundState s, double* out) {
     if (q < s.Q) out[q] = query_bsf(s, q);
 }
 
-// Lazy filter inference for every query with a finite bsf (see pairs_count_kernel).
-static int predict_step(lf_session* ss) {
+// One in-search prediction pass (see pairs_range_kernel), enqueued on the device only:
+// all = 1 right after round 0 (every query with a finite bsf), all = 0 for the queries
+// that asked for one (their bsf was still +inf after round 0).
+static int predict_pass(lf_session* ss, int all) {
     RoundState& s = ss->s;
     const lf_index& idx = ss->idx;
     const lf_search_opts& o = ss->opts;
@@ -745,46 +718,29 @@ static int predict_step(lf_session* ss) {
         LF_CUDA(cudaEventRecord(e0, st));
     }
     LF_CUDA(cudaMemsetAsync(ss->fhist.p, 0, sizeof(int) * std::max(1, F), st));
-    LF_CUDA(cudaMemsetAsync(ss->ptotal.p, 0, sizeof(unsigned long long), st));
-    const unsigned wgrid = (unsigned)((Q * 32 + 255) / 256);
-    pairs_count_kernel<<<wgrid, 256, 0, st>>>(s, ss->pend.as<int>(), ss->fhist.as<int>(),
-                                              ss->ptotal.as<unsigned long long>(), idx, ss->round == 0 ? 1 : 0);
+    pairs_range_kernel<<<(unsigned)((Q + 255) / 256), 256, 0, st>>>(s, ss->pcount.as<int>(), ss->pstart.as<int>(),
+                                                                    ss->pend.as<int>(), all);
     LF_CUDA(cudaGetLastError());
-    unsigned long long total = 0;
-    LF_CUDA(cudaMemcpyAsync(&total, ss->ptotal.p, sizeof(total), cudaMemcpyDeviceToHost, st));
-    LF_CUDA(cudaStreamSynchronize(st));
-    ss->kernels += 1;
-    if (total == 0) {
-        LF_CUDA(cudaMemcpyAsync(ss->pcount.p, ss->pend.p, sizeof(int) * Q, cudaMemcpyDeviceToDevice, st));
-    } else {
-        const int64_t P = (int64_t)total;
-        Scratch rows, dst, tiles;
-        LF_CUDA(rows.alloc(sizeof(float) * (size_t)P * idx.m, st));
-        LF_CUDA(dst.alloc(sizeof(int2) * (size_t)P, st));
-        LF_CUDA(tiles.alloc(sizeof(int4) * (size_t)(P / 128 + F + 1), st));
-        pair_tiles_kernel<<<1, 1024, 0, st>>>(ss->fhist.as<int>(), F, ss->fcur.as<int>(), tiles.as<int4>(),
-                                              ss->ntiles.as<int>());
-        LF_CUDA(cudaGetLastError());
-        pairs_fill_kernel<<<wgrid, 256, 0, st>>>(s, idx, ss->d_q, idx.m, ss->pcount.as<int>(), ss->pend.as<int>(),
-                                                 ss->fcur.as<int>(), dst.as<int2>(), rows.as<float>());
-        LF_CUDA(cudaGetLastError());
-        pairs_gather_kernel<<<(unsigned)((P * 32 + 255) / 256), 256, 0, st>>>(ss->d_q, idx.m, dst.as<int2>(), P,
-                                                                             rows.as<float>());
-        LF_CUDA(cudaGetLastError());
-        int rc = filter_pairs_tc(rows.as<float>(), P, idx.m, o.d_W1T, o.d_b1, o.d_W2, o.d_b2, F, tiles.as<int4>(),
-                                 ss->ntiles.as<int>(), dst.as<int2>(), o.d_offset, ss->adj.as<double>(), idx.n_leaves,
-                                 st);
-        if (rc) return rc;
-        ss->kernels += 4;
-        ss->pairs += P;
-        ++ss->predict_steps;
-    }
+    const int64_t Lr = idx.n_leaves;
+    const unsigned pgrid = (unsigned)((Q * ((Lr + PAIR_SPAN - 1) / PAIR_SPAN) * 32 + 255) / 256);
+    pairs_pos_kernel<false><<<pgrid, 256, 0, st>>>(Q, (int)Lr, ss->pstart.as<int>(), ss->pend.as<int>(), s.leafo,
+                                                   idx.d_leaf_filter, ss->fhist.as<int>(), nullptr,
+                                                   ss->prof ? ss->ptotal.as<unsigned long long>() : nullptr);
+    LF_CUDA(cudaGetLastError());
+    int rc = pair_tiles(ss->fhist.as<int>(), F, ss->fcur.as<int>(), ss->ptiles.as<int4>(), ss->ntiles.as<int>(), st);
+    if (rc) return rc;
+    pairs_pos_kernel<true><<<pgrid, 256, 0, st>>>(Q, (int)Lr, ss->pstart.as<int>(), ss->pend.as<int>(), s.leafo,
+                                                  idx.d_leaf_filter, ss->fcur.as<int>(), ss->pdst.as<int2>(), nullptr);
+    LF_CUDA(cudaGetLastError());
+    rc = filter_reach_f16(ss->xh.as<__half>(), ss->xexp.as<int>(), Q, idx.m, o.d_W1T_h, o.d_wexp, o.d_b1, o.d_W2,
+                          o.d_b2, F, ss->ptiles.as<int4>(), ss->ntiles.as<int>(), ss->pdst.as<int2>(), o.d_offset,
+                          ss->adj.as<double>(), idx.n_leaves, st);
+    if (rc) return rc;
+    ss->kernels += 5;
+    ++ss->predict_steps;
     if (ss->prof) {
         LF_CUDA(cudaEventRecord(e1, st));
-        LF_CUDA(cudaEventSynchronize(e1));
-        ss->predict_ms += ev_ms(e0, e1);
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
+        ss->pev.emplace_back(e0, e1);
     }
     return LF_OK;
 }
@@ -802,6 +758,12 @@ static int session_enqueue(lf_session* ss, const double* d_bound, double* d_bsf_
     s.n_active = counts;
     s.n_predict = counts + 2;
     cudaEvent_t* ev = ss->rev[slot];
+    if (ss->lazy && (ss->round == 1 || ss->predict_pending)) {
+        // after round 0 every query with a finite bsf gets its reachable pairs predicted
+        int rc = predict_pass(ss, ss->round == 1 ? 1 : 0);
+        if (rc) return rc;
+        ss->predict_pending = false;
+    }
     s.bound = d_bound;
     s.R = o.sequential ? 1
                        : (int)std::min<int64_t>(s.Rcap, (int64_t)1 << std::min(ss->round * round_growth_log2(), 30));
@@ -865,10 +827,7 @@ static int session_harvest(lf_session* ss, int* active_out) {
     const int slot = r & 1;
     int* h = ss->h_active + 4 * slot;
     LF_CUDA(cudaEventSynchronize(ss->done_ev[slot]));
-    if (ss->lazy && h[0] > 0 && (r == 0 || h[2] > 0)) {
-        int rc = predict_step(ss);     // after round 0 every bsf is finite: predict what is reachable
-        if (rc) return rc;
-    }
+    if (ss->lazy && r >= 1 && h[0] > 0 && h[2] > 0) ss->predict_pending = true;   // walks stopped at pcount
     if (ss->prof) {
         double* p = o.h_profile;
         cudaEvent_t* ev = ss->rev[slot];
@@ -904,8 +863,12 @@ static int session_end(lf_session* ss, int64_t* out_ids, double* out_d, int64_t*
         p[LF_PROF_KERNELS] = (double)ss->kernels;
         p[LF_PROF_TOTAL_MS] = ev_ms(ss->ev[0], ss->ev[5]);
         p[LF_PROF_REFILLS] = 0.0;
-        p[LF_PROF_PREDICT_MS] = ss->predict_ms;
-        p[LF_PROF_PAIRS] = (double)ss->pairs;
+        double pms = 0.0;
+        for (auto& e : ss->pev) pms += ev_ms(e.first, e.second);
+        p[LF_PROF_PREDICT_MS] = pms;
+        unsigned long long pairs = 0;
+        if (ss->lazy) cudaMemcpy(&pairs, ss->ptotal.p, sizeof(pairs), cudaMemcpyDeviceToHost);
+        p[LF_PROF_PAIRS] = (double)pairs;
         p[LF_PROF_PREDICT_STEPS] = (double)ss->predict_steps;
         unsigned long long c[4] = {0, 0, 0, 0};
         cudaMemcpy(c, ss->ea_count.p, sizeof(c), cudaMemcpyDeviceToHost);
@@ -919,6 +882,10 @@ static int session_end(lf_session* ss, int64_t* out_ids, double* out_d, int64_t*
 
 static void session_free(lf_session* ss) {
     if (!ss) return;
+    for (auto& e : ss->pev) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
     for (auto& e : ss->ev)
         if (e) cudaEventDestroy(e);
     for (int sl = 0; sl < 2; ++sl) {
@@ -934,14 +901,15 @@ static int check_args(const lf_index* idx, int64_t Q, const lf_search_opts* opts
     LF_REQUIRE(Q >= 0, "negative query count");
     LF_REQUIRE(opts->k >= 1 && opts->k <= idx->n_series, "k must be in [1, n]");
     LF_REQUIRE(idx->n_seg >= 1 && idx->n_seg <= LF_MAX_SEG, "bad segment count");
-    LF_REQUIRE((opts->d_pred == nullptr && opts->d_pred_f64 == nullptr && opts->d_W1T == nullptr) ||
+    LF_REQUIRE((opts->d_pred == nullptr && opts->d_pred_f64 == nullptr && opts->d_W1T_h == nullptr) ||
                    (opts->d_offset != nullptr && idx->d_leaf_filter != nullptr),
                "filter predictions need offsets and a leaf->filter map");
-    LF_REQUIRE(opts->d_W1T == nullptr || opts->d_pred != nullptr || opts->d_pred_f64 != nullptr ||
-                   (opts->d_b1 != nullptr && opts->d_W2 != nullptr && opts->d_b2 != nullptr && idx->m % 32 == 0 &&
-                    idx->m >= 32 && idx->m <= 256 && opts->n_filters >= 1 && ((uintptr_t)opts->d_b1 & 15) == 0 &&
+    LF_REQUIRE(opts->d_W1T_h == nullptr || opts->d_pred != nullptr || opts->d_pred_f64 != nullptr ||
+                   (opts->d_wexp != nullptr && opts->d_b1 != nullptr && opts->d_W2 != nullptr && opts->d_b2 != nullptr &&
+                    idx->m % 64 == 0 && idx->m >= 64 && idx->m <= 256 && opts->n_filters >= 1 &&
+                    ((uintptr_t)opts->d_W1T_h & 15) == 0 && ((uintptr_t)opts->d_b1 & 15) == 0 &&
                     ((uintptr_t)opts->d_W2 & 15) == 0),
-               "lazy filter inference needs W1T, b1, W2, b2 (16-byte aligned) and m in {32, 64, ..., 256}");
+               "in-search filter inference needs W1T_h, wexp, b1, W2, b2 (16-byte aligned) and m in {64, 128, 192, 256}");
     LF_REQUIRE(opts->sequential || opts->max_round_leaves >= 1, "max_round_leaves must be >= 1");
     return LF_OK;
 }
@@ -979,7 +947,6 @@ int lf_search_round(lf_session* ss, const double* d_bound, double* d_bsf_out, in
 
 int lf_search_round_async(lf_session* ss, const double* d_bound, double* d_bsf_out, int32_t* d_active) {
     LF_REQUIRE(ss != nullptr, "NULL session");
-    LF_REQUIRE(!ss->lazy, "lazy filter inference needs host decisions after each round: use lf_search_round");
     LF_REQUIRE(ss->round - ss->harvested < 2, "at most two rounds in flight: call lf_search_round_wait first");
     const int slot = ss->round & 1;
     int rc = lf::session_enqueue(ss, d_bound, d_bsf_out);
@@ -1028,22 +995,15 @@ int lf_search(const lf_index* idx, const float* d_queries, int64_t Q, const lf_s
         return rc;
     }
     int active = 0;
-    if (ss->lazy) {
-        do {   // host decisions after every round (prediction passes): no pipelining
-            rc = lf_search_round(ss, nullptr, nullptr, &active);
-            if (rc) break;
-        } while (active > 0);
-    } else {
-        // one round in flight ahead of the count read-back: the host never idles the GPU
-        // between rounds; a round enqueued after the last active one finds every query done
-        // and changes nothing
+    // one round in flight ahead of the count read-back: the host never idles the GPU
+    // between rounds; a round enqueued after the last active one finds every query done
+    // and changes nothing
+    rc = lf::session_enqueue(ss, nullptr, nullptr);
+    while (rc == LF_OK) {
         rc = lf::session_enqueue(ss, nullptr, nullptr);
-        while (rc == LF_OK) {
-            rc = lf::session_enqueue(ss, nullptr, nullptr);
-            if (rc) break;
-            rc = lf::session_harvest(ss, &active);
-            if (rc || active == 0) break;
-        }
+        if (rc) break;
+        rc = lf::session_harvest(ss, &active);
+        if (rc || active == 0) break;
     }
     if (rc == LF_OK) rc = lf_search_end(ss, d_out_ids, d_out_dists);
     lf_search_free(ss);

@@ -159,9 +159,10 @@ def search_batch(index, queries, k: int = 1, *, bsf_factor: float = 1.0, predict
     predictions: device fp32 [Q, F] filter outputs (FilterPack.predict), with
     offsets [F] (fp64) and leaf_filter int32 [n_leaves] (filter slot per leaf
     slot, -1 for unfiltered leaves).
-    filters: a tensor-core FilterPack INSTEAD of predictions (lazy inference inside
-    lf_search: only the (query, leaf) pairs the walk can reach are predicted, with the
-    same kernel arithmetic, so results equal the predictions path bit for bit).
+    filters: an fp16 tensor-core FilterPack (path "tc16") INSTEAD of predictions
+    (in-search inference: one pass right after round 0 predicts only the (query, leaf)
+    pairs the walk can still reach, with the dense kernel's arithmetic, so results and
+    counters equal the predictions path bit for bit).
     """
     torch = _lib.require_cuda()
     t = as_tree(index)
@@ -188,15 +189,16 @@ def search_batch(index, queries, k: int = 1, *, bsf_factor: float = 1.0, predict
             raise ValueError("pass predictions or filters, not both")
         if offsets is None or leaf_filter is None:
             raise ValueError("filters need offsets and a leaf->filter map")
-        if filters.path != "tc":
-            raise ValueError("lazy filter inference needs the tensor-core filter path")
+        if filters.path != "tc16":
+            raise ValueError("in-search filter inference needs the fp16 tensor-core filter pack (path 'tc16')")
         off = torch.as_tensor(np.asarray(offsets, dtype=np.float64) if not isinstance(offsets, torch.Tensor)
                               else offsets, dtype=torch.float64).to(dev).contiguous()
         lf = leaf_filter.to(device=dev, dtype=torch.int32).contiguous()
         if off.shape[0] != filters.n_filters or lf.shape != (di.n_leaves,):
             raise ValueError("filter / offset / leaf map shapes do not agree")
         keep += [off, lf]
-        opts.d_W1T, opts.d_b1 = filters.W1T.data_ptr(), filters.b1.data_ptr()
+        opts.d_W1T_h, opts.d_wexp = filters.W1T_h.data_ptr(), filters.wexp.data_ptr()
+        opts.d_b1 = filters.b1.data_ptr()
         opts.d_W2, opts.d_b2 = filters.W2.data_ptr(), filters.b2.data_ptr()
         opts.d_offset, opts.n_filters = off.data_ptr(), int(off.shape[0])
         ist = di.struct(lf)

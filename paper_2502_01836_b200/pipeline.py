@@ -239,13 +239,13 @@ def _as_enhanced(eidx) -> EnhancedIndex:
 
 def search_queries(eidx, queries, k: int = 1, *, target: float | None = None, exact: bool = False,
                    sequential: bool = False, max_round_leaves: int = 256, want_trace: bool = False,
-                   stream=None, copy_out: bool = True, profile=None, lazy: bool = False):
-    """Batched LeaFi search in one lf_search call.  lazy=False (default): one
-    lf_filter_predict over every (query, filter) pair first; lazy=True (tensor-core
-    packs): filters are evaluated inside the search, only for the (query, leaf) pairs
-    the walk can still reach.  Both give identical results and counters.  On the bench
-    workload the dense pass wins (1.3 ms for 4.1M pairs vs 2.4 ms for 0.31M lazy pairs:
-    every lazy pass re-reads the 1 GB of first-layer weights)."""
+                   stream=None, copy_out: bool = True, profile=None, lazy: bool | None = None):
+    """Batched LeaFi search in one lf_search call.  lazy=True (default for the fp16
+    pack, path "tc16"): the filters are evaluated inside the search, in one tensor-core
+    pass right after round 0, only for the (query, leaf) pairs the walk can still reach
+    (lb <= bsf0 * f; 0.42M of the 4.1M pairs on the bench workload).  lazy=False: one
+    lf_filter_predict over every (query, filter) pair first.  Both give identical
+    results and counters (same kernel arithmetic)."""
     e = _as_enhanced(eidx)
     if exact or not e.filters:
         return search_batch(e.base, queries, k, sequential=sequential, max_round_leaves=max_round_leaves,
@@ -258,8 +258,10 @@ def search_queries(eidx, queries, k: int = 1, *, target: float | None = None, ex
     q = queries if isinstance(queries, torch.Tensor) else torch.from_numpy(
         np.ascontiguousarray(np.atleast_2d(queries), dtype=np.float32))
     q = q.to(device=di.device, dtype=torch.float32)
-    if lazy and pk.path != "tc":
-        raise ValueError("lazy filter inference runs on the tf32 pack (FilterPack path 'tc', LF_FILTER_PATH=tc)")
+    if lazy is None:
+        lazy = pk.path == "tc16"
+    if lazy and pk.path != "tc16":
+        raise ValueError("in-search filter inference runs on the fp16 pack (FilterPack path 'tc16')")
     if lazy:
         return search_batch(e.base, q.contiguous(), k, filters=pk, offsets=e.offset_vector(target, device=True),
                             leaf_filter=pk.leaf_filter(di), sequential=sequential,

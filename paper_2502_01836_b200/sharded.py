@@ -49,11 +49,14 @@ class GpuRoundEngine:
         o.max_round_leaves = int(max_round_leaves)
         o.early_abandon = 1 if early_abandon else 0
         lf = None
-        if filters is not None:                      # lazy inference inside the session
+        if filters is not None:                      # in-search inference (fp16 pack)
+            if filters.path != "tc16":
+                raise ValueError("in-search filter inference needs the fp16 tensor-core filter pack (path 'tc16')")
             off = torch.as_tensor(offsets, dtype=torch.float64).to(self.device).contiguous()
             lf = leaf_filter.to(device=self.device, dtype=torch.int32).contiguous()
             self._keep += [off, lf, filters]
-            o.d_W1T, o.d_b1 = filters.W1T.data_ptr(), filters.b1.data_ptr()
+            o.d_W1T_h, o.d_wexp = filters.W1T_h.data_ptr(), filters.wexp.data_ptr()
+            o.d_b1 = filters.b1.data_ptr()
             o.d_W2, o.d_b2 = filters.W2.data_ptr(), filters.b2.data_ptr()
             o.d_offset = off.data_ptr()
             o.n_filters = int(off.shape[0])
@@ -86,7 +89,7 @@ class GpuRoundEngine:
 
     @property
     def async_rounds(self) -> bool:
-        return self._opts.d_W1T is None          # lazy inference needs host decisions per round
+        return True                              # every round decision stays on the device
 
     def enqueue(self, bound, bsf_out, active_dev) -> None:
         """Enqueue one round without a host sync; its active count lands in active_dev (int32 [1])."""
@@ -233,11 +236,13 @@ class ShardedResult:
 
 def search_sharded(tree, queries, k: int = 1, *, rank: int, world: int, pack=None, offsets=None,
                    bsf_factor: float = 1.0, max_round_leaves: int = 256, group=None, copy_out: bool = True,
-                   profile=None, lazy: bool = False):
+                   profile=None, lazy: bool | None = None):
     """Leaf-sharded batched search on this rank's GPU (call on every rank).
 
     pack: this rank's FilterPack (its local filters only) with `offsets` in pack
-    order; predictions are computed for the local filters only.
+    order; predictions are computed for the local filters only.  lazy (default: when
+    the pack is fp16, path "tc16"): in-search inference after round 0 instead of a
+    dense pass over every (query, filter) pair; results are identical.
     """
     torch = _lib.require_cuda()
     di = tree.shard(rank, world)
@@ -246,9 +251,9 @@ def search_sharded(tree, queries, k: int = 1, *, rank: int, world: int, pack=Non
     q = q.to(device=di.device, dtype=torch.float32).contiguous()
     kw = {}
     if pack is not None and pack.n_filters:
+        if lazy is None:
+            lazy = pack.path == "tc16"
         if lazy:
-            if pack.path != "tc":
-                raise ValueError("lazy filter inference runs on the tf32 pack (FilterPack path 'tc')")
             kw = dict(filters=pack, offsets=offsets, leaf_filter=pack.leaf_filter(di))
         else:
             kw = dict(predictions=pack.predict(q), offsets=offsets, leaf_filter=pack.leaf_filter(di))
