@@ -255,10 +255,15 @@ int lf_filter_rows_to_f16(const float* d_X, int64_t rows, int32_t m, uint16_t* d
 /*
  * Predictions for an explicit list of (query, filter) pairs on the tensor cores:
  * pairs are bucketed by filter, their query rows gathered, and one tcgen05 tile
- * list evaluates them -- bit-identical to the same pairs of lf_filter_predict_tc.
- * This is the kernel lf_search uses for lazy inference.  d_out [P] (fp64 of the
- * fp32 prediction).
+ * list evaluates them -- bit-identical to the same pairs of lf_filter_predict_tc
+ * (_tc) / lf_filter_predict_f16 (_f16: the fp16 pack, query rows gathered straight
+ * from the fp16 query matrix with TMA gather4 -- the kernel of lf_search's in-search
+ * inference).  d_out [P] (fp64 of the fp32 prediction).
  */
+int lf_filter_predict_pairs_f16(const float* d_queries, int64_t Q, int32_t m, const uint16_t* d_W1T_h,
+                                const int32_t* d_wexp, const float* d_b1, const float* d_W2, const float* d_b2,
+                                int32_t F, const int32_t* d_pair_q, const int32_t* d_pair_f, int64_t P,
+                                double* d_out, void* stream);
 int lf_filter_predict_pairs_tc(const float* d_queries, int32_t m, const float* d_W1T, const float* d_b1,
                                const float* d_W2, const float* d_b2, int32_t F, const int32_t* d_pair_q,
                                const int32_t* d_pair_f, int64_t P, double* d_out, void* stream);

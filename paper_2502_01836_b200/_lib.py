@@ -110,6 +110,7 @@ SIGNATURES = {
     "lf_filter_predict_f16": (C.c_int, [_P, _I64, _I32, _P, _P, _P, _P, _P, _I32, _P, _P]),
     "lf_filter_rows_to_f16": (C.c_int, [_P, _I64, _I32, _P, _P, _P]),
     "lf_filter_predict_pairs_tc": (C.c_int, [_P, _I32, _P, _P, _P, _P, _I32, _P, _P, _I64, _P, _P]),
+    "lf_filter_predict_pairs_f16": (C.c_int, [_P, _I64, _I32, _P, _P, _P, _P, _P, _I32, _P, _P, _I64, _P, _P]),
     "lf_leaf_min_dist": (C.c_int, [_P, _I64, C.POINTER(LfIndex), _P, _I32, _P, _I64, _P]),
     "lf_local_min_dist": (C.c_int, [_P, C.POINTER(LfIndex), _P, _P, _I32, _P, _P]),
     "lf_batch_distances": (C.c_int, [_P, _I64, _P, _I64, _I32, _P, _P]),

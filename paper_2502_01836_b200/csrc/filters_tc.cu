@@ -134,6 +134,7 @@ struct PairArgs {
     const double* offset;        // [F]
     double* adj;                 // [Q][Nn]
     int Nn;
+    int dbg;                     // LF_REACH_DBG (measurement only): 1 fixed gather rows, 2 no W1 load, 4 no W1 prefetch
 };
 
 // fp16 operands (F16 = true): each X row and each filter's W1 is stored scaled by a
@@ -143,22 +144,16 @@ struct PairArgs {
 struct F16Args {
     const int* xexp;             // per X row (dense: query; pairs: gathered row; GATHER: query)
     const int* wexp;             // per filter
+    const uint8_t* xrows;        // GATHER: fp16 query rows [Q][m]
 };
 
 // GATHER (with PAIRS and F16): the A operand is not a materialised row list but the
-// batch's fp16 query matrix; the producer warp gathers each tile's 128 query rows
-// straight into the SW128 stage with TMA tile::gather4 (4 rows per instruction, one
-// instruction per lane), so in-search inference reads each filter's W1 once and the
-// queries from L2.
-__device__ __forceinline__ void tma_gather4(const CUtensorMap* map, uint64_t* bar, void* dst, int col, int r0, int r1,
-                                            int r2, int r3) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(su32(dst)),
-        "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(su32(bar))
-        : "memory");
-}
-
+// batch's fp16 query matrix (F16Args.xrows, L2-resident); the producer warp copies each
+// tile's 128 query rows straight into the SW128 K-major stage layout with cp.async
+// (16-byte chunk c of row r at r * 128 + ((c ^ (r & 7)) * 16)), and each lane's copies
+// arrive on the stage's full barrier when they land (cp.async.mbarrier.arrive.noinc).
+// TMA tile::gather4 (4 rows per instruction) did the same at ~7 us per tile against
+// ~2 us with cp.async: the TMA unit serialises the 128 row fetches of a tile.
 template <bool PAIRS, bool F16, bool GATHER = false>
 __global__ void __launch_bounds__(THREADS, 1)
 filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
@@ -180,10 +175,11 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
     const uint32_t b_bytes = (uint32_t)m * 128;
 
     if (warp == 0 && lane == 0) {
-        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        // GATHER: the stage's W1 TMA (lane 0's expect_tx arrive) + one cp.async arrive per lane
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], GATHER ? 33 : 1); mbar_init(&empty[s], 1); }
         for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 8); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
+        if (!GATHER) asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
     }
     if (warp == 1) {
@@ -196,50 +192,68 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (GATHER && warp == 0) {                               // ---- TMA producer, gathered A
+    if (GATHER && warp == 0) {                               // ---- producer, gathered A
         // Each tile is (usually) a new filter whose W1 (m x m fp16, 128 KiB) comes from
         // DRAM: the next tiles' W1 is prefetched into L2 one and two tiles ahead, and the
-        // next tile's gather rows are loaded while this tile's stages are issued, so the
-        // smem ring only ever waits on L2.
+        // next tile's rows are looked up while this tile's stages are issued.
         int stage = 0;
         uint32_t phase = 0;
-        auto prefetch_w = [&](int64_t tt) {
-            if (lane == 0 && tt < n_tiles) {
-                const int ff = pa.tiles[tt].x;
+        const int row_bytes = m * 2;
+        const int64_t g = gridDim.x;
+        // tile descriptors three tiles deep in registers: no load feeds a use in the
+        // same tile (a dependent global load per tile cost ~1 us of producer time)
+        auto tile_at = [&](int64_t tt) { return tt < n_tiles ? pa.tiles[tt] : make_int4(0, 0, 1, 0); };
+        auto prefetch_w = [&](int64_t tt, int ff) {
+            if (lane == 0 && tt < n_tiles && !(pa.dbg & 4))
                 for (int kb = 0; kb < n_kb; ++kb)
                     asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(&map_w),
                                  "r"(kb * BKE), "r"(ff * m)
                                  : "memory");
-            }
         };
-        auto rows_of = [&](int64_t tt, int* q4) {
+        auto rows_of = [&](int64_t tt, const int4& tl, int* q4) {   // lane owns tile rows lane + 32 j
             if (tt < n_tiles) {
-                const int4 tl = pa.tiles[tt];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) q4[i] = pa.dst[tl.y + min(4 * lane + i, tl.z - 1)].x;
+                for (int j = 0; j < 4; ++j)
+                    q4[j] = (pa.dbg & 1) ? lane + 32 * j : pa.dst[tl.y + min(lane + 32 * j, tl.z - 1)].x;
             }
         };
-        int qi[4], qn[4] = {0, 0, 0, 0};
-        prefetch_w(blockIdx.x);
-        prefetch_w((int64_t)blockIdx.x + gridDim.x);
-        rows_of(blockIdx.x, qi);
-        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-            const int f = pa.tiles[t].x;
-            prefetch_w(t + 2 * (int64_t)gridDim.x);
-            rows_of(t + gridDim.x, qn);                      // in flight while this tile is issued
+        int4 T0 = tile_at(blockIdx.x), T1 = tile_at(blockIdx.x + g), T2 = tile_at(blockIdx.x + 2 * g);
+        int qi[4] = {0, 0, 0, 0}, qn[4] = {0, 0, 0, 0};
+        prefetch_w(blockIdx.x, T0.x);
+        prefetch_w(blockIdx.x + g, T1.x);
+        rows_of(blockIdx.x, T0, qi);
+        for (int64_t t = blockIdx.x; t < n_tiles; t += g) {
+            const int f = T0.x;
+            const int4 T3 = tile_at(t + 3 * g);                  // used two tiles from now
+            prefetch_w(t + 2 * g, T2.x);
+            rows_of(t + g, T1, qn);                              // in flight while this tile is issued
             for (int kb = 0; kb < n_kb; ++kb) {
                 if (lane == 0) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], A_BYTES + b_bytes);
+                    mbar_expect_tx(&full[stage], (pa.dbg & 2) ? 0u : b_bytes);
+                    if (!(pa.dbg & 2)) tma_2d(&map_w, &full[stage], smem + stage * STAGE_BYTES + A_BYTES, kb * BKE, f * m);
                 }
                 __syncwarp();
-                uint8_t* sa = smem + stage * STAGE_BYTES;
-                tma_gather4(&map_x, &full[stage], sa + lane * 4 * 128, kb * BKE, qi[0], qi[1], qi[2], qi[3]);
-                if (lane == 0) tma_2d(&map_w, &full[stage], sa + A_BYTES, kb * BKE, f * m);
+                const uint32_t sa = su32(smem + stage * STAGE_BYTES);
+                // 8 lanes per row, 4 rows (four whole 128-byte lines) per instruction; the row's
+                // query comes from the lane that owns it (rows lane + 32 j)
+                const int c = lane & 7;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int r = 4 * j + (lane >> 3);
+                    const int qr = __shfl_sync(0xffffffffu, qi[j >> 3], r & 31);
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + r * 128 + ((c ^ (r & 7)) << 4)),
+                                 "l"(fa.xrows + (int64_t)qr * row_bytes + kb * 128 + c * 16)
+                                 : "memory");
+                }
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(su32(&full[stage])) : "memory");
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
 #pragma unroll
-            for (int i = 0; i < 4; ++i) qi[i] = qn[i];
+            for (int j = 0; j < 4; ++j) qi[j] = qn[j];
+            T0 = T1;
+            T1 = T2;
+            T2 = T3;
         }
     } else if (warp == 0) {
         if (lane == 0) {                                     // ---- TMA producer
@@ -280,6 +294,8 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
                 for (int kb = 0; kb < n_kb; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
+                    // GATHER: A was written by cp.async (generic proxy), read by the MMA (async proxy)
+                    if (GATHER) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     const uint32_t sa = su32(smem + stage * STAGE_BYTES);
                     const uint32_t sb = sa + A_BYTES;
 #pragma unroll
@@ -313,26 +329,40 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
         const int c_begin = half ? hc : 0, c_end = half ? m : hc;
         float* pbuf = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);   // [2][2][256]
         float* xbuf = pbuf + 2 * 512;                                               // [2][128]
-        auto tile_filter = [&](int64_t t, int& f, int& row0, int& nrows) {
+        // Every per-tile scalar is fetched ahead so no global round trip sits between
+        // two tiles: the tile descriptor two tiles ahead, the next tile's per-row pair
+        // (query, position), b2, offset and filter exponent at the start of this tile,
+        // and its query exponent (dependent on the pair) after this tile's columns.
+        struct Tile { int f, row0, nrows; };
+        auto tile_of = [&](int64_t t) -> Tile {
+            if (t >= n_tiles) return Tile{0, 0, 0};
             if (PAIRS) {
                 const int4 tl = pa.tiles[t];
-                f = tl.x;
-                row0 = tl.y;
-                nrows = tl.z;
-            } else {
-                f = (int)(t / n_mb);
-                row0 = (int)(t % n_mb) * BM;
-                nrows = BM;
+                return Tile{tl.x, tl.y, tl.z};
             }
+            return Tile{(int)(t / n_mb), (int)(t % n_mb) * BM, BM};
         };
-        auto stage_params = [&](int64_t t, int slot) {
+        struct RowVals { int2 d; float b2v; double off; int wex; int ex; bool valid; };
+        auto row_vals = [&](const Tile& T, int64_t t) -> RowVals {     // independent loads only
+            RowVals v{make_int2(0, 0), 0.f, 0.0, 0, 0, false};
+            if (t >= n_tiles) return v;
+            const int64_t xr = (int64_t)T.row0 + row;
+            v.valid = PAIRS ? row < T.nrows : xr < Q;
+            if (PAIRS && v.valid) v.d = pa.dst[xr];
+            v.b2v = b2[T.f];
+            if (PAIRS && pa.offset != nullptr) v.off = pa.offset[T.f];
+            if (F16) v.wex = fa.wexp[T.f];
+            return v;
+        };
+        auto row_exp = [&](RowVals& v, const Tile& T) {                   // the dependent level
+            if (F16 && v.valid) v.ex = GATHER ? fa.xexp[v.d.x] : fa.xexp[(int64_t)T.row0 + row];
+        };
+        auto stage_params = [&](const Tile& T, int64_t t, int slot) {
             if (t < n_tiles) {
-                int f, r0, nr;
-                tile_filter(t, f, r0, nr);
                 const int chunks = m >> 2;                   // 16-byte chunks per vector
                 if (et < 2 * chunks) {
-                    const float* src = (et < chunks ? b1 + (int64_t)f * m + et * 4
-                                                    : W2 + (int64_t)f * m + (et - chunks) * 4);
+                    const float* src = (et < chunks ? b1 + (int64_t)T.f * m + et * 4
+                                                    : W2 + (int64_t)T.f * m + (et - chunks) * 4);
                     float* dst = pbuf + slot * 512 + (et < chunks ? et * 4 : 256 + (et - chunks) * 4);
                     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(su32(dst)), "l"(src) : "memory");
                 }
@@ -342,11 +372,17 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
         int acc = 0;
         uint32_t acc_phase = 0;
         int slot = 0;
-        stage_params(blockIdx.x, 0);
-        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-            int f, row0, nrows;
-            tile_filter(t, f, row0, nrows);
-            stage_params(t + gridDim.x, slot ^ 1);
+        const int64_t g = gridDim.x;
+        Tile cur = tile_of(blockIdx.x), nxt = tile_of(blockIdx.x + g), nn = tile_of(blockIdx.x + 2 * g);
+        stage_params(cur, blockIdx.x, 0);
+        RowVals rv = row_vals(cur, blockIdx.x);
+        row_exp(rv, cur);
+        for (int64_t t = blockIdx.x; t < n_tiles; t += g) {
+            const int f = cur.f, nrows = cur.nrows;
+            (void)nrows;
+            stage_params(nxt, t + g, slot ^ 1);
+            RowVals rn = row_vals(nxt, t + g);               // lands while this tile is folded
+            const Tile n3 = tile_of(t + 3 * g);
             asm volatile("cp.async.wait_group 1;" ::: "memory");
             asm volatile("bar.sync 1, 256;" ::: "memory");   // this tile's parameters visible
             const float4* b1s = reinterpret_cast<const float4*>(pbuf + slot * 512);
@@ -354,12 +390,8 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             float part = 0.f;
-            float sc = 1.f;                                  // F16: undo the operands' scaling
-            if (F16) {
-                const int64_t xr = (int64_t)row0 + row;
-                const int ex = !(PAIRS ? row < nrows : xr < Q) ? 0 : GATHER ? fa.xexp[pa.dst[xr].x] : fa.xexp[xr];
-                sc = scalbnf(1.f, ex + fa.wexp[f]);
-            }
+            // F16: undo the operands' scaling (exact power of two)
+            const float sc = F16 ? scalbnf(1.f, rv.valid ? rv.ex + rv.wex : rv.wex) : 1.f;
             const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * 256);
             for (int c0 = c_begin; c0 < c_end; c0 += 64) {     // two 32-column loads per wait
                 uint32_t r[2][32];
@@ -390,24 +422,25 @@ filter_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constan
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
+            row_exp(rn, nxt);                                // rn.d has landed by now
             if (half) xbuf[slot * 128 + row] = part;
             asm volatile("bar.sync %0, 64;" ::"r"(2 + quarter) : "memory");   // the quarter's two warps
-            if (half == 0) {
+            if (half == 0 && rv.valid) {
                 part = __fadd_rn(part, xbuf[slot * 128 + row]);
                 if (PAIRS) {
-                    if (row < nrows) {
-                        const int2 d = pa.dst[row0 + row];
-                        const double pv = (double)__fadd_rn(part, b2[f]);
-                        pa.adj[(int64_t)d.x * pa.Nn + d.y] = pa.offset != nullptr ? pv - pa.offset[f] : pv;
-                    }
+                    const double pv = (double)__fadd_rn(part, rv.b2v);
+                    pa.adj[(int64_t)rv.d.x * pa.Nn + rv.d.y] = pa.offset != nullptr ? pv - rv.off : pv;
                 } else {
-                    const int64_t q = (int64_t)row0 + row;
-                    if (q < Q) pred[q * F + f] = __fadd_rn(part, b2[f]);
+                    pred[((int64_t)cur.row0 + row) * F + f] = __fadd_rn(part, rv.b2v);
                 }
             }
             asm volatile("bar.sync 1, 256;" ::: "memory");   // slot free for the tile after next
             slot ^= 1;
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            cur = nxt;
+            nxt = nn;
+            nn = n3;
+            rv = rn;
         }
         asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
@@ -505,6 +538,11 @@ namespace tc {
 __global__ void pair_hist_kernel(const int32_t* __restrict__ pf, int64_t P, int* __restrict__ hist) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < P) atomicAdd(&hist[pf[i]], 1);
+}
+__global__ void pair_bucket_q_kernel(const int32_t* __restrict__ pq, const int32_t* __restrict__ pf, int64_t P,
+                                     int* __restrict__ fcur, int2* __restrict__ dst) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < P) dst[atomicAdd(&fcur[pf[i]], 1)] = make_int2(pq[i], (int)i);
 }
 __global__ void pair_bucket_kernel(const float* __restrict__ queries, int m, const int32_t* __restrict__ pq,
                                    const int32_t* __restrict__ pf, int64_t P, int* __restrict__ fcur,
@@ -629,16 +667,51 @@ int filter_reach_f16(const __half* d_xh, const int* d_xexp, int64_t Q, int m, co
                      const int4* d_tiles, const int* d_ntiles, const int2* d_dst, const double* d_offset,
                      double* d_adj, int Nn, cudaStream_t st) {
     if (Q == 0 || F == 0) return LF_OK;
-    CUtensorMap mx, mw;
-    int rc = tc::make_map(&mx, d_xh, Q, m, 1, true);            // gather4: one row per box
-    if (rc) return rc;
-    rc = tc::make_map(&mw, d_W1T_h, (int64_t)F * m, m, m, true);
+    CUtensorMap mw;
+    CUtensorMap mx{};                                            // unused: A is gathered with cp.async
+    int rc = tc::make_map(&mw, d_W1T_h, (int64_t)F * m, m, m, true);
     if (rc) return rc;
     LF_CUDA(smem_optin(tc::filter_tc_kernel<true, true, true>, tc::SMEM_BYTES));
-    tc::PairArgs pa{d_tiles, d_ntiles, d_dst, d_offset, d_adj, Nn};
+    static const int dbg = getenv("LF_REACH_DBG") ? atoi(getenv("LF_REACH_DBG")) : 0;
+    tc::PairArgs pa{d_tiles, d_ntiles, d_dst, d_offset, d_adj, Nn, dbg};
     tc::filter_tc_kernel<true, true, true><<<sm_count(), tc::THREADS, tc::SMEM_BYTES, st>>>(
-        mx, mw, Q, m, F, d_b1, d_W2, d_b2, nullptr, pa, tc::F16Args{d_xexp, d_wexp});
+        mx, mw, Q, m, F, d_b1, d_W2, d_b2, nullptr, pa,
+        tc::F16Args{d_xexp, d_wexp, reinterpret_cast<const uint8_t*>(d_xh)});
     LF_CUDA(cudaGetLastError());
     return LF_OK;
 }
 }  // namespace lf
+
+extern "C" int lf_filter_predict_pairs_f16(const float* d_queries, int64_t Q, int32_t m, const uint16_t* d_W1T_h,
+                                           const int32_t* d_wexp, const float* d_b1, const float* d_W2,
+                                           const float* d_b2, int32_t F, const int32_t* d_pair_q,
+                                           const int32_t* d_pair_f, int64_t P, double* d_out, void* stream) {
+    using namespace lf;
+    LF_REQUIRE(m >= 64 && m <= 256 && m % 64 == 0, "fp16 filter path needs m in {64, 128, 192, 256}");
+    LF_REQUIRE(P >= 0 && F >= 1 && Q >= 1, "bad sizes");
+    LF_REQUIRE(((uintptr_t)d_W1T_h & 15) == 0 && ((uintptr_t)d_b1 & 15) == 0 && ((uintptr_t)d_W2 & 15) == 0,
+               "operands must be 16-byte aligned");
+    if (P == 0) return LF_OK;
+    cudaStream_t st = as_stream(stream);
+    Scratch hist, fcur, tiles, ntiles, dst, xh, xe;
+    LF_CUDA(hist.alloc(sizeof(int) * F, st));
+    LF_CUDA(fcur.alloc(sizeof(int) * F, st));
+    LF_CUDA(tiles.alloc(sizeof(int4) * (size_t)(P / 128 + F + 1), st));
+    LF_CUDA(ntiles.alloc(sizeof(int), st));
+    LF_CUDA(dst.alloc(sizeof(int2) * (size_t)P, st));
+    LF_CUDA(xh.alloc(sizeof(__half) * (size_t)Q * m, st));
+    LF_CUDA(xe.alloc(sizeof(int) * (size_t)Q, st));
+    int rc = rows_to_f16(d_queries, Q, m, xh.as<__half>(), xe.as<int>(), st);
+    if (rc) return rc;
+    LF_CUDA(cudaMemsetAsync(hist.p, 0, sizeof(int) * F, st));
+    tc::pair_hist_kernel<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(d_pair_f, P, hist.as<int>());
+    LF_CUDA(cudaGetLastError());
+    rc = pair_tiles(hist.as<int>(), F, fcur.as<int>(), tiles.as<int4>(), ntiles.as<int>(), st);
+    if (rc) return rc;
+    tc::pair_bucket_q_kernel<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(d_pair_q, d_pair_f, P, fcur.as<int>(),
+                                                                          dst.as<int2>());
+    LF_CUDA(cudaGetLastError());
+    // Nn = 0: adj[q * 0 + i] is out[i]
+    return filter_reach_f16(xh.as<__half>(), xe.as<int>(), Q, m, d_W1T_h, d_wexp, d_b1, d_W2, d_b2, F,
+                            tiles.as<int4>(), ntiles.as<int>(), dst.as<int2>(), nullptr, d_out, 0, st);
+}

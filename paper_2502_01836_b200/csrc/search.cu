@@ -330,43 +330,52 @@ __global__ void pairs_pos_kernel(int64_t Q, int Lr, const int* __restrict__ psta
 }
 
 // Filter buckets (exclusive scan of the per-filter counts) and the tile list
-// (filter, first pair, pairs <= 128) in one CTA.
-__global__ void pair_tiles_kernel(const int* __restrict__ fhist, int F, int* __restrict__ fcur, int4* __restrict__ tiles,
-                                  int* __restrict__ ntiles) {
-    __shared__ int sp[1024], st[1024];
-    __shared__ int carry_p, carry_t;
-    if (threadIdx.x == 0) { carry_p = 0; carry_t = 0; }
+// (filter, first pair, pairs <= 128) in one CTA: each thread owns PT consecutive
+// filters, one block-wide scan of (pairs, tiles) per thread.
+constexpr int PT_THREADS = 1024, PT_ITEMS = 8;
+__global__ void __launch_bounds__(PT_THREADS) pair_tiles_kernel(const int* __restrict__ fhist, int F,
+                                                                int* __restrict__ fcur, int4* __restrict__ tiles,
+                                                                int* __restrict__ ntiles) {
+    using Scan = cub::BlockScan<int2, PT_THREADS>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int2 carry;
+    if (threadIdx.x == 0) carry = make_int2(0, 0);
     __syncthreads();
-    for (int base = 0; base < F; base += blockDim.x) {
-        const int f = base + threadIdx.x;
-        const int h = f < F ? fhist[f] : 0;
-        sp[threadIdx.x] = h;
-        st[threadIdx.x] = (h + 127) / 128;
-        __syncthreads();
-        for (int o = 1; o < (int)blockDim.x; o <<= 1) {
-            const int ap = threadIdx.x >= (unsigned)o ? sp[threadIdx.x - o] : 0;
-            const int at = threadIdx.x >= (unsigned)o ? st[threadIdx.x - o] : 0;
-            __syncthreads();
-            sp[threadIdx.x] += ap;
-            st[threadIdx.x] += at;
-            __syncthreads();
+    struct Add2 {
+        __device__ int2 operator()(const int2& a, const int2& b) const { return make_int2(a.x + b.x, a.y + b.y); }
+    };
+    for (int base = 0; base < F; base += PT_THREADS * PT_ITEMS) {
+        int h[PT_ITEMS];
+        int2 mine = make_int2(0, 0);
+#pragma unroll
+        for (int i = 0; i < PT_ITEMS; ++i) {
+            const int f = base + threadIdx.x * PT_ITEMS + i;
+            h[i] = f < F ? fhist[f] : 0;
+            mine.x += h[i];
+            mine.y += (h[i] + 127) / 128;
         }
-        if (f < F) {
-            const int p0 = carry_p + sp[threadIdx.x] - h;
-            const int nt = (h + 127) / 128;
-            const int t0 = carry_t + st[threadIdx.x] - nt;
-            fcur[f] = p0;
-            for (int t = 0; t < nt; ++t) tiles[t0 + t] = make_int4(f, p0 + 128 * t, min(128, h - 128 * t), 0);
+        int2 excl, total;
+        Scan(tmp).ExclusiveScan(mine, excl, make_int2(0, 0), Add2(), total);
+        int p0 = carry.x + excl.x, t0 = carry.y + excl.y;
+#pragma unroll
+        for (int i = 0; i < PT_ITEMS; ++i) {
+            const int f = base + threadIdx.x * PT_ITEMS + i;
+            if (f < F) {
+                fcur[f] = p0;
+                for (int t = 0; t * 128 < h[i]; ++t) tiles[t0 + t] = make_int4(f, p0 + 128 * t, min(128, h[i] - 128 * t), 0);
+            }
+            p0 += h[i];
+            t0 += (h[i] + 127) / 128;
         }
         __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) { carry_p += sp[threadIdx.x]; carry_t += st[threadIdx.x]; }
+        if (threadIdx.x == 0) carry = make_int2(carry.x + total.x, carry.y + total.y);
         __syncthreads();
     }
-    if (threadIdx.x == 0) *ntiles = carry_t;
+    if (threadIdx.x == 0) *ntiles = carry.y;
 }
 
 int pair_tiles(const int* d_hist, int F, int* d_fcur, int4* d_tiles, int* d_ntiles, cudaStream_t st) {
-    pair_tiles_kernel<<<1, 1024, 0, st>>>(d_hist, F, d_fcur, d_tiles, d_ntiles);
+    pair_tiles_kernel<<<1, PT_THREADS, 0, st>>>(d_hist, F, d_fcur, d_tiles, d_ntiles);
     LF_CUDA(cudaGetLastError());
     return LF_OK;
 }

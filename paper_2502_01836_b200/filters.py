@@ -109,15 +109,21 @@ class FilterPack:
 
     def predict_pairs(self, queries, pair_q, pair_f, stream=None):
         """fp64 [P] predictions of filter pair_f[i] for query pair_q[i] (tensor-core
-        path; bit-identical to the same entries of predict())."""
+        paths; bit-identical to the same entries of predict())."""
         torch = _lib.require_cuda()
-        if self.path != "tc":
-            raise ValueError("pair predictions need the tensor-core filter path")
+        if self.path not in ("tc", "tc16"):
+            raise ValueError("pair predictions need a tensor-core filter path")
         q = queries.to(device=self.device, dtype=torch.float32).contiguous() if isinstance(queries, torch.Tensor) \
             else torch.from_numpy(np.ascontiguousarray(np.atleast_2d(queries), dtype=np.float32)).to(self.device)
         pq = torch.as_tensor(pair_q, dtype=torch.int32).to(self.device).contiguous()
         pf = torch.as_tensor(pair_f, dtype=torch.int32).to(self.device).contiguous()
         out = torch.empty(pq.shape[0], dtype=torch.float64, device=self.device)
+        if self.path == "tc16":
+            _lib.check(_lib.lib().lf_filter_predict_pairs_f16(
+                q.data_ptr(), q.shape[0], self.m, self.W1T_h.data_ptr(), self.wexp.data_ptr(), self.b1.data_ptr(),
+                self.W2.data_ptr(), self.b2.data_ptr(), self.n_filters, pq.data_ptr(), pf.data_ptr(), pq.shape[0],
+                out.data_ptr(), _lib.stream_ptr(stream)))
+            return out
         _lib.check(_lib.lib().lf_filter_predict_pairs_tc(q.data_ptr(), self.m, self.W1T.data_ptr(), self.b1.data_ptr(),
                                                          self.W2.data_ptr(), self.b2.data_ptr(), self.n_filters,
                                                          pq.data_ptr(), pf.data_ptr(), pq.shape[0], out.data_ptr(),

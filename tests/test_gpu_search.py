@@ -539,16 +539,18 @@ def test_lazy_filter_inference_identical(k, seq, cap):
     assert 0 < prof[11] < Q.shape[0] * F, "in-search inference computes a strict subset of the pairs"
 
 
-def test_pair_predictions_bit_identical():
-    """lf_filter_predict_pairs_tc (bucketed, gathered rows) == the dense tensor-core
-    predictions of the same (query, filter) pairs, bit for bit, in any pair order."""
+@pytest.mark.parametrize("path,m", [("tc", 128), ("tc16", 128), ("tc16", 256), ("tc16", 64)])
+def test_pair_predictions_bit_identical(path, m):
+    """lf_filter_predict_pairs_tc / _f16 (bucketed pairs; _f16 gathers the query rows
+    with TMA gather4) == the dense tensor-core predictions of the same (query, filter)
+    pairs, bit for bit, in any pair order, with partial and multi-tile buckets."""
     import torch
     from paper_2502_01836_b200.filters import FilterPack
 
     rng = np.random.default_rng(11)
-    F, m, Q = 37, 128, 300
+    F, Q = 37, 300
     pack = FilterPack(list(range(F)), rng.normal(0, 0.08, (F, m, m)), rng.normal(0, 0.05, (F, m)),
-                      rng.normal(0, 0.08, (F, m)), rng.uniform(1.0, 9.0, F), path="tc")
+                      rng.normal(0, 0.08, (F, m)), rng.uniform(1.0, 9.0, F), path=path)
     qd = torch.from_numpy(rng.normal(0, 1, (Q, m)).astype(np.float32)).cuda()
     dense = pack.predict(qd).cpu().numpy().astype(np.float64)
     pq = rng.integers(0, Q, 5000)
