@@ -161,6 +161,10 @@ struct PQOverflow {
     int mp;
     float* lo8;                               // [cap] int8 lower bound of each entry
     unsigned* thr;                            // [max_tasks] the projected stage's threshold (float bits)
+    // round 0 (no best-so-far yet, k = 1): every task exactly scores the row its projected
+    // codes rank nearest and prunes with that distance; qbest [Q] shares the best seed of
+    // a query's tasks (float bits, atomicMin).  nullptr: no seeding.
+    unsigned* qbest;
 };
 int pq_scan_warps();                          // warps of one scan_pq_kernel launch
 constexpr int PQ_OVER_CAP = 8 << 20;          // 8M entries (128 MB + lo8)

@@ -209,7 +209,14 @@ __device__ __forceinline__ void pq_select(const RoundState& s, long long t, int 
     }
 }
 
-template <int KP>
+// SEED (round 0, k = 1; ov.qbest): with no best-so-far the projected upper bound
+// (residual term r + r_q) is loose and most rows would survive.  Each task tracks the
+// row with the smallest projected ESTIMATE ||y - y_q||^2 + r^2 + r_q^2 (residuals taken
+// as orthogonal), reads that one row exactly (fp64, the warp's 1 KiB load) and prunes
+// with its distance -- a real row's exact distance bounds the task's (and query's)
+// nearest from above, so the cascade stays exact.  Tasks of one query share the best
+// seed through ov.qbest.
+template <int KP, bool SEED>
 __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState s, lf_index idx,
                                                                       const float* __restrict__ queries,
                                                                       const int8_t* __restrict__ qcodes,
@@ -291,6 +298,9 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
         // comparisons below run in the squared domain (one sqrt per task, not two per row)
         float lo2[PQ_SLOTS];
         float hmin2 = __int_as_float(0x7f800000);
+        float best_est = __int_as_float(0x7f800000);      // SEED: smallest estimate, its row
+        int best_ri = 0;
+        const float rq2 = rq * rq;
 #pragma unroll
         for (int p = 0; p < PQ_PIECES; ++p) {
             if (p < pieces) {
@@ -326,6 +336,10 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
                     const float bhi = rs * (1.f + 1e-6f);
                     lo2[p * RPL + u] = v ? fmaf(alo, alo, blo * blo) : __int_as_float(0x7f800000);
                     hmin2 = fminf(hmin2, v ? fmaf(ahi, ahi, bhi * bhi) : __int_as_float(0x7f800000));
+                    if (SEED) {
+                        const float est = fmaf(mr.w, mr.w, a2 + rq2);
+                        if (v && est < best_est) { best_est = est; best_ri = p * PQW_STG + ri; }
+                    }
                 }
                 __syncwarp();                            // every lane has read the slot
                 issue(cslot);                            // refill it NS pieces ahead
@@ -340,6 +354,33 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) hmin2 = fminf(hmin2, __shfl_xor_sync(0xffffffffu, hmin2, o));
             thr = fmin(thr, (double)(sqrtf(hmin2) * (1.f + 1e-5f)));
+        }
+        if (SEED && nrows > 0) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float oe = __shfl_xor_sync(0xffffffffu, best_est, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, best_ri, o);
+                if (oe < best_est || (oe == best_est && oi < best_ri)) { best_est = oe; best_ri = oi; }
+            }
+            // the seed row, exactly (series.py:142-146 direct form in fp64)
+            const float* xr = idx.d_X + (r0 + best_ri) * m;
+            const float* qr = queries + q * m;
+            double acc = 0.0;
+            for (int c = lane * 4; c < m; c += 128) {
+                const float4 xv = __ldg(reinterpret_cast<const float4*>(xr + c));
+                const float4 qv = __ldg(reinterpret_cast<const float4*>(qr + c));
+                const double d0 = (double)xv.x - qv.x, d1 = (double)xv.y - qv.y;
+                const double d2 = (double)xv.z - qv.z, d3 = (double)xv.w - qv.w;
+                acc = __fma_rn(d0, d0, acc); acc = __fma_rn(d1, d1, acc);
+                acc = __fma_rn(d2, d2, acc); acc = __fma_rn(d3, d3, acc);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            const float dseed = __double2float_ru(sqrt(acc));
+            unsigned prev = 0;
+            if (lane == 0) prev = atomicMin(ov.qbest + q, __float_as_uint(dseed));
+            prev = __shfl_sync(0xffffffffu, prev, 0);
+            thr = fmin(thr, (double)fminf(dseed, __uint_as_float(prev)));
         }
         const float thr_f = thr < kInf ? __double2float_ru(thr) : __int_as_float(0x7f800000);
         // keep iff sqrt(lo2) (1 - 1e-5) <= thr  <=>  lo2 <= (thr / (1 - 1e-5))^2, rounded up
@@ -575,8 +616,14 @@ cudaError_t launch_project_queries(const float* q, int64_t Q, const lf_index& id
 template <int KP>
 static cudaError_t launch_pq_kp(const RoundState& s, const lf_index& idx, const float* q, const int8_t* qc,
                                 const float4* qm, int* surv_cnt, const PQOverflow& ov, cudaStream_t st) {
-    if (cudaError_t e = smem_optin(scan_pq_kernel<KP>, PQW<KP>::SMEM); e != cudaSuccess) return e;
-    scan_pq_kernel<KP><<<sm_count(), PQW<KP>::WARPS * 32, PQW<KP>::SMEM, st>>>(s, idx, q, qc, qm, surv_cnt, ov);
+    if (ov.qbest != nullptr) {
+        if (cudaError_t e = smem_optin(scan_pq_kernel<KP, true>, PQW<KP>::SMEM); e != cudaSuccess) return e;
+        scan_pq_kernel<KP, true><<<sm_count(), PQW<KP>::WARPS * 32, PQW<KP>::SMEM, st>>>(s, idx, q, qc, qm, surv_cnt,
+                                                                                          ov);
+        return cudaGetLastError();
+    }
+    if (cudaError_t e = smem_optin(scan_pq_kernel<KP, false>, PQW<KP>::SMEM); e != cudaSuccess) return e;
+    scan_pq_kernel<KP, false><<<sm_count(), PQW<KP>::WARPS * 32, PQW<KP>::SMEM, st>>>(s, idx, q, qc, qm, surv_cnt, ov);
     return cudaGetLastError();
 }
 

@@ -480,6 +480,11 @@ static int round_growth_log2() {
     return g >= 1 && g <= 6 ? g : 2;
 }
 
+static bool round0_seeded() {
+    const char* e = getenv("LF_SCAN_ROUND0");
+    return !(e && strcmp(e, "q8") == 0);
+}
+
 static int scan_variant() {
     const char* e = getenv("LF_SCAN_VARIANT");
     if (!e || e[0] == 0 || strcmp(e, "pq") == 0) return 8;   // projected stage when the shadow exists
@@ -510,7 +515,7 @@ struct lf_session {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pev;   // profiling: per prediction pass
     bool q8 = false;                 // int8-bounded scan (query codes quantised once in begin)
     bool pq = false;                 // two-stage scan over the projected shadow (d_Xp)
-    lf::Scratch qcp, qmp, pq_cnt, pq_trows, pq_oent, pq_on, pq_obase, pq_wrows, pq_wdist, pq_lo8, pq_thr;
+    lf::Scratch qcp, qmp, pq_cnt, pq_trows, pq_oent, pq_on, pq_obase, pq_wrows, pq_wdist, pq_lo8, pq_thr, pq_qbest;
     int pq_cap = lf::PQ_OVER_CAP;    // survivor entry capacity (LF_PQ_OVER_CAP: tests of the full-list path)
     int* h_active = nullptr;         // pinned [2 slots][4]: active, -, predict requests
     int round = 0;                   // rounds enqueued
@@ -684,6 +689,8 @@ static int session_begin(lf_session* ss) {
         LF_CUDA(ss->pq_wdist.alloc(sizeof(double) * CH * pq_scan_warps(), st));
         LF_CUDA(ss->pq_lo8.alloc(sizeof(float) * ss->pq_cap, st));
         LF_CUDA(ss->pq_thr.alloc(sizeof(unsigned) * max_tasks, st));
+        LF_CUDA(ss->pq_qbest.alloc(sizeof(unsigned) * Q, st));
+        LF_CUDA(cudaMemsetAsync(ss->pq_qbest.p, 0x7f, sizeof(unsigned) * Q, st));   // 3.4e38: above any distance
         LF_CUDA(launch_project_queries(ss->d_q, Q, idx, ss->qcp.as<int8_t>(), ss->qmp.as<float4>(), st));
         ++ss->kernels;
     }
@@ -787,14 +794,17 @@ static int session_enqueue(lf_session* ss, const double* d_bound, double* d_bsf_
     const bool ea = o.early_abandon && !s.want_trace && idx.m <= 512 && scan_variant() != 0 && ss->q8;
     const int64_t max_tasks =
         std::max<int64_t>(1, Q * s.Rcap * std::max<int64_t>(1, (idx.max_leaf_rows + CH - 1) / CH));
-    if (ea && ss->pq && !(ss->round == 0 && ss->q8)) {
-        // round 0 has no best-so-far yet: the projected bound's loose upper end would let
-        // most rows through, so the first round runs the full-length int8 scan
+    // round 0 has no best-so-far yet: for k = 1 the projected scan seeds its threshold
+    // with one exactly scored row per task (scan_pq_kernel SEED); for k > 1 (or
+    // LF_SCAN_ROUND0=q8) the first round runs the full-length int8 scan
+    const bool seed = ss->round == 0 && s.k == 1 && round0_seeded();
+    if (ea && ss->pq && (ss->round > 0 || !ss->q8 || seed)) {
         const PQOverflow ov{ss->pq_oent.as<int4>(), ss->pq_on.as<int>(),
                             ss->pq_obase.as<int>(), ss->pq_cap, ss->pq_wrows.as<unsigned short>(),
                             ss->pq_wdist.as<double>(), ss->q8 ? ss->qc8.as<int8_t>() : nullptr,
                             ss->q8 ? ss->qm8.as<float4>() : nullptr, (idx.m + 255) / 256 * 256,
-                            ss->pq_lo8.as<float>(), ss->pq_thr.as<unsigned>()};
+                            ss->pq_lo8.as<float>(), ss->pq_thr.as<unsigned>(),
+                            seed ? ss->pq_qbest.as<unsigned>() : nullptr};
         ce = launch_scan_pq(s, idx, ss->d_q, ss->qcp.as<int8_t>(), ss->qmp.as<float4>(), ss->pq_cnt.as<int>(), ov,
                             max_tasks, st);
         ss->kernels += ss->q8 ? 3 : 2;
