@@ -185,6 +185,24 @@ int lf_search(const lf_index* idx, const float* d_queries, int64_t Q,
               int64_t* d_out_stats, const lf_trace* trace, void* stream);
 
 /*
+ * Search plans: the batched search above as ONE CUDA graph, built once for an
+ * (index, Q, opts) and launched per query batch.  The plan owns its scratch; the
+ * graph holds the prologue (bounds, visit orders, query codes), round 0, the
+ * in-search prediction pass and a conditional WHILE node over the rounds (the round
+ * counter and the "any walk active" test live on the device), so a search is a
+ * query copy, one graph launch and the result copies -- no host round trips.
+ * Results and counters are those of lf_search with the same opts (no traces or
+ * profiles: want_trace and h_profile must be 0).  The index, predictions, offsets
+ * and filter buffers named by idx / opts must stay allocated and unchanged for the
+ * plan's life; d_queries [Q][m] may change per run.
+ */
+typedef struct lf_search_plan lf_search_plan;
+lf_search_plan* lf_search_plan_create(const lf_index* idx, int64_t Q, const lf_search_opts* opts, void* stream);
+int lf_search_plan_run(lf_search_plan* plan, const float* d_queries, int64_t* d_out_ids, double* d_out_dists,
+                       int64_t* d_out_stats, void* stream);
+void lf_search_plan_free(lf_search_plan* plan);
+
+/*
  * The same search split into rounds, for callers that exchange the per-query
  * best-so-far between rounds (leaf-sharded multi-GPU: allreduce-min over NVLink).
  *   s = lf_search_begin(idx, q, Q, opts, trace, d_stats, stream)   bounds + order

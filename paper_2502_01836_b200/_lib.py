@@ -99,6 +99,9 @@ SIGNATURES = {
     "lf_bounds": (C.c_int, [_P, _I64, C.POINTER(LfIndex), _P, _P, _I32, _I32, _P, _P, _P]),
     "lf_search": (C.c_int, [C.POINTER(LfIndex), _P, _I64, C.POINTER(LfSearchOpts), _P, _P, _P,
                             C.POINTER(LfTrace), _P]),
+    "lf_search_plan_create": (_P, [C.POINTER(LfIndex), _I64, C.POINTER(LfSearchOpts), _P]),
+    "lf_search_plan_run": (C.c_int, [_P, _P, _P, _P, _P, _P]),
+    "lf_search_plan_free": (None, [_P]),
     "lf_search_begin": (_P, [C.POINTER(LfIndex), _P, _I64, C.POINTER(LfSearchOpts), C.POINTER(LfTrace), _P, _P]),
     "lf_search_round": (C.c_int, [_P, _P, _P, C.POINTER(_I32)]),
     "lf_search_round_async": (C.c_int, [_P, _P, _P, _P]),

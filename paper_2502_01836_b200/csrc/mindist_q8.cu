@@ -135,8 +135,11 @@ mindist_q8_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_consta
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
         for (int s = 0; s < 2; ++s) {
-            mbar_init(&bfull[s], 1);
-            mbar_init(&bempty[s], 1 + EPI_WARPS);
+            // every writer / reader lane arrives itself (the producer's 32 lanes write the
+            // chunk's bound terms; all epilogue lanes read them), so the happens-before
+            // edges are per thread (compute-sanitizer racecheck models them that way)
+            mbar_init(&bfull[s], 32);
+            mbar_init(&bempty[s], 1 + EPI_WARPS * 32);
             mbar_init(&tfull[s], 1);
             mbar_init(&tempty[s], EPI_WARPS);
         }
@@ -185,6 +188,8 @@ mindist_q8_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_consta
                     mbar_expect_tx(&bfull[bb], (uint32_t)(n_kb * B_KB_BYTES));
                     for (int kb = 0; kb < n_kb; ++kb)
                         tma_2d(&map_x, &bfull[bb], Bs + bb * B_BYTES + kb * B_KB_BYTES, kb * KBB, (int)r0);
+                } else {
+                    mbar_arrive(&bfull[bb]);
                 }
                 for (int qb = 0; qb < n_qb; ++qb) {
                     for (int kb = 0; kb < n_kb; ++kb) {
@@ -369,7 +374,7 @@ mindist_q8_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_consta
                     if (++acc == 2) { acc = 0; acc_phase ^= 1; }
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&bempty[bb]);                 // bound terms may be replaced
+                mbar_arrive(&bempty[bb]);                                // bound terms may be replaced
             }
         }
     }

@@ -19,6 +19,8 @@ struct RoundState {
     int64_t Q;
     int k, kc;                   // kc = candidates kept per task = min(k, CH)
     int R, Rcap;                 // leaves per query this round, and the buffer stride
+    int seq, growth;             // sequential schedule; leaves per round grow as 2^(round * growth)
+    const int* d_round;          // device round counter (graph-launched plans): R derived from it, else s.R
     double f;                    // bsf_factor
     const int* order;            // [Q][L] visit-order leaf records (bounds.cuh OrderArgs): node ids (traces)
     const double* lbs;           // [Q][L] leaf bound
@@ -35,7 +37,7 @@ struct RoundState {
     double* top_d;               // [Q][k]   running top-k (round-start state)
     long long* top_i;            // [Q][k]
     int* top_n;                  // [Q]
-    double* top_d_out;           // merge writes here; host swaps after each round
+    double* top_d_out;           // merge's scratch: the new top-k, copied back into top_d
     long long* top_i_out;
     int* top_n_out;
     int n_leaves;

@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(Q8_THREADS, 2) scan_q8_kernel(RoundState s, lf
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
             q8_bar_init(&full[i], 1);
-            q8_bar_init(&empty[i], Q8_CONS_WARPS);
+            q8_bar_init(&empty[i], Q8_CONS_WARPS * 32);   // every consumer lane releases itself
         }
         hi_bits[0] = hi_bits[1] = 0x7f800000u;
         n_surv[0] = n_surv[1] = 0;
@@ -180,8 +180,7 @@ __global__ void __launch_bounds__(Q8_THREADS, 2) scan_q8_kernel(RoundState s, lf
                     if (s.k > 1) hi_s[j + myrow] = hi;
                 }
             }
-            __syncwarp();
-            if (lane == 0) q8_arrive(&empty[slot]);
+            q8_arrive(&empty[slot]);
             if (++slot == S) { slot = 0; ph ^= 1; }
         }
         if (s.k == 1) {

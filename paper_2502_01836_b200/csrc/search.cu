@@ -43,6 +43,8 @@ __global__ void plan_warp_kernel(RoundState s, lf_index idx) {
     if (q >= s.Q) return;
     const unsigned below = (1u << lane) - 1u;
     const int Lr = s.n_leaves;                 // records per query: the leaf slots
+    const int R = s.d_round == nullptr ? s.R
+                  : s.seq ? 1 : (int)min((long long)s.Rcap, 1ll << min(*s.d_round * s.growth, 30));
     int* pre = s.sel_pre + q * (s.Rcap + 1);
     int ns = 0, nch = 0;
     if (!s.done[q]) {
@@ -95,7 +97,7 @@ __global__ void plan_warp_kernel(RoundState s, lf_index idx) {
             const bool fpr = fs >= 0 && ad_c > thr;        // (pred - offset) > bsf * f, tree.py:282
             const bool scan = visit && !fpr;
             const unsigned smask = __ballot_sync(0xffffffffu, scan);
-            const int need = s.R - ns;
+            const int need = R - ns;
             int end;                       // lanes [0, end) are consumed this iteration
             bool quota = false;
             if (__popc(smask) >= need) {
@@ -395,11 +397,7 @@ __global__ void merge_kernel(RoundState s) {
     double* od = s.top_d_out + q * s.k;
     long long* oi = s.top_i_out + q * s.k;
     const int tn = s.top_n[q];
-    if (ns == 0) {
-        for (int i = lane; i < tn; i += 32) { od[i] = td[i]; oi[i] = ti[i]; }
-        if (lane == 0) s.top_n_out[q] = tn;
-        return;
-    }
+    if (ns == 0) return;                       // nothing scanned: the top-k stands
     const long long c0 = s.chunk_off[q], c1 = s.chunk_off[q + 1];
     const long long nc = (c1 - c0) * s.kc;
     const double* cd = s.cand_d + c0 * s.kc;
@@ -444,7 +442,12 @@ __global__ void merge_kernel(RoundState s) {
         last_i = bi;
         ++filled;
     }
-    if (lane == 0) s.top_n_out[q] = filled;
+    // the new top-k back into the running state (every lane has finished reading it)
+    __syncwarp();
+    double* wd = s.top_d + q * s.k;
+    long long* wi = s.top_i + q * s.k;
+    for (int i = lane; i < filled; i += 32) { wd[i] = od[i]; wi[i] = oi[i]; }
+    if (lane == 0) s.top_n[q] = filled;
 }
 
 __global__ void init_state_kernel(RoundState s) {
@@ -507,16 +510,16 @@ struct lf_session {
     lf::RoundState s{};
     lf::Scratch qsumm, lb, lbs, gap, order, cursor, done, topd, topi, topn, topd2, topi2, topn2, sel_leaf,
         sel_trace, sel_pre, n_sel, chunk_off, cand_d, cand_i, task_min, n_active, tasks, ea_count, qc8, qm8,
-        leafo, adj, olen, pcount, pstart, pend, preq, fhist, fcur, ntiles, ptotal, pdst, ptiles, xh, xexp;
+        leafo, adj, olen, pcount, pstart, pend, preq, fhist, fcur, ntiles, ptotal, pdst, ptiles, xh, xexp, round_ctr;
     lf::OrderArgs oa{};
     bool lazy = false;               // in-search filter inference (opts.d_W1T_h instead of predictions)
-    bool predict_pending = false;    // a harvested round asked for predictions (bsf was +inf after round 0)
     int predict_steps = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pev;   // profiling: per prediction pass
     bool q8 = false;                 // int8-bounded scan (query codes quantised once in begin)
     bool pq = false;                 // two-stage scan over the projected shadow (d_Xp)
     lf::Scratch qcp, qmp, pq_cnt, pq_trows, pq_oent, pq_on, pq_obase, pq_wrows, pq_wdist, pq_lo8, pq_thr, pq_qbest;
     int pq_cap = lf::PQ_OVER_CAP;    // survivor entry capacity (LF_PQ_OVER_CAP: tests of the full-list path)
+    int64_t max_tasks = 1;
     int* h_active = nullptr;         // pinned [2 slots][4]: active, -, predict requests
     int round = 0;                   // rounds enqueued
     int harvested = 0;               // rounds whose counts were read back
@@ -529,7 +532,9 @@ struct lf_session {
 
 namespace lf {
 
-static int session_begin(lf_session* ss) {
+// Scratch of one search session, sized once for (index, Q, opts); a search plan keeps
+// it across calls (lf_search_plan_*), lf_search / lf_search_begin allocate per call.
+static int session_alloc(lf_session* ss) {
     const lf_index& idx = ss->idx;
     const lf_search_opts& o = ss->opts;
     cudaStream_t st = ss->st;
@@ -541,6 +546,9 @@ static int session_begin(lf_session* ss) {
     s.kc = std::min(o.k, CH);
     s.f = o.bsf_factor;
     s.Rcap = o.sequential ? 1 : std::max(1, std::min(o.max_round_leaves, std::max(1, idx.n_leaves)));
+    s.seq = o.sequential ? 1 : 0;
+    s.growth = round_growth_log2();
+    s.d_round = nullptr;
     s.pred = o.d_pred;
     s.pred64 = o.d_pred_f64;
     s.offset = o.d_offset;
@@ -552,6 +560,7 @@ static int session_begin(lf_session* ss) {
 
     const int64_t max_chunks_leaf = std::max<int64_t>(1, (idx.max_leaf_rows + CH - 1) / CH);
     const int64_t max_tasks = std::max<int64_t>(1, Q * s.Rcap * max_chunks_leaf);
+    ss->max_tasks = max_tasks;
     LF_CUDA(ss->qsumm.alloc(sizeof(double) * Q * idx.n_seg * (idx.d_sd_min != nullptr ? 2 : 1), st));
     LF_CUDA(ss->lb.alloc(sizeof(double) * Q * Nn, st));        // node bounds (L2-resident at 1K x 8K)
     LF_CUDA(ss->lbs.alloc(sizeof(double) * Q * L, st));        // leaf records in visit order
@@ -577,6 +586,7 @@ static int session_begin(lf_session* ss) {
     LF_CUDA(ss->cand_i.alloc(sizeof(long long) * max_tasks * s.kc, st));
     LF_CUDA(ss->task_min.alloc(sizeof(double) * (s.want_trace ? max_tasks : 1), st));
     LF_CUDA(ss->n_active.alloc(sizeof(int) * 8, st));   // [2 slots][active, refill, predict requests, -]
+    LF_CUDA(ss->round_ctr.alloc(sizeof(int), st));
     for (int sl = 0; sl < 2; ++sl) {
         LF_CUDA(cudaEventCreateWithFlags(&ss->done_ev[sl], cudaEventDisableTiming));
         if (o.h_profile)
@@ -586,41 +596,32 @@ static int session_begin(lf_session* ss) {
     if (ss->lazy) {
         const int F = std::max(1, o.n_filters);
         LF_CUDA(ss->pcount.alloc(sizeof(int) * Q, st));
-        LF_CUDA(cudaMemsetAsync(ss->pcount.p, 0, sizeof(int) * Q, st));
         LF_CUDA(ss->pstart.alloc(sizeof(int) * Q, st));
         LF_CUDA(ss->pend.alloc(sizeof(int) * Q, st));
         LF_CUDA(ss->preq.alloc(sizeof(int) * Q, st));
-        LF_CUDA(cudaMemsetAsync(ss->preq.p, 0, sizeof(int) * Q, st));
         LF_CUDA(ss->fhist.alloc(sizeof(int) * F, st));
         LF_CUDA(ss->fcur.alloc(sizeof(int) * F, st));
         LF_CUDA(ss->ntiles.alloc(sizeof(int), st));
         LF_CUDA(ss->ptotal.alloc(sizeof(unsigned long long), st));
-        LF_CUDA(cudaMemsetAsync(ss->ptotal.p, 0, sizeof(unsigned long long), st));
         const int64_t max_pairs = Q * (int64_t)L;     // every (query, leaf) pair, worst case
         LF_CUDA(ss->pdst.alloc(sizeof(int2) * max_pairs, st));
         LF_CUDA(ss->ptiles.alloc(sizeof(int4) * (max_pairs / 128 + F + 1), st));
         LF_CUDA(ss->xh.alloc(sizeof(__half) * Q * idx.m, st));
         LF_CUDA(ss->xexp.alloc(sizeof(int) * Q, st));
-        int rc = rows_to_f16(ss->d_q, Q, idx.m, ss->xh.as<__half>(), ss->xexp.as<int>(), st);
-        if (rc) return rc;
-        ++ss->kernels;
     }
     LF_CUDA(ss->tasks.alloc(sizeof(int4) * max_tasks, st));
     LF_CUDA(ss->ea_count.alloc(sizeof(unsigned long long) * 4, st));
-    LF_CUDA(cudaMemsetAsync(ss->ea_count.p, 0, sizeof(unsigned long long) * 4, st));
-    {   // one pinned word per host thread; a round reads it right after its own sync
-        static thread_local int* pinned = nullptr;
-        if (pinned == nullptr) LF_CUDA(cudaMallocHost(&pinned, sizeof(int) * 8));
-        ss->h_active = pinned;
+    {   // one pinned word per host thread (freed with the thread); a round reads it right after its own sync
+        struct Pinned {
+            int* p = nullptr;
+            ~Pinned() {
+                if (p) cudaFreeHost(p);
+            }
+        };
+        static thread_local Pinned pinned;
+        if (pinned.p == nullptr) LF_CUDA(cudaMallocHost(&pinned.p, sizeof(int) * 8));
+        ss->h_active = pinned.p;
     }
-
-    if (o.h_profile) {
-        ss->prof = true;
-        for (int i = 0; i < LF_N_PROF; ++i) o.h_profile[i] = 0.0;
-        for (auto& e : ss->ev) LF_CUDA(cudaEventCreate(&e));
-        LF_CUDA(cudaEventRecord(ss->ev[0], st));
-    }
-    int nk = 0;
     OrderArgs& oa = ss->oa;
     oa.lbs = ss->lbs.as<double>();
     oa.gap = ss->gap.as<double>();
@@ -633,11 +634,6 @@ static int session_begin(lf_session* ss) {
     oa.offset = o.d_offset;
     oa.F = o.n_filters;
     oa.lazy = ss->lazy ? 1 : 0;
-    int rc = bounds_and_order(ss->d_q, Q, idx, ss->qsumm.as<double>(), ss->lb.as<double>(), oa, st, &nk);
-    if (rc) return rc;
-    if (ss->prof) LF_CUDA(cudaEventRecord(ss->ev[1], st));     // LF_PROF_BOUNDS_MS: means + bounds + order
-    ss->kernels += nk;
-
     s.order = oa.order;
     s.lbs = ss->lbs.as<double>();
     s.gap = ss->gap.as<double>();
@@ -667,10 +663,6 @@ static int session_begin(lf_session* ss) {
     s.n_active = ss->n_active.as<int>();
     s.tasks = ss->tasks.as<int4>();
     s.ea_count = o.h_profile ? ss->ea_count.as<unsigned long long>() : nullptr;
-
-    init_state_kernel<<<(unsigned)((Q + 127) / 128), 128, 0, st>>>(s);
-    LF_CUDA(cudaGetLastError());
-    ++ss->kernels;
     ss->q8 = idx.d_X8 != nullptr && idx.d_qmeta != nullptr && o.early_abandon && !s.want_trace &&
              (idx.m % 4) == 0 && idx.m <= 512 && (scan_variant() == 8 || scan_variant() == 9);
     ss->pq = idx.d_Xp != nullptr && idx.d_pmeta != nullptr && (idx.pca_k == 32 || idx.pca_k == 64) &&
@@ -690,20 +682,65 @@ static int session_begin(lf_session* ss) {
         LF_CUDA(ss->pq_lo8.alloc(sizeof(float) * ss->pq_cap, st));
         LF_CUDA(ss->pq_thr.alloc(sizeof(unsigned) * max_tasks, st));
         LF_CUDA(ss->pq_qbest.alloc(sizeof(unsigned) * Q, st));
+    }
+    if (ss->q8) {
+        const int MP = (idx.m + 255) / 256 * 256;
+        LF_CUDA(ss->qc8.alloc((size_t)Q * MP, st));
+        LF_CUDA(ss->qm8.alloc(sizeof(float4) * Q, st));
+    }
+    return LF_OK;
+}
+
+// Per-batch work before round 0: query summaries, bounds, visit orders, state reset,
+// query codes (stream-ordered; captured into the plan's graph).
+static int session_prologue(lf_session* ss) {
+    const lf_index& idx = ss->idx;
+    const lf_search_opts& o = ss->opts;
+    cudaStream_t st = ss->st;
+    const int64_t Q = ss->Q;
+    RoundState& s = ss->s;
+    LF_CUDA(cudaMemsetAsync(ss->ea_count.p, 0, sizeof(unsigned long long) * 4, st));
+    LF_CUDA(cudaMemsetAsync(ss->round_ctr.p, 0, sizeof(int), st));
+    if (ss->lazy) {
+        LF_CUDA(cudaMemsetAsync(ss->pcount.p, 0, sizeof(int) * Q, st));
+        LF_CUDA(cudaMemsetAsync(ss->preq.p, 0, sizeof(int) * Q, st));
+        LF_CUDA(cudaMemsetAsync(ss->ptotal.p, 0, sizeof(unsigned long long), st));
+        int rc = rows_to_f16(ss->d_q, Q, idx.m, ss->xh.as<__half>(), ss->xexp.as<int>(), st);
+        if (rc) return rc;
+        ++ss->kernels;
+    }
+    if (o.h_profile) {
+        ss->prof = true;
+        for (int i = 0; i < LF_N_PROF; ++i) o.h_profile[i] = 0.0;
+        for (auto& e : ss->ev) LF_CUDA(cudaEventCreate(&e));
+        LF_CUDA(cudaEventRecord(ss->ev[0], st));
+    }
+    int nk = 0;
+    int rc = bounds_and_order(ss->d_q, Q, idx, ss->qsumm.as<double>(), ss->lb.as<double>(), ss->oa, st, &nk);
+    if (rc) return rc;
+    if (ss->prof) LF_CUDA(cudaEventRecord(ss->ev[1], st));     // LF_PROF_BOUNDS_MS: means + bounds + order
+    ss->kernels += nk;
+    init_state_kernel<<<(unsigned)((Q + 127) / 128), 128, 0, st>>>(s);
+    LF_CUDA(cudaGetLastError());
+    ++ss->kernels;
+    if (ss->pq) {
         LF_CUDA(cudaMemsetAsync(ss->pq_qbest.p, 0x7f, sizeof(unsigned) * Q, st));   // 3.4e38: above any distance
         LF_CUDA(launch_project_queries(ss->d_q, Q, idx, ss->qcp.as<int8_t>(), ss->qmp.as<float4>(), st));
         ++ss->kernels;
     }
     if (ss->q8) {
         const int MP = (idx.m + 255) / 256 * 256;
-        LF_CUDA(ss->qc8.alloc((size_t)Q * MP, st));
-        LF_CUDA(ss->qm8.alloc(sizeof(float4) * Q, st));
         int rq = quantize_queries(ss->d_q, Q, idx.m, MP, ss->qc8.as<int8_t>(), ss->qm8.as<float4>(), st);
         if (rq) return rq;
         ++ss->kernels;
     }
     if (ss->prof) LF_CUDA(cudaEventRecord(ss->ev[2], st));
     return LF_OK;
+}
+
+static int session_begin(lf_session* ss) {
+    int rc = session_alloc(ss);
+    return rc ? rc : session_prologue(ss);
 }
 
 static float ev_ms(cudaEvent_t a, cudaEvent_t b) {
@@ -761,44 +798,31 @@ static int predict_pass(lf_session* ss, int all) {
     return LF_OK;
 }
 
-// Enqueue one round (plan, scan, merge) into count slot round & 1; the counts are
-// copied back asynchronously (done_ev).  session_harvest reads them.
-static int session_enqueue(lf_session* ss, const double* d_bound, double* d_bsf_out) {
+// The kernels of one round -- plan, chunk offsets, task expansion, scan, merge -- with
+// `counts` as the round's counters.  In a graph-launched plan (s.d_round set) the plan
+// kernel derives R from the device round counter; otherwise s.R holds it.
+static int round_kernels(lf_session* ss, int* counts, bool round0, cudaEvent_t* ev) {
     RoundState& s = ss->s;
     const lf_index& idx = ss->idx;
     const lf_search_opts& o = ss->opts;
     cudaStream_t st = ss->st;
     const int64_t Q = ss->Q;
-    const int slot = ss->round & 1;
-    int* counts = ss->n_active.as<int>() + 4 * slot;
     s.n_active = counts;
     s.n_predict = counts + 2;
-    cudaEvent_t* ev = ss->rev[slot];
-    if (ss->lazy && (ss->round == 1 || ss->predict_pending)) {
-        // after round 0 every query with a finite bsf gets its reachable pairs predicted
-        int rc = predict_pass(ss, ss->round == 1 ? 1 : 0);
-        if (rc) return rc;
-        ss->predict_pending = false;
-    }
-    s.bound = d_bound;
-    s.R = o.sequential ? 1
-                       : (int)std::min<int64_t>(s.Rcap, (int64_t)1 << std::min(ss->round * round_growth_log2(), 30));
     LF_CUDA(cudaMemsetAsync(counts, 0, sizeof(int) * 3, st));
-    if (ss->prof) cudaEventRecord(ev[0], st);
+    if (ev) cudaEventRecord(ev[0], st);
     plan_warp_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s, idx);
     offsets_kernel<<<1, 1024, 0, st>>>(s.chunk_off, Q);
     expand_tasks_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s, idx.d_leaf_ptr);
-    if (ss->prof) cudaEventRecord(ev[1], st);
+    if (ev) cudaEventRecord(ev[1], st);
     cudaError_t ce;
     // the bounded scans take m % 4 == 0 (codes zero-padded to a multiple of 64)
     const bool ea = o.early_abandon && !s.want_trace && idx.m <= 512 && scan_variant() != 0 && ss->q8;
-    const int64_t max_tasks =
-        std::max<int64_t>(1, Q * s.Rcap * std::max<int64_t>(1, (idx.max_leaf_rows + CH - 1) / CH));
     // round 0 has no best-so-far yet: for k = 1 the projected scan seeds its threshold
     // with one exactly scored row per task (scan_pq_kernel SEED); for k > 1 (or
     // LF_SCAN_ROUND0=q8) the first round runs the full-length int8 scan
-    const bool seed = ss->round == 0 && s.k == 1 && round0_seeded();
-    if (ea && ss->pq && (ss->round > 0 || !ss->q8 || seed)) {
+    const bool seed = round0 && s.k == 1 && round0_seeded();
+    if (ea && ss->pq && (!round0 || !ss->q8 || seed)) {
         const PQOverflow ov{ss->pq_oent.as<int4>(), ss->pq_on.as<int>(),
                             ss->pq_obase.as<int>(), ss->pq_cap, ss->pq_wrows.as<unsigned short>(),
                             ss->pq_wdist.as<double>(), ss->q8 ? ss->qc8.as<int8_t>() : nullptr,
@@ -806,7 +830,7 @@ static int session_enqueue(lf_session* ss, const double* d_bound, double* d_bsf_
                             ss->pq_lo8.as<float>(), ss->pq_thr.as<unsigned>(),
                             seed ? ss->pq_qbest.as<unsigned>() : nullptr};
         ce = launch_scan_pq(s, idx, ss->d_q, ss->qcp.as<int8_t>(), ss->qmp.as<float4>(), ss->pq_cnt.as<int>(), ov,
-                            max_tasks, st);
+                            ss->max_tasks, st);
         ss->kernels += ss->q8 ? 3 : 2;
     } else if (ea) {
         ce = launch_scan_q8(s, idx, ss->d_q, ss->qc8.as<int8_t>(), ss->qm8.as<float4>(), st);
@@ -815,14 +839,35 @@ static int session_enqueue(lf_session* ss, const double* d_bound, double* d_bsf_
         ce = launch_scan_full(s, idx, ss->d_q, st);
     }
     if (ce != cudaSuccess) return fail(LF_ECUDA, cudaGetErrorString(ce));
-    if (ss->prof) cudaEventRecord(ev[2], st);
+    if (ev) cudaEventRecord(ev[2], st);
     merge_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s);
     LF_CUDA(cudaGetLastError());
-    if (ss->prof) cudaEventRecord(ev[3], st);
+    if (ev) cudaEventRecord(ev[3], st);
     ss->kernels += 5;
-    std::swap(s.top_d, s.top_d_out);
-    std::swap(s.top_i, s.top_i_out);
-    std::swap(s.top_n, s.top_n_out);
+    return LF_OK;
+}
+
+// Enqueue one round into count slot round & 1; the counts are copied back
+// asynchronously (done_ev).  session_harvest reads them.
+static int session_enqueue(lf_session* ss, const double* d_bound, double* d_bsf_out) {
+    RoundState& s = ss->s;
+    const lf_search_opts& o = ss->opts;
+    cudaStream_t st = ss->st;
+    const int64_t Q = ss->Q;
+    const int slot = ss->round & 1;
+    int* counts = ss->n_active.as<int>() + 4 * slot;
+    if (ss->lazy && (ss->round == 1 || (ss->round > 1 && s.k > 1))) {
+        // after round 0 every query with a finite bsf gets its reachable pairs predicted;
+        // with k > 1 a walk whose bsf was still +inf then asks later (preq), and every
+        // round starts with a pass over those requests (the same schedule as the graph)
+        int rc = predict_pass(ss, ss->round == 1 ? 1 : 0);
+        if (rc) return rc;
+    }
+    s.bound = d_bound;
+    s.R = o.sequential ? 1
+                       : (int)std::min<int64_t>(s.Rcap, (int64_t)1 << std::min(ss->round * s.growth, 30));
+    int rc = round_kernels(ss, counts, ss->round == 0, ss->prof ? ss->rev[slot] : nullptr);
+    if (rc) return rc;
     if (d_bsf_out) {
         bsf_out_kernel<<<(unsigned)((Q + 255) / 256), 256, 0, st>>>(s, d_bsf_out);
         LF_CUDA(cudaGetLastError());
@@ -846,7 +891,6 @@ static int session_harvest(lf_session* ss, int* active_out) {
     const int slot = r & 1;
     int* h = ss->h_active + 4 * slot;
     LF_CUDA(cudaEventSynchronize(ss->done_ev[slot]));
-    if (ss->lazy && r >= 1 && h[0] > 0 && h[2] > 0) ss->predict_pending = true;   // walks stopped at pcount
     if (ss->prof) {
         double* p = o.h_profile;
         cudaEvent_t* ev = ss->rev[slot];
@@ -933,9 +977,182 @@ static int check_args(const lf_index* idx, int64_t Q, const lf_search_opts* opts
     return LF_OK;
 }
 
+// ------------------------------------------------------------ search plans ----
+// A plan owns one session's scratch for (index, Q, opts) and the whole batched
+// search as ONE CUDA graph: prologue (bounds, visit orders, query codes), round 0,
+// the in-search prediction pass, then a conditional WHILE node whose body is one
+// round followed by round_cond_kernel, which advances the device round counter and
+// keeps the loop going while any walk is active.  A search is then a query copy,
+// one graph launch and the result copies: no host round trips, no per-call
+// allocations, tensor-map encodes or launch latency between rounds.
+__global__ void round_cond_kernel(const int* __restrict__ counts, int* __restrict__ d_round, int max_rounds,
+                                  cudaGraphConditionalHandle h) {
+    const int r = *d_round + 1;
+    *d_round = r;
+    cudaGraphSetConditional(h, (counts[0] > 0 && r < max_rounds) ? 1u : 0u);
+}
+
+static int plan_capture(lf_session* ss, cudaStream_t cs, cudaStream_t cs2, int64_t* d_ids, double* d_dists,
+                        cudaGraph_t* out) {
+    RoundState& s = ss->s;
+    const int64_t Q = ss->Q;
+    int* counts = ss->n_active.as<int>();
+    const int max_rounds = 2 * std::max(1, ss->idx.n_leaves) + 8;
+    ss->st = cs;
+    LF_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+    int rc = session_prologue(ss);
+    if (!rc) rc = round_kernels(ss, counts, true, nullptr);
+    if (!rc && ss->lazy) rc = predict_pass(ss, 1);
+    cudaGraph_t g = nullptr;
+    cudaGraphConditionalHandle h;
+    cudaGraphNode_t cnode = nullptr;
+    if (!rc) {
+        cudaStreamCaptureStatus cst;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        cudaError_t e = cudaStreamGetCaptureInfo(cs, &cst, nullptr, &g, &deps, &nd);
+        if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&h, g, 0, 0);
+        if (e == cudaSuccess) {
+            round_cond_kernel<<<1, 1, 0, cs>>>(counts, ss->round_ctr.as<int>(), max_rounds, h);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaStreamGetCaptureInfo(cs, &cst, nullptr, &g, &deps, &nd);
+        cudaGraphNodeParams cp = {};
+        if (e == cudaSuccess) {
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = h;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            e = cudaGraphAddNode(&cnode, g, deps, nd, &cp);
+        }
+        if (e == cudaSuccess) e = cudaStreamBeginCaptureToGraph(cs2, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                                cudaStreamCaptureModeRelaxed);
+        if (e != cudaSuccess) rc = fail(LF_ECUDA, std::string("conditional graph node: ") + cudaGetErrorString(e));
+        if (!rc) {
+            ss->st = cs2;
+            if (ss->lazy && s.k > 1) rc = predict_pass(ss, 0);   // walks whose bsf was +inf after round 0
+            if (!rc) rc = round_kernels(ss, counts, false, nullptr);
+            if (!rc) {
+                round_cond_kernel<<<1, 1, 0, cs2>>>(counts, ss->round_ctr.as<int>(), max_rounds, h);
+                if (cudaGetLastError() != cudaSuccess) rc = fail(LF_ECUDA, "round_cond_kernel launch");
+            }
+            cudaGraph_t body = nullptr;
+            const cudaError_t e2 = cudaStreamEndCapture(cs2, &body);
+            if (!rc && e2 != cudaSuccess) rc = fail(LF_ECUDA, std::string("body capture: ") + cudaGetErrorString(e2));
+            ss->st = cs;
+        }
+        if (!rc) {
+            const cudaError_t e3 = cudaStreamUpdateCaptureDependencies(cs, &cnode, 1, cudaStreamSetCaptureDependencies);
+            if (e3 != cudaSuccess) rc = fail(LF_ECUDA, std::string("capture dependencies: ") + cudaGetErrorString(e3));
+        }
+        if (!rc) {
+            finish_kernel<<<(unsigned)((Q * s.k + 255) / 256), 256, 0, cs>>>(s, d_ids, d_dists);
+            if (cudaGetLastError() != cudaSuccess) rc = fail(LF_ECUDA, "finish_kernel launch");
+        }
+    }
+    cudaGraph_t full = nullptr;
+    const cudaError_t ee = cudaStreamEndCapture(cs, &full);
+    if (!rc && ee != cudaSuccess) rc = fail(LF_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ee));
+    if (rc) {
+        if (full) cudaGraphDestroy(full);
+        return rc;
+    }
+    *out = full;
+    return LF_OK;
+}
+
 }  // namespace lf
 
+struct lf_search_plan {
+    lf_session* ss = nullptr;
+    lf::Scratch qbuf, ids, dists, stats;
+    cudaStream_t cs = nullptr, cs2 = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int64_t Q = 0;
+    int m = 0, k = 0;
+};
+
+static void plan_free(lf_search_plan* p) {
+    if (!p) return;
+    if (p->exec) cudaGraphExecDestroy(p->exec);
+    if (p->graph) cudaGraphDestroy(p->graph);
+    if (p->cs) cudaStreamSynchronize(p->cs);
+    if (p->ss) lf::session_free(p->ss);              // its scratch is freed on p->cs
+    for (lf::Scratch* b : {&p->qbuf, &p->ids, &p->dists, &p->stats})
+        if (b->p) {
+            cudaFreeAsync(b->p, b->s);
+            b->p = nullptr;
+        }
+    if (p->cs) cudaStreamSynchronize(p->cs);
+    if (p->cs) cudaStreamDestroy(p->cs);
+    if (p->cs2) cudaStreamDestroy(p->cs2);
+    delete p;
+}
+
 extern "C" {
+
+lf_search_plan* lf_search_plan_create(const lf_index* idx, int64_t Q, const lf_search_opts* opts, void* stream) {
+    if (lf::check_args(idx, Q, opts) != LF_OK) return nullptr;
+    if (Q < 1) { lf::fail(LF_EINVAL, "empty query batch"); return nullptr; }
+    if (opts->want_trace || opts->h_profile) {
+        lf::fail(LF_EINVAL, "search plans do not trace or profile: use lf_search");
+        return nullptr;
+    }
+    auto* p = new lf_search_plan();
+    p->Q = Q;
+    p->m = idx->m;
+    p->k = opts->k;
+    cudaStream_t st = lf::as_stream(stream);
+    auto bail = [&](const char* what, cudaError_t e) -> lf_search_plan* {
+        if (e != cudaSuccess) lf::fail(LF_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+        plan_free(p);
+        return nullptr;
+    };
+    cudaError_t e = cudaStreamCreateWithFlags(&p->cs, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->cs2, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return bail("plan streams", e);
+    if ((e = p->qbuf.alloc(sizeof(float) * Q * idx->m, p->cs)) != cudaSuccess ||
+        (e = p->ids.alloc(sizeof(int64_t) * Q * opts->k, p->cs)) != cudaSuccess ||
+        (e = p->dists.alloc(sizeof(double) * Q * opts->k, p->cs)) != cudaSuccess ||
+        (e = p->stats.alloc(sizeof(int64_t) * Q * LF_N_STATS, p->cs)) != cudaSuccess)
+        return bail("plan buffers", e);
+    auto* ss = new lf_session();
+    p->ss = ss;
+    ss->idx = *idx;
+    ss->opts = *opts;
+    ss->opts.want_trace = 0;
+    ss->st = p->cs;
+    ss->Q = Q;
+    ss->d_q = p->qbuf.as<float>();
+    ss->s.stats = p->stats.as<long long>();
+    if (lf::session_alloc(ss) != LF_OK) return bail("", cudaSuccess);
+    ss->s.d_round = ss->round_ctr.as<int>();
+    if ((e = cudaStreamSynchronize(p->cs)) != cudaSuccess) return bail("plan allocation", e);
+    (void)st;
+    if (lf::plan_capture(ss, p->cs, p->cs2, p->ids.as<int64_t>(), p->dists.as<double>(), &p->graph) != LF_OK)
+        return bail("", cudaSuccess);
+    if ((e = cudaGraphInstantiate(&p->exec, p->graph, 0)) != cudaSuccess) return bail("graph instantiate", e);
+    return p;
+}
+
+int lf_search_plan_run(lf_search_plan* p, const float* d_queries, int64_t* d_out_ids, double* d_out_dists,
+                       int64_t* d_out_stats, void* stream) {
+    LF_REQUIRE(p != nullptr && d_queries != nullptr, "NULL argument");
+    cudaStream_t st = lf::as_stream(stream);
+    LF_CUDA(cudaMemcpyAsync(p->qbuf.p, d_queries, sizeof(float) * p->Q * p->m, cudaMemcpyDeviceToDevice, st));
+    LF_CUDA(cudaGraphLaunch(p->exec, st));
+    if (d_out_ids)
+        LF_CUDA(cudaMemcpyAsync(d_out_ids, p->ids.p, sizeof(int64_t) * p->Q * p->k, cudaMemcpyDeviceToDevice, st));
+    if (d_out_dists)
+        LF_CUDA(cudaMemcpyAsync(d_out_dists, p->dists.p, sizeof(double) * p->Q * p->k, cudaMemcpyDeviceToDevice, st));
+    if (d_out_stats)
+        LF_CUDA(cudaMemcpyAsync(d_out_stats, p->stats.p, sizeof(int64_t) * p->Q * LF_N_STATS,
+                                cudaMemcpyDeviceToDevice, st));
+    return LF_OK;
+}
+
+void lf_search_plan_free(lf_search_plan* p) { plan_free(p); }
 
 lf_session* lf_search_begin(const lf_index* idx, const float* d_queries, int64_t Q,
                             const lf_search_opts* opts, const lf_trace* trace, int64_t* d_stats,

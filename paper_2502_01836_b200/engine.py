@@ -149,29 +149,14 @@ def _queries_device(queries, m: int, dev):
     return q.contiguous()
 
 
-def search_batch(index, queries, k: int = 1, *, bsf_factor: float = 1.0, predictions=None,
-                 offsets=None, leaf_filter=None, sequential: bool = False,
-                 max_round_leaves: int = 256, want_trace: bool = False, stream=None,
-                 copy_out: bool = True, profile: np.ndarray | None = None, early_abandon: bool = True,
-                 filters=None):
-    """Search a batch of queries in one lf_search call.
-
-    predictions: device fp32 [Q, F] filter outputs (FilterPack.predict), with
-    offsets [F] (fp64) and leaf_filter int32 [n_leaves] (filter slot per leaf
-    slot, -1 for unfiltered leaves).
-    filters: an fp16 tensor-core FilterPack (path "tc16") INSTEAD of predictions
-    (in-search inference: one pass right after round 0 predicts only the (query, leaf)
-    pairs the walk can still reach, with the dense kernel's arithmetic, so results and
-    counters equal the predictions path bit for bit).
-    """
+def _search_options(t, di, Q: int, k: int, *, bsf_factor: float = 1.0, predictions=None, offsets=None,
+                    leaf_filter=None, sequential: bool = False, max_round_leaves: int = 256,
+                    want_trace: bool = False, profile=None, early_abandon: bool = True, filters=None):
+    """lf_search_opts + lf_index of one batched search, and the tensors they point into."""
     torch = _lib.require_cuda()
-    t = as_tree(index)
-    di = index if isinstance(index, DeviceIndex) else t.device()
     dev = di.device
     if not 1 <= k <= t.n:
         raise ValueError(f"k must be in [1, {t.n}], got {k}")
-    q = _queries_device(queries, t.m, dev)
-    Q = q.shape[0]
     opts = _lib.LfSearchOpts()
     opts.k = int(k)
     opts.bsf_factor = float(bsf_factor)
@@ -196,7 +181,7 @@ def search_batch(index, queries, k: int = 1, *, bsf_factor: float = 1.0, predict
         lf = leaf_filter.to(device=dev, dtype=torch.int32).contiguous()
         if off.shape[0] != filters.n_filters or lf.shape != (di.n_leaves,):
             raise ValueError("filter / offset / leaf map shapes do not agree")
-        keep += [off, lf]
+        keep += [off, lf, filters]
         opts.d_W1T_h, opts.d_wexp = filters.W1T_h.data_ptr(), filters.wexp.data_ptr()
         opts.d_b1 = filters.b1.data_ptr()
         opts.d_W2, opts.d_b2 = filters.W2.data_ptr(), filters.b2.data_ptr()
@@ -221,6 +206,81 @@ def search_batch(index, queries, k: int = 1, *, bsf_factor: float = 1.0, predict
         ist = di.struct(lf)
     else:
         ist = di.struct(None)
+    return opts, ist, keep
+
+
+class SearchPlan:
+    """A batched search captured once as a CUDA graph (lf_search_plan_*) for a fixed
+    index, batch size Q, k and filter set; `run` launches it for a new query batch.
+    Results and counters equal search_batch's with the same arguments.  Predictions
+    passed here are fixed for the plan's life (use `filters` -- the fp16 pack, predicted
+    inside the search -- for per-batch filtering)."""
+
+    def __init__(self, index, Q: int, k: int = 1, *, stream=None, **kw):
+        torch = _lib.require_cuda()
+        t = as_tree(index)
+        self.di = index if isinstance(index, DeviceIndex) else t.device()
+        self.tree, self.Q, self.k = t, int(Q), int(k)
+        opts, ist, self._keep = _search_options(t, self.di, self.Q, self.k, **kw)
+        self._opts, self._ist = opts, ist
+        self._h = None
+        with torch.cuda.device(self.di.device):
+            h = _lib.lib().lf_search_plan_create(ist, self.Q, opts, _lib.stream_ptr(stream))
+        if not h:
+            _lib.check(_lib.LF_ECUDA)
+        self._h = h
+
+    def run(self, queries, stream=None, copy_out: bool = True):
+        torch = _lib.require_cuda()
+        q = _queries_device(queries, self.tree.m, self.di.device)
+        if q.shape[0] != self.Q:
+            raise ValueError(f"plan was built for {self.Q} queries, got {q.shape[0]}")
+        dev = self.di.device
+        ids = torch.empty((self.Q, self.k), dtype=torch.int64, device=dev)
+        dists = torch.empty((self.Q, self.k), dtype=torch.float64, device=dev)
+        stats = torch.empty((self.Q, _lib.N_STATS), dtype=torch.int64, device=dev)
+        with torch.cuda.device(dev):
+            _lib.check(_lib.lib().lf_search_plan_run(self._h, q.data_ptr(), ids.data_ptr(), dists.data_ptr(),
+                                                     stats.data_ptr(), _lib.stream_ptr(stream)))
+        if not copy_out:
+            return ids, dists, stats
+        return BatchResult(self.tree.n, ids.cpu().numpy(), dists.cpu().numpy(), stats.cpu().numpy())
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            try:
+                _lib.lib().lf_search_plan_free(h)
+            except Exception:
+                pass
+
+
+
+def search_batch(index, queries, k: int = 1, *, bsf_factor: float = 1.0, predictions=None,
+                 offsets=None, leaf_filter=None, sequential: bool = False,
+                 max_round_leaves: int = 256, want_trace: bool = False, stream=None,
+                 copy_out: bool = True, profile: np.ndarray | None = None, early_abandon: bool = True,
+                 filters=None):
+    """Search a batch of queries in one lf_search call.
+
+    predictions: device fp32 [Q, F] filter outputs (FilterPack.predict), with
+    offsets [F] (fp64) and leaf_filter int32 [n_leaves] (filter slot per leaf
+    slot, -1 for unfiltered leaves).
+    filters: an fp16 tensor-core FilterPack (path "tc16") INSTEAD of predictions
+    (in-search inference: one pass right after round 0 predicts only the (query, leaf)
+    pairs the walk can still reach, with the dense kernel's arithmetic, so results and
+    counters equal the predictions path bit for bit).
+    """
+    torch = _lib.require_cuda()
+    t = as_tree(index)
+    di = index if isinstance(index, DeviceIndex) else t.device()
+    dev = di.device
+    q = _queries_device(queries, t.m, dev)
+    Q = q.shape[0]
+    opts, ist, keep = _search_options(t, di, Q, k, bsf_factor=bsf_factor, predictions=predictions,
+                                      offsets=offsets, leaf_filter=leaf_filter, sequential=sequential,
+                                      max_round_leaves=max_round_leaves, want_trace=want_trace,
+                                      profile=profile, early_abandon=early_abandon, filters=filters)
     ids = torch.empty((Q, k), dtype=torch.int64, device=dev)
     dists = torch.empty((Q, k), dtype=torch.float64, device=dev)
     stats = torch.empty((Q, _lib.N_STATS), dtype=torch.int64, device=dev)

@@ -239,13 +239,17 @@ def _as_enhanced(eidx) -> EnhancedIndex:
 
 def search_queries(eidx, queries, k: int = 1, *, target: float | None = None, exact: bool = False,
                    sequential: bool = False, max_round_leaves: int = 256, want_trace: bool = False,
-                   stream=None, copy_out: bool = True, profile=None, lazy: bool | None = None):
+                   stream=None, copy_out: bool = True, profile=None, lazy: bool | None = None,
+                   graph: bool = True):
     """Batched LeaFi search in one lf_search call.  lazy=True (default for the fp16
     pack, path "tc16"): the filters are evaluated inside the search, in one tensor-core
     pass right after round 0, only for the (query, leaf) pairs the walk can still reach
     (lb <= bsf0 * f; 0.42M of the 4.1M pairs on the bench workload).  lazy=False: one
     lf_filter_predict over every (query, filter) pair first.  Both give identical
-    results and counters (same kernel arithmetic)."""
+    results and counters (same kernel arithmetic).  graph=True (default; in-search
+    inference, no trace / profile): the search runs as a cached CUDA-graph plan
+    (engine.SearchPlan, one per (batch size, k, target, schedule)) -- same results,
+    no per-call host work beyond one graph launch."""
     e = _as_enhanced(eidx)
     if exact or not e.filters:
         return search_batch(e.base, queries, k, sequential=sequential, max_round_leaves=max_round_leaves,
@@ -262,6 +266,18 @@ def search_queries(eidx, queries, k: int = 1, *, target: float | None = None, ex
         lazy = pk.path == "tc16"
     if lazy and pk.path != "tc16":
         raise ValueError("in-search filter inference runs on the fp16 pack (FilterPack path 'tc16')")
+    if lazy and graph and profile is None and not want_trace:
+        plans = e.__dict__.setdefault("_plans", {})
+        key = (int(q.shape[0]), int(k), float(target), bool(sequential), int(max_round_leaves), str(di.device))
+        plan = plans.get(key)
+        if plan is None:
+            from .engine import SearchPlan
+
+            plan = SearchPlan(e.base, q.shape[0], k, filters=pk, offsets=e.offset_vector(target, device=True),
+                              leaf_filter=pk.leaf_filter(di), sequential=sequential,
+                              max_round_leaves=max_round_leaves, stream=stream)
+            plans[key] = plan
+        return plan.run(q, stream=stream, copy_out=copy_out)
     if lazy:
         return search_batch(e.base, q.contiguous(), k, filters=pk, offsets=e.offset_vector(target, device=True),
                             leaf_filter=pk.leaf_filter(di), sequential=sequential,
