@@ -396,7 +396,10 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
         c_rows += (unsigned long long)nrows;
         c_surv += (unsigned long long)ns;
         if (ns == 0) {
-            if (lane == 0) surv_cnt[t] = 0;
+            if (lane == 0) {
+                surv_cnt[t] = 0;
+                if (ov.xd != nullptr) { s.cand_d[t] = kInf; s.cand_i[t] = LLONG_MAX; }   // k = 1 entry tail
+            }
             continue;
         }
         // survivors -> (task, query, row) entries for the int8 stage (pq_q8_bound_kernel)
@@ -425,6 +428,7 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
                 surv_cnt[t] = ns;
                 ov.base[t] = base;
                 ov.thr[t] = __float_as_uint(thr_f);
+                if (ov.xd != nullptr) { s.cand_d[t] = kInf; s.cand_i[t] = LLONG_MAX; }   // k = 1 entry tail
             }
             continue;
         }
@@ -606,6 +610,86 @@ __global__ void __launch_bounds__(PQT_WARPS * 32) pq_tail_kernel(RoundState s, l
     }
 }
 
+// k = 1 tail, ENTRY-parallel (no per-task chain of dependent loads): every entry whose
+// int8 lower bound reaches its task's final threshold is re-read exactly (8 lanes per
+// row, all loads in flight) and min'ed into the task's candidate distance (the bits of
+// non-negative doubles order like the values); a second pass gives each task the
+// smallest row id among its entries at that distance (tree.py:207-214 tie rule).
+__global__ void __launch_bounds__(256) pq_tail_e1_kernel(RoundState s, lf_index idx, const float* __restrict__ queries,
+                                                        PQOverflow ov) {
+    const int lane = threadIdx.x & 31, sl = lane & 7;
+    const long long n = min((long long)*ov.n, (long long)ov.cap);
+    const long long ng = ((long long)gridDim.x * blockDim.x) >> 3;
+    const int m = idx.m;
+    unsigned long long cnt = 0;
+    for (long long e = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3; e < n + ((32 - (n & 31)) & 31);
+         e += ng) {
+        int4 en = e < n ? ov.ent[e] : make_int4(-1, 0, 0, 0);
+        bool go = en.x >= 0 && ov.lo8[e] <= __uint_as_float(ov.thr[en.x]);
+        double acc = 0.0;
+        if (go) {
+            const float4* xr = reinterpret_cast<const float4*>(idx.d_X + ent_row(en) * m);
+            const float4* qr = reinterpret_cast<const float4*>(queries + (int64_t)en.y * m);
+            float4 xv[8], qv[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int c = sl + 8 * i;
+                const bool v = c * 4 < m;
+                xv[i] = v ? __ldcs(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                qv[i] = v ? __ldg(qr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            for (int c0 = 64 * 4; c0 < m; c0 += 32 * 4) {           // m > 256
+                const int c = c0 / 4 + sl;
+                for (int cc = c; cc < c0 / 4 + 32 && cc * 4 < m; cc += 8) {
+                    const float4 x = __ldcs(xr + cc), q = __ldg(qr + cc);
+                    const double d0 = (double)x.x - q.x, d1 = (double)x.y - q.y, d2 = (double)x.z - q.z,
+                                 d3 = (double)x.w - q.w;
+                    acc = __fma_rn(d0, d0, acc); acc = __fma_rn(d1, d1, acc);
+                    acc = __fma_rn(d2, d2, acc); acc = __fma_rn(d3, d3, acc);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const double d0 = (double)xv[i].x - qv[i].x, d1 = (double)xv[i].y - qv[i].y;
+                const double d2 = (double)xv[i].z - qv[i].z, d3 = (double)xv[i].w - qv[i].w;
+                acc = __fma_rn(d0, d0, acc); acc = __fma_rn(d1, d1, acc);
+                acc = __fma_rn(d2, d2, acc); acc = __fma_rn(d3, d3, acc);
+            }
+        }
+        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        if (sl == 0 && e < n) {
+            const double d = go ? sqrt(acc) : -1.0;
+            ov.xd[e] = d;
+            if (go) {
+                atomicMin(reinterpret_cast<unsigned long long*>(s.cand_d) + en.x,
+                          (unsigned long long)__double_as_longlong(d));
+                ++cnt;
+            }
+        }
+    }
+    if (s.ea_count != nullptr) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (lane == 0 && cnt > 0) {
+            atomicAdd(&s.ea_count[1], cnt);
+            atomicAdd(&s.ea_count[3], cnt * (unsigned long long)m * 4ull);
+        }
+    }
+}
+
+__global__ void pq_tail_e2_kernel(RoundState s, lf_index idx, PQOverflow ov) {
+    const long long n = min((long long)*ov.n, (long long)ov.cap);
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        const double d = ov.xd[e];
+        if (!(d >= 0.0)) continue;
+        const int4 en = ov.ent[e];
+        if (d == s.cand_d[en.x]) atomicMin(reinterpret_cast<unsigned long long*>(s.cand_i) + en.x,
+                                           (unsigned long long)idx.d_row_id[ent_row(en)]);
+    }
+}
+
 cudaError_t launch_project_queries(const float* q, int64_t Q, const lf_index& idx, int8_t* qc, float4* qm,
                                    cudaStream_t st) {
     project_queries_kernel<<<(unsigned)Q, PJ_WARPS * 32, 0, st>>>(q, Q, idx.m, idx.pca_k, idx.pca_k, idx.d_P,
@@ -641,6 +725,13 @@ cudaError_t launch_scan_pq(const RoundState& s, const lf_index& idx, const float
         pq_q8_bound_kernel<<<sm_count() * 8, 256, 0, st>>>(s, idx, ov);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
+    }
+    if (ov.xd != nullptr) {                          // k = 1: entry-parallel tail
+        pq_tail_e1_kernel<<<sm_count() * 8, 256, 0, st>>>(s, idx, q, ov);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        pq_tail_e2_kernel<<<sm_count() * 4, 256, 0, st>>>(s, idx, ov);
+        return cudaGetLastError();
     }
     const long long warps = std::min<long long>(max_tasks, (long long)sm_count() * 64);
     pq_tail_kernel<<<(unsigned)((warps + PQT_WARPS - 1) / PQT_WARPS), PQT_WARPS * 32, 0, st>>>(s, idx, q, surv_cnt, ov);

@@ -413,6 +413,35 @@ __global__ void merge_kernel(RoundState s) {
         }
     }
 
+    if (s.k == 1) {                            // one pass, four candidates' loads in flight per lane
+        double bd = tn > 0 ? td[0] : kInf;
+        long long bi = tn > 0 ? ti[0] : LLONG_MAX;
+        for (long long i0 = lane; i0 < nc; i0 += 128) {
+            double dv[4];
+            long long iv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const long long i = i0 + 32 * u;
+                iv[u] = i < nc ? ci[i] : -1;
+                dv[u] = i < nc ? cd[i] : kInf;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (iv[u] >= 0 && pair_less(dv[u], iv[u], bd, bi)) { bd = dv[u]; bi = iv[u]; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double xd = __shfl_xor_sync(0xffffffffu, bd, o);
+            const long long xi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (pair_less(xd, xi, bd, bi)) { bd = xd; bi = xi; }
+        }
+        if (lane == 0 && bi != LLONG_MAX) {
+            s.top_d[q] = bd;
+            s.top_i[q] = bi;
+            s.top_n[q] = 1;
+        }
+        return;
+    }
     double last_d = -1.0;
     long long last_i = -1;
     int filled = 0;
@@ -517,7 +546,7 @@ struct lf_session {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pev;   // profiling: per prediction pass
     bool q8 = false;                 // int8-bounded scan (query codes quantised once in begin)
     bool pq = false;                 // two-stage scan over the projected shadow (d_Xp)
-    lf::Scratch qcp, qmp, pq_cnt, pq_trows, pq_oent, pq_on, pq_obase, pq_wrows, pq_wdist, pq_lo8, pq_thr, pq_qbest;
+    lf::Scratch qcp, qmp, pq_cnt, pq_trows, pq_oent, pq_on, pq_obase, pq_wrows, pq_wdist, pq_lo8, pq_thr, pq_qbest, pq_xd;
     int pq_cap = lf::PQ_OVER_CAP;    // survivor entry capacity (LF_PQ_OVER_CAP: tests of the full-list path)
     int64_t max_tasks = 1;
     int* h_active = nullptr;         // pinned [2 slots][4]: active, -, predict requests
@@ -682,6 +711,7 @@ static int session_alloc(lf_session* ss) {
         LF_CUDA(ss->pq_lo8.alloc(sizeof(float) * ss->pq_cap, st));
         LF_CUDA(ss->pq_thr.alloc(sizeof(unsigned) * max_tasks, st));
         LF_CUDA(ss->pq_qbest.alloc(sizeof(unsigned) * Q, st));
+        if (s.k == 1 && ss->q8) LF_CUDA(ss->pq_xd.alloc(sizeof(double) * ss->pq_cap, st));
     }
     if (ss->q8) {
         const int MP = (idx.m + 255) / 256 * 256;
@@ -828,7 +858,8 @@ static int round_kernels(lf_session* ss, int* counts, bool round0, cudaEvent_t* 
                             ss->pq_wdist.as<double>(), ss->q8 ? ss->qc8.as<int8_t>() : nullptr,
                             ss->q8 ? ss->qm8.as<float4>() : nullptr, (idx.m + 255) / 256 * 256,
                             ss->pq_lo8.as<float>(), ss->pq_thr.as<unsigned>(),
-                            seed ? ss->pq_qbest.as<unsigned>() : nullptr};
+                            seed ? ss->pq_qbest.as<unsigned>() : nullptr,
+                            s.k == 1 && ss->q8 ? ss->pq_xd.as<double>() : nullptr};
         ce = launch_scan_pq(s, idx, ss->d_q, ss->qcp.as<int8_t>(), ss->qmp.as<float4>(), ss->pq_cnt.as<int>(), ov,
                             ss->max_tasks, st);
         ss->kernels += ss->q8 ? 3 : 2;
