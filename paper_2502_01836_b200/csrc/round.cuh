@@ -167,7 +167,9 @@ struct PQOverflow {
     // codes rank nearest and prunes with that distance; qbest [Q] shares the best seed of
     // a query's tasks (float bits, atomicMin).  nullptr: no seeding.
     unsigned* qbest;
-    double* xd;                               // [cap] k = 1 entry tail: exact distance of an entry (-1: none)
+    double* xd;                               // k = 1 entry tail: exact distances of the listed entries
+    int* xlist;                               // [cap] entries re-read exactly (k = 1 entry tail)
+    int* xn;                                  // their count
 };
 int pq_scan_warps();                          // warps of one scan_pq_kernel launch
 constexpr int PQ_OVER_CAP = 8 << 20;          // 8M entries (128 MB + lo8)

@@ -610,83 +610,84 @@ __global__ void __launch_bounds__(PQT_WARPS * 32) pq_tail_kernel(RoundState s, l
     }
 }
 
-// k = 1 tail, ENTRY-parallel (no per-task chain of dependent loads): every entry whose
-// int8 lower bound reaches its task's final threshold is re-read exactly (8 lanes per
-// row, all loads in flight) and min'ed into the task's candidate distance (the bits of
-// non-negative doubles order like the values); a second pass gives each task the
-// smallest row id among its entries at that distance (tree.py:207-214 tie rule).
+// k = 1 tail, ENTRY-parallel (no per-task chain of dependent loads):
+//   e0: thread per entry -- the entries whose int8 lower bound reaches their task's
+//       final threshold (~3% of them) are compacted into a list;
+//   e1: 8 lanes per listed entry re-read the row exactly (all loads in flight) and
+//       min it into the task's candidate distance (the bits of non-negative doubles
+//       order like the values);
+//   e2: each task gets the smallest row id among its entries at that distance
+//       (tree.py:207-214 tie rule).
+__global__ void pq_tail_e0_kernel(PQOverflow ov) {
+    const long long n = min((long long)*ov.n, (long long)ov.cap);
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        const int t = ov.ent[e].x;
+        const bool go = t >= 0 && ov.lo8[e] <= __uint_as_float(ov.thr[t]);
+        const unsigned bal = __ballot_sync(__activemask(), go);
+        if (bal == 0) continue;
+        const int lane = threadIdx.x & 31;
+        const int leader = __ffs(bal) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(ov.xn, __popc(bal));
+        base = __shfl_sync(__activemask(), base, leader);
+        if (go) ov.xlist[base + __popc(bal & ((1u << lane) - 1u))] = (int)e;
+    }
+}
+
 __global__ void __launch_bounds__(256) pq_tail_e1_kernel(RoundState s, lf_index idx, const float* __restrict__ queries,
                                                         PQOverflow ov) {
     const int lane = threadIdx.x & 31, sl = lane & 7;
-    const long long n = min((long long)*ov.n, (long long)ov.cap);
+    const int n = *ov.xn;
     const long long ng = ((long long)gridDim.x * blockDim.x) >> 3;
     const int m = idx.m;
-    unsigned long long cnt = 0;
-    for (long long e = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3; e < n + ((32 - (n & 31)) & 31);
-         e += ng) {
-        int4 en = e < n ? ov.ent[e] : make_int4(-1, 0, 0, 0);
-        bool go = en.x >= 0 && ov.lo8[e] <= __uint_as_float(ov.thr[en.x]);
+    const long long bound = ((long long)n + 3) & ~3ll;      // warp-uniform trip count (4 entries per warp)
+    for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3; i < bound; i += ng) {
+        const bool go = i < n;
+        const int e = go ? ov.xlist[i] : 0;
+        const int4 en = go ? ov.ent[e] : make_int4(0, 0, 0, 0);
         double acc = 0.0;
         if (go) {
             const float4* xr = reinterpret_cast<const float4*>(idx.d_X + ent_row(en) * m);
             const float4* qr = reinterpret_cast<const float4*>(queries + (int64_t)en.y * m);
-            float4 xv[8], qv[8];
+            for (int c0 = 0; c0 < m / 4; c0 += 64) {               // 8 float4 per lane in flight
+                float4 xv[8], qv[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int c = sl + 8 * i;
-                const bool v = c * 4 < m;
-                xv[i] = v ? __ldcs(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-                qv[i] = v ? __ldg(qr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            for (int c0 = 64 * 4; c0 < m; c0 += 32 * 4) {           // m > 256
-                const int c = c0 / 4 + sl;
-                for (int cc = c; cc < c0 / 4 + 32 && cc * 4 < m; cc += 8) {
-                    const float4 x = __ldcs(xr + cc), q = __ldg(qr + cc);
-                    const double d0 = (double)x.x - q.x, d1 = (double)x.y - q.y, d2 = (double)x.z - q.z,
-                                 d3 = (double)x.w - q.w;
+                for (int u = 0; u < 8; ++u) {
+                    const int c = c0 + sl + 8 * u;
+                    const bool v = c < m / 4;
+                    xv[u] = v ? __ldcs(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    qv[u] = v ? __ldg(qr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const double d0 = (double)xv[u].x - qv[u].x, d1 = (double)xv[u].y - qv[u].y;
+                    const double d2 = (double)xv[u].z - qv[u].z, d3 = (double)xv[u].w - qv[u].w;
                     acc = __fma_rn(d0, d0, acc); acc = __fma_rn(d1, d1, acc);
                     acc = __fma_rn(d2, d2, acc); acc = __fma_rn(d3, d3, acc);
                 }
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const double d0 = (double)xv[i].x - qv[i].x, d1 = (double)xv[i].y - qv[i].y;
-                const double d2 = (double)xv[i].z - qv[i].z, d3 = (double)xv[i].w - qv[i].w;
-                acc = __fma_rn(d0, d0, acc); acc = __fma_rn(d1, d1, acc);
-                acc = __fma_rn(d2, d2, acc); acc = __fma_rn(d3, d3, acc);
             }
         }
         acc += __shfl_xor_sync(0xffffffffu, acc, 4);
         acc += __shfl_xor_sync(0xffffffffu, acc, 2);
         acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        if (sl == 0 && e < n) {
-            const double d = go ? sqrt(acc) : -1.0;
-            ov.xd[e] = d;
-            if (go) {
-                atomicMin(reinterpret_cast<unsigned long long*>(s.cand_d) + en.x,
-                          (unsigned long long)__double_as_longlong(d));
-                ++cnt;
-            }
+        if (go && sl == 0) {
+            const double d = sqrt(acc);
+            ov.xd[i] = d;
+            atomicMin(reinterpret_cast<unsigned long long*>(s.cand_d) + en.x, (unsigned long long)__double_as_longlong(d));
         }
     }
-    if (s.ea_count != nullptr) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        if (lane == 0 && cnt > 0) {
-            atomicAdd(&s.ea_count[1], cnt);
-            atomicAdd(&s.ea_count[3], cnt * (unsigned long long)m * 4ull);
-        }
+    if (s.ea_count != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && n > 0) {
+        atomicAdd(&s.ea_count[1], (unsigned long long)n);
+        atomicAdd(&s.ea_count[3], (unsigned long long)n * (unsigned long long)m * 4ull);
     }
 }
 
 __global__ void pq_tail_e2_kernel(RoundState s, lf_index idx, PQOverflow ov) {
-    const long long n = min((long long)*ov.n, (long long)ov.cap);
-    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
-        const double d = ov.xd[e];
-        if (!(d >= 0.0)) continue;
-        const int4 en = ov.ent[e];
-        if (d == s.cand_d[en.x]) atomicMin(reinterpret_cast<unsigned long long*>(s.cand_i) + en.x,
-                                           (unsigned long long)idx.d_row_id[ent_row(en)]);
+    const int n = *ov.xn;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int4 en = ov.ent[ov.xlist[i]];
+        if (ov.xd[i] == s.cand_d[en.x])
+            atomicMin(reinterpret_cast<unsigned long long*>(s.cand_i) + en.x, (unsigned long long)idx.d_row_id[ent_row(en)]);
     }
 }
 
@@ -727,10 +728,11 @@ cudaError_t launch_scan_pq(const RoundState& s, const lf_index& idx, const float
         if (e != cudaSuccess) return e;
     }
     if (ov.xd != nullptr) {                          // k = 1: entry-parallel tail
-        pq_tail_e1_kernel<<<sm_count() * 8, 256, 0, st>>>(s, idx, q, ov);
-        e = cudaGetLastError();
+        e = cudaMemsetAsync(ov.xn, 0, sizeof(int), st);
         if (e != cudaSuccess) return e;
-        pq_tail_e2_kernel<<<sm_count() * 4, 256, 0, st>>>(s, idx, ov);
+        pq_tail_e0_kernel<<<sm_count() * 8, 256, 0, st>>>(ov);
+        pq_tail_e1_kernel<<<sm_count() * 4, 256, 0, st>>>(s, idx, q, ov);
+        pq_tail_e2_kernel<<<sm_count() * 2, 256, 0, st>>>(s, idx, ov);
         return cudaGetLastError();
     }
     const long long warps = std::min<long long>(max_tasks, (long long)sm_count() * 64);

@@ -546,7 +546,7 @@ struct lf_session {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pev;   // profiling: per prediction pass
     bool q8 = false;                 // int8-bounded scan (query codes quantised once in begin)
     bool pq = false;                 // two-stage scan over the projected shadow (d_Xp)
-    lf::Scratch qcp, qmp, pq_cnt, pq_trows, pq_oent, pq_on, pq_obase, pq_wrows, pq_wdist, pq_lo8, pq_thr, pq_qbest, pq_xd;
+    lf::Scratch qcp, qmp, pq_cnt, pq_trows, pq_oent, pq_on, pq_obase, pq_wrows, pq_wdist, pq_lo8, pq_thr, pq_qbest, pq_xd, pq_xlist, pq_xn;
     int pq_cap = lf::PQ_OVER_CAP;    // survivor entry capacity (LF_PQ_OVER_CAP: tests of the full-list path)
     int64_t max_tasks = 1;
     int* h_active = nullptr;         // pinned [2 slots][4]: active, -, predict requests
@@ -711,7 +711,11 @@ static int session_alloc(lf_session* ss) {
         LF_CUDA(ss->pq_lo8.alloc(sizeof(float) * ss->pq_cap, st));
         LF_CUDA(ss->pq_thr.alloc(sizeof(unsigned) * max_tasks, st));
         LF_CUDA(ss->pq_qbest.alloc(sizeof(unsigned) * Q, st));
-        if (s.k == 1 && ss->q8) LF_CUDA(ss->pq_xd.alloc(sizeof(double) * ss->pq_cap, st));
+        if (s.k == 1 && ss->q8) {
+            LF_CUDA(ss->pq_xd.alloc(sizeof(double) * ss->pq_cap, st));
+            LF_CUDA(ss->pq_xlist.alloc(sizeof(int) * ss->pq_cap, st));
+            LF_CUDA(ss->pq_xn.alloc(sizeof(int), st));
+        }
     }
     if (ss->q8) {
         const int MP = (idx.m + 255) / 256 * 256;
@@ -859,7 +863,9 @@ static int round_kernels(lf_session* ss, int* counts, bool round0, cudaEvent_t* 
                             ss->q8 ? ss->qm8.as<float4>() : nullptr, (idx.m + 255) / 256 * 256,
                             ss->pq_lo8.as<float>(), ss->pq_thr.as<unsigned>(),
                             seed ? ss->pq_qbest.as<unsigned>() : nullptr,
-                            s.k == 1 && ss->q8 ? ss->pq_xd.as<double>() : nullptr};
+                            s.k == 1 && ss->q8 ? ss->pq_xd.as<double>() : nullptr,
+                            s.k == 1 && ss->q8 ? ss->pq_xlist.as<int>() : nullptr,
+                            s.k == 1 && ss->q8 ? ss->pq_xn.as<int>() : nullptr};
         ce = launch_scan_pq(s, idx, ss->d_q, ss->qcp.as<int8_t>(), ss->qmp.as<float4>(), ss->pq_cnt.as<int>(), ov,
                             ss->max_tasks, st);
         ss->kernels += ss->q8 ? 3 : 2;

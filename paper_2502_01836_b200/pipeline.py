@@ -21,6 +21,7 @@ be passed to both: its filters are packed onto the GPU and its curves used.
 from __future__ import annotations
 
 import logging
+import os
 import math
 import time
 from dataclasses import dataclass, field
@@ -266,7 +267,7 @@ def search_queries(eidx, queries, k: int = 1, *, target: float | None = None, ex
         lazy = pk.path == "tc16"
     if lazy and pk.path != "tc16":
         raise ValueError("in-search filter inference runs on the fp16 pack (FilterPack path 'tc16')")
-    if lazy and graph and profile is None and not want_trace:
+    if lazy and graph and profile is None and not want_trace and os.environ.get("LF_SEARCH_GRAPH", "1") != "0":
         plans = e.__dict__.setdefault("_plans", {})
         key = (int(q.shape[0]), int(k), float(target), bool(sequential), int(max_round_leaves), str(di.device))
         plan = plans.get(key)

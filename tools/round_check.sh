@@ -8,7 +8,9 @@ if [ -z "$SKIP_TESTS" ]; then
 fi
 timeout 600 python bench.py ${BENCH_ARGS:-} > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo "bench rc=$?"
 if [ -z "$SKIP_NCU" ]; then
-  timeout 500 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
+  # ncu cannot profile kernel nodes of graphs with conditional nodes: the launch list
+  # runs the same kernels through the stream-ordered path (LF_SEARCH_GRAPH=0)
+  LF_SEARCH_GRAPH=0 timeout 500 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
     --log-file $OUT/launches_$TAG.csv python bench.py --ncu --steps 1 --warmup 3 --no-cpu-baseline --tdg-queries 0 \
     > /dev/null 2>&1; echo "ncu rc=$?"
 fi
