@@ -47,7 +47,8 @@ struct RoundState {
     int* sel_trace;              // [Q][Rcap]
     int* sel_pre;                // [Q][Rcap+1] chunk prefix within the query
     int* n_sel;                  // [Q]
-    long long* chunk_off;        // [Q+1]
+    long long* chunk_off;        // [Q+1]: first task of query q; [Q] = the round's task count (atomic)
+    int* chunk_cnt;              // [Q] tasks of query q this round
     int4* tasks;                 // [max_tasks] (query, leaf slot, chunk, selection index)
     int4* task_rows;             // [max_tasks] (r0 lo, r0 hi, rows, query) or NULL
     unsigned long long* ea_count;  // [2] rows tested / survivors (profiling only, may be NULL)

@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) scan_kernel(RoundState s, lf_ind
     const bool vec_ok = (m & 3) == 0;
     for (long long t = blockIdx.x; t < total; t += gridDim.x) {
         // locate (query, selected leaf, chunk)
-        const int4 tk = s.tasks[t];             // (query, leaf slot, chunk) from expand_tasks_kernel
+        const int4 tk = s.tasks[t];             // (query, leaf slot, chunk) from plan_warp_kernel
         const int64_t q = tk.x;
         const int leaf = tk.y;
         const int c = tk.z;

@@ -199,54 +199,28 @@ __global__ void plan_warp_kernel(RoundState s, lf_index idx) {
             }
         }
     }
+    // this query's tasks: a contiguous range claimed from the round's task counter
+    // (chunk_off[Q]; ranges of different queries land in any order, each stays
+    // contiguous), then one lane per selected leaf writes (query, leaf, chunk) and the
+    // chunk's row range, so a scan producer needs no dependent loads
+    long long base = 0;
     if (lane == 0) {
         pre[ns] = nch;
         s.n_sel[q] = ns;
-        s.chunk_off[q + 1] = nch;
+        if (nch) base = (long long)atomicAdd(reinterpret_cast<unsigned long long*>(s.chunk_off + s.Q),
+                                             (unsigned long long)nch);
+        s.chunk_off[q] = base;
+        s.chunk_cnt[q] = nch;
     }
-}
-
-// Exclusive scan of per-query chunk counts (single CTA; Q is small).
-__global__ void offsets_kernel(long long* off, int64_t Q) {
-    __shared__ long long part[1024];
-    __shared__ long long carry;
-    if (threadIdx.x == 0) { carry = 0; off[0] = 0; }
-    __syncthreads();
-    for (int64_t base = 0; base < Q; base += blockDim.x) {
-        int64_t i = base + threadIdx.x;
-        long long v = i < Q ? off[i + 1] : 0;
-        part[threadIdx.x] = v;
-        __syncthreads();
-        for (int o = 1; o < (int)blockDim.x; o <<= 1) {
-            long long add = threadIdx.x >= (unsigned)o ? part[threadIdx.x - o] : 0;
-            __syncthreads();
-            part[threadIdx.x] += add;
-            __syncthreads();
-        }
-        if (i < Q) off[i + 1] = carry + part[threadIdx.x];
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) carry += part[threadIdx.x];
-        __syncthreads();
-    }
-}
-
-// Materialise this round's scan tasks: one warp per query writes
-// (query, leaf, chunk) for each chunk of each selected leaf at chunk_off[q] + ...
-__global__ void expand_tasks_kernel(RoundState s, const int64_t* __restrict__ leaf_ptr) {
-    const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (q >= s.Q) return;
-    const int ns = s.n_sel[q];
-    const long long base = s.chunk_off[q];
-    const int* pre = s.sel_pre + q * (s.Rcap + 1);
-    // lane per selected leaf (up to 32 leaves' loads in flight), its chunks in order
+    base = __shfl_sync(0xffffffffu, base, 0);
+    __syncwarp();                                  // sel_leaf / pre of every lane visible
     for (int j = lane; j < ns; j += 32) {
         const int leaf = s.sel_leaf[q * s.Rcap + j];
         const int c0 = pre[j], n = pre[j + 1] - c0;
-        const long long lb = leaf_ptr[leaf], le = leaf_ptr[leaf + 1];
+        const long long lb = idx.d_leaf_ptr[leaf], le = idx.d_leaf_ptr[leaf + 1];
         for (int c = 0; c < n; ++c) {
             s.tasks[base + c0 + c] = make_int4((int)q, leaf, c, j);
-            if (s.task_rows != nullptr) {   // row range of the task, so a producer needs no dependent loads
+            if (s.task_rows != nullptr) {
                 const long long r0 = lb + (long long)c * CH;
                 s.task_rows[base + c0 + c] = make_int4((int)(r0 & 0xffffffffLL), (int)(r0 >> 32),
                                                        (int)min((long long)CH, le - r0), (int)q);
@@ -398,7 +372,7 @@ __global__ void merge_kernel(RoundState s) {
     long long* oi = s.top_i_out + q * s.k;
     const int tn = s.top_n[q];
     if (ns == 0) return;                       // nothing scanned: the top-k stands
-    const long long c0 = s.chunk_off[q], c1 = s.chunk_off[q + 1];
+    const long long c0 = s.chunk_off[q], c1 = c0 + s.chunk_cnt[q];
     const long long nc = (c1 - c0) * s.kc;
     const double* cd = s.cand_d + c0 * s.kc;
     const long long* ci = s.cand_i + c0 * s.kc;
@@ -538,7 +512,7 @@ struct lf_session {
     const float* d_q = nullptr;
     lf::RoundState s{};
     lf::Scratch qsumm, lb, lbs, gap, order, cursor, done, topd, topi, topn, topd2, topi2, topn2, sel_leaf,
-        sel_trace, sel_pre, n_sel, chunk_off, cand_d, cand_i, task_min, n_active, tasks, ea_count, qc8, qm8,
+        sel_trace, sel_pre, n_sel, chunk_off, chunk_cnt, cand_d, cand_i, task_min, n_active, tasks, ea_count, qc8, qm8,
         leafo, adj, olen, pcount, pstart, pend, preq, fhist, fcur, ntiles, ptotal, pdst, ptiles, xh, xexp, round_ctr;
     lf::OrderArgs oa{};
     bool lazy = false;               // in-search filter inference (opts.d_W1T_h instead of predictions)
@@ -611,6 +585,7 @@ static int session_alloc(lf_session* ss) {
     LF_CUDA(ss->sel_pre.alloc(sizeof(int) * Q * (s.Rcap + 1), st));
     LF_CUDA(ss->n_sel.alloc(sizeof(int) * Q, st));
     LF_CUDA(ss->chunk_off.alloc(sizeof(long long) * (Q + 1), st));
+    LF_CUDA(ss->chunk_cnt.alloc(sizeof(int) * Q, st));
     LF_CUDA(ss->cand_d.alloc(sizeof(double) * max_tasks * s.kc, st));
     LF_CUDA(ss->cand_i.alloc(sizeof(long long) * max_tasks * s.kc, st));
     LF_CUDA(ss->task_min.alloc(sizeof(double) * (s.want_trace ? max_tasks : 1), st));
@@ -686,6 +661,7 @@ static int session_alloc(lf_session* ss) {
     s.sel_pre = ss->sel_pre.as<int>();
     s.n_sel = ss->n_sel.as<int>();
     s.chunk_off = ss->chunk_off.as<long long>();
+    s.chunk_cnt = ss->chunk_cnt.as<int>();
     s.cand_d = ss->cand_d.as<double>();
     s.cand_i = ss->cand_i.as<long long>();
     s.task_min = ss->task_min.as<double>();
@@ -845,9 +821,8 @@ static int round_kernels(lf_session* ss, int* counts, bool round0, cudaEvent_t* 
     s.n_predict = counts + 2;
     LF_CUDA(cudaMemsetAsync(counts, 0, sizeof(int) * 3, st));
     if (ev) cudaEventRecord(ev[0], st);
+    LF_CUDA(cudaMemsetAsync(s.chunk_off + Q, 0, sizeof(long long), st));   // the round's task counter
     plan_warp_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s, idx);
-    offsets_kernel<<<1, 1024, 0, st>>>(s.chunk_off, Q);
-    expand_tasks_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s, idx.d_leaf_ptr);
     if (ev) cudaEventRecord(ev[1], st);
     cudaError_t ce;
     // the bounded scans take m % 4 == 0 (codes zero-padded to a multiple of 64)
@@ -880,7 +855,7 @@ static int round_kernels(lf_session* ss, int* counts, bool round0, cudaEvent_t* 
     merge_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s);
     LF_CUDA(cudaGetLastError());
     if (ev) cudaEventRecord(ev[3], st);
-    ss->kernels += 5;
+    ss->kernels += 3;
     return LF_OK;
 }
 

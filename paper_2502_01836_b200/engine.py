@@ -244,7 +244,15 @@ class SearchPlan:
                                                      stats.data_ptr(), _lib.stream_ptr(stream)))
         if not copy_out:
             return ids, dists, stats
-        return BatchResult(self.tree.n, ids.cpu().numpy(), dists.cpu().numpy(), stats.cpu().numpy())
+        # results to pinned host buffers, stream-ordered, one synchronisation for all three
+        if getattr(self, "_host", None) is None:
+            self._host = tuple(torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in (ids, dists, stats))
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        with torch.cuda.stream(st):
+            for h, x in zip(self._host, (ids, dists, stats)):
+                h.copy_(x, non_blocking=True)
+        st.synchronize()
+        return BatchResult(self.tree.n, *(h.numpy().copy() for h in self._host))
 
     def __del__(self):
         h, self._h = getattr(self, "_h", None), None

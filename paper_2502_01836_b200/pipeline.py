@@ -262,7 +262,7 @@ def search_queries(eidx, queries, k: int = 1, *, target: float | None = None, ex
     pk = e.pack
     q = queries if isinstance(queries, torch.Tensor) else torch.from_numpy(
         np.ascontiguousarray(np.atleast_2d(queries), dtype=np.float32))
-    q = q.to(device=di.device, dtype=torch.float32)
+    q = q.to(device=di.device, dtype=torch.float32, non_blocking=True)   # stream-ordered from pinned memory
     if lazy is None:
         lazy = pk.path == "tc16"
     if lazy and pk.path != "tc16":
