@@ -205,14 +205,30 @@ def recall_of(res, exact) -> float:
 _OR = {}
 
 
+def bench_config(args, tree, n_filters: int, nQ: int, world: int) -> dict:
+    """The workload a bench line is quoted on -- one definition for both arms."""
+    return {
+        "workload": f"{'iSAX' if args.index == 'isax' else 'DSTree'}+LeaFi {args.n}x{args.m} "
+                    f"{'Gaussian mixture' if args.dataset == 'gmm' else 'random walk'}, leaf cap {args.leaf_cap}, "
+                    f"{nQ} queries (noise {'/'.join(map(str, NOISE_LEVELS))}), {args.k}-NN, target {args.target}",
+        "n_series": args.n, "length": args.m, "leaf_cap": args.leaf_cap, "leaves": tree.n_leaves,
+        "filters": n_filters, "queries_per_step": nQ, "k": args.k, "recall_target": args.target,
+        "parallelism": f"leaf-sharded x{world}" if world > 1 else "1 GPU",
+        "l2": "inputs larger than L2 (25.6 GB collection)",
+    }
+
+
 def _oracle_worker(qi_list):
+    from threadpoolctl import threadpool_limits
+
     from oracle import leafi_oracle as lo
 
     t, preds, offs, Qh = _OR["tree"], _OR["preds"], _OR["offs"], _OR["Q"]
     out = []
-    for qi in qi_list:
-        o = lo.search(t, Qh[qi], _OR.get("k", 1), predictors=preds, offsets=offs)
-        out.append((qi, o.results[0][0], o.stats["series_scanned"]))
+    with threadpool_limits(limits=1):              # one core per worker: BLAS stays single-threaded
+        for qi in qi_list:
+            o = lo.search(t, Qh[qi], _OR.get("k", 1), predictors=preds, offsets=offs)
+            out.append((qi, o.results[0][0], o.stats["series_scanned"]))
     return out
 
 
@@ -673,15 +689,7 @@ def run_ours(args, rank, world, device):
             "filters on fp16 operands (power-of-two scaled, tf32 mantissa) with f32 accumulation"
             if eidx.pack.path == "tc16" else "tf32 filters" if eidx.pack.path == "tc" else "f32 filters"),
         "data": "synthetic random walk generated on device (reference law, Philox stream), 25.6 GB >> L2: no flush needed",
-        "config": {
-            "workload": f"{'iSAX' if args.index == 'isax' else 'DSTree'}+LeaFi {args.n}x{args.m} "
-                        f"{'Gaussian mixture' if args.dataset == 'gmm' else 'random walk'}, leaf cap {args.leaf_cap}, "
-                        f"{nQ} queries (noise {'/'.join(map(str, NOISE_LEVELS))}), {args.k}-NN, target {args.target}",
-            "n_series": args.n, "length": args.m, "leaf_cap": args.leaf_cap, "leaves": tree.n_leaves,
-            "filters": len(eidx.filters), "queries_per_step": nQ, "k": args.k, "recall_target": args.target,
-            "parallelism": f"leaf-sharded x{world}" if world > 1 else "1 GPU",
-            "l2": "inputs larger than L2 (25.6 GB collection)",
-        },
+        "config": bench_config(args, tree, len(eidx.filters), nQ, world),
         "recall_at_1": recall,
         **({f"recall_at_{args.k}": recall_k} if args.k > 1 else {}),
         "leaves_pruned_pct": 100.0 * leaves_pruned,
@@ -748,8 +756,12 @@ def run_ours(args, rank, world, device):
         line["cpu_baseline"] = {"value": len(idx) / el, "unit": "queries/s", "cores": workers, "kind": "port",
                                 "sample": f"{len(idx)} of the {nQ} benchmark queries (evenly spaced over the 4 noise "
                                           f"levels), oracle/leafi_oracle.search with the same tree, filters and "
-                                          f"offsets, {workers} forked processes, {el:.1f}s",
+                                          f"offsets, {workers} forked processes (one BLAS thread each), {el:.1f}s",
                                 "ids_agree_with_gpu": agree}
+        idx1 = np.linspace(0, nQ - 1, max(4, min(nQ, len(idx) // (4 * workers)))).astype(int)
+        t1, _ = oracle_time(idx1, 1)
+        line["cpu_baseline"]["one_core"] = {"value": len(idx1) / t1, "unit": "queries/s", "cores": 1,
+                                            "sample": f"{len(idx1)} queries evenly spaced over the noise levels"}
     return line
 
 
@@ -772,17 +784,23 @@ def run_reference(args, rank, world, device):
         times.append(el)
         n_done += len(idx)
     value = n_done / sum(times)
+    # one core: the reference's own single-threaded search loop (BASELINE.md asks for it)
+    n1 = max(4, min(nQ, int(args.ref_step_s * 0.25 / max(1e-3, sum(times) / max(1, n_done) * workers))))
+    t1, _ = oracle_time(idx_all[np.linspace(0, nQ - 1, n1).astype(int)], 1)
     return {
         "impl": "reference",
         "metric": metric_name(args),
         "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64 (numpy oracle)", "data": "same synthetic workload as the ours arm",
-        "config": {"workload": f"DSTree+LeaFi {args.n}x{args.m}, leaf cap {args.leaf_cap}, 1-NN, target {args.target}",
-                   "queries_per_step": n_s},
+        "config": bench_config(args, w["tree"], len(w["eidx"].filters), nQ, world),
         "cpu_baseline": {"value": value, "unit": "queries/s", "cores": workers, "kind": "port",
-                         "sample": f"{n_s} queries per step over {workers} forked processes "
-                                   f"(oracle/leafi_oracle.search, reference algorithm restated)"},
+                         "sample": f"{n_s} of the {nQ} benchmark queries per step over {workers} forked processes, "
+                                   f"one BLAS thread each (oracle/leafi_oracle.search, the reference algorithm "
+                                   f"restated; tree, filters and offsets are the ours-arm ones, built before "
+                                   f"the timed region)",
+                         "one_core": {"value": n1 / t1, "unit": "queries/s", "cores": 1,
+                                      "sample": f"{n1} queries evenly spaced over the noise levels"}},
         "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
