@@ -727,13 +727,24 @@ def run_ours(args, rank, world, device):
         "filter_inference": {
             "mode": ("in-search: one pass right after round 0 over the (query, filtered leaf) pairs with "
                      "lb <= bsf0 * f (all the walk can still reach), tcgen05 kind::f16 with the query rows "
-                     "gathered by TMA gather4, bit-identical to the dense kernel") if lazy_on else
+                     "gathered by cp.async, bit-identical to the dense kernel") if lazy_on else
                     ("dense: one tcgen05 pass over every (query, filter) pair before lf_search ("
                      + ("kind::f16 over power-of-two-scaled fp16 operands" if eidx.pack.path == "tc16"
                         else eidx.pack.path) + ")"),
             "pairs_per_step": lazy_pairs / args.steps, "dense_pairs_per_step": nQ * F,
             "ms_per_step": pred_ms / args.steps, "passes_per_step": pred_steps / args.steps,
             "pair_flops_per_step": 2.0 * (lazy_pairs / args.steps) * tree.m * (tree.m + 1),
+            # the in-search pass (pair lists + GEMM) streams every filter's fp16 W1 once: HBM-bound
+            "in_search_roofline": ({
+                "bound": "hbm", "unit": "GB/s", "peak": hbm, "peak_source": peak_src,
+                "algorithmic_bytes": float(F) * tree.m * tree.m * 2 + (lazy_pairs / args.steps) * 16,
+                "definition": "F x m x m x 2 B (each filter's fp16 W1 once) + 16 B per predicted pair "
+                              "(pair record + record update); ms = the whole pass (pair ranges, buckets, GEMM)",
+                "achieved": (float(F) * tree.m * tree.m * 2 + (lazy_pairs / args.steps) * 16)
+                            / (pred_ms / args.steps / 1e3) / 1e9,
+                "frac": (float(F) * tree.m * tree.m * 2 + (lazy_pairs / args.steps) * 16)
+                        / (pred_ms / args.steps / 1e3) / 1e9 / hbm,
+            } if lazy_on and pred_ms > 0 else None),
             "dense_kernel": {
                 "path": eidx.pack.path, "bound": "tensor", "ms": filter_ms, "achieved": filter_tflops,
                 "unit": "TFLOP/s", "peak": fpk, "frac": filter_tflops / fpk,
