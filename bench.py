@@ -214,7 +214,7 @@ def bench_config(args, tree, n_filters: int, nQ: int, world: int) -> dict:
         "n_series": args.n, "length": args.m, "leaf_cap": args.leaf_cap, "leaves": tree.n_leaves,
         "filters": n_filters, "queries_per_step": nQ, "k": args.k, "recall_target": args.target,
         "parallelism": f"leaf-sharded x{world}" if world > 1 else "1 GPU",
-        "l2": "inputs larger than L2 (25.6 GB collection)",
+        "l2": f"inputs larger than L2 ({args.n * args.m * 4 / 1e9:.1f} GB collection)",
     }
 
 
@@ -688,7 +688,8 @@ def run_ours(args, rank, world, device):
         "dtype": "f64-accumulated f32 series (scan/bounds), " + (
             "filters on fp16 operands (power-of-two scaled, tf32 mantissa) with f32 accumulation"
             if eidx.pack.path == "tc16" else "tf32 filters" if eidx.pack.path == "tc" else "f32 filters"),
-        "data": "synthetic random walk generated on device (reference law, Philox stream), 25.6 GB >> L2: no flush needed",
+        "data": (f"synthetic {'Gaussian mixture' if args.dataset == 'gmm' else 'random walk (reference law, Philox stream)'} "
+                 f"generated on device, {args.n * args.m * 4 / 1e9:.1f} GB >> L2: no flush needed"),
         "config": bench_config(args, tree, len(eidx.filters), nQ, world),
         "recall_at_1": recall,
         **({f"recall_at_{args.k}": recall_k} if args.k > 1 else {}),
