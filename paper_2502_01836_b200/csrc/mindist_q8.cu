@@ -358,10 +358,14 @@ mindist_q8_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_consta
                         // 16 three-way integer maxima instead of ~8 fp32 ops per element
                         bool live = qv;
                         if (live) {
-                            int dmax = (int)r[0];
+                            // tree of three-way maxima (depth 4, not a 15-long dependent chain)
+                            int m1[11];
 #pragma unroll
-                            for (int j = 1; j + 1 < 32; j += 2) dmax = __vimax3_s32(dmax, (int)r[j], (int)r[j + 1]);
-                            dmax = max(dmax, (int)r[31]);
+                            for (int j = 0; j < 10; ++j) m1[j] = __vimax3_s32((int)r[3 * j], (int)r[3 * j + 1], (int)r[3 * j + 2]);
+                            m1[10] = max((int)r[30], (int)r[31]);
+                            const int m2a = __vimax3_s32(m1[0], m1[1], m1[2]), m2b = __vimax3_s32(m1[3], m1[4], m1[5]);
+                            const int m2c = __vimax3_s32(m1[6], m1[7], m1[8]), m2d = max(m1[9], m1[10]);
+                            const int dmax = max(__vimax3_s32(m2a, m2b, m2c), m2d);
                             const float4 gm = gmeta[bb * N_GRP + grp * 4 + (c0 >> 5)];
                             const float L = fmaf(-gamma, gm.y, gm.x + beta);
                             const float Rm = cq2 * (float)dmax * (dmax > 0 ? gm.z : gm.w);
