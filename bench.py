@@ -657,9 +657,9 @@ def run_ours(args, rank, world, device):
     ref_bytes = scanned_per_step * tree.m * 4 * args.steps
     if stream_b > 0:
         alg_bytes = stream_b + exact_b
-        bytes_def = ("bytes the scan kernels must move, counted in the kernels: per tested row its codes + 16 B "
-                     "metadata (round 0: int8 shadow, m bytes; later rounds: projected shadow, pca_k bytes), plus "
-                     "m x 4 B for every surviving row re-read exactly")
+        bytes_def = ("bytes the scan kernels must move, counted in the kernels: per tested row its projected "
+                     "codes (pca_k bytes) + 8 B fp16 metadata; per projected survivor its int8 row + 16 B "
+                     "metadata; m x 4 B for every row re-read exactly")
     else:
         alg_bytes = ref_bytes
         bytes_def = "series_scanned x m x 4 B"

@@ -58,13 +58,15 @@ typedef struct lf_index {
                                     codes (exact in fp32), ||scale * code - x||_2 rounded up, 0 */
     /* optional projected shadow for the two-stage scan (NULL = unused): an orthonormal
        basis P of pca_k directions (fp64, rows orthonormal), the mean mu, and per row the
-       int8 codes of y = P (x - mu) with {scale, sum code^2, ||scale*code - y|| rounded up,
-       ||(x - mu) - P^T y||} -- ||x - q||^2 = ||y - y_q||^2 + ||r - r_q||^2 */
+       int8 codes of y = P (x - mu) and 8 bytes of fp16 metadata {scale (the exact
+       quantisation step: codes = rint(y / scale)), ||scale*code - y|| rounded up,
+       ||(x - mu) - P^T y|| rounded to nearest, 0}; ||scale * code||^2 is recomputed from
+       the codes -- ||x - q||^2 = ||y - y_q||^2 + ||r - r_q||^2 */
     int32_t pca_k;               /* 32 or 64 (0 = no projected shadow) */
     const double* d_P;           /* [pca_k][m] */
     const double* d_mu;          /* [m] */
     const int8_t* d_Xp;          /* [n_series][pca_k] */
-    const float* d_pmeta;        /* [n_series][4] */
+    const uint16_t* d_pmeta;     /* [n_series + 2][4] fp16 bits (two rows of padding) */
     /* optional EAPCA envelopes (NULL = the reference's mean-only bound): per node the
        [min, max] of its members' segment standard deviations, SoA [n_seg][n_nodes];
        with them the search bound is the EAPCA bound (lf_bounds_eapca) */

@@ -51,7 +51,9 @@ template <int KP>
 struct PQW {
     static constexpr int WARPS = KP == 32 ? LF_PQW_WARPS32 : 8;
     static constexpr int CODE = PQW_STG * KP;
-    static constexpr int STAGE = CODE + PQW_STG * 16;
+    // codes + 8 B fp16 metadata per row; the metadata copy starts at an even row (16-byte
+    // aligned source), so a slot holds up to two more metadata rows
+    static constexpr int STAGE = CODE + (PQW_STG + 2) * 8;
     static constexpr int RING = WARPS * PQW_NS * STAGE;
     static constexpr int BAR_OFF = RING;
     static constexpr int SMEM = BAR_OFF + WARPS * PQW_NS * 8;
@@ -259,10 +261,12 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
         if (lane == 0) {
             unsigned char* dst = ring + slot * C::STAGE;
             const int64_t rr = ir0 + (int64_t)ip * PQW_STG;
-            q8_expect_tx(&bars[slot], (uint32_t)(rows > 0 ? rows * (KP + 16) : 0));
+            const int64_t ra = rr & ~1ll;                              // even: 16-byte aligned source
+            const uint32_t mb = (uint32_t)(((rr + rows - ra) * 8 + 15) & ~15);   // padded array
+            q8_expect_tx(&bars[slot], (uint32_t)(rows > 0 ? rows * KP + mb : 0));
             if (rows > 0) {
                 q8_bulk(dst, idx.d_Xp + rr * KP, (uint32_t)(rows * KP), &bars[slot], pol);
-                q8_bulk(dst + C::CODE, idx.d_pmeta + rr * 4, (uint32_t)(rows * 16), &bars[slot], pol);
+                q8_bulk(dst + C::CODE, idx.d_pmeta + ra * 4, mb, &bars[slot], pol);
             }
         }
         if (++ip * PQW_STG >= inrows) {
@@ -290,6 +294,7 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
         const int64_t r0 = (int64_t)(unsigned)tr.x | ((int64_t)tr.y << 32);
         const int nrows = tr.z;
         const int64_t q = tr.w;
+        const int mo = (int)(r0 & 1);                 // metadata rows start one early when r0 is odd
         const int pieces = nrows > 0 ? (nrows + PQW_STG - 1) / PQW_STG : 1;
         const float sq = qmv.x, eq = qmv.z, rq = qmv.w;
         const float sq2qq = sq * sq * qmv.y;
@@ -314,30 +319,38 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
                     int4 w[V];
 #pragma unroll
                     for (int c = 0; c < V; ++c) w[c] = *reinterpret_cast<const int4*>(stg + ri * KP + c * 16);
-                    const float4 mr = *reinterpret_cast<const float4*>(stg + C::CODE + ri * 16);
-                    int dot = 0;
+                    const uint2 mp = *reinterpret_cast<const uint2*>(stg + C::CODE + (ri + mo) * 8);
+                    const float msc = __half2float(__ushort_as_half((unsigned short)(mp.x & 0xffffu)));
+                    const float mer = __half2float(__ushort_as_half((unsigned short)(mp.x >> 16)));
+                    const float mrn = __half2float(__ushort_as_half((unsigned short)(mp.y & 0xffffu)));
+                    int dot = 0, cc = 0;
 #pragma unroll
                     for (int c = 0; c < V; ++c) {
                         dot = __dp4a(w[c].x, qw[c].x, dot);
                         dot = __dp4a(w[c].y, qw[c].y, dot);
                         dot = __dp4a(w[c].z, qw[c].z, dot);
                         dot = __dp4a(w[c].w, qw[c].w, dot);
+                        cc = __dp4a(w[c].x, w[c].x, cc);
+                        cc = __dp4a(w[c].y, w[c].y, cc);
+                        cc = __dp4a(w[c].z, w[c].z, cc);
+                        cc = __dp4a(w[c].w, w[c].w, cc);
                     }
-                    const float nn = mr.y + sq2qq;               // ||x_c||^2 + ||q_c||^2
-                    const float a2 = fmaf(-(mr.x * sq2), (float)dot, nn);
+                    const float nn = fmaf(msc * msc, (float)cc, sq2qq);  // ||x_c||^2 + ||q_c||^2
+                    const float a2 = fmaf(-(msc * sq2), (float)dot, nn);
                     const float tol = 1e-5f * nn;
-                    const float e = mr.z + eq;
+                    const float e = mer + eq;
                     // sqrt.approx (rel err < 2^-22): the tol slack (>= 2.5e-6 sqrt(a2)) and the
                     // final 1 -+ 1e-5 factors cover it, so both ends stay rigorous
                     const float alo = fmaxf(sqrt_approx(fmaxf(a2 - tol, 0.f)) - e, 0.f);
                     const float ahi = sqrt_approx(fmaxf(a2 + tol, 0.f)) + e;
-                    const float rs = mr.w + rq;
-                    const float blo = fmaxf(fmaf(-1e-6f, rs, fabsf(mr.w - rq)), 0.f);
-                    const float bhi = rs * (1.f + 1e-6f);
+                    // the residual norm is fp16 (nearest): |r - r16| <= 2^-11 r16, widened to 2^-10
+                    const float rs = mrn + rq;
+                    const float blo = fmaxf(fabsf(mrn - rq) - fmaf(1e-6f, rs, 9.765625e-4f * mrn), 0.f);
+                    const float bhi = fmaf(9.765625e-4f, mrn, rs) * (1.f + 1e-6f);
                     lo2[p * RPL + u] = v ? fmaf(alo, alo, blo * blo) : __int_as_float(0x7f800000);
                     hmin2 = fminf(hmin2, v ? fmaf(ahi, ahi, bhi * bhi) : __int_as_float(0x7f800000));
                     if (SEED) {
-                        const float est = fmaf(mr.w, mr.w, a2 + rq2);
+                        const float est = fmaf(mrn, mrn, a2 + rq2);
                         if (v && est < best_est) { best_est = est; best_ri = p * PQW_STG + ri; }
                     }
                 }
@@ -442,7 +455,7 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
     }
     if (s.ea_count != nullptr && lane == 0 && c_rows > 0) {
         atomicAdd(&s.ea_count[0], c_rows);
-        atomicAdd(&s.ea_count[2], c_rows * (unsigned long long)(KP + 16));
+        atomicAdd(&s.ea_count[2], c_rows * (unsigned long long)(KP + 8));
         if (ov.qc8 == nullptr) {                      // else the int8 stage / re-read count theirs
             atomicAdd(&s.ea_count[1], c_surv);
             atomicAdd(&s.ea_count[3], c_surv * (unsigned long long)m * 4ull);

@@ -427,21 +427,24 @@ class DeviceIndex:
                 return False
             P = V[:k].contiguous()
             codes = torch.empty((n, k), dtype=torch.int8, device=self.device)
-            meta = torch.empty((n, 4), dtype=torch.float32, device=self.device)
-            inf32 = torch.tensor(float("inf"), dtype=torch.float32, device=self.device)
+            # 8 B of fp16 metadata per row (+ 2 rows of padding: the scan's bulk copies
+            # round a piece's metadata up to 16 bytes)
+            meta = torch.zeros((n + 2, 4), dtype=torch.float16, device=self.device)
+            inf16 = torch.tensor(float("inf"), dtype=torch.float16, device=self.device)
             for r0 in range(0, n, 1 << 20):
                 A = X[r0:r0 + (1 << 20)].double() - mu
                 y = A @ P.T
                 r = (A - y @ P).norm(dim=1)
-                s32 = (y.abs().amax(1) / 127).float()
-                s32 = torch.where(s32 > 0, s32, torch.ones_like(s32))
-                c = torch.round(y / s32.double()[:, None]).clamp(-127, 127)
-                e = ((c * s32.double()[:, None] - y).norm(dim=1) * (1 + 1e-9) + 1e-30)
-                e32 = e.float()
-                e32 = torch.where(e32.double() < e, torch.nextafter(e32, inf32), e32)      # rounded up
+                s = y.abs().amax(1) / 127
+                s16 = torch.where(s > 0, s, torch.ones_like(s)).half()
+                s16 = torch.where(s16.double() < s, torch.nextafter(s16, inf16), s16)   # up: |y| / s <= 127
+                sd = s16.double()
+                c = torch.round(y / sd[:, None]).clamp(-127, 127)
+                e = ((c * sd[:, None] - y).norm(dim=1) * (1 + 1e-9) + 1e-30)
+                e16 = e.half()
+                e16 = torch.where(e16.double() < e, torch.nextafter(e16, inf16), e16)   # rounded up
                 codes[r0:r0 + (1 << 20)] = c.to(torch.int8)
-                xx = (s32.double() ** 2 * (c * c).sum(1)).float()      # ||scale * code||^2
-                meta[r0:r0 + (1 << 20)] = torch.stack([s32, xx, e32, r.float()], dim=1)
+                meta[r0:r0 + A.shape[0]] = torch.stack([s16, e16, r.half(), torch.zeros_like(s16)], dim=1)
         self.pca_k, self.P, self.mu, self.Xp, self.pmeta = k, P, mu.contiguous(), codes, meta
         return True
 
