@@ -101,7 +101,8 @@ __global__ void __launch_bounds__(LBT_NODES, MODE == 2 ? 2 : 4)
     lb_tile_kernel(const double* __restrict__ qsumm, int64_t Q, int ns, lf_index idx,
                    const double* __restrict__ env_min, const double* __restrict__ env_max,
                    const double* __restrict__ sd_min, const double* __restrict__ sd_max, int n_env,
-                   double* __restrict__ lb, unsigned* __restrict__ qmax, unsigned* __restrict__ qmin) {
+                   double* __restrict__ lb, unsigned* __restrict__ qmax, unsigned* __restrict__ qmin,
+                   double* __restrict__ plb, int* __restrict__ pnode) {
     constexpr int QW = MODE == 2 ? 2 * LBT_SEG : LBT_SEG;
     __shared__ double qs[LBT_Q][QW];
     __shared__ double ws[LBT_SEG];
@@ -150,6 +151,22 @@ __global__ void __launch_bounds__(LBT_NODES, MODE == 2 ? 2 : 4)
                 atomicMax(qmax + q0 + qq, hi);
                 atomicMin(qmin + q0 + qq, lo);
             }
+            if (plb != nullptr) {       // the warp's minimum (lb, node) over its leaves, exactly:
+                // bound bits order like the non-negative values; three integer reductions
+                const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+                const unsigned bh = (unsigned)(b >> 32), bl = (unsigned)b;
+                const unsigned mh = __reduce_min_sync(0xffffffffu, isl ? bh : 0xffffffffu);
+                const bool c1 = isl && bh == mh;
+                const unsigned ml = __reduce_min_sync(0xffffffffu, c1 ? bl : 0xffffffffu);
+                const bool c2 = c1 && bl == ml;
+                const unsigned mn = __reduce_min_sync(0xffffffffu, c2 ? (unsigned)node : 0xffffffffu);
+                if (lane == 0 && node < n_env) {                 // warps past the last node own no slot
+                    const int W = (n_env + 31) >> 5;
+                    const int64_t at = (q0 + qq) * W + (node >> 5);
+                    plb[at] = mn == 0xffffffffu ? kInf : __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+                    pnode[at] = mn == 0xffffffffu ? -1 : (int)mn;
+                }
+            }
         }
     }
 }
@@ -157,7 +174,7 @@ __global__ void __launch_bounds__(LBT_NODES, MODE == 2 ? 2 : 4)
 int launch_bounds(const float* d_q, int64_t Q, const lf_index& idx, const double* env_min,
                   const double* env_max, int n_env, int mode, double* d_qsumm, double* d_lb,
                   cudaStream_t st, unsigned* d_qmax, unsigned* d_qmin, const double* sd_min,
-                  const double* sd_max) {
+                  const double* sd_max, double* d_plb, int* d_pnode) {
     if (Q == 0) return LF_OK;
     {
         int64_t n = Q * idx.n_seg;
@@ -176,7 +193,8 @@ int launch_bounds(const float* d_q, int64_t Q, const lf_index& idx, const double
         }
         dim3 grid((unsigned)((n_env + LBT_NODES - 1) / LBT_NODES), (unsigned)((Q + LBT_Q - 1) / LBT_Q));
 #define LF_TILE(M) lb_tile_kernel<M><<<grid, LBT_NODES, 0, st>>>(d_qsumm, Q, idx.n_seg, idx, env_min, env_max, \
-                                                                sd_min, sd_max, n_env, d_lb, d_qmax, d_qmin)
+                                                                sd_min, sd_max, n_env, d_lb, d_qmax, d_qmin, \
+                                                                d_plb, d_pnode)
         if (mode == 0) LF_TILE(0);
         else if (mode == 1) LF_TILE(1);
         else LF_TILE(2);
@@ -241,7 +259,9 @@ __device__ __forceinline__ void put_records(const OrderArgs& o, const lf_index& 
         o.lbs[at] = lbv[i];
         o.gap[at] = gapv[i];
         o.leafo[at] = rec;
-        o.adj[at] = a;
+        // in-search inference writes adj of every pair the walk can reach before the walk
+        // reads it (plan reads adj only below pcount), so the lazy order leaves it unset
+        if (!o.lazy) o.adj[at] = a;
         if (o.order != nullptr) o.order[at] = node[i];
     }
 }
@@ -285,6 +305,10 @@ struct LoSmem {
     int bend[LO_NB];                               // bucket counts -> starts -> ends
     int big[LO_BIG_LIST];
     int nstage, nbig;
+    double tlb_w[LO_WARPS];                        // pruned orders: the first leaf past thr
+    int tnode_w[LO_WARPS];
+    double tlb;
+    int tnode;
 };
 
 __device__ __forceinline__ int lo_bucket(double v, double lo, double scale) {
@@ -308,9 +332,17 @@ __global__ void __launch_bounds__(LO_THREADS, 2) leaf_order_kernel(const double*
     const int Nn = idx.n_nodes;
     const int Lr = idx.n_leaves;
     const double* lbq = lb + q * Nn;
+    double thr = kInf;                                   // pruned orders: leaves past thr are not records
+    if (o.prune) {
+        double b = o.top_n[q] == o.k ? o.top_d[q * o.k + o.k - 1] : kInf;
+        if (o.bound != nullptr) b = fmin(b, o.bound[q]);
+        thr = b * o.f;
+    }
     const double lo = (double)__uint_as_float(qmin[q]);
-    const double span = (double)__uint_as_float(qmax[q]) - lo;
+    const double span = fmin((double)__uint_as_float(qmax[q]), thr) - lo;
     const double scale = (span > 0.0 && span < kInf) ? (double)(LO_NB - 1) / span : 0.0;
+    double tv = kInf;                                    // this thread's first leaf past thr
+    int tn = 0x7fffffff;
     for (int b = tid; b < LO_NB; b += LO_THREADS) sm.bend[b] = 0;
     if (tid == 0) {
         sm.nstage = 0;
@@ -336,13 +368,18 @@ __global__ void __launch_bounds__(LO_THREADS, 2) leaf_order_kernel(const double*
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
             const bool isl = nl[e] >= 0;
-            const unsigned bm = __ballot_sync(0xffffffffu, isl);
+            if (isl) flags |= 1u << (h + e);
+            const bool stage = isl && v[e] <= thr;
+            if (isl && !stage && lo_less(v[e], (h + e) * LO_THREADS + tid, tv, tn)) {
+                tv = v[e];
+                tn = (h + e) * LO_THREADS + tid;
+            }
+            const unsigned bm = __ballot_sync(0xffffffffu, stage);
             if (bm == 0) continue;
             int base = 0;
             if (lane == 0) base = atomicAdd(&sm.nstage, __popc(bm));
             base = __shfl_sync(0xffffffffu, base, 0);
-            if (isl) {
-                flags |= 1u << (h + e);
+            if (stage) {
                 const int pos = base + __popc(bm & below);
                 sm.u.st.lb[pos] = v[e];
                 sm.u.st.node[pos] = (h + e) * LO_THREADS + tid;
@@ -350,8 +387,25 @@ __global__ void __launch_bounds__(LO_THREADS, 2) leaf_order_kernel(const double*
             }
         }
     }
+    if (o.prune) {                                       // the first leaf past thr: block minimum
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, tv, d);
+            const int on = __shfl_xor_sync(0xffffffffu, tn, d);
+            if (lo_less(ov, on, tv, tn)) { tv = ov; tn = on; }
+        }
+        if (lane == 0) { sm.tlb_w[warp] = tv; sm.tnode_w[warp] = tn; }
+    }
     __syncthreads();
     const int L = sm.nstage;
+    if (o.prune && tid == 0) {
+        double bv = kInf;
+        int bn = 0x7fffffff;
+        for (int w = 0; w < LO_WARPS; ++w)
+            if (lo_less(sm.tlb_w[w], sm.tnode_w[w], bv, bn)) { bv = sm.tlb_w[w]; bn = sm.tnode_w[w]; }
+        sm.tlb = bv;
+        sm.tnode = bn == 0x7fffffff ? -1 : bn;
+    }
     // 2. exclusive scan of the counts (8 consecutive buckets per thread), then scatter
     {
         constexpr int PT = LO_NB / LO_THREADS;
@@ -430,7 +484,8 @@ __global__ void __launch_bounds__(LO_THREADS, 2) leaf_order_kernel(const double*
         }
         __syncthreads();
     }
-    for (int p = tid; p < L; p += LO_THREADS) sm.u.gap[p] = 0ull;
+    const bool has_term = o.prune && sm.tnode >= 0;      // (visible: written before the last barriers)
+    for (int p = tid; p < L + (has_term ? 1 : 0); p += LO_THREADS) sm.u.gap[p] = 0ull;
     __syncthreads();
     // 4. gap bounds of the non-leaf nodes
 #pragma unroll
@@ -445,11 +500,13 @@ __global__ void __launch_bounds__(LO_THREADS, 2) leaf_order_kernel(const double*
         for (int e = 0; e < 8; ++e) {
             if (v[e] < 0.0) continue;
             const int node = (h + e) * LO_THREADS + tid;
+            if (v[e] > thr && !(has_term && lo_less(v[e], node, sm.tlb, sm.tnode))) continue;   // past the end
             const int b = lo_bucket(v[e], lo, scale);
             int p = b == 0 ? 0 : sm.bend[b - 1];
             const int e0 = sm.bend[b];
             while (p < e0 && lo_less(sm.lb[p], sm.node[p], v[e], node)) ++p;
-            if (p < L) atomicMax(&sm.u.gap[p], (unsigned long long)__double_as_longlong(v[e]));
+            if (p < L || (p == L && has_term))
+                atomicMax(&sm.u.gap[p], (unsigned long long)__double_as_longlong(v[e]));
         }
     }
     __syncthreads();
@@ -468,7 +525,14 @@ __global__ void __launch_bounds__(LO_THREADS, 2) leaf_order_kernel(const double*
         }
         put_records<4>(o, idx, q, Lr, L, p, node, lbv, gv);
     }
-    if (tid == 0) o.olen[q] = L;
+    if (tid == 0) {
+        if (has_term) {                                  // the terminal record
+            const int p1[1] = {L}, n1[1] = {sm.tnode};
+            const double l1[1] = {sm.tlb}, g1[1] = {__longlong_as_double((long long)sm.u.gap[L])};
+            put_records<1>(o, idx, q, Lr, L + 1, p1, n1, l1, g1);
+        }
+        o.olen[q] = L + (has_term ? 1 : 0);
+    }
 }
 
 // Any tree size: one warp per query walks the FULL sorted (lb, node id) order
@@ -526,6 +590,27 @@ static int launch_leaf_order(const double* d_lb, int64_t Q, const lf_index& idx,
     return LF_OK;
 }
 
+bool fused_order_ok(const lf_index& idx, int64_t Q) {
+    return idx.n_nodes <= LO_THREADS * LO_MAX_NI && idx.n_leaves <= LO_MAX_LEAVES && idx.n_seg <= LBT_SEG &&
+           (Q + LBT_Q - 1) / LBT_Q <= 65535 && Q <= 0x7fffffff;
+}
+
+int bounds_phase(const float* d_q, int64_t Q, const lf_index& idx, double* d_qsumm, double* d_lb, unsigned* qmax,
+                 unsigned* qmin, double* plb, int* pnode, cudaStream_t st, int* kernels) {
+    LF_REQUIRE(fused_order_ok(idx, Q), "bounds_phase: tree too large for the single-CTA leaf order");
+    const bool eapca = idx.d_sd_min != nullptr && idx.d_sd_max != nullptr;
+    int rc = launch_bounds(d_q, Q, idx, idx.d_env_min, idx.d_env_max, idx.n_nodes, eapca ? 2 : 0, d_qsumm, d_lb, st,
+                           qmax, qmin, idx.d_sd_min, idx.d_sd_max, plb, pnode);
+    if (rc == LF_OK && kernels) *kernels += 2;
+    return rc;
+}
+
+int order_phase(const double* d_lb, int64_t Q, const lf_index& idx, const unsigned* qmax, const unsigned* qmin,
+                const OrderArgs& oa, cudaStream_t st) {
+    if (idx.n_nodes <= LO_THREADS * 8) return launch_leaf_order<8>(d_lb, Q, idx, qmax, qmin, oa, st);
+    return launch_leaf_order<16>(d_lb, Q, idx, qmax, qmin, oa, st);
+}
+
 // Segment means + node bounds + per-query leaf records: the bound matrix
 // (lb_tile_kernel) feeds the per-query leaf sort when the tree fits one CTA
 // (<= 8192 nodes, <= 4096 leaf slots), else CUB's segmented sort of all nodes
@@ -534,8 +619,7 @@ int bounds_and_order(const float* d_q, int64_t Q, const lf_index& idx, double* d
                      const OrderArgs& oa, cudaStream_t st, int* kernels) {
     const int n = idx.n_nodes;
     if (Q == 0 || n == 0) return LF_OK;
-    const bool fused = n <= LO_THREADS * LO_MAX_NI && idx.n_leaves <= LO_MAX_LEAVES && idx.n_seg <= LBT_SEG &&
-                       (Q + LBT_Q - 1) / LBT_Q <= 65535 && Q <= 0x7fffffff;
+    const bool fused = fused_order_ok(idx, Q);
     Scratch range;
     if (fused) LF_CUDA(range.alloc(sizeof(unsigned) * 2 * Q, st));
     unsigned* qmax = fused ? range.as<unsigned>() : nullptr;

@@ -229,6 +229,71 @@ __global__ void plan_warp_kernel(RoundState s, lf_index idx) {
     }
 }
 
+// Round 0 of a pruned-order search (the visit orders are built after round 0): every
+// walk pops its first leaf -- the minimum (lb, node id) over the leaves, from
+// lb_tile's per-group minima -- and scans it; bsf is +inf, so nothing is pruned
+// and the counters are the reference's for one visited, searched leaf.
+__global__ void first_leaf_plan_kernel(RoundState s, lf_index idx, const double* __restrict__ plb,
+                                       const int* __restrict__ pnode, int W) {
+    const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (q >= s.Q) return;
+    double bv = kInf;
+    int bn = 0x7fffffff;
+    for (int w = lane; w < W; w += 32) {
+        const int nd = pnode[q * W + w];
+        if (nd < 0) continue;
+        const double v = plb[q * W + w];
+        if (v < bv || (v == bv && nd < bn)) { bv = v; bn = nd; }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, d);
+        const int on = __shfl_xor_sync(0xffffffffu, bn, d);
+        if (ov < bv || (ov == bv && on < bn)) { bv = ov; bn = on; }
+    }
+    int* pre = s.sel_pre + q * (s.Rcap + 1);
+    if (bn == 0x7fffffff) {                            // no leaf on this shard
+        if (lane == 0) {
+            s.n_sel[q] = 0;
+            pre[0] = 0;
+            s.chunk_off[q] = 0;
+            s.chunk_cnt[q] = 0;
+            s.done[q] = 1;
+        }
+        return;
+    }
+    const int leaf = idx.d_node_leaf[bn];
+    const long long lb0 = idx.d_leaf_ptr[leaf], le0 = idx.d_leaf_ptr[leaf + 1];
+    const int nch = (int)((le0 - lb0 + CH - 1) / CH);
+    long long base = 0;
+    if (lane == 0) {
+        long long* st = s.stats + q * LF_N_STATS;
+        st[0] += 1;                                    // visited
+        st[1] += 1;                                    // searched
+        if (idx.d_leaf_filter != nullptr && s.F > 0 && idx.d_leaf_filter[leaf] >= 0) st[4] += 1;   // inference
+        st[5] += le0 - lb0;
+        s.cursor[q] = 1;
+        atomicAdd(s.n_active, 1);
+        s.sel_leaf[q * s.Rcap] = leaf;
+        pre[0] = 0;
+        pre[1] = nch;
+        s.n_sel[q] = 1;
+        base = (long long)atomicAdd(reinterpret_cast<unsigned long long*>(s.chunk_off + s.Q), (unsigned long long)nch);
+        s.chunk_off[q] = base;
+        s.chunk_cnt[q] = nch;
+    }
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (int c = lane; c < nch; c += 32) {
+        s.tasks[base + c] = make_int4((int)q, leaf, c, 0);
+        if (s.task_rows != nullptr) {
+            const long long r0 = lb0 + (long long)c * CH;
+            s.task_rows[base + c] = make_int4((int)(r0 & 0xffffffffLL), (int)(r0 >> 32), (int)min((long long)CH, le0 - r0),
+                                              (int)q);
+        }
+    }
+}
+
 // ------------------------------------------------- in-search inference ----
 // Round 0 needs no prediction (bsf = +inf: the filter rule never fires).  After it,
 // a query with a finite bsf0 can only ever reach the visit-order positions
@@ -515,6 +580,10 @@ struct lf_session {
         sel_trace, sel_pre, n_sel, chunk_off, chunk_cnt, cand_d, cand_i, task_min, n_active, tasks, ea_count, qc8, qm8,
         leafo, adj, olen, pcount, pstart, pend, preq, fhist, fcur, ntiles, ptotal, pdst, ptiles, xh, xexp, round_ctr;
     lf::OrderArgs oa{};
+    bool pruned = false;             // visit orders built after round 0, only up to bsf0 * f
+    lf::Scratch orng, plb, pnode;    // pruned: leaf-bound ranges, per-group first-leaf candidates
+    int W = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> oev;   // profiling: the order phase
     bool lazy = false;               // in-search filter inference (opts.d_W1T_h instead of predictions)
     int predict_steps = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pev;   // profiling: per prediction pass
@@ -571,6 +640,9 @@ static int session_alloc(lf_session* ss) {
     if (s.want_trace) LF_CUDA(ss->order.alloc(sizeof(int) * Q * L, st));
     LF_CUDA(ss->leafo.alloc(sizeof(int) * Q * L, st));
     LF_CUDA(ss->adj.alloc(sizeof(double) * Q * L, st));
+    // NaN once: with in-search inference the visit orders leave adj unset (the pass fills
+    // every entry a walk can reach), so nothing ever reads uninitialised memory
+    LF_CUDA(cudaMemsetAsync(ss->adj.p, 0xff, sizeof(double) * Q * L, st));
     LF_CUDA(ss->olen.alloc(sizeof(int) * Q, st));
     LF_CUDA(ss->cursor.alloc(sizeof(int) * Q, st));
     LF_CUDA(ss->done.alloc(sizeof(int) * Q, st));
@@ -626,7 +698,25 @@ static int session_alloc(lf_session* ss) {
         if (pinned.p == nullptr) LF_CUDA(cudaMallocHost(&pinned.p, sizeof(int) * 8));
         ss->h_active = pinned.p;
     }
+    // pruned visit orders: with the reference's bsf_factor 1, no traces, and a tree the
+    // single-CTA order kernel takes (LF_PRUNED_ORDER=0 builds full orders first)
+    {
+        const char* e = getenv("LF_PRUNED_ORDER");
+        ss->pruned = !s.want_trace && o.bsf_factor == 1.0 && fused_order_ok(idx, Q) && !(e && strcmp(e, "0") == 0);
+    }
+    if (ss->pruned) {
+        ss->W = (Nn + 31) / 32;
+        LF_CUDA(ss->orng.alloc(sizeof(unsigned) * 2 * Q, st));
+        LF_CUDA(ss->plb.alloc(sizeof(double) * Q * ss->W, st));
+        LF_CUDA(ss->pnode.alloc(sizeof(int) * Q * ss->W, st));
+    }
     OrderArgs& oa = ss->oa;
+    oa.prune = ss->pruned ? 1 : 0;
+    oa.top_d = ss->topd.as<double>();
+    oa.top_n = ss->topn.as<int>();
+    oa.k = o.k;
+    oa.f = o.bsf_factor;
+    oa.bound = nullptr;
     oa.lbs = ss->lbs.as<double>();
     oa.gap = ss->gap.as<double>();
     oa.order = s.want_trace ? ss->order.as<int>() : nullptr;
@@ -726,7 +816,16 @@ static int session_prologue(lf_session* ss) {
         LF_CUDA(cudaEventRecord(ss->ev[0], st));
     }
     int nk = 0;
-    int rc = bounds_and_order(ss->d_q, Q, idx, ss->qsumm.as<double>(), ss->lb.as<double>(), ss->oa, st, &nk);
+    int rc;
+    if (ss->pruned) {
+        unsigned* qmax = ss->orng.as<unsigned>();
+        LF_CUDA(cudaMemsetAsync(qmax, 0, sizeof(unsigned) * Q, st));
+        LF_CUDA(cudaMemsetAsync(qmax + Q, 0xff, sizeof(unsigned) * Q, st));
+        rc = bounds_phase(ss->d_q, Q, idx, ss->qsumm.as<double>(), ss->lb.as<double>(), qmax, qmax + Q,
+                          ss->plb.as<double>(), ss->pnode.as<int>(), st, &nk);
+    } else {
+        rc = bounds_and_order(ss->d_q, Q, idx, ss->qsumm.as<double>(), ss->lb.as<double>(), ss->oa, st, &nk);
+    }
     if (rc) return rc;
     if (ss->prof) LF_CUDA(cudaEventRecord(ss->ev[1], st));     // LF_PROF_BOUNDS_MS: means + bounds + order
     ss->kernels += nk;
@@ -767,6 +866,27 @@ __global__ void bsf_out_kernel(RoundState s, double* out) {
 // One in-search prediction pass (see pairs_range_kernel), enqueued on the device only:
 // all = 1 right after round 0 (every query with a finite bsf), all = 0 for the queries
 // that asked for one (their bsf was still +inf after round 0).
+// Pruned orders: the leaf records, built right after round 0 with thr = bsf0 * f
+// (bound: the other shards' best-so-far, tightening it).
+static int order_after_round0(lf_session* ss, const double* d_bound) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ss->prof) {
+        LF_CUDA(cudaEventCreate(&e0));
+        LF_CUDA(cudaEventCreate(&e1));
+        LF_CUDA(cudaEventRecord(e0, ss->st));
+    }
+    ss->oa.bound = d_bound;
+    const unsigned* qmax = ss->orng.as<unsigned>();
+    int rc = order_phase(ss->lb.as<double>(), ss->Q, ss->idx, qmax, qmax + ss->Q, ss->oa, ss->st);
+    if (rc) return rc;
+    ++ss->kernels;
+    if (ss->prof) {
+        LF_CUDA(cudaEventRecord(e1, ss->st));
+        ss->oev.emplace_back(e0, e1);
+    }
+    return LF_OK;
+}
+
 static int predict_pass(lf_session* ss, int all) {
     RoundState& s = ss->s;
     const lf_index& idx = ss->idx;
@@ -822,7 +942,11 @@ static int round_kernels(lf_session* ss, int* counts, bool round0, cudaEvent_t* 
     LF_CUDA(cudaMemsetAsync(counts, 0, sizeof(int) * 3, st));
     if (ev) cudaEventRecord(ev[0], st);
     LF_CUDA(cudaMemsetAsync(s.chunk_off + Q, 0, sizeof(long long), st));   // the round's task counter
-    plan_warp_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s, idx);
+    if (round0 && ss->pruned)
+        first_leaf_plan_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s, idx, ss->plb.as<double>(),
+                                                                                   ss->pnode.as<int>(), ss->W);
+    else
+        plan_warp_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s, idx);
     if (ev) cudaEventRecord(ev[1], st);
     cudaError_t ce;
     // the bounded scans take m % 4 == 0 (codes zero-padded to a multiple of 64)
@@ -868,6 +992,10 @@ static int session_enqueue(lf_session* ss, const double* d_bound, double* d_bsf_
     const int64_t Q = ss->Q;
     const int slot = ss->round & 1;
     int* counts = ss->n_active.as<int>() + 4 * slot;
+    if (ss->pruned && ss->round == 1) {
+        int rc = order_after_round0(ss, d_bound);
+        if (rc) return rc;
+    }
     if (ss->lazy && (ss->round == 1 || (ss->round > 1 && s.k > 1))) {
         // after round 0 every query with a finite bsf gets its reachable pairs predicted;
         // with k > 1 a walk whose bsf was still +inf then asks later (preq), and every
@@ -938,6 +1066,7 @@ static int session_end(lf_session* ss, int64_t* out_ids, double* out_d, int64_t*
         p[LF_PROF_KERNELS] = (double)ss->kernels;
         p[LF_PROF_TOTAL_MS] = ev_ms(ss->ev[0], ss->ev[5]);
         p[LF_PROF_REFILLS] = 0.0;
+        for (auto& e : ss->oev) p[LF_PROF_BOUNDS_MS] += ev_ms(e.first, e.second);   // pruned orders
         double pms = 0.0;
         for (auto& e : ss->pev) pms += ev_ms(e.first, e.second);
         p[LF_PROF_PREDICT_MS] = pms;
@@ -957,10 +1086,11 @@ static int session_end(lf_session* ss, int64_t* out_ids, double* out_d, int64_t*
 
 static void session_free(lf_session* ss) {
     if (!ss) return;
-    for (auto& e : ss->pev) {
-        cudaEventDestroy(e.first);
-        cudaEventDestroy(e.second);
-    }
+    for (auto* v : {&ss->pev, &ss->oev})
+        for (auto& e : *v) {
+            cudaEventDestroy(e.first);
+            cudaEventDestroy(e.second);
+        }
     for (auto& e : ss->ev)
         if (e) cudaEventDestroy(e);
     for (int sl = 0; sl < 2; ++sl) {
@@ -1014,6 +1144,7 @@ static int plan_capture(lf_session* ss, cudaStream_t cs, cudaStream_t cs2, int64
     LF_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
     int rc = session_prologue(ss);
     if (!rc) rc = round_kernels(ss, counts, true, nullptr);
+    if (!rc && ss->pruned) rc = order_after_round0(ss, nullptr);
     if (!rc && ss->lazy) rc = predict_pass(ss, 1);
     cudaGraph_t g = nullptr;
     cudaGraphConditionalHandle h;

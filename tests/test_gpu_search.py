@@ -650,3 +650,26 @@ def test_search_plan_graph_identical(k, seq, cap, filt):
         np.testing.assert_array_equal(got.stats, ref.stats)
     with pytest.raises(ValueError):
         plan.run(qd[:10])
+
+
+@pytest.mark.parametrize("kind,k,seq", [("dstree", 1, False), ("dstree", 5, False), ("dstree", 1, True),
+                                        ("isax", 1, False), ("isax", 5, False), ("isax", 3, True)])
+def test_pruned_orders_identical(kind, k, seq, monkeypatch):
+    """Visit orders built after round 0 up to bsf0 * f (first leaf from lb_tile's group
+    minima, a terminal record past the threshold) == the full orders: ids, distances,
+    counters -- on trees whose node count is not a multiple of the kernels' tiles."""
+    from paper_2502_01836_b200 import build_index, search_batch
+    from paper_2502_01836_b200.isax import build_isax_index
+
+    data = lo.randwalk(30000, 128, 33)
+    t = build_isax_index(data, 400) if kind == "isax" else build_index(data, 333)
+    Q = np.concatenate([lo.noisy_queries(data, 30, nz, 77 + int(10 * nz)) for nz in (0.1, 0.4, 0.8)])
+    monkeypatch.setenv("LF_PRUNED_ORDER", "0")
+    full = search_batch(t, Q, k, sequential=seq)
+    monkeypatch.setenv("LF_PRUNED_ORDER", "1")
+    pruned = search_batch(t, Q, k, sequential=seq)
+    np.testing.assert_array_equal(pruned.ids, full.ids)
+    np.testing.assert_array_equal(pruned.dists, full.dists)
+    np.testing.assert_array_equal(pruned.stats, full.stats)
+    for i in range(0, Q.shape[0], 9):
+        assert pruned.ids[i].tolist() == [a for a, _ in lo.linear_scan(data, Q[i], k)]
