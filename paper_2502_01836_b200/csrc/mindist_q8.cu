@@ -49,9 +49,7 @@ constexpr int OFF_B = 0;
 constexpr int OFF_A = OFF_B + 2 * B_BYTES;
 constexpr int OFF_META = OFF_A + STAGES * A_BYTES;
 constexpr int OFF_EMAX = OFF_META + 2 * BN * 16;
-constexpr int N_GRP = BN / 32;                  // 32-row groups of a chunk (one TMEM load each)
-constexpr int OFF_GMETA = OFF_EMAX + 16;        // [2][N_GRP] {min alpha, max e, max s, min s}
-constexpr int OFF_BAR = OFF_GMETA + 2 * N_GRP * 16;
+constexpr int OFF_BAR = OFF_EMAX + 16;
 constexpr int N_BAR = 2 * STAGES + 2 + 2 + 2 + 2;
 constexpr int OFF_TMEM = OFF_BAR + N_BAR * 8;
 constexpr int OFF_LIST = OFF_TMEM + 16;
@@ -121,7 +119,6 @@ mindist_q8_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_consta
     uint8_t* As = smem + OFF_A;
     float4* meta = reinterpret_cast<float4*>(smem + OFF_META);        // [2][BN] {s^2 xx, s, e, alpha}
     float* emax_s = reinterpret_cast<float*>(smem + OFF_EMAX);        // [2]
-    float4* gmeta = reinterpret_cast<float4*>(smem + OFF_GMETA);      // [2][N_GRP]
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
     uint64_t* empty = full + STAGES;
     uint64_t* bfull = empty + STAGES;
@@ -175,23 +172,12 @@ mindist_q8_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_consta
                 for (int i = lane; i < BN; i += 32) {
                     const long long r = r0 + i;
                     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                    // group bounds over the valid rows of this 32-row group (i / 32)
-                    float ga = __int_as_float(0x7f800000), ge = 0.f, gs = 0.f, gsm = __int_as_float(0x7f800000);
                     if (r < le) {
                         const float4 mr = __ldg(rmeta + r);
                         const float a = mr.x * mr.x * mr.y;
                         v = make_float4(a, mr.x, mr.z, fmaf(-(1.f + 3e-5f) * mr.z, mr.z, (1.f - 2e-5f) * a));
                         em = fmaxf(em, mr.z);
-                        ga = v.w; ge = mr.z; gs = mr.x; gsm = mr.x;
                     }
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) {
-                        ga = fminf(ga, __shfl_xor_sync(0xffffffffu, ga, o));
-                        ge = fmaxf(ge, __shfl_xor_sync(0xffffffffu, ge, o));
-                        gs = fmaxf(gs, __shfl_xor_sync(0xffffffffu, gs, o));
-                        gsm = fminf(gsm, __shfl_xor_sync(0xffffffffu, gsm, o));
-                    }
-                    if (lane == 0) gmeta[bb * N_GRP + i / 32] = make_float4(ga, ge, gs, gsm);
                     meta[bb * BN + i] = v;
                 }
 #pragma unroll
@@ -350,30 +336,7 @@ mindist_q8_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_consta
                                               : -__int_as_float(0x7f800000);
                         const float gamma = vf ? 2.f * (1.f + 3e-5f) * V : 0.f;
                         unsigned bits = 0;
-                        // group pre-reject: with Dmax the group's largest code dot, no element
-                        // can pass if min_j lhs_j >= (min alpha + beta) - gamma max e exceeds
-                        // max_j cq2 D_j s_j <= cq2 Dmax s_(max or min by the sign of Dmax) --
-                        // with a 1e-5 margin on the magnitudes involved (far above fp32
-                        // rounding), so it only rejects what every element test would reject;
-                        // 16 three-way integer maxima instead of ~8 fp32 ops per element
-                        bool live = qv;
-                        if (live) {
-                            // tree of three-way maxima (depth 4, not a 15-long dependent chain)
-                            int m1[11];
-#pragma unroll
-                            for (int j = 0; j < 10; ++j) m1[j] = __vimax3_s32((int)r[3 * j], (int)r[3 * j + 1], (int)r[3 * j + 2]);
-                            m1[10] = max((int)r[30], (int)r[31]);
-                            const int m2a = __vimax3_s32(m1[0], m1[1], m1[2]), m2b = __vimax3_s32(m1[3], m1[4], m1[5]);
-                            const int m2c = __vimax3_s32(m1[6], m1[7], m1[8]), m2d = max(m1[9], m1[10]);
-                            const int dmax = max(__vimax3_s32(m2a, m2b, m2c), m2d);
-                            const float4 gm = gmeta[bb * N_GRP + grp * 4 + (c0 >> 5)];
-                            const float L = fmaf(-gamma, gm.y, gm.x + beta);
-                            const float Rm = cq2 * (float)dmax * (dmax > 0 ? gm.z : gm.w);
-                            // margin relative to the magnitudes that cancel in L - Rm
-                            const float mag = fabsf(gm.x) + fabsf(beta) + gamma * gm.y + fabsf(Rm);
-                            live = !(L - Rm > 1e-5f * mag);
-                        }
-                        if (live) {
+                        if (qv) {
                             if (c0 + 32 <= ncols) {
 #pragma unroll
                                 for (int j = 0; j < 32; ++j) {
