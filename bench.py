@@ -690,7 +690,7 @@ def run_ours(args, rank, world, device):
             if eidx.pack.path == "tc16" else "tf32 filters" if eidx.pack.path == "tc" else "f32 filters"),
         "data": (f"synthetic {'Gaussian mixture' if args.dataset == 'gmm' else 'random walk (reference law, Philox stream)'} "
                  f"generated on device, {args.n * args.m * 4 / 1e9:.1f} GB >> L2: no flush needed"),
-        "config": bench_config(args, tree, len(eidx.filters), nQ, world),
+        "config": bench_config(args, tree, len(eidx.curves) if world > 1 else len(eidx.filters), nQ, world),
         "recall_at_1": recall,
         **({f"recall_at_{args.k}": recall_k} if args.k > 1 else {}),
         "leaves_pruned_pct": 100.0 * leaves_pruned,
@@ -824,7 +824,7 @@ def make_parser():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--n", "--rows", dest="n", type=int, default=25_000_000)
-    ap.add_argument("--m", type=int, default=256)
+    ap.add_argument("--m", "--length", dest="m", type=int, default=256)
     ap.add_argument("--leaf-cap", type=int, default=10_000)
     ap.add_argument("--queries", type=int, default=1000)
     ap.add_argument("--target", type=float, default=0.99)
@@ -867,9 +867,13 @@ def main():
         with socket.socket() as sk:
             sk.bind(("127.0.0.1", 0))
             port = sk.getsockname()[1]
+        # torch.distributed.run would read the short "--n" / "--m" as ambiguous prefixes of
+        # its own options: pass their long aliases
+        alias = {"--n": "--rows", "--m": "--length"}
+        passed = [alias.get(a.split("=")[0], a.split("=")[0]) + ("=" + a.split("=", 1)[1] if "=" in a else "")
+                  if a.startswith("--") else a for a in sys.argv[1:]]
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
-               "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()),
-               *sys.argv[1:]]
+               "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *passed]
         log("launching", args.gpus, "ranks:", " ".join(cmd[1:6]))
         sys.exit(subprocess.call(cmd))
 
