@@ -283,54 +283,87 @@ __device__ __forceinline__ void put_records(const OrderArgs& o, const lf_index& 
 //      bound to its own bound (atomicMax on the bits: bounds are non-negative).
 // Global round trips: one for the leaves' bounds, one for the non-leaves', and
 // the record gathers.
-constexpr int LO_THREADS = 512;
-constexpr int LO_WARPS = LO_THREADS / 32;
-constexpr int LO_LEAF_ITEMS = 8;
-constexpr int LO_MAX_LEAVES = LO_THREADS * LO_LEAF_ITEMS;
-constexpr int LO_MAX_NI = 16;                            // node items per thread: <= 8192 nodes
-constexpr int LO_NB = 4096;                              // buckets of the counting sort
+// Two shapes of the same kernel (LoCfg):
+//   small: <= 8192 nodes / 4096 leaf slots, 512 threads, everything in shared memory;
+//   big:   <= 32768 nodes / 16384 leaf slots, 1024 threads, the bucket counts in
+//          shared memory and the staged / sorted leaves and gap bits in a per-query
+//          global scratch (L2) -- the trees of BASELINE config 5, without a library sort.
+template <bool BIG>
+struct LoCfg {
+    static constexpr int THREADS = BIG ? 1024 : 512;
+    static constexpr int WARPS = THREADS / 32;
+    static constexpr int LEAF_ITEMS = BIG ? 16 : 8;
+    static constexpr int MAX_LEAVES = THREADS * LEAF_ITEMS;
+    static constexpr int MAX_NI = BIG ? 32 : 16;          // node items per thread (flags: 32 bits)
+    static constexpr int NB = BIG ? 16384 : 4096;         // buckets of the counting sort
+    static constexpr int BIG_LIST = MAX_LEAVES / 33 + 1;
+    static constexpr int SMEM_LEAVES = BIG ? 1 : MAX_LEAVES;
+};
+constexpr int LO_THREADS = LoCfg<false>::THREADS;       // (the small shape's limits, used by callers)
+constexpr int LO_MAX_LEAVES = LoCfg<false>::MAX_LEAVES;
+constexpr int LO_MAX_NI = LoCfg<false>::MAX_NI;
 constexpr int LO_BIG = 32;
-constexpr int LO_BIG_LIST = LO_MAX_LEAVES / (LO_BIG + 1) + 1;
 
+template <bool BIG>
 struct LoSmem {
+    using C = LoCfg<BIG>;
     union {
         struct {
-            double lb[LO_MAX_LEAVES];              // staged leaves (any order)
-            int node[LO_MAX_LEAVES];
+            double lb[C::SMEM_LEAVES];             // staged leaves (any order)
+            int node[C::SMEM_LEAVES];
         } st;
-        unsigned long long gap[LO_MAX_LEAVES];     // after the sort: gap bound bits per position
+        unsigned long long gap[C::SMEM_LEAVES];    // after the sort: gap bound bits per position
     } u;
-    double lb[LO_MAX_LEAVES];                      // leaves in (lb, node id) order
-    int node[LO_MAX_LEAVES];
-    int bend[LO_NB];                               // bucket counts -> starts -> ends
-    int big[LO_BIG_LIST];
+    double lb[C::SMEM_LEAVES];                     // leaves in (lb, node id) order
+    int node[C::SMEM_LEAVES];
+    int bend[C::NB];                               // bucket counts -> starts -> ends
+    int big[C::BIG_LIST];
     int nstage, nbig;
-    double tlb_w[LO_WARPS];                        // pruned orders: the first leaf past thr
-    int tnode_w[LO_WARPS];
+    double tlb_w[C::WARPS];                        // pruned orders: the first leaf past thr
+    int tnode_w[C::WARPS];
     double tlb;
     int tnode;
+    int wsum[C::WARPS];
 };
 
+// Global scratch of the big shape, [Q][n_leaves] each.
+struct LoScratch {
+    double* st_lb;
+    int* st_node;
+    double* lb;
+    int* node;
+    unsigned long long* gap;
+};
+
+template <int NB>
 __device__ __forceinline__ int lo_bucket(double v, double lo, double scale) {
     const double k = floor((v - lo) * scale);
-    return k <= 0.0 ? 0 : (k >= (double)(LO_NB - 1) ? LO_NB - 1 : (int)k);
+    return k <= 0.0 ? 0 : (k >= (double)(NB - 1) ? NB - 1 : (int)k);
 }
 
 __device__ __forceinline__ bool lo_less(double la, int na, double lb_, int nb) {
     return la < lb_ || (la == lb_ && na < nb);
 }
 
-template <int NI>
-__global__ void __launch_bounds__(LO_THREADS, 2) leaf_order_kernel(const double* __restrict__ lb, lf_index idx,
-                                                                   const unsigned* __restrict__ qmax,
-                                                                   const unsigned* __restrict__ qmin, OrderArgs o) {
+template <int NI, bool BIG>
+__global__ void __launch_bounds__(LoCfg<BIG>::THREADS, BIG ? 1 : 2)
+    leaf_order_kernel(const double* __restrict__ lb, lf_index idx, const unsigned* __restrict__ qmax,
+                      const unsigned* __restrict__ qmin, OrderArgs o, LoScratch gs) {
+    using C = LoCfg<BIG>;
+    constexpr int T = C::THREADS, NB = C::NB;
     extern __shared__ __align__(16) uint8_t lo_smem[];
-    LoSmem& sm = *reinterpret_cast<LoSmem*>(lo_smem);
+    LoSmem<BIG>& sm = *reinterpret_cast<LoSmem<BIG>*>(lo_smem);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned below = (1u << lane) - 1u;
     const int64_t q = blockIdx.x;
     const int Nn = idx.n_nodes;
     const int Lr = idx.n_leaves;
+    // staged / sorted leaves and gap bits: shared memory, or this query's global scratch
+    double* st_lb = BIG ? gs.st_lb + q * Lr : sm.u.st.lb;
+    int* st_node = BIG ? gs.st_node + q * Lr : sm.u.st.node;
+    double* s_lb = BIG ? gs.lb + q * Lr : sm.lb;
+    int* s_node = BIG ? gs.node + q * Lr : sm.node;
+    unsigned long long* gapb = BIG ? gs.gap + q * Lr : sm.u.gap;
     const double* lbq = lb + q * Nn;
     double thr = kInf;                                   // pruned orders: leaves past thr are not records
     if (o.prune) {
@@ -340,10 +373,10 @@ __global__ void __launch_bounds__(LO_THREADS, 2) leaf_order_kernel(const double*
     }
     const double lo = (double)__uint_as_float(qmin[q]);
     const double span = fmin((double)__uint_as_float(qmax[q]), thr) - lo;
-    const double scale = (span > 0.0 && span < kInf) ? (double)(LO_NB - 1) / span : 0.0;
+    const double scale = (span > 0.0 && span < kInf) ? (double)(NB - 1) / span : 0.0;
     double tv = kInf;                                    // this thread's first leaf past thr
     int tn = 0x7fffffff;
-    for (int b = tid; b < LO_NB; b += LO_THREADS) sm.bend[b] = 0;
+    for (int b = tid; b < NB; b += T) sm.bend[b] = 0;
     if (tid == 0) {
         sm.nstage = 0;
         sm.nbig = 0;
@@ -357,12 +390,12 @@ __global__ void __launch_bounds__(LO_THREADS, 2) leaf_order_kernel(const double*
         double v[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-            const int node = (h + e) * LO_THREADS + tid;
+            const int node = (h + e) * T + tid;
             nl[e] = node < Nn ? __ldg(idx.d_node_leaf + node) : -1;
         }
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-            const int node = (h + e) * LO_THREADS + tid;
+            const int node = (h + e) * T + tid;
             v[e] = nl[e] >= 0 ? lbq[node] : 0.0;
         }
 #pragma unroll
@@ -370,9 +403,9 @@ __global__ void __launch_bounds__(LO_THREADS, 2) leaf_order_kernel(const double*
             const bool isl = nl[e] >= 0;
             if (isl) flags |= 1u << (h + e);
             const bool stage = isl && v[e] <= thr;
-            if (isl && !stage && lo_less(v[e], (h + e) * LO_THREADS + tid, tv, tn)) {
+            if (isl && !stage && lo_less(v[e], (h + e) * T + tid, tv, tn)) {
                 tv = v[e];
-                tn = (h + e) * LO_THREADS + tid;
+                tn = (h + e) * T + tid;
             }
             const unsigned bm = __ballot_sync(0xffffffffu, stage);
             if (bm == 0) continue;
@@ -381,9 +414,9 @@ __global__ void __launch_bounds__(LO_THREADS, 2) leaf_order_kernel(const double*
             base = __shfl_sync(0xffffffffu, base, 0);
             if (stage) {
                 const int pos = base + __popc(bm & below);
-                sm.u.st.lb[pos] = v[e];
-                sm.u.st.node[pos] = (h + e) * LO_THREADS + tid;
-                atomicAdd(&sm.bend[lo_bucket(v[e], lo, scale)], 1);
+                st_lb[pos] = v[e];
+                st_node[pos] = (h + e) * T + tid;
+                atomicAdd(&sm.bend[lo_bucket<NB>(v[e], lo, scale)], 1);
             }
         }
     }
@@ -401,14 +434,14 @@ __global__ void __launch_bounds__(LO_THREADS, 2) leaf_order_kernel(const double*
     if (o.prune && tid == 0) {
         double bv = kInf;
         int bn = 0x7fffffff;
-        for (int w = 0; w < LO_WARPS; ++w)
+        for (int w = 0; w < C::WARPS; ++w)
             if (lo_less(sm.tlb_w[w], sm.tnode_w[w], bv, bn)) { bv = sm.tlb_w[w]; bn = sm.tnode_w[w]; }
         sm.tlb = bv;
         sm.tnode = bn == 0x7fffffff ? -1 : bn;
     }
-    // 2. exclusive scan of the counts (8 consecutive buckets per thread), then scatter
+    // 2. exclusive scan of the counts (PT consecutive buckets per thread), then scatter
     {
-        constexpr int PT = LO_NB / LO_THREADS;
+        constexpr int PT = NB / T;
         int c[PT], sum = 0;
 #pragma unroll
         for (int j = 0; j < PT; ++j) {
@@ -421,11 +454,10 @@ __global__ void __launch_bounds__(LO_THREADS, 2) leaf_order_kernel(const double*
             const int t = __shfl_up_sync(0xffffffffu, incl, d);
             if (lane >= d) incl += t;
         }
-        __shared__ int wsum[LO_WARPS];
-        if (lane == 31) wsum[warp] = incl;
+        if (lane == 31) sm.wsum[warp] = incl;
         __syncthreads();
         int run = incl - sum;
-        for (int w = 0; w < warp; ++w) run += wsum[w];
+        for (int w = 0; w < warp; ++w) run += sm.wsum[w];
 #pragma unroll
         for (int j = 0; j < PT; ++j) {
             sm.bend[tid * PT + j] = run;
@@ -433,59 +465,59 @@ __global__ void __launch_bounds__(LO_THREADS, 2) leaf_order_kernel(const double*
         }
     }
     __syncthreads();
-    for (int p = tid; p < L; p += LO_THREADS) {
-        const double v = sm.u.st.lb[p];
-        const int pos = atomicAdd(&sm.bend[lo_bucket(v, lo, scale)], 1);   // start -> end
-        sm.lb[pos] = v;
-        sm.node[pos] = sm.u.st.node[p];
+    for (int p = tid; p < L; p += T) {
+        const double v = st_lb[p];
+        const int pos = atomicAdd(&sm.bend[lo_bucket<NB>(v, lo, scale)], 1);   // start -> end
+        s_lb[pos] = v;
+        s_node[pos] = st_node[p];
     }
     __syncthreads();
     // 3. exact (lb, node id) order inside each bucket
 #pragma unroll
-    for (int j = 0; j < LO_NB / LO_THREADS; ++j) {
-        const int b = j * LO_THREADS + tid;
+    for (int j = 0; j < NB / T; ++j) {
+        const int b = j * T + tid;
         const int s0 = b == 0 ? 0 : sm.bend[b - 1], e0 = sm.bend[b];
         if (e0 - s0 > LO_BIG) {
             const int t = atomicAdd(&sm.nbig, 1);
-            if (t < LO_BIG_LIST) sm.big[t] = b;
+            if (t < C::BIG_LIST) sm.big[t] = b;
             continue;
         }
         for (int a = s0 + 1; a < e0; ++a) {
-            const double la = sm.lb[a];
-            const int na = sm.node[a];
+            const double la = s_lb[a];
+            const int na = s_node[a];
             int c = a - 1;
-            while (c >= s0 && !lo_less(sm.lb[c], sm.node[c], la, na)) {
-                sm.lb[c + 1] = sm.lb[c];
-                sm.node[c + 1] = sm.node[c];
+            while (c >= s0 && !lo_less(s_lb[c], s_node[c], la, na)) {
+                s_lb[c + 1] = s_lb[c];
+                s_node[c + 1] = s_node[c];
                 --c;
             }
-            sm.lb[c + 1] = la;
-            sm.node[c + 1] = na;
+            s_lb[c + 1] = la;
+            s_node[c + 1] = na;
         }
     }
     __syncthreads();
     if (sm.nbig > 0) {                                   // rare: a warp ranks each big bucket
-        for (int t = warp; t < sm.nbig; t += LO_WARPS) {
+        for (int t = warp; t < sm.nbig; t += C::WARPS) {
             const int b = sm.big[t];
             const int s0 = b == 0 ? 0 : sm.bend[b - 1], e0 = sm.bend[b];
             for (int i = s0 + lane; i < e0; i += 32) {
-                const double li = sm.lb[i];
-                const int ni = sm.node[i];
+                const double li = s_lb[i];
+                const int ni = s_node[i];
                 int r = 0;
-                for (int j2 = s0; j2 < e0; ++j2) r += lo_less(sm.lb[j2], sm.node[j2], li, ni);
-                sm.u.st.lb[s0 + r] = li;                 // the staging area is free now
-                sm.u.st.node[s0 + r] = ni;
+                for (int j2 = s0; j2 < e0; ++j2) r += lo_less(s_lb[j2], s_node[j2], li, ni);
+                st_lb[s0 + r] = li;                      // the staging area is free now
+                st_node[s0 + r] = ni;
             }
             __syncwarp();
             for (int i = s0 + lane; i < e0; i += 32) {
-                sm.lb[i] = sm.u.st.lb[i];
-                sm.node[i] = sm.u.st.node[i];
+                s_lb[i] = st_lb[i];
+                s_node[i] = st_node[i];
             }
         }
         __syncthreads();
     }
     const bool has_term = o.prune && sm.tnode >= 0;      // (visible: written before the last barriers)
-    for (int p = tid; p < L + (has_term ? 1 : 0); p += LO_THREADS) sm.u.gap[p] = 0ull;
+    for (int p = tid; p < L + (has_term ? 1 : 0); p += T) gapb[p] = 0ull;
     __syncthreads();
     // 4. gap bounds of the non-leaf nodes
 #pragma unroll
@@ -493,42 +525,42 @@ __global__ void __launch_bounds__(LO_THREADS, 2) leaf_order_kernel(const double*
         double v[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-            const int node = (h + e) * LO_THREADS + tid;
+            const int node = (h + e) * T + tid;
             v[e] = (node < Nn && !((flags >> (h + e)) & 1u)) ? lbq[node] : -1.0;
         }
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
             if (v[e] < 0.0) continue;
-            const int node = (h + e) * LO_THREADS + tid;
+            const int node = (h + e) * T + tid;
             if (v[e] > thr && !(has_term && lo_less(v[e], node, sm.tlb, sm.tnode))) continue;   // past the end
-            const int b = lo_bucket(v[e], lo, scale);
+            const int b = lo_bucket<NB>(v[e], lo, scale);
             int p = b == 0 ? 0 : sm.bend[b - 1];
             const int e0 = sm.bend[b];
-            while (p < e0 && lo_less(sm.lb[p], sm.node[p], v[e], node)) ++p;
+            while (p < e0 && lo_less(s_lb[p], s_node[p], v[e], node)) ++p;
             if (p < L || (p == L && has_term))
-                atomicMax(&sm.u.gap[p], (unsigned long long)__double_as_longlong(v[e]));
+                atomicMax(&gapb[p], (unsigned long long)__double_as_longlong(v[e]));
         }
     }
     __syncthreads();
     // 5. records, 4 positions per thread at a time
 #pragma unroll
-    for (int h = 0; h < LO_LEAF_ITEMS; h += 4) {
+    for (int h = 0; h < C::LEAF_ITEMS; h += 4) {
         int p[4], node[4];
         double lbv[4], gv[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            p[e] = (h + e) * LO_THREADS + tid;
+            p[e] = (h + e) * T + tid;
             const bool ok = p[e] < L;
-            node[e] = ok ? sm.node[p[e]] : 0;
-            lbv[e] = ok ? sm.lb[p[e]] : 0.0;
-            gv[e] = ok ? __longlong_as_double((long long)sm.u.gap[p[e]]) : 0.0;
+            node[e] = ok ? s_node[p[e]] : 0;
+            lbv[e] = ok ? s_lb[p[e]] : 0.0;
+            gv[e] = ok ? __longlong_as_double((long long)gapb[p[e]]) : 0.0;
         }
         put_records<4>(o, idx, q, Lr, L, p, node, lbv, gv);
     }
     if (tid == 0) {
         if (has_term) {                                  // the terminal record
             const int p1[1] = {L}, n1[1] = {sm.tnode};
-            const double l1[1] = {sm.tlb}, g1[1] = {__longlong_as_double((long long)sm.u.gap[L])};
+            const double l1[1] = {sm.tlb}, g1[1] = {__longlong_as_double((long long)gapb[L])};
             put_records<1>(o, idx, q, Lr, L + 1, p1, n1, l1, g1);
         }
         o.olen[q] = L + (has_term ? 1 : 0);
@@ -580,19 +612,36 @@ __global__ void leaf_records_kernel(const double* __restrict__ slb, const int* _
     if (lane == 0) o.olen[q] = outp;
 }
 
-template <int NI>
+template <int NI, bool BIG>
 static int launch_leaf_order(const double* d_lb, int64_t Q, const lf_index& idx, const unsigned* qmax,
                              const unsigned* qmin, const OrderArgs& oa, cudaStream_t st) {
-    const int bytes = (int)sizeof(LoSmem);
-    LF_CUDA(smem_optin(leaf_order_kernel<NI>, bytes));
-    leaf_order_kernel<NI><<<(unsigned)Q, LO_THREADS, bytes, st>>>(d_lb, idx, qmax, qmin, oa);
+    const int bytes = (int)sizeof(LoSmem<BIG>);
+    LF_CUDA(smem_optin(leaf_order_kernel<NI, BIG>, bytes));
+    Scratch g;                                           // big shape: per-query staging in L2
+    LoScratch gs{};
+    if (BIG) {
+        const size_t per = (size_t)Q * idx.n_leaves;
+        LF_CUDA(g.alloc(per * (8 + 4 + 8 + 4 + 8), st));
+        gs.st_lb = g.as<double>();
+        gs.lb = gs.st_lb + per;
+        gs.gap = reinterpret_cast<unsigned long long*>(gs.lb + per);
+        gs.st_node = reinterpret_cast<int*>(gs.gap + per);
+        gs.node = gs.st_node + per;
+    }
+    leaf_order_kernel<NI, BIG><<<(unsigned)Q, LoCfg<BIG>::THREADS, bytes, st>>>(d_lb, idx, qmax, qmin, oa, gs);
     LF_CUDA(cudaGetLastError());
     return LF_OK;
 }
 
 bool fused_order_ok(const lf_index& idx, int64_t Q) {
-    return idx.n_nodes <= LO_THREADS * LO_MAX_NI && idx.n_leaves <= LO_MAX_LEAVES && idx.n_seg <= LBT_SEG &&
+    using B = LoCfg<true>;
+    return idx.n_nodes <= B::THREADS * B::MAX_NI && idx.n_leaves <= B::MAX_LEAVES && idx.n_seg <= LBT_SEG &&
            (Q + LBT_Q - 1) / LBT_Q <= 65535 && Q <= 0x7fffffff;
+}
+
+static bool small_order(const lf_index& idx) {
+    using S = LoCfg<false>;
+    return idx.n_nodes <= S::THREADS * S::MAX_NI && idx.n_leaves <= S::MAX_LEAVES;
 }
 
 int bounds_phase(const float* d_q, int64_t Q, const lf_index& idx, double* d_qsumm, double* d_lb, unsigned* qmax,
@@ -607,8 +656,12 @@ int bounds_phase(const float* d_q, int64_t Q, const lf_index& idx, double* d_qsu
 
 int order_phase(const double* d_lb, int64_t Q, const lf_index& idx, const unsigned* qmax, const unsigned* qmin,
                 const OrderArgs& oa, cudaStream_t st) {
-    if (idx.n_nodes <= LO_THREADS * 8) return launch_leaf_order<8>(d_lb, Q, idx, qmax, qmin, oa, st);
-    return launch_leaf_order<16>(d_lb, Q, idx, qmax, qmin, oa, st);
+    if (small_order(idx)) {
+        if (idx.n_nodes <= LO_THREADS * 8) return launch_leaf_order<8, false>(d_lb, Q, idx, qmax, qmin, oa, st);
+        return launch_leaf_order<16, false>(d_lb, Q, idx, qmax, qmin, oa, st);
+    }
+    if (idx.n_nodes <= LoCfg<true>::THREADS * 16) return launch_leaf_order<16, true>(d_lb, Q, idx, qmax, qmin, oa, st);
+    return launch_leaf_order<32, true>(d_lb, Q, idx, qmax, qmin, oa, st);
 }
 
 // Segment means + node bounds + per-query leaf records: the bound matrix
@@ -631,8 +684,7 @@ int bounds_and_order(const float* d_q, int64_t Q, const lf_index& idx, double* d
     if (kernels) *kernels += 2;
     if (fused) {
         if (kernels) *kernels += 1;
-        if (n <= LO_THREADS * 8) return launch_leaf_order<8>(d_lb, Q, idx, qmax, qmin, oa, st);
-        return launch_leaf_order<16>(d_lb, Q, idx, qmax, qmin, oa, st);
+        return order_phase(d_lb, Q, idx, qmax, qmin, oa, st);
     }
     Scratch slb, sord;
     LF_CUDA(slb.alloc(sizeof(double) * Q * n, st));

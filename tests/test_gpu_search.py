@@ -336,8 +336,9 @@ def test_early_abandon_identical(m, k):
 
 
 def test_large_tree_unfused_order():
-    """> 8192 nodes: bounds kernel + CUB segmented sort instead of the fused block
-    sort; visit order, results and counters still equal the oracle's."""
+    """> 8192 nodes: the leaf order's big shape (1,024 threads, staging in a global
+    scratch) instead of the shared-memory one; visit order, results and counters
+    still equal the oracle's."""
     from paper_2502_01836_b200 import build_index, search_batch
 
     data = lo.randwalk(60000, 16, 12)
@@ -653,7 +654,8 @@ def test_search_plan_graph_identical(k, seq, cap, filt):
 
 
 @pytest.mark.parametrize("kind,k,seq", [("dstree", 1, False), ("dstree", 5, False), ("dstree", 1, True),
-                                        ("isax", 1, False), ("isax", 5, False), ("isax", 3, True)])
+                                        ("isax", 1, False), ("isax", 5, False), ("isax", 3, True),
+                                        ("big", 1, False), ("big", 4, True)])
 def test_pruned_orders_identical(kind, k, seq, monkeypatch):
     """Visit orders built after round 0 up to bsf0 * f (first leaf from lb_tile's group
     minima, a terminal record past the threshold) == the full orders: ids, distances,
@@ -661,8 +663,11 @@ def test_pruned_orders_identical(kind, k, seq, monkeypatch):
     from paper_2502_01836_b200 import build_index, search_batch
     from paper_2502_01836_b200.isax import build_isax_index
 
-    data = lo.randwalk(30000, 128, 33)
-    t = build_isax_index(data, 400) if kind == "isax" else build_index(data, 333)
+    data = lo.randwalk(120000 if kind == "big" else 30000, 32 if kind == "big" else 128, 33)
+    # "big": > 8,192 nodes -- the leaf order's global-scratch shape
+    t = build_isax_index(data, 400) if kind == "isax" else build_index(data, 18 if kind == "big" else 333)
+    if kind == "big":
+        assert 8192 < t.n_nodes <= 32768, t.n_nodes
     Q = np.concatenate([lo.noisy_queries(data, 30, nz, 77 + int(10 * nz)) for nz in (0.1, 0.4, 0.8)])
     monkeypatch.setenv("LF_PRUNED_ORDER", "0")
     full = search_batch(t, Q, k, sequential=seq)
