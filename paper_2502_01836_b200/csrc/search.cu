@@ -426,6 +426,7 @@ int pair_tiles(const int* d_hist, int F, int* d_fcur, int4* d_tiles, int* d_ntil
 // round's candidates (each series is scanned at most once per query, so all
 // (d, id) pairs are distinct and repeated "next larger than the last pick"
 // selection is exact).  Reads top_* (round-start state), writes top_*_out.
+constexpr int MERGE_KMAX = 16;                 // k up to this: register top-k per lane
 __global__ void merge_kernel(RoundState s) {
     const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -479,6 +480,67 @@ __global__ void merge_kernel(RoundState s) {
             s.top_i[q] = bi;
             s.top_n[q] = 1;
         }
+        return;
+    }
+    if (s.k <= MERGE_KMAX) {
+        // one pass: every lane keeps the k best of its strided share in registers
+        // (sorted; candidates and the running top-k alike), then k warp-wide pops
+        double ld[MERGE_KMAX];
+        long long li[MERGE_KMAX];
+#pragma unroll
+        for (int j = 0; j < MERGE_KMAX; ++j) { ld[j] = kInf; li[j] = LLONG_MAX; }
+        const long long total = (long long)tn + nc;
+        double kd = kInf;                                  // the k-th kept (ld[k - 1], kept in registers)
+        long long ki = LLONG_MAX;
+        for (long long i = lane; i < total; i += 32) {
+            const bool top = i < tn;
+            const long long id = top ? ti[i] : ci[i - tn];
+            if (id < 0) continue;
+            const double d = top ? td[i] : cd[i - tn];
+            if (!pair_less(d, id, kd, ki)) continue;
+            // insert (d, id): the sorted list's "greater than (d, id)" flags are monotone,
+            // so slot j takes slot j-1's entry or (d, id) -- static indices only
+            bool gt[MERGE_KMAX];
+#pragma unroll
+            for (int j = 0; j < MERGE_KMAX; ++j) gt[j] = j < s.k && pair_less(d, id, ld[j], li[j]);
+#pragma unroll
+            for (int j = MERGE_KMAX - 1; j > 0; --j)
+                if (gt[j]) {
+                    ld[j] = gt[j - 1] ? ld[j - 1] : d;
+                    li[j] = gt[j - 1] ? li[j - 1] : id;
+                }
+            if (gt[0]) { ld[0] = d; li[0] = id; }
+            kd = -1.0;                                     // the largest of the first k (sorted: ld[k-1])
+            ki = -1;
+#pragma unroll
+            for (int j = 0; j < MERGE_KMAX; ++j)
+                if (j < s.k && pair_less(kd, ki, ld[j], li[j])) { kd = ld[j]; ki = li[j]; }
+        }
+        int filled = 0;
+        for (int sel = 0; sel < s.k; ++sel) {
+            double bd = ld[0];
+            long long bi = li[0];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double xd = __shfl_xor_sync(0xffffffffu, bd, o);
+                const long long xi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (pair_less(xd, xi, bd, bi)) { bd = xd; bi = xi; }
+            }
+            if (bi == LLONG_MAX) continue;             // (every later pop is empty too)
+            if (lane == 0) { od[sel] = bd; oi[sel] = bi; }
+            ++filled;
+            if (li[0] == bi && ld[0] == bd) {          // the owner pops its head
+#pragma unroll
+                for (int j = 0; j + 1 < MERGE_KMAX; ++j) { ld[j] = ld[j + 1]; li[j] = li[j + 1]; }
+                ld[MERGE_KMAX - 1] = kInf;
+                li[MERGE_KMAX - 1] = LLONG_MAX;
+            }
+        }
+        __syncwarp();
+        double* wd = s.top_d + q * s.k;
+        long long* wi = s.top_i + q * s.k;
+        for (int i = lane; i < filled; i += 32) { wd[i] = od[i]; wi[i] = oi[i]; }
+        if (lane == 0) s.top_n[q] = filled;
         return;
     }
     double last_d = -1.0;
