@@ -156,6 +156,20 @@ __global__ void plan_warp_kernel(RoundState s, lf_index idx) {
             if (quota) {
                 cur += end;
                 quota_hit = true;
+                // the walk's next record already breaks at this round's bound; bsf only
+                // shrinks, so the next round would stop there with the same counters:
+                // stop now (saves the round that only finds every walk done)
+                if (!s.want_trace && cur < len) {
+                    const double plb = end < 32 ? __shfl_sync(0xffffffffu, lb_c, end) : __shfl_sync(0xffffffffu, lb_n, 0);
+                    const double pgp = end < 32 ? __shfl_sync(0xffffffffu, gp_c, end) : __shfl_sync(0xffffffffu, gp_n, 0);
+                    if (pgp > thr || plb > thr) {
+                        if (!(pgp > thr)) {               // a leaf: visited + lb-pruned (tree.py:261-269)
+                            c_vis += 1;
+                            c_lbp += 1;
+                        }
+                        fin = true;
+                    }
+                }
             } else if (first_brk < 32 && first_brk < len - cur) {
                 // the break entry: a leaf counts as visited + lb-pruned (tree.py:261-269),
                 // an internal node (gap) ends the walk uncounted
@@ -662,6 +676,8 @@ struct lf_session {
     long long kernels = 0;
     cudaEvent_t ev[6] = {};
     bool prof = false;
+    cudaStream_t st2 = nullptr;      // prologue branch: query codes, concurrent with the bounds
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
 };
 
 namespace lf {
@@ -725,6 +741,9 @@ static int session_alloc(lf_session* ss) {
     LF_CUDA(ss->task_min.alloc(sizeof(double) * (s.want_trace ? max_tasks : 1), st));
     LF_CUDA(ss->n_active.alloc(sizeof(int) * 8, st));   // [2 slots][active, refill, predict requests, -]
     LF_CUDA(ss->round_ctr.alloc(sizeof(int), st));
+    LF_CUDA(cudaStreamCreateWithFlags(&ss->st2, cudaStreamNonBlocking));
+    LF_CUDA(cudaEventCreateWithFlags(&ss->fork_ev, cudaEventDisableTiming));
+    LF_CUDA(cudaEventCreateWithFlags(&ss->join_ev, cudaEventDisableTiming));
     for (int sl = 0; sl < 2; ++sl) {
         LF_CUDA(cudaEventCreateWithFlags(&ss->done_ev[sl], cudaEventDisableTiming));
         if (o.h_profile)
@@ -861,15 +880,35 @@ static int session_prologue(lf_session* ss) {
     cudaStream_t st = ss->st;
     const int64_t Q = ss->Q;
     RoundState& s = ss->s;
+    // the query-side codes (fp16 rows, projected and int8 codes) do not depend on the
+    // bounds: a second stream computes them while the bound matrix is built (a parallel
+    // branch of the plan's graph), joined before round 0
+    cudaStream_t st2 = ss->st2;
+    LF_CUDA(cudaEventRecord(ss->fork_ev, st));
+    LF_CUDA(cudaStreamWaitEvent(st2, ss->fork_ev, 0));
+    if (ss->lazy) {
+        int rc = rows_to_f16(ss->d_q, Q, idx.m, ss->xh.as<__half>(), ss->xexp.as<int>(), st2);
+        if (rc) return rc;
+        ++ss->kernels;
+    }
+    if (ss->pq) {
+        LF_CUDA(cudaMemsetAsync(ss->pq_qbest.p, 0x7f, sizeof(unsigned) * Q, st2));   // 3.4e38: above any distance
+        LF_CUDA(launch_project_queries(ss->d_q, Q, idx, ss->qcp.as<int8_t>(), ss->qmp.as<float4>(), st2));
+        ++ss->kernels;
+    }
+    if (ss->q8) {
+        const int MP = (idx.m + 255) / 256 * 256;
+        int rq = quantize_queries(ss->d_q, Q, idx.m, MP, ss->qc8.as<int8_t>(), ss->qm8.as<float4>(), st2);
+        if (rq) return rq;
+        ++ss->kernels;
+    }
+    LF_CUDA(cudaEventRecord(ss->join_ev, st2));
     LF_CUDA(cudaMemsetAsync(ss->ea_count.p, 0, sizeof(unsigned long long) * 4, st));
     LF_CUDA(cudaMemsetAsync(ss->round_ctr.p, 0, sizeof(int), st));
     if (ss->lazy) {
         LF_CUDA(cudaMemsetAsync(ss->pcount.p, 0, sizeof(int) * Q, st));
         LF_CUDA(cudaMemsetAsync(ss->preq.p, 0, sizeof(int) * Q, st));
         LF_CUDA(cudaMemsetAsync(ss->ptotal.p, 0, sizeof(unsigned long long), st));
-        int rc = rows_to_f16(ss->d_q, Q, idx.m, ss->xh.as<__half>(), ss->xexp.as<int>(), st);
-        if (rc) return rc;
-        ++ss->kernels;
     }
     if (o.h_profile) {
         ss->prof = true;
@@ -894,17 +933,7 @@ static int session_prologue(lf_session* ss) {
     init_state_kernel<<<(unsigned)((Q + 127) / 128), 128, 0, st>>>(s);
     LF_CUDA(cudaGetLastError());
     ++ss->kernels;
-    if (ss->pq) {
-        LF_CUDA(cudaMemsetAsync(ss->pq_qbest.p, 0x7f, sizeof(unsigned) * Q, st));   // 3.4e38: above any distance
-        LF_CUDA(launch_project_queries(ss->d_q, Q, idx, ss->qcp.as<int8_t>(), ss->qmp.as<float4>(), st));
-        ++ss->kernels;
-    }
-    if (ss->q8) {
-        const int MP = (idx.m + 255) / 256 * 256;
-        int rq = quantize_queries(ss->d_q, Q, idx.m, MP, ss->qc8.as<int8_t>(), ss->qm8.as<float4>(), st);
-        if (rq) return rq;
-        ++ss->kernels;
-    }
+    LF_CUDA(cudaStreamWaitEvent(st, ss->join_ev, 0));
     if (ss->prof) LF_CUDA(cudaEventRecord(ss->ev[2], st));
     return LF_OK;
 }
@@ -1148,6 +1177,12 @@ static int session_end(lf_session* ss, int64_t* out_ids, double* out_d, int64_t*
 
 static void session_free(lf_session* ss) {
     if (!ss) return;
+    if (ss->fork_ev) cudaEventDestroy(ss->fork_ev);
+    if (ss->join_ev) cudaEventDestroy(ss->join_ev);
+    if (ss->st2) {
+        cudaStreamSynchronize(ss->st2);
+        cudaStreamDestroy(ss->st2);
+    }
     for (auto* v : {&ss->pev, &ss->oev})
         for (auto& e : *v) {
             cudaEventDestroy(e.first);
