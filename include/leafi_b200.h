@@ -277,7 +277,7 @@ int lf_filter_rows_to_f16(const float* d_X, int64_t rows, int32_t m, uint16_t* d
  * pairs are bucketed by filter, their query rows gathered, and one tcgen05 tile
  * list evaluates them -- bit-identical to the same pairs of lf_filter_predict_tc
  * (_tc) / lf_filter_predict_f16 (_f16: the fp16 pack, query rows gathered straight
- * from the fp16 query matrix with TMA gather4 -- the kernel of lf_search's in-search
+ * from the fp16 query matrix with coalesced cp.async -- the kernel of lf_search's in-search
  * inference).  d_out [P] (fp64 of the fp32 prediction).
  */
 int lf_filter_predict_pairs_f16(const float* d_queries, int64_t Q, int32_t m, const uint16_t* d_W1T_h,

@@ -91,7 +91,8 @@ __global__ void lb_kernel(const double* __restrict__ qsumm, int64_t Q, int n_seg
 // envelopes are read from L2 once per QT queries instead of once per query.
 // Same arithmetic as lb_kernel (bit-identical bounds).  With qmax / qmin set it
 // also records, per query, the range of its leaf bounds as float bits (rounded:
-// the leaf-order kernel only needs it to spread its buckets).
+// the leaf-order kernel only needs it to spread its buckets); qmin holds the
+// complement of the minimum's bits.
 constexpr int LBT_NODES = 128;
 constexpr int LBT_Q = 16;
 constexpr int LBT_SEG = 8;
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(LBT_NODES, MODE == 2 ? 2 : 4)
             const unsigned lo = __reduce_min_sync(0xffffffffu, isl ? fb : 0xffffffffu);
             if (lane == 0 && lo != 0xffffffffu) {
                 atomicMax(qmax + q0 + qq, hi);
-                atomicMin(qmin + q0 + qq, lo);
+                atomicMax(qmin + q0 + qq, ~lo);     // complemented: both start at 0, one memset
             }
             if (plb != nullptr) {       // the warp's minimum (lb, node) over its leaves, exactly:
                 // bound bits order like the non-negative values; three integer reductions
@@ -188,8 +189,12 @@ int launch_bounds(const float* d_q, int64_t Q, const lf_index& idx, const double
     if (n_env == 0) return LF_OK;
     if (idx.n_seg <= LBT_SEG && (Q + LBT_Q - 1) / LBT_Q <= 65535) {
         if (d_qmax != nullptr) {
-            LF_CUDA(cudaMemsetAsync(d_qmax, 0, sizeof(unsigned) * Q, st));
-            LF_CUDA(cudaMemsetAsync(d_qmin, 0xff, sizeof(unsigned) * Q, st));
+            if (d_qmin == d_qmax + Q) {
+                LF_CUDA(cudaMemsetAsync(d_qmax, 0, sizeof(unsigned) * 2 * Q, st));
+            } else {
+                LF_CUDA(cudaMemsetAsync(d_qmax, 0, sizeof(unsigned) * Q, st));
+                LF_CUDA(cudaMemsetAsync(d_qmin, 0, sizeof(unsigned) * Q, st));
+            }
         }
         dim3 grid((unsigned)((n_env + LBT_NODES - 1) / LBT_NODES), (unsigned)((Q + LBT_Q - 1) / LBT_Q));
 #define LF_TILE(M) lb_tile_kernel<M><<<grid, LBT_NODES, 0, st>>>(d_qsumm, Q, idx.n_seg, idx, env_min, env_max, \
@@ -371,7 +376,7 @@ __global__ void __launch_bounds__(LoCfg<BIG>::THREADS, BIG ? 1 : 2)
         if (o.bound != nullptr) b = fmin(b, o.bound[q]);
         thr = b * o.f;
     }
-    const double lo = (double)__uint_as_float(qmin[q]);
+    const double lo = (double)__uint_as_float(~qmin[q]);
     const double span = fmin((double)__uint_as_float(qmax[q]), thr) - lo;
     const double scale = (span > 0.0 && span < kInf) ? (double)(NB - 1) / span : 0.0;
     double tv = kInf;                                    // this thread's first leaf past thr

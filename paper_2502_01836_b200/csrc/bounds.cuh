@@ -5,7 +5,8 @@
 
 namespace lf {
 // mode 0 / 1: the reference's search / traingen bound; 2: EAPCA (sd_min / sd_max).
-// d_qmax / d_qmin (nullable, [Q]): per query the range of its leaf bounds as float bits.
+// d_qmax / d_qmin (nullable, [Q]): per query the range of its leaf bounds as float bits
+// (d_qmin complemented, so both are zero-initialised here).
 int launch_bounds(const float* d_q, int64_t Q, const lf_index& idx, const double* env_min,
                   const double* env_max, int n_env, int mode, double* d_qsumm, double* d_lb,
                   cudaStream_t st, unsigned* d_qmax = nullptr, unsigned* d_qmin = nullptr,

@@ -560,7 +560,7 @@ __global__ void pair_bucket_kernel(const float* __restrict__ queries, int m, con
     for (int c = lane; c < m; c += 32) rows[(int64_t)slot * m + c] = src[c];
 }
 }  // namespace tc
-int pair_tiles(const int* d_hist, int F, int* d_fcur, int4* d_tiles, int* d_ntiles, cudaStream_t st);
+int pair_tiles(const int* d_hist, int F, int* d_fcur, int4* d_tiles, int* d_ntiles, cudaStream_t st, int stride = 0);
 }  // namespace lf
 
 extern "C" int lf_filter_predict_pairs_tc(const float* d_queries, int32_t m, const float* d_W1T, const float* d_b1,

@@ -317,7 +317,7 @@ __global__ void first_leaf_plan_kernel(RoundState s, lf_index idx, const double*
 // the cascade may evaluate (tree.py:277-286).  One pass predicts them all: pass 1
 // counts them per filter, a single-CTA scan turns the counts into filter buckets and
 // a 128-pair tile list, pass 2 fills the buckets, and filter_reach_f16 (tcgen05
-// kind::f16, the dense kernel's arithmetic, query rows gathered with TMA gather4)
+// kind::f16, the dense kernel's arithmetic, query rows gathered with cp.async)
 // writes pred - offset into the records.  On the bench workload that is 0.42M pairs
 // instead of the 4.1M of a dense pass.  All on the device: rounds stay pipelined.
 // Thread per query: the range of the visit order the walk can still reach.  The
@@ -357,7 +357,8 @@ constexpr int PAIR_SPAN = 256;
 template <bool FILL>
 __global__ void pairs_pos_kernel(int64_t Q, int Lr, const int* __restrict__ pstart, const int* __restrict__ pair_end,
                                  const int* __restrict__ leafo, const int* __restrict__ leaf_filter,
-                                 int* __restrict__ cnt, int2* __restrict__ dst, unsigned long long* total) {
+                                 int* __restrict__ cnt, int2* __restrict__ dst, unsigned long long* total,
+                                 int stride) {
     const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int spans = (Lr + PAIR_SPAN - 1) / PAIR_SPAN;
@@ -372,12 +373,12 @@ __global__ void pairs_pos_kernel(int64_t Q, int Lr, const int* __restrict__ psta
         const int rec = lrec[k];
         if (rec >= 0 && (rec & LF_REC_HASF)) {
             const int f = leaf_filter[rec & LF_REC_LEAF];
-            if (FILL) dst[atomicAdd(&cnt[f], 1)] = make_int2((int)q, k);
+            if (FILL) dst[(int64_t)f * stride + atomicAdd(&cnt[f], 1)] = make_int2((int)q, k);
             else atomicAdd(&cnt[f], 1);
             ++n;
         }
     }
-    if (!FILL && total) {
+    if (total) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
         if (lane == 0 && n) atomicAdd(total, (unsigned long long)n);
@@ -390,7 +391,7 @@ __global__ void pairs_pos_kernel(int64_t Q, int Lr, const int* __restrict__ psta
 constexpr int PT_THREADS = 1024, PT_ITEMS = 8;
 __global__ void __launch_bounds__(PT_THREADS) pair_tiles_kernel(const int* __restrict__ fhist, int F,
                                                                 int* __restrict__ fcur, int4* __restrict__ tiles,
-                                                                int* __restrict__ ntiles) {
+                                                                int* __restrict__ ntiles, int stride) {
     using Scan = cub::BlockScan<int2, PT_THREADS>;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ int2 carry;
@@ -416,8 +417,10 @@ __global__ void __launch_bounds__(PT_THREADS) pair_tiles_kernel(const int* __res
         for (int i = 0; i < PT_ITEMS; ++i) {
             const int f = base + threadIdx.x * PT_ITEMS + i;
             if (f < F) {
-                fcur[f] = p0;
-                for (int t = 0; t * 128 < h[i]; ++t) tiles[t0 + t] = make_int4(f, p0 + 128 * t, min(128, h[i] - 128 * t), 0);
+                // stride > 0: the buckets were filled in place, bucket f at f * stride
+                const int b0 = stride > 0 ? f * stride : p0;
+                if (stride == 0) fcur[f] = p0;
+                for (int t = 0; t * 128 < h[i]; ++t) tiles[t0 + t] = make_int4(f, b0 + 128 * t, min(128, h[i] - 128 * t), 0);
             }
             p0 += h[i];
             t0 += (h[i] + 127) / 128;
@@ -429,8 +432,8 @@ __global__ void __launch_bounds__(PT_THREADS) pair_tiles_kernel(const int* __res
     if (threadIdx.x == 0) *ntiles = carry.y;
 }
 
-int pair_tiles(const int* d_hist, int F, int* d_fcur, int4* d_tiles, int* d_ntiles, cudaStream_t st) {
-    pair_tiles_kernel<<<1, PT_THREADS, 0, st>>>(d_hist, F, d_fcur, d_tiles, d_ntiles);
+int pair_tiles(const int* d_hist, int F, int* d_fcur, int4* d_tiles, int* d_ntiles, cudaStream_t st, int stride) {
+    pair_tiles_kernel<<<1, PT_THREADS, 0, st>>>(d_hist, F, d_fcur, d_tiles, d_ntiles, stride);
     LF_CUDA(cudaGetLastError());
     return LF_OK;
 }
@@ -919,9 +922,7 @@ static int session_prologue(lf_session* ss) {
     int nk = 0;
     int rc;
     if (ss->pruned) {
-        unsigned* qmax = ss->orng.as<unsigned>();
-        LF_CUDA(cudaMemsetAsync(qmax, 0, sizeof(unsigned) * Q, st));
-        LF_CUDA(cudaMemsetAsync(qmax + Q, 0xff, sizeof(unsigned) * Q, st));
+        unsigned* qmax = ss->orng.as<unsigned>();     // zeroed by launch_bounds
         rc = bounds_phase(ss->d_q, Q, idx, ss->qsumm.as<double>(), ss->lb.as<double>(), qmax, qmax + Q,
                           ss->plb.as<double>(), ss->pnode.as<int>(), st, &nk);
     } else {
@@ -997,15 +998,15 @@ static int predict_pass(lf_session* ss, int all) {
     LF_CUDA(cudaGetLastError());
     const int64_t Lr = idx.n_leaves;
     const unsigned pgrid = (unsigned)((Q * ((Lr + PAIR_SPAN - 1) / PAIR_SPAN) * 32 + 255) / 256);
-    pairs_pos_kernel<false><<<pgrid, 256, 0, st>>>(Q, (int)Lr, ss->pstart.as<int>(), ss->pend.as<int>(), s.leafo,
-                                                   idx.d_leaf_filter, ss->fhist.as<int>(), nullptr,
-                                                   ss->prof ? ss->ptotal.as<unsigned long long>() : nullptr);
-    LF_CUDA(cudaGetLastError());
-    int rc = pair_tiles(ss->fhist.as<int>(), F, ss->fcur.as<int>(), ss->ptiles.as<int4>(), ss->ntiles.as<int>(), st);
-    if (rc) return rc;
+    // each query contributes at most one pair per filter: bucket f is filled in place at
+    // f * Q (no counting pass), then the tile list is built from the bucket sizes
     pairs_pos_kernel<true><<<pgrid, 256, 0, st>>>(Q, (int)Lr, ss->pstart.as<int>(), ss->pend.as<int>(), s.leafo,
-                                                  idx.d_leaf_filter, ss->fcur.as<int>(), ss->pdst.as<int2>(), nullptr);
+                                                  idx.d_leaf_filter, ss->fhist.as<int>(), ss->pdst.as<int2>(),
+                                                  ss->prof ? ss->ptotal.as<unsigned long long>() : nullptr, (int)Q);
     LF_CUDA(cudaGetLastError());
+    int rc = pair_tiles(ss->fhist.as<int>(), F, ss->fcur.as<int>(), ss->ptiles.as<int4>(), ss->ntiles.as<int>(), st,
+                        (int)Q);
+    if (rc) return rc;
     rc = filter_reach_f16(ss->xh.as<__half>(), ss->xexp.as<int>(), Q, idx.m, o.d_W1T_h, o.d_wexp, o.d_b1, o.d_W2,
                           o.d_b2, F, ss->ptiles.as<int4>(), ss->ntiles.as<int>(), ss->pdst.as<int2>(), o.d_offset,
                           ss->adj.as<double>(), idx.n_leaves, st);

@@ -254,13 +254,17 @@ class SearchPlan:
         st.synchronize()
         return BatchResult(self.tree.n, *(h.numpy().copy() for h in self._host))
 
-    def __del__(self):
+    def close(self) -> None:
+        """Free the graph, its streams and scratch now (also done on garbage collection)."""
         h, self._h = getattr(self, "_h", None), None
         if h:
-            try:
-                _lib.lib().lf_search_plan_free(h)
-            except Exception:
-                pass
+            _lib.lib().lf_search_plan_free(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 

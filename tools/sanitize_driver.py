@@ -1,11 +1,13 @@
 """Small end-to-end workload for compute-sanitizer (tools/sanitize.sh): every kernel
 family of the library once, at sizes the sanitizer finishes in minutes.  Results are
 checked against the oracle so a silent corruption also fails the run."""
+import os
 import sys
 import tempfile
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
 import numpy as np
 import torch
 
@@ -38,6 +40,23 @@ lf = pack.leaf_filter(di)
 dense = search_batch(t, qd, 1, predictions=pack.predict(qd), offsets=offs, leaf_filter=lf)
 reach = search_batch(t, qd, 1, filters=pack, offsets=offs, leaf_filter=lf)
 assert np.array_equal(dense.ids, reach.ids) and np.array_equal(dense.stats, reach.stats)
+
+from paper_2502_01836_b200.engine import SearchPlan
+
+# the CUDA-graph path (conditional WHILE node set from the device).  racecheck and
+# synccheck abort on device-updated conditional graphs, so only memcheck / initcheck
+# run it; the kernels inside are the ones search_batch launched above.
+if os.environ.get("SAN_TOOL", "memcheck") in ("memcheck", "initcheck"):
+    plan = SearchPlan(t, Q.shape[0], 1, filters=pack, offsets=offs, leaf_filter=lf)
+    for _ in range(2):
+        g = plan.run(qd)
+        assert np.array_equal(g.ids, reach.ids) and np.array_equal(g.stats, reach.stats)
+    plan.close()
+big = build_index(lo.randwalk(60000, 32, 9), 18)                   # > 8,192 nodes: the big leaf order
+Qb = lo.noisy_queries(lo.randwalk(60000, 32, 9), 8, 0.3, 5)
+rb = search_batch(big, Qb, 3)
+for i in range(0, 8, 3):
+    assert rb.ids[i].tolist() == [a for a, _ in lo.linear_scan(lo.randwalk(60000, 32, 9), Qb[i], 3)]
 
 dl = leaf_min_distances(t, qd, list(range(di.n_leaves))).cpu().numpy()
 for i in range(0, len(Q), 6):
