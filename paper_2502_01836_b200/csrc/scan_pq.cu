@@ -477,15 +477,29 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
 // 1.55 / 1.46 / 1.48 / 1.60 ms per batch)
 #define LF_PQB_MINB 3
 #endif
-__global__ void __launch_bounds__(256, LF_PQB_MINB) pq_q8_bound_kernel(RoundState s, lf_index idx, PQOverflow ov) {
-    constexpr int R = 2;            // entries per 8-lane group in flight (3 and 4 at 2 CTAs / SM: 1.81 / 1.82 vs 1.75 ms per batch)
+template <bool FIX256, int R = 2, int MINB = LF_PQB_MINB>
+__global__ void __launch_bounds__(256, MINB) pq_q8_bound_kernel(RoundState s, lf_index idx, PQOverflow ov) {
+    // R: entries per 8-lane group in flight (3 and 4 at 2 CTAs / SM: 1.81 / 1.82 vs 1.75 ms per batch)
     const int lane = threadIdx.x & 31, sl = lane & 7, grp = lane >> 3;
     const long long n = min((long long)*ov.n, (long long)ov.cap);
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-    const int M8 = (idx.m + 63) / 64 * 64;
+    const int M8 = FIX256 ? 256 : (idx.m + 63) / 64 * 64;
     unsigned long long cnt = 0;
-    for (long long w0 = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (4 * R); w0 < n;
-         w0 += nw * 4 * R) {
+    // FIX256 (m <= 256): a lane's 32 query-code bytes stay in registers while its
+    // group's entries keep the same query (entries of a task are contiguous), and the
+    // next iteration's entries are loaded while this one's rows are in flight
+    int64_t cq[R];
+    int4 cqv[R][2];
+    long long w0 = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (4 * R);
+    int4 en[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+        cq[u] = -1;
+        cqv[u][0] = cqv[u][1] = make_int4(0, 0, 0, 0);
+        const long long i = w0 + u * 4 + grp;
+        en[u] = i < n ? ov.ent[i] : make_int4(-1, 0, 0, 0);
+    }
+    for (; w0 < n; w0 += nw * 4 * R) {
         long long ii[R];
         int4 e[R];
         int64_t row[R];
@@ -494,7 +508,7 @@ __global__ void __launch_bounds__(256, LF_PQB_MINB) pq_q8_bound_kernel(RoundStat
 #pragma unroll
         for (int u = 0; u < R; ++u) {
             ii[u] = w0 + u * 4 + grp;
-            e[u] = ii[u] < n ? ov.ent[ii[u]] : make_int4(-1, 0, 0, 0);
+            e[u] = en[u];
             row[u] = (int64_t)(unsigned)e[u].z | ((int64_t)e[u].w << 32);
             qq[u] = e[u].y;
         }
@@ -506,29 +520,66 @@ __global__ void __launch_bounds__(256, LF_PQB_MINB) pq_q8_bound_kernel(RoundStat
             mr[u] = v ? __ldcs(reinterpret_cast<const float4*>(idx.d_qmeta) + row[u]) : make_float4(0.f, 0.f, 0.f, 0.f);
             qmv[u] = v ? __ldg(ov.qm8 + qq[u]) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        // both 128-byte halves of a 256-byte row in flight together (longer rows loop)
-        for (int c0 = sl * 16; c0 < M8; c0 += 256) {
-            int4 w[R][2], qv[R][2];
+        if constexpr (FIX256) {
+            int4 w[R][2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int u = 0; u < R; ++u)
+                    w[u][h] = e[u].x >= 0 ? __ldcs(reinterpret_cast<const int4*>(idx.d_X8 + row[u] * 256 + sl * 16 + h * 128))
+                                          : make_int4(0, 0, 0, 0);
+#pragma unroll
+            for (int u = 0; u < R; ++u)
+                if (e[u].x >= 0 && qq[u] != cq[u]) {
+                    cq[u] = qq[u];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        cqv[u][h] = __ldg(reinterpret_cast<const int4*>(ov.qc8 + qq[u] * ov.mp + sl * 16 + h * 128));
+                }
+#pragma unroll
+            for (int u = 0; u < R; ++u) {          // next iteration's entries
+                const long long i = w0 + nw * 4 * R + u * 4 + grp;
+                en[u] = i < n ? ov.ent[i] : make_int4(-1, 0, 0, 0);
+            }
 #pragma unroll
             for (int h = 0; h < 2; ++h)
 #pragma unroll
                 for (int u = 0; u < R; ++u) {
-                    const int c = c0 + h * 128;
-                    const bool v = e[u].x >= 0 && c < M8;
-                    w[u][h] = v ? __ldcs(reinterpret_cast<const int4*>(idx.d_X8 + row[u] * M8 + c))
-                                : make_int4(0, 0, 0, 0);
-                    qv[u][h] = v ? __ldg(reinterpret_cast<const int4*>(ov.qc8 + qq[u] * ov.mp + c))
-                                 : make_int4(0, 0, 0, 0);
+                    dot[u] = __dp4a(w[u][h].x, cqv[u][h].x, dot[u]);
+                    dot[u] = __dp4a(w[u][h].y, cqv[u][h].y, dot[u]);
+                    dot[u] = __dp4a(w[u][h].z, cqv[u][h].z, dot[u]);
+                    dot[u] = __dp4a(w[u][h].w, cqv[u][h].w, dot[u]);
                 }
+        } else {
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
+            for (int u = 0; u < R; ++u) {
+                const long long i = w0 + nw * 4 * R + u * 4 + grp;
+                en[u] = i < n ? ov.ent[i] : make_int4(-1, 0, 0, 0);
+            }
+            // both 128-byte halves of a 256-byte row in flight together (longer rows loop)
+            for (int c0 = sl * 16; c0 < M8; c0 += 256) {
+                int4 w[R][2], qv[R][2];
 #pragma unroll
-                for (int u = 0; u < R; ++u) {
-                    dot[u] = __dp4a(w[u][h].x, qv[u][h].x, dot[u]);
-                    dot[u] = __dp4a(w[u][h].y, qv[u][h].y, dot[u]);
-                    dot[u] = __dp4a(w[u][h].z, qv[u][h].z, dot[u]);
-                    dot[u] = __dp4a(w[u][h].w, qv[u][h].w, dot[u]);
-                }
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int u = 0; u < R; ++u) {
+                        const int c = c0 + h * 128;
+                        const bool v = e[u].x >= 0 && c < M8;
+                        w[u][h] = v ? __ldcs(reinterpret_cast<const int4*>(idx.d_X8 + row[u] * M8 + c))
+                                    : make_int4(0, 0, 0, 0);
+                        qv[u][h] = v ? __ldg(reinterpret_cast<const int4*>(ov.qc8 + qq[u] * ov.mp + c))
+                                     : make_int4(0, 0, 0, 0);
+                    }
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int u = 0; u < R; ++u) {
+                        dot[u] = __dp4a(w[u][h].x, qv[u][h].x, dot[u]);
+                        dot[u] = __dp4a(w[u][h].y, qv[u][h].y, dot[u]);
+                        dot[u] = __dp4a(w[u][h].z, qv[u][h].z, dot[u]);
+                        dot[u] = __dp4a(w[u][h].w, qv[u][h].w, dot[u]);
+                    }
+            }
         }
 #pragma unroll
         for (int u = 0; u < R; ++u) {
@@ -736,7 +787,12 @@ cudaError_t launch_scan_pq(const RoundState& s, const lf_index& idx, const float
                         : launch_pq_kp<64>(s, idx, q, qc, qm, surv_cnt, ov, st);
     if (e != cudaSuccess) return e;
     if (ov.qc8 != nullptr) {
-        pq_q8_bound_kernel<<<sm_count() * 8, 256, 0, st>>>(s, idx, ov);
+        // (R = 3 / 4 at 2 CTAs per SM, 1 at 6 and 2 at 4: 1.54-1.60 vs 1.53 ms per batch; a
+        // warp-level min before the per-entry threshold atomics: 1.93 ms)
+        if ((idx.m + 63) / 64 * 64 == 256)
+            pq_q8_bound_kernel<true><<<sm_count() * 8, 256, 0, st>>>(s, idx, ov);
+        else
+            pq_q8_bound_kernel<false><<<sm_count() * 8, 256, 0, st>>>(s, idx, ov);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
