@@ -38,10 +38,13 @@ __global__ void eapca_kernel(const float* __restrict__ q, int64_t Q, lf_index id
 }
 
 // max(mn - q, q - mx, 0) (summarize.py:103-104): mn <= mx, so at most one of the
-// two differences is positive -- selects instead of fmax, bit-identical.
+// two differences is positive -- selects instead of fmax, bit-identical.  The sign
+// tests read the high words on the integer pipe (no DSETP on the fp64 pipe): hi > 0
+// is x > 0 except for positive subnormals with a zero high word, whose square
+// underflows to an exact 0 in every bound mode, so the bound is unchanged.
 __device__ __forceinline__ double env_gap(double mn, double mx, double q) {
     const double a = mn - q, b = q - mx;
-    return a > 0.0 ? a : (b > 0.0 ? b : 0.0);
+    return __double2hiint(a) > 0 ? a : (__double2hiint(b) > 0 ? b : 0.0);
 }
 
 // The per-segment term of each bound mode, folded into acc:
@@ -97,14 +100,17 @@ constexpr int LBT_NODES = 128;
 constexpr int LBT_Q = 16;
 constexpr int LBT_SEG = 8;
 
-template <int MODE>
+// NS > 0: n_seg known at compile time (no per-segment guards; 246 -> fewer issued
+// instructions per (query, node) at n_seg = 8), 0: any n_seg <= 8.
+template <int MODE, int NS = 0>
 __global__ void __launch_bounds__(LBT_NODES, MODE == 2 ? 2 : 4)
-    lb_tile_kernel(const double* __restrict__ qsumm, int64_t Q, int ns, lf_index idx,
+    lb_tile_kernel(const double* __restrict__ qsumm, int64_t Q, int ns_, lf_index idx,
                    const double* __restrict__ env_min, const double* __restrict__ env_max,
                    const double* __restrict__ sd_min, const double* __restrict__ sd_max, int n_env,
                    double* __restrict__ lb, unsigned* __restrict__ qmax, unsigned* __restrict__ qmin,
                    double* __restrict__ plb, int* __restrict__ pnode) {
     constexpr int QW = MODE == 2 ? 2 * LBT_SEG : LBT_SEG;
+    const int ns = NS > 0 ? NS : ns_;
     __shared__ double qs[LBT_Q][QW];
     __shared__ double ws[LBT_SEG];
     const int node = blockIdx.x * LBT_NODES + threadIdx.x;
@@ -197,12 +203,13 @@ int launch_bounds(const float* d_q, int64_t Q, const lf_index& idx, const double
             }
         }
         dim3 grid((unsigned)((n_env + LBT_NODES - 1) / LBT_NODES), (unsigned)((Q + LBT_Q - 1) / LBT_Q));
-#define LF_TILE(M) lb_tile_kernel<M><<<grid, LBT_NODES, 0, st>>>(d_qsumm, Q, idx.n_seg, idx, env_min, env_max, \
-                                                                sd_min, sd_max, n_env, d_lb, d_qmax, d_qmin, \
-                                                                d_plb, d_pnode)
-        if (mode == 0) LF_TILE(0);
-        else if (mode == 1) LF_TILE(1);
-        else LF_TILE(2);
+#define LF_TILE(M, N) lb_tile_kernel<M, N><<<grid, LBT_NODES, 0, st>>>(d_qsumm, Q, idx.n_seg, idx, env_min, env_max, \
+                                                                      sd_min, sd_max, n_env, d_lb, d_qmax, d_qmin, \
+                                                                      d_plb, d_pnode)
+        if (mode == 0 && idx.n_seg == LBT_SEG) LF_TILE(0, LBT_SEG);
+        else if (mode == 0) LF_TILE(0, 0);
+        else if (mode == 1) LF_TILE(1, 0);
+        else LF_TILE(2, 0);
 #undef LF_TILE
         LF_CUDA(cudaGetLastError());
         return LF_OK;
