@@ -788,7 +788,10 @@ cudaError_t launch_scan_pq(const RoundState& s, const lf_index& idx, const float
     if (e != cudaSuccess) return e;
     if (ov.qc8 != nullptr) {
         // (R = 3 / 4 at 2 CTAs per SM, 1 at 6 and 2 at 4: 1.54-1.60 vs 1.53 ms per batch; a
-        // warp-level min before the per-entry threshold atomics: 1.93 ms)
+        // warp-level min before the per-entry threshold atomics: 1.93 ms; the gathers through
+        // a per-warp shared-memory ring of 8-entry pieces -- cp.async.bulk per row and
+        // mbarrier: 1.54, 16-byte cp.async with 4 / 6 / 8 pieces in flight: 1.68 / 1.62 /
+        // 1.82, vs 1.48 ms for this kernel)
         if ((idx.m + 63) / 64 * 64 == 256)
             pq_q8_bound_kernel<true><<<sm_count() * 8, 256, 0, st>>>(s, idx, ov);
         else
