@@ -15,10 +15,12 @@
 
 namespace lf {
 
-// One thread per (query, segment).
+// One thread per (query, segment).  zero2 (nullable, [2 Q]): the leaf-bound range
+// words lb_tile_kernel accumulates into, zeroed here (no memset node in the graphs).
 __global__ void paa_kernel(const float* __restrict__ q, int64_t Q, lf_index idx,
-                           double* __restrict__ qsumm) {
+                           double* __restrict__ qsumm, unsigned* __restrict__ zero2 = nullptr) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (zero2 != nullptr && t < 2 * Q) zero2[t] = 0u;
     if (t >= Q * idx.n_seg) return;
     int64_t qi = t / idx.n_seg;
     int s = (int)(t - qi * idx.n_seg);
@@ -183,24 +185,25 @@ int launch_bounds(const float* d_q, int64_t Q, const lf_index& idx, const double
                   cudaStream_t st, unsigned* d_qmax, unsigned* d_qmin, const double* sd_min,
                   const double* sd_max, double* d_plb, int* d_pnode) {
     if (Q == 0) return LF_OK;
+    const bool tiled = n_env > 0 && idx.n_seg <= LBT_SEG && (Q + LBT_Q - 1) / LBT_Q <= 65535;
+    // the range words: zeroed by paa_kernel when contiguous ([qmax | qmin], the callers' layout)
+    const bool zero_in_paa = tiled && d_qmax != nullptr && d_qmin == d_qmax + Q && mode != 2;
     {
         int64_t n = Q * idx.n_seg;
+        if (zero_in_paa) n = std::max<int64_t>(n, 2 * Q);
         int thr = 256;
         if (mode == 2)
             eapca_kernel<<<(unsigned)((n + thr - 1) / thr), thr, 0, st>>>(d_q, Q, idx, d_qsumm);
         else
-            paa_kernel<<<(unsigned)((n + thr - 1) / thr), thr, 0, st>>>(d_q, Q, idx, d_qsumm);
+            paa_kernel<<<(unsigned)((n + thr - 1) / thr), thr, 0, st>>>(d_q, Q, idx, d_qsumm,
+                                                                        zero_in_paa ? d_qmax : nullptr);
         LF_CUDA(cudaGetLastError());
     }
     if (n_env == 0) return LF_OK;
-    if (idx.n_seg <= LBT_SEG && (Q + LBT_Q - 1) / LBT_Q <= 65535) {
-        if (d_qmax != nullptr) {
-            if (d_qmin == d_qmax + Q) {
-                LF_CUDA(cudaMemsetAsync(d_qmax, 0, sizeof(unsigned) * 2 * Q, st));
-            } else {
-                LF_CUDA(cudaMemsetAsync(d_qmax, 0, sizeof(unsigned) * Q, st));
-                LF_CUDA(cudaMemsetAsync(d_qmin, 0, sizeof(unsigned) * Q, st));
-            }
+    if (tiled) {
+        if (d_qmax != nullptr && !zero_in_paa) {
+            LF_CUDA(cudaMemsetAsync(d_qmax, 0, sizeof(unsigned) * Q, st));
+            LF_CUDA(cudaMemsetAsync(d_qmin, 0, sizeof(unsigned) * Q, st));
         }
         dim3 grid((unsigned)((n_env + LBT_NODES - 1) / LBT_NODES), (unsigned)((Q + LBT_Q - 1) / LBT_Q));
 #define LF_TILE(M, N) lb_tile_kernel<M, N><<<grid, LBT_NODES, 0, st>>>(d_qsumm, Q, idx.n_seg, idx, env_min, env_max, \
@@ -379,7 +382,8 @@ __global__ void __launch_bounds__(LoCfg<BIG>::THREADS, BIG ? 1 : 2)
     const double* lbq = lb + q * Nn;
     double thr = kInf;                                   // pruned orders: leaves past thr are not records
     if (o.prune) {
-        double b = o.top_n[q] == o.k ? o.top_d[q * o.k + o.k - 1] : kInf;
+        double b = o.seed != nullptr ? (double)__uint_as_float(o.seed[q])
+                                     : (o.top_n[q] == o.k ? o.top_d[q * o.k + o.k - 1] : kInf);
         if (o.bound != nullptr) b = fmin(b, o.bound[q]);
         thr = b * o.f;
     }

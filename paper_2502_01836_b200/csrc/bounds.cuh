@@ -52,6 +52,11 @@ struct OrderArgs {
     int k;
     double f;
     const double* bound;         // [Q] or NULL
+    // k = 1 seeded round 0: thr = seed * f instead of the top-k, seed = float bits of the
+    // exactly scored seed rows' minimum per query (>= bsf0, so the order is a superset of
+    // the bsf0-pruned one with the same prefix) -- available before round 0's merge, so
+    // the order is built concurrently with the rest of round 0
+    const unsigned* seed;        // [Q] or NULL
 };
 // Two phases of bounds_and_order, for orders built after round 0:
 //   bounds_phase: segment means, bound matrix, the range of each query's leaf

@@ -174,8 +174,10 @@ struct PQOverflow {
 };
 int pq_scan_warps();                          // warps of one scan_pq_kernel launch
 constexpr int PQ_OVER_CAP = 8 << 20;          // 8M entries (128 MB + lo8)
+// after_scan (nullable): recorded right after the streaming scan kernel (round 0: the
+// seed minima in ov.qbest are final there)
 cudaError_t launch_scan_pq(const RoundState& s, const lf_index& idx, const float* q, const int8_t* qc,
                            const float4* qm, int* surv_cnt, const PQOverflow& ov, int64_t max_tasks,
-                           cudaStream_t st);
+                           cudaStream_t st, cudaEvent_t after_scan = nullptr);
 
 }  // namespace lf

@@ -780,12 +780,13 @@ int pq_scan_warps() { return sm_count() * PQW<32>::WARPS; }   // >= PQW<64>: 16 
 
 cudaError_t launch_scan_pq(const RoundState& s, const lf_index& idx, const float* q, const int8_t* qc,
                            const float4* qm, int* surv_cnt, const PQOverflow& ov, int64_t max_tasks,
-                           cudaStream_t st) {
+                           cudaStream_t st, cudaEvent_t after_scan) {
     cudaError_t e = cudaMemsetAsync(ov.n, 0, sizeof(int), st);
     if (e != cudaSuccess) return e;
     e = idx.pca_k == 32 ? launch_pq_kp<32>(s, idx, q, qc, qm, surv_cnt, ov, st)
                         : launch_pq_kp<64>(s, idx, q, qc, qm, surv_cnt, ov, st);
     if (e != cudaSuccess) return e;
+    if (after_scan != nullptr && (e = cudaEventRecord(after_scan, st)) != cudaSuccess) return e;
     if (ov.qc8 != nullptr) {
         // (R = 3 / 4 at 2 CTAs per SM, 1 at 6 and 2 at 4: 1.54-1.60 vs 1.53 ms per batch; a
         // warp-level min before the per-entry threshold atomics: 1.93 ms; the gathers through

@@ -715,6 +715,11 @@ struct lf_session {
     bool prof = false;
     cudaStream_t st2 = nullptr;      // prologue branch: query codes, concurrent with the bounds
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    // k = 1 seeded round 0: the pruned visit orders are cut at the seed minima (qbest) and
+    // built on st2 right after round 0's streaming scan, concurrent with its int8 stage,
+    // tail and merge (graph plans); joined before the prediction pass
+    bool order_seed = false;
+    cudaEvent_t scan0_ev = nullptr, order_ev = nullptr;
 };
 
 namespace lf {
@@ -781,6 +786,8 @@ static int session_alloc(lf_session* ss) {
     LF_CUDA(cudaStreamCreateWithFlags(&ss->st2, cudaStreamNonBlocking));
     LF_CUDA(cudaEventCreateWithFlags(&ss->fork_ev, cudaEventDisableTiming));
     LF_CUDA(cudaEventCreateWithFlags(&ss->join_ev, cudaEventDisableTiming));
+    LF_CUDA(cudaEventCreateWithFlags(&ss->scan0_ev, cudaEventDisableTiming));
+    LF_CUDA(cudaEventCreateWithFlags(&ss->order_ev, cudaEventDisableTiming));
     for (int sl = 0; sl < 2; ++sl) {
         LF_CUDA(cudaEventCreateWithFlags(&ss->done_ev[sl], cudaEventDisableTiming));
         if (o.h_profile)
@@ -835,6 +842,7 @@ static int session_alloc(lf_session* ss) {
     oa.k = o.k;
     oa.f = o.bsf_factor;
     oa.bound = nullptr;
+    oa.seed = nullptr;
     oa.lbs = ss->lbs.as<double>();
     oa.gap = ss->gap.as<double>();
     oa.order = s.want_trace ? ss->order.as<int>() : nullptr;
@@ -1002,6 +1010,7 @@ static int order_after_round0(lf_session* ss, const double* d_bound) {
         LF_CUDA(cudaEventRecord(e0, ss->st));
     }
     ss->oa.bound = d_bound;
+    ss->oa.seed = ss->order_seed ? ss->pq_qbest.as<unsigned>() : nullptr;
     const unsigned* qmax = ss->orng.as<unsigned>();
     int rc = order_phase(ss->lb.as<double>(), ss->Q, ss->idx, qmax, qmax + ss->Q, ss->oa, ss->st);
     if (rc) return rc;
@@ -1091,8 +1100,9 @@ static int round_kernels(lf_session* ss, int* counts, bool round0, cudaEvent_t* 
                             s.k == 1 && ss->q8 ? ss->pq_xd.as<double>() : nullptr,
                             s.k == 1 && ss->q8 ? ss->pq_xlist.as<int>() : nullptr,
                             s.k == 1 && ss->q8 ? ss->pq_xn.as<int>() : nullptr};
+        if (round0) ss->order_seed = seed && ss->pruned && !std::getenv("LF_ORDER_AFTER_ROUND0");
         ce = launch_scan_pq(s, idx, ss->d_q, ss->qcp.as<int8_t>(), ss->qmp.as<float4>(), ss->pq_cnt.as<int>(), ov,
-                            ss->max_tasks, st);
+                            ss->max_tasks, st, round0 && ss->order_seed ? ss->scan0_ev : nullptr);
         ss->kernels += ss->q8 ? 3 : 2;
     } else if (ea) {
         ce = launch_scan_q8(s, idx, ss->d_q, ss->qc8.as<int8_t>(), ss->qm8.as<float4>(), st);
@@ -1214,6 +1224,8 @@ static void session_free(lf_session* ss) {
     if (!ss) return;
     if (ss->fork_ev) cudaEventDestroy(ss->fork_ev);
     if (ss->join_ev) cudaEventDestroy(ss->join_ev);
+    if (ss->scan0_ev) cudaEventDestroy(ss->scan0_ev);
+    if (ss->order_ev) cudaEventDestroy(ss->order_ev);
     if (ss->st2) {
         cudaStreamSynchronize(ss->st2);
         cudaStreamDestroy(ss->st2);
@@ -1276,7 +1288,21 @@ static int plan_capture(lf_session* ss, cudaStream_t cs, cudaStream_t cs2, int64
     LF_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
     int rc = session_prologue(ss);
     if (!rc) rc = round_kernels(ss, counts, true, nullptr);
-    if (!rc && ss->pruned) rc = order_after_round0(ss, nullptr);
+    if (!rc && ss->pruned && ss->order_seed) {
+        // the order branch: st2 from the seeded scan's end, joined before the prediction pass
+        cudaError_t e = cudaStreamWaitEvent(ss->st2, ss->scan0_ev, 0);
+        if (e != cudaSuccess) rc = fail(LF_ECUDA, cudaGetErrorString(e));
+        if (!rc) {
+            ss->st = ss->st2;
+            rc = order_after_round0(ss, nullptr);
+            ss->st = cs;
+        }
+        if (!rc && (e = cudaEventRecord(ss->order_ev, ss->st2)) == cudaSuccess)
+            e = cudaStreamWaitEvent(cs, ss->order_ev, 0);
+        if (!rc && e != cudaSuccess) rc = fail(LF_ECUDA, cudaGetErrorString(e));
+    } else if (!rc && ss->pruned) {
+        rc = order_after_round0(ss, nullptr);
+    }
     if (!rc && ss->lazy) rc = predict_pass(ss, 1);
     cudaGraph_t g = nullptr;
     cudaGraphConditionalHandle h;

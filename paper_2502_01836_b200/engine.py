@@ -230,15 +230,25 @@ class SearchPlan:
             _lib.check(_lib.LF_ECUDA)
         self._h = h
 
-    def run(self, queries, stream=None, copy_out: bool = True):
+    def run(self, queries, stream=None, copy_out: bool = True, outputs=None):
+        """outputs: optional preallocated device (ids [Q, k] int64, dists [Q, k] fp64,
+        stats [Q, N_STATS] int64) the results are copied into (copy_out=False returns them)."""
         torch = _lib.require_cuda()
         q = _queries_device(queries, self.tree.m, self.di.device)
         if q.shape[0] != self.Q:
             raise ValueError(f"plan was built for {self.Q} queries, got {q.shape[0]}")
         dev = self.di.device
-        ids = torch.empty((self.Q, self.k), dtype=torch.int64, device=dev)
-        dists = torch.empty((self.Q, self.k), dtype=torch.float64, device=dev)
-        stats = torch.empty((self.Q, _lib.N_STATS), dtype=torch.int64, device=dev)
+        if outputs is not None:
+            ids, dists, stats = outputs
+            if (tuple(ids.shape) != (self.Q, self.k) or tuple(dists.shape) != (self.Q, self.k)
+                    or tuple(stats.shape) != (self.Q, _lib.N_STATS) or ids.dtype != torch.int64
+                    or dists.dtype != torch.float64 or stats.dtype != torch.int64
+                    or not all(x.is_cuda and x.is_contiguous() for x in (ids, dists, stats))):
+                raise ValueError("outputs must be contiguous device (int64 [Q, k], fp64 [Q, k], int64 [Q, N_STATS])")
+        else:
+            ids = torch.empty((self.Q, self.k), dtype=torch.int64, device=dev)
+            dists = torch.empty((self.Q, self.k), dtype=torch.float64, device=dev)
+            stats = torch.empty((self.Q, _lib.N_STATS), dtype=torch.int64, device=dev)
         with torch.cuda.device(dev):
             _lib.check(_lib.lib().lf_search_plan_run(self._h, q.data_ptr(), ids.data_ptr(), dists.data_ptr(),
                                                      stats.data_ptr(), _lib.stream_ptr(stream)))

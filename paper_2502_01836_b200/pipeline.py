@@ -33,7 +33,7 @@ import numpy as np
 
 from . import _lib
 from .calibration import DeviceReplay, build_skeleton, compute_alphas, fit_auto_tuners, tune
-from .engine import SearchOutcome, as_tree, search_batch
+from .engine import BatchResult, SearchOutcome, as_tree, search_batch
 from .filters import FilterPack
 from .synth import generate_global_queries, generate_local_queries
 from .targets import collect_targets, local_targets_all
@@ -238,6 +238,118 @@ def _as_enhanced(eidx) -> EnhancedIndex:
     return got
 
 
+def _plan_for(e, Q: int, k: int, target: float, sequential: bool, max_round_leaves: int, stream=None):
+    """The cached graph plan of (batch size, k, target, schedule) on e's device."""
+    di = e.base.device()
+    plans = e.__dict__.setdefault("_plans", {})
+    key = (int(Q), int(k), float(target), bool(sequential), int(max_round_leaves), str(di.device))
+    plan = plans.get(key)
+    if plan is None:
+        from .engine import SearchPlan
+
+        pk = e.pack
+        plan = SearchPlan(e.base, Q, k, filters=pk, offsets=e.offset_vector(target, device=True),
+                          leaf_filter=pk.leaf_filter(di), sequential=sequential,
+                          max_round_leaves=max_round_leaves, stream=stream)
+        plans[key] = plan
+    return plan
+
+
+class SearchPipeline:
+    """Serving form of `search_queries` (in-search inference, graph plan): batches
+    submitted back to back overlap their copies with the search of the batch before.
+    Each batch's queries go host -> device on one copy stream, the plan runs on a
+    compute stream, the results come back device -> host on a third; `depth` slots of
+    device queries, device results and pinned host results rotate.  Results and
+    counters equal `search_queries`' for the same batch.
+
+        pipe = SearchPipeline(eidx, batch=1000, k=1, target=0.99)
+        t = pipe.submit(q0)              # pinned host tensors overlap best
+        for q in rest:
+            t_next = pipe.submit(q)
+            res = pipe.result(t)         # BatchResult of the earlier batch
+            t = t_next
+        res = pipe.result(t)
+
+    At most `depth` batches are in flight: a slot's result must be collected before the
+    slot is submitted again.  The caller keeps a submitted host tensor unchanged until
+    its result is collected."""
+
+    def __init__(self, eidx, batch: int, k: int = 1, *, target: float, depth: int = 2,
+                 sequential: bool = False, max_round_leaves: int = 256):
+        torch = _lib.require_cuda()
+        e = _as_enhanced(eidx)
+        if not e.filters or e.pack.path != "tc16":
+            raise ValueError("SearchPipeline needs an enhanced index with the fp16 filter pack (path 'tc16')")
+        if not 0.0 <= target <= 1.0:
+            raise ValueError(f"target must be in [0, 1], got {target}")
+        if depth < 1:
+            raise ValueError(f"depth must be >= 1, got {depth}")
+        di = e.base.device()
+        dev = di.device
+        self.n_series, self.batch, self.k, self.depth = e.base.n, int(batch), int(k), int(depth)
+        self._plan = _plan_for(e, self.batch, self.k, float(target), sequential, max_round_leaves)
+        m = e.base.m
+        with torch.cuda.device(dev):
+            self._comp, self._h2d, self._d2h = (torch.cuda.Stream(dev) for _ in range(3))
+            self._qd = [torch.empty((self.batch, m), dtype=torch.float32, device=dev) for _ in range(depth)]
+            self._out = [(torch.empty((self.batch, self.k), dtype=torch.int64, device=dev),
+                          torch.empty((self.batch, self.k), dtype=torch.float64, device=dev),
+                          torch.empty((self.batch, _lib.N_STATS), dtype=torch.int64, device=dev))
+                         for _ in range(depth)]
+            self._host = [tuple(torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in o) for o in self._out]
+            self._ev = [[torch.cuda.Event() for _ in range(3)] for _ in range(depth)]   # h2d, search, d2h
+        self._qh = [None] * depth
+        self._slot_ticket = [None] * depth
+        self._pending = {}
+        self._n = 0
+
+    def submit(self, queries) -> int:
+        """Enqueue one batch ([batch, m] fp32: a pinned host tensor, any host array, or a
+        device tensor); returns its ticket."""
+        torch = _lib.require_cuda()
+        i = self._n % self.depth
+        if self._slot_ticket[i] is not None and self._slot_ticket[i] in self._pending:
+            raise RuntimeError(f"collect result({self._slot_ticket[i]}) before submitting more than "
+                               f"{self.depth} batches")
+        q = queries if isinstance(queries, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(np.atleast_2d(queries), dtype=np.float32))
+        if tuple(q.shape) != (self.batch, self._qd[i].shape[1]):
+            raise ValueError(f"batch of shape {tuple(q.shape)}, pipeline built for {(self.batch, self._qd[i].shape[1])}")
+        ev_h2d, ev_run, ev_d2h = self._ev[i]
+        reuse = self._n >= self.depth
+        with torch.cuda.stream(self._h2d):
+            if reuse:
+                self._h2d.wait_event(ev_run)             # the slot's previous search read its queries
+            self._qd[i].copy_(q.to(torch.float32), non_blocking=True)
+            ev_h2d.record(self._h2d)
+        self._qh[i] = q
+        self._comp.wait_event(ev_h2d)
+        if reuse:
+            self._comp.wait_event(ev_d2h)                # the slot's previous results left the device
+        self._plan.run(self._qd[i], stream=self._comp, copy_out=False, outputs=self._out[i])
+        ev_run.record(self._comp)
+        self._d2h.wait_event(ev_run)
+        with torch.cuda.stream(self._d2h):
+            for h, x in zip(self._host[i], self._out[i]):
+                h.copy_(x, non_blocking=True)
+            ev_d2h.record(self._d2h)
+        t = self._n
+        self._pending[t] = i
+        self._slot_ticket[i] = t
+        self._n += 1
+        return t
+
+    def result(self, ticket: int) -> BatchResult:
+        """Wait for a submitted batch and return its BatchResult (host arrays)."""
+        if ticket not in self._pending:
+            raise KeyError(f"no pending batch with ticket {ticket}")
+        i = self._pending.pop(ticket)
+        self._ev[i][2].synchronize()
+        self._qh[i] = None
+        return BatchResult(self.n_series, *(h.numpy().copy() for h in self._host[i]))
+
+
 def search_queries(eidx, queries, k: int = 1, *, target: float | None = None, exact: bool = False,
                    sequential: bool = False, max_round_leaves: int = 256, want_trace: bool = False,
                    stream=None, copy_out: bool = True, profile=None, lazy: bool | None = None,
@@ -268,16 +380,7 @@ def search_queries(eidx, queries, k: int = 1, *, target: float | None = None, ex
     if lazy and pk.path != "tc16":
         raise ValueError("in-search filter inference runs on the fp16 pack (FilterPack path 'tc16')")
     if lazy and graph and profile is None and not want_trace and os.environ.get("LF_SEARCH_GRAPH", "1") != "0":
-        plans = e.__dict__.setdefault("_plans", {})
-        key = (int(q.shape[0]), int(k), float(target), bool(sequential), int(max_round_leaves), str(di.device))
-        plan = plans.get(key)
-        if plan is None:
-            from .engine import SearchPlan
-
-            plan = SearchPlan(e.base, q.shape[0], k, filters=pk, offsets=e.offset_vector(target, device=True),
-                              leaf_filter=pk.leaf_filter(di), sequential=sequential,
-                              max_round_leaves=max_round_leaves, stream=stream)
-            plans[key] = plan
+        plan = _plan_for(e, int(q.shape[0]), k, target, sequential, max_round_leaves, stream)
         return plan.run(q, stream=stream, copy_out=copy_out)
     if lazy:
         return search_batch(e.base, q.contiguous(), k, filters=pk, offsets=e.offset_vector(target, device=True),

@@ -300,3 +300,51 @@ def test_device_replay_bit_identical():
     for l in a:
         np.testing.assert_array_equal(a[l].knot_quality, b[l].knot_quality)
         np.testing.assert_array_equal(a[l].knot_offset, b[l].knot_offset)
+
+
+@pytest.fixture(scope="module")
+def pipe64():
+    """A small m = 64 collection enhanced on the GPU: the fp16 pack (in-search inference)."""
+    from paper_2502_01836_b200 import build_index
+    from paper_2502_01836_b200 import pipeline as pl
+    from paper_2502_01836_b200.training import TrainConfig
+
+    data = lo.randwalk(6000, 64, 29)
+    t = build_index(data, 200)
+    e = pl.enhance(t, pl.SplitPlan(240, 80, 60), pl.SelectionBudget(16 * 1024 * 1024), seed=31,
+                   constants=pl.RuntimeConstants(**FIXED), train_cfg=TrainConfig(max_epochs=60))
+    return {"tree": t, "eidx": e, "queries": lo.noisy_queries(data, 96, 0.2, 37)}
+
+
+def test_search_pipeline_matches_search_queries(pipe64):
+    """pipeline.SearchPipeline (copies on their own streams, rotating slots) returns
+    exactly search_queries' results and counters, batch by batch."""
+    import torch
+
+    from paper_2502_01836_b200.pipeline import SearchPipeline, search_queries
+
+    e = pipe64["eidx"]
+    assert e.pack.path == "tc16"
+    Q = np.asarray(pipe64["queries"], dtype=np.float32)
+    Qr = np.ascontiguousarray(Q[::-1])
+    refs = [search_queries(e, Q, 1, target=0.99), search_queries(e, Qr, 1, target=0.99)]
+    sp = SearchPipeline(e, Q.shape[0], 1, target=0.99, depth=2)
+    batches = [torch.from_numpy(b).pin_memory() for b in (Q, Qr, Q, Qr, Q)]
+    pending, outs = [], []
+    for b in batches:
+        pending.append(sp.submit(b))
+        if len(pending) == 2:
+            outs.append(sp.result(pending.pop(0)))
+    outs.append(sp.result(pending.pop(0)))
+    for j, r in enumerate(outs):
+        ref = refs[j % 2]
+        np.testing.assert_array_equal(r.ids, ref.ids)
+        np.testing.assert_array_equal(r.dists, ref.dists)
+        np.testing.assert_array_equal(r.stats, ref.stats)
+    t0, t1 = sp.submit(Q), sp.submit(Qr)
+    with pytest.raises(RuntimeError):
+        sp.submit(Q)                                # both slots still hold uncollected batches
+    assert np.array_equal(sp.result(t0).ids, refs[0].ids)
+    assert np.array_equal(sp.result(t1).ids, refs[1].ids)
+    with pytest.raises(KeyError):
+        sp.result(t1)
