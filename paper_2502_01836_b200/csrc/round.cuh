@@ -29,7 +29,7 @@ struct RoundState {
     const double* adj;           // [Q][L] pred - offset of the leaf's filter
     const int* olen;             // [Q] records of the order (= L)
     int lazy;                    // in-search filter inference: adj valid for positions < pcount[q]
-    const int* pcount;           // [Q]
+    int* pcount;                 // [Q]
     int* preq;                   // [Q] set when the walk stopped at pcount (more predictions needed)
     int* n_predict;              // walks that reached pcount with a finite bsf (= n_active + 2)
     int* cursor;                 // [Q]
@@ -56,6 +56,14 @@ struct RoundState {
     long long* cand_i;
     double* task_min;            // [max_tasks] (trace only)
     int* n_active;
+    // counters zeroed inside kernels instead of graph memset nodes (~0.85 us per node):
+    int* pq_n;                   // projected-scan entry count: zeroed by the plan kernels
+    int* pq_xn;                  // exact-tail list length: zeroed by the int8 stage
+    int* cnt_all;                // [8] round counters (both slots): zeroed by init_state
+    int* zero_counts;            // stream-ordered rounds: the next round's counter slot, zeroed by merge
+    int* rctr;                   // graph round counter, or NULL: zeroed by init_state
+    unsigned long long* ptotal;  // pair total (profiling), or NULL: zeroed by init_state
+    unsigned* qbest;             // seeded round 0: per-query seed minimum, set to 3.4e38 by init_state
     const float* pred;           // [Q][F]
     const double* pred64;        // [Q][F] (alternative to pred)
     const double* offset;        // [F]

@@ -481,6 +481,7 @@ template <bool FIX256, int R = 2, int MINB = LF_PQB_MINB>
 __global__ void __launch_bounds__(256, MINB) pq_q8_bound_kernel(RoundState s, lf_index idx, PQOverflow ov) {
     // R: entries per 8-lane group in flight (3 and 4 at 2 CTAs / SM: 1.81 / 1.82 vs 1.75 ms per batch)
     const int lane = threadIdx.x & 31, sl = lane & 7, grp = lane >> 3;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && ov.xn != nullptr) *ov.xn = 0;   // the exact tail's list
     const long long n = min((long long)*ov.n, (long long)ov.cap);
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
     const int M8 = FIX256 ? 256 : (idx.m + 63) / 64 * 64;
@@ -781,9 +782,8 @@ int pq_scan_warps() { return sm_count() * PQW<32>::WARPS; }   // >= PQW<64>: 16 
 cudaError_t launch_scan_pq(const RoundState& s, const lf_index& idx, const float* q, const int8_t* qc,
                            const float4* qm, int* surv_cnt, const PQOverflow& ov, int64_t max_tasks,
                            cudaStream_t st, cudaEvent_t after_scan) {
-    cudaError_t e = cudaMemsetAsync(ov.n, 0, sizeof(int), st);
-    if (e != cudaSuccess) return e;
-    e = idx.pca_k == 32 ? launch_pq_kp<32>(s, idx, q, qc, qm, surv_cnt, ov, st)
+    // (ov.n: zeroed by the round's plan kernel; ov.xn: by the int8 stage)
+    cudaError_t e = idx.pca_k == 32 ? launch_pq_kp<32>(s, idx, q, qc, qm, surv_cnt, ov, st)
                         : launch_pq_kp<64>(s, idx, q, qc, qm, surv_cnt, ov, st);
     if (e != cudaSuccess) return e;
     if (after_scan != nullptr && (e = cudaEventRecord(after_scan, st)) != cudaSuccess) return e;
@@ -801,8 +801,6 @@ cudaError_t launch_scan_pq(const RoundState& s, const lf_index& idx, const float
         if (e != cudaSuccess) return e;
     }
     if (ov.xd != nullptr) {                          // k = 1: entry-parallel tail
-        e = cudaMemsetAsync(ov.xn, 0, sizeof(int), st);
-        if (e != cudaSuccess) return e;
         pq_tail_e0_kernel<<<sm_count() * 8, 256, 0, st>>>(ov);
         pq_tail_e1_kernel<<<sm_count() * 4, 256, 0, st>>>(s, idx, q, ov);
         pq_tail_e2_kernel<<<sm_count() * 2, 256, 0, st>>>(s, idx, ov);

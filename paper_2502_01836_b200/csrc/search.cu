@@ -44,6 +44,7 @@ constexpr int PLAN_PF = LF_PLAN_PF;
 __global__ void plan_warp_kernel(RoundState s, lf_index idx) {
     const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && s.pq_n != nullptr) *s.pq_n = 0;   // the scan's entry counter
     if (q >= s.Q) return;
     const unsigned below = (1u << lane) - 1u;
     const int Lr = s.n_leaves;                 // records per query: the leaf slots
@@ -285,6 +286,7 @@ __global__ void first_leaf_plan_kernel(RoundState s, lf_index idx, const double*
                                        const int* __restrict__ pnode, int W) {
     const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && s.pq_n != nullptr) *s.pq_n = 0;   // the scan's entry counter
     if (q >= s.Q) return;
     double bv = kInf;
     int bn = 0x7fffffff;
@@ -361,9 +363,11 @@ __global__ void first_leaf_plan_kernel(RoundState s, lf_index idx, const double*
 // Warp per query: a 32-way search (one ballot per step, ~3 dependent loads for 4,096
 // records instead of 12).
 __global__ void pairs_range_kernel(RoundState s, int* __restrict__ pcount, int* __restrict__ pstart,
-                                   int* __restrict__ pair_end, int all) {
+                                   int* __restrict__ pair_end, int all, int* __restrict__ fhist, int F) {
     const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
+    for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < F; f += (int64_t)gridDim.x * blockDim.x)
+        fhist[f] = 0;                                    // the pass's filter buckets (no memset node)
     if (q >= s.Q) return;
     const int pc = pcount[q];
     const int start = max(pc, s.cursor[q]);              // the walk never goes back
@@ -497,6 +501,11 @@ constexpr int MERGE_KMAX = 16;                 // k up to this: register top-k p
 __global__ void merge_kernel(RoundState s) {
     const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {     // the next round's task counter and counts
+        s.chunk_off[s.Q] = 0;
+        if (s.zero_counts != nullptr)
+            for (int i = 0; i < 3; ++i) s.zero_counts[i] = 0;
+    }
     if (q >= s.Q) return;
     const int ns = s.n_sel[q];
     const double* td = s.top_d + q * s.k;
@@ -649,10 +658,25 @@ __global__ void merge_kernel(RoundState s) {
 
 __global__ void init_state_kernel(RoundState s) {
     int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q == 0) {
+        s.chunk_off[s.Q] = 0;
+        if (s.ea_count != nullptr)
+            for (int i = 0; i < 4; ++i) s.ea_count[i] = 0ull;
+        if (s.cnt_all != nullptr)
+            for (int i = 0; i < 8; ++i) s.cnt_all[i] = 0;
+        if (s.rctr != nullptr) *s.rctr = 0;
+        if (s.ptotal != nullptr) *s.ptotal = 0ull;
+        if (s.pq_n != nullptr) *s.pq_n = 0;
+    }
     if (q >= s.Q) return;
     s.cursor[q] = 0;
     s.done[q] = 0;
     s.top_n[q] = 0;
+    if (s.lazy) {
+        s.pcount[q] = 0;
+        s.preq[q] = 0;
+    }
+    if (s.qbest != nullptr) s.qbest[q] = 0x7f7f7f7fu;          // 3.4e38: above any distance
     for (int i = 0; i < LF_N_STATS; ++i) s.stats[q * LF_N_STATS + i] = 0;
     if (s.want_trace) s.tr.d_len[q] = 0;
 }
@@ -735,6 +759,7 @@ struct lf_session {
     // built on st2 right after round 0's streaming scan, concurrent with its int8 stage,
     // tail and merge (graph plans); joined before the prediction pass
     bool order_seed = false;
+    bool capturing = false;          // plan_capture: the body's rounds share one count slot
     cudaEvent_t scan0_ev = nullptr, order_ev = nullptr;
 };
 
@@ -930,6 +955,13 @@ static int session_alloc(lf_session* ss) {
         LF_CUDA(ss->qc8.alloc((size_t)Q * MP, st));
         LF_CUDA(ss->qm8.alloc(sizeof(float4) * Q, st));
     }
+    // counters zeroed inside kernels (RoundState)
+    s.pq_n = ss->pq ? ss->pq_on.as<int>() : nullptr;
+    s.pq_xn = ss->pq_xn.p ? ss->pq_xn.as<int>() : nullptr;
+    s.cnt_all = ss->n_active.as<int>();
+    s.rctr = ss->round_ctr.as<int>();
+    s.ptotal = ss->lazy ? ss->ptotal.as<unsigned long long>() : nullptr;
+    s.qbest = ss->pq ? ss->pq_qbest.as<unsigned>() : nullptr;
     return LF_OK;
 }
 
@@ -953,7 +985,6 @@ static int session_prologue(lf_session* ss) {
         ++ss->kernels;
     }
     if (ss->pq) {
-        LF_CUDA(cudaMemsetAsync(ss->pq_qbest.p, 0x7f, sizeof(unsigned) * Q, st2));   // 3.4e38: above any distance
         LF_CUDA(launch_project_queries(ss->d_q, Q, idx, ss->qcp.as<int8_t>(), ss->qmp.as<float4>(), st2));
         ++ss->kernels;
     }
@@ -964,13 +995,7 @@ static int session_prologue(lf_session* ss) {
         ++ss->kernels;
     }
     LF_CUDA(cudaEventRecord(ss->join_ev, st2));
-    LF_CUDA(cudaMemsetAsync(ss->ea_count.p, 0, sizeof(unsigned long long) * 4, st));
-    LF_CUDA(cudaMemsetAsync(ss->round_ctr.p, 0, sizeof(int), st));
-    if (ss->lazy) {
-        LF_CUDA(cudaMemsetAsync(ss->pcount.p, 0, sizeof(int) * Q, st));
-        LF_CUDA(cudaMemsetAsync(ss->preq.p, 0, sizeof(int) * Q, st));
-        LF_CUDA(cudaMemsetAsync(ss->ptotal.p, 0, sizeof(unsigned long long), st));
-    }
+    // (ea_count, round counter, pcount / preq / ptotal, qbest, counters: init_state_kernel)
     if (o.h_profile) {
         ss->prof = true;
         for (int i = 0; i < LF_N_PROF; ++i) o.h_profile[i] = 0.0;
@@ -1051,9 +1076,8 @@ static int predict_pass(lf_session* ss, int all) {
         LF_CUDA(cudaEventCreate(&e1));
         LF_CUDA(cudaEventRecord(e0, st));
     }
-    LF_CUDA(cudaMemsetAsync(ss->fhist.p, 0, sizeof(int) * std::max(1, F), st));
     pairs_range_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s, ss->pcount.as<int>(), ss->pstart.as<int>(),
-                                                                         ss->pend.as<int>(), all);
+                                                                         ss->pend.as<int>(), all, ss->fhist.as<int>(), F);
     LF_CUDA(cudaGetLastError());
     const int64_t Lr = idx.n_leaves;
     const unsigned pgrid = (unsigned)((Q * ((Lr + PAIR_SPAN - 1) / PAIR_SPAN) * 32 + 255) / 256);
@@ -1090,9 +1114,16 @@ static int round_kernels(lf_session* ss, int* counts, bool round0, cudaEvent_t* 
     const int64_t Q = ss->Q;
     s.n_active = counts;
     s.n_predict = counts + 2;
-    LF_CUDA(cudaMemsetAsync(counts, 0, sizeof(int) * 3, st));
+    {   // stream-ordered rounds alternate two count slots: this round's merge zeroes the other
+        int* base = ss->n_active.as<int>();
+        s.zero_counts = ss->capturing ? nullptr : (counts == base ? base + 4 : base);
+    }
+    // the round's counters: zeroed by the previous round's consumer (graph: round_cond_kernel
+    // after reading them; stream-ordered rounds alternate two slots, each zeroed by the
+    // merge two rounds later's predecessor -- here, simply by the merge of the round
+    // before, whose slot is the other one); the task counter chunk_off[Q] by the merge
+    // of the round before, the entry counter by the plan kernel (init_state for round 0)
     if (ev) cudaEventRecord(ev[0], st);
-    LF_CUDA(cudaMemsetAsync(s.chunk_off + Q, 0, sizeof(long long), st));   // the round's task counter
     if (round0 && ss->pruned)
         first_leaf_plan_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s, idx, ss->plb.as<double>(),
                                                                                    ss->pnode.as<int>(), ss->W);
@@ -1287,11 +1318,12 @@ static int check_args(const lf_index* idx, int64_t Q, const lf_search_opts* opts
 // keeps the loop going while any walk is active.  A search is then a query copy,
 // one graph launch and the result copies: no host round trips, no per-call
 // allocations, tensor-map encodes or launch latency between rounds.
-__global__ void round_cond_kernel(const int* __restrict__ counts, int* __restrict__ d_round, int max_rounds,
+__global__ void round_cond_kernel(int* __restrict__ counts, int* __restrict__ d_round, int max_rounds,
                                   cudaGraphConditionalHandle h) {
     const int r = *d_round + 1;
     *d_round = r;
     cudaGraphSetConditional(h, (counts[0] > 0 && r < max_rounds) ? 1u : 0u);
+    for (int i = 0; i < 3; ++i) counts[i] = 0;     // the next round's counters (no memset node)
 }
 
 static int plan_capture(lf_session* ss, cudaStream_t cs, cudaStream_t cs2, int64_t* d_ids, double* d_dists,
@@ -1301,6 +1333,7 @@ static int plan_capture(lf_session* ss, cudaStream_t cs, cudaStream_t cs2, int64
     int* counts = ss->n_active.as<int>();
     const int max_rounds = 2 * std::max(1, ss->idx.n_leaves) + 8;
     ss->st = cs;
+    ss->capturing = true;
     LF_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
     int rc = session_prologue(ss);
     if (!rc) rc = round_kernels(ss, counts, true, nullptr);
@@ -1369,6 +1402,7 @@ static int plan_capture(lf_session* ss, cudaStream_t cs, cudaStream_t cs2, int64
     }
     cudaGraph_t full = nullptr;
     const cudaError_t ee = cudaStreamEndCapture(cs, &full);
+    ss->capturing = false;
     if (!rc && ee != cudaSuccess) rc = fail(LF_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ee));
     if (rc) {
         if (full) cudaGraphDestroy(full);
