@@ -61,6 +61,7 @@ struct RoundState {
     int* pq_xn;                  // exact-tail list length: zeroed by the int8 stage
     int* cnt_all;                // [8] round counters (both slots): zeroed by init_state
     int* zero_counts;            // stream-ordered rounds: the next round's counter slot, zeroed by merge
+    unsigned long long* cand16;  // k = 1 entry tail: per task (d bits, id), 16-byte aligned, min'ed by a 128-bit CAS, or NULL
     int* rctr;                   // graph round counter, or NULL: zeroed by init_state
     unsigned long long* ptotal;  // pair total (profiling), or NULL: zeroed by init_state
     unsigned* qbest;             // seeded round 0: per-query seed minimum, set to 3.4e38 by init_state
@@ -176,8 +177,7 @@ struct PQOverflow {
     // codes rank nearest and prunes with that distance; qbest [Q] shares the best seed of
     // a query's tasks (float bits, atomicMin).  nullptr: no seeding.
     unsigned* qbest;
-    double* xd;                               // k = 1 entry tail: exact distances of the listed entries
-    int* xlist;                               // [cap] entries re-read exactly (k = 1 entry tail)
+    int* xlist;                               // [cap] entries re-read exactly (k = 1 entry tail; s.cand16 set)
     int* xn;                                  // their count
 };
 int pq_scan_warps();                          // warps of one scan_pq_kernel launch

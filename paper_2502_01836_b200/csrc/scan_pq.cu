@@ -411,7 +411,10 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
         if (ns == 0) {
             if (lane == 0) {
                 surv_cnt[t] = 0;
-                if (ov.xd != nullptr) { s.cand_d[t] = kInf; s.cand_i[t] = LLONG_MAX; }   // k = 1 entry tail
+                if (s.cand16 != nullptr) {                       // k = 1 entry tail
+                    s.cand16[2 * t] = (unsigned long long)__double_as_longlong(kInf);
+                    s.cand16[2 * t + 1] = (unsigned long long)LLONG_MAX;
+                }
             }
             continue;
         }
@@ -441,7 +444,10 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
                 surv_cnt[t] = ns;
                 ov.base[t] = base;
                 ov.thr[t] = __float_as_uint(thr_f);
-                if (ov.xd != nullptr) { s.cand_d[t] = kInf; s.cand_i[t] = LLONG_MAX; }   // k = 1 entry tail
+                if (s.cand16 != nullptr) {                       // k = 1 entry tail
+                    s.cand16[2 * t] = (unsigned long long)__double_as_longlong(kInf);
+                    s.cand16[2 * t + 1] = (unsigned long long)LLONG_MAX;
+                }
             }
             continue;
         }
@@ -451,6 +457,11 @@ __global__ void __launch_bounds__(PQW<KP>::WARPS * 32) scan_pq_kernel(RoundState
         if (ov.qc8 != nullptr) c_fall += (unsigned long long)ns;
         pq_select(s, t, lane, ns, bsf, [&](int i) { return dist_w[i]; },
                   [&](int i) { return idx.d_row_id[r0 + rows_w[i]]; });
+        if (s.cand16 != nullptr && lane == 0) {          // (lane 0 wrote the selection)
+            const long long ci = s.cand_i[t];
+            s.cand16[2 * t] = (unsigned long long)__double_as_longlong(ci < 0 ? kInf : s.cand_d[t]);
+            s.cand16[2 * t + 1] = (unsigned long long)(ci < 0 ? LLONG_MAX : ci);
+        }
         __syncwarp();
     }
     if (s.ea_count != nullptr && lane == 0 && c_rows > 0) {
@@ -679,10 +690,10 @@ __global__ void __launch_bounds__(PQT_WARPS * 32) pq_tail_kernel(RoundState s, l
 //   e0: thread per entry -- the entries whose int8 lower bound reaches their task's
 //       final threshold (~3% of them) are compacted into a list;
 //   e1: 8 lanes per listed entry re-read the row exactly (all loads in flight) and
-//       min it into the task's candidate distance (the bits of non-negative doubles
-//       order like the values);
-//   e2: each task gets the smallest row id among its entries at that distance
-//       (tree.py:207-214 tie rule).
+//       fold (distance, row id) into the task's pair by a 128-bit compare-and-swap
+//       loop -- the lexicographic minimum, i.e. the smallest id among equal distances
+//       (tree.py:207-214 tie rule), in the same pass.  (A separate tie-break pass
+//       after a 64-bit atomicMin of the distance cost one more launch per round.)
 __global__ void pq_tail_e0_kernel(PQOverflow ov) {
     const long long n = min((long long)*ov.n, (long long)ov.cap);
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
@@ -737,8 +748,30 @@ __global__ void __launch_bounds__(256) pq_tail_e1_kernel(RoundState s, lf_index 
         acc += __shfl_xor_sync(0xffffffffu, acc, 1);
         if (go && sl == 0) {
             const double d = sqrt(acc);
-            ov.xd[i] = d;
-            atomicMin(reinterpret_cast<unsigned long long*>(s.cand_d) + en.x, (unsigned long long)__double_as_longlong(d));
+            {
+                // (d, id) lexicographic minimum per task in one 128-bit CAS loop: the id
+                // tie-break (tree.py:207-214) without a second pass
+                const long long id = idx.d_row_id[ent_row(en)];
+                unsigned long long* c = s.cand16 + 2 * (long long)en.x;
+                // (starts from the initial value: the CAS returns the current pair atomically)
+                unsigned long long cx = (unsigned long long)__double_as_longlong(kInf), cy = (unsigned long long)LLONG_MAX;
+                while (pair_less(d, id, __longlong_as_double((long long)cx), (long long)cy)) {
+                    unsigned long long ox, oy;
+                    asm volatile(
+                        "{\n\t.reg .b128 cmp, val, old;\n\t"
+                        "mov.b128 cmp, {%2, %3};\n\t"
+                        "mov.b128 val, {%4, %5};\n\t"
+                        "atom.cas.relaxed.gpu.b128 old, [%6], cmp, val;\n\t"
+                        "mov.b128 {%0, %1}, old;\n\t}"
+                        : "=l"(ox), "=l"(oy)
+                        : "l"(cx), "l"(cy), "l"((unsigned long long)__double_as_longlong(d)), "l"((unsigned long long)id),
+                          "l"(c)
+                        : "memory");
+                    if (ox == cx && oy == cy) break;
+                    cx = ox;
+                    cy = oy;
+                }
+            }
         }
     }
     if (s.ea_count != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && n > 0) {
@@ -747,14 +780,6 @@ __global__ void __launch_bounds__(256) pq_tail_e1_kernel(RoundState s, lf_index 
     }
 }
 
-__global__ void pq_tail_e2_kernel(RoundState s, lf_index idx, PQOverflow ov) {
-    const int n = *ov.xn;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int4 en = ov.ent[ov.xlist[i]];
-        if (ov.xd[i] == s.cand_d[en.x])
-            atomicMin(reinterpret_cast<unsigned long long*>(s.cand_i) + en.x, (unsigned long long)idx.d_row_id[ent_row(en)]);
-    }
-}
 
 cudaError_t launch_project_queries(const float* q, int64_t Q, const lf_index& idx, int8_t* qc, float4* qm,
                                    cudaStream_t st) {
@@ -800,10 +825,9 @@ cudaError_t launch_scan_pq(const RoundState& s, const lf_index& idx, const float
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
-    if (ov.xd != nullptr) {                          // k = 1: entry-parallel tail
+    if (s.cand16 != nullptr) {                       // k = 1: entry-parallel tail
         pq_tail_e0_kernel<<<sm_count() * 8, 256, 0, st>>>(ov);
         pq_tail_e1_kernel<<<sm_count() * 4, 256, 0, st>>>(s, idx, q, ov);
-        pq_tail_e2_kernel<<<sm_count() * 2, 256, 0, st>>>(s, idx, ov);
         return cudaGetLastError();
     }
     const long long warps = std::min<long long>(max_tasks, (long long)sm_count() * 64);

@@ -122,10 +122,12 @@ __global__ void plan_warp_kernel(RoundState s, lf_index idx) {
             const unsigned smask = __ballot_sync(0xffffffffu, scan);
             if ((bmask | smask) == 0u && !s.want_trace && cur + 32 < len) {
                 // a whole batch of filter-pruned leaves (the long stretches of a walk under
-                // a tight bound): counters only, no selection bookkeeping
-                c_vis += __popc(__ballot_sync(0xffffffffu, visit));
-                c_inf += __popc(__ballot_sync(0xffffffffu, fs >= 0));
-                c_fp += __popc(__ballot_sync(0xffffffffu, fpr));
+                // a tight bound): counters only, no selection bookkeeping.  No break and no
+                // scan: every visited leaf has a filter and was pruned by it
+                const int nv = __popc(__ballot_sync(0xffffffffu, visit));
+                c_vis += nv;
+                c_inf += nv;
+                c_fp += nv;
                 cur += 32;
                 lb_c = lb_n; gp_c = gp_n; rec_c = rec_n; ad_c = ad_n;
                 continue;
@@ -538,8 +540,15 @@ __global__ void merge_kernel(RoundState s) {
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const long long i = i0 + 32 * u;
-                iv[u] = i < nc ? ci[i] : -1;
-                dv[u] = i < nc ? cd[i] : kInf;
+                if (s.cand16 != nullptr) {              // k = 1 entry tail: (d bits, id) pairs
+                    const ulonglong2 c = i < nc ? reinterpret_cast<const ulonglong2*>(s.cand16)[c0 + i]
+                                                : make_ulonglong2(0ull, ~0ull);
+                    iv[u] = (long long)c.y;
+                    dv[u] = __longlong_as_double((long long)c.x);
+                } else {
+                    iv[u] = i < nc ? ci[i] : -1;
+                    dv[u] = i < nc ? cd[i] : kInf;
+                }
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u)
@@ -742,7 +751,8 @@ struct lf_session {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pev;   // profiling: per prediction pass
     bool q8 = false;                 // int8-bounded scan (query codes quantised once in begin)
     bool pq = false;                 // two-stage scan over the projected shadow (d_Xp)
-    lf::Scratch qcp, qmp, pq_cnt, pq_trows, pq_oent, pq_on, pq_obase, pq_wrows, pq_wdist, pq_lo8, pq_thr, pq_qbest, pq_xd, pq_xlist, pq_xn;
+    lf::Scratch qcp, qmp, pq_cnt, pq_trows, pq_oent, pq_on, pq_obase, pq_wrows, pq_wdist, pq_lo8, pq_thr, pq_qbest, pq_xlist, pq_xn,
+        pq_c16;
     int pq_cap = lf::PQ_OVER_CAP;    // survivor entry capacity (LF_PQ_OVER_CAP: tests of the full-list path)
     int64_t max_tasks = 1;
     int* h_active = nullptr;         // pinned [2 slots][4]: active, -, predict requests
@@ -945,9 +955,9 @@ static int session_alloc(lf_session* ss) {
         LF_CUDA(ss->pq_thr.alloc(sizeof(unsigned) * max_tasks, st));
         LF_CUDA(ss->pq_qbest.alloc(sizeof(unsigned) * Q, st));
         if (s.k == 1 && ss->q8) {
-            LF_CUDA(ss->pq_xd.alloc(sizeof(double) * ss->pq_cap, st));
             LF_CUDA(ss->pq_xlist.alloc(sizeof(int) * ss->pq_cap, st));
             LF_CUDA(ss->pq_xn.alloc(sizeof(int), st));
+            LF_CUDA(ss->pq_c16.alloc(16 * max_tasks, st));
         }
     }
     if (ss->q8) {
@@ -1137,6 +1147,9 @@ static int round_kernels(lf_session* ss, int* counts, bool round0, cudaEvent_t* 
     // with one exactly scored row per task (scan_pq_kernel SEED); for k > 1 (or
     // LF_SCAN_ROUND0=q8) the first round runs the full-length int8 scan
     const bool seed = round0 && s.k == 1 && round0_seeded();
+    // k = 1 entry tail: the per-task (d, id) pairs, min'ed by 128-bit CAS (merge reads them)
+    s.cand16 = (ea && ss->pq && (!round0 || !ss->q8 || seed) && s.k == 1 && ss->q8)
+                   ? ss->pq_c16.as<unsigned long long>() : nullptr;
     if (ea && ss->pq && (!round0 || !ss->q8 || seed)) {
         const PQOverflow ov{ss->pq_oent.as<int4>(), ss->pq_on.as<int>(),
                             ss->pq_obase.as<int>(), ss->pq_cap, ss->pq_wrows.as<unsigned short>(),
@@ -1144,7 +1157,6 @@ static int round_kernels(lf_session* ss, int* counts, bool round0, cudaEvent_t* 
                             ss->q8 ? ss->qm8.as<float4>() : nullptr, (idx.m + 255) / 256 * 256,
                             ss->pq_lo8.as<float>(), ss->pq_thr.as<unsigned>(),
                             seed ? ss->pq_qbest.as<unsigned>() : nullptr,
-                            s.k == 1 && ss->q8 ? ss->pq_xd.as<double>() : nullptr,
                             s.k == 1 && ss->q8 ? ss->pq_xlist.as<int>() : nullptr,
                             s.k == 1 && ss->q8 ? ss->pq_xn.as<int>() : nullptr};
         if (round0) ss->order_seed = seed && ss->pruned && !std::getenv("LF_ORDER_AFTER_ROUND0");
