@@ -37,6 +37,45 @@ namespace lf {
 // and the R-th selected leaf, and prefix counts place selections and trace
 // entries in visit order.  Counters, selections and traces are identical to a
 // serial walk of the same entries (tree.py:256-297 with the round-start bsf).
+// k = 1 with the entry tail's (distance, id) pairs: fold the query's tasks of the round
+// just scanned into its best (warp per query, eight pairs in flight per lane).  (Folding
+// them in the next round's plan kernel instead, to save the merge launch of every graph
+// round >= 1: 1.424 vs 1.427 ms per batch -- not kept.)
+__device__ __forceinline__ void merge_pairs_k1(const RoundState& s, int64_t q, int lane) {
+    if (s.n_sel[q] == 0) return;
+    const int tn = s.top_n[q];
+    double bd = tn > 0 ? s.top_d[q] : kInf;
+    long long bi = tn > 0 ? s.top_i[q] : LLONG_MAX;
+    const long long c0 = s.chunk_off[q], nc = s.chunk_cnt[q];
+    const ulonglong2* cp = reinterpret_cast<const ulonglong2*>(s.cand16) + c0;
+    for (long long i0 = lane; i0 < nc; i0 += 256) {
+        ulonglong2 c[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const long long i = i0 + 32 * u;
+            c[u] = i < nc ? cp[i] : make_ulonglong2(0ull, ~0ull);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const long long id = (long long)c[u].y;
+            const double d = __longlong_as_double((long long)c[u].x);
+            if (id >= 0 && pair_less(d, id, bd, bi)) { bd = d; bi = id; }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double xd = __shfl_xor_sync(0xffffffffu, bd, o);
+        const long long xi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (pair_less(xd, xi, bd, bi)) { bd = xd; bi = xi; }
+    }
+    if (lane == 0 && bi != LLONG_MAX) {
+        s.top_d[q] = bd;
+        s.top_i[q] = bi;
+        s.top_n[q] = 1;
+    }
+    __syncwarp();
+}
+
 #ifndef LF_PLAN_PF
 #define LF_PLAN_PF 8
 #endif
@@ -531,6 +570,10 @@ __global__ void merge_kernel(RoundState s) {
         }
     }
 
+    if (s.k == 1 && s.cand16 != nullptr) {
+        merge_pairs_k1(s, q, lane);
+        return;
+    }
     if (s.k == 1) {                            // one pass, eight candidates' loads in flight per lane
         double bd = tn > 0 ? td[0] : kInf;
         long long bi = tn > 0 ? ti[0] : LLONG_MAX;
@@ -540,15 +583,8 @@ __global__ void merge_kernel(RoundState s) {
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const long long i = i0 + 32 * u;
-                if (s.cand16 != nullptr) {              // k = 1 entry tail: (d bits, id) pairs
-                    const ulonglong2 c = i < nc ? reinterpret_cast<const ulonglong2*>(s.cand16)[c0 + i]
-                                                : make_ulonglong2(0ull, ~0ull);
-                    iv[u] = (long long)c.y;
-                    dv[u] = __longlong_as_double((long long)c.x);
-                } else {
-                    iv[u] = i < nc ? ci[i] : -1;
-                    dv[u] = i < nc ? cd[i] : kInf;
-                }
+                iv[u] = i < nc ? ci[i] : -1;
+                dv[u] = i < nc ? cd[i] : kInf;
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u)
@@ -1134,6 +1170,15 @@ static int round_kernels(lf_session* ss, int* counts, bool round0, cudaEvent_t* 
     // before, whose slot is the other one); the task counter chunk_off[Q] by the merge
     // of the round before, the entry counter by the plan kernel (init_state for round 0)
     if (ev) cudaEventRecord(ev[0], st);
+    // the bounded scans take m % 4 == 0 (codes zero-padded to a multiple of 64)
+    const bool ea = o.early_abandon && !s.want_trace && idx.m <= 512 && scan_variant() != 0 && ss->q8;
+    // round 0 has no best-so-far yet: for k = 1 the projected scan seeds its threshold
+    // with one exactly scored row per task (scan_pq_kernel SEED); for k > 1 (or
+    // LF_SCAN_ROUND0=q8) the first round runs the full-length int8 scan
+    const bool seed = round0 && s.k == 1 && round0_seeded();
+    const bool pq_round = ea && ss->pq && (!round0 || !ss->q8 || seed);
+    // k = 1 entry tail: the per-task (d, id) pairs, min'ed by 128-bit CAS (merge reads them)
+    s.cand16 = (pq_round && s.k == 1 && ss->q8) ? ss->pq_c16.as<unsigned long long>() : nullptr;
     if (round0 && ss->pruned)
         first_leaf_plan_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s, idx, ss->plb.as<double>(),
                                                                                    ss->pnode.as<int>(), ss->W);
@@ -1141,16 +1186,7 @@ static int round_kernels(lf_session* ss, int* counts, bool round0, cudaEvent_t* 
         plan_warp_kernel<<<(unsigned)((Q * 32 + 255) / 256), 256, 0, st>>>(s, idx);
     if (ev) cudaEventRecord(ev[1], st);
     cudaError_t ce;
-    // the bounded scans take m % 4 == 0 (codes zero-padded to a multiple of 64)
-    const bool ea = o.early_abandon && !s.want_trace && idx.m <= 512 && scan_variant() != 0 && ss->q8;
-    // round 0 has no best-so-far yet: for k = 1 the projected scan seeds its threshold
-    // with one exactly scored row per task (scan_pq_kernel SEED); for k > 1 (or
-    // LF_SCAN_ROUND0=q8) the first round runs the full-length int8 scan
-    const bool seed = round0 && s.k == 1 && round0_seeded();
-    // k = 1 entry tail: the per-task (d, id) pairs, min'ed by 128-bit CAS (merge reads them)
-    s.cand16 = (ea && ss->pq && (!round0 || !ss->q8 || seed) && s.k == 1 && ss->q8)
-                   ? ss->pq_c16.as<unsigned long long>() : nullptr;
-    if (ea && ss->pq && (!round0 || !ss->q8 || seed)) {
+    if (pq_round) {
         const PQOverflow ov{ss->pq_oent.as<int4>(), ss->pq_on.as<int>(),
                             ss->pq_obase.as<int>(), ss->pq_cap, ss->pq_wrows.as<unsigned short>(),
                             ss->pq_wdist.as<double>(), ss->q8 ? ss->qc8.as<int8_t>() : nullptr,
