@@ -12,7 +12,12 @@
 
 namespace lf {
 
-template <int NCH>
+// MINB resident CTAs per SM (register and shared-memory budgets follow).  Each CTA
+// works one task at a time and its tail (survivor list, exact re-check, per-task top-k)
+// is separated by CTA barriers, so more resident CTAs keep the memory pipe busy between
+// tasks: m <= 256 runs 4 per SM (C5, 100M x 96, k = 10: 46.3 -> 31.3 ms per batch;
+// 25M x 256 k = 10: 10.29 -> 10.11 ms), longer rows keep 2.
+template <int NCH, int MINB = 2>
 struct Q8Cfg {
     static constexpr int M = NCH * 64;
     static constexpr int P = (M + 255) / 256;              // 256-code passes per row (16 codes per lane)
@@ -22,7 +27,8 @@ struct Q8Cfg {
     static constexpr int QM_OFF = QC_OFF + P * 256;         // query metadata float4
     static constexpr int HDR_OFF = QM_OFF + 16;             // {r0 (i64), q (i32), nrows (i32)}
     static constexpr int STAGE_BYTES = (HDR_OFF + 16 + 127) / 128 * 128;
-    static constexpr int STAGES = (81920 / CODE_BYTES) < 2 ? 2 : ((81920 / CODE_BYTES) > 8 ? 8 : 81920 / CODE_BYTES);
+    static constexpr int BUDGET = MINB == 2 ? 81920 : MINB == 3 ? 45056 : 32768;
+    static constexpr int STAGES = (BUDGET / CODE_BYTES) < 2 ? 2 : ((BUDGET / CODE_BYTES) > 8 ? 8 : BUDGET / CODE_BYTES);
     static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
     static constexpr int LO_OFF = BAR_OFF + 2 * STAGES * 8;
     static constexpr int SR_OFF = LO_OFF + CH * 4;
@@ -33,12 +39,12 @@ struct Q8Cfg {
     static constexpr int SMEM = MISC_OFF + 32;
 };
 
-template <int NCH>
-__global__ void __launch_bounds__(Q8_THREADS, 2) scan_q8_kernel(RoundState s, lf_index idx,
-                                                                const float* __restrict__ queries,
-                                                                const int8_t* __restrict__ qcodes,
-                                                                const float4* __restrict__ qmeta) {
-    using Cfg = Q8Cfg<NCH>;
+template <int NCH, int MINB = 2>
+__global__ void __launch_bounds__(Q8_THREADS, MINB) scan_q8_kernel(RoundState s, lf_index idx,
+                                                                   const float* __restrict__ queries,
+                                                                   const int8_t* __restrict__ qcodes,
+                                                                   const float4* __restrict__ qmeta) {
+    using Cfg = Q8Cfg<NCH, MINB>;
     constexpr int M = Cfg::M, P = Cfg::P, S = Cfg::STAGES;
     extern __shared__ __align__(128) unsigned char q8_smem[];
     unsigned char* stages = q8_smem;
@@ -315,21 +321,22 @@ __global__ void __launch_bounds__(Q8_THREADS, 2) scan_q8_kernel(RoundState s, lf
         }
     }
 }
-template <int NCH>
+template <int NCH, int MINB = 2>
 static cudaError_t launch_q8_nch(const RoundState& s, const lf_index& idx, const float* q, const int8_t* qc8,
                                  const float4* qm8, cudaStream_t st) {
-    if (cudaError_t e = smem_optin(scan_q8_kernel<NCH>, Q8Cfg<NCH>::SMEM); e != cudaSuccess) return e;
-    scan_q8_kernel<NCH><<<sm_count() * 2, Q8_THREADS, Q8Cfg<NCH>::SMEM, st>>>(s, idx, q, qc8, qm8);
+    using Cfg = Q8Cfg<NCH, MINB>;
+    if (cudaError_t e = smem_optin(scan_q8_kernel<NCH, MINB>, Cfg::SMEM); e != cudaSuccess) return e;
+    scan_q8_kernel<NCH, MINB><<<sm_count() * MINB, Q8_THREADS, Cfg::SMEM, st>>>(s, idx, q, qc8, qm8);
     return cudaGetLastError();
 }
 
 cudaError_t launch_scan_q8(const RoundState& s, const lf_index& idx, const float* q, const int8_t* qc8,
                            const float4* qm8, cudaStream_t st) {
     switch ((idx.m + 63) / 64) {
-        case 1: return launch_q8_nch<1>(s, idx, q, qc8, qm8, st);
-        case 2: return launch_q8_nch<2>(s, idx, q, qc8, qm8, st);
-        case 3: return launch_q8_nch<3>(s, idx, q, qc8, qm8, st);
-        case 4: return launch_q8_nch<4>(s, idx, q, qc8, qm8, st);
+        case 1: return launch_q8_nch<1, 4>(s, idx, q, qc8, qm8, st);
+        case 2: return launch_q8_nch<2, 4>(s, idx, q, qc8, qm8, st);
+        case 3: return launch_q8_nch<3, 4>(s, idx, q, qc8, qm8, st);
+        case 4: return launch_q8_nch<4, 4>(s, idx, q, qc8, qm8, st);
         case 5: return launch_q8_nch<5>(s, idx, q, qc8, qm8, st);
         case 6: return launch_q8_nch<6>(s, idx, q, qc8, qm8, st);
         case 7: return launch_q8_nch<7>(s, idx, q, qc8, qm8, st);

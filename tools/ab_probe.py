@@ -27,12 +27,12 @@ for rep in range(2):
                 k, v = kv.split("=")
                 os.environ[k] = v
         e.__dict__.pop("_plans", None)
-        r = search_queries(e, Q, 1, target=0.99)
+        r = search_queries(e, Q, args.k, target=0.99)
         s = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
         for _ in range(20):
-            search_queries(e, Q, 1, target=0.99, copy_out=False)
+            search_queries(e, Q, args.k, target=0.99, copy_out=False)
         e1.record(s)
         torch.cuda.synchronize()
         print(f"[{rep}] {cfg:40s} ms={e0.elapsed_time(e1) / 20:7.3f} scanned={int(r.stats[:, 5].sum())} "
