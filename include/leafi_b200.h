@@ -53,7 +53,7 @@ typedef struct lf_index {
     const double* d_env_max;     /* [n_seg][n_nodes] SoA envelope maxima */
     const int32_t* d_leaf_filter;/* [n_leaves] filter slot or -1 (may be NULL) */
     /* optional int8 shadow of X for the bounded scan (lf_quantize_rows); all NULL = unused */
-    const int8_t* d_X8;          /* [n_series][roundup(m, 64)] round(x / scale), zero-padded */
+    const int8_t* d_X8;          /* [n_series][roundup(m, 32)] round(x / scale), zero-padded */
     const float* d_qmeta;        /* [n_series][4] per row: scale = max|x| / 127, sum of squared
                                     codes (exact in fp32), ||scale * code - x||_2 rounded up, 0 */
     /* optional projected shadow for the two-stage scan (NULL = unused): an orthonormal

@@ -17,7 +17,7 @@ __global__ void quantize_kernel(const float* __restrict__ X, int64_t n, int m, i
     const int lane = threadIdx.x & 31;
     if (r >= n) return;
     const float* x = X + r * m;
-    const int m8 = (m + 63) / 64 * 64;            // code rows are zero-padded to a multiple of 64
+    const int m8 = (m + 31) / 32 * 32;            // code rows are zero-padded to a multiple of 32
     float mx = 0.f;
     for (int i = lane; i < m; i += 32) mx = fmaxf(mx, fabsf(x[i]));
 #pragma unroll

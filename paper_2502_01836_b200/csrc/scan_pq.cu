@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(256, MINB) pq_q8_bound_kernel(RoundState s, lf
     if (blockIdx.x == 0 && threadIdx.x == 0 && ov.xn != nullptr) *ov.xn = 0;   // the exact tail's list
     const long long n = min((long long)*ov.n, (long long)ov.cap);
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-    const int M8 = FIX256 ? 256 : (idx.m + 63) / 64 * 64;
+    const int M8 = FIX256 ? 256 : (idx.m + 31) / 32 * 32;   // the shadow's row stride
     unsigned long long cnt = 0;
     // FIX256 (m <= 256): a lane's 32 query-code bytes stay in registers while its
     // group's entries keep the same query (entries of a task are contiguous), and the
@@ -818,7 +818,7 @@ cudaError_t launch_scan_pq(const RoundState& s, const lf_index& idx, const float
         // a per-warp shared-memory ring of 8-entry pieces -- cp.async.bulk per row and
         // mbarrier: 1.54, 16-byte cp.async with 4 / 6 / 8 pieces in flight: 1.68 / 1.62 /
         // 1.82, vs 1.48 ms for this kernel)
-        if ((idx.m + 63) / 64 * 64 == 256)
+        if ((idx.m + 31) / 32 * 32 == 256)
             pq_q8_bound_kernel<true><<<sm_count() * 8, 256, 0, st>>>(s, idx, ov);
         else
             pq_q8_bound_kernel<false><<<sm_count() * 8, 256, 0, st>>>(s, idx, ov);

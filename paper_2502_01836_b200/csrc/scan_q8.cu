@@ -17,9 +17,9 @@ namespace lf {
 // is separated by CTA barriers, so more resident CTAs keep the memory pipe busy between
 // tasks: m <= 256 runs 4 per SM (C5, 100M x 96, k = 10: 46.3 -> 31.3 ms per batch;
 // 25M x 256 k = 10: 10.29 -> 10.11 ms), longer rows keep 2.
-template <int NCH, int MINB = 2>
+template <int M32, int MINB = 2>
 struct Q8Cfg {
-    static constexpr int M = NCH * 64;
+    static constexpr int M = M32 * 32;                      // code row stride (roundup(m, 32))
     static constexpr int P = (M + 255) / 256;              // 256-code passes per row (16 codes per lane)
     static constexpr int CODE_BYTES = Q8_ROWS * M;
     static constexpr int META_OFF = CODE_BYTES;             // 64 x float4 row metadata
@@ -39,12 +39,13 @@ struct Q8Cfg {
     static constexpr int SMEM = MISC_OFF + 32;
 };
 
-template <int NCH, int MINB = 2>
+template <int M32, int MINB = 2>
 __global__ void __launch_bounds__(Q8_THREADS, MINB) scan_q8_kernel(RoundState s, lf_index idx,
                                                                    const float* __restrict__ queries,
                                                                    const int8_t* __restrict__ qcodes,
                                                                    const float4* __restrict__ qmeta) {
-    using Cfg = Q8Cfg<NCH, MINB>;
+    using Cfg = Q8Cfg<M32, MINB>;
+    constexpr int NCH = (M32 * 32 + 63) / 64;          // 64-float chunks of the fp32 row (exact re-check)
     constexpr int M = Cfg::M, P = Cfg::P, S = Cfg::STAGES;
     extern __shared__ __align__(128) unsigned char q8_smem[];
     unsigned char* stages = q8_smem;
@@ -321,26 +322,34 @@ __global__ void __launch_bounds__(Q8_THREADS, MINB) scan_q8_kernel(RoundState s,
         }
     }
 }
-template <int NCH, int MINB = 2>
-static cudaError_t launch_q8_nch(const RoundState& s, const lf_index& idx, const float* q, const int8_t* qc8,
-                                 const float4* qm8, cudaStream_t st) {
-    using Cfg = Q8Cfg<NCH, MINB>;
-    if (cudaError_t e = smem_optin(scan_q8_kernel<NCH, MINB>, Cfg::SMEM); e != cudaSuccess) return e;
-    scan_q8_kernel<NCH, MINB><<<sm_count() * MINB, Q8_THREADS, Cfg::SMEM, st>>>(s, idx, q, qc8, qm8);
+template <int M32, int MINB = (M32 <= 8 ? 4 : 2)>
+static cudaError_t launch_q8_m(const RoundState& s, const lf_index& idx, const float* q, const int8_t* qc8,
+                               const float4* qm8, cudaStream_t st) {
+    using Cfg = Q8Cfg<M32, MINB>;
+    if (cudaError_t e = smem_optin(scan_q8_kernel<M32, MINB>, Cfg::SMEM); e != cudaSuccess) return e;
+    scan_q8_kernel<M32, MINB><<<sm_count() * MINB, Q8_THREADS, Cfg::SMEM, st>>>(s, idx, q, qc8, qm8);
     return cudaGetLastError();
 }
 
 cudaError_t launch_scan_q8(const RoundState& s, const lf_index& idx, const float* q, const int8_t* qc8,
                            const float4* qm8, cudaStream_t st) {
-    switch ((idx.m + 63) / 64) {
-        case 1: return launch_q8_nch<1, 4>(s, idx, q, qc8, qm8, st);
-        case 2: return launch_q8_nch<2, 4>(s, idx, q, qc8, qm8, st);
-        case 3: return launch_q8_nch<3, 4>(s, idx, q, qc8, qm8, st);
-        case 4: return launch_q8_nch<4, 4>(s, idx, q, qc8, qm8, st);
-        case 5: return launch_q8_nch<5>(s, idx, q, qc8, qm8, st);
-        case 6: return launch_q8_nch<6>(s, idx, q, qc8, qm8, st);
-        case 7: return launch_q8_nch<7>(s, idx, q, qc8, qm8, st);
-        case 8: return launch_q8_nch<8>(s, idx, q, qc8, qm8, st);
+    switch ((idx.m + 31) / 32) {                     // the shadow's row stride, in 32-byte units
+        case 1: return launch_q8_m<1>(s, idx, q, qc8, qm8, st);
+        case 2: return launch_q8_m<2>(s, idx, q, qc8, qm8, st);
+        case 3: return launch_q8_m<3>(s, idx, q, qc8, qm8, st);
+        case 4: return launch_q8_m<4>(s, idx, q, qc8, qm8, st);
+        case 5: return launch_q8_m<5>(s, idx, q, qc8, qm8, st);
+        case 6: return launch_q8_m<6>(s, idx, q, qc8, qm8, st);
+        case 7: return launch_q8_m<7>(s, idx, q, qc8, qm8, st);
+        case 8: return launch_q8_m<8>(s, idx, q, qc8, qm8, st);
+        case 9: return launch_q8_m<9>(s, idx, q, qc8, qm8, st);
+        case 10: return launch_q8_m<10>(s, idx, q, qc8, qm8, st);
+        case 11: return launch_q8_m<11>(s, idx, q, qc8, qm8, st);
+        case 12: return launch_q8_m<12>(s, idx, q, qc8, qm8, st);
+        case 13: return launch_q8_m<13>(s, idx, q, qc8, qm8, st);
+        case 14: return launch_q8_m<14>(s, idx, q, qc8, qm8, st);
+        case 15: return launch_q8_m<15>(s, idx, q, qc8, qm8, st);
+        case 16: return launch_q8_m<16>(s, idx, q, qc8, qm8, st);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -1170,7 +1170,7 @@ static int round_kernels(lf_session* ss, int* counts, bool round0, cudaEvent_t* 
     // before, whose slot is the other one); the task counter chunk_off[Q] by the merge
     // of the round before, the entry counter by the plan kernel (init_state for round 0)
     if (ev) cudaEventRecord(ev[0], st);
-    // the bounded scans take m % 4 == 0 (codes zero-padded to a multiple of 64)
+    // the bounded scans take m % 4 == 0 (codes zero-padded to a multiple of 32)
     const bool ea = o.early_abandon && !s.want_trace && idx.m <= 512 && scan_variant() != 0 && ss->q8;
     // round 0 has no best-so-far yet: for k = 1 the projected scan seeds its threshold
     // with one exactly scored row per task (scan_pq_kernel SEED); for k > 1 (or

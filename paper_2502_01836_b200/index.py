@@ -378,7 +378,7 @@ class DeviceIndex:
             self.X8 = self.qmeta = None
             n_rows, m = int(self.X.shape[0]), int(self.X.shape[1])
             if m % 4 == 0 and m <= 512 and n_rows:     # codes zero-padded to a multiple of 64
-                self.X8 = torch.empty((n_rows, (m + 63) // 64 * 64), dtype=torch.int8, device=dev)
+                self.X8 = torch.empty((n_rows, (m + 31) // 32 * 32), dtype=torch.int8, device=dev)
                 self.qmeta = torch.empty((n_rows, 4), dtype=torch.float32, device=dev)
                 _lib.check(_lib.lib().lf_quantize_rows(self.X.data_ptr(), n_rows, m, self.X8.data_ptr(),
                                                        self.qmeta.data_ptr(), _lib.stream_ptr()))
