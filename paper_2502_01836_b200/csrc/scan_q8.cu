@@ -114,10 +114,16 @@ __global__ void __launch_bounds__(Q8_THREADS, MINB) scan_q8_kernel(RoundState s,
     // ------------------------------------------------------------ consumers
     const int cw = warp - 1;
     const int ctid = threadIdx.x - 32;
-    const int hl = lane & 15;
+    // Rows of <= 128 codes (SHORT): 8 lanes per row, 16 codes each, the warp's 8 rows of a
+    // stage in two passes of 4; longer rows: 16 lanes per row and 256-code passes, a
+    // half-warp's 4 rows summed by a transposing butterfly.
+    constexpr bool SHORT = M <= 128;
+    const int hl = SHORT ? (lane & 7) : (lane & 15);
     const int rbase = cw * 8 + (lane >> 4) * 4;        // this half-warp's 4 rows of a stage
     const bool b8 = (hl & 8) != 0, b4 = (hl & 4) != 0;
-    const int myrow = rbase + (b8 ? 2 : 0) + (b4 ? 1 : 0);   // row whose total this lane ends with
+    // row whose total this lane ends with
+    const int myrow = SHORT ? cw * 8 + (hl & 1) * 4 + (lane >> 3) : rbase + (b8 ? 2 : 0) + (b4 ? 1 : 0);
+    const bool writer = SHORT ? hl < 2 : (hl & 3) == 0;
     int slot = 0;
     uint32_t ph = 0;
     int par = 0;
@@ -146,6 +152,25 @@ __global__ void __launch_bounds__(Q8_THREADS, MINB) scan_q8_kernel(RoundState s,
             const int rows = min(Q8_ROWS, nrows - j);
             const unsigned char* stg = stages + slot * Cfg::STAGE_BYTES;
             int d[4];
+            if constexpr (SHORT) {
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int r = cw * 8 + u * 4 + (lane >> 3);
+                    int dot = 0;
+                    if (r < rows && hl * 16 < M) {
+                        const int4 w = *reinterpret_cast<const int4*>(stg + r * M + hl * 16);
+                        dot = __dp4a(w.x, qw[0][0], dot);
+                        dot = __dp4a(w.y, qw[0][1], dot);
+                        dot = __dp4a(w.z, qw[0][2], dot);
+                        dot = __dp4a(w.w, qw[0][3], dot);
+                    }
+                    dot += __shfl_xor_sync(0xffffffffu, dot, 4);
+                    dot += __shfl_xor_sync(0xffffffffu, dot, 2);
+                    dot += __shfl_xor_sync(0xffffffffu, dot, 1);
+                    d[u] = dot;
+                }
+                d[0] = (hl & 1) ? d[1] : d[0];
+            } else {
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int r = rbase + u;
@@ -173,6 +198,7 @@ __global__ void __launch_bounds__(Q8_THREADS, MINB) scan_q8_kernel(RoundState s,
                 v += __shfl_xor_sync(0xffffffffu, v, 1);
                 d[0] = v;
             }
+            }
             if (myrow < rows) {
                 const float4 mr = *reinterpret_cast<const float4*>(stg + Cfg::META_OFF + myrow * 16);
                 const float sx2xx = mr.x * mr.x * mr.y;
@@ -182,7 +208,7 @@ __global__ void __launch_bounds__(Q8_THREADS, MINB) scan_q8_kernel(RoundState s,
                 const float lo = (sqrtf(fmaxf(d2 - tol, 0.f)) - e) * (1.f - 1e-6f);
                 const float hi = (sqrtf(fmaxf(d2 + tol, 0.f)) + e) * (1.f + 1e-6f);
                 hmin = fminf(hmin, hi);
-                if ((hl & 3) == 0) {
+                if (writer) {
                     lo_s[j + myrow] = lo;
                     if (s.k > 1) hi_s[j + myrow] = hi;
                 }
@@ -255,6 +281,7 @@ __global__ void __launch_bounds__(Q8_THREADS, MINB) scan_q8_kernel(RoundState s,
             const float* X0 = idx.d_X + r0 * mr;
             const float* qrow = queries + q * mr;
             const int hslot = cw * 2 + (lane >> 4);
+            const int hx = lane & 15;                    // 16 lanes per survivor row
             for (int b0 = 0; b0 < ns; b0 += 16) {
                 const int jj = b0 + hslot;
                 const bool v = jj < ns;
@@ -262,14 +289,14 @@ __global__ void __launch_bounds__(Q8_THREADS, MINB) scan_q8_kernel(RoundState s,
                 float4 x[NCH];
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch)
-                    x[ch] = (v && ch * 64 + hl * 4 < mr)
-                                ? __ldg(reinterpret_cast<const float4*>(X0 + (int64_t)r * mr) + ch * 16 + hl)
+                    x[ch] = (v && ch * 64 + hx * 4 < mr)
+                                ? __ldg(reinterpret_cast<const float4*>(X0 + (int64_t)r * mr) + ch * 16 + hx)
                                 : make_float4(0.f, 0.f, 0.f, 0.f);
                 double acc = 0.0;
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch) {
-                    const float4 qv = ch * 64 + hl * 4 < mr
-                                          ? __ldg(reinterpret_cast<const float4*>(qrow) + ch * 16 + hl)
+                    const float4 qv = ch * 64 + hx * 4 < mr
+                                          ? __ldg(reinterpret_cast<const float4*>(qrow) + ch * 16 + hx)
                                           : make_float4(0.f, 0.f, 0.f, 0.f);
                     const double d0 = (double)x[ch].x - (double)qv.x, d1 = (double)x[ch].y - (double)qv.y;
                     const double d2 = (double)x[ch].z - (double)qv.z, d3 = (double)x[ch].w - (double)qv.w;
@@ -278,7 +305,7 @@ __global__ void __launch_bounds__(Q8_THREADS, MINB) scan_q8_kernel(RoundState s,
                 }
 #pragma unroll
                 for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                if (v && hl == 0) surv_d[jj] = sqrt(acc);
+                if (v && hx == 0) surv_d[jj] = sqrt(acc);
             }
         }
         q8_cons_sync();
