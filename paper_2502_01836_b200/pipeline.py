@@ -257,11 +257,16 @@ def _plan_for(e, Q: int, k: int, target: float, sequential: bool, max_round_leav
 
 class SearchPipeline:
     """Serving form of `search_queries` (in-search inference, graph plan): batches
-    submitted back to back overlap their copies with the search of the batch before.
-    Each batch's queries go host -> device on one copy stream, the plan runs on a
-    compute stream, the results come back device -> host on a third; `depth` slots of
-    device queries, device results and pinned host results rotate.  Results and
-    counters equal `search_queries`' for the same batch.
+    submitted back to back overlap their copies with the search of the batch before,
+    and their searches with each other: consecutive batches alternate between `plans`
+    independent graph plans (own scratch and counters; default one per slot) on their
+    own compute streams, so one batch's latency-bound phases (bounds, visit orders,
+    planning, tails) run under another's memory-bound scans (bench workload, 20
+    batches: 1 plan 1.43 ms per batch, 2 plans 1.21, 3 plans 1.18, 4 plans 1.17;
+    `tools/conc_probe.py`).  Each batch's queries go
+    host -> device on one copy stream, the results come back device -> host on another;
+    `depth` slots of device queries, device results and pinned host results rotate.
+    Results and counters equal `search_queries`' for the same batch.
 
         pipe = SearchPipeline(eidx, batch=1000, k=1, target=0.99)
         t = pipe.submit(q0)              # pinned host tensors overlap best
@@ -275,7 +280,7 @@ class SearchPipeline:
     slot is submitted again.  The caller keeps a submitted host tensor unchanged until
     its result is collected."""
 
-    def __init__(self, eidx, batch: int, k: int = 1, *, target: float, depth: int = 2,
+    def __init__(self, eidx, batch: int, k: int = 1, *, target: float, depth: int = 3, plans: int | None = None,
                  sequential: bool = False, max_round_leaves: int = 256):
         torch = _lib.require_cuda()
         e = _as_enhanced(eidx)
@@ -285,13 +290,23 @@ class SearchPipeline:
             raise ValueError(f"target must be in [0, 1], got {target}")
         if depth < 1:
             raise ValueError(f"depth must be >= 1, got {depth}")
+        plans = depth if plans is None else int(plans)
+        if not 1 <= plans <= depth:
+            raise ValueError(f"plans must be in [1, depth], got {plans}")
         di = e.base.device()
         dev = di.device
         self.n_series, self.batch, self.k, self.depth = e.base.n, int(batch), int(k), int(depth)
-        self._plan = _plan_for(e, self.batch, self.k, float(target), sequential, max_round_leaves)
+        from .engine import SearchPlan
+
+        first = _plan_for(e, self.batch, self.k, float(target), sequential, max_round_leaves)
+        self._plans = [first] + [
+            SearchPlan(e.base, self.batch, self.k, filters=e.pack, offsets=e.offset_vector(float(target), device=True),
+                       leaf_filter=e.pack.leaf_filter(di), sequential=sequential, max_round_leaves=max_round_leaves)
+            for _ in range(plans - 1)]
         m = e.base.m
         with torch.cuda.device(dev):
-            self._comp, self._h2d, self._d2h = (torch.cuda.Stream(dev) for _ in range(3))
+            self._comps = [torch.cuda.Stream(dev) for _ in range(plans)]
+            self._h2d, self._d2h = (torch.cuda.Stream(dev) for _ in range(2))
             self._qd = [torch.empty((self.batch, m), dtype=torch.float32, device=dev) for _ in range(depth)]
             self._out = [(torch.empty((self.batch, self.k), dtype=torch.int64, device=dev),
                           torch.empty((self.batch, self.k), dtype=torch.float64, device=dev),
@@ -318,17 +333,19 @@ class SearchPipeline:
             raise ValueError(f"batch of shape {tuple(q.shape)}, pipeline built for {(self.batch, self._qd[i].shape[1])}")
         ev_h2d, ev_run, ev_d2h = self._ev[i]
         reuse = self._n >= self.depth
+        j = self._n % len(self._plans)                   # this batch's plan and compute stream
+        comp = self._comps[j]
         with torch.cuda.stream(self._h2d):
             if reuse:
                 self._h2d.wait_event(ev_run)             # the slot's previous search read its queries
             self._qd[i].copy_(q.to(torch.float32), non_blocking=True)
             ev_h2d.record(self._h2d)
         self._qh[i] = q
-        self._comp.wait_event(ev_h2d)
+        comp.wait_event(ev_h2d)
         if reuse:
-            self._comp.wait_event(ev_d2h)                # the slot's previous results left the device
-        self._plan.run(self._qd[i], stream=self._comp, copy_out=False, outputs=self._out[i])
-        ev_run.record(self._comp)
+            comp.wait_event(ev_d2h)                      # the slot's previous results left the device
+        self._plans[j].run(self._qd[i], stream=comp, copy_out=False, outputs=self._out[i])
+        ev_run.record(comp)
         self._d2h.wait_event(ev_run)
         with torch.cuda.stream(self._d2h):
             for h, x in zip(self._host[i], self._out[i]):
@@ -339,6 +356,33 @@ class SearchPipeline:
         self._slot_ticket[i] = t
         self._n += 1
         return t
+
+    def run_resident(self, queries, steps: int, stream=None):
+        """`steps` batches of the same device-resident queries ([batch, m] fp32 on the
+        index's device) through the alternating plans, no host copies: the caller's
+        stream forks to the compute streams and joins them again, so events recorded on
+        it around the call time the whole job (device-timed throughput).  Not to be
+        interleaved with pending submit() batches.  Returns the last batch's device
+        (ids, dists, stats)."""
+        torch = _lib.require_cuda()
+        if self._pending:
+            raise RuntimeError("collect the submitted batches before run_resident")
+        dev = self._qd[0].device
+        main = stream if stream is not None else torch.cuda.current_stream(dev)
+        fork = torch.cuda.Event()
+        fork.record(main)
+        for c in self._comps:
+            c.wait_event(fork)
+        last = None
+        for n in range(int(steps)):
+            j = n % len(self._plans)
+            last = self._out[j]
+            self._plans[j].run(queries, stream=self._comps[j], copy_out=False, outputs=last)
+        for c in self._comps:
+            e = torch.cuda.Event()
+            e.record(c)
+            main.wait_event(e)
+        return last
 
     def result(self, ticket: int) -> BatchResult:
         """Wait for a submitted batch and return its BatchResult (host arrays)."""

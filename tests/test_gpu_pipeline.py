@@ -348,3 +348,8 @@ def test_search_pipeline_matches_search_queries(pipe64):
     assert np.array_equal(sp.result(t1).ids, refs[1].ids)
     with pytest.raises(KeyError):
         sp.result(t1)
+    # device-resident batches through the alternating plans (bench.py's device-timed form)
+    ids, dists, stats = sp.run_resident(torch.from_numpy(Q).cuda(), 3)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(ids.cpu().numpy(), refs[0].ids)
+    np.testing.assert_array_equal(stats.cpu().numpy(), refs[0].stats)
