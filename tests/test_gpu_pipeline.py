@@ -353,3 +353,26 @@ def test_search_pipeline_matches_search_queries(pipe64):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(ids.cpu().numpy(), refs[0].ids)
     np.testing.assert_array_equal(stats.cpu().numpy(), refs[0].stats)
+
+
+def test_search_pipeline_k3_plans(pipe64):
+    """k > 1 (a prediction pass inside the graph body) with 1, 2 and 3 plans in flight:
+    every batch equals search_queries'."""
+    import torch
+
+    from paper_2502_01836_b200.pipeline import SearchPipeline, search_queries
+
+    e = pipe64["eidx"]
+    Q = np.asarray(pipe64["queries"], dtype=np.float32)
+    ref = search_queries(e, Q, 3, target=0.95)
+    for plans in (1, 2, 3):
+        sp = SearchPipeline(e, Q.shape[0], 3, target=0.95, depth=3, plans=plans)
+        ts = [sp.submit(torch.from_numpy(Q).pin_memory()) for _ in range(3)]
+        for t in ts:
+            r = sp.result(t)
+            np.testing.assert_array_equal(r.ids, ref.ids)
+            np.testing.assert_array_equal(r.dists, ref.dists)
+            np.testing.assert_array_equal(r.stats, ref.stats)
+        ids = sp.run_resident(torch.from_numpy(Q).cuda(), 4)[0]
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(ids.cpu().numpy(), ref.ids)
