@@ -298,11 +298,12 @@ class SearchPipeline:
         self.n_series, self.batch, self.k, self.depth = e.base.n, int(batch), int(k), int(depth)
         from .engine import SearchPlan
 
-        first = _plan_for(e, self.batch, self.k, float(target), sequential, max_round_leaves)
-        self._plans = [first] + [
+        # private plans (not search_queries' cached one): a search_queries call on another
+        # stream never shares scratch with a batch in flight here
+        self._plans = [
             SearchPlan(e.base, self.batch, self.k, filters=e.pack, offsets=e.offset_vector(float(target), device=True),
                        leaf_filter=e.pack.leaf_filter(di), sequential=sequential, max_round_leaves=max_round_leaves)
-            for _ in range(plans - 1)]
+            for _ in range(plans)]
         m = e.base.m
         with torch.cuda.device(dev):
             self._comps = [torch.cuda.Stream(dev) for _ in range(plans)]
