@@ -107,6 +107,9 @@ typedef struct lf_search_opts {
     const float* d_b1;
     const float* d_W2;
     const float* d_b2;
+    int32_t filter_m;            /* width of the in-search filter operands: 0 = m; else
+                                    roundup(m, 64) <= 256, the fp16 pack's W1T_h / b1 / W2
+                                    zero-padded to it (query rows are padded on the device) */
 } lf_search_opts;
 
 #define LF_N_PROF 15

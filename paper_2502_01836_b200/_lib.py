@@ -65,6 +65,7 @@ class LfSearchOpts(C.Structure):
         ("d_b1", C.c_void_p),
         ("d_W2", C.c_void_p),
         ("d_b2", C.c_void_p),
+        ("filter_m", C.c_int32),
     ]
 
 

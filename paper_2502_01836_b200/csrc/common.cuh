@@ -132,6 +132,7 @@ int filter_reach_f16(const __half* d_xh, const int* d_xexp, int64_t Q, int m, co
                      const int4* d_tiles, const int* d_ntiles, const int2* d_dst, const double* d_offset,
                      double* d_adj, int Nn, cudaStream_t st);
 // fp32 rows -> power-of-two-scaled fp16 rows + exponents (filters_tc.cu).
-int rows_to_f16(const float* d_X, int64_t rows, int m, __half* d_out, int* d_exps, cudaStream_t st);
+// mo: output row stride (> m: zero-padded columns; 0 = m)
+int rows_to_f16(const float* d_X, int64_t rows, int m, __half* d_out, int* d_exps, cudaStream_t st, int mo = 0);
 
 }  // namespace lf

@@ -598,7 +598,7 @@ extern "C" int lf_filter_predict_pairs_tc(const float* d_queries, int32_t m, con
 namespace lf {
 namespace tc {
 __global__ void rows_to_f16_kernel(const float* __restrict__ X, int64_t rows, int m, __half* __restrict__ out,
-                                   int* __restrict__ exps) {
+                                   int* __restrict__ exps, int mo) {
     const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (r >= rows) return;
@@ -608,14 +608,16 @@ __global__ void rows_to_f16_kernel(const float* __restrict__ X, int64_t rows, in
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     const int e = amax > 0.f ? ilogbf(amax) - 13 : 0;    // max |x| 2^-e in [2^13, 2^14)
-    for (int c = lane; c < m; c += 32) out[r * m + c] = __float2half_rn(scalbnf(x[c], -e));
+    for (int c = lane; c < m; c += 32) out[r * mo + c] = __float2half_rn(scalbnf(x[c], -e));
+    for (int c = m + lane; c < mo; c += 32) out[r * mo + c] = __float2half_rn(0.f);   // zero padding
     if (lane == 0) exps[r] = e;
 }
 }  // namespace tc
 
-int rows_to_f16(const float* d_X, int64_t rows, int m, __half* d_out, int* d_exps, cudaStream_t st) {
+int rows_to_f16(const float* d_X, int64_t rows, int m, __half* d_out, int* d_exps, cudaStream_t st, int mo) {
     if (rows == 0) return LF_OK;
-    tc::rows_to_f16_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, st>>>(d_X, rows, m, d_out, d_exps);
+    tc::rows_to_f16_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, st>>>(d_X, rows, m, d_out, d_exps,
+                                                                                 mo > 0 ? mo : m);
     LF_CUDA(cudaGetLastError());
     return LF_OK;
 }

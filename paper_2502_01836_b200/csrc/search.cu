@@ -813,6 +813,9 @@ namespace lf {
 
 // Scratch of one search session, sized once for (index, Q, opts); a search plan keeps
 // it across calls (lf_search_plan_*), lf_search / lf_search_begin allocate per call.
+// the in-search filter operands' width: the pack's (zero-padded) dimension, or m
+static int filter_width(const lf_index& idx, const lf_search_opts& o) { return o.filter_m > 0 ? o.filter_m : idx.m; }
+
 static int session_alloc(lf_session* ss) {
     const lf_index& idx = ss->idx;
     const lf_search_opts& o = ss->opts;
@@ -894,7 +897,7 @@ static int session_alloc(lf_session* ss) {
         const int64_t max_pairs = Q * (int64_t)L;     // every (query, leaf) pair, worst case
         LF_CUDA(ss->pdst.alloc(sizeof(int2) * max_pairs, st));
         LF_CUDA(ss->ptiles.alloc(sizeof(int4) * (max_pairs / 128 + F + 1), st));
-        LF_CUDA(ss->xh.alloc(sizeof(__half) * Q * idx.m, st));
+        LF_CUDA(ss->xh.alloc(sizeof(__half) * Q * filter_width(idx, o), st));
         LF_CUDA(ss->xexp.alloc(sizeof(int) * Q, st));
     }
     LF_CUDA(ss->tasks.alloc(sizeof(int4) * max_tasks, st));
@@ -1026,7 +1029,7 @@ static int session_prologue(lf_session* ss) {
     LF_CUDA(cudaEventRecord(ss->fork_ev, st));
     LF_CUDA(cudaStreamWaitEvent(st2, ss->fork_ev, 0));
     if (ss->lazy) {
-        int rc = rows_to_f16(ss->d_q, Q, idx.m, ss->xh.as<__half>(), ss->xexp.as<int>(), st2);
+        int rc = rows_to_f16(ss->d_q, Q, idx.m, ss->xh.as<__half>(), ss->xexp.as<int>(), st2, filter_width(idx, o));
         if (rc) return rc;
         ++ss->kernels;
     }
@@ -1136,7 +1139,7 @@ static int predict_pass(lf_session* ss, int all) {
     int rc = pair_tiles(ss->fhist.as<int>(), F, ss->fcur.as<int>(), ss->ptiles.as<int4>(), ss->ntiles.as<int>(), st,
                         (int)Q);
     if (rc) return rc;
-    rc = filter_reach_f16(ss->xh.as<__half>(), ss->xexp.as<int>(), Q, idx.m, o.d_W1T_h, o.d_wexp, o.d_b1, o.d_W2,
+    rc = filter_reach_f16(ss->xh.as<__half>(), ss->xexp.as<int>(), Q, filter_width(idx, o), o.d_W1T_h, o.d_wexp, o.d_b1, o.d_W2,
                           o.d_b2, F, ss->ptiles.as<int4>(), ss->ntiles.as<int>(), ss->pdst.as<int2>(), o.d_offset,
                           ss->adj.as<double>(), idx.n_leaves, st);
     if (rc) return rc;
@@ -1350,10 +1353,12 @@ static int check_args(const lf_index* idx, int64_t Q, const lf_search_opts* opts
                "filter predictions need offsets and a leaf->filter map");
     LF_REQUIRE(opts->d_W1T_h == nullptr || opts->d_pred != nullptr || opts->d_pred_f64 != nullptr ||
                    (opts->d_wexp != nullptr && opts->d_b1 != nullptr && opts->d_W2 != nullptr && opts->d_b2 != nullptr &&
-                    idx->m % 64 == 0 && idx->m >= 64 && idx->m <= 256 && opts->n_filters >= 1 &&
+                    filter_width(*idx, *opts) % 64 == 0 && filter_width(*idx, *opts) >= 64 &&
+                    filter_width(*idx, *opts) <= 256 && filter_width(*idx, *opts) >= idx->m && opts->n_filters >= 1 &&
                     ((uintptr_t)opts->d_W1T_h & 15) == 0 && ((uintptr_t)opts->d_b1 & 15) == 0 &&
                     ((uintptr_t)opts->d_W2 & 15) == 0),
-               "in-search filter inference needs W1T_h, wexp, b1, W2, b2 (16-byte aligned) and m in {64, 128, 192, 256}");
+               "in-search filter inference needs W1T_h, wexp, b1, W2, b2 (16-byte aligned) and a filter width "
+               "(filter_m, else m) in {64, 128, 192, 256}, >= m");
     LF_REQUIRE(opts->sequential || opts->max_round_leaves >= 1, "max_round_leaves must be >= 1");
     return LF_OK;
 }

@@ -183,8 +183,9 @@ def _search_options(t, di, Q: int, k: int, *, bsf_factor: float = 1.0, predictio
             raise ValueError("filter / offset / leaf map shapes do not agree")
         keep += [off, lf, filters]
         opts.d_W1T_h, opts.d_wexp = filters.W1T_h.data_ptr(), filters.wexp.data_ptr()
-        opts.d_b1 = filters.b1.data_ptr()
-        opts.d_W2, opts.d_b2 = filters.W2.data_ptr(), filters.b2.data_ptr()
+        opts.d_b1 = filters.h_b1.data_ptr()
+        opts.d_W2, opts.d_b2 = filters.h_W2.data_ptr(), filters.b2.data_ptr()
+        opts.filter_m = filters.mp if filters.mp != filters.m else 0
         opts.d_offset, opts.n_filters = off.data_ptr(), int(off.shape[0])
         ist = di.struct(lf)
     elif predictions is not None:

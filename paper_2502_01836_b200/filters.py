@@ -21,9 +21,10 @@ from . import _lib
 
 class FilterPack:
     """path: "tc16" (tcgen05 kind::f16 over power-of-two-scaled fp16 operands --
-    tf32's mantissa at twice its rate; default when m is a multiple of 64 up to 256),
-    "tc" (tcgen05 tf32; default for other multiples of 32; the lazy in-search
-    inference runs on it) or "simt" (fp32 CUDA-core FFMA).  LF_FILTER_PATH overrides
+    tf32's mantissa at twice its rate; default for m up to 256 that is a multiple of 64
+    or above 64 -- the operands are then zero-padded to the next multiple of 64; the
+    in-search inference runs on it), "tc" (tcgen05 tf32; default for m = 32) or
+    "simt" (fp32 CUDA-core FFMA).  LF_FILTER_PATH overrides
     the default.  Calibration and search must use the same pack (same path) --
     predictions are then bit-identical (F6)."""
 
@@ -51,21 +52,31 @@ class FilterPack:
         self.device = dev
         self._slot_maps = weakref.WeakKeyDictionary()   # DeviceIndex -> leaf->filter map
         tc_ok = F > 0 and m % 32 == 0 and 32 <= m <= 256
-        tc16_ok = tc_ok and m % 64 == 0
+        # fp16 path: m a multiple of 64, or 64 < m <= 256 with the operands zero-padded to
+        # the next multiple of 64 (exact: padded inputs, hidden units and weights are 0)
+        tc16_ok = tc_ok and (m % 64 == 0 or m > 64)
         self.path = path or os.environ.get("LF_FILTER_PATH") or ("tc16" if tc16_ok else "tc" if tc_ok else "simt")
         if self.path in ("tc", "tc16"):
             if not tc_ok:
                 raise ValueError("tensor-core filter path needs m in {32, 64, ..., 256}")
             if self.path == "tc16" and not tc16_ok:
-                raise ValueError("fp16 tensor-core filter path needs m in {64, 128, 192, 256}")
+                raise ValueError("fp16 tensor-core filter path needs m a multiple of 64, or 64 < m <= 256")
             self.W1T = self.W1.transpose(1, 2).contiguous()     # K-major B operand [F][hidden][in]
             if self.path == "tc16":
-                self.W1T_h = torch.empty((F, m, m), dtype=torch.float16, device=dev)
+                mp = (m + 63) // 64 * 64
+                pad = mp - m
+                W1T = self.W1T if not pad else torch.nn.functional.pad(self.W1T, (0, pad, 0, pad)).contiguous()
+                self.mp = mp
+                self.h_b1 = self.b1 if not pad else torch.nn.functional.pad(self.b1, (0, pad)).contiguous()
+                self.h_W2 = self.W2 if not pad else torch.nn.functional.pad(self.W2, (0, pad)).contiguous()
+                self.W1T_h = torch.empty((F, mp, mp), dtype=torch.float16, device=dev)
                 self.wexp = torch.empty(F, dtype=torch.int32, device=dev)
-                _lib.check(_lib.lib().lf_filter_rows_to_f16(self.W1T.data_ptr(), F, m * m, self.W1T_h.data_ptr(),
+                _lib.check(_lib.lib().lf_filter_rows_to_f16(W1T.data_ptr(), F, mp * mp, self.W1T_h.data_ptr(),
                                                            self.wexp.data_ptr(), _lib.stream_ptr()))
         elif self.path != "simt":
             raise ValueError(f"unknown filter path {self.path!r}")
+        if self.path != "tc16":
+            self.mp, self.h_b1, self.h_W2 = m, self.b1, self.W2
 
     @property
     def n_filters(self) -> int:
@@ -96,9 +107,10 @@ class FilterPack:
             if q.shape[1] != self.m:
                 raise ValueError(f"input shape {tuple(q.shape)} does not match model dim {self.m}")
             if self.path == "tc16":
-                _lib.check(_lib.lib().lf_filter_predict_f16(q.data_ptr(), Q, self.m, self.W1T_h.data_ptr(),
-                                                            self.wexp.data_ptr(), self.b1.data_ptr(),
-                                                            self.W2.data_ptr(), self.b2.data_ptr(), self.n_filters,
+                qp = self._pad_rows(q)
+                _lib.check(_lib.lib().lf_filter_predict_f16(qp.data_ptr(), Q, self.mp, self.W1T_h.data_ptr(),
+                                                            self.wexp.data_ptr(), self.h_b1.data_ptr(),
+                                                            self.h_W2.data_ptr(), self.b2.data_ptr(), self.n_filters,
                                                             out.data_ptr(), _lib.stream_ptr(stream)))
                 return out
             fn = _lib.lib().lf_filter_predict_tc if self.path == "tc" else _lib.lib().lf_filter_predict
@@ -119,9 +131,10 @@ class FilterPack:
         pf = torch.as_tensor(pair_f, dtype=torch.int32).to(self.device).contiguous()
         out = torch.empty(pq.shape[0], dtype=torch.float64, device=self.device)
         if self.path == "tc16":
+            qp = self._pad_rows(q)
             _lib.check(_lib.lib().lf_filter_predict_pairs_f16(
-                q.data_ptr(), q.shape[0], self.m, self.W1T_h.data_ptr(), self.wexp.data_ptr(), self.b1.data_ptr(),
-                self.W2.data_ptr(), self.b2.data_ptr(), self.n_filters, pq.data_ptr(), pf.data_ptr(), pq.shape[0],
+                qp.data_ptr(), q.shape[0], self.mp, self.W1T_h.data_ptr(), self.wexp.data_ptr(), self.h_b1.data_ptr(),
+                self.h_W2.data_ptr(), self.b2.data_ptr(), self.n_filters, pq.data_ptr(), pf.data_ptr(), pq.shape[0],
                 out.data_ptr(), _lib.stream_ptr(stream)))
             return out
         _lib.check(_lib.lib().lf_filter_predict_pairs_tc(q.data_ptr(), self.m, self.W1T.data_ptr(), self.b1.data_ptr(),
@@ -129,6 +142,11 @@ class FilterPack:
                                                          pq.data_ptr(), pf.data_ptr(), pq.shape[0], out.data_ptr(),
                                                          _lib.stream_ptr(stream)))
         return out
+
+    def _pad_rows(self, q):
+        """[Q, m] fp32 -> [Q, mp] with zero columns (the fp16 pack's padded width)."""
+        torch = _lib.require_cuda()
+        return q if self.mp == self.m else torch.nn.functional.pad(q, (0, self.mp - self.m)).contiguous()
 
     def leaf_filter(self, dindex):
         """int32 [n_leaves]: filter slot of each leaf slot of a DeviceIndex, -1 if none."""

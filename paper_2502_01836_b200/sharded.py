@@ -56,8 +56,9 @@ class GpuRoundEngine:
             lf = leaf_filter.to(device=self.device, dtype=torch.int32).contiguous()
             self._keep += [off, lf, filters]
             o.d_W1T_h, o.d_wexp = filters.W1T_h.data_ptr(), filters.wexp.data_ptr()
-            o.d_b1 = filters.b1.data_ptr()
-            o.d_W2, o.d_b2 = filters.W2.data_ptr(), filters.b2.data_ptr()
+            o.d_b1 = filters.h_b1.data_ptr()
+            o.d_W2, o.d_b2 = filters.h_W2.data_ptr(), filters.b2.data_ptr()
+            o.filter_m = filters.mp if filters.mp != filters.m else 0
             o.d_offset = off.data_ptr()
             o.n_filters = int(off.shape[0])
         elif predictions is not None:
