@@ -96,7 +96,8 @@ typedef struct lf_search_opts {
     /* In-search filter inference (used when d_pred and d_pred_f64 are NULL and d_W1T_h
        is set): the fp16 filter pack -- W1T_h [F][hidden][in] fp16 bits with per-filter
        power-of-two exponents d_wexp (lf_filter_predict_f16's operands), b1 [F][m],
-       W2 [F][m], b2 [F]; m in {64, 128, 192, 256}.  Round 0 needs no prediction (bsf is
+       W2 [F][m], b2 [F]; m in {64, 128, 192, 256}, or (filter_m below) any m <= 256 with
+       the pack zero-padded to filter_m = roundup(m, 64).  Round 0 needs no prediction (bsf is
        +inf); right after it ONE tensor-core pass predicts exactly the (query, filtered
        leaf) pairs with lb <= bsf0 * f -- every pair the walk can still reach, since bsf
        only decreases -- bit-identical to lf_filter_predict_f16's predictions.  (A query
