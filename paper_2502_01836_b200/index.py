@@ -377,7 +377,7 @@ class DeviceIndex:
             # int8 shadow for the bounded scan (scan_q8_kernel), when the layout allows it
             self.X8 = self.qmeta = None
             n_rows, m = int(self.X.shape[0]), int(self.X.shape[1])
-            if m % 4 == 0 and m <= 512 and n_rows:     # codes zero-padded to a multiple of 64
+            if m % 4 == 0 and m <= 512 and n_rows:     # codes zero-padded to a multiple of 32
                 self.X8 = torch.empty((n_rows, (m + 31) // 32 * 32), dtype=torch.int8, device=dev)
                 self.qmeta = torch.empty((n_rows, 4), dtype=torch.float32, device=dev)
                 _lib.check(_lib.lib().lf_quantize_rows(self.X.data_ptr(), n_rows, m, self.X8.data_ptr(),
